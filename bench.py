@@ -1,0 +1,370 @@
+"""Benchmark: rank-k randomized SVD on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+
+One step = one rank-k randomized SVD of the configuration's A as the
+reference CLI composes it (cli.py:128-165 Stage A + direct_svd; SURVEY.md
+§8a a13): Stage A (Alg 4.1 / 4.4 / 4.5) + Alg 5.1, i.e. 2q+2 passes over A.
+The posterior estimator (one more pass, r = 10) is timed separately, as in
+the reference's CPU plan.
+
+value = whole-job A-GB/s = passes x bytes(A) / step time (higher is better);
+ms_per_step is the rSVD time.  A is device-resident before timing starts;
+A (>= 1 GiB for the default config) exceeds the 126 MB L2, so no explicit
+flush is needed between steps.  `e2e` repeats the measurement through the
+public API with host buffers: the pinned host A is copied to the device,
+validated, factored, and U / sigma / V copied back, every step.
+
+--impl reference times the CPU oracle (oracle/lowrank_oracle.py, a numpy
+restatement of the reference package, pinned to the reference's golden
+vectors) on the host cores with all BLAS threads.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads  # noqa: E402
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--config", type=int, default=2)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    return p.parse_args()
+
+
+def env_rank():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(
+        os.environ.get("LOCAL_RANK", "0"))
+
+
+# ---------------------------------------------------------------------------
+# clocks (nvidia-smi sampled during the timed region)
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.stop = threading.Event()
+        self.th = None
+
+    def _run(self):
+        while not self.stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                for line in out.stdout.strip().splitlines():
+                    self.rows.append([x.strip() for x in line.split(",")])
+            except Exception:
+                pass
+            self.stop.wait(0.2)
+
+    def __enter__(self):
+        self.th = threading.Thread(target=self._run, daemon=True)
+        self.th.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.th.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for nm, v in zip(names, r[4:8]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# inputs
+
+def build_input(cfg, device="cuda"):
+    """Device-resident A for the configuration (see workloads.py)."""
+    import torch
+    if cfg.idx in (1, 2):
+        A, _ = workloads.build_synthetic_device(cfg.m, cfg.n, workloads.spectrum(cfg.idx, cfg.n),
+                                                cfg.seed, device=device)
+        return A
+    if cfg.idx == 3:
+        return torch.from_numpy(workloads.build_cfg3()).to(device)
+    if cfg.idx == 4:
+        A, _ = workloads.build_cfg4_device(device=device)
+        return A
+    raise ValueError("config 5 is built by build_sparse")
+
+
+def measured_fp64_peak():
+    """cuBLAS DGEMM 8192^3 (best of 5) -- the FP64 tensor peak the roofline
+    uses (MEASURED_PEAKS.json has only HBM and bf16)."""
+    import torch
+    n = 8192
+    a = torch.randn(n, n, dtype=torch.float64, device="cuda")
+    b = torch.randn(n, n, dtype=torch.float64, device="cuda")
+    for _ in range(2):
+        torch.matmul(a, b)
+    best = 1e9
+    for _ in range(5):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        torch.matmul(a, b)
+        e.record()
+        torch.cuda.synchronize()
+        best = min(best, s.elapsed_time(e) / 1e3)
+    del a, b
+    return 2.0 * n ** 3 / best / 1e12
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+def cpu_baseline(cfg, A_host, steps=1):
+    """The CPU oracle on the same A with all host threads (kind "port")."""
+    from oracle import lowrank_oracle as O
+    cores = os.cpu_count()
+    op = O.Dense(A_host, promote=True)
+    best = None
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        O.rsvd(op, cfg.k, cfg.p, cfg.q, cfg.seed, sketch=cfg.sketch, estimate=False)
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    return best, cores
+
+
+# ---------------------------------------------------------------------------
+
+def run_ours(args, cfg):
+    import torch
+    import paper_0909_4061_b200 as lr
+    from paper_0909_4061_b200 import core as lrcore
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    A = build_input(cfg)
+    torch.cuda.synchronize()
+    op = lr.DenseOperator(A)
+    a_bytes = A.numel() * A.element_size()
+    passes = cfg.passes()
+
+    def step():
+        return lr.randomized_svd(op, cfg.k, cfg.p, cfg.q, cfg.seed, sketch=cfg.sketch,
+                                 estimate=False)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # timed region: K steps, CUDA events on the launching stream
+    lrcore.PASS_EVENTS = []
+    l0 = lr._lib.launch_count()
+    with ClockSampler(local) as clk:
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(args.steps):
+            step()
+        e.record()
+        torch.cuda.synchronize()
+    launches = lr._lib.launch_count() - l0
+    ms = s.elapsed_time(e) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    pev = lrcore.PASS_EVENTS
+    lrcore.PASS_EVENTS = None
+    pass_ms = [a.elapsed_time(b) for a, b, *_ in pev]
+    flops_per = [f for _, _, f, _, _ in pev]
+    avg_pass_ms = sum(pass_ms) / len(pass_ms)
+    avg_flops = sum(flops_per) / len(flops_per)
+
+    # estimator pass, timed separately
+    est_s, est_e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    b, f, _ = step()
+    est_s.record()
+    est = lr.posterior_error_estimate(op, b.Q, r=10, alpha=10.0, seed=cfg.seed + 13)
+    est_e.record()
+    torch.cuda.synchronize()
+    est_ms = est_s.elapsed_time(est_e)
+
+    value = passes * a_bytes / (ms / 1e3) / 1e9
+    pk, src = peaks()
+    if A.dtype in (torch.float64, torch.complex128):
+        peak_tf = measured_fp64_peak()
+        bound, peak_src = "tensor", "measured in-run: cuBLAS DGEMM 8192^3 (torch.matmul)"
+    else:
+        peak_tf = pk["bf16_tflops"]
+        bound, peak_src = "tensor", f"{src} bf16 (MEASURED_PEAKS.json)"
+    achieved_tf = avg_flops / (avg_pass_ms / 1e3) / 1e12
+    hbm = pk["hbm_gbs"]
+    # per-pass roofline: max(flops / tensor peak, bytes(A) / HBM)
+    roof_pass_s = max(avg_flops / (peak_tf * 1e12), a_bytes / (hbm * 1e9))
+    roof_step_ms = passes * roof_pass_s * 1e3
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get(f"cfg{cfg.idx}")
+
+    line = {
+        "metric": "rank-k rSVD time & A-GB/s (% roofline) at 1/2/4/8 B200 vs host-CPU ref",
+        "value": round(value, 3), "unit": "A-GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None,
+        "dtype": {torch.float64: "f64", torch.float32: "f32", torch.complex64: "c64",
+                  torch.complex128: "c128"}[A.dtype],
+        "data": "synthetic (seeded, BASELINE.json config recipe; see workloads.py)",
+        "config": {"workload": cfg.name, "config_index": cfg.idx, "m": cfg.m, "n": cfg.n,
+                   "k": cfg.k, "ell": cfg.ell, "q": cfg.q, "sketch": cfg.sketch,
+                   "passes": passes, "a_bytes": a_bytes,
+                   "l2": "inputs larger than L2 (A >= 1 GiB), no flush",
+                   "parallelism": f"rows x{world}" if world > 1 else "single GPU"},
+        "roofline": {"bound": bound, "achieved": round(achieved_tf, 3), "peak": round(peak_tf, 3),
+                     "unit": "TFLOP/s", "frac": round(achieved_tf / peak_tf, 4),
+                     "traffic": traffic, "kernel": "lr_gemm pass over A (K1/K2)",
+                     "peak_source": peak_src, "avg_pass_ms": round(avg_pass_ms, 4),
+                     "pass_a_gbs": round(a_bytes / (avg_pass_ms / 1e3) / 1e9, 1),
+                     "step_roofline_ms": round(roof_step_ms, 4),
+                     "step_roofline_frac": round(roof_step_ms / ms, 4),
+                     "pass_share_of_step": round(sum(pass_ms) / (ms * args.steps), 4)},
+        "estimator_ms": round(est_ms, 4),
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+
+    if not args.no_e2e and rank == 0:
+        line["e2e"] = e2e_measure(args, cfg, A, lr)
+    if not args.no_cpu and rank == 0 and world == 1:
+        A_host = A.cpu().numpy()
+        t_cpu, cores = cpu_baseline(cfg, A_host)
+        line["cpu_baseline"] = {"value": round(passes * a_bytes / t_cpu / 1e9, 4),
+                                "unit": "A-GB/s", "cores": cores, "kind": "port",
+                                "sample": f"one full {cfg.name} rSVD (Stage A + direct SVD) "
+                                          f"by oracle/lowrank_oracle.py, "
+                                          f"{t_cpu:.2f} s",
+                                "seconds": round(t_cpu, 3)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def e2e_measure(args, cfg, A, lr):
+    """Same metric through the public API with pinned host buffers."""
+    import torch
+    host = torch.empty(A.shape, dtype=A.dtype, pin_memory=True)
+    host.copy_(A)
+    A_np = host.numpy()
+    steps = max(1, min(args.steps, 5))
+
+    def once():
+        b, f, _ = lr.randomized_svd(A_np, cfg.k, cfg.p, cfg.q, cfg.seed, sketch=cfg.sketch,
+                                    estimate=False)
+        return f
+
+    once()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        f = once()
+    dt = (time.perf_counter() - t0) / steps
+    a_bytes = A.numel() * A.element_size()
+    d2h = f.U.nbytes + f.sigma.nbytes + f.V.nbytes
+    return {"value": round(cfg.passes() * a_bytes / dt / 1e9, 3), "unit": "A-GB/s",
+            "ms_per_step": round(dt * 1e3, 3), "h2d_bytes_per_step": int(a_bytes),
+            "d2h_bytes_per_step": int(d2h), "steps": steps}
+
+
+def run_reference(args, cfg):
+    rank, world, local = env_rank()
+    if rank != 0:
+        return
+    import torch
+    if torch.cuda.is_available():
+        torch.cuda.set_device(local)
+        A_host = build_input(cfg).cpu().numpy()
+        torch.cuda.empty_cache()
+    else:
+        A_host, _ = workloads.synthetic_explicit(cfg.m, cfg.n, workloads.spectrum(cfg.idx, cfg.n),
+                                                 cfg.seed)
+    from oracle import lowrank_oracle as O
+    op = O.Dense(A_host)
+    a_bytes = A_host.size * A_host.itemsize
+    for _ in range(args.warmup):
+        O.rsvd(op, cfg.k, cfg.p, cfg.q, cfg.seed, sketch=cfg.sketch, estimate=False)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        O.rsvd(op, cfg.k, cfg.p, cfg.q, cfg.seed, sketch=cfg.sketch, estimate=False)
+    dt = (time.perf_counter() - t0) / args.steps
+    v = cfg.passes() * a_bytes / dt / 1e9
+    line = {
+        "metric": "rank-k rSVD time & A-GB/s (% roofline) at 1/2/4/8 B200 vs host-CPU ref",
+        "impl": "reference", "value": round(v, 4), "unit": "A-GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded, BASELINE.json config recipe; see workloads.py)",
+        "config": {"workload": cfg.name, "config_index": cfg.idx, "m": cfg.m, "n": cfg.n,
+                   "k": cfg.k, "ell": cfg.ell, "q": cfg.q, "passes": cfg.passes()},
+        "cpu_baseline": {"value": round(v, 4), "unit": "A-GB/s", "cores": os.cpu_count(),
+                         "kind": "port",
+                         "sample": f"full {cfg.name} rSVD per step (oracle/lowrank_oracle.py, "
+                                   "numpy/OpenBLAS, all host threads; Stage A + direct SVD)"},
+        "e2e": {"value": round(v, 4), "unit": "A-GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    cfg = workloads.CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,189 @@
+/*
+ * lowrank_b200 -- C ABI of the B200-native randomized range finder / SVD.
+ *
+ * This is the drop-in boundary for the passes over A of the reference
+ * package `lowrank` (/root/reference/pkg/src/lowrank).  The reference is
+ * pure Python; its plug-in point is the MatVecOperator protocol
+ * (core.py:343-380) plus the dense kernels the range finders call.  Each
+ * entry point below replaces one of those call sites; the Python package
+ * paper_0909_4061_b200 binds them with ctypes (INTEGRATION.md shows the
+ * binding a maintainer of the reference would add).
+ *
+ * Conventions
+ *   - All matrices are row-major (C order, as numpy arrays in the
+ *     reference); `ld*` is the row stride in elements.
+ *   - All pointers are device pointers owned by the caller; the library
+ *     never frees caller memory.  Scratch comes from a handle-owned pool.
+ *   - Every call is stream-ordered and asynchronous on the handle's stream
+ *     unless documented as synchronizing (composites that must make a
+ *     host-side decision say "syncs").
+ *   - Return value: LR_OK (0) or an lr_status code; lr_last_error() gives a
+ *     thread-local message.  Codes map to the reference's exceptions:
+ *     LR_EINVAL -> ValueError, LR_ECONV -> ConvergenceError (core.py:25-30).
+ *   - One handle per (host thread, device); handles are not thread-safe.
+ */
+#ifndef LOWRANK_B200_H
+#define LOWRANK_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LR_ABI_VERSION 1
+
+typedef struct lr_handle_s* lr_handle_t;
+
+typedef enum { LR_F32 = 0, LR_F64 = 1, LR_C64 = 2, LR_C128 = 3 } lr_dtype_t;
+typedef enum { LR_OP_N = 0, LR_OP_T = 1, LR_OP_C = 2 } lr_op_t;
+typedef enum {
+  LR_OK = 0,
+  LR_EINVAL = 1,       /* ValueError */
+  LR_ECONV = 2,        /* ConvergenceError */
+  LR_ENOTPSD = 3,      /* NotPSDError */
+  LR_ECUDA = 4,        /* CUDA runtime failure */
+  LR_ENOMEM = 5,       /* device allocation failed */
+  LR_EUNSUPPORTED = 6  /* dtype/shape combination not built */
+} lr_status_t;
+
+/* fp32 GEMM arithmetic schemes (LR_F32 only) */
+typedef enum {
+  LR_F32_SPLIT3 = 0,   /* default: 3-product split on tcgen05 kind::f16 */
+  LR_F32_SIMT = 1      /* plain fp32 FFMA (reference arithmetic check) */
+} lr_f32_mode_t;
+
+int lr_abi_version(void);
+const char* lr_last_error(void);
+/* Number of kernels this library has launched in the process (evidence
+ * for bench.py's "gpu_launches"). */
+uint64_t lr_launch_count(void);
+
+/* Handle: device + stream + scratch pool.  `stream` is a cudaStream_t (or
+ * NULL for the legacy default stream). */
+int lr_create(int device, void* stream, lr_handle_t* out);
+int lr_destroy(lr_handle_t h);
+int lr_set_stream(lr_handle_t h, void* stream);
+int lr_set_f32_mode(lr_handle_t h, int mode);
+/* Bytes currently reserved by the scratch pool. */
+int64_t lr_workspace_bytes(lr_handle_t h);
+/* Pre-size the scratch pool (needed before CUDA-graph capture). */
+int lr_reserve(lr_handle_t h, int64_t bytes);
+
+/* K1/K2 -- one pass over A (replaces DenseOperator._apply / _apply_adjoint,
+ * reference core.py:391-395):
+ *   op = LR_OP_N :  Y (m x ell)  = A   (m x n) . X (n x ell)
+ *   op = LR_OP_T :  Y (n x ell)  = A^T (n x m) . X (m x ell)
+ *   op = LR_OP_C :  Y (n x ell)  = A^H (n x m) . X (m x ell)
+ * Deterministic: split-K partials are reduced in a fixed order. */
+int lr_gemm(lr_handle_t h, int dtype, int op, int64_t m, int64_t n, int64_t ell,
+            const void* A, int64_t lda, const void* X, int64_t ldx,
+            void* Y, int64_t ldy);
+
+/* Gram matrix G = Y^H Y (ell x ell), accumulated in fp64 (real dtypes) or
+ * complex128 (complex dtypes) regardless of the input precision.  G is
+ * written as double / double2 row-major with leading dimension ell.  Used
+ * by lr_orth and, between ranks, by the row-sharded path (all-reduce of G). */
+int lr_gram(lr_handle_t h, int dtype, int64_t m, int64_t ell,
+            const void* Y, int64_t ldy, void* G);
+
+/* Cholesky with column deletion on a Gram matrix (the rank decision of
+ * orthonormalize_double_gs, reference core.py:104-106):
+ *   pivot d_j <= drop_thr2           -> column j dropped
+ *   pivot d_j <= unres_rel * G_jj    -> counted as unresolved (too small to
+ *                                       be trusted from a Gram; caller falls back)
+ * `shift` is added to the diagonal first (shifted CholeskyQR).
+ * Outputs (device): P (ell x ell, row-major, ld ell): Q = Y . P[:, :rank];
+ * R (ell x ell upper, kept rows/cols only, others 0); info[0] = rank,
+ * info[1] = unresolved pivots, info[2] = non-positive pivots among kept. */
+int lr_chol_drop(lr_handle_t h, int dtype, int64_t ell, const void* G,
+                 double drop_thr2, double unres_rel, double shift,
+                 void* P, void* R, int32_t* info);
+
+/* Orthonormalize the columns of Y (m x ell) -- replaces
+ * orthonormalize_double_gs (reference core.py:84-115).  CholeskyQR2 with a
+ * fp64 Gram; guarded fallbacks (shifted CholeskyQR3, then column-wise CGS2
+ * on the device) when pivots cannot be resolved.  Writes Q (m x rank) into
+ * Q (ld ldq, may alias Y) and the rank into *rank_out.  Syncs. */
+int lr_orth(lr_handle_t h, int dtype, int64_t m, int64_t ell, const void* Y, int64_t ldy,
+            void* Q, int64_t ldq, double tol, int64_t* rank_out);
+
+/* Small SVD of B (ell x ncols, ell <= ncols) given through Bh = B^H
+ * (ncols x ell, row-major) -- which is exactly what the adjoint pass of
+ * direct_svd produces (reference factor.py:163-164, core.py:199-230).
+ * Outputs: U (ell x ell), S (ell, double), V (ncols x ell) with
+ * B = U diag(S) V^H, S descending, and the reference sign convention (first
+ * entry with |u| > 1e-10 max|u| of each U column real positive).  Bh is
+ * overwritten.  Syncs. */
+int lr_small_svd(lr_handle_t h, int dtype, int64_t ell, int64_t ncols,
+                 void* Bh, void* U, double* S, void* V);
+
+/* One-sided Jacobi SVD of a square ell x ell matrix M (row-major):
+ * M = W diag(S) J^H.  Outputs W, S (descending), J, sign-fixed so that J's
+ * columns follow the reference convention.  info[0] = sweeps used
+ * (negative if not converged). */
+int lr_jacobi_svd(lr_handle_t h, int dtype, int64_t ell, const void* M,
+                  void* W, double* S, void* J, int32_t* info);
+
+/* Posterior estimator tail (reference rangefinder.py:79-82): given
+ * Z = A W (m x r) and Q (m x k), compute
+ * alpha sqrt(2/pi) max_i ||(I - QQ^H) z_i|| into *est (device double). */
+int lr_estimate_tail(lr_handle_t h, int dtype, int64_t m, int64_t k, int64_t r,
+                     const void* Q, int64_t ldq, void* Z, int64_t ldz,
+                     double alpha, double* est);
+
+/* SRFT sketch (reference sketch.py:306-320): for complex A (m x n, n a
+ * power of two), Y[:, t] = scale * (F_unitary (A_i * d))[picks[t]]. */
+int lr_srft(lr_handle_t h, int dtype, int64_t m, int64_t n, int64_t ell,
+            const void* A, int64_t lda, const void* d, const int32_t* picks,
+            double scale, void* Y, int64_t ldy);
+
+/* Unitary DFT of each row of X (rows x n, n a power of two), in place
+ * (reference sketch.py:179-200). */
+int lr_dft_rows(lr_handle_t h, int dtype, int64_t rows, int64_t n, void* X, int64_t ldx);
+
+/* CSR SpMM (config 5): Y (m x ell) = S . X (n x ell) with int64 row
+ * pointers and int32 column indices.  For S^T . X pass the CSR of S^T. */
+int lr_csr_spmm(lr_handle_t h, int dtype, int64_t m, int64_t n, int64_t ell,
+                const int64_t* rowptr, const int32_t* colidx, const void* vals,
+                const void* X, int64_t ldx, void* Y, int64_t ldy, int accumulate);
+
+/* Input validation of as_matrix (reference core.py:44-49) fused with a max
+ * |a| reduction: info[0] = number of non-finite entries, amax[0] = max |a|. */
+int lr_check_finite(lr_handle_t h, int dtype, int64_t m, int64_t n, const void* A,
+                    int64_t lda, int64_t* nonfinite, double* amax);
+
+/* dst (rows x cols, dst_dtype) = src (src_dtype), or src^H when
+ * conj_transpose (then src is cols x rows).  Real -> complex casts zero the
+ * imaginary part.  Layout plumbing for the Python layer (e.g. B -> B^H for
+ * small_svd, reference core.py:211). */
+int lr_copy(lr_handle_t h, int src_dtype, const void* src, int64_t lds, int dst_dtype,
+            void* dst, int64_t ldd, int64_t rows, int64_t cols, int conj_transpose);
+
+/* Reference sign convention on U (rows x cols): the first entry of each
+ * column with |u| > 1e-10 max|u| is rotated onto the positive real axis and
+ * V's matching column absorbs the same phase (core.py:221-229). */
+int lr_sign_fix(lr_handle_t h, int dtype, int64_t rows, int64_t vrows, int64_t cols, void* U,
+                int64_t ldu, void* V, int64_t ldv);
+
+/* max |imag(Y)| over a complex matrix (fast_range_finder's
+ * diagnostics["max_imag_sample"], reference rangefinder.py:261-262). */
+int lr_max_abs_imag(lr_handle_t h, int dtype, int64_t m, int64_t n, const void* Y, int64_t ldy,
+                    double* out);
+
+/* BLAS-1 helpers for the column-wise paths (device CGS2 / the unsafeguarded
+ * Gram-Schmidt of power_iteration_range(safeguarded=False), reference
+ * rangefinder.py:169-184):  Z -= T;  out[j] = sum_i |Z_ij|^2 (fp64, fixed
+ * reduction order);  dst[:, 0] = src[:, 0] * inv. */
+int lr_axpy_sub(lr_handle_t h, int dtype, int64_t rows, int64_t cols, const void* T, int64_t ldt,
+                void* Z, int64_t ldz);
+int lr_col_sumsq(lr_handle_t h, int dtype, int64_t m, int64_t r, const void* Z, int64_t ldz,
+                 double* out);
+int lr_scale_col(lr_handle_t h, int dtype, int64_t rows, const void* src, int64_t lds, double inv,
+                 void* dst, int64_t ldd);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LOWRANK_B200_H */

@@ -1,0 +1,545 @@
+"""numpy restatement of the reference's randomized-SVD hot path (CPU oracle).
+
+TEST INFRASTRUCTURE ONLY -- see oracle/__init__.py.  This module is the
+checker the CUDA path is compared against, and the CPU reference arm that
+bench.py times.  It restates the algorithms of the reference package
+``lowrank`` (``/root/reference/pkg/src/lowrank``) function by function; each
+function names the reference file:line it follows.  The reference is not
+imported here (it does not exist on the GPU box); instead tests/golden holds
+vectors produced by the reference itself (tests/golden/make_golden.py) and
+tests/test_oracle_golden.py pins this restatement to them.
+
+Arithmetic matches the reference: everything is promoted to float64 /
+complex128 (reference core.py:44-47, sketch.py:189), matrix products go
+through numpy/OpenBLAS, the small SVD through LAPACK gesdd.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+# reference config.py:9,19,22-23
+GS_DROP_TOL = 1e-10
+DEFAULT_OVERSAMPLE = 5
+DEFAULT_PROBES = 10
+DEFAULT_ALPHA = 10.0
+
+# Philox stream tags, reference sketch.py:26-29 and rangefinder.py:78
+STREAM_GAUSS = 0x67617573      # "gaus"
+STREAM_SRFT = 0x73726674       # "srft"
+STREAM_PROBE = 0x70726F62      # "prob"
+STREAM_SYNTH = 0x73796E74      # "synt"  (oracle.py:120)
+
+
+# ---------------------------------------------------------------------------
+# Random draws (host side; the CUDA path uploads the same arrays)
+
+def rng_for(seed, stream=0, index=0):
+    """Philox generator keyed by seed | stream<<64 | index<<96.
+
+    Follows reference sketch.py:32-42: the 128-bit Philox key packs the
+    64-bit seed, a 32-bit stream tag and a 32-bit draw index.
+    """
+    key = int(seed) % (1 << 64)
+    key |= (int(stream) % (1 << 32)) << 64
+    key |= (int(index) % (1 << 32)) << 96
+    return np.random.Generator(np.random.Philox(key=key))
+
+
+def gaussian_matrix(n, ell, seed):
+    """n x ell standard normals, row-major draw order (sketch.py:96-100)."""
+    if n < 1 or ell < 1:
+        raise ValueError("dimensions must be >= 1")
+    return rng_for(seed, STREAM_GAUSS).standard_normal((n, ell))
+
+
+def probe_matrix(n, r, seed):
+    """Estimator probes W (rangefinder.py:78)."""
+    return rng_for(seed, STREAM_PROBE).standard_normal((n, r))
+
+
+@dataclass
+class SrftDraw:
+    """Materialized SRFT test matrix scale * diag(d) F R (sketch.py:207-218)."""
+
+    n: int
+    ell: int
+    d: np.ndarray
+    picks: np.ndarray
+    scale: float
+
+
+def srft_operator(n, ell, seed):
+    """d = exp(2 pi i U[0,1)), then picks = permutation(n)[:ell] from the
+    same stream (sketch.py:246-256)."""
+    if ell > n:
+        raise ValueError("sample count exceeds dimension")
+    g = rng_for(seed, STREAM_SRFT)
+    d = np.exp(2j * np.pi * g.random(n))
+    picks = g.permutation(n)[:ell]
+    return SrftDraw(n=n, ell=ell, d=d, picks=picks, scale=float(np.sqrt(n / ell)))
+
+
+# ---------------------------------------------------------------------------
+# FFT (reference sketch.py:115-200): radix-2 for powers of two, chirp-z
+# (Bluestein) otherwise, unitary scaling n^-1/2.
+
+def _bit_reversal(n):
+    bits = n.bit_length() - 1
+    idx = np.arange(n)
+    rev = np.zeros(n, dtype=np.int64)
+    for b in range(bits):
+        rev |= ((idx >> b) & 1) << (bits - 1 - b)
+    return rev
+
+
+def fft_radix2(X, inverse=False):
+    """Unnormalized iterative radix-2 DIT FFT along the last axis
+    (sketch.py:129-148): bit-reverse, then log2(n) butterfly stages."""
+    n = X.shape[-1]
+    Y = np.ascontiguousarray(X[..., _bit_reversal(n)], dtype=np.complex128)
+    sgn = 1.0 if inverse else -1.0
+    span = 2
+    while span <= n:
+        h = span // 2
+        tw = np.exp(sgn * 2j * np.pi * np.arange(h) / span)
+        view = Y.reshape(Y.shape[:-1] + (n // span, span))
+        top = view[..., :h]
+        bot = view[..., h:] * tw
+        lo = top - bot
+        view[..., :h] = top + bot
+        view[..., h:] = lo
+        span *= 2
+    return Y
+
+
+def fft_bluestein(X, inverse=False):
+    """Arbitrary-length DFT by chirp convolution (sketch.py:155-176)."""
+    n = X.shape[-1]
+    sgn = 1.0 if inverse else -1.0
+    t = np.arange(n, dtype=np.int64)
+    w = np.exp(sgn * 1j * np.pi * ((t * t) % (2 * n)) / n)
+    L = 1 << (2 * n - 2).bit_length()
+    a = np.zeros(X.shape[:-1] + (L,), dtype=np.complex128)
+    a[..., :n] = X * w
+    b = np.zeros(L, dtype=np.complex128)
+    b[:n] = np.conj(w)
+    b[L - n + 1:] = np.conj(w[1:][::-1])
+    conv = fft_radix2(fft_radix2(a) * fft_radix2(b[None, :])[0], inverse=True) / L
+    return conv[..., :n] * w
+
+
+def dft(v, axis=-1):
+    """Unitary DFT, f_pq = n^-1/2 exp(-2 pi i pq / n) (sketch.py:179-200)."""
+    v = np.asarray(v)
+    if v.ndim == 0:
+        raise ValueError("dft expects a vector or matrix")
+    X = np.moveaxis(v, axis, -1).astype(np.complex128)
+    n = X.shape[-1]
+    if n == 1:
+        out = X.copy()
+    elif n & (n - 1) == 0:
+        out = fft_radix2(X)
+    else:
+        out = fft_bluestein(X)
+    return np.moveaxis(out / np.sqrt(n), -1, axis)
+
+
+def srft_apply(A, draw):
+    """Y = scale * dft(A * d)[:, picks] (sketch.py:306-320)."""
+    A = np.asarray(A)
+    if draw.n != A.shape[1]:
+        raise ValueError("operator dimension does not match matrix columns")
+    return dft(A * draw.d[None, :], axis=1)[:, draw.picks] * draw.scale
+
+
+# ---------------------------------------------------------------------------
+# Dense kernels (reference core.py)
+
+def as_matrix(a):
+    """2-D, nonempty, finite; promoted to float64/complex128 (core.py:33-50)."""
+    arr = np.asarray(a)
+    if arr.ndim != 2:
+        raise ValueError(f"matrix must be 2-D, got shape {arr.shape}")
+    if arr.size == 0:
+        raise ValueError("matrix must be nonempty")
+    arr = arr.astype(np.complex128 if np.iscomplexobj(arr) else np.float64, copy=False)
+    if not np.all(np.isfinite(arr)):
+        raise ValueError("matrix contains non-finite entries")
+    return arr
+
+
+def orthonormalize_double_gs(Y, tol=GS_DROP_TOL):
+    """Column-wise classical Gram-Schmidt with one reorthogonalization
+    (core.py:84-115).  Column j is dropped when its residual after the first
+    projection is <= tol * ||Y||_F (or exactly zero), or when the residual
+    after the second projection is exactly zero.  Accepted columns are kept
+    in a Fortran-ordered buffer instead of being re-stacked every step; the
+    arithmetic per column is the reference's w - Q (Q* w), twice."""
+    Y = np.asarray(Y)
+    m, ell = Y.shape
+    cplx = np.iscomplexobj(Y)
+    dt = np.complex128 if cplx else np.float64
+    fro = np.linalg.norm(Y)
+    buf = np.zeros((m, ell), dtype=dt, order="F")
+    kept = 0
+    for j in range(ell):
+        w = Y[:, j].astype(dt)
+        Q = buf[:, :kept]
+        if kept:
+            w = w - Q @ (Q.conj().T @ w)
+        nrm = np.linalg.norm(w)
+        if nrm <= tol * fro or nrm == 0.0:
+            continue
+        if kept:
+            w = w - Q @ (Q.conj().T @ w)
+        nrm = np.linalg.norm(w)
+        if nrm == 0.0:
+            continue
+        buf[:, kept] = w / nrm
+        kept += 1
+    if kept == 0:
+        return np.zeros((m, 0), dtype=Y.dtype)
+    return np.ascontiguousarray(buf[:, :kept])
+
+
+def plain_gs(Y):
+    """Unsafeguarded single-pass CGS, no drops (rangefinder.py:169-184)."""
+    Q = np.array(Y, dtype=np.complex128 if np.iscomplexobj(Y) else np.float64)
+    for j in range(Q.shape[1]):
+        for i in range(j):
+            Q[:, j] -= Q[:, i] * np.vdot(Q[:, i], Q[:, j])
+        nrm = np.linalg.norm(Q[:, j])
+        if nrm > 0:
+            Q[:, j] /= nrm
+    return Q
+
+
+@dataclass
+class SmallSVD:
+    U: np.ndarray
+    sigma: np.ndarray
+    V: np.ndarray
+
+
+def sign_fix(U, V):
+    """Rotate the first entry of each left vector with |u| > 1e-10 max|u|
+    onto the positive real axis; V absorbs the same phase (core.py:221-229)."""
+    for j in range(U.shape[1]):
+        mag = np.abs(U[:, j])
+        top = mag.max() if mag.size else 0.0
+        idx = np.flatnonzero(mag > 1e-10 * top)
+        if idx.size == 0:
+            continue
+        z = U[idx[0], j]
+        ph = z / abs(z)
+        U[:, j] *= np.conj(ph)
+        V[:, j] *= np.conj(ph)
+    return U, V
+
+
+def small_svd(B):
+    """Thin SVD by LAPACK gesdd, gesvd retry (core.py:199-230)."""
+    B = np.asarray(B)
+    try:
+        U, s, Vh = np.linalg.svd(B, full_matrices=False)
+    except np.linalg.LinAlgError:
+        import scipy.linalg
+        U, s, Vh = scipy.linalg.svd(B, full_matrices=False, lapack_driver="gesvd")
+    V = Vh.conj().T
+    U, V = sign_fix(U, V)
+    return SmallSVD(U=U, sigma=s.astype(np.float64), V=V)
+
+
+# ---------------------------------------------------------------------------
+# Operators (core.py:332-402)
+
+@dataclass
+class Counters:
+    matvecs: int = 0
+    adjoint_matvecs: int = 0
+    passes: int = 0
+    flops: int = 0
+
+
+class Operator:
+    """Counting m x n operator: apply / apply_adjoint add cols matvecs, one
+    pass and 2*m*n*cols flops each (core.py:360-374)."""
+
+    def __init__(self, m, n):
+        self.m, self.n = int(m), int(n)
+        self.counters = Counters()
+
+    @property
+    def shape(self):
+        return (self.m, self.n)
+
+    def _count(self, X, adjoint):
+        cols = 1 if np.ndim(X) == 1 else np.shape(X)[1]
+        if adjoint:
+            self.counters.adjoint_matvecs += cols
+        else:
+            self.counters.matvecs += cols
+        self.counters.passes += 1
+        self.counters.flops += 2 * self.m * self.n * cols
+
+    def apply(self, X):
+        self._count(X, False)
+        return self._apply(np.asarray(X))
+
+    def apply_adjoint(self, Y):
+        self._count(Y, True)
+        return self._apply_adjoint(np.asarray(Y))
+
+
+class Dense(Operator):
+    """In-memory dense A (core.py:383-395), promoted by as_matrix."""
+
+    def __init__(self, A, promote=True):
+        A = as_matrix(A) if promote else np.asarray(A)
+        super().__init__(*A.shape)
+        self.array = A
+
+    def _apply(self, X):
+        return self.array @ X
+
+    def _apply_adjoint(self, Y):
+        return self.array.conj().T @ Y
+
+
+class Blockwise(Operator):
+    """Row-block fp64 application of a lower-precision stored A.
+
+    Arithmetic-identical to Dense(A) (each block is promoted to float64 and
+    multiplied) without holding an fp64 copy of all of A; the row-block
+    structure follows the reference's RowBlockStream (io.py:319-388).  Used
+    for the config-4 CPU baseline, whose fp64 upcast would not fit in host
+    RAM."""
+
+    def __init__(self, A, block_rows=65536):
+        super().__init__(*A.shape)
+        self.array = A
+        self.block = int(block_rows)
+
+    def _apply(self, X):
+        X = np.asarray(X, dtype=np.float64)
+        out = np.empty((self.m,) + X.shape[1:], dtype=np.float64)
+        for r in range(0, self.m, self.block):
+            out[r:r + self.block] = self.array[r:r + self.block].astype(np.float64) @ X
+        return out
+
+    def _apply_adjoint(self, Y):
+        Y = np.asarray(Y, dtype=np.float64)
+        acc = np.zeros((self.n,) + Y.shape[1:], dtype=np.float64)
+        for r in range(0, self.m, self.block):
+            acc += self.array[r:r + self.block].astype(np.float64).T @ Y[r:r + self.block]
+        return acc
+
+
+class SparsePlusLowRank(Operator):
+    """S + L R^T with S in scipy CSR (config 5; no reference code exists for
+    sparse A -- SURVEY.md §8c "parity unpinned" -- so this is the user
+    MatVecOperator subclass the survey prescribes)."""
+
+    def __init__(self, S, L, R):
+        super().__init__(*S.shape)
+        self.S, self.L, self.R = S, np.asarray(L), np.asarray(R)
+        self.St = S.T.tocsr()
+
+    def _apply(self, X):
+        return self.S @ X + self.L @ (self.R.T @ X)
+
+    def _apply_adjoint(self, Y):
+        return self.St @ Y + self.R @ (self.L.T @ Y)
+
+
+def as_operator(A):
+    return A if isinstance(A, Operator) else Dense(A)
+
+
+# ---------------------------------------------------------------------------
+# Stage A (rangefinder.py)
+
+@dataclass
+class RangeBasis:
+    Q: np.ndarray
+    samples_used: int
+    passes: int
+    est_error: float | None
+    kind: str = "gaussian"
+    ell: int = 1
+    power_q: int = 0
+    seed: int = 0
+    diagnostics: dict = field(default_factory=dict)
+
+
+def _check_ell(op, ell):
+    if not 1 <= ell <= min(op.shape):
+        raise ValueError("ell must satisfy 1 <= ell <= min(m, n)")
+
+
+def randomized_range_finder(A, ell, seed, ortho_tol=GS_DROP_TOL):
+    """Alg 4.1 (rangefinder.py:49-62): Q = DGS(A Omega), one pass."""
+    op = as_operator(A)
+    _check_ell(op, ell)
+    Q = orthonormalize_double_gs(op.apply(gaussian_matrix(op.n, ell, seed)), tol=ortho_tol)
+    return RangeBasis(Q=Q, samples_used=ell, passes=1,
+                      est_error=0.0 if Q.shape[1] == 0 else None, ell=ell, seed=seed)
+
+
+def power_iteration_range(A, ell, q, seed, ortho_tol=GS_DROP_TOL, safeguarded=True):
+    """Alg 4.3 (rangefinder.py:187-218): orthonormalize (A A*)^q A Omega."""
+    if q < 0:
+        raise ValueError("q must be nonnegative")
+    op = as_operator(A)
+    _check_ell(op, ell)
+    Y = op.apply(gaussian_matrix(op.n, ell, seed))
+    for _ in range(q):
+        Y = op.apply(op.apply_adjoint(Y))
+    Q = orthonormalize_double_gs(Y, tol=ortho_tol) if safeguarded else plain_gs(Y)
+    return RangeBasis(Q=Q, samples_used=ell, passes=2 * q + 2,
+                      est_error=0.0 if Q.shape[1] == 0 else None, ell=ell,
+                      power_q=q, seed=seed)
+
+
+def subspace_iteration_range(A, ell, q, seed, ortho_tol=GS_DROP_TOL):
+    """Alg 4.4 (rangefinder.py:221-243): re-orthonormalize after every
+    application of A and A*."""
+    if q < 0:
+        raise ValueError("q must be nonnegative")
+    op = as_operator(A)
+    _check_ell(op, ell)
+    Q = orthonormalize_double_gs(op.apply(gaussian_matrix(op.n, ell, seed)), tol=ortho_tol)
+    for _ in range(q):
+        Qt = orthonormalize_double_gs(op.apply_adjoint(Q), tol=ortho_tol)
+        Q = orthonormalize_double_gs(op.apply(Qt), tol=ortho_tol)
+    return RangeBasis(Q=Q, samples_used=ell, passes=2 * q + 2,
+                      est_error=0.0 if Q.shape[1] == 0 else None, ell=ell,
+                      power_q=q, seed=seed)
+
+
+def fast_range_finder(A, ell, seed, ortho_tol=GS_DROP_TOL):
+    """Alg 4.5 with the SRFT (rangefinder.py:246-266)."""
+    A = np.asarray(A)
+    Y = srft_apply(A, srft_operator(A.shape[1], ell, seed))
+    diag = {}
+    if not np.iscomplexobj(A):
+        diag["max_imag_sample"] = float(np.abs(Y.imag).max())
+    Q = orthonormalize_double_gs(Y, tol=ortho_tol)
+    return RangeBasis(Q=Q, samples_used=ell, passes=1,
+                      est_error=0.0 if Q.shape[1] == 0 else None, kind="srft",
+                      ell=ell, seed=seed, diagnostics=diag)
+
+
+def posterior_error_estimate(A, Q, r=DEFAULT_PROBES, alpha=DEFAULT_ALPHA, seed=0):
+    """alpha sqrt(2/pi) max_i ||(I - QQ*) A w_i|| (rangefinder.py:65-82)."""
+    if r < 1:
+        raise ValueError("r must be >= 1")
+    if alpha <= 1:
+        raise ValueError("alpha must exceed 1")
+    op = as_operator(A)
+    Z = op.apply(probe_matrix(op.n, r, seed))
+    if Q.shape[1]:
+        Z = Z - Q @ (Q.conj().T @ Z)
+    return float(alpha * math.sqrt(2.0 / math.pi) * np.linalg.norm(Z, axis=0).max())
+
+
+# ---------------------------------------------------------------------------
+# Stage B (factor.py)
+
+@dataclass
+class PartialSVD:
+    U: np.ndarray
+    sigma: np.ndarray
+    V: np.ndarray
+
+    def compose(self):
+        return (self.U * self.sigma) @ self.V.conj().T
+
+
+def direct_svd(A, Q):
+    """Alg 5.1 (factor.py:154-165): B = (A* Q)*, small SVD, U = Q U~."""
+    op = as_operator(A)
+    if Q.shape[0] != op.m:
+        raise ValueError("basis rows must match matrix rows")
+    f = small_svd(op.apply_adjoint(Q).conj().T)
+    return PartialSVD(U=Q @ f.U, sigma=f.sigma, V=f.V)
+
+
+def truncate_rank(f, k):
+    """Top-k slice (factor.py:408-426, PartialSVD branch)."""
+    if k > len(f.sigma):
+        raise ValueError("k exceeds current rank")
+    return PartialSVD(U=f.U[:, :k], sigma=f.sigma[:k], V=f.V[:, :k])
+
+
+# ---------------------------------------------------------------------------
+# Verification helpers (reference oracle.py)
+
+def exact_projection_error(A, Q, norm="spectral"):
+    """||(I - QQ*) A|| by explicit residual (oracle.py:25-40)."""
+    A = np.asarray(A)
+    R = A - Q @ (Q.conj().T @ A) if Q.shape[1] else A
+    if norm == "spectral":
+        return float(np.linalg.svd(R, compute_uv=False)[0]) if min(R.shape) else 0.0
+    return float(np.linalg.norm(R))
+
+
+def principal_angles(Q1, Q2):
+    """Principal angles between two orthonormal bases."""
+    s = np.linalg.svd(Q1.conj().T @ Q2, compute_uv=False)
+    return np.arccos(np.clip(s, -1.0, 1.0))
+
+
+def jacobi_singular_values(A, sweeps=60, tol=1e-15):
+    """One-sided cyclic Jacobi singular values -- an SVD cross-check that does
+    not share LAPACK's code path (cf. reference oracle.py:230-267)."""
+    M = np.array(A, dtype=np.float64)
+    if M.shape[0] < M.shape[1]:
+        M = M.T.copy()
+    n = M.shape[1]
+    for _ in range(sweeps):
+        off = 0.0
+        for p in range(n - 1):
+            for q in range(p + 1, n):
+                a = M[:, p] @ M[:, p]
+                b = M[:, q] @ M[:, q]
+                c = M[:, p] @ M[:, q]
+                if abs(c) <= tol * math.sqrt(a * b) or c == 0.0:
+                    continue
+                off = max(off, abs(c) / math.sqrt(a * b))
+                zeta = (b - a) / (2.0 * c)
+                t = math.copysign(1.0, zeta) / (abs(zeta) + math.sqrt(1.0 + zeta * zeta))
+                cs = 1.0 / math.sqrt(1.0 + t * t)
+                sn = cs * t
+                mp = M[:, p].copy()
+                M[:, p] = cs * mp - sn * M[:, q]
+                M[:, q] = sn * mp + cs * M[:, q]
+        if off <= tol:
+            break
+    return np.sort(np.linalg.norm(M, axis=0))[::-1]
+
+
+def rsvd(A, k, p, q, seed, sketch="gauss", probes=DEFAULT_PROBES, alpha=DEFAULT_ALPHA,
+         estimate=True):
+    """The composition the reference CLI calls "randomized SVD"
+    (cli.py:128-173 Stage-A dispatch, 222-262 _cmd_svd): ell = k + p;
+    gauss q>0 -> Alg 4.4, gauss q=0 -> Alg 4.1, srft -> Alg 4.5; then
+    direct_svd and the posterior estimate with seed + 13."""
+    op = as_operator(A)
+    ell = k + p
+    if sketch == "gauss":
+        basis = (subspace_iteration_range(op, ell, q, seed) if q > 0
+                 else randomized_range_finder(op, ell, seed))
+    else:
+        if q > 0:
+            raise ValueError("power iterations are not available with structured sketches")
+        basis = fast_range_finder(op.array, ell, seed)
+    f = direct_svd(op, basis.Q)
+    est = basis.est_error
+    if est is None and estimate:
+        est = posterior_error_estimate(op, basis.Q, r=probes, alpha=alpha, seed=seed + 13)
+    return basis, f, est

@@ -1,0 +1,11 @@
+"""Numerical defaults of the hot path (reference config.py:9,19,22-23)."""
+
+# Gram-Schmidt drop tolerance relative to ||Y||_F (orthonormalize_double_gs).
+GS_DROP_TOL = 1e-10
+
+# Fixed-rank sketches default to k + DEFAULT_OVERSAMPLE samples.
+DEFAULT_OVERSAMPLE = 5
+
+# Posterior error estimator: probe count and inflation factor.
+DEFAULT_PROBES = 10
+DEFAULT_ALPHA = 10.0

@@ -1,0 +1,421 @@
+"""Dense kernels and the operator protocol, computed on the GPU.
+
+Mirrors the hot-path part of the reference's ``lowrank.core``
+(/root/reference/pkg/src/lowrank/core.py): the MatVecOperator protocol with
+its pass / matvec / flop counters (core.py:332-380), a dense operator
+(core.py:383-395), double-Gram-Schmidt orthonormalization (core.py:84-115)
+and the small SVD with the reference sign convention (core.py:190-230).
+
+Arrays: numpy inputs give numpy outputs (the reference's contract); torch
+CUDA tensors stay on the device and give torch tensors.  All arithmetic runs
+in liblowrank_b200 (no CPU fallback).  One deliberate difference
+(SURVEY.md §7 H9): the reference promotes every input to float64 /
+complex128 (core.py:44-47); here float32 / complex64 inputs are computed in
+their own precision (with the tensor-core split scheme of DESIGN.md for the
+passes over A), float64 / complex128 in theirs, anything else is promoted
+to float64 / complex128 like the reference.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib, config
+from ._lib import ConvergenceError, NotPSDError  # noqa: F401  (re-exported, core.py:25-30)
+
+
+def _torch():
+    import torch
+    return torch
+
+
+# ---------------------------------------------------------------------------
+# array plumbing
+
+_NP_KEEP = (np.float32, np.float64, np.complex64, np.complex128)
+
+
+def _np_compute_dtype(dt):
+    dt = np.dtype(dt)
+    if dt.type in _NP_KEEP:
+        return dt
+    return np.dtype(np.complex128) if np.issubdtype(dt, np.complexfloating) else np.dtype(np.float64)
+
+
+def _torch_compute_dtype(t):
+    torch = _torch()
+    if t.dtype in (torch.float32, torch.float64, torch.complex64, torch.complex128):
+        return t.dtype
+    return torch.complex128 if t.is_complex() else torch.float64
+
+
+def is_device_array(x):
+    torch = _torch()
+    return torch.is_tensor(x)
+
+
+def to_device(x, dtype=None, device=None):
+    """numpy / torch -> row-major CUDA tensor (H2D copy for host data)."""
+    torch = _torch()
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    if torch.is_tensor(x):
+        t = x
+        if t.device != dev:
+            t = t.to(dev, non_blocking=True)
+        if dtype is not None and t.dtype != dtype:
+            t = cast_dev(t, dtype)
+    else:
+        a = np.asarray(x)
+        a = a.astype(_np_compute_dtype(a.dtype), copy=False)
+        if dtype is not None:
+            want = {torch.float32: np.float32, torch.float64: np.float64,
+                    torch.complex64: np.complex64, torch.complex128: np.complex128}[dtype]
+            a = a.astype(want, copy=False)
+        t = torch.from_numpy(np.ascontiguousarray(a)).to(dev, non_blocking=False)
+    if t.dim() == 2 and t.shape[1] > 1 and t.stride(1) != 1:
+        t = t.contiguous()
+    if t.dim() == 1 and t.stride(0) != 1:
+        t = t.contiguous()
+    return t
+
+
+def cast_dev(t, dtype):
+    """Device dtype conversion with the library's cast kernel (real ->
+    complex zero-fills the imaginary part)."""
+    if t.dtype == dtype:
+        return t
+    torch = _torch()
+    t2, vec = _as2d(t)
+    if t2.shape[1] > 1 and t2.stride(1) != 1:
+        t2 = t2.contiguous()
+    out = torch.empty(t2.shape, dtype=dtype, device=t2.device)
+    if out.numel():
+        _lib.call("lr_copy", _lib.handle(t2.device.index), _lib.dtype_code(t2.dtype), _lib.ptr(t2),
+                  _lib.ld(t2), _lib.dtype_code(dtype), _lib.ptr(out), _lib.ld(out),
+                  t2.shape[0], t2.shape[1], 0)
+    return out.reshape(-1) if vec else out
+
+
+def to_host(t):
+    return t.detach().cpu().numpy()
+
+
+def _out(t, host):
+    return to_host(t) if host else t
+
+
+def _as2d(t):
+    return (t.reshape(-1, 1), True) if t.dim() == 1 else (t, False)
+
+
+# ---------------------------------------------------------------------------
+# operators (reference core.py:332-402)
+
+@dataclass
+class OperatorCounters:
+    matvecs: int = 0
+    adjoint_matvecs: int = 0
+    passes: int = 0
+    flops: int = 0
+
+    def reset(self):
+        self.matvecs = self.adjoint_matvecs = self.passes = self.flops = 0
+
+
+class MatVecOperator:
+    """Abstract m-by-n linear map with matvec / pass / flop accounting.
+
+    Same protocol as reference core.py:343-380: subclasses implement
+    ``_apply`` / ``_apply_adjoint`` on column blocks; ``apply`` counts
+    ``cols`` matvecs, one pass and 2*m*n*cols flops.  Operators that set
+    ``device_native = True`` receive and return CUDA tensors; others (e.g. a
+    user's numpy operator) receive numpy arrays from the GPU pipeline.
+    """
+
+    device_native = False
+
+    def __init__(self, m, n):
+        self.m = int(m)
+        self.n = int(n)
+        self.counters = OperatorCounters()
+
+    @property
+    def shape(self):
+        return (self.m, self.n)
+
+    def _count(self, X, adjoint):
+        cols = 1 if X.ndim == 1 else X.shape[1]
+        if adjoint:
+            self.counters.adjoint_matvecs += cols
+        else:
+            self.counters.matvecs += cols
+        self.counters.passes += 1
+        self.counters.flops += 2 * self.m * self.n * cols
+
+    def apply(self, X):
+        if not is_device_array(X):
+            X = np.asarray(X)
+        self._count(X, False)
+        return self._apply(X)
+
+    def apply_adjoint(self, Y):
+        if not is_device_array(Y):
+            Y = np.asarray(Y)
+        self._count(Y, True)
+        return self._apply_adjoint(Y)
+
+    def _apply(self, X):  # pragma: no cover - abstract
+        raise NotImplementedError
+
+    def _apply_adjoint(self, Y):  # pragma: no cover - abstract
+        raise NotImplementedError
+
+
+class DenseOperator(MatVecOperator):
+    """GPU-resident dense A: one pass per apply (K1 / K2 kernels).
+
+    Replaces the reference DenseOperator (core.py:383-395).  Construction
+    performs the as_matrix checks (2-D, nonempty, finite; core.py:33-50) on
+    the device and keeps A in HBM; numpy inputs are uploaded once.
+    """
+
+    device_native = True
+
+    def __init__(self, A, device=None, validate=True):
+        torch = _torch()
+        host = not torch.is_tensor(A)
+        shape = np.shape(A) if host else tuple(A.shape)
+        if len(shape) != 2:
+            raise ValueError(f"matrix must be 2-D, got shape {shape}")
+        if shape[0] == 0 or shape[1] == 0:
+            raise ValueError("matrix must be nonempty")
+        t = to_device(A, None if host else _torch_compute_dtype(A), device)
+        super().__init__(*t.shape)
+        self.array = t
+        self.code = _lib.dtype_code(t.dtype)
+        self.host_io = host
+        self.amax = None
+        if validate:
+            self.validate()
+
+    def validate(self):
+        torch = _torch()
+        res = torch.empty(2, dtype=torch.float64, device=self.array.device)
+        bad = torch.empty(1, dtype=torch.int64, device=self.array.device)
+        _lib.call("lr_check_finite", _lib.handle(self.array.device.index), self.code, self.m,
+                  self.n, _lib.ptr(self.array), _lib.ld(self.array), _lib.ptr(bad), _lib.ptr(res))
+        nb = int(bad.item())
+        if nb:
+            raise ValueError("matrix contains non-finite entries")
+        self.amax = float(res[0].item())
+
+    @property
+    def dtype(self):
+        return self.array.dtype
+
+    def _prep(self, X):
+        host = not is_device_array(X)
+        t = to_device(X, self.array.dtype, self.array.device.index)
+        t, vec = _as2d(t)
+        return t, host, vec
+
+    def _apply(self, X):
+        torch = _torch()
+        t, host, vec = self._prep(X)
+        if t.shape[0] != self.n:
+            raise ValueError(f"dimension mismatch: A is {self.shape}, X has {t.shape[0]} rows")
+        Y = torch.empty((self.m, t.shape[1]), dtype=self.array.dtype, device=self.array.device)
+        _timed_pass(self.array, t, Y, False)
+        Y = Y.reshape(-1) if vec else Y
+        return _out(Y, host)
+
+    def _apply_adjoint(self, Y):
+        torch = _torch()
+        t, host, vec = self._prep(Y)
+        if t.shape[0] != self.m:
+            raise ValueError(f"dimension mismatch: A is {self.shape}, Y has {t.shape[0]} rows")
+        Z = torch.empty((self.n, t.shape[1]), dtype=self.array.dtype, device=self.array.device)
+        _timed_pass(self.array, t, Z, True)
+        Z = Z.reshape(-1) if vec else Z
+        return _out(Z, host)
+
+
+CudaDenseOperator = DenseOperator
+
+# Optional per-pass timing (bench.py): a list that receives
+# (start_event, end_event, algorithmic_flops, a_bytes, cols) for every pass
+# over a dense A, recorded on the launching stream.
+PASS_EVENTS = None
+
+
+def _timed_pass(A, X, Y, adjoint):
+    if PASS_EVENTS is None:
+        gemm(A, X, Y, adjoint=adjoint)
+        return
+    torch = _torch()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    gemm(A, X, Y, adjoint=adjoint)
+    e.record()
+    m, n = A.shape
+    mult = 4 if A.is_complex() else 1
+    PASS_EVENTS.append((s, e, 2 * mult * m * n * X.shape[1], A.numel() * A.element_size(),
+                        X.shape[1]))
+
+
+class ForeignOperator(MatVecOperator):
+    """Adapter for duck-typed operators (e.g. the reference's own
+    MatVecOperator subclasses): host numpy in, host numpy out."""
+
+    def __init__(self, op):
+        super().__init__(*op.shape)
+        self.op = op
+
+    def _apply(self, X):
+        return np.asarray(self.op.apply(X))
+
+    def _apply_adjoint(self, Y):
+        return np.asarray(self.op.apply_adjoint(Y))
+
+
+def as_operator(A):
+    """Wrap a dense array as DenseOperator; pass operators through
+    (reference core.py:398-402)."""
+    if isinstance(A, MatVecOperator):
+        return A
+    if hasattr(A, "apply") and hasattr(A, "apply_adjoint") and hasattr(A, "shape"):
+        return ForeignOperator(A)
+    return DenseOperator(A)
+
+
+def apply_dev(op, X, adjoint=False):
+    """Apply an operator to a device tensor, whatever kind of operator it is."""
+    if op.device_native:
+        return op.apply_adjoint(X) if adjoint else op.apply(X)
+    Xh = to_host(X)
+    R = op.apply_adjoint(Xh) if adjoint else op.apply(Xh)
+    return to_device(np.asarray(R), X.dtype, X.device.index)
+
+
+# ---------------------------------------------------------------------------
+# thin wrappers over the C ABI (device tensors in, device tensors out)
+
+def gemm(A, X, Y, adjoint=False):
+    """Y = A X (adjoint=False) or Y = A^H X -- one pass over A."""
+    code = _lib.dtype_code(A.dtype)
+    op = _lib.OP_N if not adjoint else (_lib.OP_C if A.is_complex() else _lib.OP_T)
+    m, n = A.shape
+    _lib.call("lr_gemm", _lib.handle(A.device.index), code, op, m, n, X.shape[1], _lib.ptr(A),
+              _lib.ld(A), _lib.ptr(X), _lib.ld(X), _lib.ptr(Y), _lib.ld(Y))
+    return Y
+
+
+def gemm_dev(A, X, Y):
+    """Y = A X for device matrices (the small products U = Q U~ etc.)."""
+    return gemm(A, X, Y, adjoint=False)
+
+
+def small_svd_from_adjoint(Z):
+    """SVD of B = Z^H given Z (c x r, r <= c) -- the layout the adjoint pass
+    of direct_svd produces.  Z is consumed (overwritten)."""
+    torch = _torch()
+    c, r = Z.shape
+    if Z.stride(1) != 1 or Z.stride(0) != r:
+        Z = Z.contiguous()
+    code = _lib.dtype_code(Z.dtype)
+    U = torch.empty((r, r), dtype=Z.dtype, device=Z.device)
+    S = torch.empty(r, dtype=torch.float64, device=Z.device)
+    V = torch.empty((c, r), dtype=Z.dtype, device=Z.device)
+    _lib.call("lr_small_svd", _lib.handle(Z.device.index), code, r, c, _lib.ptr(Z), _lib.ptr(U),
+              _lib.ptr(S), _lib.ptr(V))
+    return U, S, V
+
+
+def orth_dev(Y, tol=config.GS_DROP_TOL):
+    """Device orthonormalization; returns a (possibly narrower) view."""
+    torch = _torch()
+    m, ell = Y.shape
+    if ell == 0 or m == 0:
+        return torch.zeros((m, 0), dtype=Y.dtype, device=Y.device)
+    Q = torch.empty((m, ell), dtype=Y.dtype, device=Y.device)
+    rank = C.c_int64(0)
+    _lib.call("lr_orth", _lib.handle(Y.device.index), _lib.dtype_code(Y.dtype), m, ell,
+              _lib.ptr(Y), _lib.ld(Y), _lib.ptr(Q), _lib.ld(Q), float(tol), C.byref(rank))
+    r = int(rank.value)
+    return Q if r == ell else Q[:, :r]
+
+
+def orthonormalize_double_gs(Y, tol=config.GS_DROP_TOL):
+    """Orthonormalize the columns of Y (replaces reference core.py:84-115).
+
+    Same contract as the reference: columns whose residual after projection
+    onto the previously accepted columns is <= tol * ||Y||_F are dropped;
+    the result spans a subspace of range(Y); an all-zero Y gives a
+    zero-column result.  Computed on the GPU by CholeskyQR2 with an fp64 Gram
+    (the Cholesky pivots *are* the residual norms), falling back to shifted
+    CholeskyQR3 and then to column-wise CGS2 when a pivot is too small to be
+    resolved from the Gram.
+    """
+    host = not is_device_array(Y)
+    t = to_device(Y)
+    if t.dim() != 2:
+        raise ValueError("Y must be 2-D")
+    return _out(orth_dev(t, tol), host)
+
+
+@dataclass
+class SmallSVD:
+    """Full SVD B = U @ diag(sigma) @ V*, singular values descending."""
+
+    U: object
+    sigma: object
+    V: object
+
+
+def small_svd_dev(B):
+    """Thin SVD of a device matrix B (r x c); returns device tensors."""
+    torch = _torch()
+    r, c = B.shape
+    code = _lib.dtype_code(B.dtype)
+    h = _lib.handle(B.device.index)
+    if r == 0 or c == 0:
+        k = min(r, c)
+        return (torch.zeros((r, k), dtype=B.dtype, device=B.device),
+                torch.zeros(k, dtype=torch.float64, device=B.device),
+                torch.zeros((c, k), dtype=B.dtype, device=B.device))
+    if r <= c:
+        Bh = torch.empty((c, r), dtype=B.dtype, device=B.device)
+        _lib.call("lr_copy", h, code, _lib.ptr(B), _lib.ld(B), code, _lib.ptr(Bh), _lib.ld(Bh),
+                  c, r, 1)
+        U = torch.empty((r, r), dtype=B.dtype, device=B.device)
+        S = torch.empty(r, dtype=torch.float64, device=B.device)
+        V = torch.empty((c, r), dtype=B.dtype, device=B.device)
+        _lib.call("lr_small_svd", h, code, r, c, _lib.ptr(Bh), _lib.ptr(U), _lib.ptr(S),
+                  _lib.ptr(V))
+        return U, S, V
+    # tall B: SVD of B^H (c x r, c < r), B = V' S U'^H
+    Bc = B.contiguous().clone()
+    U1 = torch.empty((c, c), dtype=B.dtype, device=B.device)
+    S = torch.empty(c, dtype=torch.float64, device=B.device)
+    V1 = torch.empty((r, c), dtype=B.dtype, device=B.device)
+    _lib.call("lr_small_svd", h, code, c, r, _lib.ptr(Bc), _lib.ptr(U1), _lib.ptr(S),
+              _lib.ptr(V1))
+    U, V = V1, U1
+    _lib.call("lr_sign_fix", h, code, r, c, c, _lib.ptr(U), _lib.ld(U), _lib.ptr(V), _lib.ld(V))
+    return U, S, V
+
+
+def small_svd(B):
+    """Thin SVD with the reference's deterministic sign convention
+    (core.py:199-230): sigma descending; the first entry of each left
+    vector with |u| > 1e-10 max|u| is real positive and V absorbs the
+    phase.  A non-converging iteration raises ConvergenceError."""
+    host = not is_device_array(B)
+    t = to_device(B)
+    if t.dim() != 2:
+        raise ValueError("B must be 2-D")
+    U, S, V = small_svd_dev(t)
+    return SmallSVD(U=_out(U, host), sigma=_out(S, host), V=_out(V, host))

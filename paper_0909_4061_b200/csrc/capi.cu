@@ -1,0 +1,676 @@
+// extern "C" entry points of liblowrank_b200 and the composite algorithms
+// (orthonormalization, small SVD, estimator tail) built from the kernels.
+#include <cstring>
+#include <stdexcept>
+
+#include "common.cuh"
+
+namespace lr {
+
+unsigned long long g_launches = 0;
+
+namespace {
+thread_local std::string g_err;
+
+// unit roundoff of the arithmetic the Gram / Cholesky run in (always fp64)
+constexpr double U64 = 1.1102230246251565e-16;
+
+int wide_of(int dtype) { return is_complex(dtype) ? LR_C128 : LR_F64; }
+size_t wide_size(int dtype) { return is_complex(dtype) ? 16 : 8; }
+
+struct Info {
+  int32_t rank, unresolved, bad;
+};
+
+Info read_info(Handle* h, const int32_t* d) {
+  LR_CUDA(cudaMemcpyAsync(h->h_info, d, 3 * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
+  LR_CUDA(cudaStreamSynchronize(h->stream));
+  return Info{h->h_info[0], h->h_info[1], h->h_info[2]};
+}
+
+// ---- dtype dispatch of the kernels ------------------------------------------------
+
+void gemm_any(Handle* h, int dtype, bool trans, bool conj, int64_t M, int64_t N, int64_t K,
+              const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc) {
+  switch (dtype) {
+    case LR_F64:
+      gemm_f64(h, trans, M, N, K, static_cast<const double*>(A), lda,
+               static_cast<const double*>(B), ldb, static_cast<double*>(C), ldc);
+      return;
+    case LR_C128:
+      gemm_c128(h, trans, conj, M, N, K, static_cast<const double2*>(A), lda,
+                static_cast<const double2*>(B), ldb, static_cast<double2*>(C), ldc);
+      return;
+    case LR_F32:
+      if (h->f32_mode == LR_F32_SIMT)
+        gemm_f32_simt(h, trans, M, N, K, static_cast<const float*>(A), lda,
+                      static_cast<const float*>(B), ldb, static_cast<float*>(C), ldc);
+      else
+        gemm_f32(h, trans, M, N, K, static_cast<const float*>(A), lda,
+                 static_cast<const float*>(B), ldb, static_cast<float*>(C), ldc);
+      return;
+    case LR_C64:
+      if (h->f32_mode == LR_F32_SIMT)
+        gemm_c64_simt(h, trans, conj, M, N, K, static_cast<const float2*>(A), lda,
+                      static_cast<const float2*>(B), ldb, static_cast<float2*>(C), ldc);
+      else
+        gemm_c64(h, trans, conj, M, N, K, static_cast<const float2*>(A), lda,
+                 static_cast<const float2*>(B), ldb, static_cast<float2*>(C), ldc);
+      return;
+  }
+  throw Error{LR_EINVAL, "unknown dtype"};
+}
+
+// G (ell x ell, wide) = Y^H Y
+void gram_any(Handle* h, int dtype, int64_t m, int64_t ell, const void* Y, int64_t ldy, void* G) {
+  switch (dtype) {
+    case LR_F64:
+      gemm_f64(h, true, ell, ell, m, static_cast<const double*>(Y), ldy,
+               static_cast<const double*>(Y), ldy, static_cast<double*>(G), ell);
+      return;
+    case LR_C128:
+      gemm_c128(h, true, true, ell, ell, m, static_cast<const double2*>(Y), ldy,
+                static_cast<const double2*>(Y), ldy, static_cast<double2*>(G), ell);
+      return;
+    case LR_F32:
+      gram_f32(h, m, ell, static_cast<const float*>(Y), ldy, static_cast<double*>(G));
+      return;
+    case LR_C64:
+      gram_c64(h, m, ell, static_cast<const float2*>(Y), ldy, static_cast<double2*>(G));
+      return;
+  }
+  throw Error{LR_EINVAL, "unknown dtype"};
+}
+
+void chol_any(Handle* h, int dtype, int64_t ell, const void* G, double tol, double unres,
+              double shift, void* P, void* R, int32_t* info) {
+  if (is_complex(dtype))
+    chol_drop_c128(h, ell, static_cast<const double2*>(G), tol, unres, shift,
+                   static_cast<double2*>(P), static_cast<double2*>(R), info);
+  else
+    chol_drop_f64(h, ell, static_cast<const double*>(G), tol, unres, shift,
+                  static_cast<double*>(P), static_cast<double*>(R), info);
+}
+
+// Y (m x k) . P (k x ncols, wide, ld ldp) in the working dtype.  P is cast
+// to the panel precision first for fp32 / complex64 panels.
+void apply_right(Handle* h, int dtype, int64_t m, int64_t k, int64_t ncols, const void* Y,
+                 int64_t ldy, const void* P, int64_t ldp, void* out, int64_t ldo) {
+  if (dtype == LR_F64 || dtype == LR_C128) {
+    gemm_any(h, dtype, false, false, m, ncols, k, Y, ldy, P, ldp, out, ldo);
+    return;
+  }
+  void* Pc = pool_alloc(h, size_t(k) * ncols * elem_size(dtype));
+  cast_copy(h, wide_of(dtype), P, ldp, dtype, Pc, ncols, k, ncols, false);
+  gemm_any(h, dtype, false, false, m, ncols, k, Y, ldy, Pc, ncols, out, ldo);
+}
+
+int64_t unres_threshold_scale(int64_t ell) { return ell; }
+
+// ---- orthonormalization (replaces orthonormalize_double_gs, core.py:84-115) --------
+
+// One CholeskyQR pass: out = Y . P where G = Y^H Y = R^H R (with deletion).
+Info cholqr_pass(Handle* h, int dtype, int64_t m, int64_t ell, const void* Y, int64_t ldy,
+                 double tol, double shift_coef, void* out, int64_t ldo, void* Rwide,
+                 void* Gwide, void* Pwide, int32_t* dinfo, bool apply) {
+  gram_any(h, dtype, m, ell, Y, ldy, Gwide);
+  const double unres = 4.0 * double(unres_threshold_scale(ell)) * U64;
+  chol_any(h, dtype, ell, Gwide, tol, unres, shift_coef, Pwide, Rwide, dinfo);
+  Info inf = read_info(h, dinfo);
+  if (apply && inf.rank > 0)
+    apply_right(h, dtype, m, ell, inf.rank, Y, ldy, Pwide, ell, out, ldo);
+  return inf;
+}
+
+// Column-wise CGS2 on the device, the reference algorithm verbatim
+// (core.py:99-114); host loop, used only when Gram-based QR cannot resolve
+// the rank decision.  Returns the rank; Q written to out (ld ldo).
+int64_t cgs2_device(Handle* h, int dtype, int64_t m, int64_t ell, const void* Y, int64_t ldy,
+                    void* out, int64_t ldo, double tol, double fro) {
+  const size_t es = elem_size(dtype);
+  void* w = pool_alloc(h, size_t(m) * es);
+  void* t = pool_alloc(h, size_t(m) * es);
+  void* c = pool_alloc(h, size_t(ell) * es);
+  double* nrm = pool_alloc_t<double>(h, 1);
+  double hn = 0.0;
+  int64_t kept = 0;
+  auto norm_of = [&](const void* v) {
+    col_sumsq(h, dtype, m, 1, v, 1, nrm);
+    LR_CUDA(cudaMemcpyAsync(&hn, nrm, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    LR_CUDA(cudaStreamSynchronize(h->stream));
+    return std::sqrt(hn);
+  };
+  auto project = [&]() {
+    // w -= Q (Q^H w), Q = out[:, :kept]
+    gemm_any(h, dtype, true, true, kept, 1, m, out, ldo, w, 1, c, 1);
+    gemm_any(h, dtype, false, false, m, 1, kept, out, ldo, c, 1, t, 1);
+    axpy_sub(h, dtype, m, 1, t, 1, w, 1);
+  };
+  for (int64_t j = 0; j < ell; ++j) {
+    cast_copy(h, dtype, static_cast<const char*>(Y) + j * es, ldy, dtype, w, 1, m, 1, false);
+    if (kept) project();
+    const double n1 = norm_of(w);
+    if (n1 <= tol * fro || n1 == 0.0) continue;
+    if (kept) project();
+    const double n2 = norm_of(w);
+    if (n2 == 0.0) continue;
+    scale_col(h, dtype, m, w, 1, 1.0 / n2, static_cast<char*>(out) + kept * es, ldo);
+    ++kept;
+  }
+  return kept;
+}
+
+double trace_host(Handle* h, int dtype, int64_t ell, const void* Gwide) {
+  // diagonal of the Gram (small): copy the whole matrix
+  std::vector<double> buf(size_t(ell) * ell * (is_complex(dtype) ? 2 : 1));
+  LR_CUDA(cudaMemcpyAsync(buf.data(), Gwide, buf.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                          h->stream));
+  LR_CUDA(cudaStreamSynchronize(h->stream));
+  double tr = 0.0;
+  for (int64_t i = 0; i < ell; ++i)
+    tr += is_complex(dtype) ? buf[2 * (i * ell + i)] : buf[i * ell + i];
+  return tr;
+}
+
+// Shifted CholeskyQR3 (no drops).  Returns false if a pass failed.  On
+// success, out holds Q (m x ell) and Rwide = R3 R2 R1.
+bool scholqr3(Handle* h, int dtype, int64_t m, int64_t ell, const void* Y, int64_t ldy,
+              void* out, int64_t ldo, void* Rwide, int32_t* dinfo) {
+  const size_t ws = wide_size(dtype), es = elem_size(dtype);
+  void* G = pool_alloc(h, size_t(ell) * ell * ws);
+  void* P = pool_alloc(h, size_t(ell) * ell * ws);
+  void* R1 = pool_alloc(h, size_t(ell) * ell * ws);
+  void* R2 = pool_alloc(h, size_t(ell) * ell * ws);
+  void* T = pool_alloc(h, size_t(ell) * ell * ws);
+  void* Q1 = pool_alloc(h, size_t(m) * ell * es);
+  // Fukaya et al. shift: 11 (m n + n (n + 1)) u ||Y||^2  (||Y||_2^2 <= trace G)
+  const double shift = 11.0 * (double(m) * ell + double(ell) * (ell + 1)) * U64;
+  Info a = cholqr_pass(h, dtype, m, ell, Y, ldy, 0.0, shift, Q1, ell, R1, G, P, dinfo, true);
+  if (a.rank != ell || a.bad) return false;
+  Info b = cholqr_pass(h, dtype, m, ell, Q1, ell, 0.0, 0.0, out, ldo, R2, G, P, dinfo, true);
+  if (b.rank != ell || b.bad) return false;
+  trmm_upper(h, wide_of(dtype), ell, R2, R1, T);
+  // third pass in place: Q1 <- out, out <- Q1 P
+  LR_CUDA(cudaMemcpy2DAsync(Q1, ell * es, out, ldo * es, ell * es, m, cudaMemcpyDeviceToDevice,
+                            h->stream));
+  Info c = cholqr_pass(h, dtype, m, ell, Q1, ell, 0.0, 0.0, out, ldo, R2, G, P, dinfo, true);
+  if (c.rank != ell || c.bad || c.unresolved) return false;
+  trmm_upper(h, wide_of(dtype), ell, R2, T, Rwide);
+  return true;
+}
+
+int64_t orth_impl(Handle* h, int dtype, int64_t m, int64_t ell, const void* Y, int64_t ldy,
+                  void* Q, int64_t ldq, double tol) {
+  const size_t ws = wide_size(dtype), es = elem_size(dtype);
+  void* G = pool_alloc(h, size_t(ell) * ell * ws);
+  void* P = pool_alloc(h, size_t(ell) * ell * ws);
+  void* R = pool_alloc(h, size_t(ell) * ell * ws);
+  void* Q1 = pool_alloc(h, size_t(m) * ell * es);
+  int32_t* dinfo = h->d_info;
+
+  const bool alias = (Q == Y);
+  // fast path: CholeskyQR2 with the drop rule applied in pass 1
+  Info a = cholqr_pass(h, dtype, m, ell, Y, ldy, tol, 0.0, Q1, ell, R, G, P, dinfo, true);
+  LR_REQUIRE(a.bad == 0, LR_EINVAL, "orthonormalize: non-finite entries in the sample matrix");
+  if (a.rank == 0) return 0;
+  if (a.unresolved == 0) {
+    void* dst = alias ? pool_alloc(h, size_t(m) * ell * es) : Q;
+    const int64_t ldd = alias ? ell : ldq;
+    Info b = cholqr_pass(h, dtype, m, a.rank, Q1, ell, tol, 0.0, dst, ldd, R, G, P, dinfo, true);
+    if (b.rank == a.rank && b.unresolved == 0 && b.bad == 0) {
+      if (alias)
+        LR_CUDA(cudaMemcpy2DAsync(Q, ldq * es, dst, ldd * es, a.rank * es, m,
+                                  cudaMemcpyDeviceToDevice, h->stream));
+      return a.rank;
+    }
+  }
+  // robust paths read Y again: keep a private copy when Q aliases it
+  if (alias) {
+    void* Yc = pool_alloc(h, size_t(m) * ell * es);
+    LR_CUDA(cudaMemcpy2DAsync(Yc, ell * es, Y, ldy * es, ell * es, m, cudaMemcpyDeviceToDevice,
+                              h->stream));
+    Y = Yc;
+    ldy = ell;
+  }
+  // robust path 1: shifted CholeskyQR3, then the drop rule on diag(R)
+  gram_any(h, dtype, m, ell, Y, ldy, G);
+  const double tr = trace_host(h, dtype, ell, G);
+  const double fro = std::sqrt(tr);
+  void* Rw = pool_alloc(h, size_t(ell) * ell * ws);
+  if (scholqr3(h, dtype, m, ell, Y, ldy, Q, ldq, Rw, dinfo)) {
+    std::vector<double> rb(size_t(ell) * ell * (is_complex(dtype) ? 2 : 1));
+    LR_CUDA(cudaMemcpyAsync(rb.data(), Rw, rb.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                            h->stream));
+    LR_CUDA(cudaStreamSynchronize(h->stream));
+    bool all = true;
+    for (int64_t i = 0; i < ell; ++i) {
+      const double d = is_complex(dtype) ? rb[2 * (i * ell + i)] : rb[i * ell + i];
+      if (!(std::fabs(d) > tol * fro) || d == 0.0) all = false;
+    }
+    if (all) return ell;
+  }
+  // robust path 2: device CGS2 (reference semantics, column by column)
+  return cgs2_device(h, dtype, m, ell, Y, ldy, Q, ldq, tol, fro);
+}
+
+// ---- small SVD (replaces small_svd, core.py:199-230, on B = Bh^H) -----------------
+
+void small_svd_impl(Handle* h, int dtype, int64_t r, int64_t c, void* Bh, void* U, double* S,
+                    void* V) {
+  const int wd = wide_of(dtype);
+  const size_t ws = wide_size(dtype), es = elem_size(dtype);
+  void* G = pool_alloc(h, size_t(r) * r * ws);
+  void* P = pool_alloc(h, size_t(r) * r * ws);
+  void* R1 = pool_alloc(h, size_t(r) * r * ws);
+  void* R2 = pool_alloc(h, size_t(r) * r * ws);
+  void* R = pool_alloc(h, size_t(r) * r * ws);
+  void* Q1 = pool_alloc(h, size_t(c) * r * es);
+  void* Q2 = pool_alloc(h, size_t(c) * r * es);
+  void* W = pool_alloc(h, size_t(c) * r * ws);
+  void* J = pool_alloc(h, size_t(r) * r * ws);
+  int32_t* dinfo = h->d_info;
+
+  const void* Qf = nullptr;   // c x r orthonormal factor of Bh (dtype)
+  bool ok = false;
+  // CholeskyQR2 of Bh (no drops), R = R2 R1
+  Info a = cholqr_pass(h, dtype, c, r, Bh, r, 0.0, 0.0, Q1, r, R1, G, P, dinfo, true);
+  LR_REQUIRE(a.bad == 0, LR_EINVAL, "small_svd: non-finite entries");
+  if (a.rank == r && a.unresolved == 0) {
+    Info b = cholqr_pass(h, dtype, c, r, Q1, r, 0.0, 0.0, Q2, r, R2, G, P, dinfo, true);
+    if (b.rank == r && b.unresolved == 0 && b.bad == 0) {
+      trmm_upper(h, wd, r, R2, R1, R);
+      Qf = Q2;
+      ok = true;
+    }
+  }
+  if (!ok && scholqr3(h, dtype, c, r, Bh, r, Q2, r, R, dinfo)) {
+    Qf = Q2;
+    ok = true;
+  }
+  if (ok) {
+    // R = W diag(S) J^H  =>  B = J diag(S) (Qf W)^H
+    void* Wr = pool_alloc(h, size_t(r) * r * ws);
+    if (is_complex(dtype))
+      jacobi_svd_c128(h, r, r, static_cast<double2*>(R), static_cast<double2*>(Wr), S,
+                      static_cast<double2*>(J), dinfo);
+    else
+      jacobi_svd_f64(h, r, r, static_cast<double*>(R), static_cast<double*>(Wr), S,
+                     static_cast<double*>(J), dinfo);
+    int32_t sweeps = 0;
+    LR_CUDA(cudaMemcpyAsync(&sweeps, dinfo, sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
+    LR_CUDA(cudaStreamSynchronize(h->stream));
+    if (sweeps < 0) throw Error{LR_ECONV, "SVD did not converge (Jacobi sweep limit)"};
+    cast_copy(h, wd, J, r, dtype, U, r, r, r, false);
+    apply_right(h, dtype, c, r, r, Qf, r, Wr, r, V, r);
+    return;
+  }
+  // degenerate (numerically rank-deficient) B: one-sided Jacobi on Bh itself
+  void* Bw = pool_alloc(h, size_t(c) * r * ws);
+  cast_copy(h, dtype, Bh, r, wd, Bw, r, c, r, false);
+  if (is_complex(dtype))
+    jacobi_svd_c128(h, c, r, static_cast<double2*>(Bw), static_cast<double2*>(W), S,
+                    static_cast<double2*>(J), dinfo);
+  else
+    jacobi_svd_f64(h, c, r, static_cast<double*>(Bw), static_cast<double*>(W), S,
+                   static_cast<double*>(J), dinfo);
+  int32_t sweeps = 0;
+  LR_CUDA(cudaMemcpyAsync(&sweeps, dinfo, sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
+  LR_CUDA(cudaStreamSynchronize(h->stream));
+  if (sweeps < 0) throw Error{LR_ECONV, "SVD did not converge (Jacobi sweep limit)"};
+  cast_copy(h, wd, J, r, dtype, U, r, r, r, false);
+  cast_copy(h, wd, W, r, dtype, V, r, c, r, false);
+}
+
+}  // namespace
+
+void set_error(const std::string& msg) { g_err = msg; }
+const char* get_error() { return g_err.c_str(); }
+
+// ---- pool ------------------------------------------------------------------------
+
+void pool_reset(Handle* h) {
+  Pool& p = h->pool;
+  if (p.chunks.size() > 1) {
+    LR_CUDA(cudaStreamSynchronize(h->stream));
+    for (auto& c : p.chunks) LR_CUDA(cudaFree(c.base));
+    p.chunks.clear();
+    const size_t sz = (p.peak + (size_t(1) << 20)) & ~((size_t(1) << 20) - 1);
+    char* base = nullptr;
+    LR_CUDA(cudaMalloc(&base, sz));
+    p.chunks.push_back({base, sz});
+  }
+  p.cur = 0;
+  p.off = 0;
+  p.used = 0;
+}
+
+void* pool_alloc(Handle* h, size_t bytes) {
+  Pool& p = h->pool;
+  bytes = (bytes + 255) & ~size_t(255);
+  if (bytes == 0) bytes = 256;
+  if (p.chunks.empty() || p.off + bytes > p.chunks[p.cur].size) {
+    // next chunk (existing or new)
+    if (!p.chunks.empty() && p.cur + 1 < p.chunks.size() &&
+        p.chunks[p.cur + 1].size >= bytes) {
+      ++p.cur;
+      p.off = 0;
+    } else {
+      size_t sz = std::max<size_t>(bytes, p.chunks.empty() ? (size_t(64) << 20)
+                                                           : p.chunks.back().size);
+      char* base = nullptr;
+      cudaError_t e = cudaMalloc(&base, sz);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        throw Error{LR_ENOMEM, "scratch pool: cudaMalloc failed"};
+      }
+      p.chunks.push_back({base, sz});
+      p.cur = p.chunks.size() - 1;
+      p.off = 0;
+    }
+  }
+  void* ptr = p.chunks[p.cur].base + p.off;
+  p.off += bytes;
+  p.used += bytes;
+  p.peak = std::max(p.peak, p.used);
+  return ptr;
+}
+
+}  // namespace lr
+
+using lr::Error;
+using lr::Handle;
+
+#define API_BEGIN try {
+#define API_END                                   \
+  }                                               \
+  catch (const Error& e) {                        \
+    lr::set_error(e.msg);                         \
+    return e.code;                                \
+  }                                               \
+  catch (const std::exception& e) {               \
+    lr::set_error(e.what());                      \
+    return LR_ECUDA;                              \
+  }                                               \
+  return LR_OK;
+
+static Handle* H(lr_handle_t h) { return reinterpret_cast<Handle*>(h); }
+
+static void check_dtype(int dtype) {
+  LR_REQUIRE(dtype == LR_F32 || dtype == LR_F64 || dtype == LR_C64 || dtype == LR_C128,
+             LR_EINVAL, "unknown dtype");
+}
+
+extern "C" {
+
+int lr_abi_version(void) { return LR_ABI_VERSION; }
+uint64_t lr_launch_count(void) { return __atomic_load_n(&lr::g_launches, __ATOMIC_RELAXED); }
+const char* lr_last_error(void) { return lr::get_error(); }
+
+int lr_create(int device, void* stream, lr_handle_t* out) {
+  API_BEGIN
+  LR_REQUIRE(out != nullptr, LR_EINVAL, "lr_create: null output");
+  int cur = -1;
+  LR_CUDA(cudaGetDevice(&cur));
+  if (cur != device) LR_CUDA(cudaSetDevice(device));
+  Handle* h = new Handle();
+  h->device = device;
+  h->stream = static_cast<cudaStream_t>(stream);
+  LR_CUDA(cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, device));
+  LR_CUDA(cudaMalloc(&h->d_info, 64 * sizeof(int32_t)));
+  LR_CUDA(cudaMallocHost(&h->h_info, 64 * sizeof(int32_t)));
+  *out = reinterpret_cast<lr_handle_t>(h);
+  API_END
+}
+
+int lr_destroy(lr_handle_t hh) {
+  API_BEGIN
+  Handle* h = H(hh);
+  if (!h) return LR_OK;
+  cudaStreamSynchronize(h->stream);
+  for (auto& c : h->pool.chunks) cudaFree(c.base);
+  cudaFree(h->d_info);
+  cudaFreeHost(h->h_info);
+  delete h;
+  API_END
+}
+
+int lr_set_stream(lr_handle_t h, void* stream) {
+  API_BEGIN
+  H(h)->stream = static_cast<cudaStream_t>(stream);
+  API_END
+}
+
+int lr_set_f32_mode(lr_handle_t h, int mode) {
+  API_BEGIN
+  LR_REQUIRE(mode == LR_F32_SPLIT3 || mode == LR_F32_SIMT, LR_EINVAL, "bad f32 mode");
+  H(h)->f32_mode = mode;
+  API_END
+}
+
+int64_t lr_workspace_bytes(lr_handle_t h) {
+  int64_t s = 0;
+  for (auto& c : H(h)->pool.chunks) s += int64_t(c.size);
+  return s;
+}
+
+int lr_reserve(lr_handle_t hh, int64_t bytes) {
+  API_BEGIN
+  Handle* h = H(hh);
+  lr::pool_reset(h);
+  lr::pool_alloc(h, size_t(bytes));
+  lr::pool_reset(h);
+  API_END
+}
+
+int lr_gemm(lr_handle_t hh, int dtype, int op, int64_t m, int64_t n, int64_t ell, const void* A,
+            int64_t lda, const void* X, int64_t ldx, void* Y, int64_t ldy) {
+  API_BEGIN
+  Handle* h = H(hh);
+  check_dtype(dtype);
+  LR_REQUIRE(m >= 0 && n >= 0 && ell >= 0, LR_EINVAL, "lr_gemm: negative dimension");
+  LR_REQUIRE(op == LR_OP_N || op == LR_OP_T || op == LR_OP_C, LR_EINVAL, "lr_gemm: bad op");
+  LR_REQUIRE(lda >= n, LR_EINVAL, "lr_gemm: lda < n");
+  lr::pool_reset(h);
+  if (op == LR_OP_N) {
+    LR_REQUIRE(ldx >= ell && ldy >= ell, LR_EINVAL, "lr_gemm: ld < ell");
+    lr::gemm_any(h, dtype, false, false, m, ell, n, A, lda, X, ldx, Y, ldy);
+  } else {
+    LR_REQUIRE(ldx >= ell && ldy >= ell, LR_EINVAL, "lr_gemm: ld < ell");
+    lr::gemm_any(h, dtype, true, op == LR_OP_C, n, ell, m, A, lda, X, ldx, Y, ldy);
+  }
+  API_END
+}
+
+int lr_gram(lr_handle_t hh, int dtype, int64_t m, int64_t ell, const void* Y, int64_t ldy,
+            void* G) {
+  API_BEGIN
+  Handle* h = H(hh);
+  check_dtype(dtype);
+  LR_REQUIRE(ldy >= ell, LR_EINVAL, "lr_gram: ldy < ell");
+  lr::pool_reset(h);
+  lr::gram_any(h, dtype, m, ell, Y, ldy, G);
+  API_END
+}
+
+int lr_chol_drop(lr_handle_t hh, int dtype, int64_t ell, const void* G, double drop_tol,
+                 double unres_rel, double shift_coef, void* P, void* R, int32_t* info) {
+  API_BEGIN
+  Handle* h = H(hh);
+  check_dtype(dtype);
+  lr::pool_reset(h);
+  lr::chol_any(h, dtype, ell, G, drop_tol, unres_rel, shift_coef, P, R, info);
+  API_END
+}
+
+int lr_orth(lr_handle_t hh, int dtype, int64_t m, int64_t ell, const void* Y, int64_t ldy,
+            void* Q, int64_t ldq, double tol, int64_t* rank_out) {
+  API_BEGIN
+  Handle* h = H(hh);
+  check_dtype(dtype);
+  LR_REQUIRE(m >= 1 && ell >= 1 && ldy >= ell && ldq >= ell, LR_EINVAL, "lr_orth: bad shape");
+  lr::pool_reset(h);
+  *rank_out = lr::orth_impl(h, dtype, m, ell, Y, ldy, Q, ldq, tol);
+  API_END
+}
+
+int lr_small_svd(lr_handle_t hh, int dtype, int64_t ell, int64_t ncols, void* Bh, void* U,
+                 double* S, void* V) {
+  API_BEGIN
+  Handle* h = H(hh);
+  check_dtype(dtype);
+  LR_REQUIRE(ell >= 1 && ncols >= ell, LR_EINVAL, "lr_small_svd: need 1 <= ell <= ncols");
+  lr::pool_reset(h);
+  lr::small_svd_impl(h, dtype, ell, ncols, Bh, U, S, V);
+  API_END
+}
+
+int lr_jacobi_svd(lr_handle_t hh, int dtype, int64_t ell, const void* M, void* W, double* S,
+                  void* J, int32_t* info) {
+  API_BEGIN
+  Handle* h = H(hh);
+  LR_REQUIRE(dtype == LR_F64 || dtype == LR_C128, LR_EINVAL,
+             "lr_jacobi_svd: fp64 / complex128 only");
+  lr::pool_reset(h);
+  if (dtype == LR_F64)
+    lr::jacobi_svd_f64(h, ell, ell, static_cast<const double*>(M), static_cast<double*>(W), S,
+                       static_cast<double*>(J), info);
+  else
+    lr::jacobi_svd_c128(h, ell, ell, static_cast<const double2*>(M), static_cast<double2*>(W), S,
+                        static_cast<double2*>(J), info);
+  API_END
+}
+
+int lr_estimate_tail(lr_handle_t hh, int dtype, int64_t m, int64_t k, int64_t r, const void* Q,
+                     int64_t ldq, void* Z, int64_t ldz, double alpha, double* est) {
+  API_BEGIN
+  Handle* h = H(hh);
+  check_dtype(dtype);
+  lr::pool_reset(h);
+  const size_t es = lr::elem_size(dtype);
+  if (k > 0) {
+    void* C = lr::pool_alloc(h, size_t(k) * r * es);
+    void* T = lr::pool_alloc(h, size_t(m) * r * es);
+    lr::gemm_any(h, dtype, true, true, k, r, m, Q, ldq, Z, ldz, C, r);
+    lr::gemm_any(h, dtype, false, false, m, r, k, Q, ldq, C, r, T, r);
+    lr::axpy_sub(h, dtype, m, r, T, r, Z, ldz);
+  }
+  double* ss = lr::pool_alloc_t<double>(h, size_t(r));
+  lr::col_sumsq(h, dtype, m, r, Z, ldz, ss);
+  lr::estimate_finish(h, r, ss, alpha, est);
+  API_END
+}
+
+int lr_srft(lr_handle_t hh, int dtype, int64_t m, int64_t n, int64_t ell, const void* A,
+            int64_t lda, const void* d, const int32_t* picks, double scale, void* Y,
+            int64_t ldy) {
+  API_BEGIN
+  Handle* h = H(hh);
+  LR_REQUIRE(dtype == LR_C64 || dtype == LR_C128, LR_EINVAL, "lr_srft: complex dtypes only");
+  LR_REQUIRE(n >= 1 && (n & (n - 1)) == 0, LR_EUNSUPPORTED,
+             "lr_srft: n must be a power of two (Bluestein path not built)");
+  lr::pool_reset(h);
+  if (dtype == LR_C64)
+    lr::srft_c64(h, m, n, ell, static_cast<const float2*>(A), lda, static_cast<const float2*>(d),
+                 picks, float(scale), static_cast<float2*>(Y), ldy);
+  else
+    lr::srft_c128(h, m, n, ell, static_cast<const double2*>(A), lda,
+                  static_cast<const double2*>(d), picks, scale, static_cast<double2*>(Y), ldy);
+  API_END
+}
+
+int lr_dft_rows(lr_handle_t hh, int dtype, int64_t rows, int64_t n, void* X, int64_t ldx) {
+  API_BEGIN
+  Handle* h = H(hh);
+  LR_REQUIRE(dtype == LR_C64 || dtype == LR_C128, LR_EINVAL, "lr_dft_rows: complex dtypes only");
+  LR_REQUIRE(n >= 1 && (n & (n - 1)) == 0, LR_EUNSUPPORTED,
+             "lr_dft_rows: n must be a power of two");
+  lr::pool_reset(h);
+  lr::dft_rows(h, dtype, rows, n, X, ldx);
+  API_END
+}
+
+int lr_csr_spmm(lr_handle_t hh, int dtype, int64_t m, int64_t n, int64_t ell,
+                const int64_t* rowptr, const int32_t* colidx, const void* vals, const void* X,
+                int64_t ldx, void* Y, int64_t ldy, int accumulate) {
+  API_BEGIN
+  Handle* h = H(hh);
+  LR_REQUIRE(dtype == LR_F64, LR_EUNSUPPORTED, "lr_csr_spmm: fp64 only");
+  (void)n;
+  lr::pool_reset(h);
+  lr::csr_spmm_f64(h, m, ell, rowptr, colidx, static_cast<const double*>(vals),
+                   static_cast<const double*>(X), ldx, static_cast<double*>(Y), ldy,
+                   accumulate != 0);
+  API_END
+}
+
+int lr_check_finite(lr_handle_t hh, int dtype, int64_t m, int64_t n, const void* A, int64_t lda,
+                    int64_t* nonfinite, double* amax) {
+  API_BEGIN
+  Handle* h = H(hh);
+  check_dtype(dtype);
+  lr::pool_reset(h);
+  lr::check_finite(h, dtype, m, n, A, lda, nonfinite, amax);
+  API_END
+}
+
+int lr_copy(lr_handle_t hh, int src_dtype, const void* src, int64_t lds, int dst_dtype,
+            void* dst, int64_t ldd, int64_t rows, int64_t cols, int conj_transpose) {
+  API_BEGIN
+  Handle* h = H(hh);
+  check_dtype(src_dtype);
+  check_dtype(dst_dtype);
+  lr::pool_reset(h);
+  lr::cast_copy(h, src_dtype, src, lds, dst_dtype, dst, ldd, rows, cols, conj_transpose != 0);
+  API_END
+}
+
+int lr_sign_fix(lr_handle_t hh, int dtype, int64_t rows, int64_t vrows, int64_t cols, void* U,
+                int64_t ldu, void* V, int64_t ldv) {
+  API_BEGIN
+  Handle* h = H(hh);
+  check_dtype(dtype);
+  lr::pool_reset(h);
+  lr::sign_fix(h, dtype, rows, vrows, cols, U, ldu, V, ldv);
+  API_END
+}
+
+int lr_max_abs_imag(lr_handle_t hh, int dtype, int64_t m, int64_t n, const void* Y, int64_t ldy,
+                    double* out) {
+  API_BEGIN
+  Handle* h = H(hh);
+  lr::pool_reset(h);
+  lr::max_abs_imag(h, dtype, m, n, Y, ldy, out);
+  API_END
+}
+
+int lr_axpy_sub(lr_handle_t hh, int dtype, int64_t rows, int64_t cols, const void* T,
+                int64_t ldt, void* Z, int64_t ldz) {
+  API_BEGIN
+  Handle* h = H(hh);
+  check_dtype(dtype);
+  lr::pool_reset(h);
+  lr::axpy_sub(h, dtype, rows, cols, T, ldt, Z, ldz);
+  API_END
+}
+
+int lr_col_sumsq(lr_handle_t hh, int dtype, int64_t m, int64_t r, const void* Z, int64_t ldz,
+                 double* out) {
+  API_BEGIN
+  Handle* h = H(hh);
+  check_dtype(dtype);
+  lr::pool_reset(h);
+  lr::col_sumsq(h, dtype, m, r, Z, ldz, out);
+  API_END
+}
+
+int lr_scale_col(lr_handle_t hh, int dtype, int64_t rows, const void* src, int64_t lds,
+                 double inv, void* dst, int64_t ldd) {
+  API_BEGIN
+  Handle* h = H(hh);
+  check_dtype(dtype);
+  lr::pool_reset(h);
+  lr::scale_col(h, dtype, rows, src, lds, inv, dst, ldd);
+  API_END
+}
+
+}  // extern "C"

@@ -1,0 +1,171 @@
+// Shared runtime pieces of liblowrank_b200: handle, scratch pool, errors.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuComplex.h>
+#include <stdint.h>
+#include <algorithm>
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "../../include/lowrank_b200.h"
+
+namespace lr {
+
+// ---------------------------------------------------------------------------
+// errors: thread-local message + status code
+
+void set_error(const std::string& msg);
+const char* get_error();
+
+struct Error {
+  int code;
+  std::string msg;
+};
+
+#define LR_CUDA(call)                                                                  \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      throw ::lr::Error{LR_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)}; \
+  } while (0)
+
+extern unsigned long long g_launches;
+#define LR_CHECK_LAUNCH()                 \
+  do {                                    \
+    __atomic_add_fetch(&::lr::g_launches, 1ULL, __ATOMIC_RELAXED); \
+    LR_CUDA(cudaGetLastError());          \
+  } while (0)
+
+#define LR_REQUIRE(cond, code, msg)              \
+  do {                                           \
+    if (!(cond)) throw ::lr::Error{(code), (msg)}; \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// handle + scratch pool.  The pool is a list of device chunks with a bump
+// pointer; reset() at the start of every API call rewinds it (stream order
+// makes reuse across calls safe).  If one call needs more than the current
+// chunk, a new chunk is appended; at the next reset the chunks are merged
+// into one (after a stream sync), so steady state is one cudaMalloc total.
+
+struct Pool {
+  struct Chunk {
+    char* base;
+    size_t size;
+  };
+  std::vector<Chunk> chunks;
+  size_t cur = 0;     // index of chunk in use
+  size_t off = 0;     // bump offset within chunk
+  size_t peak = 0;    // bytes needed by the largest call so far
+  size_t used = 0;    // bytes handed out in this call
+};
+
+struct Handle {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int sm_count = 148;
+  int f32_mode = LR_F32_SPLIT3;
+  Pool pool;
+  int32_t* d_info = nullptr;   // small device scratch for composite decisions
+  int32_t* h_info = nullptr;   // pinned mirror
+  double* d_dscratch = nullptr;
+};
+
+void pool_reset(Handle* h);
+void* pool_alloc(Handle* h, size_t bytes);
+template <typename T>
+T* pool_alloc_t(Handle* h, size_t count) {
+  return reinterpret_cast<T*>(pool_alloc(h, count * sizeof(T)));
+}
+
+inline int elem_size(int dtype) {
+  switch (dtype) {
+    case LR_F32: return 4;
+    case LR_F64: return 8;
+    case LR_C64: return 8;
+    case LR_C128: return 16;
+  }
+  return 0;
+}
+inline bool is_complex(int dtype) { return dtype == LR_C64 || dtype == LR_C128; }
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// ---------------------------------------------------------------------------
+// kernels launched from capi.cu (defined in the per-kernel .cu files)
+
+// gemm_f64.cu ---------------------------------------------------------------
+int64_t choose_splits(int sm_count, int64_t tiles, int64_t K);
+// C (M x N) = op(A) . B, op(A) = A (A M x K, lda) or A^T (A K x M, lda);
+// B is K x N (ldb); C M x N (ldc).  conjA applies for complex.
+void gemm_f64(Handle* h, bool transA, int64_t M, int64_t N, int64_t K, const double* A,
+              int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc);
+void gemm_c128(Handle* h, bool transA, bool conjA, int64_t M, int64_t N, int64_t K,
+               const double2* A, int64_t lda, const double2* B, int64_t ldb, double2* C,
+               int64_t ldc);
+
+// gemm_f32.cu (tcgen05) -----------------------------------------------------
+void gemm_f32(Handle* h, bool transA, int64_t M, int64_t N, int64_t K, const float* A,
+              int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc);
+void gemm_c64(Handle* h, bool transA, bool conjA, int64_t M, int64_t N, int64_t K,
+              const float2* A, int64_t lda, const float2* B, int64_t ldb, float2* C,
+              int64_t ldc);
+// gemm_simt.cu: honest-fp32 SIMT fallbacks (LR_F32_SIMT)
+void gemm_f32_simt(Handle* h, bool transA, int64_t M, int64_t N, int64_t K, const float* A,
+                   int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc);
+void gemm_c64_simt(Handle* h, bool transA, bool conjA, int64_t M, int64_t N, int64_t K,
+                   const float2* A, int64_t lda, const float2* B, int64_t ldb, float2* C,
+                   int64_t ldc);
+// fp64-accumulated Gram of fp32 / complex64 panels
+void gram_f32(Handle* h, int64_t m, int64_t ell, const float* Y, int64_t ldy, double* G);
+void gram_c64(Handle* h, int64_t m, int64_t ell, const float2* Y, int64_t ldy, double2* G);
+
+// chol.cu ---------------------------------------------------------------------
+// Cholesky with column deletion + triangular inverse, single CTA.
+// drop threshold = drop_tol^2 * trace(G); shift = shift_coef * trace(G).
+void chol_drop_f64(Handle* h, int64_t ell, const double* G, double drop_tol,
+                   double unres_rel, double shift_coef, double* P, double* R, int32_t* info);
+void chol_drop_c128(Handle* h, int64_t ell, const double2* G, double drop_tol,
+                    double unres_rel, double shift_coef, double2* P, double2* R, int32_t* info);
+
+// jacobi.cu -------------------------------------------------------------------
+// M (rows x n, rows >= n) = W diag(S) J^H; W rows x n, J n x n.
+void jacobi_svd_f64(Handle* h, int64_t rows, int64_t n, const double* M, double* W, double* S,
+                    double* J, int32_t* info);
+void jacobi_svd_c128(Handle* h, int64_t rows, int64_t n, const double2* M, double2* W,
+                     double* S, double2* J, int32_t* info);
+
+// misc.cu ---------------------------------------------------------------------
+void cast_copy(Handle* h, int src_dtype, const void* src, int64_t lds, int dst_dtype,
+               void* dst, int64_t ldd, int64_t rows, int64_t cols, bool conj_transpose);
+void col_sumsq(Handle* h, int dtype, int64_t m, int64_t r, const void* Z, int64_t ldz,
+               double* out);
+void estimate_finish(Handle* h, int64_t r, const double* sumsq, double alpha, double* est);
+void check_finite(Handle* h, int dtype, int64_t m, int64_t n, const void* A, int64_t lda,
+                  int64_t* nonfinite, double* amax);
+void trmm_upper(Handle* h, int dtype, int64_t n, const void* R2, const void* R1, void* R);
+void sign_fix(Handle* h, int dtype, int64_t rows, int64_t vrows, int64_t cols, void* U,
+              int64_t ldu, void* V, int64_t ldv);
+void max_abs_imag(Handle* h, int dtype, int64_t m, int64_t n, const void* Y, int64_t ldy,
+                  double* out);
+// Z (rows x cols) -= T ; Z[:, j] = src / s  helpers for CGS2 / estimator
+void axpy_sub(Handle* h, int dtype, int64_t rows, int64_t cols, const void* T, int64_t ldt,
+              void* Z, int64_t ldz);
+void scale_col(Handle* h, int dtype, int64_t rows, const void* src, int64_t lds, double inv,
+               void* dst, int64_t ldd);
+
+// srft.cu ---------------------------------------------------------------------
+void srft_c64(Handle* h, int64_t m, int64_t n, int64_t ell, const float2* A, int64_t lda,
+              const float2* d, const int32_t* picks, float scale, float2* Y, int64_t ldy);
+void srft_c128(Handle* h, int64_t m, int64_t n, int64_t ell, const double2* A, int64_t lda,
+               const double2* d, const int32_t* picks, double scale, double2* Y, int64_t ldy);
+void dft_rows(Handle* h, int dtype, int64_t rows, int64_t n, void* X, int64_t ldx);
+
+// spmm.cu -----------------------------------------------------------------------
+void csr_spmm_f64(Handle* h, int64_t m, int64_t ell, const int64_t* rowptr,
+                  const int32_t* colidx, const double* vals, const double* X, int64_t ldx,
+                  double* Y, int64_t ldy, bool accumulate);
+
+}  // namespace lr

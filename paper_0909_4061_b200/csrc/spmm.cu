@@ -1,0 +1,79 @@
+// K6: CSR SpMM for the sparse operator of config 5 (no reference code path
+// exists for sparse A -- SURVEY.md §8c; this is the MatVecOperator plug-in
+// the survey prescribes, core.py:343-380).
+//
+// Y (m x ell) (+)= S . X with S in CSR (int64 row pointers, int32 column
+// indices, fp64 values) and X (n x ell) row-major.  One warp per row: the
+// warp streams the row's nonzeros (coalesced), broadcasts (col, val) by
+// shuffle, and each lane accumulates ell/32 columns of the gathered X rows
+// (each gather is a contiguous 8*ell-byte row of X).  The transpose product
+// uses the CSR of S^T (built once by the operator), so no atomics are needed
+// and the result is deterministic.
+#include "common.cuh"
+
+namespace lr {
+namespace {
+
+template <int CPL>   // columns per lane (ell <= 32 * CPL)
+__global__ void __launch_bounds__(256)
+csr_spmm_kernel(int64_t m, int ell, const int64_t* __restrict__ rowptr,
+                const int32_t* __restrict__ colidx, const double* __restrict__ vals,
+                const double* __restrict__ X, int64_t ldx, double* __restrict__ Y, int64_t ldy,
+                bool accumulate) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t row = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); row < m;
+       row += warps) {
+    double acc[CPL];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) acc[c] = 0.0;
+    const int64_t b = rowptr[row], e = rowptr[row + 1];
+    for (int64_t base = b; base < e; base += 32) {
+      const int64_t idx = base + lane;
+      int32_t cl = 0;
+      double vl = 0.0;
+      if (idx < e) {
+        cl = colidx[idx];
+        vl = vals[idx];
+      }
+      const int cnt = int(min(int64_t(32), e - base));
+      for (int k = 0; k < cnt; ++k) {
+        const int32_t col = __shfl_sync(0xffffffffu, cl, k);
+        const double v = __shfl_sync(0xffffffffu, vl, k);
+        const double* xr = X + int64_t(col) * ldx;
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          const int j = c * 32 + lane;
+          if (j < ell) acc[c] = fma(v, __ldg(xr + j), acc[c]);
+        }
+      }
+    }
+    double* yr = Y + row * ldy;
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      const int j = c * 32 + lane;
+      if (j < ell) yr[j] = accumulate ? yr[j] + acc[c] : acc[c];
+    }
+  }
+}
+
+}  // namespace
+
+void csr_spmm_f64(Handle* h, int64_t m, int64_t ell, const int64_t* rowptr,
+                  const int32_t* colidx, const double* vals, const double* X, int64_t ldx,
+                  double* Y, int64_t ldy, bool accumulate) {
+  if (m == 0 || ell == 0) return;
+  LR_REQUIRE(ell <= 256, LR_EUNSUPPORTED, "csr_spmm: ell > 256 not built");
+  const int blocks = int(std::min<int64_t>(ceil_div(m, 8), int64_t(h->sm_count) * 16));
+  const int cpl = int(ceil_div(ell, 32));
+  switch (cpl) {
+    case 1: csr_spmm_kernel<1><<<blocks, 256, 0, h->stream>>>(m, int(ell), rowptr, colidx, vals, X, ldx, Y, ldy, accumulate); break;
+    case 2: csr_spmm_kernel<2><<<blocks, 256, 0, h->stream>>>(m, int(ell), rowptr, colidx, vals, X, ldx, Y, ldy, accumulate); break;
+    case 3:
+    case 4: csr_spmm_kernel<4><<<blocks, 256, 0, h->stream>>>(m, int(ell), rowptr, colidx, vals, X, ldx, Y, ldy, accumulate); break;
+    default: csr_spmm_kernel<8><<<blocks, 256, 0, h->stream>>>(m, int(ell), rowptr, colidx, vals, X, ldx, Y, ldy, accumulate); break;
+  }
+  LR_CHECK_LAUNCH();
+}
+
+}  // namespace lr

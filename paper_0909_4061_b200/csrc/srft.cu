@@ -1,0 +1,131 @@
+// K5: SRFT sketch Y = scale * (A o d) F R and the unitary row DFT.
+//
+// Replaces srft_apply -> dft -> _fft_pow2 (reference sketch.py:306-320,
+// 179-200, 129-148): for each row a_i of A (length n, a power of two),
+//   y_i[t] = scale * n^{-1/2} * sum_k a_ik d_k exp(-2 pi i k picks_t / n).
+// One CTA per row: the row is loaded once from HBM (coalesced), multiplied
+// by d and stored into shared memory in bit-reversed order, transformed by
+// an in-place radix-2 DIT FFT in shared memory, and only the ell picked bins
+// are written back (the sketch is HBM-read-bound: one pass over A, ell/n of
+// it written).  Twiddles come from sincospi of exact dyadic arguments.
+#include "common.cuh"
+
+namespace lr {
+namespace {
+
+template <typename C>
+struct Cx;
+template <>
+struct Cx<float2> {
+  using R = float;
+  __device__ static float2 mul(float2 a, float2 b) {
+    return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+  }
+  __device__ static float2 tw(int k, int span) {  // exp(-2 pi i k / span)
+    float s, c;
+    sincospif(-2.0f * float(k) / float(span), &s, &c);
+    return make_float2(c, s);
+  }
+  __device__ static float2 add(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+  __device__ static float2 sub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+  __device__ static float2 scl(float2 a, double s) { return make_float2(a.x * float(s), a.y * float(s)); }
+};
+template <>
+struct Cx<double2> {
+  using R = double;
+  __device__ static double2 mul(double2 a, double2 b) {
+    return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+  }
+  __device__ static double2 tw(int k, int span) {
+    double s, c;
+    sincospi(-2.0 * double(k) / double(span), &s, &c);
+    return make_double2(c, s);
+  }
+  __device__ static double2 add(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+  __device__ static double2 sub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+  __device__ static double2 scl(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+};
+
+__device__ __forceinline__ int bitrev(int x, int bits) { return int(__brev(unsigned(x)) >> (32 - bits)); }
+
+// In-place radix-2 DIT FFT of buf (bit-reversed input) in shared memory.
+template <typename C>
+__device__ void fft_smem(C* buf, int n, int bits) {
+  for (int span = 2; span <= n; span <<= 1) {
+    const int half = span >> 1;
+    for (int b = threadIdx.x; b < (n >> 1); b += blockDim.x) {
+      const int grp = b / half, k = b % half;
+      const int i0 = grp * span + k, i1 = i0 + half;
+      const C w = Cx<C>::tw(k, span);
+      const C t = Cx<C>::mul(buf[i1], w);
+      const C u = buf[i0];
+      buf[i0] = Cx<C>::add(u, t);
+      buf[i1] = Cx<C>::sub(u, t);
+    }
+    __syncthreads();
+  }
+}
+
+template <typename C>
+__global__ void srft_kernel(int64_t m, int n, int bits, int ell, const C* A,
+                            int64_t lda, const C* __restrict__ d, const int32_t* __restrict__ picks,
+                            double scale, C* Y, int64_t ldy) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  C* buf = reinterpret_cast<C*>(smem_raw);
+  const double s = scale * rsqrt(double(n));
+  for (int64_t row = blockIdx.x; row < m; row += gridDim.x) {
+    const C* a = A + row * lda;
+    for (int k = threadIdx.x; k < n; k += blockDim.x)
+      buf[bitrev(k, bits)] = d ? Cx<C>::mul(a[k], d[k]) : a[k];
+    __syncthreads();
+    fft_smem(buf, n, bits);
+    for (int t = threadIdx.x; t < ell; t += blockDim.x) {
+      const int p = picks ? picks[t] : t;
+      Y[row * ldy + t] = Cx<C>::scl(buf[p], s);
+    }
+    __syncthreads();
+  }
+}
+
+template <typename C>
+void launch_srft(Handle* h, int64_t m, int64_t n, int64_t ell, const C* A, int64_t lda,
+                 const C* d, const int32_t* picks, double scale, C* Y, int64_t ldy) {
+  const size_t smem = size_t(n) * sizeof(C);
+  int max_smem = 0;
+  LR_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
+  LR_REQUIRE(smem <= size_t(max_smem), LR_EUNSUPPORTED,
+             "srft: row length exceeds the shared-memory FFT size");
+  int bits = 0;
+  while ((int64_t(1) << bits) < n) ++bits;
+  auto kern = srft_kernel<C>;
+  LR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  const int blocks = int(std::min<int64_t>(m, int64_t(h->sm_count) * 8));
+  if (blocks == 0) return;
+  kern<<<blocks, 512, smem, h->stream>>>(m, int(n), bits, int(ell), A, lda, d, picks, scale, Y,
+                                         ldy);
+  LR_CHECK_LAUNCH();
+}
+
+}  // namespace
+
+void srft_c64(Handle* h, int64_t m, int64_t n, int64_t ell, const float2* A, int64_t lda,
+              const float2* d, const int32_t* picks, float scale, float2* Y, int64_t ldy) {
+  launch_srft<float2>(h, m, n, ell, A, lda, d, picks, double(scale), Y, ldy);
+}
+
+void srft_c128(Handle* h, int64_t m, int64_t n, int64_t ell, const double2* A, int64_t lda,
+               const double2* d, const int32_t* picks, double scale, double2* Y, int64_t ldy) {
+  launch_srft<double2>(h, m, n, ell, A, lda, d, picks, scale, Y, ldy);
+}
+
+void dft_rows(Handle* h, int dtype, int64_t rows, int64_t n, void* X, int64_t ldx) {
+  // unitary DFT of every row, in place: picks = identity, d = 1, scale = 1
+  if (dtype == LR_C64)
+    launch_srft<float2>(h, rows, n, n, static_cast<const float2*>(X), ldx, nullptr, nullptr, 1.0,
+                        static_cast<float2*>(X), ldx);
+  else
+    launch_srft<double2>(h, rows, n, n, static_cast<const double2*>(X), ldx, nullptr, nullptr,
+                         1.0, static_cast<double2*>(X), ldx);
+}
+
+}  // namespace lr

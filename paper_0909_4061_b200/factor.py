@@ -1,0 +1,126 @@
+"""Stage B on the GPU: the direct SVD (Alg 5.1) and the rSVD composition.
+
+Mirrors ``direct_svd`` / ``PartialSVD`` / ``truncate_rank`` of the
+reference's ``lowrank.factor`` (factor.py:41-50,154-165,408-426), and the
+CLI's "randomized SVD" composition (cli.py:128-173 Stage-A dispatch +
+direct_svd + posterior estimate with seed + 13, cli.py:222-262) as
+``randomized_svd``, which keeps every intermediate in HBM and only copies
+the final factors back.  Other Stage-B routes (ID / row extraction,
+Nystrom, one-pass) are outside this build's scope.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+from . import config
+from .core import (_out, _torch, apply_dev, as_operator, gemm_dev, is_device_array,
+                   small_svd_from_adjoint, to_device)
+from .rangefinder import (RangeBasis, _check_ell, _host_io, posterior_error_estimate_dev,
+                          subspace_iteration_range_dev, SketchSpec, orth_dev, _cast_like_op,
+                          _sketch_dev)
+from .sketch import srft_dev, srft_operator
+
+
+@dataclass
+class PartialSVD:
+    """A ~= U @ diag(sigma) @ V*, orthonormal factors, sigma descending."""
+
+    U: object
+    sigma: object
+    V: object
+
+    def compose(self):
+        if is_device_array(self.U):
+            return (self.U * self.sigma.to(self.U.dtype)) @ self.V.conj().T
+        return (self.U * self.sigma) @ self.V.conj().T
+
+
+def direct_svd_dev(op, Q):
+    """Alg 5.1 on the device: Z = A^H Q (one pass), small SVD of B = Z^H,
+    U = Q U~.  Returns device (U, sigma, V)."""
+    torch = _torch()
+    k = Q.shape[1]
+    if k == 0:
+        return (torch.zeros((op.m, 0), dtype=Q.dtype, device=Q.device),
+                torch.zeros(0, dtype=torch.float64, device=Q.device),
+                torch.zeros((op.n, 0), dtype=Q.dtype, device=Q.device))
+    Z = apply_dev(op, Q, adjoint=True)            # n x k  (= B^H)
+    Ub, S, V = small_svd_from_adjoint(Z)
+    U = torch.empty((op.m, k), dtype=Q.dtype, device=Q.device)
+    gemm_dev(Q, Ub, U)
+    return U, S, V
+
+
+def direct_svd(A, Q):
+    """Partial SVD through B = Q*A (factor.py:154-165); the approximation
+    error equals the basis residual ||A - QQ*A||."""
+    op = as_operator(A)
+    if Q.shape[0] != op.m:
+        raise ValueError("basis rows must match matrix rows")
+    host = _host_io(A, op) and not is_device_array(Q)
+    dt = getattr(op, "dtype", None)
+    Qd = to_device(Q, dt if op.device_native else None)
+    U, S, V = direct_svd_dev(op, Qd)
+    return PartialSVD(U=_out(U, host), sigma=_out(S, host), V=_out(V, host))
+
+
+def truncate_rank(f, k):
+    """Keep the k leading components (factor.py:408-426, PartialSVD branch)."""
+    if isinstance(f, PartialSVD):
+        if k > len(f.sigma):
+            raise ValueError("k exceeds current rank")
+        return PartialSVD(U=f.U[:, :k], sigma=f.sigma[:k], V=f.V[:, :k])
+    raise TypeError("expected PartialSVD")
+
+
+def randomized_svd(A, k, p=config.DEFAULT_OVERSAMPLE, q=0, seed=0, sketch="gauss",
+                   probes=config.DEFAULT_PROBES, alpha=config.DEFAULT_ALPHA, truncate=False,
+                   estimate=True):
+    """The reference CLI's rank-k randomized SVD (cli.py:128-173, 222-262):
+
+      ell = k + p;  gauss & q > 0 -> Alg 4.4;  gauss & q = 0 -> Alg 4.1;
+      srft -> Alg 4.5 (q > 0 rejected);  then direct_svd (Alg 5.1) and the
+      posterior estimate with seed + 13 (cli.py:168-173).
+
+    All intermediates stay on the GPU.  Returns (RangeBasis, PartialSVD,
+    est_error) with numpy outputs for numpy input."""
+    op = as_operator(A)
+    ell = int(k) + int(p)
+    host = _host_io(A, op)
+    if sketch in ("gauss", "gaussian"):
+        _check_ell(op, ell)
+        if q > 0:
+            Q = subspace_iteration_range_dev(op, ell, q, seed)
+            passes = 2 * q + 2
+        else:
+            Q = orth_dev(apply_dev(op, _cast_like_op(op, _sketch_dev(op, ell, seed))))
+            passes = 1
+        spec = SketchSpec(kind="gaussian", ell=ell, power_q=q, seed=seed)
+    elif sketch == "srft":
+        if q > 0:
+            raise ValueError("power iterations are not available with structured sketches")
+        if ell > op.n:
+            raise ValueError(f"rank+oversample {ell} exceeds the column count {op.n}")
+        Q = orth_dev(srft_dev(op.array, srft_operator(op.n, ell, seed)))
+        passes = 1
+        spec = SketchSpec(kind="srft", ell=ell, seed=seed)
+    else:
+        raise ValueError(f"unknown sketch {sketch!r}")
+    U, S, V = direct_svd_dev(op, Q)
+    est_dev = None
+    if Q.shape[1] == 0:
+        est = 0.0
+    elif estimate:
+        est_dev = posterior_error_estimate_dev(op, Q, probes, alpha, seed + 13)
+        est = None
+    else:
+        est = None
+    if truncate:
+        kk = min(int(k), U.shape[1])
+        U, S, V = U[:, :kk], S[:kk], V[:, :kk]
+    if est_dev is not None:
+        est = float(est_dev.item())
+    basis = RangeBasis(Q=_out(Q, host), samples_used=ell, passes=passes, est_error=est,
+                       spec=spec)
+    return basis, PartialSVD(U=_out(U, host), sigma=_out(S, host), V=_out(V, host)), est

@@ -1,0 +1,180 @@
+"""Random test matrices and the SRFT fast apply.
+
+Mirrors the hot-path part of the reference's ``lowrank.sketch``
+(/root/reference/pkg/src/lowrank/sketch.py).  Every random draw is made on
+the host with the reference's counter-based Philox keying (sketch.py:32-42)
+so the same (dimensions, seed) give bitwise the same Omega / D / R as the
+reference; the draws are uploaded and all arithmetic runs on the GPU
+(K5 SRFT kernel, K1 GEMM).  The Givens-chain variant (GSRFT) and the
+Bluestein path for non-power-of-two lengths are outside this build's scope
+ and raise NotImplementedError.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .core import _out, _torch, is_device_array, to_device
+
+_STREAM_GAUSS = 0x67617573
+_STREAM_SRFT = 0x73726674
+_STREAM_GSRFT = 0x67737266
+_STREAM_ORTHO = 0x6F727468
+
+
+def rng_for(seed, stream=0, index=0):
+    """Philox generator keyed by seed | stream<<64 | index<<96 (sketch.py:32-42)."""
+    key = (int(seed) & (2**64 - 1)) | ((int(stream) & (2**32 - 1)) << 64) | (
+        (int(index) & (2**32 - 1)) << 96)
+    return np.random.Generator(np.random.Philox(key=key))
+
+
+@dataclass
+class SketchSpec:
+    """Configuration of one randomized sketch draw (sketch.py:69-93)."""
+
+    kind: str = "gaussian"
+    ell: int = 1
+    power_q: int = 0
+    seed: int = 0
+
+    def __post_init__(self):
+        if self.kind not in ("gaussian", "srft", "gsrft"):
+            raise ValueError(f"unknown sketch kind {self.kind!r}")
+        if self.ell < 1:
+            raise ValueError("sample count ell must be >= 1")
+        if self.power_q < 0:
+            raise ValueError("power exponent must be nonnegative")
+
+    @classmethod
+    def fixed_rank(cls, kind, k, p=5, q=0, seed=0):
+        return cls(kind=kind, ell=int(k) + int(p), power_q=q, seed=seed)
+
+
+def gaussian_matrix(n, ell, seed):
+    """n-by-ell i.i.d. standard normals keyed by seed (sketch.py:96-100).
+
+    Drawn on the host (bitwise identical to the reference); the range
+    finders upload it in the operator's precision."""
+    if n < 1 or ell < 1:
+        raise ValueError("dimensions must be >= 1")
+    return rng_for(seed, _STREAM_GAUSS).standard_normal((n, ell))
+
+
+@dataclass
+class SrftOperator:
+    """Materialized SRFT draw: scale * D F R with unimodular diagonal d
+    (sketch.py:207-218)."""
+
+    n: int
+    ell: int
+    d: np.ndarray
+    picks: np.ndarray
+    scale: float
+
+    def to_dense(self):
+        return srft_apply(np.eye(self.n), self)
+
+
+def srft_operator(n, ell, seed):
+    """d = exp(2 pi i U[0,1)) then picks = permutation(n)[:ell], one stream
+    (sketch.py:250-256)."""
+    if ell > n:
+        raise ValueError("sample count exceeds dimension")
+    rng = rng_for(seed, _STREAM_SRFT)
+    d = np.exp(2j * np.pi * rng.random(n))
+    picks = rng.permutation(n)[:ell]
+    return SrftOperator(n=n, ell=ell, d=d, picks=picks, scale=float(np.sqrt(n / ell)))
+
+
+def _resolve(spec_or_op, n):
+    if isinstance(spec_or_op, SrftOperator):
+        op = spec_or_op
+    elif isinstance(spec_or_op, SketchSpec):
+        if spec_or_op.kind == "gsrft":
+            raise NotImplementedError("GSRFT is outside this build's scope (SURVEY.md §8f #3)")
+        op = srft_operator(n, spec_or_op.ell, spec_or_op.seed)
+    else:
+        raise TypeError("expected a SketchSpec or a materialized operator")
+    if op.n != n:
+        raise ValueError("operator dimension does not match matrix columns")
+    return op
+
+
+def _complex_of(t):
+    """Complex compute dtype for an input tensor (real inputs are promoted,
+    as in the reference's A * d, sketch.py:315)."""
+    torch = _torch()
+    if t.dtype in (torch.complex64, torch.float32):
+        return torch.complex64
+    return torch.complex128
+
+
+def srft_dev(A, op):
+    """Y = scale * dft(A o d)[:, picks] for a device matrix A (K5 kernel)."""
+    torch = _torch()
+    m, n = A.shape
+    if n & (n - 1):
+        raise NotImplementedError(
+            "SRFT for non-power-of-two n needs the Bluestein path (SURVEY.md §8f #3)")
+    cdt = _complex_of(A)
+    code = _lib.dtype_code(cdt)
+    h = _lib.handle(A.device.index)
+    if A.dtype != cdt:
+        Ac = torch.empty((m, n), dtype=cdt, device=A.device)
+        _lib.call("lr_copy", h, _lib.dtype_code(A.dtype), _lib.ptr(A), _lib.ld(A), code,
+                  _lib.ptr(Ac), _lib.ld(Ac), m, n, 0)
+        A = Ac
+    d = torch.from_numpy(np.ascontiguousarray(op.d)).to(device=A.device, dtype=cdt)
+    picks = torch.from_numpy(np.ascontiguousarray(op.picks, dtype=np.int32)).to(A.device)
+    Y = torch.empty((m, op.ell), dtype=cdt, device=A.device)
+    _lib.call("lr_srft", h, code, m, n, op.ell, _lib.ptr(A), _lib.ld(A), _lib.ptr(d),
+              _lib.ptr(picks), float(op.scale), _lib.ptr(Y), _lib.ld(Y))
+    return Y
+
+
+def srft_apply(A, spec_or_op):
+    """Y = A @ Omega for an SRFT Omega (sketch.py:306-320), on the GPU.
+
+    The result is complex and agrees with the explicit dense product to
+    roundoff of the compute precision."""
+    host = not is_device_array(A)
+    t = to_device(A)
+    if t.dim() != 2:
+        raise ValueError("A must be 2-D")
+    op = _resolve(spec_or_op, t.shape[1])
+    return _out(srft_dev(t, op), host)
+
+
+def dft(v, axis=-1):
+    """Unitary DFT along `axis`, f_pq = n^-1/2 exp(-2 pi i pq / n)
+    (sketch.py:179-200); power-of-two lengths only in this build."""
+    torch = _torch()
+    host = not is_device_array(v)
+    t = to_device(v)
+    if t.dim() == 0:
+        raise ValueError("dft expects a vector or matrix")
+    t = torch.movedim(t, axis, -1)
+    shape = t.shape
+    n = shape[-1]
+    cdt = _complex_of(t)
+    X = t.to(cdt).reshape(-1, n).contiguous()
+    if n > 1:
+        if n & (n - 1):
+            raise NotImplementedError(
+                "dft for non-power-of-two n needs the Bluestein path (SURVEY.md §8f #3)")
+        _lib.call("lr_dft_rows", _lib.handle(X.device.index), _lib.dtype_code(cdt), X.shape[0], n,
+                  _lib.ptr(X), _lib.ld(X))
+    out = torch.movedim(X.reshape(shape), -1, axis)
+    return _out(out, host)
+
+
+def gsrft_operator(n, ell, seed):
+    raise NotImplementedError("GSRFT is outside this build's scope (SURVEY.md §8f #3)")
+
+
+def gsrft_apply(A, spec_or_op):
+    raise NotImplementedError("GSRFT is outside this build's scope (SURVEY.md §8f #3)")

@@ -1,0 +1,103 @@
+"""Sparse-plus-low-rank operator on the GPU (configuration 5).
+
+The reference has no sparse code; its extension point for matrix-free A is
+the MatVecOperator protocol (core.py:343-380) -- a user subclass with
+``_apply`` / ``_apply_adjoint``.  CudaCsrOperator is that subclass on the
+device: A = S + L R^T with S in CSR (K6 SpMM kernel) and an optional
+implicit low-rank term applied as two skinny GEMMs.  The transpose product
+uses a CSR copy of S^T built once at construction (no atomics, so the
+product is deterministic).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+from .core import MatVecOperator, _as2d, _out, _torch, is_device_array, to_device
+
+
+class CudaCsrOperator(MatVecOperator):
+    """A = S + L R^T, S sparse (scipy CSR/CSC/COO or (rowptr, col, val, shape))."""
+
+    device_native = True
+
+    def __init__(self, S, L=None, R=None, device=None):
+        torch = _torch()
+        import scipy.sparse as sp
+        if isinstance(S, tuple):
+            rowptr, col, val, shape = S
+            S = sp.csr_matrix((np.asarray(val), np.asarray(col), np.asarray(rowptr)), shape=shape)
+        S = sp.csr_matrix(S)
+        S.sum_duplicates()
+        m, n = S.shape
+        super().__init__(m, n)
+        St = S.T.tocsr()
+        St.sum_duplicates()
+        dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        self.device = dev
+
+        def up(csr):
+            return (torch.from_numpy(csr.indptr.astype(np.int64)).to(dev),
+                    torch.from_numpy(csr.indices.astype(np.int32)).to(dev),
+                    torch.from_numpy(csr.data.astype(np.float64)).to(dev))
+
+        self.S = up(S)
+        self.St = up(St)
+        self.nnz = int(S.nnz)
+        self.L = None if L is None else to_device(L, torch.float64, dev.index)
+        self.R = None if R is None else to_device(R, torch.float64, dev.index)
+        if (self.L is None) != (self.R is None):
+            raise ValueError("L and R must be given together")
+        if self.L is not None and (self.L.shape[0] != m or self.R.shape[0] != n
+                                   or self.L.shape[1] != self.R.shape[1]):
+            raise ValueError("low-rank factors do not match the sparse part")
+        self.host_io = True
+        self.dtype = torch.float64
+
+    def csr_bytes(self):
+        """Bytes of one pass over the CSR data (values, column indices, row pointers)."""
+        return self.nnz * (8 + 4) + (self.m + 1) * 8
+
+    def _spmm(self, csr, rows, X, Y, accumulate):
+        rowptr, col, val = csr
+        _lib.call("lr_csr_spmm", _lib.handle(X.device.index), _lib.F64, rows, X.shape[0],
+                  X.shape[1], _lib.ptr(rowptr), _lib.ptr(col), _lib.ptr(val), _lib.ptr(X),
+                  _lib.ld(X), _lib.ptr(Y), _lib.ld(Y), 1 if accumulate else 0)
+
+    def _lowrank(self, P, Qf, X, Y):
+        """Y = P (Qf^T X)  (P: rows x r, Qf: cols x r)."""
+        torch = _torch()
+        r = P.shape[1]
+        Cm = torch.empty((r, X.shape[1]), dtype=torch.float64, device=X.device)
+        h = _lib.handle(X.device.index)
+        _lib.call("lr_gemm", h, _lib.F64, _lib.OP_T, Qf.shape[0], r, X.shape[1], _lib.ptr(Qf),
+                  _lib.ld(Qf), _lib.ptr(X), _lib.ld(X), _lib.ptr(Cm), _lib.ld(Cm))
+        _lib.call("lr_gemm", h, _lib.F64, _lib.OP_N, P.shape[0], r, X.shape[1], _lib.ptr(P),
+                  _lib.ld(P), _lib.ptr(Cm), _lib.ld(Cm), _lib.ptr(Y), _lib.ld(Y))
+
+    def _run(self, X, adjoint):
+        torch = _torch()
+        host = not is_device_array(X)
+        t = to_device(X, torch.float64, self.device.index)
+        t, vec = _as2d(t)
+        rows = self.n if adjoint else self.m
+        if t.shape[0] != (self.m if adjoint else self.n):
+            raise ValueError("dimension mismatch")
+        Y = torch.empty((rows, t.shape[1]), dtype=torch.float64, device=t.device)
+        acc = False
+        if self.L is not None:
+            if adjoint:
+                self._lowrank(self.R, self.L, t, Y)      # R (L^T Y)
+            else:
+                self._lowrank(self.L, self.R, t, Y)      # L (R^T X)
+            acc = True
+        self._spmm(self.St if adjoint else self.S, rows, t, Y, acc)
+        Y = Y.reshape(-1) if vec else Y
+        return _out(Y, host)
+
+    def _apply(self, X):
+        return self._run(X, False)
+
+    def _apply_adjoint(self, Y):
+        return self._run(Y, True)

@@ -1,0 +1,192 @@
+"""Generate golden vectors by running the REFERENCE package itself.
+
+Run in the build container only (the reference lives at /root/reference and
+does not travel to the GPU box):
+
+    python tests/golden/make_golden.py [name ...]
+
+Writes small .npz fixtures next to this script.  Each fixture stores the
+inputs' seeds/recipes (matrices are regenerated from seeds by workloads.py)
+and the reference's outputs: singular values, estimator values, pass counts
+and leading slices of Q/U/V.  tests/test_oracle_golden.py pins the oracle
+to these; tests/test_gpu_parity.py pins the CUDA path to them.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, ROOT)
+
+import lowrank  # noqa: E402  (the reference)
+from lowrank import core, factor, rangefinder, sketch  # noqa: E402
+from lowrank.oracle import SyntheticSpec, synthetic_matrix  # noqa: E402
+
+import workloads  # noqa: E402
+
+
+def save(name, **arrs):
+    path = os.path.join(HERE, f"{name}.npz")
+    np.savez_compressed(path, **arrs)
+    print(f"wrote {path} ({os.path.getsize(path)} B)", flush=True)
+
+
+def g_kats():
+    out = {}
+    # Philox draws (sketch.py:32-42,96-100; rangefinder.py:78)
+    out["gauss_7x3_s11"] = sketch.gaussian_matrix(7, 3, 11)
+    out["probe_6x2_s5"] = sketch.rng_for(5, 0x70726F62).standard_normal((6, 2))
+    op = sketch.srft_operator(64, 8, 3)
+    out["srft64_d"], out["srft64_picks"] = op.d, op.picks
+    op = sketch.srft_operator(8192, 120, 3)
+    out["srft8192_d_head"], out["srft8192_picks"] = op.d[:64], op.picks
+    out["srft8192_d_sum"] = np.array([op.d.sum()])
+    # orthonormalize_double_gs (core.py:84-115) KATs, test_core.py:75-93
+    out["dgs_collinear"] = core.orthonormalize_double_gs(np.array([[1.0, 2.0], [0.0, 0.0]]))
+    rng = np.random.default_rng(11)
+    Y = rng.standard_normal((100, 10))
+    Y[:, 1] = 1e-14 * Y[:, 0]
+    out["dgs_neardep_Y"], out["dgs_neardep_Q"] = Y, core.orthonormalize_double_gs(Y)
+    rng = np.random.default_rng(12)
+    Y = rng.standard_normal((40, 12))
+    out["dgs_rand_Y"], out["dgs_rand_Q"] = Y, core.orthonormalize_double_gs(Y)
+    Yc = rng.standard_normal((30, 7)) + 1j * rng.standard_normal((30, 7))
+    out["dgs_cplx_Y"], out["dgs_cplx_Q"] = Yc, core.orthonormalize_double_gs(Yc)
+    # small_svd (core.py:199-230) KATs, test_core.py:144-184
+    f = core.small_svd(np.array([[1.0, 1.0], [0.0, 1.0]]))
+    out["svd_golden_s"] = f.sigma
+    rng = np.random.default_rng(8)
+    B = rng.standard_normal((7, 9))
+    f = core.small_svd(B)
+    out["svd_rand_B"], out["svd_rand_U"], out["svd_rand_s"], out["svd_rand_V"] = B, f.U, f.sigma, f.V
+    Bc = rng.standard_normal((6, 11)) + 1j * rng.standard_normal((6, 11))
+    f = core.small_svd(Bc)
+    out["svd_cplx_B"], out["svd_cplx_U"], out["svd_cplx_s"], out["svd_cplx_V"] = Bc, f.U, f.sigma, f.V
+    # direct_svd KAT (tests/test_factor.py:46-51)
+    f = factor.direct_svd(core.DenseOperator(np.diag([5.0, 4.0, 3.0, 2.0, 1.0])), np.eye(5)[:, :3])
+    out["dsvd_diag_s"] = f.sigma
+    # dft (sketch.py:179-200), test_sketch.py:90-107
+    out["dft_n2"] = sketch.dft(np.array([1.0, 0.0]))
+    out["dft_n4"] = sketch.dft(np.ones(4))
+    rng = np.random.default_rng(16)
+    v = rng.standard_normal((3, 16)) + 1j * rng.standard_normal((3, 16))
+    out["dft16_in"], out["dft16_out"] = v, sketch.dft(v, axis=1)
+    v = rng.standard_normal((2, 12))
+    out["dft12_in"], out["dft12_out"] = v, sketch.dft(v, axis=1)
+    # srft_apply (sketch.py:306-320), test_sketch.py:147-151
+    rng = np.random.default_rng(6)
+    A = rng.standard_normal((16, 16))
+    op = sketch.srft_operator(16, 4, 1)
+    out["srft_A"], out["srft_Y"] = A, sketch.srft_apply(A, op)
+    # small range-finder runs (rangefinder.py), exercised at every entry point
+    rng = np.random.default_rng(10)
+    A = rng.standard_normal((25, 18))
+    out["rf_A"] = A
+    b = rangefinder.randomized_range_finder(A, 6, 11)
+    out["rf_basic_Q"] = b.Q
+    b = rangefinder.power_iteration_range(A, 6, 2, 11)
+    out["rf_power_Q"] = b.Q
+    b = rangefinder.subspace_iteration_range(A, 6, 2, 11)
+    out["rf_subspace_Q"] = b.Q
+    f = factor.direct_svd(A, b.Q)
+    out["rf_dsvd_U"], out["rf_dsvd_s"], out["rf_dsvd_V"] = f.U, f.sigma, f.V
+    out["rf_est"] = np.array([rangefinder.posterior_error_estimate(A, b.Q, seed=3)])
+    b = rangefinder.fast_range_finder(A[:, :16], 5, 4)
+    out["rf_fast_Q"] = b.Q
+    out["rf_fast_maximag"] = np.array([b.diagnostics["max_imag_sample"]])
+    save("kats", **out)
+
+
+def run_cfg(A_or_op, k, p, q, seed, sketch_kind="gauss", A_dense=None):
+    op = core.as_operator(A_or_op)
+    ell = k + p
+    t0 = time.perf_counter()
+    if sketch_kind == "gauss":
+        basis = (rangefinder.subspace_iteration_range(op, ell, q, seed) if q > 0
+                 else rangefinder.randomized_range_finder(op, ell, seed))
+    else:
+        basis = rangefinder.fast_range_finder(A_dense, ell, seed, kind="srft")
+    f = factor.direct_svd(op, basis.Q)
+    t1 = time.perf_counter()
+    est = rangefinder.posterior_error_estimate(op, basis.Q, r=10, alpha=10.0, seed=seed + 13)
+    t2 = time.perf_counter()
+    print(f"  reference stage A + direct_svd {t1 - t0:.2f}s, estimator {t2 - t1:.2f}s", flush=True)
+    return dict(sigma=f.sigma, est=np.array([est]), passes=np.array([basis.passes]),
+                samples=np.array([basis.samples_used]), rank=np.array([basis.Q.shape[1]]),
+                Q_head=basis.Q[:8], U_head=f.U[:8], V_head=f.V[:8],
+                Q_colsum=basis.Q.sum(axis=0), U_colsum=f.U.sum(axis=0), V_colsum=f.V.sum(axis=0),
+                counters=np.array([op.counters.matvecs, op.counters.adjoint_matvecs,
+                                   op.counters.passes, op.counters.flops], dtype=np.int64),
+                t_ref=np.array([t1 - t0, t2 - t1]))
+
+
+def g_cfg1():
+    c = workloads.CONFIGS[1]
+    A, s = synthetic_matrix(SyntheticSpec(c.m, c.n, "explicit", workloads.spectrum(1, c.n), c.seed))
+    Aw, _ = workloads.build_cfg1()
+    assert np.array_equal(A, Aw), "workloads.build_cfg1 must reproduce the reference builder"
+    save("cfg1", **run_cfg(A, c.k, c.p, c.q, c.seed), A_head=A[:4, :8], A_fro=np.array([np.linalg.norm(A)]))
+
+
+def g_cfg2():
+    c = workloads.CONFIGS[2]
+    t0 = time.time()
+    A, _ = synthetic_matrix(SyntheticSpec(c.m, c.n, "explicit", workloads.spectrum(2, c.n), c.seed))
+    print(f"  cfg2 A built in {time.time() - t0:.0f}s", flush=True)
+    save("cfg2", **run_cfg(A, c.k, c.p, c.q, c.seed), A_head=A[:4, :8], A_fro=np.array([np.linalg.norm(A)]))
+
+
+def g_cfg3():
+    c = workloads.CONFIGS[3]
+    A = workloads.build_cfg3()
+    save("cfg3", **run_cfg(A, c.k, c.p, c.q, c.seed, "srft", A_dense=A), A_head=A[:4, :8],
+         A_fro=np.array([np.linalg.norm(A.astype(np.complex128))]))
+
+
+def g_cfg4s():
+    """cfg4 recipe at one 65536-row block (the full 2^20 rows need a 32 GiB
+    fp64 upcast and ~15 min of CGS2 in the reference)."""
+    c = workloads.CONFIGS[4]
+    A, _ = workloads.build_cfg4_host(m=65536)
+    save("cfg4s", **run_cfg(A, c.k, c.p, c.q, c.seed), A_head=A[:4, :8],
+         A_fro=np.array([np.linalg.norm(A.astype(np.float64))]))
+
+
+class _CsrPlusLowRank(core.MatVecOperator):
+    """A user MatVecOperator plug-in over scipy CSR (the
+    reference has no sparse code; this is the oracle the survey prescribes)."""
+
+    def __init__(self, S, L, R):
+        super().__init__(*S.shape)
+        self.S, self.St, self.L, self.R = S, S.T.tocsr(), L, R
+
+    def _apply(self, X):
+        return self.S @ X + self.L @ (self.R.T @ X)
+
+    def _apply_adjoint(self, Y):
+        return self.St @ Y + self.R @ (self.L.T @ Y)
+
+
+def g_cfg5s():
+    """cfg5 recipe at n = 2^16 rows/cols."""
+    c = workloads.CONFIGS[5]
+    S, L, R = workloads.build_cfg5(n=1 << 16)
+    op = _CsrPlusLowRank(S, L, R)
+    save("cfg5s", **run_cfg(op, c.k, c.p, c.q, c.seed), nnz=np.array([S.nnz]))
+
+
+ALL = {"kats": g_kats, "cfg1": g_cfg1, "cfg3": g_cfg3, "cfg4s": g_cfg4s, "cfg5s": g_cfg5s,
+       "cfg2": g_cfg2}
+
+if __name__ == "__main__":
+    names = sys.argv[1:] or list(ALL)
+    for nm in names:
+        print(f"[{nm}]", flush=True)
+        ALL[nm]()

@@ -1,0 +1,250 @@
+"""Kernel-level parity on the GPU: each C-ABI entry point against numpy /
+the CPU oracle on seeded inputs (bit-exact where integer, stated tolerance
+where floating point)."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def lr():
+    import paper_0909_4061_b200 as m
+    return m
+
+
+def rand(shape, dtype, seed):
+    g = np.random.default_rng(seed)
+    a = g.standard_normal(shape)
+    if np.dtype(dtype).kind == "c":
+        a = a + 1j * g.standard_normal(shape)
+    return a.astype(dtype)
+
+
+GEMM_SHAPES = [(300, 257, 30), (1, 5, 1), (129, 64, 110), (64, 1000, 10), (513, 77, 128),
+               (200, 300, 130), (2048, 2048, 30), (37, 1, 3)]
+
+
+@pytest.mark.parametrize("m,n,ell", GEMM_SHAPES)
+@pytest.mark.parametrize("dtype", [np.float64, np.complex128])
+def test_gemm_f64_family(m, n, ell, dtype):
+    from paper_0909_4061_b200.core import DenseOperator
+    A = rand((m, n), dtype, m + n)
+    X = rand((n, ell), dtype, ell)
+    W = rand((m, ell), dtype, ell + 1)
+    op = DenseOperator(A)
+    Y = op.apply(X)
+    ref = A @ X
+    scale = np.abs(A).max() * np.abs(X).max() * n
+    assert np.abs(Y - ref).max() <= 1e-14 * scale
+    Z = op.apply_adjoint(W)
+    ref = A.conj().T @ W
+    assert np.abs(Z - ref).max() <= 1e-14 * np.abs(A).max() * np.abs(W).max() * m
+    assert op.counters.passes == 2 and op.counters.matvecs == ell
+
+
+@pytest.mark.parametrize("m,n,ell", [(300, 257, 30), (129, 64, 110), (1000, 512, 64)])
+@pytest.mark.parametrize("dtype", [np.float32, np.complex64])
+def test_gemm_f32_family(m, n, ell, dtype):
+    from paper_0909_4061_b200.core import DenseOperator
+    A = rand((m, n), dtype, m + n)
+    X = rand((n, ell), dtype, ell)
+    op = DenseOperator(A)
+    Y = op.apply(X)
+    ref = A.astype(np.complex128 if A.dtype.kind == "c" else np.float64) @ X
+    assert np.abs(Y - ref).max() <= 2e-6 * np.abs(ref).max()
+    W = rand((m, ell), dtype, 3)
+    Z = op.apply_adjoint(W)
+    ref = A.conj().T.astype(ref.dtype) @ W
+    assert np.abs(Z - ref).max() <= 2e-6 * np.abs(ref).max()
+
+
+def test_gemm_vector_and_strided_inputs():
+    from paper_0909_4061_b200.core import DenseOperator
+    A = rand((50, 40), np.float64, 1)
+    op = DenseOperator(A)
+    x = rand(40, np.float64, 2)
+    assert op.apply(x).shape == (50,)
+    assert np.allclose(op.apply(x), A @ x, rtol=0, atol=1e-13)
+    Xt = torch.from_numpy(rand((40, 9), np.float64, 3)).cuda()[:, 2:7]   # strided view
+    Y = op.apply(Xt)
+    assert torch.is_tensor(Y)
+    assert np.allclose(Y.cpu().numpy(), A @ Xt.cpu().numpy(), atol=1e-13)
+
+
+def test_nonfinite_rejected():
+    from paper_0909_4061_b200.core import DenseOperator
+    A = np.ones((4, 3))
+    A[2, 1] = np.nan
+    with pytest.raises(ValueError):
+        DenseOperator(A)
+    with pytest.raises(ValueError):
+        DenseOperator(np.ones((3,)))
+    with pytest.raises(ValueError):
+        DenseOperator(np.ones((0, 3)))
+
+
+@pytest.mark.parametrize("m,ell,dtype", [(500, 30, np.float64), (2000, 110, np.float64),
+                                         (300, 7, np.complex128), (5000, 256, np.float64),
+                                         (1000, 48, np.float32), (400, 20, np.complex64)])
+def test_orth_matches_cgs2(m, ell, dtype):
+    from oracle import lowrank_oracle as O
+    Y = rand((m, ell), dtype, m * ell)
+    Q = lr().orthonormalize_double_gs(Y)
+    Qo = O.orthonormalize_double_gs(Y.astype(np.complex128 if Y.dtype.kind == "c" else np.float64))
+    assert Q.shape == Qo.shape
+    tol = 1e-12 if Y.dtype in (np.float64, np.complex128) else 2e-5
+    assert np.abs(Q - Qo).max() <= tol
+    k = Q.shape[1]
+    assert np.linalg.norm(Q.conj().T @ Q - np.eye(k)) <= (1e-12 if tol < 1e-6 else 1e-5) * k
+
+
+def test_orth_ill_conditioned_panel():
+    """kappa(Y) ~ 1e7 (cfg5-like): fp64 Gram CholQR2 cannot resolve it; the
+    guarded fallback must still give the reference's Q."""
+    from oracle import lowrank_oracle as O
+    g = np.random.default_rng(5)
+    U = np.linalg.qr(g.standard_normal((3000, 48)))[0]
+    V = np.linalg.qr(g.standard_normal((48, 48)))[0]
+    s = np.logspace(0, -7.5, 48)
+    Y = (U * s) @ V.T
+    Q = lr().orthonormalize_double_gs(Y)
+    Qo = O.orthonormalize_double_gs(Y)
+    assert Q.shape == Qo.shape
+    assert np.linalg.norm(Q.T @ Q - np.eye(Q.shape[1])) <= 1e-12 * 48
+    # span agreement: the projector difference is tiny where the oracle is accurate
+    assert np.linalg.norm(Q @ (Q.T @ Qo) - Qo) <= 1e-6
+
+
+def test_orth_golden_kats(golden):
+    g = golden("kats")
+    m = lr()
+    Q = m.orthonormalize_double_gs(np.array([[1.0, 2.0], [0.0, 0.0]]))
+    assert Q.shape == (2, 1) and np.allclose(Q, g["dgs_collinear"], atol=1e-14)
+    Q = m.orthonormalize_double_gs(g["dgs_neardep_Y"])
+    assert Q.shape == (100, 9)
+    assert np.abs(Q - g["dgs_neardep_Q"]).max() <= 1e-10
+    for key in ("dgs_rand", "dgs_cplx"):
+        Q = m.orthonormalize_double_gs(g[f"{key}_Y"])
+        assert np.abs(Q - g[f"{key}_Q"]).max() <= 1e-12
+    assert m.orthonormalize_double_gs(np.zeros((5, 3))).shape == (5, 0)
+    Q = m.orthonormalize_double_gs(np.eye(4))
+    assert np.allclose(np.abs(Q), np.eye(4))
+
+
+def test_orth_tol_zero_keeps_tiny_columns():
+    Y = np.random.default_rng(1).standard_normal((50, 4))
+    Y[:, 2] = Y[:, 0] + 1e-9 * Y[:, 2]
+    Q = lr().orthonormalize_double_gs(Y, tol=0.0)
+    assert Q.shape == (50, 4)
+    Q = lr().orthonormalize_double_gs(Y, tol=1e-8)
+    assert Q.shape == (50, 3)
+
+
+def test_small_svd_golden(golden):
+    g = golden("kats")
+    m = lr()
+    s = m.small_svd(np.array([[1.0, 1.0], [0.0, 1.0]])).sigma
+    assert s[0] == pytest.approx(1.6180339887, abs=1e-9)
+    assert s[1] == pytest.approx(0.6180339887, abs=1e-9)
+    for key in ("svd_rand", "svd_cplx"):
+        f = m.small_svd(g[f"{key}_B"])
+        assert np.abs(f.sigma - g[f"{key}_s"]).max() <= 1e-13
+        assert np.abs(f.U - g[f"{key}_U"]).max() <= 1e-11
+        assert np.abs(f.V - g[f"{key}_V"]).max() <= 1e-11
+    assert np.allclose(m.small_svd(np.diag([3.0, 1.0])).sigma, [3.0, 1.0])
+    assert np.allclose(m.small_svd(np.array([[0.0, 1.0], [1.0, 0.0]])).sigma, [1.0, 1.0])
+
+
+@pytest.mark.parametrize("r,c", [(30, 2048), (110, 8192), (10, 7), (7, 7), (120, 300)])
+def test_small_svd_vs_oracle(r, c):
+    from oracle import lowrank_oracle as O
+    B = rand((r, c), np.float64, r * c)
+    f = lr().small_svd(B)
+    fo = O.small_svd(B)
+    assert np.abs(f.sigma - fo.sigma).max() <= 1e-13 * fo.sigma[0]
+    k = min(r, c)
+    assert np.abs(f.U - fo.U).max() <= 1e-10
+    assert np.abs(f.V - fo.V).max() <= 1e-10
+    assert np.linalg.norm((f.U * f.sigma) @ f.V.T - B) <= 1e-13 * np.linalg.norm(B) * k
+
+
+def test_small_svd_graded():
+    """Graded spectrum down to 1e-8 (cfg5-like): relative accuracy of the
+    small singular values through CholeskyQR + one-sided Jacobi."""
+    from oracle import lowrank_oracle as O
+    g = np.random.default_rng(3)
+    U = np.linalg.qr(g.standard_normal((48, 48)))[0]
+    V = np.linalg.qr(g.standard_normal((5000, 48)))[0]
+    s = np.logspace(0, -8, 48)
+    B = (U * s) @ V.T
+    f = lr().small_svd(B)
+    assert np.all(np.abs(f.sigma - s) <= 1e-8 * s + 1e-15)
+
+
+def test_small_svd_rank_deficient():
+    B = np.zeros((3, 6))
+    B[0, 0] = 2.0
+    f = lr().small_svd(B)
+    assert np.allclose(f.sigma, [2.0, 0.0, 0.0])
+    assert np.allclose((f.U * f.sigma) @ f.V.T, B, atol=1e-14)
+
+
+def test_dft_and_srft_golden(golden):
+    g = golden("kats")
+    m = lr()
+    assert np.allclose(m.dft(np.array([1.0, 0.0])), g["dft_n2"], atol=1e-15)
+    assert np.allclose(m.dft(np.ones(4)), g["dft_n4"], atol=1e-15)
+    assert np.abs(m.dft(g["dft16_in"], axis=1) - g["dft16_out"]).max() <= 1e-13
+    Y = m.srft_apply(g["srft_A"], m.srft_operator(16, 4, 1))
+    assert np.abs(Y - g["srft_Y"]).max() <= 1e-13
+    with pytest.raises(NotImplementedError):
+        m.dft(g["dft12_in"], axis=1)
+
+
+@pytest.mark.parametrize("n", [64, 1024, 8192])
+def test_srft_vs_oracle(n):
+    from oracle import lowrank_oracle as O
+    A = rand((33, n), np.complex128, n)
+    op = O.srft_operator(n, 17, 9)
+    Y = lr().srft_apply(A, lr().srft_operator(n, 17, 9))
+    Yo = O.srft_apply(A, op)
+    assert np.abs(Y - Yo).max() <= 1e-12 * np.abs(Yo).max()
+    A32 = A.astype(np.complex64)
+    Y32 = lr().srft_apply(A32, lr().srft_operator(n, 17, 9))
+    assert np.abs(Y32 - Yo).max() <= 2e-5 * np.abs(Yo).max()
+
+
+def test_csr_spmm_vs_scipy():
+    import scipy.sparse as sp
+    from paper_0909_4061_b200.sparse import CudaCsrOperator
+    g = np.random.default_rng(4)
+    S = sp.random(3000, 2500, density=0.004, random_state=4, format="csr")
+    L = g.standard_normal((3000, 5))
+    R = g.standard_normal((2500, 5))
+    op = CudaCsrOperator(S, L, R)
+    X = g.standard_normal((2500, 48))
+    Y = g.standard_normal((3000, 48))
+    assert np.abs(op.apply(X) - (S @ X + L @ (R.T @ X))).max() <= 1e-12 * 50
+    assert np.abs(op.apply_adjoint(Y) - (S.T @ Y + R @ (L.T @ Y))).max() <= 1e-12 * 50
+    op2 = CudaCsrOperator(S)
+    assert np.abs(op2.apply(X) - S @ X).max() <= 1e-12
+
+
+def test_estimate_matches_oracle():
+    from oracle import lowrank_oracle as O
+    A = rand((400, 300), np.float64, 7)
+    Q = np.linalg.qr(rand((400, 20), np.float64, 8))[0]
+    e = lr().posterior_error_estimate(A, Q, r=10, alpha=10.0, seed=5)
+    eo = O.posterior_error_estimate(A, Q, r=10, alpha=10.0, seed=5)
+    assert e == pytest.approx(eo, rel=1e-12)
+    assert lr().posterior_error_estimate(A, np.zeros((400, 0)), seed=5) == pytest.approx(
+        O.posterior_error_estimate(A, np.zeros((400, 0)), seed=5), rel=1e-12)

@@ -1,0 +1,184 @@
+"""Pipeline parity on the GPU against the reference's own outputs
+(tests/golden, produced by tests/golden/make_golden.py from the reference)
+on the same A and the same Omega / D / R / probes.
+
+Tolerances (north_star): singular values relative <= 1e-10
+(fp64) / <= 1e-4 (fp32, complex64) where sigma_j is above the dtype noise
+floor; posterior estimate within 1%; Q / U / V elementwise after the
+reference sign convention; pass counts and operator counters identical.
+"""
+
+import numpy as np
+import pytest
+
+import workloads
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def lr():
+    import paper_0909_4061_b200 as m
+    return m
+
+
+def test_small_range_finders_match_reference(golden):
+    g = golden("kats")
+    m = lr()
+    A = g["rf_A"]
+    assert np.abs(m.randomized_range_finder(A, 6, 11).Q - g["rf_basic_Q"]).max() <= 1e-12
+    b = m.power_iteration_range(A, 6, 2, 11)
+    assert np.abs(b.Q - g["rf_power_Q"]).max() <= 1e-9 and b.passes == 6
+    b = m.subspace_iteration_range(A, 6, 2, 11)
+    assert np.abs(b.Q - g["rf_subspace_Q"]).max() <= 1e-12 and b.passes == 6
+    f = m.direct_svd(A, b.Q)
+    assert np.abs(f.sigma - g["rf_dsvd_s"]).max() <= 1e-12
+    assert np.abs(f.U - g["rf_dsvd_U"]).max() <= 1e-11
+    assert np.abs(f.V - g["rf_dsvd_V"]).max() <= 1e-11
+    assert m.posterior_error_estimate(A, b.Q, seed=3) == pytest.approx(g["rf_est"][0], rel=1e-10)
+    bf = m.fast_range_finder(A[:, :16], 5, 4)
+    assert np.abs(bf.Q - g["rf_fast_Q"]).max() <= 1e-11
+    assert bf.diagnostics["max_imag_sample"] == pytest.approx(g["rf_fast_maximag"][0], rel=1e-10)
+
+
+def test_reference_contracts():
+    """Drop-in semantics: validation errors, est_error,
+    q = 0 == Alg 4.1 bitwise, pass formulas, zero matrix."""
+    m = lr()
+    A = np.random.default_rng(10).standard_normal((25, 18))
+    with pytest.raises(ValueError):
+        m.randomized_range_finder(np.eye(4), 9, seed=0)
+    with pytest.raises(ValueError):
+        m.subspace_iteration_range(A, 6, -1, 0)
+    with pytest.raises(ValueError):
+        m.posterior_error_estimate(A, np.zeros((25, 0)), r=0)
+    with pytest.raises(ValueError):
+        m.posterior_error_estimate(A, np.zeros((25, 0)), alpha=1.0)
+    b0 = m.randomized_range_finder(A, 6, 11)
+    b1 = m.power_iteration_range(A, 6, 0, 11)
+    assert np.array_equal(b0.Q, b1.Q) and b1.passes == 2 and b0.passes == 1
+    assert b0.est_error is None and b0.samples_used == 6
+    for q in (0, 1, 3):
+        assert m.subspace_iteration_range(A, 4, q, 0).passes == 2 * q + 2
+    bz = m.randomized_range_finder(np.zeros((4, 3)), 2, seed=0)
+    assert bz.Q.shape == (4, 0) and bz.est_error == 0.0
+    fz = m.direct_svd(np.zeros((6, 4)), np.eye(6)[:, :2])
+    assert np.allclose(fz.sigma, 0.0)
+    f = m.direct_svd(np.diag([5.0, 4.0, 3.0, 2.0, 1.0]), np.eye(5)[:, :3])
+    assert np.allclose(f.sigma, [5.0, 4.0, 3.0])
+    assert np.linalg.norm(np.diag([5.0, 4, 3, 2, 1]) - f.compose(), 2) == pytest.approx(2.0, abs=1e-12)
+
+
+def test_roundoff_robustness_vs_naive_power():
+    """reference tests/test_rangefinder.py:258-272 on the GPU path."""
+    from oracle import lowrank_oracle as O
+    m = lr()
+    n = 12
+    A, _ = workloads.synthetic_explicit(n, n, [1.0, 1e-6] + [1e-14] * (n - 2), 17)
+    U = O.small_svd(A).U
+    bs = m.subspace_iteration_range(A, 4, 2, seed=5, ortho_tol=0.0)
+    bp = m.power_iteration_range(A, 4, 2, seed=5, safeguarded=False)
+    miss_s = np.linalg.norm(U[:, 1] - bs.Q @ (bs.Q.conj().T @ U[:, 1]))
+    miss_p = np.linalg.norm(U[:, 1] - bp.Q @ (bp.Q.conj().T @ U[:, 1]))
+    assert miss_s <= 1e-6
+    assert miss_p >= 0.5
+
+
+def test_exact_rank_recovery():
+    """acceptance #01 (test_acceptance.py:69-84), numerics part."""
+    from oracle import lowrank_oracle as O
+    m = lr()
+    A, _ = workloads.synthetic_explicit(100, 80, [1.0] * 10, 101)
+    norm_a = np.linalg.norm(A, 2)
+    op = m.DenseOperator(A)
+    for seed in range(20):
+        b = m.randomized_range_finder(op, 15, seed=seed)
+        assert O.exact_projection_error(A, b.Q) <= 1e-10 * norm_a
+
+
+def check_against_golden(g, f, basis, est, rel_tol, floor=None, vec_tol=None):
+    s_ref = g["sigma"]
+    s = np.asarray(f.sigma)
+    assert s.shape == s_ref.shape
+    mask = np.ones_like(s_ref, dtype=bool) if floor is None else s_ref >= floor * s_ref[0]
+    rel = np.abs(s - s_ref) / s_ref
+    assert np.all(rel[mask] <= rel_tol), f"max rel err {rel[mask].max():.3e} at {np.argmax(rel * mask)}"
+    assert est == pytest.approx(g["est"][0], rel=1e-2)
+    assert basis.passes == g["passes"][0]
+    assert basis.samples_used == g["samples"][0]
+    assert basis.Q.shape[1] == g["rank"][0]
+    if vec_tol is not None:
+        k = int(mask.sum())
+        assert np.abs(np.asarray(f.U)[:8, :k] - g["U_head"][:, :k]).max() <= vec_tol
+        assert np.abs(np.asarray(f.V)[:8, :k] - g["V_head"][:, :k]).max() <= vec_tol
+
+
+def test_cfg1_full(golden):
+    g = golden("cfg1")
+    c = workloads.CONFIGS[1]
+    A, _ = workloads.build_cfg1()
+    op = lr().DenseOperator(A)
+    basis, f, est = lr().randomized_svd(op, c.k, c.p, c.q, c.seed)
+    check_against_golden(g, f, basis, est, 1e-10, vec_tol=1e-9)
+    assert np.abs(basis.Q[:8] - g["Q_head"]).max() <= 1e-11
+    # counters identical to the reference (Stage A + direct_svd + estimator)
+    cnt = op.counters
+    assert [cnt.matvecs, cnt.adjoint_matvecs, cnt.passes, cnt.flops] == list(g["counters"])
+
+
+def test_cfg1_public_api_sequence(golden):
+    """The exact call sequence of the reference tests."""
+    g = golden("cfg1")
+    A, _ = workloads.build_cfg1()
+    m = lr()
+    b = m.randomized_range_finder(A, 30, 1)
+    f = m.direct_svd(A, b.Q)
+    est = m.posterior_error_estimate(A, b.Q, r=10, alpha=10.0, seed=14)
+    check_against_golden(g, f, b, est, 1e-10, vec_tol=1e-9)
+
+
+def test_cfg2_full(golden):
+    g = golden("cfg2")
+    c = workloads.CONFIGS[2]
+    A, _ = workloads.build_synthetic_device(c.m, c.n, workloads.spectrum(2, c.n), c.seed)
+    assert np.abs(A[:4, :8].cpu().numpy() - g["A_head"]).max() <= 1e-13
+    op = lr().DenseOperator(A)
+    basis, f, est = lr().randomized_svd(op, c.k, c.p, c.q, c.seed)
+    f.sigma = f.sigma.cpu().numpy()
+    f.U, f.V = f.U.cpu().numpy(), f.V.cpu().numpy()
+    check_against_golden(g, f, basis, est, 1e-10, vec_tol=1e-8)
+
+
+def test_cfg3_full(golden):
+    g = golden("cfg3")
+    c = workloads.CONFIGS[3]
+    A = workloads.build_cfg3()
+    assert np.array_equal(A[:4, :8], g["A_head"])
+    basis, f, est = lr().randomized_svd(A, c.k, c.p, c.q, c.seed, sketch="srft")
+    # complex64 arithmetic: 1e-4 on the planted rank-50 part
+    check_against_golden(g, f, basis, est, 1e-4, floor=1e-2)
+
+
+def test_cfg4_reduced_rows(golden):
+    """cfg4 recipe at one 65536-row block, fp32 arithmetic vs the reference's
+    fp64 run: 1e-4 relative above the fp32 floor."""
+    g = golden("cfg4s")
+    c = workloads.CONFIGS[4]
+    A, _ = workloads.build_cfg4_host(m=65536)
+    basis, f, est = lr().randomized_svd(A, c.k, c.p, c.q, c.seed)
+    check_against_golden(g, f, basis, est, 1e-4, floor=2e-5)
+
+
+def test_cfg5_reduced(golden):
+    g = golden("cfg5s")
+    c = workloads.CONFIGS[5]
+    S, L, R = workloads.build_cfg5(n=1 << 16)
+    op = lr().CudaCsrOperator(S, L, R)
+    basis, f, est = lr().randomized_svd(op, c.k, c.p, c.q, c.seed)
+    check_against_golden(g, f, basis, est, 1e-10, floor=1e-6)

@@ -1,0 +1,103 @@
+"""Pin the CPU oracle (oracle/lowrank_oracle.py) to vectors produced by the
+reference itself (tests/golden/make_golden.py).  CPU only."""
+
+import numpy as np
+import pytest
+
+import workloads
+from oracle import lowrank_oracle as O
+
+
+def test_philox_draws_bitwise(golden):
+    g = golden("kats")
+    assert np.array_equal(O.gaussian_matrix(7, 3, 11), g["gauss_7x3_s11"])
+    assert np.array_equal(O.probe_matrix(6, 2, 5), g["probe_6x2_s5"])
+    d = O.srft_operator(64, 8, 3)
+    assert np.array_equal(d.d, g["srft64_d"]) and np.array_equal(d.picks, g["srft64_picks"])
+    d = O.srft_operator(8192, 120, 3)
+    assert np.array_equal(d.d[:64], g["srft8192_d_head"])
+    assert np.array_equal(d.picks, g["srft8192_picks"])
+    assert np.allclose(d.d.sum(), g["srft8192_d_sum"][0], rtol=0, atol=1e-9)
+
+
+def test_dgs_kats(golden):
+    g = golden("kats")
+    assert np.allclose(O.orthonormalize_double_gs(np.array([[1.0, 2.0], [0.0, 0.0]])),
+                       g["dgs_collinear"])
+    Q = O.orthonormalize_double_gs(g["dgs_neardep_Y"])
+    assert Q.shape == g["dgs_neardep_Q"].shape == (100, 9)
+    assert np.abs(Q - g["dgs_neardep_Q"]).max() <= 1e-13
+    for key in ("dgs_rand", "dgs_cplx"):
+        Q = O.orthonormalize_double_gs(g[f"{key}_Y"])
+        assert np.abs(Q - g[f"{key}_Q"]).max() <= 1e-13
+    assert O.orthonormalize_double_gs(np.zeros((5, 3))).shape == (5, 0)
+
+
+def test_small_svd_kats(golden):
+    g = golden("kats")
+    s = O.small_svd(np.array([[1.0, 1.0], [0.0, 1.0]])).sigma
+    assert np.allclose(s, g["svd_golden_s"], rtol=0, atol=1e-14)
+    assert s[0] == pytest.approx(1.6180339887, abs=1e-9)
+    for key in ("svd_rand", "svd_cplx"):
+        f = O.small_svd(g[f"{key}_B"])
+        assert np.abs(f.sigma - g[f"{key}_s"]).max() <= 1e-13
+        assert np.abs(f.U - g[f"{key}_U"]).max() <= 1e-12
+        assert np.abs(f.V - g[f"{key}_V"]).max() <= 1e-12
+
+
+def test_dft_srft_kats(golden):
+    g = golden("kats")
+    assert np.allclose(O.dft(np.array([1.0, 0.0])), g["dft_n2"])
+    assert np.allclose(O.dft(np.ones(4)), g["dft_n4"])
+    assert np.abs(O.dft(g["dft16_in"], axis=1) - g["dft16_out"]).max() <= 1e-13
+    assert np.abs(O.dft(g["dft12_in"], axis=1) - g["dft12_out"]).max() <= 1e-12
+    Y = O.srft_apply(g["srft_A"], O.srft_operator(16, 4, 1))
+    assert np.abs(Y - g["srft_Y"]).max() <= 1e-13
+
+
+def test_range_finders_small(golden):
+    g = golden("kats")
+    A = g["rf_A"]
+    assert np.abs(O.randomized_range_finder(A, 6, 11).Q - g["rf_basic_Q"]).max() <= 1e-12
+    assert np.abs(O.power_iteration_range(A, 6, 2, 11).Q - g["rf_power_Q"]).max() <= 1e-10
+    b = O.subspace_iteration_range(A, 6, 2, 11)
+    assert np.abs(b.Q - g["rf_subspace_Q"]).max() <= 1e-12
+    f = O.direct_svd(A, b.Q)
+    assert np.abs(f.sigma - g["rf_dsvd_s"]).max() <= 1e-12
+    assert np.abs(f.U - g["rf_dsvd_U"]).max() <= 1e-12
+    assert np.abs(f.V - g["rf_dsvd_V"]).max() <= 1e-12
+    assert O.posterior_error_estimate(A, b.Q, seed=3) == pytest.approx(g["rf_est"][0], rel=1e-12)
+    bf = O.fast_range_finder(A[:, :16], 5, 4)
+    assert np.abs(bf.Q - g["rf_fast_Q"]).max() <= 1e-12
+    assert bf.diagnostics["max_imag_sample"] == pytest.approx(g["rf_fast_maximag"][0], rel=1e-12)
+
+
+def test_cfg1_oracle_matches_reference(golden):
+    g = golden("cfg1")
+    c = workloads.CONFIGS[1]
+    A, _ = workloads.build_cfg1()
+    assert np.array_equal(A[:4, :8], g["A_head"])
+    op = O.Dense(A)
+    basis, f, est = O.rsvd(op, c.k, c.p, c.q, c.seed)
+    assert np.abs(f.sigma - g["sigma"]).max() / g["sigma"][0] <= 1e-13
+    assert np.all(np.abs(f.sigma - g["sigma"]) <= 1e-10 * g["sigma"])
+    assert est == pytest.approx(g["est"][0], rel=1e-10)
+    assert basis.passes == g["passes"][0] and basis.Q.shape[1] == g["rank"][0]
+    assert np.abs(basis.Q[:8] - g["Q_head"]).max() <= 1e-12
+    assert np.abs(f.U[:8] - g["U_head"]).max() <= 1e-11
+    assert np.abs(f.V[:8] - g["V_head"]).max() <= 1e-11
+    assert [op.counters.matvecs, op.counters.adjoint_matvecs, op.counters.passes,
+            op.counters.flops] == list(g["counters"])
+
+
+def test_cfg5_reduced_oracle_matches_reference(golden):
+    g = golden("cfg5s")
+    c = workloads.CONFIGS[5]
+    S, L, R = workloads.build_cfg5(n=1 << 16)
+    assert S.nnz == g["nnz"][0]
+    op = O.SparsePlusLowRank(S, L, R)
+    basis, f, est = O.rsvd(op, c.k, c.p, c.q, c.seed)
+    top = g["sigma"] > 1e-6 * g["sigma"][0]
+    assert np.all(np.abs(f.sigma - g["sigma"])[top] <= 1e-10 * g["sigma"][top])
+    assert est == pytest.approx(g["est"][0], rel=1e-6)
+    assert basis.passes == g["passes"][0]
