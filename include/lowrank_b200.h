@@ -108,6 +108,22 @@ int lr_chol_drop(lr_handle_t h, int dtype, int64_t ell, const void* G,
 int lr_orth(lr_handle_t h, int dtype, int64_t m, int64_t ell, const void* Y, int64_t ldy,
             void* Q, int64_t ldq, double tol, int64_t* rank_out);
 
+/* Speculative (host-sync-free) variant of lr_orth for pipelines that are
+ * enqueued ahead / captured in a CUDA graph: CholeskyQR2 with the drop rule
+ * and the pivot-resolvability test evaluated on the device.  Writes Q
+ * (m x ell) and ORs flags into *status (device int32): 1 = a pivot too
+ * small to be resolved from the Gram, 2 = a column was dropped, 4 =
+ * non-finite input.  status == 0 afterwards means Q is exactly what lr_orth
+ * returns with rank == ell; otherwise the caller re-runs with lr_orth.
+ * Q must not alias Y. */
+int lr_orth_fast(lr_handle_t h, int dtype, int64_t m, int64_t ell, const void* Y, int64_t ldy,
+                 void* Q, int64_t ldq, double tol, int32_t* status);
+
+/* Speculative variant of lr_small_svd (no host sync; Bh is not modified);
+ * flags as lr_orth_fast plus 8 = Jacobi sweep limit reached. */
+int lr_small_svd_fast(lr_handle_t h, int dtype, int64_t ell, int64_t ncols, const void* Bh,
+                      void* U, double* S, void* V, int32_t* status);
+
 /* Small SVD of B (ell x ncols, ell <= ncols) given through Bh = B^H
  * (ncols x ell, row-major) -- which is exactly what the adjoint pass of
  * direct_svd produces (reference factor.py:163-164, core.py:199-230).
@@ -170,6 +186,17 @@ int lr_sign_fix(lr_handle_t h, int dtype, int64_t rows, int64_t vrows, int64_t c
  * diagnostics["max_imag_sample"], reference rangefinder.py:261-262). */
 int lr_max_abs_imag(lr_handle_t h, int dtype, int64_t m, int64_t n, const void* Y, int64_t ldy,
                     double* out);
+
+/* The reference's Gaussian draws on the device (replaces the host draw of
+ * gaussian_matrix, reference sketch.py:32-42,96-100, and of the estimator
+ * probes, rangefinder.py:78): writes the first `count` values of numpy's
+ * Generator(Philox(key)).standard_normal stream -- Philox4x64-10 with the
+ * 128-bit key (key_lo = seed, key_hi = stream | index << 32) and numpy's
+ * 256-layer ziggurat -- as f64 or f32 (rounded like numpy's astype).
+ * Flags ORed into *status (device, may be NULL): 16 = a tail attempt
+ * exceeded 63 draws, 32 = internal stream margin too short.  Async. */
+int lr_gaussian(lr_handle_t h, uint64_t key_lo, uint64_t key_hi, int64_t count, int dtype,
+                void* out, int32_t* status);
 
 /* BLAS-1 helpers for the column-wise paths (device CGS2 / the unsafeguarded
  * Gram-Schmidt of power_iteration_range(safeguarded=False), reference

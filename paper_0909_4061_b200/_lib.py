@@ -52,6 +52,8 @@ _SIGS = {
     "lr_chol_drop": [_vp, _int, _i64, _vp, C.c_double, C.c_double, C.c_double, _vp, _vp, _vp],
     "lr_orth": [_vp, _int, _i64, _i64, _vp, _i64, _vp, _i64, C.c_double, C.POINTER(_i64)],
     "lr_small_svd": [_vp, _int, _i64, _i64, _vp, _vp, _vp, _vp],
+    "lr_orth_fast": [_vp, _int, _i64, _i64, _vp, _i64, _vp, _i64, C.c_double, _vp],
+    "lr_small_svd_fast": [_vp, _int, _i64, _i64, _vp, _vp, _vp, _vp, _vp],
     "lr_jacobi_svd": [_vp, _int, _i64, _vp, _vp, _vp, _vp, _vp],
     "lr_estimate_tail": [_vp, _int, _i64, _i64, _i64, _vp, _i64, _vp, _i64, C.c_double, _vp],
     "lr_srft": [_vp, _int, _i64, _i64, _i64, _vp, _i64, _vp, _vp, C.c_double, _vp, _i64],
@@ -61,6 +63,7 @@ _SIGS = {
     "lr_copy": [_vp, _int, _vp, _i64, _int, _vp, _i64, _i64, _i64, _int],
     "lr_sign_fix": [_vp, _int, _i64, _i64, _i64, _vp, _i64, _vp, _i64],
     "lr_max_abs_imag": [_vp, _int, _i64, _i64, _vp, _i64, _vp],
+    "lr_gaussian": [_vp, C.c_uint64, C.c_uint64, _i64, _int, _vp, _vp],
     "lr_axpy_sub": [_vp, _int, _i64, _i64, _vp, _i64, _vp, _i64],
     "lr_col_sumsq": [_vp, _int, _i64, _i64, _vp, _i64, _vp],
     "lr_scale_col": [_vp, _int, _i64, _vp, _i64, C.c_double, _vp, _i64],
@@ -122,8 +125,19 @@ def check(status):
     raise RuntimeError(f"liblowrank_b200: {msg} (status {status})")
 
 
+HOST_PROFILE = {} if os.environ.get("LR_PROFILE_HOST") else None
+
+
 def call(name, *args):
+    if HOST_PROFILE is None:
+        check(getattr(load(), name)(*args))
+        return
+    import time
+    t0 = time.perf_counter()
     check(getattr(load(), name)(*args))
+    dt = time.perf_counter() - t0
+    c, s = HOST_PROFILE.get(name, (0, 0.0))
+    HOST_PROFILE[name] = (c + 1, s + dt)
 
 
 # ---------------------------------------------------------------------------

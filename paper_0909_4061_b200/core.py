@@ -18,7 +18,9 @@ to float64 / complex128 like the reference.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -318,6 +320,27 @@ def gemm_dev(A, X, Y):
     return gemm(A, X, Y, adjoint=False)
 
 
+class _Spec(threading.local):
+    status = None
+
+
+_SPEC = _Spec()
+
+
+@contextlib.contextmanager
+def speculate(status):
+    """Run orthonormalizations / small SVDs through the host-sync-free
+    speculative kernels, OR-ing their flags into the device int32 `status`
+    (see lr_orth_fast).  The caller checks status once at the end and
+    re-runs on the synchronous path if any flag is set."""
+    prev = _SPEC.status
+    _SPEC.status = status
+    try:
+        yield status
+    finally:
+        _SPEC.status = prev
+
+
 def small_svd_from_adjoint(Z):
     """SVD of B = Z^H given Z (c x r, r <= c) -- the layout the adjoint pass
     of direct_svd produces.  Z is consumed (overwritten)."""
@@ -329,8 +352,13 @@ def small_svd_from_adjoint(Z):
     U = torch.empty((r, r), dtype=Z.dtype, device=Z.device)
     S = torch.empty(r, dtype=torch.float64, device=Z.device)
     V = torch.empty((c, r), dtype=Z.dtype, device=Z.device)
-    _lib.call("lr_small_svd", _lib.handle(Z.device.index), code, r, c, _lib.ptr(Z), _lib.ptr(U),
-              _lib.ptr(S), _lib.ptr(V))
+    h = _lib.handle(Z.device.index)
+    if _SPEC.status is not None:
+        _lib.call("lr_small_svd_fast", h, code, r, c, _lib.ptr(Z), _lib.ptr(U), _lib.ptr(S),
+                  _lib.ptr(V), _lib.ptr(_SPEC.status))
+    else:
+        _lib.call("lr_small_svd", h, code, r, c, _lib.ptr(Z), _lib.ptr(U), _lib.ptr(S),
+                  _lib.ptr(V))
     return U, S, V
 
 
@@ -341,6 +369,11 @@ def orth_dev(Y, tol=config.GS_DROP_TOL):
     if ell == 0 or m == 0:
         return torch.zeros((m, 0), dtype=Y.dtype, device=Y.device)
     Q = torch.empty((m, ell), dtype=Y.dtype, device=Y.device)
+    if _SPEC.status is not None:
+        _lib.call("lr_orth_fast", _lib.handle(Y.device.index), _lib.dtype_code(Y.dtype), m, ell,
+                  _lib.ptr(Y), _lib.ld(Y), _lib.ptr(Q), _lib.ld(Q), float(tol),
+                  _lib.ptr(_SPEC.status))
+        return Q
     rank = C.c_int64(0)
     _lib.call("lr_orth", _lib.handle(Y.device.index), _lib.dtype_code(Y.dtype), m, ell,
               _lib.ptr(Y), _lib.ld(Y), _lib.ptr(Q), _lib.ld(Q), float(tol), C.byref(rank))

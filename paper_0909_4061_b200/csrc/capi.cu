@@ -199,16 +199,97 @@ bool scholqr3(Handle* h, int dtype, int64_t m, int64_t ell, const void* Y, int64
   return true;
 }
 
+// Speculative CholeskyQR2 with no host synchronization: the drop rule and
+// pivot resolvability are evaluated on the device and reported through
+// h->status (bit 1 unresolved pivot, 2 column dropped, 4 non-finite).  When
+// no bit is set the result equals the synchronous path's.
+void orth_fast_impl(Handle* h, int dtype, int64_t m, int64_t ell, const void* Y, int64_t ldy,
+                    void* Q, int64_t ldq, double tol) {
+  const size_t ws = wide_size(dtype), es = elem_size(dtype);
+  void* G = pool_alloc(h, size_t(ell) * ell * ws);
+  void* P = pool_alloc(h, size_t(ell) * ell * ws);
+  void* R = pool_alloc(h, size_t(ell) * ell * ws);
+  void* Q1 = pool_alloc(h, size_t(m) * ell * es);
+  const double unres = 4.0 * double(ell) * U64;
+  gram_any(h, dtype, m, ell, Y, ldy, G);
+  chol_any(h, dtype, ell, G, tol, unres, 0.0, P, R, h->d_info);
+  apply_right(h, dtype, m, ell, ell, Y, ldy, P, ell, Q1, ell);
+  gram_any(h, dtype, m, ell, Q1, ell, G);
+  chol_any(h, dtype, ell, G, tol, unres, 0.0, P, R, h->d_info);
+  apply_right(h, dtype, m, ell, ell, Q1, ell, P, ell, Q, ldq);
+}
+
+// Speculative small SVD (CholeskyQR2 of Bh + Jacobi), no host sync; flags
+// as orth_fast_impl plus 8 = Jacobi sweep limit.
+void small_svd_fast_impl(Handle* h, int dtype, int64_t r, int64_t c, const void* Bh, void* U,
+                         double* S, void* V) {
+  const int wd = wide_of(dtype);
+  const size_t ws = wide_size(dtype), es = elem_size(dtype);
+  void* G = pool_alloc(h, size_t(r) * r * ws);
+  void* P = pool_alloc(h, size_t(r) * r * ws);
+  void* R1 = pool_alloc(h, size_t(r) * r * ws);
+  void* R2 = pool_alloc(h, size_t(r) * r * ws);
+  void* R = pool_alloc(h, size_t(r) * r * ws);
+  void* Wr = pool_alloc(h, size_t(r) * r * ws);
+  void* J = pool_alloc(h, size_t(r) * r * ws);
+  void* Q1 = pool_alloc(h, size_t(c) * r * es);
+  void* Q2 = pool_alloc(h, size_t(c) * r * es);
+  const double unres = 4.0 * double(r) * U64;
+  gram_any(h, dtype, c, r, Bh, r, G);
+  chol_any(h, dtype, r, G, 0.0, unres, 0.0, P, R1, h->d_info);
+  apply_right(h, dtype, c, r, r, Bh, r, P, r, Q1, r);
+  gram_any(h, dtype, c, r, Q1, r, G);
+  chol_any(h, dtype, r, G, 0.0, unres, 0.0, P, R2, h->d_info);
+  apply_right(h, dtype, c, r, r, Q1, r, P, r, Q2, r);
+  trmm_upper(h, wd, r, R2, R1, R);
+  if (is_complex(dtype))
+    jacobi_svd_c128(h, r, r, static_cast<double2*>(R), static_cast<double2*>(Wr), S,
+                    static_cast<double2*>(J), h->d_info);
+  else
+    jacobi_svd_f64(h, r, r, static_cast<double*>(R), static_cast<double*>(Wr), S,
+                   static_cast<double*>(J), h->d_info);
+  cast_copy(h, wd, J, r, dtype, U, r, r, r, false);
+  apply_right(h, dtype, c, r, r, Q2, r, Wr, r, V, r);
+}
+
+int32_t read_status(Handle* h, int32_t* d) {
+  int32_t v = 0;
+  LR_CUDA(cudaMemcpyAsync(h->h_info, d, sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
+  LR_CUDA(cudaStreamSynchronize(h->stream));
+  v = h->h_info[0];
+  return v;
+}
+
 int64_t orth_impl(Handle* h, int dtype, int64_t m, int64_t ell, const void* Y, int64_t ldy,
                   void* Q, int64_t ldq, double tol) {
   const size_t ws = wide_size(dtype), es = elem_size(dtype);
+  const bool alias = (Q == Y);
+  {
+    // one synchronization: speculative CholeskyQR2, then check its flags
+    int32_t* st = h->d_info + 32;
+    LR_CUDA(cudaMemsetAsync(st, 0, sizeof(int32_t), h->stream));
+    int32_t* saved = h->status;
+    h->status = st;
+    void* dst = alias ? pool_alloc(h, size_t(m) * ell * es) : Q;
+    const int64_t ldd = alias ? ell : ldq;
+    orth_fast_impl(h, dtype, m, ell, Y, ldy, dst, ldd, tol);
+    h->status = saved;
+    const int32_t flags = read_status(h, st);
+    LR_REQUIRE((flags & 4) == 0, LR_EINVAL,
+               "orthonormalize: non-finite entries in the sample matrix");
+    if (flags == 0) {
+      if (alias)
+        LR_CUDA(cudaMemcpy2DAsync(Q, ldq * es, dst, ldd * es, ell * es, m,
+                                  cudaMemcpyDeviceToDevice, h->stream));
+      return ell;
+    }
+  }
   void* G = pool_alloc(h, size_t(ell) * ell * ws);
   void* P = pool_alloc(h, size_t(ell) * ell * ws);
   void* R = pool_alloc(h, size_t(ell) * ell * ws);
   void* Q1 = pool_alloc(h, size_t(m) * ell * es);
   int32_t* dinfo = h->d_info;
 
-  const bool alias = (Q == Y);
   // fast path: CholeskyQR2 with the drop rule applied in pass 1
   Info a = cholqr_pass(h, dtype, m, ell, Y, ldy, tol, 0.0, Q1, ell, R, G, P, dinfo, true);
   LR_REQUIRE(a.bad == 0, LR_EINVAL, "orthonormalize: non-finite entries in the sample matrix");
@@ -259,6 +340,17 @@ void small_svd_impl(Handle* h, int dtype, int64_t r, int64_t c, void* Bh, void* 
                     void* V) {
   const int wd = wide_of(dtype);
   const size_t ws = wide_size(dtype), es = elem_size(dtype);
+  {
+    int32_t* st = h->d_info + 32;
+    LR_CUDA(cudaMemsetAsync(st, 0, sizeof(int32_t), h->stream));
+    int32_t* saved = h->status;
+    h->status = st;
+    small_svd_fast_impl(h, dtype, r, c, Bh, U, S, V);
+    h->status = saved;
+    const int32_t flags = read_status(h, st);
+    LR_REQUIRE((flags & 4) == 0, LR_EINVAL, "small_svd: non-finite entries");
+    if (flags == 0) return;
+  }
   void* G = pool_alloc(h, size_t(r) * r * ws);
   void* P = pool_alloc(h, size_t(r) * r * ws);
   void* R1 = pool_alloc(h, size_t(r) * r * ws);
@@ -513,6 +605,46 @@ int lr_orth(lr_handle_t hh, int dtype, int64_t m, int64_t ell, const void* Y, in
   API_END
 }
 
+int lr_orth_fast(lr_handle_t hh, int dtype, int64_t m, int64_t ell, const void* Y, int64_t ldy,
+                 void* Q, int64_t ldq, double tol, int32_t* status) {
+  API_BEGIN
+  Handle* h = H(hh);
+  check_dtype(dtype);
+  LR_REQUIRE(m >= 1 && ell >= 1 && ldy >= ell && ldq >= ell && status, LR_EINVAL,
+             "lr_orth_fast: bad arguments");
+  LR_REQUIRE(Q != Y, LR_EINVAL, "lr_orth_fast: Q must not alias Y");
+  lr::pool_reset(h);
+  int32_t* saved = h->status;
+  h->status = status;
+  try {
+    lr::orth_fast_impl(h, dtype, m, ell, Y, ldy, Q, ldq, tol);
+  } catch (...) {
+    h->status = saved;
+    throw;
+  }
+  h->status = saved;
+  API_END
+}
+
+int lr_small_svd_fast(lr_handle_t hh, int dtype, int64_t ell, int64_t ncols, const void* Bh,
+                      void* U, double* S, void* V, int32_t* status) {
+  API_BEGIN
+  Handle* h = H(hh);
+  check_dtype(dtype);
+  LR_REQUIRE(ell >= 1 && ncols >= ell && status, LR_EINVAL, "lr_small_svd_fast: bad arguments");
+  lr::pool_reset(h);
+  int32_t* saved = h->status;
+  h->status = status;
+  try {
+    lr::small_svd_fast_impl(h, dtype, ell, ncols, Bh, U, S, V);
+  } catch (...) {
+    h->status = saved;
+    throw;
+  }
+  h->status = saved;
+  API_END
+}
+
 int lr_small_svd(lr_handle_t hh, int dtype, int64_t ell, int64_t ncols, void* Bh, void* U,
                  double* S, void* V) {
   API_BEGIN
@@ -640,6 +772,25 @@ int lr_max_abs_imag(lr_handle_t hh, int dtype, int64_t m, int64_t n, const void*
   Handle* h = H(hh);
   lr::pool_reset(h);
   lr::max_abs_imag(h, dtype, m, n, Y, ldy, out);
+  API_END
+}
+
+int lr_gaussian(lr_handle_t hh, uint64_t key_lo, uint64_t key_hi, int64_t count, int dtype,
+                void* out, int32_t* status) {
+  API_BEGIN
+  Handle* h = H(hh);
+  LR_REQUIRE(dtype == LR_F32 || dtype == LR_F64, LR_EINVAL, "lr_gaussian: f32 or f64 output");
+  LR_REQUIRE(count >= 0, LR_EINVAL, "lr_gaussian: negative count");
+  lr::pool_reset(h);
+  int32_t* saved = h->status;
+  h->status = status;
+  try {
+    lr::gaussian_stream(h, key_lo, key_hi, count, dtype, out);
+  } catch (...) {
+    h->status = saved;
+    throw;
+  }
+  h->status = saved;
   API_END
 }
 

@@ -9,9 +9,20 @@
 // projection (its row of R is skipped), exactly like the reference skipping
 // it in the basis.  ||Y||_F^2 = trace(G).
 //
-// Outputs: P (ell x ell): Q = Y . P[:, :rank] has orthonormal columns,
-// P[kept_i][c] = (R_SS^{-1})[i][c];  R (ell x ell) the factor restricted to
-// kept rows/cols; info = {rank, unresolved pivots, bad pivots}.
+// The kernel is latency-bound (one SM, ell^3/3 flops), so it is written for
+// short critical paths: one n x n row-major buffer in shared memory (LDS/STS
+// via a template specialisation; global scratch only for very large ell),
+// 32 warps, ONE barrier per column.  Every thread reads the pivot itself and
+// forms 1/sqrt(d) with rsqrt (no divides on the critical path); the trailing
+// update uses the unscaled pivot row times 1/d and the scaling of row j is
+// deferred to step j+1.  The inverse X = R~^{-1} (R~ = R with dropped
+// rows/cols replaced by the identity) is formed right-looking into the lower
+// triangle (X^T), again one barrier per row, then scattered into P with the
+// kept columns compacted.
+//
+// Outputs: P (ell x ell): Q = Y . P[:, :rank] has orthonormal columns;
+// R (ell x ell) the factor restricted to kept rows/cols;
+// info = {rank, unresolved pivots, bad (non-finite) pivots}.
 #include "common.cuh"
 #include "scalar.cuh"
 
@@ -19,196 +30,198 @@ namespace lr {
 namespace {
 
 constexpr int CHOL_THREADS = 1024;
+constexpr int NW = CHOL_THREADS / 32;
 
-__device__ __forceinline__ int up_idx(int i, int j, int n) {
-  // packed upper triangle, row-major: row i holds columns i..n-1
-  return i * n - (i * (i - 1)) / 2 + (j - i);
-}
+// 1/sqrt(d) to full double precision (MUFU seed + two Newton steps)
+__device__ __forceinline__ double rsqrt_full(double d) { return rsqrt(d); }
 
-template <typename T>
-__device__ __forceinline__ bool finite_sc(T v);
-template <>
-__device__ __forceinline__ bool finite_sc<double>(double v) { return isfinite(v); }
-template <>
-__device__ __forceinline__ bool finite_sc<double2>(double2 v) {
-  return isfinite(v.x) && isfinite(v.y);
-}
-
-template <typename T>
+template <typename T, bool SMEM>
 __global__ void __launch_bounds__(CHOL_THREADS, 1)
 chol_drop_kernel(int n, const T* __restrict__ G, double drop_tol, double unres_rel,
                  double shift_coef, T* __restrict__ P, T* __restrict__ Rout,
-                 int32_t* __restrict__ info, T* gW, bool w_in_smem) {
+                 int32_t* __restrict__ info, T* gW, int32_t* status) {
   using S = Sc<T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int np = n * (n + 1) / 2;
-  T* W;
-  T* X;
+  T* __restrict__ W;
   unsigned char* tail;
-  if (w_in_smem) {
+  if constexpr (SMEM) {
     W = reinterpret_cast<T*>(smem_raw);
-    X = W + np;
-    tail = reinterpret_cast<unsigned char*>(X + np);
+    tail = reinterpret_cast<unsigned char*>(W + size_t(n) * n);
   } else {
     W = gW;
-    X = gW + np;
     tail = smem_raw;
   }
-  double* d0 = reinterpret_cast<double*>(tail);         // original pivots (shifted)
-  int* pos = reinterpret_cast<int*>(d0 + n);            // compact index or -1
+  double* d0 = reinterpret_cast<double*>(tail);         // original (shifted) pivots
+  double* rd = d0 + n;                                  // R diagonal (0 = dropped)
+  double* ri = rd + n;                                  // 1 / R diagonal
+  int* pos = reinterpret_cast<int*>(ri + n);            // compact index or -1
   int* kidx = pos + n;                                  // compact -> original
 
-  __shared__ double s_red[32];
-  __shared__ double s_thr2, s_shift, s_rjj;
-  __shared__ int s_keep, s_unres, s_bad, s_rank;
+  __shared__ double s_red[NW];
+  __shared__ int s_unres, s_bad, s_rank;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nwarps = blockDim.x >> 5;
 
-  // 1. load upper triangle, trace
+  // 1. load the upper triangle, trace
   double tr = 0.0;
-  for (int i = warp; i < n; i += nwarps) {
+  for (int i = warp; i < n; i += NW) {
     for (int j = i + lane; j < n; j += 32) {
-      T g = G[int64_t(i) * n + j];
-      W[up_idx(i, j, n)] = g;
+      const T g = G[size_t(i) * n + j];
+      W[i * n + j] = g;
       if (j == i) tr += S::re(g);
     }
   }
   for (int m = 16; m > 0; m >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, m);
   if (lane == 0) s_red[warp] = tr;
+  if (tid == 0) { s_unres = 0; s_bad = 0; }
   __syncthreads();
-  if (tid == 0) {
-    double t = 0.0;
-    for (int w = 0; w < nwarps; ++w) t += s_red[w];
-    s_thr2 = drop_tol * drop_tol * t;
-    s_shift = shift_coef * t;
-    s_unres = 0;
-    s_bad = 0;
-  }
-  __syncthreads();
-  for (int i = tid; i < n; i += blockDim.x) {
-    T w = W[up_idx(i, i, n)];
-    double d = S::re(w) + s_shift;
-    W[up_idx(i, i, n)] = S::make(d, 0.0);
+  double trace = 0.0;
+#pragma unroll
+  for (int w = 0; w < NW; ++w) trace += s_red[w];
+  const double thr2 = drop_tol * drop_tol * trace;
+  const double shift = shift_coef * trace;
+  for (int i = tid; i < n; i += CHOL_THREADS) {
+    const double d = S::re(W[i * n + i]) + shift;
+    W[i * n + i] = S::make(d, 0.0);
     d0[i] = d;
   }
   __syncthreads();
 
-  // 2. right-looking factorization with deletion
-  for (int j = 0; j < n; ++j) {
-    if (tid == 0) {
-      const double d = S::re(W[up_idx(j, j, n)]);
-      int keep = 0;
-      double r = 0.0;
-      if (!isfinite(d)) {
-        s_bad += 1;
-      } else if (d > s_thr2 && d > 0.0) {
-        keep = 1;
-        r = sqrt(d);
+  // 2. right-looking factorization, one barrier per column
+  for (int j = 0; j <= n; ++j) {
+    if (j > 0) {   // deferred scaling of row j-1
+      const int p = j - 1;
+      const double inv = ri[p];
+      T* rowp = W + p * n;
+      for (int c = p + 1 + tid; c < n; c += CHOL_THREADS) rowp[c] = S::scale(rowp[c], inv);
+    }
+    if (j == n) break;
+    const double d = S::re(W[j * n + j]);
+    const bool fin = isfinite(d);
+    const bool keep = fin && d > thr2 && d > 0.0;
+    if (keep) {
+      const double iv = rsqrt_full(d);       // 1 / r_jj
+      const double invd = iv * iv;           // 1 / d
+      if (tid == 0) {
+        rd[j] = d * iv;
+        ri[j] = iv;
         if (d <= unres_rel * d0[j]) s_unres += 1;
       }
-      s_keep = keep;
-      s_rjj = r;
-    }
-    __syncthreads();
-    const int keep = s_keep;
-    const double rjj = s_rjj;
-    if (keep) {
-      const double inv = 1.0 / rjj;
-      for (int i = j + 1 + tid; i < n; i += blockDim.x)
-        W[up_idx(j, i, n)] = S::scale(W[up_idx(j, i, n)], inv);
-      if (tid == 0) W[up_idx(j, j, n)] = S::make(rjj, 0.0);
-    } else {
-      for (int i = j + tid; i < n; i += blockDim.x) W[up_idx(j, i, n)] = S::zero();
-    }
-    __syncthreads();
-    if (keep) {
-      for (int a = j + 1 + warp; a < n; a += nwarps) {
-        const T rja = S::conj(W[up_idx(j, a, n)]);
-        for (int b = a + lane; b < n; b += 32) {
-          const int ib = up_idx(a, b, n);
-          W[ib] = S::sub(W[ib], S::mul(rja, W[up_idx(j, b, n)]));
-        }
+      const T* rowj = W + j * n;
+      for (int a = j + 1 + warp; a < n; a += NW) {
+        const T f = S::scale(S::conj(rowj[a]), invd);
+        T* rowa = W + a * n;
+        for (int b = a + lane; b < n; b += 32) rowa[b] = S::sub(rowa[b], S::mul(f, rowj[b]));
       }
+    } else if (tid == 0) {
+      if (!fin) s_bad += 1;
+      rd[j] = 0.0;
+      ri[j] = 0.0;   // deferred scaling zeroes the row
     }
     __syncthreads();
   }
 
-  // 3. compaction of kept columns
-  if (tid == 0) {
-    int r = 0;
-    for (int j = 0; j < n; ++j) {
-      const bool k = S::re(W[up_idx(j, j, n)]) > 0.0;
-      pos[j] = k ? r : -1;
-      if (k) kidx[r++] = j;
+  // 3. compaction; zero R entries in rows/columns of dropped pivots
+  if (warp == 0) {
+    int base = 0;
+    for (int j0 = 0; j0 < n; j0 += 32) {
+      const int j = j0 + lane;
+      const bool k = j < n && rd[j] > 0.0;
+      const unsigned bal = __ballot_sync(0xffffffffu, k);
+      const int pj = base + __popc(bal & ((1u << lane) - 1u));
+      if (j < n) pos[j] = k ? pj : -1;
+      if (k) kidx[pj] = j;
+      base += __popc(bal);
     }
-    s_rank = r;
+    if (lane == 0) s_rank = base;
   }
   __syncthreads();
   const int rank = s_rank;
-
-  // 4. X = R_SS^{-1} (upper, rank x rank, packed with dimension rank)
-  for (int c = warp; c < rank; c += nwarps) {
-    const int oc = kidx[c];
-    const double rcc = S::re(W[up_idx(oc, oc, n)]);
-    if (lane == 0) X[up_idx(c, c, rank)] = S::make(1.0 / rcc, 0.0);
-    __syncwarp();
-    for (int i = c - 1; i >= 0; --i) {
-      const int oi = kidx[i];
-      T acc = S::zero();
-      for (int k = i + 1 + lane; k <= c; k += 32)
-        acc = S::add(acc, S::mul(W[up_idx(oi, kidx[k], n)], X[up_idx(k, c, rank)]));
-      acc = warp_sum(acc);
-      if (lane == 0) {
-        const double rii = S::re(W[up_idx(oi, oi, n)]);
-        X[up_idx(i, c, rank)] = S::scale(acc, -1.0 / rii);
-      }
-      __syncwarp();
+  if (rank < n) {
+    for (int e = tid; e < n * n; e += CHOL_THREADS) {
+      const int i = e / n, c = e - (e / n) * n;
+      if (c > i && (pos[i] < 0 || pos[c] < 0)) W[e] = S::zero();
     }
+  }
+  // X initialised to the identity in the lower triangle (X[i][c] at W[c][i])
+  for (int e = tid; e < n * n; e += CHOL_THREADS) {
+    const int c = e / n, i = e - (e / n) * n;
+    if (i <= c) W[e] = (i == c) ? S::one() : S::zero();
   }
   __syncthreads();
 
+  // 4. X = R~^{-1}, right-looking from the last row, one barrier per row
+  for (int k = n - 1; k >= -1; --k) {
+    if (k + 1 < n) {   // deferred scaling of row k+1 of X
+      const int p = k + 1;
+      const double inv = ri[p];
+      if (inv != 0.0)
+        for (int c = p + tid; c < n; c += CHOL_THREADS) W[c * n + p] = S::scale(W[c * n + p], inv);
+    }
+    if (k < 0) break;
+    const double inv = ri[k];
+    if (inv != 0.0) {
+      // X[i][c] -= R[i][k] * X[k][c] / r_kk   for i < k <= c
+      for (int c = k + warp; c < n; c += NW) {
+        T* xc = W + c * n;
+        const T xk = S::scale(xc[k], inv);
+        for (int i = lane; i < k; i += 32) xc[i] = S::sub(xc[i], S::mul(W[i * n + k], xk));
+      }
+    }
+    __syncthreads();
+  }
+
   // 5. outputs
-  for (int e = tid; e < n * n; e += blockDim.x) {
-    const int i = e / n, j = e % n;
-    // P: row i (original column of Y), column j (compact basis index)
-    T p = S::zero();
-    const int pi = pos[i];
-    if (pi >= 0 && j < rank && pi <= j) p = X[up_idx(pi, j, rank)];
-    P[e] = p;
+  for (int e = tid; e < n * n; e += CHOL_THREADS) {
+    const int i = e / n, j = e - (e / n) * n;
     T r = S::zero();
-    if (j >= i && pos[i] >= 0 && pos[j] >= 0) r = W[up_idx(i, j, n)];
+    if (pos[i] >= 0 && pos[j] >= 0) {
+      if (j > i) r = W[e];
+      else if (j == i) r = S::make(rd[i], 0.0);
+    }
     Rout[e] = r;
+    // P[i][c'] = X[i][c] with c' = pos[c] (gathered by destination)
+    T pv = S::zero();
+    if (pos[i] >= 0 && j < rank) {
+      const int c = kidx[j];
+      if (i <= c) pv = W[c * n + i];
+    }
+    P[e] = pv;
   }
   if (tid == 0) {
     info[0] = rank;
     info[1] = s_unres;
     info[2] = s_bad;
+    if (status) {
+      // speculative-path flags: 1 unresolved pivot, 2 column dropped, 4 non-finite
+      const int bits = (s_unres ? 1 : 0) | (rank < n ? 2 : 0) | (s_bad ? 4 : 0);
+      if (bits) atomicOr(status, bits);
+    }
   }
 }
 
 template <typename T>
 void launch_chol(Handle* h, int64_t ell, const T* G, double drop_tol, double unres_rel,
                  double shift_coef, T* P, T* R, int32_t* info) {
-  LR_REQUIRE(ell >= 1 && ell <= 2048, LR_EINVAL, "chol_drop: ell out of range [1, 2048]");
+  LR_REQUIRE(ell >= 1 && ell <= 4096, LR_EINVAL, "chol_drop: ell out of range [1, 4096]");
   const int n = int(ell);
-  const size_t np = size_t(n) * (n + 1) / 2;
-  const size_t tail = size_t(n) * (sizeof(double) + 2 * sizeof(int));
-  const size_t full = 2 * np * sizeof(T) + tail;
+  const size_t tail = size_t(n) * (3 * sizeof(double) + 2 * sizeof(int));
+  const size_t full = size_t(n) * n * sizeof(T) + tail;
   int max_smem = 0;
   LR_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
-  const size_t limit = size_t(max_smem) - 4096;   // static shared + slack
-  bool in_smem = full <= limit;
-  T* gW = nullptr;
-  size_t dyn = full;
-  if (!in_smem) {
-    gW = pool_alloc_t<T>(h, 2 * np);
-    dyn = tail;
+  const bool in_smem = full <= size_t(max_smem) - 1024;
+  if (in_smem) {
+    auto kern = chol_drop_kernel<T, true>;
+    LR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(full)));
+    kern<<<1, CHOL_THREADS, full, h->stream>>>(n, G, drop_tol, unres_rel, shift_coef, P, R,
+                                               info, nullptr, h->status);
+  } else {
+    T* gW = pool_alloc_t<T>(h, size_t(n) * n);
+    auto kern = chol_drop_kernel<T, false>;
+    LR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(tail)));
+    kern<<<1, CHOL_THREADS, tail, h->stream>>>(n, G, drop_tol, unres_rel, shift_coef, P, R,
+                                               info, gW, h->status);
   }
-  auto kern = chol_drop_kernel<T>;
-  LR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dyn)));
-  kern<<<1, CHOL_THREADS, dyn, h->stream>>>(n, G, drop_tol, unres_rel, shift_coef, P, R, info,
-                                            gW, in_smem);
   LR_CHECK_LAUNCH();
 }
 

@@ -68,6 +68,7 @@ struct Handle {
   int sm_count = 148;
   int f32_mode = LR_F32_SPLIT3;
   Pool pool;
+  int32_t* status = nullptr;   // speculative-path flags (device, set per call)
   int32_t* d_info = nullptr;   // small device scratch for composite decisions
   int32_t* h_info = nullptr;   // pinned mirror
   double* d_dscratch = nullptr;
@@ -162,6 +163,11 @@ void srft_c64(Handle* h, int64_t m, int64_t n, int64_t ell, const float2* A, int
 void srft_c128(Handle* h, int64_t m, int64_t n, int64_t ell, const double2* A, int64_t lda,
                const double2* d, const int32_t* picks, double scale, double2* Y, int64_t ldy);
 void dft_rows(Handle* h, int dtype, int64_t rows, int64_t n, void* X, int64_t ldx);
+
+// gauss.cu ----------------------------------------------------------------------
+// first `count` draws of numpy Generator(Philox(key)).standard_normal
+void gaussian_stream(Handle* h, uint64_t key_lo, uint64_t key_hi, int64_t count, int out_dtype,
+                     void* out);
 
 // spmm.cu -----------------------------------------------------------------------
 void csr_spmm_f64(Handle* h, int64_t m, int64_t ell, const int64_t* rowptr,

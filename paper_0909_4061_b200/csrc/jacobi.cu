@@ -1,4 +1,4 @@
-// K4: one-sided (Hestenes) Jacobi SVD of a small square matrix, one CTA.
+// K4: one-sided (Hestenes) Jacobi SVD of a small matrix, one CTA.
 //
 // Used by the small SVD of direct_svd (reference core.py:199-230,
 // factor.py:163-165): B^H = Q2 R2 (CholeskyQR), then R2 = W diag(S) J^H by
@@ -6,7 +6,13 @@
 // Then B = J diag(S) (Q2 W)^H, i.e. U_B = J and V_B = Q2 W.  One-sided Jacobi
 // is used instead of bidiagonalization because it is accurate in a relative
 // sense for the graded triangular factors CholeskyQR produces and maps onto
-// warp-parallel column pairs (round-robin ordering, n/2 pairs per round).
+// parallel column pairs (round-robin ordering, n/2 pairs per round).
+//
+// Parallel layout: each pair of a round is owned by a group of GS lanes
+// (GS = 8..32, chosen so all n/2 pairs of a round run at once); the three
+// dot products are reduced with xor-shuffles inside the group; one barrier
+// per round.  Columns are stored contiguously (column-major working copies)
+// so a group's loads are conflict-free.
 //
 // Outputs follow the reference conventions: S descending, and the first
 // entry of each J column with |j| > 1e-10 max|j| made real positive (the W
@@ -20,16 +26,22 @@ namespace {
 constexpr int JAC_THREADS = 1024;
 
 template <typename T>
+__device__ __forceinline__ T group_sum(T v, int gs) {
+  for (int m = gs >> 1; m > 0; m >>= 1) v = Sc<T>::add(v, Sc<T>::shfl_xor(v, m));
+  return v;
+}
+
+template <typename T, bool SMEM>
 __global__ void __launch_bounds__(JAC_THREADS, 1)
 jacobi_kernel(int rows, int n, const T* __restrict__ M, T* __restrict__ Wout,
               double* __restrict__ Sout, T* __restrict__ Jout, int32_t* __restrict__ info, T* gbuf,
-              bool in_smem, double tol, int max_sweeps) {
+              double tol, int max_sweeps, int gs, int32_t* status) {
   using S = Sc<T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* Mc;
-  T* Jc;
+  T* __restrict__ Mc;
+  T* __restrict__ Jc;
   unsigned char* tail;
-  if (in_smem) {
+  if constexpr (SMEM) {
     Mc = reinterpret_cast<T*>(smem_raw);
     Jc = Mc + size_t(rows) * n;
     tail = reinterpret_cast<unsigned char*>(Jc + size_t(n) * n);
@@ -38,12 +50,19 @@ jacobi_kernel(int rows, int n, const T* __restrict__ M, T* __restrict__ Wout,
     Jc = gbuf + size_t(rows) * n;
     tail = smem_raw;
   }
-  double* sig = reinterpret_cast<double*>(tail);
-  int* order = reinterpret_cast<int*>(sig + n);   // order[o] = source column
+  const int np2 = n + (n & 1);
+  const int pairs = np2 / 2;
+  T* pgm = reinterpret_cast<T*>(tail);                // pairs: m_p^H m_q, then s e
+  double* sig = reinterpret_cast<double*>(pgm + pairs);  // n
+  double* pa = sig + n;                               // pairs: ||m_p||^2
+  double* pb = pa + pairs;                            // pairs: ||m_q||^2
+  double* pc = pb + pairs;                            // pairs: c (0 = no rotation)
+  int* order = reinterpret_cast<int*>(pc + pairs);    // n: order[o] = source column
 
-  __shared__ int s_rot;
+  __shared__ int s_rot[2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nwarps = blockDim.x >> 5;
+  const int glane = tid % gs, group = tid / gs, ngroups = blockDim.x / gs;
 
   // column-major working copies
   for (int64_t e = tid; e < int64_t(rows) * n; e += blockDim.x) {
@@ -54,62 +73,100 @@ jacobi_kernel(int rows, int n, const T* __restrict__ M, T* __restrict__ Wout,
     const int i = e / n, j = e % n;
     Jc[size_t(j) * n + i] = (i == j) ? S::one() : S::zero();
   }
+  if (tid == 0) { s_rot[0] = 0; s_rot[1] = 0; }
   __syncthreads();
 
-  const int np2 = n + (n & 1);
-  const int rounds = np2 - 1, pairs = np2 / 2;
+  const int rounds = np2 - 1;
+  const int iters = (pairs + ngroups - 1) / ngroups;
   int sweep = 0;
   bool converged = (n == 1);
   for (; sweep < max_sweeps && !converged; ++sweep) {
-    if (tid == 0) s_rot = 0;
-    __syncthreads();
+    const int flag = sweep & 1;   // double-buffered "rotated" flag
     for (int r = 0; r < rounds; ++r) {
-      for (int k = warp; k < pairs; k += nwarps) {
+      // phase 1: the three inner products of every pair (one group per pair)
+      for (int it = 0; it < iters; ++it) {
+        const int k = group + it * ngroups;
+        int p = -1, q = -1;
+        if (k < pairs) {
+          const int ia = k, ib = np2 - 1 - k;
+          p = (ia == 0) ? 0 : 1 + (ia - 1 + r) % rounds;
+          q = (ib == 0) ? 0 : 1 + (ib - 1 + r) % rounds;
+          if (p > q) { const int t = p; p = q; q = t; }
+          if (q >= n) p = q = -1;
+        }
+        double a = 0.0, b = 0.0;
+        T gmm = S::zero();
+        if (p >= 0) {
+          const T* mp = Mc + size_t(p) * rows;
+          const T* mq = Mc + size_t(q) * rows;
+          for (int i = glane; i < rows; i += gs) {
+            const T x = mp[i], y = mq[i];
+            a += S::abs2(x);
+            b += S::abs2(y);
+            gmm = S::add(gmm, S::cmul(x, y));
+          }
+        }
+        a = group_sum(a, gs);
+        b = group_sum(b, gs);
+        gmm = group_sum(gmm, gs);
+        if (k < pairs && glane == 0) {
+          pa[k] = (p >= 0) ? a : -1.0;
+          pb[k] = b;
+          pgm[k] = gmm;
+        }
+      }
+      __syncthreads();
+      // phase 2: rotation parameters, one pair per lane of the first warps
+      for (int k = tid; k < pairs; k += blockDim.x) {
+        const double a = pa[k], b = pb[k];
+        const T gmm = pgm[k];
+        const double g2 = S::abs2(gmm);
+        double c = 0.0;
+        T se = S::zero();
+        if (a >= 0.0 && g2 > 0.0 && g2 > tol * tol * a * b) {
+          const double iag = rsqrt(g2);                 // 1 / |gamma|
+          const double zeta = 0.5 * (b - a) * iag;
+          const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          c = rsqrt(1.0 + t * t);
+          se = S::scale(gmm, c * t * iag);              // s * phase(gamma)
+          s_rot[flag] = 1;
+        }
+        pc[k] = c;
+        pgm[k] = se;
+      }
+      __syncthreads();
+      // phase 3: apply the rotations to the columns of M and J
+      for (int it = 0; it < iters; ++it) {
+        const int k = group + it * ngroups;
+        if (k >= pairs) continue;
+        const double c = pc[k];
+        if (c == 0.0) continue;
         const int ia = k, ib = np2 - 1 - k;
         int p = (ia == 0) ? 0 : 1 + (ia - 1 + r) % rounds;
         int q = (ib == 0) ? 0 : 1 + (ib - 1 + r) % rounds;
         if (p > q) { const int t = p; p = q; q = t; }
-        if (q >= n) continue;
+        const T se = pgm[k];
+        const T sec = S::conj(se);
         T* mp = Mc + size_t(p) * rows;
         T* mq = Mc + size_t(q) * rows;
-        double a = 0.0, b = 0.0;
-        T gmm = S::zero();
-        for (int i = lane; i < rows; i += 32) {
-          const T x = mp[i], y = mq[i];
-          a += S::abs2(x);
-          b += S::abs2(y);
-          gmm = S::add(gmm, S::cmul(x, y));
-        }
-        a = warp_sum(a);
-        b = warp_sum(b);
-        gmm = warp_sum(gmm);
-        const double ag = sqrt(S::abs2(gmm));
-        if (!(ag > tol * sqrt(a * b)) || ag == 0.0) continue;
-        const double zeta = (b - a) / (2.0 * ag);
-        const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-        const double c = 1.0 / sqrt(1.0 + t * t);
-        const double s = c * t;
-        const T e = S::scale(gmm, 1.0 / ag);        // phase of gamma
-        const T se = S::scale(e, s);                 // s e
-        const T sec = S::conj(se);                   // s conj(e)
-        for (int i = lane; i < rows; i += 32) {
+        for (int i = glane; i < rows; i += gs) {
           const T x = mp[i], y = mq[i];
           mp[i] = S::sub(S::scale(x, c), S::mul(sec, y));
           mq[i] = S::add(S::mul(se, x), S::scale(y, c));
         }
         T* jp = Jc + size_t(p) * n;
         T* jq = Jc + size_t(q) * n;
-        for (int i = lane; i < n; i += 32) {
+        for (int i = glane; i < n; i += gs) {
           const T x = jp[i], y = jq[i];
           jp[i] = S::sub(S::scale(x, c), S::mul(sec, y));
           jq[i] = S::add(S::mul(se, x), S::scale(y, c));
         }
-        if (lane == 0) s_rot = 1;
       }
       __syncthreads();
     }
-    converged = (s_rot == 0);
+    converged = (s_rot[flag] == 0);
     __syncthreads();
+    if (tid == 0) s_rot[flag] = 0;   // re-arm this buffer for sweep + 2
   }
 
   // singular values, descending order (ties by index)
@@ -136,7 +193,6 @@ jacobi_kernel(int rows, int n, const T* __restrict__ M, T* __restrict__ Wout,
     double mx = 0.0;
     for (int i = lane; i < n; i += 32) mx = fmax(mx, sqrt(S::abs2(jc[i])));
     for (int m = 16; m > 0; m >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, m));
-    // first index with |j_i| > 1e-10 * max
     int first = n;
     for (int base = 0; base < n && first == n; base += 32) {
       const int i = base + lane;
@@ -156,7 +212,10 @@ jacobi_kernel(int rows, int n, const T* __restrict__ M, T* __restrict__ Wout,
       Wout[size_t(i) * n + o] = S::mul(S::scale(mc[i], inv), ph);
     if (lane == 0) Sout[o] = sj;
   }
-  if (tid == 0) info[0] = converged ? sweep : -sweep;
+  if (tid == 0) {
+    info[0] = converged ? sweep : -sweep;
+    if (!converged && status) atomicOr(status, 8);   // speculative-path flag
+  }
 }
 
 template <typename T>
@@ -165,20 +224,30 @@ void launch_jacobi(Handle* h, int64_t rows64, int64_t n64, const T* M, T* W, dou
   LR_REQUIRE(n64 >= 1 && n64 <= 4096 && rows64 >= n64 && rows64 < (int64_t(1) << 31),
              LR_EINVAL, "jacobi_svd: need 1 <= cols <= 4096 and rows >= cols");
   const int n = int(n64), rows = int(rows64);
-  const size_t tail = size_t(n) * (sizeof(double) + sizeof(int));
+  const int pairs = (n + (n & 1)) / 2;
+  const size_t tail = size_t(n) * (sizeof(double) + sizeof(int)) +
+                      size_t(pairs) * (3 * sizeof(double) + sizeof(T)) + 64;
   const size_t full = (size_t(rows) + n) * n * sizeof(T) + tail;
   int max_smem = 0;
   LR_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
   const bool in_smem = full <= size_t(max_smem) - 1024;
-  T* gbuf = nullptr;
-  size_t dyn = full;
-  if (!in_smem) {
-    gbuf = pool_alloc_t<T>(h, (size_t(rows) + n) * n);
-    dyn = tail;
+  // lanes per pair: all pairs of a round in flight, 8..32 lanes each
+  int gs = 32;
+  while (gs > 8 && pairs * gs > JAC_THREADS) gs >>= 1;
+  while (gs > 8 && gs / 2 >= rows) gs >>= 1;
+  const double tol = 4e-15;
+  if (in_smem) {
+    auto kern = jacobi_kernel<T, true>;
+    LR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(full)));
+    kern<<<1, JAC_THREADS, full, h->stream>>>(rows, n, M, W, S, J, info, nullptr, tol, 60, gs,
+                                              h->status);
+  } else {
+    T* gbuf = pool_alloc_t<T>(h, (size_t(rows) + n) * n);
+    auto kern = jacobi_kernel<T, false>;
+    LR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(tail)));
+    kern<<<1, JAC_THREADS, tail, h->stream>>>(rows, n, M, W, S, J, info, gbuf, tol, 60, gs,
+                                              h->status);
   }
-  auto kern = jacobi_kernel<T>;
-  LR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dyn)));
-  kern<<<1, JAC_THREADS, dyn, h->stream>>>(rows, n, M, W, S, J, info, gbuf, in_smem, 1e-15, 80);
   LR_CHECK_LAUNCH();
 }
 

@@ -15,10 +15,10 @@ from dataclasses import dataclass
 
 from . import config
 from .core import (_out, _torch, apply_dev, as_operator, gemm_dev, is_device_array,
-                   small_svd_from_adjoint, to_device)
-from .rangefinder import (RangeBasis, _check_ell, _host_io, posterior_error_estimate_dev,
-                          subspace_iteration_range_dev, SketchSpec, orth_dev, _cast_like_op,
-                          _sketch_dev)
+                   small_svd_from_adjoint, speculate, to_device)
+from .rangefinder import (RangeBasis, SketchSpec, _cast_like_op, _check_ell, _host_io,
+                          _sketch_dev, orth_dev, posterior_error_estimate_dev, probes_dev,
+                          subspace_iteration_range_dev)
 from .sketch import srft_dev, srft_operator
 
 
@@ -85,42 +85,74 @@ def randomized_svd(A, k, p=config.DEFAULT_OVERSAMPLE, q=0, seed=0, sketch="gauss
 
     All intermediates stay on the GPU.  Returns (RangeBasis, PartialSVD,
     est_error) with numpy outputs for numpy input."""
+    torch = _torch()
     op = as_operator(A)
     ell = int(k) + int(p)
     host = _host_io(A, op)
     if sketch in ("gauss", "gaussian"):
         _check_ell(op, ell)
-        if q > 0:
-            Q = subspace_iteration_range_dev(op, ell, q, seed)
-            passes = 2 * q + 2
-        else:
-            Q = orth_dev(apply_dev(op, _cast_like_op(op, _sketch_dev(op, ell, seed))))
-            passes = 1
+        passes = 2 * q + 2 if q > 0 else 1
         spec = SketchSpec(kind="gaussian", ell=ell, power_q=q, seed=seed)
     elif sketch == "srft":
         if q > 0:
             raise ValueError("power iterations are not available with structured sketches")
         if ell > op.n:
             raise ValueError(f"rank+oversample {ell} exceeds the column count {op.n}")
-        Q = orth_dev(srft_dev(op.array, srft_operator(op.n, ell, seed)))
+        if not hasattr(op, "array"):
+            raise TypeError("the SRFT sketch needs a dense matrix")
         passes = 1
         spec = SketchSpec(kind="srft", ell=ell, seed=seed)
     else:
         raise ValueError(f"unknown sketch {sketch!r}")
-    U, S, V = direct_svd_dev(op, Q)
-    est_dev = None
-    if Q.shape[1] == 0:
-        est = 0.0
-    elif estimate:
-        est_dev = posterior_error_estimate_dev(op, Q, probes, alpha, seed + 13)
-        est = None
-    else:
-        est = None
+
+    # SRFT draws (d, picks) come from the host Philox stream (permutation is
+    # sequential); Gaussian Omega / probes are drawn on the device in body().
+    srft = srft_operator(op.n, ell, seed) if spec.kind == "srft" else None
+
+    def body():
+        W = probes_dev(op, probes, seed + 13) if estimate else None
+        if spec.kind == "gaussian":
+            omega = _cast_like_op(op, _sketch_dev(op, ell, seed))
+            if q > 0:
+                Q = subspace_iteration_range_dev(op, ell, q, seed, omega=omega)
+            else:
+                Q = orth_dev(apply_dev(op, omega))
+        else:
+            Q = orth_dev(srft_dev(op.array, srft))
+        U, S, V = direct_svd_dev(op, Q)
+        est_dev = None
+        if estimate and Q.shape[1]:
+            est_dev = posterior_error_estimate_dev(op, Q, probes, alpha, seed + 13, W=W)
+        return Q, U, S, V, est_dev
+
+    counters = _snapshot(op)
+    result = None
+    if getattr(op, "device_native", False):
+        # speculative pass: no host synchronization until the flags are read
+        status = torch.zeros(1, dtype=torch.int32, device=op.array.device if hasattr(
+            op, "array") else torch.device("cuda", torch.cuda.current_device()))
+        with speculate(status):
+            result = body()
+        if int(status.item()) != 0:       # rank drop / unresolved pivot: exact path
+            _restore(op, counters)
+            result = None
+    if result is None:
+        result = body()
+    Q, U, S, V, est_dev = result
+    est = 0.0 if Q.shape[1] == 0 else (float(est_dev.item()) if est_dev is not None else None)
     if truncate:
         kk = min(int(k), U.shape[1])
         U, S, V = U[:, :kk], S[:kk], V[:, :kk]
-    if est_dev is not None:
-        est = float(est_dev.item())
     basis = RangeBasis(Q=_out(Q, host), samples_used=ell, passes=passes, est_error=est,
                        spec=spec)
     return basis, PartialSVD(U=_out(U, host), sigma=_out(S, host), V=_out(V, host)), est
+
+
+def _snapshot(op):
+    c = op.counters
+    return (c.matvecs, c.adjoint_matvecs, c.passes, c.flops)
+
+
+def _restore(op, snap):
+    c = op.counters
+    c.matvecs, c.adjoint_matvecs, c.passes, c.flops = snap

@@ -20,7 +20,7 @@ import numpy as np
 from . import _lib, config
 from .core import (MatVecOperator, _out, _torch, apply_dev, as_operator, cast_dev,
                    is_device_array, orth_dev, to_device)
-from .sketch import SketchSpec, gaussian_matrix, rng_for, srft_dev, srft_operator
+from .sketch import SketchSpec, gaussian_dev, srft_dev, srft_operator
 
 _STREAM_PROBE = 0x70726F62
 
@@ -53,13 +53,15 @@ def _op_dtype(op):
     return torch.float64
 
 
-def _sketch_dev(op, ell, seed):
+def _real_of(dt):
     torch = _torch()
-    Om = gaussian_matrix(op.n, ell, seed)
-    dt = _op_dtype(op)
-    if dt in (torch.complex64, torch.complex128):
-        dt = torch.float32 if dt == torch.complex64 else torch.float64
-    return to_device(Om, dt)
+    return torch.float32 if dt in (torch.float32, torch.complex64) else torch.float64
+
+
+def _sketch_dev(op, ell, seed):
+    """Omega = gaussian_matrix(n, ell, seed) (sketch.py:96-100), drawn on the
+    device from the same Philox stream, in the operator's real precision."""
+    return gaussian_dev(op.n, ell, seed, dtype=_real_of(_op_dtype(op)))
 
 
 def _check_ell(op, ell):
@@ -137,9 +139,11 @@ def power_iteration_range(A, ell, q, seed, ortho_tol=config.GS_DROP_TOL, safegua
                       est_error=est, spec=spec)
 
 
-def subspace_iteration_range_dev(op, ell, q, seed, ortho_tol=config.GS_DROP_TOL):
+def subspace_iteration_range_dev(op, ell, q, seed, ortho_tol=config.GS_DROP_TOL, omega=None):
     """Alg 4.4 on a device operator; returns the device basis."""
-    Q = orth_dev(apply_dev(op, _cast_like_op(op, _sketch_dev(op, ell, seed))), ortho_tol)
+    if omega is None:
+        omega = _cast_like_op(op, _sketch_dev(op, ell, seed))
+    Q = orth_dev(apply_dev(op, omega), ortho_tol)
     for _ in range(q):
         Qt = orth_dev(apply_dev(op, Q, adjoint=True), ortho_tol)
         Q = orth_dev(apply_dev(op, Qt), ortho_tol)
@@ -192,14 +196,19 @@ def fast_range_finder(A, ell, seed, kind="srft", ortho_tol=config.GS_DROP_TOL):
                       diagnostics=diagnostics)
 
 
+def probes_dev(op, r, seed):
+    """Estimator probes W (rangefinder.py:78), drawn on the host and uploaded."""
+    Wd = gaussian_dev(op.n, r, seed, stream=_STREAM_PROBE, dtype=_real_of(_op_dtype(op)))
+    return _cast_like_op(op, Wd)
+
+
 def posterior_error_estimate_dev(op, Q, r=config.DEFAULT_PROBES, alpha=config.DEFAULT_ALPHA,
-                                 seed=0):
+                                 seed=0, W=None):
     """Device estimator; returns a 1-element float64 device tensor."""
     torch = _torch()
-    W = rng_for(seed, _STREAM_PROBE).standard_normal((op.n, r))
-    dt = _op_dtype(op)
-    Wd = to_device(W, torch.float64 if dt in (torch.float64, torch.complex128) else torch.float32)
-    Z = apply_dev(op, _cast_like_op(op, Wd))
+    if W is None:
+        W = probes_dev(op, r, seed)
+    Z = apply_dev(op, W)
     Z = Z.contiguous() if Z.stride(-1) != 1 else Z
     est = torch.empty(1, dtype=torch.float64, device=Z.device)
     Qd = cast_dev(Q if is_device_array(Q) else to_device(Q), Z.dtype)

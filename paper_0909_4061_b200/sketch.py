@@ -64,6 +64,29 @@ def gaussian_matrix(n, ell, seed):
     return rng_for(seed, _STREAM_GAUSS).standard_normal((n, ell))
 
 
+def gaussian_dev(n, ell, seed, stream=_STREAM_GAUSS, index=0, dtype=None, device=None):
+    """The same n x ell draw as gaussian_matrix / rng_for(seed, stream,
+    index).standard_normal((n, ell)), generated on the GPU (K0 kernel: the
+    Philox4x64-10 stream and numpy's ziggurat).  Returns a CUDA tensor in
+    `dtype` (float64 default; float32 is numpy's astype rounding)."""
+    torch = _torch()
+    from .core import _SPEC
+    dt = torch.float64 if dtype is None else dtype
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+    out = torch.empty((n, ell), dtype=dt, device=dev)
+    key_lo = int(seed) & (2**64 - 1)
+    key_hi = (int(stream) & (2**32 - 1)) | ((int(index) & (2**32 - 1)) << 32)
+    st = _SPEC.status
+    local = st is None
+    if local:
+        st = torch.zeros(1, dtype=torch.int32, device=dev)
+    _lib.call("lr_gaussian", _lib.handle(dev.index), key_lo, key_hi, n * ell,
+              _lib.dtype_code(dt), _lib.ptr(out), _lib.ptr(st))
+    if local and int(st.item()) != 0:
+        raise RuntimeError("device Gaussian stream: ziggurat cap exceeded (status %d)" % int(st.item()))
+    return out
+
+
 @dataclass
 class SrftOperator:
     """Materialized SRFT draw: scale * D F R with unimodular diagonal d

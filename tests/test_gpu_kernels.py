@@ -248,3 +248,21 @@ def test_estimate_matches_oracle():
     assert e == pytest.approx(eo, rel=1e-12)
     assert lr().posterior_error_estimate(A, np.zeros((400, 0)), seed=5) == pytest.approx(
         O.posterior_error_estimate(A, np.zeros((400, 0)), seed=5), rel=1e-12)
+
+
+@pytest.mark.parametrize("seed,stream,n,ell", [(2, 0x67617573, 8192, 110), (1, 0x67617573, 2048, 30),
+                                               (15, 0x70726F62, 8192, 10), (4, 0x67617573, 4096, 256),
+                                               (123456789, 0x67617573, 1 << 16, 48)])
+def test_device_gaussian_matches_numpy_stream(seed, stream, n, ell):
+    """K0: the device Philox/ziggurat stream equals numpy's (reference
+    sketch.py:32-42,96-100) -- all but at most the last ulp of tail draws."""
+    from paper_0909_4061_b200.sketch import gaussian_dev, rng_for
+    ref = rng_for(seed, stream).standard_normal((n, ell))
+    got = gaussian_dev(n, ell, seed, stream=stream).cpu().numpy()
+    diff = np.flatnonzero(ref != got)
+    assert diff.size <= max(2, ref.size // 200000)
+    if diff.size:
+        assert np.all(np.abs(ref.ravel()[diff]) > 3.654)
+        assert np.abs(ref.ravel()[diff] - got.ravel()[diff]).max() <= 4e-15 * np.abs(ref).max()
+    g32 = gaussian_dev(n, ell, seed, stream=stream, dtype=torch.float32).cpu().numpy()
+    assert (g32 != ref.astype(np.float32)).sum() <= diff.size
