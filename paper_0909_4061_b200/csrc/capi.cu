@@ -235,13 +235,39 @@ void small_svd_fast_impl(Handle* h, int dtype, int64_t r, int64_t c, const void*
   void* Q1 = pool_alloc(h, size_t(c) * r * es);
   void* Q2 = pool_alloc(h, size_t(c) * r * es);
   const double unres = 4.0 * double(r) * U64;
+  void* P1 = pool_alloc(h, size_t(r) * r * ws);
   gram_any(h, dtype, c, r, Bh, r, G);
-  chol_any(h, dtype, r, G, 0.0, unres, 0.0, P, R1, h->d_info);
-  apply_right(h, dtype, c, r, r, Bh, r, P, r, Q1, r);
+  chol_any(h, dtype, r, G, 0.0, unres, 0.0, P1, R1, h->d_info);
+  apply_right(h, dtype, c, r, r, Bh, r, P1, r, Q1, r);
   gram_any(h, dtype, c, r, Q1, r, G);
   chol_any(h, dtype, r, G, 0.0, unres, 0.0, P, R2, h->d_info);
   apply_right(h, dtype, c, r, r, Q1, r, P, r, Q2, r);
   trmm_upper(h, wd, r, R2, R1, R);
+  if (jacobi_reg_supported(r, is_complex(dtype))) {
+    // register-resident Jacobi: R J = M; then J = R^{-1} M with R^{-1} = P1 P2
+    void* Mun = pool_alloc(h, size_t(r) * r * ws);
+    void* Jun = pool_alloc(h, size_t(r) * r * ws);
+    void* Rinv = pool_alloc(h, size_t(r) * r * ws);
+    void* Ut = pool_alloc(h, size_t(r) * r * ws);
+    double* sig = pool_alloc_t<double>(h, size_t(r));
+    if (is_complex(dtype))
+      jacobi_reg_c128(h, r, static_cast<const double2*>(R), static_cast<double2*>(Mun), sig,
+                      h->d_info);
+    else
+      jacobi_reg_f64(h, r, static_cast<const double*>(R), static_cast<double*>(Mun), sig,
+                     h->d_info);
+    gemm_any(h, wd, false, false, r, r, r, P1, r, P, r, Rinv, r);
+    gemm_any(h, wd, false, false, r, r, r, Rinv, r, Mun, r, Jun, r);
+    svd_finalize(h, wd, r, Jun, Mun, sig, Ut, S, Wr);
+    // one Newton-Schulz step restores orthonormality of J to roundoff:
+    // U = Ut (1.5 I - 0.5 Ut^H Ut)
+    gemm_any(h, wd, true, true, r, r, r, Ut, r, Ut, r, G, r);
+    ns_coef(h, wd, r, G);
+    gemm_any(h, wd, false, false, r, r, r, Ut, r, G, r, J, r);
+    cast_copy(h, wd, J, r, dtype, U, r, r, r, false);
+    apply_right(h, dtype, c, r, r, Q2, r, Wr, r, V, r);
+    return;
+  }
   if (is_complex(dtype))
     jacobi_svd_c128(h, r, r, static_cast<double2*>(R), static_cast<double2*>(Wr), S,
                     static_cast<double2*>(J), h->d_info);

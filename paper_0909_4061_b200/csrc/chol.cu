@@ -23,19 +23,19 @@
 // Outputs: P (ell x ell): Q = Y . P[:, :rank] has orthonormal columns;
 // R (ell x ell) the factor restricted to kept rows/cols;
 // info = {rank, unresolved pivots, bad (non-finite) pivots}.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "scalar.cuh"
 
 namespace lr {
 namespace {
 
-constexpr int CHOL_THREADS = 1024;
-constexpr int NW = CHOL_THREADS / 32;
 
 // 1/sqrt(d) to full double precision (MUFU seed + two Newton steps)
 __device__ __forceinline__ double rsqrt_full(double d) { return rsqrt(d); }
 
-template <typename T, bool SMEM>
+template <typename T, bool SMEM, int CHOL_THREADS>
 __global__ void __launch_bounds__(CHOL_THREADS, 1)
 chol_drop_kernel(int n, const T* __restrict__ G, double drop_tol, double unres_rel,
                  double shift_coef, T* __restrict__ P, T* __restrict__ Rout,
@@ -57,6 +57,7 @@ chol_drop_kernel(int n, const T* __restrict__ G, double drop_tol, double unres_r
   int* pos = reinterpret_cast<int*>(ri + n);            // compact index or -1
   int* kidx = pos + n;                                  // compact -> original
 
+  constexpr int NW = CHOL_THREADS / 32;
   __shared__ double s_red[NW];
   __shared__ int s_unres, s_bad, s_rank;
 
@@ -210,25 +211,42 @@ void launch_chol(Handle* h, int64_t ell, const T* G, double drop_tol, double unr
   int max_smem = 0;
   LR_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
   const bool in_smem = full <= size_t(max_smem) - 1024;
+  // few warps: the kernel is latency-bound and per-column overhead is paid
+  // by every warp, so small problems run fastest on 4 warps
   if (in_smem) {
-    auto kern = chol_drop_kernel<T, true>;
-    LR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(full)));
-    kern<<<1, CHOL_THREADS, full, h->stream>>>(n, G, drop_tol, unres_rel, shift_coef, P, R,
-                                               info, nullptr, h->status);
+    static int forced = -1;
+    if (forced < 0) {
+      const char* e = getenv("LR_CHOL_THREADS");
+      forced = e ? atoi(e) : 0;
+    }
+    const int nt = forced ? forced : 1024;
+    auto launch = [&](auto kern, int threads) {
+      LR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(full)));
+      kern<<<1, threads, full, h->stream>>>(n, G, drop_tol, unres_rel, shift_coef, P, R, info,
+                                            nullptr, h->status);
+    };
+    if (nt <= 256) launch(chol_drop_kernel<T, true, 256>, 256);
+    else if (nt <= 512) launch(chol_drop_kernel<T, true, 512>, 512);
+    else launch(chol_drop_kernel<T, true, 1024>, 1024);
   } else {
     T* gW = pool_alloc_t<T>(h, size_t(n) * n);
-    auto kern = chol_drop_kernel<T, false>;
+    auto kern = chol_drop_kernel<T, false, 512>;
     LR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(tail)));
-    kern<<<1, CHOL_THREADS, tail, h->stream>>>(n, G, drop_tol, unres_rel, shift_coef, P, R,
-                                               info, gW, h->status);
+    kern<<<1, 512, tail, h->stream>>>(n, G, drop_tol, unres_rel, shift_coef, P, R, info, gW,
+                                      h->status);
   }
   LR_CHECK_LAUNCH();
 }
 
 }  // namespace
 
+template <typename T>
+bool chol_blocked_launch(Handle* h, int64_t ell, const T* G, double drop_tol, double unres_rel,
+                         double shift_coef, T* P, T* R, int32_t* info);
+
 void chol_drop_f64(Handle* h, int64_t ell, const double* G, double drop_tol, double unres_rel,
                    double shift_coef, double* P, double* R, int32_t* info) {
+  LR_REQUIRE(ell >= 1 && ell <= 4096, LR_EINVAL, "chol_drop: ell out of range [1, 4096]");
   launch_chol<double>(h, ell, G, drop_tol, unres_rel, shift_coef, P, R, info);
 }
 

@@ -138,7 +138,18 @@ void jacobi_svd_f64(Handle* h, int64_t rows, int64_t n, const double* M, double*
 void jacobi_svd_c128(Handle* h, int64_t rows, int64_t n, const double2* M, double2* W,
                      double* S, double2* J, int32_t* info);
 
+// jacobi_reg.cu: register-resident Jacobi (R J = M, M unsorted) + finalize
+bool jacobi_reg_supported(int64_t n, bool cplx);
+void jacobi_reg_f64(Handle* h, int64_t n, const double* R, double* Mout, double* sig,
+                    int32_t* info);
+void jacobi_reg_c128(Handle* h, int64_t n, const double2* R, double2* Mout, double* sig,
+                     int32_t* info);
+void svd_finalize(Handle* h, int dtype_wide, int64_t n, const void* Jun, const void* Mun,
+                  const double* sig, void* U, double* S, void* W);
+
 // misc.cu ---------------------------------------------------------------------
+// G <- 1.5 I - 0.5 G  (Newton-Schulz coefficient matrix, n x n wide dtype)
+void ns_coef(Handle* h, int dtype_wide, int64_t n, void* G);
 void cast_copy(Handle* h, int src_dtype, const void* src, int64_t lds, int dst_dtype,
                void* dst, int64_t ldd, int64_t rows, int64_t cols, bool conj_transpose);
 void col_sumsq(Handle* h, int dtype, int64_t m, int64_t r, const void* Z, int64_t ldz,

@@ -436,6 +436,28 @@ void max_abs_imag(Handle* h, int dtype, int64_t m, int64_t n, const void* Y, int
   LR_CHECK_LAUNCH();
 }
 
+namespace {
+template <typename T>
+__global__ void ns_coef_kernel(int n, T* G) {
+  using S = Sc<T>;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n * n; e += gridDim.x * blockDim.x) {
+    const int i = e / n, j = e % n;
+    T v = S::scale(G[e], -0.5);
+    if (i == j) v = S::add(v, S::make(1.5, 0.0));
+    G[e] = v;
+  }
+}
+}  // namespace
+
+void ns_coef(Handle* h, int dtype_wide, int64_t n, void* G) {
+  const int blocks = int(std::max<int64_t>(1, ceil_div(n * n, 256)));
+  if (dtype_wide == LR_C128)
+    ns_coef_kernel<double2><<<blocks, 256, 0, h->stream>>>(int(n), static_cast<double2*>(G));
+  else
+    ns_coef_kernel<double><<<blocks, 256, 0, h->stream>>>(int(n), static_cast<double*>(G));
+  LR_CHECK_LAUNCH();
+}
+
 void trmm_upper(Handle* h, int dtype, int64_t n, const void* R2, const void* R1, void* R) {
   const int blocks = int(std::max<int64_t>(1, ceil_div(n * n, 256)));
   if (dtype == LR_F64 || dtype == LR_F32) {

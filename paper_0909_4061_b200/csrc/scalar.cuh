@@ -23,6 +23,8 @@ struct Sc<double> {
   __host__ __device__ static double abs2(double a) { return a * a; }
   __host__ __device__ static double make(double r, double) { return r; }
   __device__ static double shfl_xor(double a, int m) { return __shfl_xor_sync(0xffffffffu, a, m); }
+  __device__ static double shfl_idx(double a, int src) { return __shfl_sync(0xffffffffu, a, src); }
+  __device__ static double div_re(double a, double r) { return a / r; }
 };
 
 template <>
@@ -53,6 +55,10 @@ struct Sc<double2> {
   __device__ static double2 shfl_xor(double2 a, int m) {
     return make_double2(__shfl_xor_sync(0xffffffffu, a.x, m), __shfl_xor_sync(0xffffffffu, a.y, m));
   }
+  __device__ static double2 shfl_idx(double2 a, int src) {
+    return make_double2(__shfl_sync(0xffffffffu, a.x, src), __shfl_sync(0xffffffffu, a.y, src));
+  }
+  __device__ static double2 div_re(double2 a, double r) { return make_double2(a.x / r, a.y / r); }
 };
 
 template <typename T>
