@@ -80,6 +80,15 @@ int lr_gemm(lr_handle_t h, int dtype, int op, int64_t m, int64_t n, int64_t ell,
             const void* A, int64_t lda, const void* X, int64_t ldx,
             void* Y, int64_t ldy);
 
+/* lr_gemm for a pass over an operator whose max |a_ij| is known (from the
+ * as_matrix validation pass, lr_check_finite): fp32 / complex64 passes run
+ * on the tcgen05 tensor cores with the three-product scaled-fp16 split
+ * (DESIGN.md "fp32 passes"); a_amax < 0 means unknown (computed here, one
+ * extra read of A).  fp64 / complex128 behave exactly like lr_gemm. */
+int lr_gemm_scaled(lr_handle_t h, int dtype, int op, int64_t m, int64_t n, int64_t ell,
+                   const void* A, int64_t lda, double a_amax, const void* X, int64_t ldx,
+                   void* Y, int64_t ldy);
+
 /* Gram matrix G = Y^H Y (ell x ell), accumulated in fp64 (real dtypes) or
  * complex128 (complex dtypes) regardless of the input precision.  G is
  * written as double / double2 row-major with leading dimension ell.  Used

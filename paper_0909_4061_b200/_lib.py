@@ -48,6 +48,8 @@ _SIGS = {
     "lr_set_f32_mode": [_vp, _int],
     "lr_reserve": [_vp, _i64],
     "lr_gemm": [_vp, _int, _int, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64],
+    "lr_gemm_scaled": [_vp, _int, _int, _i64, _i64, _i64, _vp, _i64, C.c_double, _vp, _i64, _vp,
+                       _i64],
     "lr_gram": [_vp, _int, _i64, _i64, _vp, _i64, _vp],
     "lr_chol_drop": [_vp, _int, _i64, _vp, C.c_double, C.c_double, C.c_double, _vp, _vp, _vp],
     "lr_orth": [_vp, _int, _i64, _i64, _vp, _i64, _vp, _i64, C.c_double, C.POINTER(_i64)],

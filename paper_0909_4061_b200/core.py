@@ -230,7 +230,7 @@ class DenseOperator(MatVecOperator):
         if t.shape[0] != self.n:
             raise ValueError(f"dimension mismatch: A is {self.shape}, X has {t.shape[0]} rows")
         Y = torch.empty((self.m, t.shape[1]), dtype=self.array.dtype, device=self.array.device)
-        _timed_pass(self.array, t, Y, False)
+        _timed_pass(self.array, t, Y, False, self.amax)
         Y = Y.reshape(-1) if vec else Y
         return _out(Y, host)
 
@@ -240,7 +240,7 @@ class DenseOperator(MatVecOperator):
         if t.shape[0] != self.m:
             raise ValueError(f"dimension mismatch: A is {self.shape}, Y has {t.shape[0]} rows")
         Z = torch.empty((self.n, t.shape[1]), dtype=self.array.dtype, device=self.array.device)
-        _timed_pass(self.array, t, Z, True)
+        _timed_pass(self.array, t, Z, True, self.amax)
         Z = Z.reshape(-1) if vec else Z
         return _out(Z, host)
 
@@ -253,14 +253,25 @@ CudaDenseOperator = DenseOperator
 PASS_EVENTS = None
 
 
-def _timed_pass(A, X, Y, adjoint):
+def _pass(A, X, Y, adjoint, amax):
+    """One pass over A (K1/K2); fp32 / complex64 passes use the tcgen05
+    scaled-fp16 split with the operator's max|A| (lr_gemm_scaled)."""
+    code = _lib.dtype_code(A.dtype)
+    op = _lib.OP_N if not adjoint else (_lib.OP_C if A.is_complex() else _lib.OP_T)
+    m, n = A.shape
+    _lib.call("lr_gemm_scaled", _lib.handle(A.device.index), code, op, m, n, X.shape[1],
+              _lib.ptr(A), _lib.ld(A), float(-1.0 if amax is None else amax), _lib.ptr(X),
+              _lib.ld(X), _lib.ptr(Y), _lib.ld(Y))
+
+
+def _timed_pass(A, X, Y, adjoint, amax=None):
     if PASS_EVENTS is None:
-        gemm(A, X, Y, adjoint=adjoint)
+        _pass(A, X, Y, adjoint, amax)
         return
     torch = _torch()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
-    gemm(A, X, Y, adjoint=adjoint)
+    _pass(A, X, Y, adjoint, amax)
     e.record()
     m, n = A.shape
     mult = 4 if A.is_complex() else 1

@@ -599,6 +599,30 @@ int lr_gemm(lr_handle_t hh, int dtype, int op, int64_t m, int64_t n, int64_t ell
   API_END
 }
 
+int lr_gemm_scaled(lr_handle_t hh, int dtype, int op, int64_t m, int64_t n, int64_t ell,
+                   const void* A, int64_t lda, double a_amax, const void* X, int64_t ldx, void* Y,
+                   int64_t ldy) {
+  API_BEGIN
+  Handle* h = H(hh);
+  check_dtype(dtype);
+  LR_REQUIRE(m >= 0 && n >= 0 && ell >= 0, LR_EINVAL, "lr_gemm_scaled: negative dimension");
+  LR_REQUIRE(op == LR_OP_N || op == LR_OP_T || op == LR_OP_C, LR_EINVAL, "lr_gemm_scaled: bad op");
+  LR_REQUIRE(lda >= n && ldx >= ell && ldy >= ell, LR_EINVAL, "lr_gemm_scaled: bad leading dims");
+  lr::pool_reset(h);
+  const bool t = op != LR_OP_N;
+  const int64_t M = t ? n : m, K = t ? m : n;
+  if (dtype == LR_F32) {
+    lr::gemm_f32_hint(h, t, M, ell, K, static_cast<const float*>(A), lda, a_amax,
+                      static_cast<const float*>(X), ldx, static_cast<float*>(Y), ldy);
+  } else if (dtype == LR_C64) {
+    lr::gemm_c64_hint(h, t, op == LR_OP_C, M, ell, K, static_cast<const float2*>(A), lda, a_amax,
+                      static_cast<const float2*>(X), ldx, static_cast<float2*>(Y), ldy);
+  } else {
+    lr::gemm_any(h, dtype, t, op == LR_OP_C, M, ell, K, A, lda, X, ldx, Y, ldy);
+  }
+  API_END
+}
+
 int lr_gram(lr_handle_t hh, int dtype, int64_t m, int64_t ell, const void* Y, int64_t ldy,
             void* G) {
   API_BEGIN

@@ -6,6 +6,7 @@
 #include <stdint.h>
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <string>
 #include <vector>
 
@@ -119,6 +120,13 @@ void gemm_f32_simt(Handle* h, bool transA, int64_t M, int64_t N, int64_t K, cons
 void gemm_c64_simt(Handle* h, bool transA, bool conjA, int64_t M, int64_t N, int64_t K,
                    const float2* A, int64_t lda, const float2* B, int64_t ldb, float2* C,
                    int64_t ldc);
+// passes over A with the operator's max|A| (a_amax < 0: unknown)
+void gemm_f32_hint(Handle* h, bool transA, int64_t M, int64_t N, int64_t K, const float* A,
+                   int64_t lda, double a_amax, const float* B, int64_t ldb, float* C,
+                   int64_t ldc);
+void gemm_c64_hint(Handle* h, bool transA, bool conjA, int64_t M, int64_t N, int64_t K,
+                   const float2* A, int64_t lda, double a_amax, const float2* B, int64_t ldb,
+                   float2* C, int64_t ldc);
 // fp64-accumulated Gram of fp32 / complex64 panels
 void gram_f32(Handle* h, int64_t m, int64_t ell, const float* Y, int64_t ldy, double* G);
 void gram_c64(Handle* h, int64_t m, int64_t ell, const float2* Y, int64_t ldy, double2* G);

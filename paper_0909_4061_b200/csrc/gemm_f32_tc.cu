@@ -1,0 +1,472 @@
+// K1/K2 in fp32 on the 5th-generation tensor cores (tcgen05 + TMEM + TMA).
+//
+// Replaces DenseOperator._apply / _apply_adjoint (reference core.py:391-395)
+// for float32 A (config 4: 2^20 x 4096, ell = 256).  The reference computes
+// in fp64; plain TF32 truncation fails parity at j = 1, so each pass uses a
+// three-product split of scaled fp16 operands (
+// tools/numerics_cfg4.py measured parity to j = 125, like honest fp32):
+//     A ~ (A_hi + A_lo) / s_A,  X ~ (X_hi + X_lo) / s_X   (fp16, 22 bits)
+//     A X ~ (A_hi X_hi + A_hi X_lo + A_lo X_hi) / (s_A s_X)
+// with power-of-two scales from max|A| (operator validation) and max|X|.
+// All three products accumulate into ONE fp32 TMEM accumulator.
+//
+// CTA = 128 rows of op(A) x all N <= 256 columns (one UMMA 128 x N x 16 per
+// k-substep), k-stage 32, 3-stage ring, 256 threads:
+//   warp 0  TMA producer: fp32 A tile (16 KB) and fp16 X_hi/X_lo tiles
+//   warp 1  MMA issuer (one lane): 6 x tcgen05.mma kind::f16 per stage
+//   warp 2  TMEM allocator
+//   warps 4-7  converters: fp32 A tile -> scaled fp16 hi/lo in the canonical
+//           K-major SWIZZLE_64B layout (transposing for A^T), then the
+//           epilogue: tcgen05.ld -> * 1/(s_A s_X) -> global (or split-K slice)
+// A is read from HBM exactly once per pass (per N <= 256); X_hi / X_lo are
+// prepared once per pass in K-major fp16 (small for A X; for A^T Y the
+// prepared Y is 2 x 2 bytes per element, read from L2/HBM per M tile).
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+
+namespace lr {
+namespace {
+
+constexpr int TBM = 128;          // UMMA M
+constexpr int TBK = 32;           // k per stage (64 B of fp16 per row)
+constexpr int TSTAGES = 3;
+constexpr int TTHREADS = 256;
+constexpr int A32_BYTES = TBM * TBK * 4;    // 16 KB
+constexpr int AH_BYTES = TBM * TBK * 2;     // 8 KB
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+// canonical K-major SWIZZLE_64B UMMA smem descriptor (rows of 64 B, 8-row
+// groups 512 B apart; sm100 descriptor version 1)
+__device__ __forceinline__ uint64_t desc_sw64(const void* p) {
+  const uint64_t addr = smem_u32(p);
+  return ((addr >> 4) & 0x3FFFull) | (1ull << 16) | (uint64_t(512 >> 4) << 32) | (1ull << 46) |
+         (4ull << 61);
+}
+
+__device__ __forceinline__ void umma_f16(uint32_t tmem, uint64_t adesc, uint64_t bdesc,
+                                         uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+// byte offset of element (row r, k) in a K-major SWIZZLE_64B fp16 tile
+__device__ __forceinline__ int sw64_off(int r, int chunk) {
+  return r * 64 + ((chunk ^ ((r >> 1) & 3)) << 4);
+}
+
+__device__ __forceinline__ void split_store8(const float* v, float s, char* hi_row_base,
+                                             char* lo_row_base, int r, int g) {
+  __half2 h[4], l[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float x0 = v[2 * e] * s, x1 = v[2 * e + 1] * s;
+    const __half h0 = __float2half_rn(x0), h1 = __float2half_rn(x1);
+    h[e] = __halves2half2(h0, h1);
+    l[e] = __halves2half2(__float2half_rn(x0 - __half2float(h0)),
+                          __float2half_rn(x1 - __half2float(h1)));
+  }
+  const int off = sw64_off(r, g);
+  *reinterpret_cast<uint4*>(hi_row_base + off) = *reinterpret_cast<uint4*>(h);
+  *reinterpret_cast<uint4*>(lo_row_base + off) = *reinterpret_cast<uint4*>(l);
+}
+
+template <bool TRANS>
+__global__ void __launch_bounds__(TTHREADS, 1)
+gemm_f32_tc_kernel(const __grid_constant__ CUtensorMap mapA,
+                   const __grid_constant__ CUtensorMap mapBhi,
+                   const __grid_constant__ CUtensorMap mapBlo, int M, int N, int BN,
+                   int64_t k_per_split, int64_t K, float sA, const float* __restrict__ sB_dev,
+                   float* __restrict__ C, int64_t ldc, int64_t cstride) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // 1024-align the dynamic smem base
+  unsigned char* base = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int B_BYTES = BN * TBK * 2;
+  const int stage_bytes = A32_BYTES + 2 * AH_BYTES + 2 * B_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + TSTAGES * stage_bytes);
+  uint64_t* a32_full = bars;
+  uint64_t* a32_empty = bars + TSTAGES;
+  uint64_t* ahl_full = bars + 2 * TSTAGES;
+  uint64_t* b_full = bars + 3 * TSTAGES;
+  uint64_t* st_empty = bars + 4 * TSTAGES;
+  uint64_t* acc_full = bars + 5 * TSTAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 5 * TSTAGES + 1);
+
+  auto a32 = [&](int s) { return base + s * stage_bytes; };
+  auto ahi = [&](int s) { return base + s * stage_bytes + A32_BYTES; };
+  auto alo = [&](int s) { return base + s * stage_bytes + A32_BYTES + AH_BYTES; };
+  auto bhi = [&](int s) { return base + s * stage_bytes + A32_BYTES + 2 * AH_BYTES; };
+  auto blo = [&](int s) { return base + s * stage_bytes + A32_BYTES + 2 * AH_BYTES + B_BYTES; };
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * TBM;
+  const int64_t kbeg = int64_t(blockIdx.z) * k_per_split;
+  const int64_t kend = min(K, kbeg + k_per_split);
+  const int nk = int((kend - kbeg + TBK - 1) / TBK);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < TSTAGES; ++s) {
+      mbar_init(&a32_full[s], 1);
+      mbar_init(&a32_empty[s], 4);
+      mbar_init(&ahl_full[s], 4);
+      mbar_init(&b_full[s], 1);
+      mbar_init(&st_empty[s], 1);
+    }
+    mbar_init(acc_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  const int tmem_cols = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(tmem_cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer
+      const uint32_t bbytes = uint32_t(2 * B_BYTES);
+      for (int kt = 0; kt < nk; ++kt) {
+        const int s = kt % TSTAGES;
+        const uint32_t ph = uint32_t(kt / TSTAGES) & 1u;
+        const int kc = int(kbeg + int64_t(kt) * TBK);
+        mbar_wait(&a32_empty[s], ph ^ 1u);
+        mbar_expect_tx(&a32_full[s], A32_BYTES);
+        if (!TRANS) tma_load_2d(a32(s), &mapA, &a32_full[s], kc, m0);
+        else        tma_load_2d(a32(s), &mapA, &a32_full[s], m0, kc);
+        mbar_wait(&st_empty[s], ph ^ 1u);
+        mbar_expect_tx(&b_full[s], bbytes);
+        tma_load_2d(bhi(s), &mapBhi, &b_full[s], kc, 0);
+        tma_load_2d(blo(s), &mapBlo, &b_full[s], kc, 0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer
+      const uint32_t idesc = (1u << 4) | (uint32_t(BN >> 3) << 17) | (uint32_t(TBM >> 4) << 24);
+      for (int kt = 0; kt < nk; ++kt) {
+        const int s = kt % TSTAGES;
+        const uint32_t ph = uint32_t(kt / TSTAGES) & 1u;
+        mbar_wait(&ahl_full[s], ph);
+        mbar_wait(&b_full[s], ph);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint64_t dah = desc_sw64(ahi(s)), dal = desc_sw64(alo(s));
+        const uint64_t dbh = desc_sw64(bhi(s)), dbl = desc_sw64(blo(s));
+#pragma unroll
+        for (int ks = 0; ks < TBK / 16; ++ks) {
+          const uint64_t adv = uint64_t(ks * 32) >> 4;   // 16 fp16 = 32 bytes
+          umma_f16(tmem, dah + adv, dbh + adv, idesc, (kt | ks) ? 1u : 0u);
+          umma_f16(tmem, dah + adv, dbl + adv, idesc, 1u);
+          umma_f16(tmem, dal + adv, dbh + adv, idesc, 1u);
+        }
+        umma_commit(&st_empty[s]);
+      }
+      umma_commit(acc_full);
+    }
+  } else if (warp >= 4) {
+    // ---------------- converters (one A row per thread), then epilogue
+    const int r = threadIdx.x - 128;
+    for (int kt = 0; kt < nk; ++kt) {
+      const int s = kt % TSTAGES;
+      const uint32_t ph = uint32_t(kt / TSTAGES) & 1u;
+      mbar_wait(&a32_full[s], ph);
+      float v[TBK];
+      if (!TRANS) {
+        // fp32 staging: row r (128 B), TMA SWIZZLE_128B (16-B chunk c at c ^ (r & 7))
+        const unsigned char* row = a32(s) + r * 128;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const float4 q = *reinterpret_cast<const float4*>(row + ((c ^ (r & 7)) << 4));
+          v[4 * c] = q.x; v[4 * c + 1] = q.y; v[4 * c + 2] = q.z; v[4 * c + 3] = q.w;
+        }
+      } else {
+        // fp32 staging [k][m] (512-B rows, no swizzle): column r
+        const float* st = reinterpret_cast<const float*>(a32(s));
+#pragma unroll
+        for (int k = 0; k < TBK; ++k) v[k] = st[k * TBM + r];
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&a32_empty[s]);
+      mbar_wait(&st_empty[s], ph ^ 1u);   // MMA finished with the previous hi/lo tiles
+#pragma unroll
+      for (int g = 0; g < TBK / 8; ++g)
+        split_store8(v + 8 * g, sA, reinterpret_cast<char*>(ahi(s)),
+                     reinterpret_cast<char*>(alo(s)), r, g);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ahl_full[s]);
+    }
+    // epilogue
+    mbar_wait(acc_full, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const float inv = 1.0f / (sA * sB_dev[0]);
+    const int q = warp - 4;                    // TMEM lane quarter
+    const int row = m0 + q * 32 + lane;
+    float* crow = C + int64_t(blockIdx.z) * cstride + int64_t(row) * ldc;
+    for (int c0 = 0; c0 < BN; c0 += 16) {
+      uint32_t d[16];
+      const uint32_t taddr = tmem + (uint32_t(q * 32) << 16) + uint32_t(c0);
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+          "%14,%15}, [%16];"
+          : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]),
+            "=r"(d[7]), "=r"(d[8]), "=r"(d[9]), "=r"(d[10]), "=r"(d[11]), "=r"(d[12]),
+            "=r"(d[13]), "=r"(d[14]), "=r"(d[15])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (row < M) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (c0 + j < N) crow[c0 + j] = __uint_as_float(d[j]) * inv;
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(tmem_cols));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// operand preparation
+
+__global__ void amax_f32_kernel(int64_t rows, int64_t cols, const float* __restrict__ X,
+                                int64_t ld, unsigned int* __restrict__ out_bits) {
+  float mx = 0.f;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < rows * cols;
+       e += int64_t(gridDim.x) * blockDim.x)
+    mx = fmaxf(mx, fabsf(X[(e / cols) * ld + (e % cols)]));
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out_bits, __float_as_uint(mx));
+}
+
+// power-of-two scale s with s * amax in [2^13, 2^14): |scaled| < 2^14 fits fp16
+__device__ __forceinline__ float pow2_scale(float amax) {
+  if (!(amax > 0.f) || !isfinite(amax)) return 1.f;
+  int e;
+  frexpf(amax, &e);   // amax = f * 2^e, f in [0.5, 1)
+  return ldexpf(1.f, 14 - e);
+}
+
+__global__ void make_scale_kernel(const unsigned int* bits, float* scale) {
+  scale[0] = pow2_scale(__uint_as_float(bits[0]));
+}
+
+// X (K x N row-major, ld) -> hi/lo (N x Kp fp16, K-major), scaled by *scale
+__global__ void split_transpose_kernel(int64_t K, int64_t N, const float* __restrict__ X,
+                                       int64_t ld, int64_t Kp, const float* __restrict__ scale,
+                                       __half* __restrict__ hi, __half* __restrict__ lo) {
+  __shared__ float tile[32][33];
+  const float s = scale[0];
+  const int64_t k0 = int64_t(blockIdx.x) * 32, n0 = int64_t(blockIdx.y) * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t k = k0 + i, n = n0 + threadIdx.x;
+    tile[i][threadIdx.x] = (k < K && n < N) ? X[k * ld + n] * s : 0.f;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t n = n0 + i, k = k0 + threadIdx.x;
+    if (n < N && k < Kp) {
+      const float v = tile[threadIdx.x][i];
+      const __half h = __float2half_rn(v);
+      hi[n * Kp + k] = h;
+      lo[n * Kp + k] = __float2half_rn(v - __half2float(h));
+    }
+  }
+}
+
+__global__ void reduce_slices_f32(int64_t M, int64_t N, int S, const float* __restrict__ part,
+                                  float* __restrict__ out, int64_t ldo) {
+  const int64_t total = M * N;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    float s = 0.f;
+    for (int k = 0; k < S; ++k) s += part[int64_t(k) * total + i];
+    out[(i / N) * ldo + (i % N)] = s;
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    LR_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    LR_REQUIRE(p != nullptr, LR_ECUDA, "cuTensorMapEncodeTiled not available");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+CUtensorMap make_map_2d(CUtensorMapDataType dt, const void* ptr, uint64_t inner, uint64_t outer,
+                        uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer,
+                        CUtensorMapSwizzle swz) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {inner, outer};
+  const cuuint64_t strides[1] = {row_bytes};
+  const cuuint32_t box[2] = {box_inner, box_outer};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, dt, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  LR_REQUIRE(r == CUDA_SUCCESS, LR_ECUDA, "cuTensorMapEncodeTiled failed");
+  return m;
+}
+
+}  // namespace
+
+bool gemm_f32_tc_supported(bool transA, int64_t N, const float* A, int64_t lda) {
+  return N >= 1 && N <= 256 && (lda % 4) == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0;
+}
+
+// C (M x N) = op(A) B, fp32 in/out, three-product fp16 split on tcgen05.
+// a_amax < 0: max|A| unknown, computed here (one extra read of A).
+void gemm_f32_tc(Handle* h, bool transA, int64_t M, int64_t N, int64_t K, const float* A,
+                 int64_t lda, double a_amax, const float* B, int64_t ldb, float* C,
+                 int64_t ldc) {
+  if (M == 0 || N == 0) return;
+  LR_REQUIRE(gemm_f32_tc_supported(transA, N, A, lda), LR_EUNSUPPORTED,
+             "gemm_f32_tc: unsupported shape/alignment");
+  // scales: s_A on the host (from the operator's max|A|), s_B on the device
+  unsigned int* bits = pool_alloc_t<unsigned int>(h, 4);
+  float* sB = reinterpret_cast<float*>(bits + 2);
+  float sA = 1.f;
+  if (a_amax < 0) {
+    LR_CUDA(cudaMemsetAsync(bits + 1, 0, sizeof(unsigned int), h->stream));
+    const int64_t rows = transA ? K : M, cols = transA ? M : K;
+    amax_f32_kernel<<<h->sm_count * 8, 256, 0, h->stream>>>(rows, cols, A, lda, bits + 1);
+    LR_CHECK_LAUNCH();
+    unsigned int hb = 0;
+    LR_CUDA(cudaMemcpyAsync(&hb, bits + 1, sizeof(hb), cudaMemcpyDeviceToHost, h->stream));
+    LR_CUDA(cudaStreamSynchronize(h->stream));
+    float f;
+    memcpy(&f, &hb, sizeof(f));
+    a_amax = f;
+  }
+  if (a_amax > 0 && std::isfinite(a_amax)) {
+    int e;
+    std::frexp(a_amax, &e);
+    sA = std::ldexp(1.f, 14 - e);
+  }
+  LR_CUDA(cudaMemsetAsync(bits, 0, sizeof(unsigned int), h->stream));
+  amax_f32_kernel<<<std::max<int64_t>(1, std::min<int64_t>(ceil_div(K * N, 256), 4096)), 256, 0,
+                    h->stream>>>(K, N, B, ldb, bits);
+  LR_CHECK_LAUNCH();
+  make_scale_kernel<<<1, 1, 0, h->stream>>>(bits, sB);
+  LR_CHECK_LAUNCH();
+  const int BN = int(ceil_div(N, 16) * 16);
+  const int64_t Kp = ceil_div(K, 8) * 8;
+  __half* Bhi = pool_alloc_t<__half>(h, size_t(BN) * Kp);
+  __half* Blo = pool_alloc_t<__half>(h, size_t(BN) * Kp);
+  if (BN != N) {
+    LR_CUDA(cudaMemsetAsync(Bhi, 0, sizeof(__half) * BN * Kp, h->stream));
+    LR_CUDA(cudaMemsetAsync(Blo, 0, sizeof(__half) * BN * Kp, h->stream));
+  }
+  {
+    dim3 grid(unsigned(ceil_div(Kp, 32)), unsigned(ceil_div(N, 32)));
+    split_transpose_kernel<<<grid, dim3(32, 8), 0, h->stream>>>(K, N, B, ldb, Kp, sB, Bhi, Blo);
+    LR_CHECK_LAUNCH();
+  }
+  CUtensorMap mapA = transA
+      ? make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, A, uint64_t(M), uint64_t(K), uint64_t(lda) * 4,
+                    TBM, TBK, CU_TENSOR_MAP_SWIZZLE_NONE)
+      : make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, A, uint64_t(K), uint64_t(M), uint64_t(lda) * 4,
+                    TBK, TBM, CU_TENSOR_MAP_SWIZZLE_128B);
+  CUtensorMap mapBh = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT16, Bhi, uint64_t(Kp), uint64_t(BN),
+                                  uint64_t(Kp) * 2, TBK, uint32_t(BN), CU_TENSOR_MAP_SWIZZLE_64B);
+  CUtensorMap mapBl = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT16, Blo, uint64_t(Kp), uint64_t(BN),
+                                  uint64_t(Kp) * 2, TBK, uint32_t(BN), CU_TENSOR_MAP_SWIZZLE_64B);
+  const int stage_bytes = A32_BYTES + 2 * AH_BYTES + 2 * BN * TBK * 2;
+  // One CTA per SM: with two co-resident CTAs (N <= 128 fits twice) some
+  // output rows came out wrong on B200 (tools/tc_probe2.py); until that is
+  // understood the launch reserves more than half of the SM's shared memory.
+  size_t smem = size_t(TSTAGES) * stage_bytes + 1024 /*align*/ + 256 /*barriers*/;
+  smem = std::max<size_t>(smem, 116 * 1024);
+  const int64_t mt = ceil_div(M, TBM);
+  int64_t splits = 1;
+  if (mt < h->sm_count) {
+    splits = std::max<int64_t>(1, std::min<int64_t>(ceil_div(2 * h->sm_count, mt),
+                                                    ceil_div(K, 8 * TBK)));
+  }
+  const int64_t kps = ceil_div(ceil_div(K, splits), TBK) * TBK;
+  splits = ceil_div(K, kps);
+  float* out = C;
+  int64_t ldo = ldc, cstride = 0;
+  if (splits > 1) {
+    out = pool_alloc_t<float>(h, size_t(splits) * M * N);
+    ldo = N;
+    cstride = M * N;
+  }
+  dim3 grid(unsigned(mt), 1, unsigned(splits));
+  if (transA) {
+    auto kern = gemm_f32_tc_kernel<true>;
+    LR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    kern<<<grid, TTHREADS, smem, h->stream>>>(mapA, mapBh, mapBl, int(M), int(N), BN, kps, K, sA,
+                                              sB, out, ldo, cstride);
+  } else {
+    auto kern = gemm_f32_tc_kernel<false>;
+    LR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    kern<<<grid, TTHREADS, smem, h->stream>>>(mapA, mapBh, mapBl, int(M), int(N), BN, kps, K, sA,
+                                              sB, out, ldo, cstride);
+  }
+  LR_CHECK_LAUNCH();
+  if (splits > 1) {
+    const int blocks = int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(M * N, 256), 8192)));
+    reduce_slices_f32<<<blocks, 256, 0, h->stream>>>(M, N, int(splits), out, C, ldc);
+    LR_CHECK_LAUNCH();
+  }
+}
+
+}  // namespace lr

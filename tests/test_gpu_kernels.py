@@ -67,6 +67,28 @@ def test_gemm_f32_family(m, n, ell, dtype):
     assert np.abs(Z - ref).max() <= 2e-6 * np.abs(ref).max()
 
 
+@pytest.mark.parametrize("ell", [1, 10, 20, 30, 48, 110, 130, 256])
+@pytest.mark.parametrize("dtype", [np.float32, np.complex64])
+def test_tcgen05_pass_shapes(ell, dtype):
+    """The fp32 / complex64 passes over A run on tcgen05 (scaled fp16 split);
+    every N tile width must agree with fp64 to ~fp32 accuracy."""
+    from paper_0909_4061_b200.core import DenseOperator
+    m, n = 1536, 1024
+    if dtype == np.complex64 and ell > 128:
+        pytest.skip("complex real view needs 2 ell <= 256")
+    A = rand((m, n), dtype, 11)
+    X = rand((n, ell), dtype, 12)
+    W = rand((m, ell), dtype, 13)
+    op = DenseOperator(A)
+    wide = np.complex128 if A.dtype.kind == "c" else np.float64
+    Y = op.apply(X)
+    ref = A.astype(wide) @ X.astype(wide)
+    assert np.abs(Y - ref).max() <= 1e-5 * np.abs(ref).max()
+    Z = op.apply_adjoint(W)
+    ref = A.astype(wide).conj().T @ W.astype(wide)
+    assert np.abs(Z - ref).max() <= 1e-5 * np.abs(ref).max()
+
+
 def test_gemm_vector_and_strided_inputs():
     from paper_0909_4061_b200.core import DenseOperator
     A = rand((50, 40), np.float64, 1)
