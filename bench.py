@@ -48,6 +48,8 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--sharded", action="store_true",
+                   help="use the row-sharded (NCCL) path even at one GPU")
     return p.parse_args()
 
 
@@ -178,9 +180,8 @@ def run_ours(args, cfg):
 
     rank, world, local = env_rank()
     torch.cuda.set_device(local)
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if world > 1 or args.sharded:
+        return run_sharded(args, cfg)
     A = build_input(cfg)
     torch.cuda.synchronize()
     op = lr.DenseOperator(A)
@@ -216,10 +217,6 @@ def run_ours(args, cfg):
         ms = float(t.item())
     pev = lrcore.PASS_EVENTS
     lrcore.PASS_EVENTS = None
-    pass_ms = [a.elapsed_time(b) for a, b, *_ in pev]
-    flops_per = [f for _, _, f, _, _ in pev]
-    avg_pass_ms = sum(pass_ms) / len(pass_ms)
-    avg_flops = sum(flops_per) / len(flops_per)
 
     # estimator pass, timed separately
     est_s, est_e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -231,23 +228,7 @@ def run_ours(args, cfg):
     est_ms = est_s.elapsed_time(est_e)
 
     value = passes * a_bytes / (ms / 1e3) / 1e9
-    pk, src = peaks()
-    if A.dtype in (torch.float64, torch.complex128):
-        peak_tf = measured_fp64_peak()
-        bound, peak_src = "tensor", "measured in-run: cuBLAS DGEMM 8192^3 (torch.matmul)"
-    else:
-        peak_tf = pk["bf16_tflops"]
-        bound, peak_src = "tensor", f"{src} bf16 (MEASURED_PEAKS.json)"
-    achieved_tf = avg_flops / (avg_pass_ms / 1e3) / 1e12
-    hbm = pk["hbm_gbs"]
-    # per-pass roofline: max(flops / tensor peak, bytes(A) / HBM)
-    roof_pass_s = max(avg_flops / (peak_tf * 1e12), a_bytes / (hbm * 1e9))
-    roof_step_ms = passes * roof_pass_s * 1e3
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath):
-        traffic = json.load(open(tpath)).get(f"cfg{cfg.idx}")
-
+    roof = roofline(A, cfg, pev, ms, args.steps, passes, a_bytes)
     line = {
         "metric": "rank-k rSVD time & A-GB/s (% roofline) at 1/2/4/8 B200 vs host-CPU ref",
         "value": round(value, 3), "unit": "A-GB/s", "n_gpus": world, "steps": args.steps,
@@ -261,14 +242,7 @@ def run_ours(args, cfg):
                    "passes": passes, "a_bytes": a_bytes,
                    "l2": "inputs larger than L2 (A >= 1 GiB), no flush",
                    "parallelism": f"rows x{world}" if world > 1 else "single GPU"},
-        "roofline": {"bound": bound, "achieved": round(achieved_tf, 3), "peak": round(peak_tf, 3),
-                     "unit": "TFLOP/s", "frac": round(achieved_tf / peak_tf, 4),
-                     "traffic": traffic, "kernel": "lr_gemm pass over A (K1/K2)",
-                     "peak_source": peak_src, "avg_pass_ms": round(avg_pass_ms, 4),
-                     "pass_a_gbs": round(a_bytes / (avg_pass_ms / 1e3) / 1e9, 1),
-                     "step_roofline_ms": round(roof_step_ms, 4),
-                     "step_roofline_frac": round(roof_step_ms / ms, 4),
-                     "pass_share_of_step": round(sum(pass_ms) / (ms * args.steps), 4)},
+        "roofline": roof,
         "estimator_ms": round(est_ms, 4),
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
@@ -289,6 +263,156 @@ def run_ours(args, cfg):
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+def roofline(A, cfg, pev, ms, steps, passes, a_bytes):
+    """Roofline of the dominant kernel (the pass over A, K1/K2), from the
+    CUDA events recorded around every pass inside the timed region."""
+    import torch
+    pass_ms = [a.elapsed_time(b) for a, b, *_ in pev]
+    flops_per = [f for _, _, f, _, _ in pev]
+    avg_pass_ms = sum(pass_ms) / len(pass_ms)
+    avg_flops = sum(flops_per) / len(flops_per)
+    pk, src = peaks()
+    if A.dtype in (torch.float64, torch.complex128):
+        peak_tf = measured_fp64_peak()
+        peak_src = "measured in-run: cuBLAS DGEMM 8192^3 (torch.matmul)"
+    else:
+        peak_tf = pk["bf16_tflops"]
+        peak_src = f"{src} bf16 (MEASURED_PEAKS.json)"
+    achieved_tf = avg_flops / (avg_pass_ms / 1e3) / 1e12
+    hbm = pk["hbm_gbs"]
+    # per-pass roofline: max(flops / tensor peak, bytes(A) / HBM)
+    roof_pass_s = max(avg_flops / (peak_tf * 1e12), a_bytes / (hbm * 1e9))
+    roof_step_ms = passes * roof_pass_s * 1e3
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get(f"cfg{cfg.idx}")
+    return {"bound": "tensor", "achieved": round(achieved_tf, 3), "peak": round(peak_tf, 3),
+            "unit": "TFLOP/s", "frac": round(achieved_tf / peak_tf, 4),
+            "traffic": traffic, "kernel": "lr_gemm pass over A (K1/K2)",
+            "peak_source": peak_src, "avg_pass_ms": round(avg_pass_ms, 4),
+            "pass_a_gbs": round(a_bytes / (avg_pass_ms / 1e3) / 1e9, 1),
+            "hbm_frac": round(a_bytes / (avg_pass_ms / 1e3) / 1e9 / hbm, 4),
+            "step_roofline_ms": round(roof_step_ms, 4),
+            "step_roofline_frac": round(roof_step_ms / ms, 4),
+            "pass_share_of_step": round(sum(pass_ms) / (ms * steps), 4)}
+
+
+def run_sharded(args, cfg):
+    """N GPUs, A split by rows (paper_0909_4061_b200.dist): Omega replicated,
+    Gram and n x ell partials all-reduced over NCCL.  Strong scaling: the
+    whole A is fixed, each rank holds m/N rows."""
+    import torch
+    import torch.distributed as dist
+    import paper_0909_4061_b200 as lr
+    from paper_0909_4061_b200 import core as lrcore
+    from paper_0909_4061_b200.dist import (Comm, GpuBackend, dist_randomized_svd, row_range,
+                                           sharded_randomized_svd)
+    rank, world, local = env_rank()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group("nccl", init_method="tcp://127.0.0.1:29533", rank=0,
+                                world_size=1, device_id=torch.device("cuda", local))
+    A_full = build_input(cfg)
+    r0, r1 = row_range(A_full.shape[0], rank, world)
+    A = A_full[r0:r1].contiguous()
+    m_total, n = A_full.shape
+    a_bytes_total = A_full.numel() * A_full.element_size()
+    del A_full
+    torch.cuda.empty_cache()
+    comm, be = Comm(), GpuBackend()
+    op = lr.DenseOperator(A)
+    amax = None
+    if A.dtype in (torch.float32, torch.complex64):
+        t = torch.tensor([op.amax], dtype=torch.float64, device="cuda")
+        amax = float(comm.allreduce_max(t).item())
+    passes = cfg.passes()
+    sketch = "srft" if cfg.sketch == "srft" else "gauss"
+
+    def step(estimate=False):
+        return dist_randomized_svd(A, n, cfg.k, cfg.p, cfg.q, cfg.seed, comm, be, amax=amax,
+                                   estimate=estimate, sketch=sketch)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    lrcore.PASS_EVENTS = []
+    l0 = lr._lib.launch_count()
+    with ClockSampler(local) as clk:
+        dist.barrier()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(args.steps):
+            step()
+        e.record()
+        torch.cuda.synchronize()
+        dist.barrier()
+    launches = lr._lib.launch_count() - l0
+    ms_local = s.elapsed_time(e) / args.steps
+    t = torch.tensor([ms_local], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    pev = lrcore.PASS_EVENTS
+    lrcore.PASS_EVENTS = None
+    a_bytes_local = A.numel() * A.element_size()
+    roof = roofline(A, cfg, pev, ms_local, args.steps, passes, a_bytes_local)
+
+    est_s, est_e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    est_s.record()
+    res = step(estimate=True)
+    est_e.record()
+    torch.cuda.synchronize()
+
+    line = {
+        "metric": "rank-k rSVD time & A-GB/s (% roofline) at 1/2/4/8 B200 vs host-CPU ref",
+        "value": round(passes * a_bytes_total / (ms / 1e3) / 1e9, 3), "unit": "A-GB/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": {torch.float64: "f64", torch.float32: "f32", torch.complex64: "c64",
+                  torch.complex128: "c128"}[A.dtype],
+        "data": "synthetic (seeded, BASELINE.json config recipe; see workloads.py)",
+        "config": {"workload": cfg.name, "config_index": cfg.idx, "m": m_total, "n": n,
+                   "k": cfg.k, "ell": cfg.ell, "q": cfg.q, "sketch": cfg.sketch,
+                   "passes": passes, "a_bytes": a_bytes_total, "rows_per_rank": r1 - r0,
+                   "l2": "inputs larger than L2 (A shard >= 126 MB), no flush",
+                   "parallelism": f"row-sharded x{world} (NCCL all-reduce of Gram and "
+                                  "n x ell partials)"},
+        "roofline": roof,
+        "rsvd_plus_estimate_ms_rank0": round(est_s.elapsed_time(est_e), 4),
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if not args.no_e2e:
+        host = torch.empty(A.shape, dtype=A.dtype, pin_memory=True)
+        host.copy_(A)
+        A_np = host.numpy()
+        k_e2e = max(1, min(args.steps, 5))
+        sharded_randomized_svd(A_np, cfg.k, cfg.p, cfg.q, cfg.seed, sketch=sketch,
+                               estimate=False)
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(k_e2e):
+            U, S, V, _ = sharded_randomized_svd(A_np, cfg.k, cfg.p, cfg.q, cfg.seed,
+                                                sketch=sketch, estimate=False)
+        dt = (time.perf_counter() - t0) / k_e2e
+        tt = torch.tensor([dt], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dt = float(tt.item())
+        line["e2e"] = {"value": round(passes * a_bytes_total / dt / 1e9, 3), "unit": "A-GB/s",
+                       "ms_per_step": round(dt * 1e3, 3),
+                       "h2d_bytes_per_step": int(a_bytes_total),
+                       "d2h_bytes_per_step": int(U.nbytes * world + S.nbytes + V.nbytes),
+                       "steps": k_e2e, "timing": "wall clock per rank, max over ranks"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
 
 
 def e2e_measure(args, cfg, A, lr):
