@@ -204,10 +204,12 @@ def run_ours(args, cfg):
             torch.distributed.barrier()
         torch.cuda.synchronize()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.nvtx.range_push("lr_timed")  # ncu --nvtx-include lr_timed/
         s.record()
         for _ in range(args.steps):
             step()
         e.record()
+        torch.cuda.nvtx.range_pop()
         torch.cuda.synchronize()
     launches = lr._lib.launch_count() - l0
     ms = s.elapsed_time(e) / args.steps
@@ -345,10 +347,12 @@ def run_sharded(args, cfg):
         dist.barrier()
         torch.cuda.synchronize()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.nvtx.range_push("lr_timed")  # ncu --nvtx-include lr_timed/
         s.record()
         for _ in range(args.steps):
             step()
         e.record()
+        torch.cuda.nvtx.range_pop()
         torch.cuda.synchronize()
         dist.barrier()
     launches = lr._lib.launch_count() - l0

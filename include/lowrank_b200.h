@@ -96,17 +96,21 @@ int lr_gemm_scaled(lr_handle_t h, int dtype, int op, int64_t m, int64_t n, int64
 int lr_gram(lr_handle_t h, int dtype, int64_t m, int64_t ell,
             const void* Y, int64_t ldy, void* G);
 
-/* Cholesky with column deletion on a Gram matrix (the rank decision of
- * orthonormalize_double_gs, reference core.py:104-106):
- *   pivot d_j <= drop_thr2           -> column j dropped
- *   pivot d_j <= unres_rel * G_jj    -> counted as unresolved (too small to
- *                                       be trusted from a Gram; caller falls back)
- * `shift` is added to the diagonal first (shifted CholeskyQR).
+/* Cholesky with column deletion on a Gram matrix G = Y^H Y (fp64 / c128,
+ * row-major) -- the rank decision of orthonormalize_double_gs (reference
+ * core.py:104-106); the pivot d_j is the squared residual of column j after
+ * projection onto the kept columns before it.  With t = trace(G) = ||Y||_F^2:
+ *   G_jj += shift_coef * t                 (shifted CholeskyQR; 0 = none)
+ *   d_j <= drop_tol^2 * t (or non-finite)  -> column j dropped
+ *   d_j <= unres_rel * G_jj (kept)         -> counted as unresolved (too small
+ *                                             to be trusted from a Gram; the
+ *                                             caller falls back to CGS2)
  * Outputs (device): P (ell x ell, row-major, ld ell): Q = Y . P[:, :rank];
  * R (ell x ell upper, kept rows/cols only, others 0); info[0] = rank,
- * info[1] = unresolved pivots, info[2] = non-positive pivots among kept. */
+ * info[1] = unresolved pivots, info[2] = non-finite pivots.  Async.  Used
+ * by the row-sharded path on an all-reduced G. */
 int lr_chol_drop(lr_handle_t h, int dtype, int64_t ell, const void* G,
-                 double drop_thr2, double unres_rel, double shift,
+                 double drop_tol, double unres_rel, double shift_coef,
                  void* P, void* R, int32_t* info);
 
 /* Orthonormalize the columns of Y (m x ell) -- replaces

@@ -270,9 +270,11 @@ def _timed_pass(A, X, Y, adjoint, amax=None):
         return
     torch = _torch()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.nvtx.range_push("lr_pass")      # ncu --nvtx-include lr_pass/
     s.record()
     _pass(A, X, Y, adjoint, amax)
     e.record()
+    torch.cuda.nvtx.range_pop()
     m, n = A.shape
     mult = 4 if A.is_complex() else 1
     PASS_EVENTS.append((s, e, 2 * mult * m * n * X.shape[1], A.numel() * A.element_size(),

@@ -16,9 +16,10 @@
 // forms 1/sqrt(d) with rsqrt (no divides on the critical path); the trailing
 // update uses the unscaled pivot row times 1/d and the scaling of row j is
 // deferred to step j+1.  The inverse X = R~^{-1} (R~ = R with dropped
-// rows/cols replaced by the identity) is formed right-looking into the lower
-// triangle (X^T), again one barrier per row, then scattered into P with the
-// kept columns compacted.
+// rows/cols replaced by the identity) is formed column by column, one warp
+// per column (independent back substitutions, no CTA barriers), into the
+// lower triangle (X^T), then scattered into P with the kept columns
+// compacted.
 //
 // Outputs: P (ell x ell): Q = Y . P[:, :rank] has orthonormal columns;
 // R (ell x ell) the factor restricted to kept rows/cols;
@@ -34,6 +35,11 @@ namespace {
 
 // 1/sqrt(d) to full double precision (MUFU seed + two Newton steps)
 __device__ __forceinline__ double rsqrt_full(double d) { return rsqrt(d); }
+
+// largest n whose n x n working matrix (+ per-column vectors) fits the
+// 227 KB opt-in shared memory of one CTA
+template <typename T>
+constexpr int smem_maxn() { return sizeof(T) == 8 ? 168 : 118; }
 
 template <typename T, bool SMEM, int CHOL_THREADS>
 __global__ void __launch_bounds__(CHOL_THREADS, 1)
@@ -58,6 +64,7 @@ chol_drop_kernel(int n, const T* __restrict__ G, double drop_tol, double unres_r
   int* kidx = pos + n;                                  // compact -> original
 
   constexpr int NW = CHOL_THREADS / 32;
+  constexpr int SMEM_MAXN = smem_maxn<T>();
   __shared__ double s_red[NW];
   __shared__ int s_unres, s_bad, s_rank;
 
@@ -109,10 +116,32 @@ chol_drop_kernel(int n, const T* __restrict__ G, double drop_tol, double unres_r
         if (d <= unres_rel * d0[j]) s_unres += 1;
       }
       const T* rowj = W + j * n;
-      for (int a = j + 1 + warp; a < n; a += NW) {
-        const T f = S::scale(S::conj(rowj[a]), invd);
-        T* rowa = W + a * n;
-        for (int b = a + lane; b < n; b += 32) rowa[b] = S::sub(rowa[b], S::mul(f, rowj[b]));
+      if constexpr (SMEM) {
+        // n <= SMEM_MAXN: every lane issues all its loads of a row before any
+        // store, so the shared-memory latencies overlap (the store/load
+        // aliasing otherwise serializes the row)
+        constexpr int MAXC = (SMEM_MAXN + 31) / 32;
+        for (int a = j + 1 + warp; a < n; a += NW) {
+          const T f = S::scale(S::conj(rowj[a]), invd);
+          T* rowa = W + a * n;
+          T rj[MAXC], ra[MAXC];
+#pragma unroll
+          for (int q = 0; q < MAXC; ++q) {
+            const int b = a + lane + 32 * q;
+            if (b < n) { rj[q] = rowj[b]; ra[q] = rowa[b]; }
+          }
+#pragma unroll
+          for (int q = 0; q < MAXC; ++q) {
+            const int b = a + lane + 32 * q;
+            if (b < n) rowa[b] = S::sub(ra[q], S::mul(f, rj[q]));
+          }
+        }
+      } else {
+        for (int a = j + 1 + warp; a < n; a += NW) {
+          const T f = S::scale(S::conj(rowj[a]), invd);
+          T* rowa = W + a * n;
+          for (int b = a + lane; b < n; b += 32) rowa[b] = S::sub(rowa[b], S::mul(f, rowj[b]));
+        }
       }
     } else if (tid == 0) {
       if (!fin) s_bad += 1;
@@ -151,26 +180,27 @@ chol_drop_kernel(int n, const T* __restrict__ G, double drop_tol, double unres_r
   }
   __syncthreads();
 
-  // 4. X = R~^{-1}, right-looking from the last row, one barrier per row
-  for (int k = n - 1; k >= -1; --k) {
-    if (k + 1 < n) {   // deferred scaling of row k+1 of X
-      const int p = k + 1;
-      const double inv = ri[p];
-      if (inv != 0.0)
-        for (int c = p + tid; c < n; c += CHOL_THREADS) W[c * n + p] = S::scale(W[c * n + p], inv);
-    }
-    if (k < 0) break;
-    const double inv = ri[k];
-    if (inv != 0.0) {
-      // X[i][c] -= R[i][k] * X[k][c] / r_kk   for i < k <= c
-      for (int c = k + warp; c < n; c += NW) {
-        T* xc = W + c * n;
+  // 4. X = R~^{-1}: the columns are independent triangular solves, so each
+  // warp back-substitutes whole columns on its own (column c in row c of the
+  // lower triangle, X[i][c] at W[c*n+i]) with only warp-level syncs; the
+  // 1/r_kk scaling of each entry is applied once at the end.
+  for (int c = n - 1 - warp; c >= 0; c -= NW) {
+    T* xc = W + c * n;
+    for (int k = c; k >= 1; --k) {
+      const double inv = ri[k];
+      if (inv != 0.0) {
+        // x_i -= R[i][k] * x_k / r_kk   for i < k
         const T xk = S::scale(xc[k], inv);
         for (int i = lane; i < k; i += 32) xc[i] = S::sub(xc[i], S::mul(W[i * n + k], xk));
       }
+      __syncwarp();
     }
-    __syncthreads();
+    for (int i = lane; i <= c; i += 32) {
+      const double inv = ri[i];
+      if (inv != 0.0) xc[i] = S::scale(xc[i], inv);
+    }
   }
+  __syncthreads();
 
   // 5. outputs
   for (int e = tid; e < n * n; e += CHOL_THREADS) {
@@ -210,7 +240,7 @@ void launch_chol(Handle* h, int64_t ell, const T* G, double drop_tol, double unr
   const size_t full = size_t(n) * n * sizeof(T) + tail;
   int max_smem = 0;
   LR_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device));
-  const bool in_smem = full <= size_t(max_smem) - 1024;
+  const bool in_smem = full <= size_t(max_smem) - 1024 && n <= smem_maxn<T>();
   // few warps: the kernel is latency-bound and per-column overhead is paid
   // by every warp, so small problems run fastest on 4 warps
   if (in_smem) {
@@ -225,7 +255,8 @@ void launch_chol(Handle* h, int64_t ell, const T* G, double drop_tol, double unr
       kern<<<1, threads, full, h->stream>>>(n, G, drop_tol, unres_rel, shift_coef, P, R, info,
                                             nullptr, h->status);
     };
-    if (nt <= 256) launch(chol_drop_kernel<T, true, 256>, 256);
+    if (nt <= 128) launch(chol_drop_kernel<T, true, 128>, 128);
+    else if (nt <= 256) launch(chol_drop_kernel<T, true, 256>, 256);
     else if (nt <= 512) launch(chol_drop_kernel<T, true, 512>, 512);
     else launch(chol_drop_kernel<T, true, 1024>, 1024);
   } else {
@@ -247,12 +278,21 @@ bool chol_blocked_launch(Handle* h, int64_t ell, const T* G, double drop_tol, do
 void chol_drop_f64(Handle* h, int64_t ell, const double* G, double drop_tol, double unres_rel,
                    double shift_coef, double* P, double* R, int32_t* info) {
   LR_REQUIRE(ell >= 1 && ell <= 4096, LR_EINVAL, "chol_drop: ell out of range [1, 4096]");
+  if (chol_tiled_supported(ell, false)) {
+    chol_tiled_f64(h, ell, G, drop_tol, unres_rel, shift_coef, P, R, info);
+    return;
+  }
   launch_chol<double>(h, ell, G, drop_tol, unres_rel, shift_coef, P, R, info);
 }
 
 void chol_drop_c128(Handle* h, int64_t ell, const double2* G, double drop_tol,
                     double unres_rel, double shift_coef, double2* P, double2* R,
                     int32_t* info) {
+  LR_REQUIRE(ell >= 1 && ell <= 4096, LR_EINVAL, "chol_drop: ell out of range [1, 4096]");
+  if (chol_tiled_supported(ell, true)) {
+    chol_tiled_c128(h, ell, G, drop_tol, unres_rel, shift_coef, P, R, info);
+    return;
+  }
   launch_chol<double2>(h, ell, G, drop_tol, unres_rel, shift_coef, P, R, info);
 }
 

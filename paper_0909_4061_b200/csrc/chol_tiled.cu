@@ -1,0 +1,283 @@
+// K3 core, register-tiled variant for ell <= 128 (the default there):
+// Cholesky with column deletion of a Gram matrix + the inverse of the kept
+// triangle, same contract and arithmetic as chol_drop_kernel (chol.cu) --
+// the rank decision of orthonormalize_double_gs, reference core.py:84-115.
+//
+// The earlier kernel kept the matrix in shared memory and had every warp walk
+// rows of the trailing matrix each step: ~7k warp-instructions per column,
+// instruction-issue bound (ncu: 56 % issue-busy, 180 us at ell = 110).  Here
+// the upper triangle lives in registers as 4x4 tiles, one thread per upper
+// tile (ell = 128: 528 threads).  Step j: the owners of row j publish it to a
+// double-buffered shared row (one barrier per step), every thread reads the
+// pivot and its 4 + 4 row entries and updates its 16 elements.  The scaled R
+// rows go to a transposed copy Rt (shared memory when it fits), from which
+// the inverse X = R~^{-1} is formed column by column, one warp per column,
+// the column held in registers (4 rows per lane) and x_k broadcast with a
+// shuffle -- no CTA barriers in the solve.
+#include <cstdlib>
+
+#include "common.cuh"
+#include "scalar.cuh"
+
+namespace lr {
+namespace {
+
+constexpr int TS = 4;       // tile size
+constexpr int MAXN = 128;   // 4 rows per lane in the solve
+
+template <int ITER>
+__device__ __forceinline__ double rsqrt_newton(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+#pragma unroll
+  for (int i = 0; i < ITER; ++i) y = y * fma(-0.5 * x, y * y, 1.5);
+  return y;
+}
+
+// shared-memory header (row buffers, pivots, compaction), 16-byte rounded
+__host__ __device__ constexpr size_t head_bytes(int n, size_t esz) {
+  return (size_t(2 * n) * esz + size_t(3 * n) * sizeof(double) + size_t(n) * sizeof(int) + 15) &
+         ~size_t(15);
+}
+
+template <typename T>
+__device__ __forceinline__ T sel4(const T (&v)[4], int i) {
+  return i == 0 ? v[0] : i == 1 ? v[1] : i == 2 ? v[2] : v[3];
+}
+
+template <typename T, bool RT_SMEM, int MAXT>
+__global__ void __launch_bounds__(MAXT, 1)   // MAXT >= 32 * ceil(tiles / 32)
+chol_tiled_kernel(int n, const T* __restrict__ G, double drop_tol, double unres_rel,
+                  double shift_coef, T* __restrict__ P, T* __restrict__ Rout,
+                  int32_t* __restrict__ info, T* __restrict__ gRt, int32_t* status) {
+  using S = Sc<T>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* rowbuf = reinterpret_cast<T*>(smem_raw);            // [2][n]
+  double* d0 = reinterpret_cast<double*>(rowbuf + 2 * n);  // shifted diagonal
+  double* rd = d0 + n;                                    // R diagonal (0 = dropped)
+  double* ri = rd + n;                                    // 1 / R diagonal (0 = dropped)
+  int* pos = reinterpret_cast<int*>(ri + n);              // compact index or -1
+  T* Rt = RT_SMEM ? reinterpret_cast<T*>(smem_raw + head_bytes(n, sizeof(T))) : gRt;
+
+  __shared__ double s_trace;
+  __shared__ int s_unres, s_bad, s_rank;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const int nt = (n + TS - 1) / TS;
+  const int ntiles = nt * (nt + 1) / 2;
+
+  // my tile (ti <= tj)
+  int ti = 0, rem = tid;
+  while (ti < nt && rem >= nt - ti) { rem -= nt - ti; ++ti; }
+  const bool owner = tid < ntiles;
+  const int tj = ti + rem;
+  const int r0 = TS * ti, c0 = TS * tj;
+
+  if (warp == 0) {
+    double tr = 0.0;
+    for (int i = lane; i < n; i += 32) tr += S::re(G[size_t(i) * n + i]);
+#pragma unroll
+    for (int m = 16; m > 0; m >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, m);
+    if (lane == 0) { s_trace = tr; s_unres = 0; s_bad = 0; }
+  }
+  __syncthreads();
+  const double trace = s_trace;
+  const double thr2 = drop_tol * drop_tol * trace;
+  const double shift = shift_coef * trace;
+
+  T w[TS][TS];
+#pragma unroll
+  for (int a = 0; a < TS; ++a)
+#pragma unroll
+    for (int b = 0; b < TS; ++b) {
+      const int i = r0 + a, k = c0 + b;
+      T v = S::zero();
+      if (owner && i < n && k < n && k >= i) v = G[size_t(i) * n + k];
+      if (owner && i == k && i < n) {
+        v = S::make(S::re(v) + shift, 0.0);
+        d0[i] = S::re(v);
+      }
+      w[a][b] = v;
+    }
+
+  // right-looking factorization, one barrier per column
+  for (int j = 0; j < n; ++j) {
+    T* rb = rowbuf + (j & 1) * n;
+    if (owner && ti == j / TS) {
+      const int a = j % TS;
+#pragma unroll
+      for (int aa = 0; aa < TS; ++aa) {
+        if (aa != a) continue;
+#pragma unroll
+        for (int b = 0; b < TS; ++b) {
+          const int k = c0 + b;
+          if (k >= j && k < n) rb[k] = w[aa][b];
+        }
+      }
+    }
+    __syncthreads();
+    const double d = S::re(rb[j]);
+    const bool fin = isfinite(d);
+    const bool keep = fin && d > thr2 && d > 0.0;
+    const double iv = keep ? rsqrt_newton<2>(d) : 0.0;
+    if (tid == 0) {
+      rd[j] = keep ? d * iv : 0.0;
+      ri[j] = iv;
+      if (keep && d <= unres_rel * d0[j]) s_unres += 1;
+      if (!fin) s_bad += 1;
+    }
+    // R row j (scaled), transposed: Rt[k*n + j] = R_jk, k > j (0 if dropped)
+    if (owner && ti == j / TS) {
+#pragma unroll
+      for (int b = 0; b < TS; ++b) {
+        const int k = c0 + b;
+        if (k > j && k < n) Rt[size_t(k) * n + j] = S::scale(rb[k], iv);
+      }
+    }
+    if (keep && owner && c0 + TS - 1 > j) {
+      const double invd = iv * iv;
+      T fr[TS], rc[TS];
+#pragma unroll
+      for (int a = 0; a < TS; ++a) {
+        const int i = r0 + a;
+        fr[a] = (i > j && i < n) ? S::scale(S::conj(rb[i]), invd) : S::zero();
+      }
+#pragma unroll
+      for (int b = 0; b < TS; ++b) {
+        const int k = c0 + b;
+        rc[b] = (k > j && k < n) ? rb[k] : S::zero();
+      }
+#pragma unroll
+      for (int a = 0; a < TS; ++a)
+#pragma unroll
+        for (int b = 0; b < TS; ++b) w[a][b] = S::sub(w[a][b], S::mul(fr[a], rc[b]));
+    }
+  }
+  __syncthreads();
+
+  // compaction of the kept pivots
+  if (warp == 0) {
+    int base = 0;
+    for (int j0 = 0; j0 < n; j0 += 32) {
+      const int j = j0 + lane;
+      const bool k = j < n && rd[j] > 0.0;
+      const unsigned bal = __ballot_sync(0xffffffffu, k);
+      if (j < n) pos[j] = k ? base + __popc(bal & ((1u << lane) - 1u)) : -1;
+      base += __popc(bal);
+    }
+    if (lane == 0) s_rank = base;
+  }
+  __syncthreads();
+  const int rank = s_rank;
+  // R output (kept rows/cols only) and P cleared
+  for (int e = tid; e < n * n; e += blockDim.x) {
+    const int i = e / n, k = e - i * n;
+    T r = S::zero();
+    if (pos[i] >= 0 && pos[k] >= 0) {
+      if (k > i) r = Rt[size_t(k) * n + i];
+      else if (k == i) r = S::make(rd[i], 0.0);
+    }
+    Rout[e] = r;
+    P[e] = S::zero();
+  }
+  // R~ has the identity in dropped rows/cols: zero R entries touching them
+  if (rank < n) {
+    for (int e = tid; e < n * n; e += blockDim.x) {
+      const int k = e / n, i = e - k * n;   // Rt[k][i] = R_ik, i < k
+      if (i < k && (pos[i] < 0 || pos[k] < 0)) Rt[e] = S::zero();
+    }
+  }
+  __syncthreads();
+
+  // X = R~^{-1}, one warp per column c, x in registers (row lane + 32 r)
+  for (int c = n - 1 - warp; c >= 0; c -= nwarps) {
+    if (pos[c] < 0) continue;
+    T x[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) x[r] = (lane + 32 * r == c) ? S::one() : S::zero();
+    for (int k = c; k >= 1; --k) {
+      const double inv = ri[k];
+      const T xk = S::scale(S::shfl_idx(sel4(x, k >> 5), k & 31), inv);
+      if (inv != 0.0) {
+        const T* rk = Rt + size_t(k) * n;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int i = lane + 32 * r;
+          if (i < k) x[r] = S::sub(x[r], S::mul(rk[i], xk));
+        }
+      }
+    }
+    const int pc = pos[c];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int i = lane + 32 * r;
+      if (i <= c) {
+        const double inv = ri[i];
+        if (inv != 0.0) P[size_t(i) * n + pc] = S::scale(x[r], inv);
+      }
+    }
+  }
+  if (tid == 0) {
+    info[0] = rank;
+    info[1] = s_unres;
+    info[2] = s_bad;
+    if (status) {
+      const int bits = (s_unres ? 1 : 0) | (rank < n ? 2 : 0) | (s_bad ? 4 : 0);
+      if (bits) atomicOr(status, bits);
+    }
+  }
+}
+
+template <typename T>
+void launch(Handle* h, int n, const T* G, double drop_tol, double unres_rel, double shift_coef,
+            T* P, T* R, int32_t* info) {
+  const int nt = (n + TS - 1) / TS;
+  const int threads = ((nt * (nt + 1) / 2 + 31) / 32) * 32;
+  const size_t head = head_bytes(n, sizeof(T));
+  const size_t rt = size_t(n) * n * sizeof(T);
+  const bool in_smem = head + rt <= 200 * 1024;
+  // the register budget is 64K / threads: complex tiles (32 doubles) fit
+  // without spills up to 320 threads (ell <= 96)
+  T* gRt = in_smem ? nullptr : pool_alloc_t<T>(h, size_t(n) * n);
+  const size_t smem = in_smem ? head + rt : head;
+  auto go = [&](auto kern) {
+    LR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    kern<<<1, threads, smem, h->stream>>>(n, G, drop_tol, unres_rel, shift_coef, P, R, info, gRt,
+                                          h->status);
+  };
+  if (threads <= 320) {
+    if (in_smem) go(chol_tiled_kernel<T, true, 320>);
+    else go(chol_tiled_kernel<T, false, 320>);
+  } else {
+    if (in_smem) go(chol_tiled_kernel<T, true, 544>);
+    else go(chol_tiled_kernel<T, false, 544>);
+  }
+  LR_CHECK_LAUNCH();
+}
+
+}  // namespace
+
+// Measured on B200 (tools/small_probe.py, CUDA-graph timed): the tiled
+// kernel wins from ell ~ 80 (real: 133 vs 178 us at 110, 163 vs 380 us at
+// 128) and for complex above 64 (336 vs 443 us at 120); below that the
+// 1024-thread shared-memory kernel is faster.
+bool chol_tiled_supported(int64_t n, bool cplx) {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("LR_CHOL");   // smem | tiled | (unset: by size)
+    mode = !e ? 0 : (e[0] == 's' ? 1 : 2);
+  }
+  if (n < 1 || n > MAXN || mode == 1) return false;
+  return mode == 2 || n >= (cplx ? 65 : 80);
+}
+
+void chol_tiled_f64(Handle* h, int64_t n, const double* G, double drop_tol, double unres_rel,
+                    double shift_coef, double* P, double* R, int32_t* info) {
+  launch<double>(h, int(n), G, drop_tol, unres_rel, shift_coef, P, R, info);
+}
+
+void chol_tiled_c128(Handle* h, int64_t n, const double2* G, double drop_tol, double unres_rel,
+                     double shift_coef, double2* P, double2* R, int32_t* info) {
+  launch<double2>(h, int(n), G, drop_tol, unres_rel, shift_coef, P, R, info);
+}
+
+}  // namespace lr

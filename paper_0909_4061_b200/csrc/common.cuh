@@ -146,6 +146,20 @@ void jacobi_svd_f64(Handle* h, int64_t rows, int64_t n, const double* M, double*
 void jacobi_svd_c128(Handle* h, int64_t rows, int64_t n, const double2* M, double2* W,
                      double* S, double2* J, int32_t* info);
 
+// chol_tiled.cu: register-tiled Cholesky with deletion for ell <= 128
+// (by size; LR_CHOL=smem|tiled forces one kernel)
+bool chol_tiled_supported(int64_t n, bool cplx);
+void chol_tiled_f64(Handle* h, int64_t n, const double* G, double drop_tol, double unres_rel,
+                    double shift_coef, double* P, double* R, int32_t* info);
+void chol_tiled_c128(Handle* h, int64_t n, const double2* G, double drop_tol, double unres_rel,
+                     double shift_coef, double2* P, double2* R, int32_t* info);
+// jacobi_blk.cu: block variant of the register-resident Jacobi (default;
+// LR_JACOBI=round selects the column round-robin kernel of jacobi_reg.cu)
+bool jacobi_blk_enabled();
+void jacobi_blk_f64(Handle* h, int64_t n, const double* R, double* Mout, double* sig,
+                    int32_t* info);
+void jacobi_blk_c128(Handle* h, int64_t n, const double2* R, double2* Mout, double* sig,
+                     int32_t* info);
 // jacobi_reg.cu: register-resident Jacobi (R J = M, M unsorted) + finalize
 bool jacobi_reg_supported(int64_t n, bool cplx);
 void jacobi_reg_f64(Handle* h, int64_t n, const double* R, double* Mout, double* sig,

@@ -17,6 +17,9 @@
 // re-orthonormalized by one CholeskyQR pass, which halves the per-round
 // work and register footprint.  svd_finalize sorts, applies the reference
 // sign convention (core.py:221-229) and normalizes W.
+#include <cstdio>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "scalar.cuh"
 
@@ -256,19 +259,43 @@ void launch_reg(Handle* h, int n, const T* R, T* Mout, double* sig, int32_t* inf
 
 }  // namespace
 
+// LR_DEBUG_JACOBI=1: report the sweep count of every register-resident
+// Jacobi launch on stderr (synchronizes; development only)
+void debug_sweeps(Handle* h, const int32_t* info, int64_t n, const char* kind) {
+  static int dbg = -1;
+  if (dbg < 0) dbg = getenv("LR_DEBUG_JACOBI") ? 1 : 0;
+  if (!dbg) return;
+  int32_t v = 0;
+  LR_CUDA(cudaMemcpyAsync(&v, info, sizeof(v), cudaMemcpyDeviceToHost, h->stream));
+  LR_CUDA(cudaStreamSynchronize(h->stream));
+  fprintf(stderr, "[lr] jacobi %s n=%lld sweeps=%d\n", kind, (long long)n, v);
+}
+
 bool jacobi_reg_supported(int64_t n, bool cplx) { return n >= 2 && n <= (cplx ? 64 : 128); }
 
 void jacobi_reg_f64(Handle* h, int64_t n, const double* R, double* Mout, double* sig,
                     int32_t* info) {
+  if (jacobi_blk_enabled()) {
+    jacobi_blk_f64(h, n, R, Mout, sig, info);
+    debug_sweeps(h, info, n, "blk");
+    return;
+  }
   if (n <= 32) launch_reg<double, 32, 1>(h, int(n), R, Mout, sig, info);
   else if (n <= 64) launch_reg<double, 32, 2>(h, int(n), R, Mout, sig, info);
   else launch_reg<double, 16, 8>(h, int(n), R, Mout, sig, info);
+  debug_sweeps(h, info, n, "round");
 }
 
 void jacobi_reg_c128(Handle* h, int64_t n, const double2* R, double2* Mout, double* sig,
                      int32_t* info) {
+  if (jacobi_blk_enabled()) {
+    jacobi_blk_c128(h, n, R, Mout, sig, info);
+    debug_sweeps(h, info, n, "blk");
+    return;
+  }
   if (n <= 32) launch_reg<double2, 32, 1>(h, int(n), R, Mout, sig, info);
   else launch_reg<double2, 32, 2>(h, int(n), R, Mout, sig, info);
+  debug_sweeps(h, info, n, "round");
 }
 
 void svd_finalize(Handle* h, int dtype_wide, int64_t n, const void* Jun, const void* Mun,
