@@ -73,7 +73,8 @@ void gram_any(Handle* h, int dtype, int64_t m, int64_t ell, const void* Y, int64
                 static_cast<const double2*>(Y), ldy, static_cast<double2*>(G), ell);
       return;
     case LR_F32:
-      gram_f32(h, m, ell, static_cast<const float*>(Y), ldy, static_cast<double*>(G));
+      gemm_f64_from_f32(h, true, ell, ell, m, static_cast<const float*>(Y), ldy,
+                        static_cast<const float*>(Y), ldy, static_cast<double*>(G), ell);
       return;
     case LR_C64:
       gram_c64(h, m, ell, static_cast<const float2*>(Y), ldy, static_cast<double2*>(G));

@@ -53,12 +53,18 @@ void gemm_f32_hint(Handle* h, bool transA, int64_t M, int64_t N, int64_t K, cons
   gemm_f32_simt(h, transA, M, N, K, A, lda, B, ldb, C, ldc);
 }
 
-// generic fp32 products (orthonormalization applies, small GEMMs): honest
-// fp32 SIMT -- per-tensor fp16 scaling is not safe for operands whose
-// columns span many orders of magnitude (e.g. R^{-1} of an ill-conditioned
-// panel), so the tensor-core split is reserved for passes over A.
+// generic fp32 products (orthonormalization applies Y R^{-1}, U = Q U~,
+// Q^T Z): large ones on the tcgen05 split with a device-side max|A| scale
+// and per-column scales of B (so the columns of an ill-conditioned R^{-1}
+// keep their low fp16 pieces); small ones on the SIMT kernel.
 void gemm_f32(Handle* h, bool transA, int64_t M, int64_t N, int64_t K, const float* A,
               int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc) {
+  const bool big = double(M) * double(N) * double(K) >= double(1 << 26) &&
+                   (transA ? K : M) >= 1024;
+  if (big && h->f32_mode == LR_F32_SPLIT3 && gemm_f32_tc_supported(transA, N, A, lda)) {
+    gemm_f32_tc(h, transA, M, N, K, A, lda, -1.0, B, ldb, C, ldc);
+    return;
+  }
   gemm_f32_simt(h, transA, M, N, K, A, lda, B, ldb, C, ldc);
 }
 

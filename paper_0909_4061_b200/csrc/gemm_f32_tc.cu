@@ -120,7 +120,8 @@ __global__ void __launch_bounds__(TTHREADS, 1)
 gemm_f32_tc_kernel(const __grid_constant__ CUtensorMap mapA,
                    const __grid_constant__ CUtensorMap mapBhi,
                    const __grid_constant__ CUtensorMap mapBlo, int M, int N, int BN,
-                   int64_t k_per_split, int64_t K, float sA, const float* __restrict__ sB_dev,
+                   int64_t k_per_split, int64_t K, float sA_host,
+                   const float* __restrict__ sA_dev, const float* __restrict__ sB_dev,
                    float* __restrict__ C, int64_t ldc, int64_t cstride) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-align the dynamic smem base
@@ -144,6 +145,7 @@ gemm_f32_tc_kernel(const __grid_constant__ CUtensorMap mapA,
   auto blo = [&](int s) { return base + s * stage_bytes + A32_BYTES + 2 * AH_BYTES + B_BYTES; };
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const float sA = sA_dev ? *sA_dev : sA_host;
   const int m0 = blockIdx.x * TBM;
   const int64_t kbeg = int64_t(blockIdx.z) * k_per_split;
   const int64_t kend = min(K, kbeg + k_per_split);
@@ -186,8 +188,9 @@ gemm_f32_tc_kernel(const __grid_constant__ CUtensorMap mapA,
         else        tma_load_2d(a32(s), &mapA, &a32_full[s], m0, kc);
         mbar_wait(&st_empty[s], ph ^ 1u);
         mbar_expect_tx(&b_full[s], bbytes);
-        tma_load_2d(bhi(s), &mapBhi, &b_full[s], kc, 0);
-        tma_load_2d(blo(s), &mapBlo, &b_full[s], kc, 0);
+        // X hi/lo are K-blocked: block kb = kc / 32 is BN contiguous rows of 64 B
+        tma_load_2d(bhi(s), &mapBhi, &b_full[s], 0, (kc / TBK) * BN);
+        tma_load_2d(blo(s), &mapBlo, &b_full[s], 0, (kc / TBK) * BN);
       }
     }
   } else if (warp == 1) {
@@ -246,29 +249,38 @@ gemm_f32_tc_kernel(const __grid_constant__ CUtensorMap mapA,
       __syncwarp();
       if (lane == 0) mbar_arrive(&ahl_full[s]);
     }
-    // epilogue
+    // epilogue: TMEM -> registers (row per thread) -> per-warp shared
+    // transpose (the ring is idle now) -> coalesced 128-B row stores
     mbar_wait(acc_full, 0);
     asm volatile("tcgen05.fence::after_thread_sync;");
-    const float inv = 1.0f / (sA * sB_dev[0]);
+    const float inv_a = 1.0f / sA;
     const int q = warp - 4;                    // TMEM lane quarter
-    const int row = m0 + q * 32 + lane;
-    float* crow = C + int64_t(blockIdx.z) * cstride + int64_t(row) * ldc;
-    for (int c0 = 0; c0 < BN; c0 += 16) {
-      uint32_t d[16];
+    float* wbuf = reinterpret_cast<float*>(base) + q * (32 * 33);
+    float* cbase = C + int64_t(blockIdx.z) * cstride;
+    for (int c0 = 0; c0 < BN; c0 += 32) {
+      uint32_t d[32];
       const uint32_t taddr = tmem + (uint32_t(q * 32) << 16) + uint32_t(c0);
       asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
-          "%14,%15}, [%16];"
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+          "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
           : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]),
             "=r"(d[7]), "=r"(d[8]), "=r"(d[9]), "=r"(d[10]), "=r"(d[11]), "=r"(d[12]),
-            "=r"(d[13]), "=r"(d[14]), "=r"(d[15])
+            "=r"(d[13]), "=r"(d[14]), "=r"(d[15]), "=r"(d[16]), "=r"(d[17]), "=r"(d[18]),
+            "=r"(d[19]), "=r"(d[20]), "=r"(d[21]), "=r"(d[22]), "=r"(d[23]), "=r"(d[24]),
+            "=r"(d[25]), "=r"(d[26]), "=r"(d[27]), "=r"(d[28]), "=r"(d[29]), "=r"(d[30]),
+            "=r"(d[31])
           : "r"(taddr));
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      if (row < M) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
-          if (c0 + j < N) crow[c0 + j] = __uint_as_float(d[j]) * inv;
+      for (int j = 0; j < 32; ++j) wbuf[lane * 33 + j] = __uint_as_float(d[j]);
+      __syncwarp();
+      const int col = c0 + lane;
+      const float sc = col < N ? inv_a / sB_dev[col] : 0.f;
+      for (int rr = 0; rr < 32; ++rr) {
+        const int row = m0 + q * 32 + rr;
+        if (row < M && col < N) cbase[int64_t(row) * ldc + col] = wbuf[rr * 33 + lane] * sc;
       }
+      __syncwarp();
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -300,17 +312,45 @@ __device__ __forceinline__ float pow2_scale(float amax) {
   return ldexpf(1.f, 14 - e);
 }
 
+// per-column power-of-two scales of X (K x N): one warp per column.  A
+// per-tensor scale is not enough for operands whose columns differ by orders
+// of magnitude (R^{-1} of an ill-conditioned panel): small columns would
+// lose their low fp16 piece to underflow.
+__global__ void col_amax_kernel(int64_t K, int64_t N, const float* __restrict__ X, int64_t ld,
+                                unsigned int* __restrict__ bits) {
+  // rows split over blocks, columns over threads: coalesced row reads
+  const int64_t rows_per = (K + gridDim.x - 1) / gridDim.x;
+  const int64_t k0 = blockIdx.x * rows_per, k1 = min(K, k0 + rows_per);
+  for (int64_t n = threadIdx.x; n < N; n += blockDim.x) {
+    float mx = 0.f;
+    for (int64_t k = k0; k < k1; ++k) mx = fmaxf(mx, fabsf(X[k * ld + n]));
+    if (mx > 0.f) atomicMax(bits + n, __float_as_uint(mx));
+  }
+}
+
 __global__ void make_scale_kernel(const unsigned int* bits, float* scale) {
   scale[0] = pow2_scale(__uint_as_float(bits[0]));
 }
 
-// X (K x N row-major, ld) -> hi/lo (N x Kp fp16, K-major), scaled by *scale
+__global__ void col_scale_kernel(int64_t N, const unsigned int* __restrict__ bits,
+                                 float* __restrict__ scale) {
+  for (int64_t n = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; n < N;
+       n += int64_t(gridDim.x) * blockDim.x)
+    scale[n] = pow2_scale(__uint_as_float(bits[n]));
+}
+
+// X (K x N row-major, ld) -> hi/lo fp16, column n scaled by scale[n], in the
+// K-blocked K-major layout the MMA reads: block kb (32 k) holds BN rows of 64 B,
+// element (n, k) at ((k / 32) * BN + n) * 32 + k % 32, so every k-stage of X
+// is one contiguous TMA box (a plain N x K layout puts the rows of one stage
+// K * 2 bytes apart -- 2 MB for A^T Y of config 4).
 __global__ void split_transpose_kernel(int64_t K, int64_t N, const float* __restrict__ X,
-                                       int64_t ld, int64_t Kp, const float* __restrict__ scale,
+                                       int64_t ld, int64_t Kp, int BN,
+                                       const float* __restrict__ scale,
                                        __half* __restrict__ hi, __half* __restrict__ lo) {
   __shared__ float tile[32][33];
-  const float s = scale[0];
   const int64_t k0 = int64_t(blockIdx.x) * 32, n0 = int64_t(blockIdx.y) * 32;
+  const float s = (n0 + threadIdx.x < N) ? scale[n0 + threadIdx.x] : 1.f;
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
     const int64_t k = k0 + i, n = n0 + threadIdx.x;
     tile[i][threadIdx.x] = (k < K && n < N) ? X[k * ld + n] * s : 0.f;
@@ -321,8 +361,9 @@ __global__ void split_transpose_kernel(int64_t K, int64_t N, const float* __rest
     if (n < N && k < Kp) {
       const float v = tile[threadIdx.x][i];
       const __half h = __float2half_rn(v);
-      hi[n * Kp + k] = h;
-      lo[n * Kp + k] = __float2half_rn(v - __half2float(h));
+      const int64_t o = ((k >> 5) * BN + n) * 32 + (k & 31);
+      hi[o] = h;
+      lo[o] = __float2half_rn(v - __half2float(h));
     }
   }
 }
@@ -379,35 +420,38 @@ void gemm_f32_tc(Handle* h, bool transA, int64_t M, int64_t N, int64_t K, const 
   if (M == 0 || N == 0) return;
   LR_REQUIRE(gemm_f32_tc_supported(transA, N, A, lda), LR_EUNSUPPORTED,
              "gemm_f32_tc: unsupported shape/alignment");
-  // scales: s_A on the host (from the operator's max|A|), s_B on the device
+  // scales: s_A on the host (from the operator's max|A|), per-column s_B on
+  // the device
   unsigned int* bits = pool_alloc_t<unsigned int>(h, 4);
-  float* sB = reinterpret_cast<float*>(bits + 2);
+  float* sB = pool_alloc_t<float>(h, size_t(N));
   float sA = 1.f;
+  float* sA_dev = nullptr;
   if (a_amax < 0) {
+    // unknown max|A|: reduce it on the device (no host synchronization)
+    sA_dev = reinterpret_cast<float*>(bits + 2);
     LR_CUDA(cudaMemsetAsync(bits + 1, 0, sizeof(unsigned int), h->stream));
     const int64_t rows = transA ? K : M, cols = transA ? M : K;
     amax_f32_kernel<<<h->sm_count * 8, 256, 0, h->stream>>>(rows, cols, A, lda, bits + 1);
     LR_CHECK_LAUNCH();
-    unsigned int hb = 0;
-    LR_CUDA(cudaMemcpyAsync(&hb, bits + 1, sizeof(hb), cudaMemcpyDeviceToHost, h->stream));
-    LR_CUDA(cudaStreamSynchronize(h->stream));
-    float f;
-    memcpy(&f, &hb, sizeof(f));
-    a_amax = f;
-  }
-  if (a_amax > 0 && std::isfinite(a_amax)) {
+    make_scale_kernel<<<1, 1, 0, h->stream>>>(bits + 1, sA_dev);
+    LR_CHECK_LAUNCH();
+  } else if (a_amax > 0 && std::isfinite(a_amax)) {
     int e;
     std::frexp(a_amax, &e);
     sA = std::ldexp(1.f, 14 - e);
   }
-  LR_CUDA(cudaMemsetAsync(bits, 0, sizeof(unsigned int), h->stream));
-  amax_f32_kernel<<<std::max<int64_t>(1, std::min<int64_t>(ceil_div(K * N, 256), 4096)), 256, 0,
-                    h->stream>>>(K, N, B, ldb, bits);
-  LR_CHECK_LAUNCH();
-  make_scale_kernel<<<1, 1, 0, h->stream>>>(bits, sB);
-  LR_CHECK_LAUNCH();
+  {
+    unsigned int* cb = pool_alloc_t<unsigned int>(h, size_t(N));
+    LR_CUDA(cudaMemsetAsync(cb, 0, sizeof(unsigned int) * N, h->stream));
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(ceil_div(K, 64),
+                                                                  int64_t(h->sm_count) * 8));
+    col_amax_kernel<<<unsigned(blocks), 256, 0, h->stream>>>(K, N, B, ldb, cb);
+    LR_CHECK_LAUNCH();
+    col_scale_kernel<<<unsigned(ceil_div(N, 256)), 256, 0, h->stream>>>(N, cb, sB);
+    LR_CHECK_LAUNCH();
+  }
   const int BN = int(ceil_div(N, 16) * 16);
-  const int64_t Kp = ceil_div(K, 8) * 8;
+  const int64_t Kp = ceil_div(K, TBK) * TBK;
   __half* Bhi = pool_alloc_t<__half>(h, size_t(BN) * Kp);
   __half* Blo = pool_alloc_t<__half>(h, size_t(BN) * Kp);
   if (BN != N) {
@@ -416,7 +460,8 @@ void gemm_f32_tc(Handle* h, bool transA, int64_t M, int64_t N, int64_t K, const 
   }
   {
     dim3 grid(unsigned(ceil_div(Kp, 32)), unsigned(ceil_div(N, 32)));
-    split_transpose_kernel<<<grid, dim3(32, 8), 0, h->stream>>>(K, N, B, ldb, Kp, sB, Bhi, Blo);
+    split_transpose_kernel<<<grid, dim3(32, 8), 0, h->stream>>>(K, N, B, ldb, Kp, BN, sB, Bhi,
+                                                                 Blo);
     LR_CHECK_LAUNCH();
   }
   CUtensorMap mapA = transA
@@ -424,10 +469,11 @@ void gemm_f32_tc(Handle* h, bool transA, int64_t M, int64_t N, int64_t K, const 
                     TBM, TBK, CU_TENSOR_MAP_SWIZZLE_NONE)
       : make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, A, uint64_t(K), uint64_t(M), uint64_t(lda) * 4,
                     TBK, TBM, CU_TENSOR_MAP_SWIZZLE_128B);
-  CUtensorMap mapBh = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT16, Bhi, uint64_t(Kp), uint64_t(BN),
-                                  uint64_t(Kp) * 2, TBK, uint32_t(BN), CU_TENSOR_MAP_SWIZZLE_64B);
-  CUtensorMap mapBl = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT16, Blo, uint64_t(Kp), uint64_t(BN),
-                                  uint64_t(Kp) * 2, TBK, uint32_t(BN), CU_TENSOR_MAP_SWIZZLE_64B);
+  const uint64_t brows = uint64_t(Kp / TBK) * BN;   // K-blocked: 64-B rows
+  CUtensorMap mapBh = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT16, Bhi, TBK, brows, TBK * 2, TBK,
+                                  uint32_t(BN), CU_TENSOR_MAP_SWIZZLE_64B);
+  CUtensorMap mapBl = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT16, Blo, TBK, brows, TBK * 2, TBK,
+                                  uint32_t(BN), CU_TENSOR_MAP_SWIZZLE_64B);
   const int stage_bytes = A32_BYTES + 2 * AH_BYTES + 2 * BN * TBK * 2;
   // One CTA per SM: with two co-resident CTAs (N <= 128 fits twice) some
   // output rows came out wrong on B200 (tools/tc_probe2.py); until that is
@@ -454,12 +500,12 @@ void gemm_f32_tc(Handle* h, bool transA, int64_t M, int64_t N, int64_t K, const 
     auto kern = gemm_f32_tc_kernel<true>;
     LR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     kern<<<grid, TTHREADS, smem, h->stream>>>(mapA, mapBh, mapBl, int(M), int(N), BN, kps, K, sA,
-                                              sB, out, ldo, cstride);
+                                              sA_dev, sB, out, ldo, cstride);
   } else {
     auto kern = gemm_f32_tc_kernel<false>;
     LR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     kern<<<grid, TTHREADS, smem, h->stream>>>(mapA, mapBh, mapBl, int(M), int(N), BN, kps, K, sA,
-                                              sB, out, ldo, cstride);
+                                              sA_dev, sB, out, ldo, cstride);
   }
   LR_CHECK_LAUNCH();
   if (splits > 1) {

@@ -25,13 +25,13 @@ constexpr int THREADS = 256;
 constexpr int AS_NN = BK + 4;    // row stride (f64) of the A tile, non-transposed
 constexpr int AS_TN = BM + 4;    // row stride of the A tile, transposed
 
-template <int NF>
+template <int NF, typename TIN = double>
 struct Smem {
   static constexpr int BN = 16 * NF;
   static constexpr int BS = BN + 4;
   static constexpr int A_ELEMS = (BM * AS_NN > BK * AS_TN) ? BM * AS_NN : BK * AS_TN;
   static constexpr int B_ELEMS = BK * BS;
-  static constexpr size_t bytes = size_t(STAGES) * (A_ELEMS + B_ELEMS) * sizeof(double);
+  static constexpr size_t bytes = size_t(STAGES) * (A_ELEMS + B_ELEMS) * sizeof(TIN);
 };
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
@@ -43,6 +43,16 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, int src_
   unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem),
                "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem, int src_bytes) {
+  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(gmem),
+               "r"(src_bytes));
+}
+template <typename TIN>
+__device__ __forceinline__ void cp_async_elem(TIN* smem, const TIN* gmem, int valid) {
+  if constexpr (sizeof(TIN) == 8) cp_async8(smem, gmem, valid * 8);
+  else cp_async4(smem, gmem, valid * 4);
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
@@ -58,38 +68,42 @@ __device__ __forceinline__ void dmma(double (&c)[4], double a0, double a1, doubl
       : "d"(a0), "d"(a1), "d"(b0));
 }
 
-// Copy a rows x cols (f64) block starting at g (row stride ld) into smem (row
-// stride ss), zero-filling out-of-range rows/cols.  vec2: 16B chunks allowed.
-__device__ __forceinline__ void load_tile(double* s, int ss, const double* g, int64_t ld,
-                                          int rows, int cols, int rows_ok, int cols_ok,
-                                          bool vec2) {
-  if (vec2) {
-    const int cpr = cols / 2;
+// Copy a rows x cols block starting at g (row stride ld) into smem (row
+// stride ss), zero-filling out-of-range rows/cols.  vec: 16-byte chunks
+// allowed (ld and the base 16-byte aligned).  fp32 inputs (the Gram of an fp32
+// panel) are staged as fp32 and widened to fp64 when the fragments are loaded:
+// products of fp32 values are exact in fp64.
+template <typename TIN>
+__device__ __forceinline__ void load_tile(TIN* s, int ss, const TIN* g, int64_t ld, int rows,
+                                          int cols, int rows_ok, int cols_ok, bool vec) {
+  constexpr int V = 16 / sizeof(TIN);   // elements per 16-byte chunk
+  if (vec) {
+    const int cpr = cols / V;
     for (int c = threadIdx.x; c < rows * cpr; c += THREADS) {
-      int r = c / cpr, cc = (c % cpr) * 2;
-      int valid = (r < rows_ok) ? max(0, min(2, cols_ok - cc)) : 0;
-      const double* src = valid ? g + int64_t(r) * ld + cc : g;
-      cp_async16(s + r * ss + cc, src, valid * 8);
+      int r = c / cpr, cc = (c % cpr) * V;
+      int valid = (r < rows_ok) ? max(0, min(V, cols_ok - cc)) : 0;
+      const TIN* src = valid ? g + int64_t(r) * ld + cc : g;
+      cp_async16(s + r * ss + cc, src, valid * int(sizeof(TIN)));
     }
   } else {
     for (int c = threadIdx.x; c < rows * cols; c += THREADS) {
       int r = c / cols, cc = c % cols;
       int valid = (r < rows_ok && cc < cols_ok) ? 1 : 0;
-      const double* src = valid ? g + int64_t(r) * ld + cc : g;
-      cp_async8(s + r * ss + cc, src, valid * 8);
+      const TIN* src = valid ? g + int64_t(r) * ld + cc : g;
+      cp_async_elem(s + r * ss + cc, src, valid);
     }
   }
 }
 
-template <bool TRANS, int NF>
+template <bool TRANS, int NF, typename TIN = double>
 __global__ void __launch_bounds__(THREADS, 1)
-gemm_f64_kernel(int64_t M, int64_t N, int64_t K, const double* __restrict__ A, int64_t lda,
-                const double* __restrict__ B, int64_t ldb, double* __restrict__ C, int64_t ldc,
+gemm_f64_kernel(int64_t M, int64_t N, int64_t K, const TIN* __restrict__ A, int64_t lda,
+                const TIN* __restrict__ B, int64_t ldb, double* __restrict__ C, int64_t ldc,
                 int64_t kchunk, int64_t cstride, bool a16, bool b16) {
-  using S = Smem<NF>;
-  extern __shared__ __align__(16) double smem[];
-  double* As = smem;
-  double* Bs = smem + STAGES * S::A_ELEMS;
+  using S = Smem<NF, TIN>;
+  extern __shared__ __align__(16) unsigned char smem_bytes[];
+  TIN* As = reinterpret_cast<TIN*>(smem_bytes);
+  TIN* Bs = As + STAGES * S::A_ELEMS;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
@@ -107,8 +121,8 @@ gemm_f64_kernel(int64_t M, int64_t N, int64_t K, const double* __restrict__ A, i
   auto issue = [&](int kt, int stage) {
     const int64_t k0 = kbeg + int64_t(kt) * BK;
     const int k_ok = int(min(int64_t(BK), kend - k0));
-    double* as = As + stage * S::A_ELEMS;
-    double* bs = Bs + stage * S::B_ELEMS;
+    TIN* as = As + stage * S::A_ELEMS;
+    TIN* bs = Bs + stage * S::B_ELEMS;
     if (!TRANS)
       load_tile(as, AS_NN, A + m0 * lda + k0, lda, BM, BK, m_ok, k_ok, a16);
     else
@@ -139,8 +153,8 @@ gemm_f64_kernel(int64_t M, int64_t N, int64_t K, const double* __restrict__ A, i
       cp_commit();
     }
     const int stage = kt % STAGES;
-    const double* as = As + stage * S::A_ELEMS;
-    const double* bs = Bs + stage * S::B_ELEMS;
+    const TIN* as = As + stage * S::A_ELEMS;
+    const TIN* bs = Bs + stage * S::B_ELEMS;
 #pragma unroll
     for (int kk = 0; kk < BK / 4; ++kk) {
       double a[2][2];
@@ -149,16 +163,16 @@ gemm_f64_kernel(int64_t M, int64_t N, int64_t K, const double* __restrict__ A, i
         const int r = wm * 32 + mf * 16 + g;
         const int k = kk * 4 + t;
         if (!TRANS) {
-          a[mf][0] = as[r * AS_NN + k];
-          a[mf][1] = as[(r + 8) * AS_NN + k];
+          a[mf][0] = double(as[r * AS_NN + k]);
+          a[mf][1] = double(as[(r + 8) * AS_NN + k]);
         } else {
-          a[mf][0] = as[k * AS_TN + r];
-          a[mf][1] = as[k * AS_TN + r + 8];
+          a[mf][0] = double(as[k * AS_TN + r]);
+          a[mf][1] = double(as[k * AS_TN + r + 8]);
         }
       }
 #pragma unroll
       for (int nf = 0; nf < NF; ++nf) {
-        const double b = bs[(kk * 4 + t) * S::BS + wn * NF * 8 + nf * 8 + g];
+        const double b = double(bs[(kk * 4 + t) * S::BS + wn * NF * 8 + nf * 8 + g]);
         dmma(acc[0][nf], a[0][0], a[0][1], b);
         dmma(acc[1][nf], a[1][0], a[1][1], b);
       }
@@ -196,11 +210,11 @@ __global__ void splitk_reduce_f64(int64_t M, int64_t N, int S, const double* __r
   }
 }
 
-template <bool TRANS, int NF>
-void launch_nf(Handle* h, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
-               const double* B, int64_t ldb, double* C, int64_t ldc) {
-  using S = Smem<NF>;
-  auto kern = gemm_f64_kernel<TRANS, NF>;
+template <bool TRANS, int NF, typename TIN>
+void launch_nf(Handle* h, int64_t M, int64_t N, int64_t K, const TIN* A, int64_t lda,
+               const TIN* B, int64_t ldb, double* C, int64_t ldc) {
+  using S = Smem<NF, TIN>;
+  auto kern = gemm_f64_kernel<TRANS, NF, TIN>;
   static bool attr_set = false;
   if (!attr_set) {
     LR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -211,8 +225,9 @@ void launch_nf(Handle* h, int64_t M, int64_t N, int64_t K, const double* A, int6
   const int64_t splits_wanted = choose_splits(h->sm_count, mt * nt, K);
   const int64_t kchunk = ceil_div(ceil_div(K, splits_wanted), BK) * BK;
   const int64_t splits = std::max<int64_t>(1, ceil_div(K, kchunk));
-  const bool a16 = (lda % 2 == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
-  const bool b16 = (ldb % 2 == 0) && ((reinterpret_cast<uintptr_t>(B) & 15) == 0);
+  constexpr int V = 16 / sizeof(TIN);
+  const bool a16 = (lda % V == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
+  const bool b16 = (ldb % V == 0) && ((reinterpret_cast<uintptr_t>(B) & 15) == 0);
   dim3 grid{unsigned(mt), unsigned(nt), unsigned(splits)};
   if (splits == 1) {
     kern<<<grid, THREADS, S::bytes, h->stream>>>(M, N, K, A, lda, B, ldb, C, ldc, kchunk, 0,
@@ -230,20 +245,20 @@ void launch_nf(Handle* h, int64_t M, int64_t N, int64_t K, const double* A, int6
   LR_CHECK_LAUNCH();
 }
 
-template <bool TRANS>
-void launch_trans(Handle* h, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
-                  const double* B, int64_t ldb, double* C, int64_t ldc) {
+template <bool TRANS, typename TIN>
+void launch_trans(Handle* h, int64_t M, int64_t N, int64_t K, const TIN* A, int64_t lda,
+                  const TIN* B, int64_t ldb, double* C, int64_t ldc) {
   // N beyond one 128-wide tile is handled by grid.y (A re-read per N tile).
   const int nf = int(std::min<int64_t>(8, ceil_div(N, 16)));
   switch (nf) {
-    case 1: launch_nf<TRANS, 1>(h, M, N, K, A, lda, B, ldb, C, ldc); break;
-    case 2: launch_nf<TRANS, 2>(h, M, N, K, A, lda, B, ldb, C, ldc); break;
-    case 3: launch_nf<TRANS, 3>(h, M, N, K, A, lda, B, ldb, C, ldc); break;
-    case 4: launch_nf<TRANS, 4>(h, M, N, K, A, lda, B, ldb, C, ldc); break;
-    case 5: launch_nf<TRANS, 5>(h, M, N, K, A, lda, B, ldb, C, ldc); break;
-    case 6: launch_nf<TRANS, 6>(h, M, N, K, A, lda, B, ldb, C, ldc); break;
-    case 7: launch_nf<TRANS, 7>(h, M, N, K, A, lda, B, ldb, C, ldc); break;
-    default: launch_nf<TRANS, 8>(h, M, N, K, A, lda, B, ldb, C, ldc); break;
+    case 1: launch_nf<TRANS, 1, TIN>(h, M, N, K, A, lda, B, ldb, C, ldc); break;
+    case 2: launch_nf<TRANS, 2, TIN>(h, M, N, K, A, lda, B, ldb, C, ldc); break;
+    case 3: launch_nf<TRANS, 3, TIN>(h, M, N, K, A, lda, B, ldb, C, ldc); break;
+    case 4: launch_nf<TRANS, 4, TIN>(h, M, N, K, A, lda, B, ldb, C, ldc); break;
+    case 5: launch_nf<TRANS, 5, TIN>(h, M, N, K, A, lda, B, ldb, C, ldc); break;
+    case 6: launch_nf<TRANS, 6, TIN>(h, M, N, K, A, lda, B, ldb, C, ldc); break;
+    case 7: launch_nf<TRANS, 7, TIN>(h, M, N, K, A, lda, B, ldb, C, ldc); break;
+    default: launch_nf<TRANS, 8, TIN>(h, M, N, K, A, lda, B, ldb, C, ldc); break;
   }
 }
 
@@ -310,8 +325,22 @@ void gemm_f64(Handle* h, bool transA, int64_t M, int64_t N, int64_t K, const dou
       LR_CUDA(cudaMemsetAsync(C + r * ldc, 0, N * sizeof(double), h->stream));
     return;
   }
-  if (transA) launch_trans<true>(h, M, N, K, A, lda, B, ldb, C, ldc);
-  else        launch_trans<false>(h, M, N, K, A, lda, B, ldb, C, ldc);
+  if (transA) launch_trans<true, double>(h, M, N, K, A, lda, B, ldb, C, ldc);
+  else        launch_trans<false, double>(h, M, N, K, A, lda, B, ldb, C, ldc);
+}
+
+// C (fp64) = op(A) B for fp32 A, B on the FP64 tensor pipe: exact products,
+// fp64 accumulation (the Gram of an fp32 panel).
+void gemm_f64_from_f32(Handle* h, bool transA, int64_t M, int64_t N, int64_t K, const float* A,
+                       int64_t lda, const float* B, int64_t ldb, double* C, int64_t ldc) {
+  if (M == 0 || N == 0) return;
+  if (K == 0) {
+    for (int64_t r = 0; r < M; ++r)
+      LR_CUDA(cudaMemsetAsync(C + r * ldc, 0, N * sizeof(double), h->stream));
+    return;
+  }
+  if (transA) launch_trans<true, float>(h, M, N, K, A, lda, B, ldb, C, ldc);
+  else        launch_trans<false, float>(h, M, N, K, A, lda, B, ldb, C, ldc);
 }
 
 void gemm_c128(Handle* h, bool transA, bool conjA, int64_t M, int64_t N, int64_t K,
