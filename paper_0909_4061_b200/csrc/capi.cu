@@ -9,26 +9,7 @@ namespace lr {
 
 unsigned long long g_launches = 0;
 
-namespace {
-thread_local std::string g_err;
-
-// unit roundoff of the arithmetic the Gram / Cholesky run in (always fp64)
-constexpr double U64 = 1.1102230246251565e-16;
-
-int wide_of(int dtype) { return is_complex(dtype) ? LR_C128 : LR_F64; }
-size_t wide_size(int dtype) { return is_complex(dtype) ? 16 : 8; }
-
-struct Info {
-  int32_t rank, unresolved, bad;
-};
-
-Info read_info(Handle* h, const int32_t* d) {
-  LR_CUDA(cudaMemcpyAsync(h->h_info, d, 3 * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
-  LR_CUDA(cudaStreamSynchronize(h->stream));
-  return Info{h->h_info[0], h->h_info[1], h->h_info[2]};
-}
-
-// ---- dtype dispatch of the kernels ------------------------------------------------
+// ---- dtype dispatch of the products (also used by chol_tiled.cu) ----------------
 
 void gemm_any(Handle* h, int dtype, bool trans, bool conj, int64_t M, int64_t N, int64_t K,
               const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc) {
@@ -60,6 +41,28 @@ void gemm_any(Handle* h, int dtype, bool trans, bool conj, int64_t M, int64_t N,
   }
   throw Error{LR_EINVAL, "unknown dtype"};
 }
+
+namespace {
+thread_local std::string g_err;
+
+// unit roundoff of the arithmetic the Gram / Cholesky run in (always fp64)
+constexpr double U64 = 1.1102230246251565e-16;
+
+int wide_of(int dtype) { return is_complex(dtype) ? LR_C128 : LR_F64; }
+size_t wide_size(int dtype) { return is_complex(dtype) ? 16 : 8; }
+
+struct Info {
+  int32_t rank, unresolved, bad;
+};
+
+Info read_info(Handle* h, const int32_t* d) {
+  LR_CUDA(cudaMemcpyAsync(h->h_info, d, 3 * sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
+  LR_CUDA(cudaStreamSynchronize(h->stream));
+  return Info{h->h_info[0], h->h_info[1], h->h_info[2]};
+}
+
+// ---- dtype dispatch of the kernels ------------------------------------------------
+
 
 // G (ell x ell, wide) = Y^H Y
 void gram_any(Handle* h, int dtype, int64_t m, int64_t ell, const void* Y, int64_t ldy, void* G) {

@@ -282,6 +282,10 @@ void chol_drop_f64(Handle* h, int64_t ell, const double* G, double drop_tol, dou
     chol_tiled_f64(h, ell, G, drop_tol, unres_rel, shift_coef, P, R, info);
     return;
   }
+  if (chol_blocked_supported(ell)) {
+    chol_blocked_f64(h, ell, G, drop_tol, unres_rel, shift_coef, P, R, info);
+    return;
+  }
   launch_chol<double>(h, ell, G, drop_tol, unres_rel, shift_coef, P, R, info);
 }
 
@@ -291,6 +295,10 @@ void chol_drop_c128(Handle* h, int64_t ell, const double2* G, double drop_tol,
   LR_REQUIRE(ell >= 1 && ell <= 4096, LR_EINVAL, "chol_drop: ell out of range [1, 4096]");
   if (chol_tiled_supported(ell, true)) {
     chol_tiled_c128(h, ell, G, drop_tol, unres_rel, shift_coef, P, R, info);
+    return;
+  }
+  if (chol_blocked_supported(ell)) {
+    chol_blocked_c128(h, ell, G, drop_tol, unres_rel, shift_coef, P, R, info);
     return;
   }
   launch_chol<double2>(h, ell, G, drop_tol, unres_rel, shift_coef, P, R, info);

@@ -47,9 +47,15 @@ __device__ __forceinline__ T sel4(const T (&v)[4], int i) {
 
 template <typename T, bool RT_SMEM, int MAXT>
 __global__ void __launch_bounds__(MAXT, 1)   // MAXT >= 32 * ceil(tiles / 32)
-chol_tiled_kernel(int n, const T* __restrict__ G, double drop_tol, double unres_rel,
+chol_tiled_kernel(int n, const T* __restrict__ G, int64_t ldg, double drop_tol, double unres_rel,
                   double shift_coef, T* __restrict__ P, T* __restrict__ Rout,
-                  int32_t* __restrict__ info, T* __restrict__ gRt, int32_t* status) {
+                  int32_t* __restrict__ info, T* __restrict__ gRt, int32_t* status,
+                  const double* __restrict__ trace_dev, const T* __restrict__ diag_src,
+                  int64_t diag_stride, bool compact) {
+  // Block calls (chol_blocked below): trace_dev supplies the trace of the
+  // whole Gram (drop threshold and shift), diag_src its original diagonal for
+  // this block (the unresolved-pivot test), and compact = false writes P
+  // uncompacted (column c of X in column c, zero for dropped c).
   using S = Sc<T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* rowbuf = reinterpret_cast<T*>(smem_raw);            // [2][n]
@@ -74,10 +80,11 @@ chol_tiled_kernel(int n, const T* __restrict__ G, double drop_tol, double unres_
 
   if (warp == 0) {
     double tr = 0.0;
-    for (int i = lane; i < n; i += 32) tr += S::re(G[size_t(i) * n + i]);
+    if (!trace_dev)
+      for (int i = lane; i < n; i += 32) tr += S::re(G[size_t(i) * ldg + i]);
 #pragma unroll
     for (int m = 16; m > 0; m >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, m);
-    if (lane == 0) { s_trace = tr; s_unres = 0; s_bad = 0; }
+    if (lane == 0) { s_trace = trace_dev ? *trace_dev : tr; s_unres = 0; s_bad = 0; }
   }
   __syncthreads();
   const double trace = s_trace;
@@ -91,10 +98,10 @@ chol_tiled_kernel(int n, const T* __restrict__ G, double drop_tol, double unres_
     for (int b = 0; b < TS; ++b) {
       const int i = r0 + a, k = c0 + b;
       T v = S::zero();
-      if (owner && i < n && k < n && k >= i) v = G[size_t(i) * n + k];
+      if (owner && i < n && k < n && k >= i) v = G[size_t(i) * ldg + k];
       if (owner && i == k && i < n) {
         v = S::make(S::re(v) + shift, 0.0);
-        d0[i] = S::re(v);
+        d0[i] = diag_src ? S::re(diag_src[size_t(i) * diag_stride]) + shift : S::re(v);
       }
       w[a][b] = v;
     }
@@ -206,7 +213,7 @@ chol_tiled_kernel(int n, const T* __restrict__ G, double drop_tol, double unres_
         }
       }
     }
-    const int pc = pos[c];
+    const int pc = compact ? pos[c] : c;
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       const int i = lane + 32 * r;
@@ -228,8 +235,9 @@ chol_tiled_kernel(int n, const T* __restrict__ G, double drop_tol, double unres_
 }
 
 template <typename T>
-void launch(Handle* h, int n, const T* G, double drop_tol, double unres_rel, double shift_coef,
-            T* P, T* R, int32_t* info) {
+void launch(Handle* h, int n, const T* G, int64_t ldg, double drop_tol, double unres_rel,
+            double shift_coef, T* P, T* R, int32_t* info, const double* trace_dev = nullptr,
+            const T* diag_src = nullptr, int64_t diag_stride = 0, bool compact = true) {
   const int nt = (n + TS - 1) / TS;
   const int threads = ((nt * (nt + 1) / 2 + 31) / 32) * 32;
   const size_t head = head_bytes(n, sizeof(T));
@@ -241,8 +249,9 @@ void launch(Handle* h, int n, const T* G, double drop_tol, double unres_rel, dou
   const size_t smem = in_smem ? head + rt : head;
   auto go = [&](auto kern) {
     LR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    kern<<<1, threads, smem, h->stream>>>(n, G, drop_tol, unres_rel, shift_coef, P, R, info, gRt,
-                                          h->status);
+    kern<<<1, threads, smem, h->stream>>>(n, G, ldg, drop_tol, unres_rel, shift_coef, P, R, info,
+                                          gRt, h->status, trace_dev, diag_src, diag_stride,
+                                          compact);
   };
   if (threads <= 320) {
     if (in_smem) go(chol_tiled_kernel<T, true, 320>);
@@ -254,7 +263,154 @@ void launch(Handle* h, int n, const T* G, double drop_tol, double unres_rel, dou
   LR_CHECK_LAUNCH();
 }
 
+// ---------------------------------------------------------------------------
+// 128 < ell <= 256: one level of 2 x 2 blocking around the tiled kernel.
+//   G = [G11 G12; G12^H G22] (+ shift on the diagonal),  R11 = chol(G11),
+//   R12 = R~11^{-H} G12 (rows of dropped block-1 pivots zero),
+//   S = G22 - R12^H R12,  R22 = chol(S),
+//   X = R~^{-1} = [X11, -X11 R12 X22; 0, X22]  (R12 columns of dropped block-2
+//   pivots zeroed: R~ has the identity there).
+// The pivots, drop and unresolved decisions are those of the unblocked
+// factorization (same Schur complements, thresholds from the whole G).
+
+template <typename T>
+__global__ void trace_kernel(int n, const T* __restrict__ G, double* __restrict__ tr) {
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += Sc<T>::re(G[size_t(i) * n + i]);
+  for (int m = 16; m > 0; m >>= 1) s += __shfl_xor_sync(0xffffffffu, s, m);
+  __shared__ double red[32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < int(blockDim.x >> 5); ++w) t += red[w];
+    *tr = t;
+  }
+}
+
+// S = G22 - T (n2 x n2; G22 inside G with ld n, T dense)
+template <typename T>
+__global__ void schur_kernel(int n2, const T* __restrict__ G22, int64_t ldg,
+                             const T* __restrict__ Tm, T* __restrict__ Sout) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n2 * n2; e += gridDim.x * blockDim.x) {
+    const int i = e / n2, k = e - i * n2;
+    Sout[e] = Sc<T>::sub(G22[size_t(i) * ldg + k], Tm[e]);
+  }
+}
+
+// zero the columns of R12 (n1 x n2) whose block-2 pivot was dropped
+template <typename T>
+__global__ void mask_cols_kernel(int n1, int n2, T* __restrict__ R12, const T* __restrict__ R22) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n1 * n2; e += gridDim.x * blockDim.x) {
+    const int c = e % n2;
+    if (Sc<T>::re(R22[size_t(c) * n2 + c]) == 0.0) R12[e] = Sc<T>::zero();
+  }
+}
+
+// assemble P (compacted), R and info from the blocks (one CTA, n <= 256)
+template <typename T>
+__global__ void assemble_kernel(int n, int n1, const T* __restrict__ X11, const T* __restrict__ X12n,
+                                const T* __restrict__ X22, const T* __restrict__ R11,
+                                const T* __restrict__ R12, const T* __restrict__ R22,
+                                const int32_t* __restrict__ info1,
+                                const int32_t* __restrict__ info2, T* __restrict__ P,
+                                T* __restrict__ Rout, int32_t* __restrict__ info) {
+  using S = Sc<T>;
+  const int n2 = n - n1;
+  __shared__ int pos[256];
+  __shared__ int s_rank;
+  const int tid = threadIdx.x, lane = tid & 31;
+  auto rdiag = [&](int j) {
+    return j < n1 ? S::re(R11[size_t(j) * n1 + j]) : S::re(R22[size_t(j - n1) * n2 + (j - n1)]);
+  };
+  if (tid < 32) {
+    int base = 0;
+    for (int j0 = 0; j0 < n; j0 += 32) {
+      const int j = j0 + lane;
+      const bool k = j < n && rdiag(j) > 0.0;
+      const unsigned bal = __ballot_sync(0xffffffffu, k);
+      if (j < n) pos[j] = k ? base + __popc(bal & ((1u << lane) - 1u)) : -1;
+      base += __popc(bal);
+    }
+    if (lane == 0) s_rank = base;
+  }
+  __syncthreads();
+  for (int e = tid; e < n * n; e += blockDim.x) {
+    const int i = e / n, c = e - i * n;
+    T r = S::zero();
+    if (i < n1 && c < n1) r = R11[size_t(i) * n1 + c];
+    else if (i < n1) r = R12[size_t(i) * n2 + (c - n1)];
+    else if (c >= n1) r = R22[size_t(i - n1) * n2 + (c - n1)];
+    if (pos[i] < 0 || pos[c] < 0) r = S::zero();
+    Rout[e] = r;
+    P[e] = S::zero();
+  }
+  __syncthreads();
+  for (int e = tid; e < n * n; e += blockDim.x) {
+    const int i = e / n, c = e - i * n;
+    if (pos[c] < 0) continue;
+    T x = S::zero();
+    if (i < n1 && c < n1) x = X11[size_t(i) * n1 + c];
+    else if (i < n1) x = S::scale(X12n[size_t(i) * n2 + (c - n1)], -1.0);
+    else if (c >= n1) x = X22[size_t(i - n1) * n2 + (c - n1)];
+    P[size_t(i) * n + pos[c]] = x;
+  }
+  if (tid == 0) {
+    info[0] = s_rank;
+    info[1] = info1[1] + info2[1];
+    info[2] = info1[2] + info2[2];
+  }
+}
+
+template <typename T>
+void chol_blocked(Handle* h, int dtype, int n, const T* G, double drop_tol, double unres_rel,
+                  double shift_coef, T* P, T* R, int32_t* info) {
+  const int n1 = MAXN, n2 = n - n1;
+  double* tr = pool_alloc_t<double>(h, 1);
+  int32_t* inf = pool_alloc_t<int32_t>(h, 8);
+  T* X11 = pool_alloc_t<T>(h, size_t(n1) * n1);
+  T* R11 = pool_alloc_t<T>(h, size_t(n1) * n1);
+  T* X22 = pool_alloc_t<T>(h, size_t(n2) * n2);
+  T* R22 = pool_alloc_t<T>(h, size_t(n2) * n2);
+  T* R12 = pool_alloc_t<T>(h, size_t(n1) * n2);
+  T* Tm = pool_alloc_t<T>(h, size_t(n2) * n2);
+  T* Sm = pool_alloc_t<T>(h, size_t(n2) * n2);
+  T* T1 = pool_alloc_t<T>(h, size_t(n1) * n2);
+  T* X12 = pool_alloc_t<T>(h, size_t(n1) * n2);
+  trace_kernel<T><<<1, 256, 0, h->stream>>>(n, G, tr);
+  LR_CHECK_LAUNCH();
+  launch<T>(h, n1, G, n, drop_tol, unres_rel, shift_coef, X11, R11, inf, tr, nullptr, 0, false);
+  // R12 = X11^H G12
+  gemm_any(h, dtype, true, true, n1, n2, n1, X11, n1, G + n1, n, R12, n2);
+  // S = G22 - R12^H R12
+  gemm_any(h, dtype, true, true, n2, n2, n1, R12, n2, R12, n2, Tm, n2);
+  schur_kernel<T><<<64, 256, 0, h->stream>>>(n2, G + size_t(n1) * n + n1, n, Tm, Sm);
+  LR_CHECK_LAUNCH();
+  launch<T>(h, n2, Sm, n2, drop_tol, unres_rel, shift_coef, X22, R22, inf + 4, tr,
+            G + size_t(n1) * n + n1, n + 1, false);
+  mask_cols_kernel<T><<<64, 256, 0, h->stream>>>(n1, n2, R12, R22);
+  LR_CHECK_LAUNCH();
+  // X12 = -(X11 R12) X22 (sign applied in the assembly)
+  gemm_any(h, dtype, false, false, n1, n2, n1, X11, n1, R12, n2, T1, n2);
+  gemm_any(h, dtype, false, false, n1, n2, n2, T1, n2, X22, n2, X12, n2);
+  assemble_kernel<T><<<1, 1024, 0, h->stream>>>(n, n1, X11, X12, X22, R11, R12, R22, inf,
+                                                 inf + 4, P, R, info);
+  LR_CHECK_LAUNCH();
+}
+
 }  // namespace
+
+bool chol_blocked_supported(int64_t n) { return n > MAXN && n <= 2 * MAXN; }
+
+void chol_blocked_f64(Handle* h, int64_t n, const double* G, double drop_tol, double unres_rel,
+                      double shift_coef, double* P, double* R, int32_t* info) {
+  chol_blocked<double>(h, LR_F64, int(n), G, drop_tol, unres_rel, shift_coef, P, R, info);
+}
+
+void chol_blocked_c128(Handle* h, int64_t n, const double2* G, double drop_tol, double unres_rel,
+                       double shift_coef, double2* P, double2* R, int32_t* info) {
+  chol_blocked<double2>(h, LR_C128, int(n), G, drop_tol, unres_rel, shift_coef, P, R, info);
+}
 
 // Measured on B200 (tools/small_probe.py, CUDA-graph timed): the tiled
 // kernel wins from ell ~ 80 (real: 133 vs 178 us at 110, 163 vs 380 us at
@@ -272,12 +428,12 @@ bool chol_tiled_supported(int64_t n, bool cplx) {
 
 void chol_tiled_f64(Handle* h, int64_t n, const double* G, double drop_tol, double unres_rel,
                     double shift_coef, double* P, double* R, int32_t* info) {
-  launch<double>(h, int(n), G, drop_tol, unres_rel, shift_coef, P, R, info);
+  launch<double>(h, int(n), G, n, drop_tol, unres_rel, shift_coef, P, R, info);
 }
 
 void chol_tiled_c128(Handle* h, int64_t n, const double2* G, double drop_tol, double unres_rel,
                      double shift_coef, double2* P, double2* R, int32_t* info) {
-  launch<double2>(h, int(n), G, drop_tol, unres_rel, shift_coef, P, R, info);
+  launch<double2>(h, int(n), G, n, drop_tol, unres_rel, shift_coef, P, R, info);
 }
 
 }  // namespace lr

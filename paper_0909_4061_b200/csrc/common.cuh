@@ -151,6 +151,14 @@ void jacobi_svd_c128(Handle* h, int64_t rows, int64_t n, const double2* M, doubl
 // chol_tiled.cu: register-tiled Cholesky with deletion for ell <= 128
 // (by size; LR_CHOL=smem|tiled forces one kernel)
 bool chol_tiled_supported(int64_t n, bool cplx);
+bool chol_blocked_supported(int64_t n);
+void chol_blocked_f64(Handle* h, int64_t n, const double* G, double drop_tol, double unres_rel,
+                      double shift_coef, double* P, double* R, int32_t* info);
+void chol_blocked_c128(Handle* h, int64_t n, const double2* G, double drop_tol,
+                       double unres_rel, double shift_coef, double2* P, double2* R,
+                       int32_t* info);
+void gemm_any(Handle* h, int dtype, bool trans, bool conj, int64_t M, int64_t N, int64_t K,
+              const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc);
 void chol_tiled_f64(Handle* h, int64_t n, const double* G, double drop_tol, double unres_rel,
                     double shift_coef, double* P, double* R, int32_t* info);
 void chol_tiled_c128(Handle* h, int64_t n, const double2* G, double drop_tol, double unres_rel,

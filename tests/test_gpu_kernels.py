@@ -129,6 +129,61 @@ def test_orth_matches_cgs2(m, ell, dtype):
     assert np.linalg.norm(Q.conj().T @ Q - np.eye(k)) <= (1e-12 if tol < 1e-6 else 1e-5) * k
 
 
+def _chol_drop_ref(G, tol, shift_coef):
+    """numpy restatement of the lr_chol_drop contract (column deletion)."""
+    n = G.shape[0]
+    tr = float(np.real(np.trace(G)))
+    thr2 = tol * tol * tr
+    W = G.astype(np.complex128 if np.iscomplexobj(G) else np.float64).copy()
+    W[np.diag_indices(n)] += shift_coef * tr
+    R = np.zeros_like(W)
+    kept = []
+    for j in range(n):
+        d = float(np.real(W[j, j] - sum(abs(R[i, j]) ** 2 for i in kept)))
+        if np.isfinite(d) and d > thr2 and d > 0:
+            R[j, j] = np.sqrt(d)
+            for k in range(j + 1, n):
+                R[j, k] = (W[j, k] - sum(np.conj(R[i, j]) * R[i, k] for i in kept)) / R[j, j]
+            kept.append(j)
+    dropped = [k for k in range(n) if k not in kept]
+    R[:, dropped] = 0      # the factor is reported on kept rows/cols only
+    return R, kept
+
+
+@pytest.mark.parametrize("ell,cplx,rank", [(30, False, 30), (100, False, 87), (128, False, 128),
+                                           (200, False, 170), (256, False, 256),
+                                           (64, True, 50), (120, True, 120), (180, True, 160)])
+def test_chol_drop_sizes(ell, cplx, rank):
+    """Cholesky with deletion on every kernel path (shared-memory <= 79,
+    register-tiled 80..128, 2x2 blocked 129..256): rank decision and
+    factor vs a numpy restatement; Q = Y P orthonormal on the kept span."""
+    from paper_0909_4061_b200 import _lib
+    g = np.random.default_rng(ell)
+    m = 3 * ell
+    B = g.standard_normal((m, rank)) + (1j * g.standard_normal((m, rank)) if cplx else 0)
+    C = g.standard_normal((rank, ell)) + (1j * g.standard_normal((rank, ell)) if cplx else 0)
+    Y = B @ C   # exact rank: the first `rank` columns are kept, the rest dropped
+    Yd = torch.from_numpy(Y).cuda()
+    G = (Yd.conj().T @ Yd).contiguous()
+    P, R = torch.empty_like(G), torch.empty_like(G)
+    info = torch.zeros(4, dtype=torch.int32, device="cuda")
+    code = _lib.C128 if cplx else _lib.F64
+    # drop_tol 1e-6: the dependent columns' Gram pivots (~u tr G) are resolvable
+    _lib.call("lr_chol_drop", _lib.handle(), code, ell, _lib.ptr(G), 1e-6, 4 * ell * 1.1e-16,
+              0.0, _lib.ptr(P), _lib.ptr(R), _lib.ptr(info))
+    torch.cuda.synchronize()
+    Rref, kept = _chol_drop_ref(G.cpu().numpy(), 1e-6, 0.0)
+    r = int(info[0].item())
+    assert r == len(kept) == rank
+    Rg = R.cpu().numpy()
+    scale = np.abs(Rref).max()
+    assert np.abs(Rg - Rref).max() <= 1e-9 * scale
+    Q = (Yd @ P[:, :r]).cpu().numpy()
+    assert np.linalg.norm(Q.conj().T @ Q - np.eye(r)) <= 1e-6 * r
+    if r < ell:
+        assert np.abs(P[:, r:].cpu().numpy()).max() == 0.0
+
+
 def test_orth_ill_conditioned_panel():
     """kappa(Y) ~ 1e7 (cfg5-like): fp64 Gram CholQR2 cannot resolve it; the
     guarded fallback must still give the reference's Q."""
