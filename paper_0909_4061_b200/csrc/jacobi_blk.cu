@@ -18,6 +18,8 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "scalar.cuh"
 
@@ -293,6 +295,178 @@ void launch_blk(Handle* h, int n, const T* Rin, T* Mout, double* sig, int32_t* i
   LR_CHECK_LAUNCH();
 }
 
+// ---------------------------------------------------------------------------
+// Cluster variant for the columns that do not fit one SM's register file
+// (real 128 < n <= 256, complex 64 < n <= 128): the same block tournament
+// over a thread-block cluster of CL CTAs x WPC warps.  Tournament position
+// pos (tops 0..P-1, bottoms P..2P-1) lives in the shared memory of the CTA
+// owning warp (pos mod P); moved blocks are written straight into the
+// owner's slot through distributed shared memory (DSMEM) and two cluster
+// barriers per round order the writes and reads.  256 threads per CTA leave
+// 255 registers per thread for the 8 x R column block.
+template <typename T, int R, int CL, int WPC>
+__global__ void __launch_bounds__(WPC * 32, 1)
+jacobi_cl_kernel(int n, const T* __restrict__ Rin, T* __restrict__ Mout, double* __restrict__ sig,
+                 int32_t* __restrict__ info, double tol, int max_sweeps, int32_t* status) {
+  namespace cg = cooperative_groups;
+  using S = Sc<T>;
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int ROWS = 32 * R;
+  constexpr int SLOTS = 2 * WPC;
+  T* xbuf = reinterpret_cast<T*>(smem_raw);                                 // [SLOTS][BW][ROWS]
+  double* nbuf = reinterpret_cast<double*>(xbuf + size_t(SLOTS) * BW * ROWS);  // [SLOTS][BW]
+  int* bid = reinterpret_cast<int*>(nbuf + SLOTS * BW);                        // [SLOTS]
+  int* cflag = bid + SLOTS;                                                    // [2][CL]
+
+  const int nb = (n + BW - 1) / BW;
+  const int nbp = nb + (nb & 1);
+  const int P = nbp / 2;
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const int rank = int(cluster.block_rank());
+  const int w = rank * WPC + wl;       // tournament slot of this warp
+  const bool active = w < P;
+  // position -> (owner CTA, local slot)
+  auto owner = [&](int pos) { return (pos < P ? pos : pos - P) / WPC; };
+  auto lslot = [&](int pos) { return (pos < P ? 0 : WPC) + (pos < P ? pos : pos - P) % WPC; };
+
+  int btop = w, bbot = nbp - 1 - w;
+  T x[WC][R];
+#pragma unroll
+  for (int c = 0; c < WC; ++c) {
+    const int col = (c < BW ? btop : bbot) * BW + (c & (BW - 1));
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int row = lane + 32 * r;
+      x[c][r] = (active && row < n && col < n) ? Rin[size_t(row) * n + col] : S::zero();
+    }
+  }
+
+  double nrmv = 0.0;
+  int sweep = 0;
+  bool converged = (n <= 1);
+  for (; sweep < max_sweeps && !converged; ++sweep) {
+    int did = 0;
+    if (active) {
+#pragma unroll
+      for (int c = 0; c < WC; ++c) {
+        const double v = col_norm2<T, R>(x[c]);
+        if (lane == c) nrmv = v;
+      }
+      subround<T, R, 0, 1, 2, 3, 4, 5, 6, 7>(x, nrmv, lane, tol, did);
+      subround<T, R, 0, 2, 1, 3, 4, 6, 5, 7>(x, nrmv, lane, tol, did);
+      subround<T, R, 0, 3, 1, 2, 4, 7, 5, 6>(x, nrmv, lane, tol, did);
+    }
+    for (int rd = 0; rd < nbp - 1; ++rd) {
+      if (active) {
+        subround<T, R, 0, 4, 1, 5, 2, 6, 3, 7>(x, nrmv, lane, tol, did);
+        subround<T, R, 0, 5, 1, 6, 2, 7, 3, 4>(x, nrmv, lane, tol, did);
+        subround<T, R, 0, 6, 1, 7, 2, 4, 3, 5>(x, nrmv, lane, tol, did);
+        subround<T, R, 0, 7, 1, 4, 2, 5, 3, 6>(x, nrmv, lane, tol, did);
+      }
+      cluster.sync();   // every slot has been read
+      if (active) {
+        const int dt = (w == 0) ? -1 : (w + 1 < P ? w + 1 : 2 * P - 1);
+        const int db = (w >= 1) ? P + w - 1 : 1;
+        if (dt >= 0) {
+          const int o = owner(dt), ls = lslot(dt);
+          T* xb = cluster.map_shared_rank(xbuf, o) + size_t(ls) * BW * ROWS;
+#pragma unroll
+          for (int c = 0; c < BW; ++c)
+#pragma unroll
+            for (int r = 0; r < R; ++r) xb[c * ROWS + lane + 32 * r] = x[c][r];
+          if (lane < BW) cluster.map_shared_rank(nbuf, o)[ls * BW + lane] = nrmv;
+          if (lane == 0) cluster.map_shared_rank(bid, o)[ls] = btop;
+        }
+        const int o = owner(db), ls = lslot(db);
+        T* xb = cluster.map_shared_rank(xbuf, o) + size_t(ls) * BW * ROWS;
+#pragma unroll
+        for (int c = 0; c < BW; ++c)
+#pragma unroll
+          for (int r = 0; r < R; ++r) xb[c * ROWS + lane + 32 * r] = x[BW + c][r];
+        if (lane >= BW && lane < WC) cluster.map_shared_rank(nbuf, o)[ls * BW + lane - BW] = nrmv;
+        if (lane == 0) cluster.map_shared_rank(bid, o)[ls] = bbot;
+      }
+      cluster.sync();   // the moves have landed
+      if (active) {
+        if (w >= 1) {
+          const T* xb = xbuf + size_t(lslot(w)) * BW * ROWS;
+#pragma unroll
+          for (int c = 0; c < BW; ++c)
+#pragma unroll
+            for (int r = 0; r < R; ++r) x[c][r] = xb[c * ROWS + lane + 32 * r];
+          btop = bid[lslot(w)];
+          if (lane < BW) nrmv = nbuf[lslot(w) * BW + lane];
+        }
+        const int lb = lslot(P + w);
+        const T* xb = xbuf + size_t(lb) * BW * ROWS;
+#pragma unroll
+        for (int c = 0; c < BW; ++c)
+#pragma unroll
+          for (int r = 0; r < R; ++r) x[BW + c][r] = xb[c * ROWS + lane + 32 * r];
+        bbot = bid[lb];
+        if (lane >= BW && lane < WC) nrmv = nbuf[lb * BW + lane - BW];
+      }
+    }
+    // cluster-wide "any rotation": per-CTA OR, gathered in rank 0
+    const int any_cta = __syncthreads_or(did);
+    int* flags = cflag + (sweep & 1) * CL;
+    if (threadIdx.x == 0) cluster.map_shared_rank(flags, 0)[rank] = any_cta;
+    cluster.sync();
+    int any = 0;
+    const int* f0 = cluster.map_shared_rank(flags, 0);
+#pragma unroll
+    for (int c = 0; c < CL; ++c) any |= f0[c];
+    converged = (any == 0);
+  }
+
+  if (active) {
+#pragma unroll
+    for (int c = 0; c < WC; ++c) {
+      const int col = (c < BW ? btop : bbot) * BW + (c & (BW - 1));
+      double nrm = 0.0;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int row = lane + 32 * r;
+        nrm += S::abs2(x[c][r]);
+        if (row < n && col < n) Mout[size_t(row) * n + col] = x[c][r];
+      }
+#pragma unroll
+      for (int m = 16; m > 0; m >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, m);
+      if (lane == 0 && col < n) sig[col] = sqrt(nrm);
+    }
+  }
+  if (rank == 0 && threadIdx.x == 0) {
+    info[0] = converged ? sweep : -sweep;
+    if (!converged && status) atomicOr(status, 8);
+  }
+  cluster.sync();   // keep every CTA's shared memory alive until all DSMEM reads are done
+}
+
+template <typename T, int R, int CL, int WPC>
+void launch_cl(Handle* h, int n, const T* Rin, T* Mout, double* sig, int32_t* info) {
+  constexpr int SLOTS = 2 * WPC;
+  const size_t smem = size_t(SLOTS) * BW * 32 * R * sizeof(T) +
+                      size_t(SLOTS) * (BW * sizeof(double) + sizeof(int)) + 2 * CL * sizeof(int);
+  auto kern = jacobi_cl_kernel<T, R, CL, WPC>;
+  LR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  LR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(CL, 1, 1);
+  cfg.blockDim = dim3(WPC * 32, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = h->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CL;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  LR_CUDA(cudaLaunchKernelEx(&cfg, kern, n, Rin, Mout, sig, info, 4e-15, 60, h->status));
+  LR_CHECK_LAUNCH();
+}
+
 }  // namespace
 
 bool jacobi_blk_enabled() {
@@ -300,6 +474,18 @@ bool jacobi_blk_enabled() {
   if (v < 0) {
     const char* e = getenv("LR_JACOBI");
     v = (e && std::strcmp(e, "round") == 0) ? 0 : 1;
+  }
+  return v == 1;
+}
+
+// 96 < n <= 128 real: a 2-CTA cluster (255 registers per thread, no spills)
+// instead of one 448/512-thread CTA (128 registers, spills); LR_JACOBI_CL=0
+// selects the single CTA.
+static bool cl_mid() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("LR_JACOBI_CL");
+    v = (e && e[0] == '0') ? 0 : 1;
   }
   return v == 1;
 }
@@ -312,15 +498,18 @@ void jacobi_blk_f64(Handle* h, int64_t n, const double* R, double* Mout, double*
   else if (n <= 64) launch_blk<double, 2, 256>(h, int(n), R, Mout, sig, info);
   else if (n <= 80) launch_blk<double, 3, 320>(h, int(n), R, Mout, sig, info);
   else if (n <= 96) launch_blk<double, 3, 384>(h, int(n), R, Mout, sig, info);
+  else if (n <= 128 && cl_mid()) launch_cl<double, 4, 2, 8>(h, int(n), R, Mout, sig, info);
   else if (n <= 112) launch_blk<double, 4, 448>(h, int(n), R, Mout, sig, info);
-  else launch_blk<double, 4, 512>(h, int(n), R, Mout, sig, info);
+  else if (n <= 128) launch_blk<double, 4, 512>(h, int(n), R, Mout, sig, info);
+  else launch_cl<double, 8, 4, 8>(h, int(n), R, Mout, sig, info);
 }
 
 void jacobi_blk_c128(Handle* h, int64_t n, const double2* R, double2* Mout, double* sig,
                      int32_t* info) {
   if (n <= 32) launch_blk<double2, 1, 128>(h, int(n), R, Mout, sig, info);
   else if (n <= 48) launch_blk<double2, 2, 192>(h, int(n), R, Mout, sig, info);
-  else launch_blk<double2, 2, 256>(h, int(n), R, Mout, sig, info);
+  else if (n <= 64) launch_blk<double2, 2, 256>(h, int(n), R, Mout, sig, info);
+  else launch_cl<double2, 4, 2, 8>(h, int(n), R, Mout, sig, info);
 }
 
 }  // namespace lr

@@ -271,7 +271,11 @@ void debug_sweeps(Handle* h, const int32_t* info, int64_t n, const char* kind) {
   fprintf(stderr, "[lr] jacobi %s n=%lld sweeps=%d\n", kind, (long long)n, v);
 }
 
-bool jacobi_reg_supported(int64_t n, bool cplx) { return n >= 2 && n <= (cplx ? 64 : 128); }
+bool jacobi_reg_supported(int64_t n, bool cplx) {
+  // register-resident: one CTA up to 128 real / 64 complex, a DSMEM cluster
+  // (jacobi_blk.cu) up to 256 real / 128 complex
+  return n >= 2 && n <= (jacobi_blk_enabled() ? (cplx ? 128 : 256) : (cplx ? 64 : 128));
+}
 
 void jacobi_reg_f64(Handle* h, int64_t n, const double* R, double* Mout, double* sig,
                     int32_t* info) {
