@@ -182,6 +182,8 @@ def run_ours(args, cfg):
     torch.cuda.set_device(local)
     if world > 1 or args.sharded:
         return run_sharded(args, cfg)
+    if cfg.idx == 5:
+        return run_sparse(args, cfg)
     A = build_input(cfg)
     torch.cuda.synchronize()
     op = lr.DenseOperator(A)
@@ -267,6 +269,27 @@ def run_ours(args, cfg):
         torch.distributed.destroy_process_group()
 
 
+def roofline_sparse(cfg, pev, ms, steps, passes):
+    """Config 5: the dominant kernel is the CSR SpMM (K6), HBM/gather bound;
+    achieved = gather-inclusive algorithmic bytes per launch / launch time."""
+    pk, src = peaks()
+    t = [a.elapsed_time(b) for a, b, *_ in pev]
+    nbytes = [x for _, _, _, x, _ in pev]
+    avg_ms = sum(t) / len(t)
+    achieved = sum(nbytes) / len(nbytes) / (avg_ms / 1e3) / 1e9
+    hbm = pk["hbm_gbs"]
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get(f"cfg{cfg.idx}")
+    return {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+            "frac": round(achieved / hbm, 4), "traffic": traffic,
+            "kernel": "csr_spmm_kernel (K6), gather-inclusive bytes model",
+            "peak_source": f"{src} HBM copy bandwidth (MEASURED_PEAKS.json)",
+            "avg_spmm_ms": round(avg_ms, 4),
+            "spmm_share_of_step": round(sum(t) / (ms * steps), 4)}
+
+
 def roofline(A, cfg, pev, ms, steps, passes, a_bytes):
     """Roofline of the dominant kernel (the pass over A, K1/K2), from the
     CUDA events recorded around every pass inside the timed region."""
@@ -300,6 +323,76 @@ def roofline(A, cfg, pev, ms, steps, passes, a_bytes):
             "step_roofline_ms": round(roof_step_ms, 4),
             "step_roofline_frac": round(roof_step_ms / ms, 4),
             "pass_share_of_step": round(sum(pass_ms) / (ms * steps), 4)}
+
+
+def run_sparse(args, cfg):
+    """Config 5: CSR S (2^21 x 2^21, ~16 nnz/row) + implicit L R^T, q = 3."""
+    import torch
+    import paper_0909_4061_b200 as lr
+    from paper_0909_4061_b200 import core as lrcore
+    rank, world, local = env_rank()
+    S, L, R = workloads.build_cfg5()
+    op = lr.CudaCsrOperator(S, L, R)
+    a_bytes = op.csr_bytes()
+    passes = cfg.passes()
+
+    def step():
+        return lr.randomized_svd(op, cfg.k, cfg.p, cfg.q, cfg.seed, estimate=False)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    lrcore.PASS_EVENTS = []
+    l0 = lr._lib.launch_count()
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.nvtx.range_push("lr_timed")
+        s.record()
+        for _ in range(args.steps):
+            step()
+        e.record()
+        torch.cuda.nvtx.range_pop()
+        torch.cuda.synchronize()
+    launches = lr._lib.launch_count() - l0
+    ms = s.elapsed_time(e) / args.steps
+    pev = lrcore.PASS_EVENTS
+    lrcore.PASS_EVENTS = None
+    line = {
+        "metric": "rank-k rSVD time & A-GB/s (% roofline) at 1/2/4/8 B200 vs host-CPU ref",
+        "value": round(passes * a_bytes / (ms / 1e3) / 1e9, 3), "unit": "A-GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded CSR + Gaussian low-rank factors, BASELINE.json config 5)",
+        "config": {"workload": cfg.name, "config_index": 5, "m": cfg.m, "n": cfg.n, "nnz": op.nnz,
+                   "k": cfg.k, "ell": cfg.ell, "q": cfg.q, "passes": passes,
+                   "a_bytes": a_bytes, "a_bytes_model": "CSR values + int32 cols + int64 rowptr",
+                   "l2": "inputs larger than L2 (CSR 0.4 GB, X 0.8 GB), no flush",
+                   "parallelism": "single GPU"},
+        "roofline": roofline_sparse(cfg, pev, ms, args.steps, passes),
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "e2e": {"skipped": "host CSR transpose of the operator constructor dominates; "
+                           "not measured for config 5 in this round"},
+    }
+    if not args.no_cpu and rank == 0:
+        # bounded CPU sample: the oracle (scipy CSR, single-threaded SpMM) on a
+        # 2^17-row instance of the same recipe, rate in A-GB/s
+        from oracle import lowrank_oracle as O
+        S2, L2, R2 = workloads.build_cfg5(n=1 << 17)
+        op2 = O.SparsePlusLowRank(S2, L2, R2)
+        t0 = time.perf_counter()
+        O.rsvd(op2, cfg.k, cfg.p, cfg.q, cfg.seed, estimate=False)
+        dt = time.perf_counter() - t0
+        b2 = S2.nnz * 12 + (S2.shape[0] + 1) * 8
+        line["cpu_baseline"] = {"value": round(passes * b2 / dt / 1e9, 4), "unit": "A-GB/s",
+                                "cores": os.cpu_count(), "kind": "port",
+                                "sample": f"config-5 recipe at n = 2^17 ({S2.nnz} nnz), one rSVD "
+                                          f"by oracle/lowrank_oracle.py (scipy CSR), {dt:.2f} s",
+                                "seconds": round(dt, 3)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
 
 
 def run_sharded(args, cfg):
@@ -394,7 +487,7 @@ def run_sharded(args, cfg):
     if not args.no_e2e:
         host = torch.empty(A.shape, dtype=A.dtype, pin_memory=True)
         host.copy_(A)
-        A_np = host.numpy()
+        A_np = host   # pinned CPU rows (async H2D)
         k_e2e = max(1, min(args.steps, 5))
         sharded_randomized_svd(A_np, cfg.k, cfg.p, cfg.q, cfg.seed, sketch=sketch,
                                estimate=False)
@@ -424,11 +517,11 @@ def e2e_measure(args, cfg, A, lr):
     import torch
     host = torch.empty(A.shape, dtype=A.dtype, pin_memory=True)
     host.copy_(A)
-    A_np = host.numpy()
     steps = max(1, min(args.steps, 5))
 
     def once():
-        b, f, _ = lr.randomized_svd(A_np, cfg.k, cfg.p, cfg.q, cfg.seed, sketch=cfg.sketch,
+        # pinned CPU tensor in (async H2D at full PCIe rate), numpy factors out
+        b, f, _ = lr.randomized_svd(host, cfg.k, cfg.p, cfg.q, cfg.seed, sketch=cfg.sketch,
                                     estimate=False)
         return f
 
@@ -445,21 +538,43 @@ def e2e_measure(args, cfg, A, lr):
             "d2h_bytes_per_step": int(d2h), "steps": steps}
 
 
+def reference_sample(cfg):
+    """(operator, A-bytes of one pass, sample description) for the reference
+    arm: the full matrix where one CPU rSVD takes seconds (configs 1, 2),
+    otherwise a bounded sample of the same recipe (rows / size reduced)."""
+    from oracle import lowrank_oracle as O
+    import torch
+    if cfg.idx in (1, 2):
+        if torch.cuda.is_available():
+            A = build_input(cfg).cpu().numpy()
+            torch.cuda.empty_cache()
+        else:
+            A, _ = workloads.synthetic_explicit(cfg.m, cfg.n, workloads.spectrum(cfg.idx, cfg.n),
+                                                cfg.seed)
+        return O.Dense(A), A.size * A.itemsize, f"full {cfg.name} matrix"
+    if cfg.idx == 3:
+        A = workloads.build_cfg3()[:1024]
+        return O.Dense(A), A.size * A.itemsize, "config-3 recipe, first 1024 of 8192 rows"
+    if cfg.idx == 4:
+        A, _ = workloads.build_cfg4_host(m=65536)
+        return O.Dense(A, promote=True), A.size * 4, "config-4 recipe at 65536 of 2^20 rows"
+    S, L, R = workloads.build_cfg5(n=1 << 17)
+    return (O.SparsePlusLowRank(S, L, R), S.nnz * 12 + (S.shape[0] + 1) * 8,
+            "config-5 recipe at n = 2^17 (scipy CSR, single-threaded SpMM)")
+
+
 def run_reference(args, cfg):
+    """--impl reference: the reference algorithm's CPU implementation (the
+    oracle port of the pure-Python reference package, numpy/OpenBLAS with
+    all host threads) on the same recipe; rank 0 only under torchrun."""
     rank, world, local = env_rank()
     if rank != 0:
         return
     import torch
     if torch.cuda.is_available():
         torch.cuda.set_device(local)
-        A_host = build_input(cfg).cpu().numpy()
-        torch.cuda.empty_cache()
-    else:
-        A_host, _ = workloads.synthetic_explicit(cfg.m, cfg.n, workloads.spectrum(cfg.idx, cfg.n),
-                                                 cfg.seed)
     from oracle import lowrank_oracle as O
-    op = O.Dense(A_host)
-    a_bytes = A_host.size * A_host.itemsize
+    op, a_bytes, sample = reference_sample(cfg)
     for _ in range(args.warmup):
         O.rsvd(op, cfg.k, cfg.p, cfg.q, cfg.seed, sketch=cfg.sketch, estimate=False)
     t0 = time.perf_counter()
@@ -471,14 +586,16 @@ def run_reference(args, cfg):
         "metric": "rank-k rSVD time & A-GB/s (% roofline) at 1/2/4/8 B200 vs host-CPU ref",
         "impl": "reference", "value": round(v, 4), "unit": "A-GB/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3),
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": {"f64": "f64", "f32": "f64 (reference upcast)", "c64": "c128 (reference upcast)"
+                  }.get(cfg.dtype, "f64"),
         "data": "synthetic (seeded, BASELINE.json config recipe; see workloads.py)",
         "config": {"workload": cfg.name, "config_index": cfg.idx, "m": cfg.m, "n": cfg.n,
                    "k": cfg.k, "ell": cfg.ell, "q": cfg.q, "passes": cfg.passes()},
         "cpu_baseline": {"value": round(v, 4), "unit": "A-GB/s", "cores": os.cpu_count(),
                          "kind": "port",
-                         "sample": f"full {cfg.name} rSVD per step (oracle/lowrank_oracle.py, "
-                                   "numpy/OpenBLAS, all host threads; Stage A + direct SVD)"},
+                         "sample": f"{sample}: one rSVD (Stage A + direct SVD) per step by "
+                                   "oracle/lowrank_oracle.py, numpy/OpenBLAS, all host threads"},
         "e2e": {"value": round(v, 4), "unit": "A-GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }

@@ -45,7 +45,11 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force=False, verbose=False, extra=()):
+def build(force=False, verbose=False, extra=(), out=None, obj=None):
+    """extra: additional nvcc flags (e.g. -D tuning macros); out/obj: build a
+    variant library elsewhere (development sweeps; LR_LIB selects it)."""
+    OUT = out or globals()["OUT"]
+    OBJ = obj or globals()["OBJ"]
     os.makedirs(OBJ, exist_ok=True)
     srcs = sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cu"))
     cc = nvcc()

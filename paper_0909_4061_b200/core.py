@@ -55,8 +55,11 @@ def _torch_compute_dtype(t):
 
 
 def is_device_array(x):
+    """CUDA tensors stay on the device (device in -> device out); numpy arrays
+    and CPU torch tensors are host data (uploaded, results returned as numpy;
+    a pinned CPU tensor is uploaded asynchronously at full PCIe rate)."""
     torch = _torch()
-    return torch.is_tensor(x)
+    return torch.is_tensor(x) and x.is_cuda
 
 
 def to_device(x, dtype=None, device=None):
@@ -188,13 +191,13 @@ class DenseOperator(MatVecOperator):
 
     def __init__(self, A, device=None, validate=True):
         torch = _torch()
-        host = not torch.is_tensor(A)
-        shape = np.shape(A) if host else tuple(A.shape)
+        host = not is_device_array(A)
+        shape = tuple(A.shape) if torch.is_tensor(A) else np.shape(A)
         if len(shape) != 2:
             raise ValueError(f"matrix must be 2-D, got shape {shape}")
         if shape[0] == 0 or shape[1] == 0:
             raise ValueError("matrix must be nonempty")
-        t = to_device(A, None if host else _torch_compute_dtype(A), device)
+        t = to_device(A, _torch_compute_dtype(A) if torch.is_tensor(A) else None, device)
         super().__init__(*t.shape)
         self.array = t
         self.code = _lib.dtype_code(t.dtype)

@@ -19,8 +19,14 @@ namespace lr {
 namespace {
 
 constexpr int BM = 128;
-constexpr int BK = 16;
-constexpr int STAGES = 3;
+#ifndef LR_DMMA_BK
+#define LR_DMMA_BK 16
+#endif
+#ifndef LR_DMMA_STAGES
+#define LR_DMMA_STAGES 3
+#endif
+constexpr int BK = LR_DMMA_BK;
+constexpr int STAGES = LR_DMMA_STAGES;
 constexpr int THREADS = 256;
 constexpr int AS_NN = BK + 4;    // row stride (f64) of the A tile, non-transposed
 constexpr int AS_TN = BM + 4;    // row stride of the A tile, transposed
@@ -299,15 +305,17 @@ __global__ void cplx_combine_t(int64_t M, int64_t N, const double* __restrict__ 
 
 int64_t choose_splits(int sm_count, int64_t tiles, int64_t K) {
   // Fill the machine with whole waves (1 CTA / SM); each split keeps >= 4
-  // k-tiles; mild preference for fewer splits (partial traffic).
-  const int64_t max_s = std::max<int64_t>(1, std::min<int64_t>(64, K / (4 * BK)));
+  // k-tiles; each extra wave costs a little (split-K partial traffic).  Few
+  // tiles (Gram / Q^T Z of a tall panel: one or two tiles) take up to one
+  // split per SM.
+  const int64_t max_s = std::max<int64_t>(1, std::min<int64_t>(4096, K / (4 * BK)));
   int64_t best_s = 1;
   double best = -1.0;
   for (int64_t s = 1; s <= max_s; ++s) {
     const double ctas = double(tiles * s);
     const double waves = ctas / double(sm_count);
     const double eff = waves / std::ceil(waves);
-    const double score = eff - 0.004 * double(s - 1);
+    const double score = eff - 0.01 * std::ceil(waves);
     if (score > best + 1e-9) {
       best = score;
       best_s = s;

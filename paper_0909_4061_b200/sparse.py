@@ -22,7 +22,10 @@ class CudaCsrOperator(MatVecOperator):
 
     device_native = True
 
-    def __init__(self, S, L=None, R=None, device=None):
+    def __init__(self, S, L=None, R=None, device=None, host_io=False):
+        """host_io: return numpy factors from the range finders / SVD (default:
+        CUDA tensors -- the operator lives on the device, like a DenseOperator
+        built from a CUDA tensor)."""
         torch = _torch()
         import scipy.sparse as sp
         if isinstance(S, tuple):
@@ -52,7 +55,7 @@ class CudaCsrOperator(MatVecOperator):
         if self.L is not None and (self.L.shape[0] != m or self.R.shape[0] != n
                                    or self.L.shape[1] != self.R.shape[1]):
             raise ValueError("low-rank factors do not match the sparse part")
-        self.host_io = True
+        self.host_io = bool(host_io)
         self.dtype = torch.float64
 
     def csr_bytes(self):
@@ -60,7 +63,25 @@ class CudaCsrOperator(MatVecOperator):
         return self.nnz * (8 + 4) + (self.m + 1) * 8
 
     def _spmm(self, csr, rows, X, Y, accumulate):
+        from . import core
         rowptr, col, val = csr
+        if core.PASS_EVENTS is not None:   # bench.py: per-launch timing + bytes model
+            torch = _torch()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.nvtx.range_push("lr_pass")
+            s.record()
+            self._spmm_launch(rowptr, col, val, rows, X, Y, accumulate)
+            e.record()
+            torch.cuda.nvtx.range_pop()
+            ell = X.shape[1]
+            # gather-inclusive algorithmic bytes: CSR arrays, one
+            # X row (ell doubles) per nonzero, Y read-modify-write
+            nbytes = self.csr_bytes() + self.nnz * ell * 8 + rows * ell * 8 * (2 if accumulate else 1)
+            core.PASS_EVENTS.append((s, e, 2 * self.nnz * ell, nbytes, ell))
+            return
+        self._spmm_launch(rowptr, col, val, rows, X, Y, accumulate)
+
+    def _spmm_launch(self, rowptr, col, val, rows, X, Y, accumulate):
         _lib.call("lr_csr_spmm", _lib.handle(X.device.index), _lib.F64, rows, X.shape[0],
                   X.shape[1], _lib.ptr(rowptr), _lib.ptr(col), _lib.ptr(val), _lib.ptr(X),
                   _lib.ld(X), _lib.ptr(Y), _lib.ld(Y), 1 if accumulate else 0)

@@ -179,6 +179,6 @@ def test_cfg5_reduced(golden):
     g = golden("cfg5s")
     c = workloads.CONFIGS[5]
     S, L, R = workloads.build_cfg5(n=1 << 16)
-    op = lr().CudaCsrOperator(S, L, R)
+    op = lr().CudaCsrOperator(S, L, R, host_io=True)
     basis, f, est = lr().randomized_svd(op, c.k, c.p, c.q, c.seed)
     check_against_golden(g, f, basis, est, 1e-10, floor=1e-6)

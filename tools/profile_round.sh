@@ -8,7 +8,7 @@
 # Each bench command first runs once without ncu (it must exit 0).
 set -u
 OUT=${OUT:-gpurun_out/prof}
-CONFIGS=${CONFIGS:-"2 4"}
+CONFIGS=${CONFIGS:-"2 4 5"}
 mkdir -p "$OUT"
 NCU=/usr/local/cuda/bin/ncu
 for C in $CONFIGS; do
@@ -16,9 +16,10 @@ for C in $CONFIGS; do
   $B > "$OUT/bench_cfg$C.json" 2> "$OUT/bench_cfg$C.err" || { echo "bench cfg$C failed"; continue; }
   $NCU --nvtx --nvtx-include "lr_timed/" --metrics gpu__time_duration.sum --clock-control none \
     --csv --log-file "$OUT/launches_cfg$C.csv" $B > /dev/null 2>&1
-  $NCU --nvtx --nvtx-include "lr_pass/" --set full --clock-control none --import-source on -c 2 \
+  $NCU --nvtx --nvtx-include "lr_pass/" --set full --clock-control none --import-source on \
+    -k regex:"gemm_f64_kernel|gemm_f32_tc_kernel|csr_spmm_kernel" -c 2 \
     -o "$OUT/full_cfg${C}_pass" -f $B > /dev/null 2>&1
   $NCU --nvtx --nvtx-include "lr_timed/" --set full --clock-control none --import-source on \
-    -k regex:"${SMALL_KERNELS:-chol_drop|jacobi}" -c 2 -o "$OUT/full_cfg${C}_small" -f $B > /dev/null 2>&1
+    -k regex:"${SMALL_KERNELS:-chol|jacobi}" -c 2 -o "$OUT/full_cfg${C}_small" -f $B > /dev/null 2>&1
 done
 ls -la "$OUT"
