@@ -219,7 +219,7 @@ void orth_fast_impl(Handle* h, int dtype, int64_t m, int64_t ell, const void* Y,
   chol_any(h, dtype, ell, G, tol, unres, 0.0, P, R, h->d_info);
   apply_right(h, dtype, m, ell, ell, Y, ldy, P, ell, Q1, ell);
   gram_any(h, dtype, m, ell, Q1, ell, G);
-  chol_any(h, dtype, ell, G, tol, unres, 0.0, P, R, h->d_info);
+  chol_near_identity(h, wide_of(dtype), ell, G, tol, unres, P, R, h->d_info);
   apply_right(h, dtype, m, ell, ell, Q1, ell, P, ell, Q, ldq);
 }
 
@@ -244,7 +244,7 @@ void small_svd_fast_impl(Handle* h, int dtype, int64_t r, int64_t c, const void*
   chol_any(h, dtype, r, G, 0.0, unres, 0.0, P1, R1, h->d_info);
   apply_right(h, dtype, c, r, r, Bh, r, P1, r, Q1, r);
   gram_any(h, dtype, c, r, Q1, r, G);
-  chol_any(h, dtype, r, G, 0.0, unres, 0.0, P, R2, h->d_info);
+  chol_near_identity(h, wd, r, G, 0.0, unres, P, R2, h->d_info);
   apply_right(h, dtype, c, r, r, Q1, r, P, r, Q2, r);
   trmm_upper(h, wd, r, R2, R1, R);
   if (jacobi_reg_supported(r, is_complex(dtype))) {

@@ -45,7 +45,9 @@ template <typename T, bool SMEM, int CHOL_THREADS>
 __global__ void __launch_bounds__(CHOL_THREADS, 1)
 chol_drop_kernel(int n, const T* __restrict__ G, double drop_tol, double unres_rel,
                  double shift_coef, T* __restrict__ P, T* __restrict__ Rout,
-                 int32_t* __restrict__ info, T* gW, int32_t* status) {
+                 int32_t* __restrict__ info, T* gW, int32_t* status,
+                 const int32_t* __restrict__ gate) {
+  if (gate && *gate == 0) return;
   using S = Sc<T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* __restrict__ W;
@@ -253,7 +255,7 @@ void launch_chol(Handle* h, int64_t ell, const T* G, double drop_tol, double unr
     auto launch = [&](auto kern, int threads) {
       LR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(full)));
       kern<<<1, threads, full, h->stream>>>(n, G, drop_tol, unres_rel, shift_coef, P, R, info,
-                                            nullptr, h->status);
+                                            nullptr, h->status, h->gate);
     };
     if (nt <= 128) launch(chol_drop_kernel<T, true, 128>, 128);
     else if (nt <= 256) launch(chol_drop_kernel<T, true, 256>, 256);
@@ -264,7 +266,7 @@ void launch_chol(Handle* h, int64_t ell, const T* G, double drop_tol, double unr
     auto kern = chol_drop_kernel<T, false, 512>;
     LR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(tail)));
     kern<<<1, 512, tail, h->stream>>>(n, G, drop_tol, unres_rel, shift_coef, P, R, info, gW,
-                                      h->status);
+                                      h->status, h->gate);
   }
   LR_CHECK_LAUNCH();
 }

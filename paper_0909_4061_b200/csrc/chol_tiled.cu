@@ -51,7 +51,8 @@ chol_tiled_kernel(int n, const T* __restrict__ G, int64_t ldg, double drop_tol, 
                   double shift_coef, T* __restrict__ P, T* __restrict__ Rout,
                   int32_t* __restrict__ info, T* __restrict__ gRt, int32_t* status,
                   const double* __restrict__ trace_dev, const T* __restrict__ diag_src,
-                  int64_t diag_stride, bool compact) {
+                  int64_t diag_stride, bool compact, const int32_t* __restrict__ gate) {
+  if (gate && *gate == 0) return;
   // Block calls (chol_blocked below): trace_dev supplies the trace of the
   // whole Gram (drop threshold and shift), diag_src its original diagonal for
   // this block (the unresolved-pivot test), and compact = false writes P
@@ -251,7 +252,7 @@ void launch(Handle* h, int n, const T* G, int64_t ldg, double drop_tol, double u
     LR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     kern<<<1, threads, smem, h->stream>>>(n, G, ldg, drop_tol, unres_rel, shift_coef, P, R, info,
                                           gRt, h->status, trace_dev, diag_src, diag_stride,
-                                          compact);
+                                          compact, h->gate);
   };
   if (threads <= 320) {
     if (in_smem) go(chol_tiled_kernel<T, true, 320>);
@@ -410,6 +411,97 @@ void chol_blocked_f64(Handle* h, int64_t n, const double* G, double drop_tol, do
 void chol_blocked_c128(Handle* h, int64_t n, const double2* G, double drop_tol, double unres_rel,
                        double shift_coef, double2* P, double2* R, int32_t* info) {
   chol_blocked<double2>(h, LR_C128, int(n), G, drop_tol, unres_rel, shift_coef, P, R, info);
+}
+
+// ---------------------------------------------------------------------------
+namespace {
+
+// Second CholeskyQR pass: G = Q1^H Q1 = I + E with E tiny when the first
+// pass succeeded.  Then R = I + N, N = triu(E, 1) + diag(Re E) / 2, gives
+// R^H R = I + E + O(E^2) and P = R^{-1} = I - N + O(E^2), so
+// (Q1 P)^H (Q1 P) = I + O(E^2): for max|E| <= 1e-8 the first-order factor is
+// as good as the exact one in double precision, with no sequential
+// dependency.  One CTA checks max|E|, writes the first-order P / R / info
+// and clears *gate; otherwise it sets *gate and the exact kernel (launched
+// right behind it, gated) runs.
+template <typename T>
+__global__ void near_identity_kernel(int n, const T* __restrict__ G, T* __restrict__ P,
+                                     T* __restrict__ Rout, int32_t* __restrict__ info,
+                                     int32_t* __restrict__ gate, double thr) {
+  using S = Sc<T>;
+  __shared__ int s_bad;
+  if (threadIdx.x == 0) s_bad = 0;
+  __syncthreads();
+  int bad = 0;
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    const int i = e / n, k = e - i * n;
+    const T g = G[e];
+    const double dev = (i == k) ? fabs(S::re(g) - 1.0) + fabs(S::abs2(g) - S::re(g) * S::re(g))
+                                : sqrt(S::abs2(g));
+    if (!(dev <= thr)) bad = 1;   // also catches NaN
+  }
+  if (bad) atomicOr(&s_bad, 1);
+  __syncthreads();
+  const bool ok = s_bad == 0;
+  if (ok) {
+    for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+      const int i = e / n, k = e - i * n;
+      T nv = S::zero();
+      if (k > i) nv = G[e];
+      else if (k == i) nv = S::make(0.5 * (S::re(G[e]) - 1.0), 0.0);
+      Rout[e] = (k == i) ? S::add(S::one(), nv) : nv;
+      P[e] = (k == i) ? S::sub(S::one(), nv) : S::scale(nv, -1.0);
+    }
+  }
+  if (threadIdx.x == 0) {
+    if (ok) {
+      info[0] = n;
+      info[1] = 0;
+      info[2] = 0;
+    }
+    *gate = ok ? 0 : 1;
+  }
+}
+
+}  // namespace
+
+void chol_near_identity(Handle* h, int dtype, int64_t n, const void* G, double drop_tol,
+                        double unres_rel, void* P, void* R, int32_t* info) {
+  const bool cplx = dtype == LR_C64 || dtype == LR_C128;
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("LR_CHOL_NEARID");
+    mode = (e && e[0] == '0') ? 0 : 1;
+  }
+  if (!mode || n > MAXN) {   // exact (the blocked path is not gated)
+    if (cplx) chol_drop_c128(h, n, static_cast<const double2*>(G), drop_tol, unres_rel, 0.0,
+                             static_cast<double2*>(P), static_cast<double2*>(R), info);
+    else chol_drop_f64(h, n, static_cast<const double*>(G), drop_tol, unres_rel, 0.0,
+                       static_cast<double*>(P), static_cast<double*>(R), info);
+    return;
+  }
+  int32_t* gate = pool_alloc_t<int32_t>(h, 1);
+  if (cplx)
+    near_identity_kernel<double2><<<1, 1024, 0, h->stream>>>(
+        int(n), static_cast<const double2*>(G), static_cast<double2*>(P),
+        static_cast<double2*>(R), info, gate, 1e-8);
+  else
+    near_identity_kernel<double><<<1, 1024, 0, h->stream>>>(
+        int(n), static_cast<const double*>(G), static_cast<double*>(P), static_cast<double*>(R),
+        info, gate, 1e-8);
+  LR_CHECK_LAUNCH();
+  const int32_t* saved = h->gate;
+  h->gate = gate;
+  try {
+    if (cplx) chol_drop_c128(h, n, static_cast<const double2*>(G), drop_tol, unres_rel, 0.0,
+                             static_cast<double2*>(P), static_cast<double2*>(R), info);
+    else chol_drop_f64(h, n, static_cast<const double*>(G), drop_tol, unres_rel, 0.0,
+                       static_cast<double*>(P), static_cast<double*>(R), info);
+  } catch (...) {
+    h->gate = saved;
+    throw;
+  }
+  h->gate = saved;
 }
 
 // Measured on B200 (tools/small_probe.py, CUDA-graph timed): the tiled

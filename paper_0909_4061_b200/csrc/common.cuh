@@ -73,6 +73,10 @@ struct Handle {
   int32_t* d_info = nullptr;   // small device scratch for composite decisions
   int32_t* h_info = nullptr;   // pinned mirror
   double* d_dscratch = nullptr;
+  // device int read by the Cholesky kernels at entry: when set and *gate == 0
+  // the launch returns at once (the near-identity fast path already produced
+  // the factor; see chol_near_identity).  Host-sync free.
+  const int32_t* gate = nullptr;
 };
 
 void pool_reset(Handle* h);
@@ -152,6 +156,11 @@ void jacobi_svd_c128(Handle* h, int64_t rows, int64_t n, const double2* M, doubl
 // (by size; LR_CHOL=smem|tiled forces one kernel)
 bool chol_tiled_supported(int64_t n, bool cplx);
 bool chol_blocked_supported(int64_t n);
+// Cholesky-with-deletion of a Gram that is expected to be I + E (second
+// CholeskyQR pass): first-order factor when max|E| <= 1e-8, exact otherwise
+// (decided on the device, no host synchronization).
+void chol_near_identity(Handle* h, int dtype, int64_t n, const void* G, double drop_tol,
+                        double unres_rel, void* P, void* R, int32_t* info);
 void chol_blocked_f64(Handle* h, int64_t n, const double* G, double drop_tol, double unres_rel,
                       double shift_coef, double* P, double* R, int32_t* info);
 void chol_blocked_c128(Handle* h, int64_t n, const double2* G, double drop_tol,
