@@ -167,6 +167,14 @@ int lr_srft(lr_handle_t h, int dtype, int64_t m, int64_t n, int64_t ell,
             const void* A, int64_t lda, const void* d, const int32_t* picks,
             double scale, void* Y, int64_t ldy);
 
+/* lr_srft given the operator's max |a| (from lr_check_finite).  complex64
+ * with ell <= 128 runs the SRFT as one tensor-core pass over A against the
+ * ell picked columns of diag(d) F (the lr_gemm_scaled kernel); a_amax < 0
+ * means unknown (reduced on the device). */
+int lr_srft_scaled(lr_handle_t h, int dtype, int64_t m, int64_t n, int64_t ell,
+                   const void* A, int64_t lda, double a_amax, const void* d,
+                   const int32_t* picks, double scale, void* Y, int64_t ldy);
+
 /* Unitary DFT of each row of X (rows x n, n a power of two), in place
  * (reference sketch.py:179-200). */
 int lr_dft_rows(lr_handle_t h, int dtype, int64_t rows, int64_t n, void* X, int64_t ldx);

@@ -49,6 +49,8 @@ thread_local std::string g_err;
 constexpr double U64 = 1.1102230246251565e-16;
 
 int wide_of(int dtype) { return is_complex(dtype) ? LR_C128 : LR_F64; }
+// max |G - I| for the first-order second CholeskyQR pass (chol_near_identity)
+double near_id_thr(int dtype) { return (dtype == LR_F32 || dtype == LR_C64) ? 1e-4 : 1e-8; }
 size_t wide_size(int dtype) { return is_complex(dtype) ? 16 : 8; }
 
 struct Info {
@@ -219,7 +221,8 @@ void orth_fast_impl(Handle* h, int dtype, int64_t m, int64_t ell, const void* Y,
   chol_any(h, dtype, ell, G, tol, unres, 0.0, P, R, h->d_info);
   apply_right(h, dtype, m, ell, ell, Y, ldy, P, ell, Q1, ell);
   gram_any(h, dtype, m, ell, Q1, ell, G);
-  chol_near_identity(h, wide_of(dtype), ell, G, tol, unres, P, R, h->d_info);
+  chol_near_identity(h, wide_of(dtype), ell, G, tol, unres, P, R, h->d_info,
+                     near_id_thr(dtype));
   apply_right(h, dtype, m, ell, ell, Q1, ell, P, ell, Q, ldq);
 }
 
@@ -244,7 +247,7 @@ void small_svd_fast_impl(Handle* h, int dtype, int64_t r, int64_t c, const void*
   chol_any(h, dtype, r, G, 0.0, unres, 0.0, P1, R1, h->d_info);
   apply_right(h, dtype, c, r, r, Bh, r, P1, r, Q1, r);
   gram_any(h, dtype, c, r, Q1, r, G);
-  chol_near_identity(h, wd, r, G, 0.0, unres, P, R2, h->d_info);
+  chol_near_identity(h, wd, r, G, 0.0, unres, P, R2, h->d_info, near_id_thr(dtype));
   apply_right(h, dtype, c, r, r, Q1, r, P, r, Q2, r);
   trmm_upper(h, wd, r, R2, R1, R);
   if (jacobi_reg_supported(r, is_complex(dtype))) {
@@ -746,22 +749,29 @@ int lr_estimate_tail(lr_handle_t hh, int dtype, int64_t m, int64_t k, int64_t r,
   API_END
 }
 
-int lr_srft(lr_handle_t hh, int dtype, int64_t m, int64_t n, int64_t ell, const void* A,
-            int64_t lda, const void* d, const int32_t* picks, double scale, void* Y,
-            int64_t ldy) {
+int lr_srft_scaled(lr_handle_t hh, int dtype, int64_t m, int64_t n, int64_t ell, const void* A,
+                   int64_t lda, double a_amax, const void* d, const int32_t* picks, double scale,
+                   void* Y, int64_t ldy) {
   API_BEGIN
   Handle* h = H(hh);
   LR_REQUIRE(dtype == LR_C64 || dtype == LR_C128, LR_EINVAL, "lr_srft: complex dtypes only");
   LR_REQUIRE(n >= 1 && (n & (n - 1)) == 0, LR_EUNSUPPORTED,
              "lr_srft: n must be a power of two (Bluestein path not built)");
+  LR_REQUIRE(ell >= 1 && ell <= n, LR_EINVAL, "lr_srft: need 1 <= ell <= n");
   lr::pool_reset(h);
   if (dtype == LR_C64)
     lr::srft_c64(h, m, n, ell, static_cast<const float2*>(A), lda, static_cast<const float2*>(d),
-                 picks, float(scale), static_cast<float2*>(Y), ldy);
+                 picks, float(scale), static_cast<float2*>(Y), ldy, a_amax);
   else
     lr::srft_c128(h, m, n, ell, static_cast<const double2*>(A), lda,
                   static_cast<const double2*>(d), picks, scale, static_cast<double2*>(Y), ldy);
   API_END
+}
+
+int lr_srft(lr_handle_t hh, int dtype, int64_t m, int64_t n, int64_t ell, const void* A,
+            int64_t lda, const void* d, const int32_t* picks, double scale, void* Y,
+            int64_t ldy) {
+  return lr_srft_scaled(hh, dtype, m, n, ell, A, lda, -1.0, d, picks, scale, Y, ldy);
 }
 
 int lr_dft_rows(lr_handle_t hh, int dtype, int64_t rows, int64_t n, void* X, int64_t ldx) {

@@ -466,7 +466,7 @@ __global__ void near_identity_kernel(int n, const T* __restrict__ G, T* __restri
 }  // namespace
 
 void chol_near_identity(Handle* h, int dtype, int64_t n, const void* G, double drop_tol,
-                        double unres_rel, void* P, void* R, int32_t* info) {
+                        double unres_rel, void* P, void* R, int32_t* info, double thr) {
   const bool cplx = dtype == LR_C64 || dtype == LR_C128;
   static int mode = -1;
   if (mode < 0) {
@@ -484,11 +484,11 @@ void chol_near_identity(Handle* h, int dtype, int64_t n, const void* G, double d
   if (cplx)
     near_identity_kernel<double2><<<1, 1024, 0, h->stream>>>(
         int(n), static_cast<const double2*>(G), static_cast<double2*>(P),
-        static_cast<double2*>(R), info, gate, 1e-8);
+        static_cast<double2*>(R), info, gate, thr);
   else
     near_identity_kernel<double><<<1, 1024, 0, h->stream>>>(
         int(n), static_cast<const double*>(G), static_cast<double*>(P), static_cast<double*>(R),
-        info, gate, 1e-8);
+        info, gate, thr);
   LR_CHECK_LAUNCH();
   const int32_t* saved = h->gate;
   h->gate = gate;

@@ -157,10 +157,11 @@ void jacobi_svd_c128(Handle* h, int64_t rows, int64_t n, const double2* M, doubl
 bool chol_tiled_supported(int64_t n, bool cplx);
 bool chol_blocked_supported(int64_t n);
 // Cholesky-with-deletion of a Gram that is expected to be I + E (second
-// CholeskyQR pass): first-order factor when max|E| <= 1e-8, exact otherwise
-// (decided on the device, no host synchronization).
+// CholeskyQR pass): first-order factor when max|E| <= thr (its O(E^2) error
+// must sit below the panel's rounding: 1e-8 for fp64 panels, 1e-4 for fp32),
+// exact otherwise (decided on the device, no host synchronization).
 void chol_near_identity(Handle* h, int dtype, int64_t n, const void* G, double drop_tol,
-                        double unres_rel, void* P, void* R, int32_t* info);
+                        double unres_rel, void* P, void* R, int32_t* info, double thr);
 void chol_blocked_f64(Handle* h, int64_t n, const double* G, double drop_tol, double unres_rel,
                       double shift_coef, double* P, double* R, int32_t* info);
 void chol_blocked_c128(Handle* h, int64_t n, const double2* G, double drop_tol,
@@ -211,7 +212,8 @@ void scale_col(Handle* h, int dtype, int64_t rows, const void* src, int64_t lds,
 
 // srft.cu ---------------------------------------------------------------------
 void srft_c64(Handle* h, int64_t m, int64_t n, int64_t ell, const float2* A, int64_t lda,
-              const float2* d, const int32_t* picks, float scale, float2* Y, int64_t ldy);
+              const float2* d, const int32_t* picks, float scale, float2* Y, int64_t ldy,
+              double a_amax = -1.0);
 void srft_c128(Handle* h, int64_t m, int64_t n, int64_t ell, const double2* A, int64_t lda,
                const double2* d, const int32_t* picks, double scale, double2* Y, int64_t ldy);
 void dft_rows(Handle* h, int dtype, int64_t rows, int64_t n, void* X, int64_t ldx);

@@ -91,6 +91,15 @@ void gemm_c64_hint(Handle* h, bool transA, bool conjA, int64_t M, int64_t N, int
 void gemm_c64(Handle* h, bool transA, bool conjA, int64_t M, int64_t N, int64_t K,
               const float2* A, int64_t lda, const float2* B, int64_t ldb, float2* C,
               int64_t ldc) {
+  // large products on the tcgen05 split (real view: 2N <= 256 columns), the
+  // rest on the SIMT kernel -- as gemm_f32
+  const bool big = double(M) * double(N) * double(K) >= double(1 << 24) &&
+                   (transA ? K : M) >= 1024 && 2 * N <= 256;
+  if (big && h->f32_mode == LR_F32_SPLIT3 && (lda % 2) == 0 &&
+      (reinterpret_cast<uintptr_t>(A) & 15) == 0) {
+    gemm_c64_hint(h, transA, conjA, M, N, K, A, lda, -1.0, B, ldb, C, ldc);
+    return;
+  }
   gemm_c64_simt(h, transA, conjA, M, N, K, A, lda, B, ldb, C, ldc);
 }
 

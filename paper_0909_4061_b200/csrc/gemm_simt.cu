@@ -163,7 +163,8 @@ void gram_c64(Handle* h, int64_t m, int64_t ell, const float2* Y, int64_t ldy, d
   // D (2 ell x 2 ell) = Y_real^T Y_real; G = combine(conj)
   double* D = pool_alloc_t<double>(h, size_t(4) * ell * ell);
   const float* Yr = reinterpret_cast<const float*>(Y);
-  simt_gemm<double, double>(h, true, 2 * ell, 2 * ell, m, Yr, 2 * ldy, Yr, 2 * ldy, D, 2 * ell);
+  // DMMA on the real view (fp32 staged, widened to fp64: exact products)
+  gemm_f64_from_f32(h, true, 2 * ell, 2 * ell, m, Yr, 2 * ldy, Yr, 2 * ldy, D, 2 * ell);
   const int blocks = int(std::max<int64_t>(1, ceil_div(ell * ell, 256)));
   cplx_combine_t_any<double, double2><<<blocks, 256, 0, h->stream>>>(ell, ell, D, true, G, ell);
   LR_CHECK_LAUNCH();

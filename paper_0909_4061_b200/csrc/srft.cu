@@ -8,6 +8,8 @@
 // an in-place radix-2 DIT FFT in shared memory, and only the ell picked bins
 // are written back (the sketch is HBM-read-bound: one pass over A, ell/n of
 // it written).  Twiddles come from sincospi of exact dyadic arguments.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace lr {
@@ -108,8 +110,50 @@ void launch_srft(Handle* h, int64_t m, int64_t n, int64_t ell, const C* A, int64
 
 }  // namespace
 
+namespace {
+
+// The SRFT restricted to its ell picked bins is the n x ell matrix
+//   X[k, t] = scale n^{-1/2} d_k exp(-2 pi i k picks_t / n),
+// so Y = A X is one more pass over A.  Entries in fp64 from the exact
+// residue (k picks_t) mod n, stored as complex64.
+__global__ void srft_matrix_kernel(int64_t n, int64_t ell, const float2* __restrict__ d,
+                                   const int32_t* __restrict__ picks, double scale,
+                                   float2* __restrict__ X) {
+  const double sn = scale / sqrt(double(n));
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n * ell;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t k = e / ell, t = e - k * ell;
+    const int64_t r = (k * int64_t(picks[t])) % n;
+    double sv, cv;
+    sincospi(-2.0 * double(r) / double(n), &sv, &cv);
+    const double dr = d[k].x, di = d[k].y;
+    X[e] = make_float2(float(sn * (dr * cv - di * sv)), float(sn * (dr * sv + di * cv)));
+  }
+}
+
+}  // namespace
+
+// complex64 SRFT: for ell <= 128 as a pass over A on the tcgen05 tensor
+// cores (Y = A X with the picked DFT columns, three-product split, the same
+// kernel as the Gaussian passes: ~0.15 ms for config 3 against ~1.7 ms for the
+// shared-memory FFT of all n bins, of which ell/n are kept); larger ell or
+// LR_SRFT=fft use the radix-2 FFT kernel.  a_amax < 0: unknown (computed).
 void srft_c64(Handle* h, int64_t m, int64_t n, int64_t ell, const float2* A, int64_t lda,
-              const float2* d, const int32_t* picks, float scale, float2* Y, int64_t ldy) {
+              const float2* d, const int32_t* picks, float scale, float2* Y, int64_t ldy,
+              double a_amax) {
+  static int fft_only = -1;
+  if (fft_only < 0) {
+    const char* e = getenv("LR_SRFT");
+    fft_only = (e && e[0] == 'f') ? 1 : 0;
+  }
+  if (!fft_only && ell <= 128 && h->f32_mode == LR_F32_SPLIT3 && m >= 1024) {
+    float2* X = pool_alloc_t<float2>(h, size_t(n) * ell);
+    const int blocks = int(std::min<int64_t>(ceil_div(n * ell, 256), 8192));
+    srft_matrix_kernel<<<blocks, 256, 0, h->stream>>>(n, ell, d, picks, double(scale), X);
+    LR_CHECK_LAUNCH();
+    gemm_c64_hint(h, false, false, m, ell, n, A, lda, a_amax, X, ell, Y, ldy);
+    return;
+  }
   launch_srft<float2>(h, m, n, ell, A, lda, d, picks, double(scale), Y, ldy);
 }
 

@@ -118,7 +118,7 @@ def randomized_svd(A, k, p=config.DEFAULT_OVERSAMPLE, q=0, seed=0, sketch="gauss
             else:
                 Q = orth_dev(apply_dev(op, omega))
         else:
-            Q = orth_dev(srft_dev(op.array, srft))
+            Q = orth_dev(srft_dev(op.array, srft, amax=getattr(op, "amax", None)))
         U, S, V = direct_svd_dev(op, Q)
         est_dev = None
         if estimate and Q.shape[1]:

@@ -177,13 +177,14 @@ def fast_range_finder(A, ell, seed, kind="srft", ortho_tol=config.GS_DROP_TOL):
     if isinstance(A, MatVecOperator):
         if not hasattr(A, "array"):
             raise TypeError("fast_range_finder needs a dense matrix")
-        host, t = A.host_io, A.array
+        host, t, amax = A.host_io, A.array, getattr(A, "amax", None)
     else:
         host = not is_device_array(A)
         t = to_device(A)
+        amax = None
     spec = SketchSpec(kind=kind, ell=ell, seed=seed)
     op = srft_operator(t.shape[1], ell, seed)
-    Y = srft_dev(t, op)
+    Y = srft_dev(t, op, amax=amax)
     diagnostics = {}
     if not t.is_complex():
         out = torch.empty(1, dtype=torch.float64, device=Y.device)

@@ -136,8 +136,10 @@ def _complex_of(t):
     return torch.complex128
 
 
-def srft_dev(A, op):
-    """Y = scale * dft(A o d)[:, picks] for a device matrix A (K5 kernel)."""
+def srft_dev(A, op, amax=None):
+    """Y = scale * dft(A o d)[:, picks] for a device matrix A (K5).  amax:
+    max |A| when known (DenseOperator.amax) -- complex64 runs as one
+    tensor-core pass over A (lr_srft_scaled)."""
     torch = _torch()
     m, n = A.shape
     if n & (n - 1):
@@ -154,8 +156,9 @@ def srft_dev(A, op):
     d = torch.from_numpy(np.ascontiguousarray(op.d)).to(device=A.device, dtype=cdt)
     picks = torch.from_numpy(np.ascontiguousarray(op.picks, dtype=np.int32)).to(A.device)
     Y = torch.empty((m, op.ell), dtype=cdt, device=A.device)
-    _lib.call("lr_srft", h, code, m, n, op.ell, _lib.ptr(A), _lib.ld(A), _lib.ptr(d),
-              _lib.ptr(picks), float(op.scale), _lib.ptr(Y), _lib.ld(Y))
+    _lib.call("lr_srft_scaled", h, code, m, n, op.ell, _lib.ptr(A), _lib.ld(A),
+              float(-1.0 if amax is None else amax), _lib.ptr(d), _lib.ptr(picks),
+              float(op.scale), _lib.ptr(Y), _lib.ld(Y))
     return Y
 
 
