@@ -81,8 +81,14 @@ def exported_symbols():
     return sorted(_SIGS) + ["lr_last_error", "lr_workspace_bytes", "lr_launch_count"]
 
 
+# kernels launched through CUDA-graph replays (factor._replay): the C
+# counter sees each captured kernel once, at capture time
+GRAPH_LAUNCHES = [0]
+
+
 def launch_count():
-    return int(load().lr_launch_count())
+    """This library's kernels launched so far: direct launches + graph replays."""
+    return int(load().lr_launch_count()) + GRAPH_LAUNCHES[0]
 
 
 def load():

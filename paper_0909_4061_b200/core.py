@@ -267,12 +267,20 @@ def _pass(A, X, Y, adjoint, amax):
               _lib.ld(X), _lib.ptr(Y), _lib.ld(Y))
 
 
+def timing_event():
+    """CUDA timing event; inside a CUDA-graph capture it becomes an event
+    record node (re-recorded by every replay)."""
+    torch = _torch()
+    return torch.cuda.Event(enable_timing=True,
+                            external=bool(torch.cuda.is_current_stream_capturing()))
+
+
 def _timed_pass(A, X, Y, adjoint, amax=None):
     if PASS_EVENTS is None:
         _pass(A, X, Y, adjoint, amax)
         return
     torch = _torch()
-    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s, e = timing_event(), timing_event()
     torch.cuda.nvtx.range_push("lr_pass")      # ncu --nvtx-include lr_pass/
     s.record()
     _pass(A, X, Y, adjoint, amax)

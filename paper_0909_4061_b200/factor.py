@@ -125,19 +125,7 @@ def randomized_svd(A, k, p=config.DEFAULT_OVERSAMPLE, q=0, seed=0, sketch="gauss
             est_dev = posterior_error_estimate_dev(op, Q, probes, alpha, seed + 13, W=W)
         return Q, U, S, V, est_dev
 
-    counters = _snapshot(op)
-    result = None
-    if getattr(op, "device_native", False):
-        # speculative pass: no host synchronization until the flags are read
-        status = torch.zeros(1, dtype=torch.int32, device=op.array.device if hasattr(
-            op, "array") else torch.device("cuda", torch.cuda.current_device()))
-        with speculate(status):
-            result = body()
-        if int(status.item()) != 0:       # rank drop / unresolved pivot: exact path
-            _restore(op, counters)
-            result = None
-    if result is None:
-        result = body()
+    result = _run_step(op, body, key=(k, p, q, seed, spec.kind, probes, alpha, estimate))
     Q, U, S, V, est_dev = result
     est = 0.0 if Q.shape[1] == 0 else (float(est_dev.item()) if est_dev is not None else None)
     if truncate:
@@ -146,6 +134,112 @@ def randomized_svd(A, k, p=config.DEFAULT_OVERSAMPLE, q=0, seed=0, sketch="gauss
     basis = RangeBasis(Q=_out(Q, host), samples_used=ell, passes=passes, est_error=est,
                        spec=spec)
     return basis, PartialSVD(U=_out(U, host), sigma=_out(S, host), V=_out(V, host)), est
+
+
+# ---------------------------------------------------------------------------
+# Step execution: speculative (one host synchronization, at the end), and
+# for a repeated call on the same device operator a CUDA graph of the whole
+# speculative step -- the launch-bound small configurations (config 1: ~40
+# kernels of a few microseconds) replay without per-kernel host overhead.
+
+_GRAPHS = {}
+
+
+def _graph_enabled():
+    import os
+    return os.environ.get("LR_GRAPH", "1") != "0"
+
+
+def _run_step(op, body, key):
+    torch = _torch()
+    counters = _snapshot(op)
+    dense = getattr(op, "device_native", False) and hasattr(op, "array")
+    graphable = dense and _graph_enabled() and key[4] == "gaussian"
+    if graphable:
+        gkey = (id(op), op.array.data_ptr(), tuple(op.array.shape), op.array.dtype,
+                getattr(op, "amax", None), torch.cuda.current_device()) + tuple(key)
+        entry = _GRAPHS.get(gkey)
+        if entry is not None and entry.get("op") is not None and entry["op"]() is not op:
+            _GRAPHS.pop(gkey, None)               # a different operator reused the id
+            entry = None
+        if entry is not None and entry.get("graph") is not None:
+            res = _replay(op, entry, counters)
+            if res is not None:
+                return res
+            return body()                       # speculation failed: exact path
+    result = None
+    if getattr(op, "device_native", False):
+        # speculative pass: no host synchronization until the flags are read
+        dev = op.array.device if hasattr(op, "array") else torch.device(
+            "cuda", torch.cuda.current_device())
+        status = torch.zeros(1, dtype=torch.int32, device=dev)
+        with speculate(status):
+            result = body()
+        if int(status.item()) != 0:       # rank drop / unresolved pivot: exact path
+            _restore(op, counters)
+            result = None
+            if graphable:
+                _GRAPHS[gkey] = {"graph": None, "bad": True}
+        elif graphable:
+            import weakref
+            if gkey not in _GRAPHS and len(_GRAPHS) >= 16:
+                _GRAPHS.pop(next(iter(_GRAPHS)))   # bounded cache, oldest first
+            entry = _GRAPHS.setdefault(gkey, {"runs": 0, "op": weakref.ref(op)})
+            if not entry.get("bad"):
+                entry["runs"] = entry.get("runs", 0) + 1
+                if entry["runs"] >= 2:            # the scratch pool has settled: capture
+                    _capture(op, body, entry, dev)
+    if result is None:
+        result = body()
+    return result
+
+
+def _capture(op, body, entry, dev):
+    from . import core
+    torch = _torch()
+    snap = _snapshot(op)
+    status = torch.zeros(1, dtype=torch.int32, device=dev)
+    g = torch.cuda.CUDAGraph()
+    torch.cuda.synchronize()
+    prev = core.PASS_EVENTS
+    core.PASS_EVENTS = []        # per-pass event record nodes, re-recorded by each replay
+    from . import _lib
+    l0 = _lib.load().lr_launch_count()
+    try:
+        with torch.cuda.graph(g, capture_error_mode="relaxed"):
+            status.zero_()
+            with speculate(status):
+                out = body()
+    except Exception:        # not capturable here (e.g. a pool growth): stay eager
+        entry["bad"] = True
+        _restore(op, snap)
+        return
+    finally:
+        entry["pass_events"] = core.PASS_EVENTS
+        entry["kernels"] = int(_lib.load().lr_launch_count() - l0)
+        core.PASS_EVENTS = prev
+    after = _snapshot(op)
+    entry["delta"] = tuple(a - b for a, b in zip(after, snap))
+    _restore(op, snap)
+    entry.update(graph=g, status=status, out=out)
+
+
+def _replay(op, entry, counters):
+    from . import core
+    entry["graph"].replay()
+    if core.PASS_EVENTS is not None:     # bench.py: the replay's pass timings
+        core.PASS_EVENTS.extend(entry.get("pass_events", []))
+    from . import _lib
+    _lib.GRAPH_LAUNCHES[0] += entry.get("kernels", 0)
+    if int(entry["status"].item()) != 0:
+        return None
+    c = op.counters
+    d = entry["delta"]
+    c.matvecs, c.adjoint_matvecs, c.passes, c.flops = (
+        counters[0] + d[0], counters[1] + d[1], counters[2] + d[2], counters[3] + d[3])
+    Q, U, S, V, est = entry["out"]
+    # the graph's buffers are reused by the next replay: hand out copies
+    return (Q.clone(), U.clone(), S.clone(), V.clone(), None if est is None else est.clone())
 
 
 def _snapshot(op):

@@ -67,7 +67,7 @@ class CudaCsrOperator(MatVecOperator):
         rowptr, col, val = csr
         if core.PASS_EVENTS is not None:   # bench.py: per-launch timing + bytes model
             torch = _torch()
-            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s, e = core.timing_event(), core.timing_event()
             torch.cuda.nvtx.range_push("lr_pass")
             s.record()
             self._spmm_launch(rowptr, col, val, rows, X, Y, accumulate)

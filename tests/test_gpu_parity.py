@@ -132,6 +132,33 @@ def test_cfg1_full(golden):
     assert [cnt.matvecs, cnt.adjoint_matvecs, cnt.passes, cnt.flops] == list(g["counters"])
 
 
+@pytest.mark.parametrize("q,estimate", [(0, True), (2, False)])
+def test_repeated_calls_replay_cuda_graph(golden, q, estimate):
+    """The third and later calls on the same device operator replay a CUDA
+    graph of the speculative step: results identical to the eager calls,
+    counters advanced exactly as if the step had run eagerly, and the
+    returned factors are private copies."""
+    import torch
+    from paper_0909_4061_b200 import factor
+    A, _ = workloads.build_cfg1()
+    op = lr().DenseOperator(torch.from_numpy(A).cuda())
+    outs = []
+    for i in range(5):
+        before = (op.counters.matvecs, op.counters.passes, op.counters.flops)
+        b, f, est = lr().randomized_svd(op, 20, 10, q, 1, estimate=estimate)
+        after = (op.counters.matvecs, op.counters.passes, op.counters.flops)
+        outs.append((b.Q.clone(), f.U, f.sigma, f.V, est, tuple(a - c for a, c in zip(after, before))))
+    assert any(e.get("graph") is not None for e in factor._GRAPHS.values())
+    for o in outs[1:]:
+        assert torch.equal(o[0], outs[0][0]) and torch.equal(o[1], outs[0][1])
+        assert torch.equal(o[2], outs[0][2]) and torch.equal(o[3], outs[0][3])
+        assert o[4] == outs[0][4] and o[5] == outs[0][5]
+    assert outs[3][1].data_ptr() != outs[4][1].data_ptr()
+    if q == 0 and estimate:
+        g = golden("cfg1")
+        assert np.max(np.abs(outs[4][2].cpu().numpy() - g["sigma"]) / g["sigma"]) <= 1e-10
+
+
 def test_cfg1_public_api_sequence(golden):
     """The exact call sequence of the reference tests."""
     g = golden("cfg1")
