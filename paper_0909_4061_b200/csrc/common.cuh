@@ -133,6 +133,11 @@ void gemm_c64_hint(Handle* h, bool transA, bool conjA, int64_t M, int64_t N, int
                    float2* C, int64_t ldc);
 // fp64-accumulated Gram of fp32 / complex64 panels
 void gram_f32(Handle* h, int64_t m, int64_t ell, const float* Y, int64_t ldy, double* G);
+bool gemm_f64_tma_ok(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
+                     const double* B, int64_t ldb);
+bool gemm_f64_tma_pick(bool transA, int64_t N, int64_t K);
+void gemm_f64_tma(Handle* h, bool transA, int64_t M, int64_t N, int64_t K, const double* A,
+                  int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc);
 void gemm_f64_from_f32(Handle* h, bool transA, int64_t M, int64_t N, int64_t K, const float* A,
                        int64_t lda, const float* B, int64_t ldb, double* C, int64_t ldc);
 void gram_c64(Handle* h, int64_t m, int64_t ell, const float2* Y, int64_t ldy, double2* G);

@@ -26,6 +26,7 @@
 #include <cudaTypedefs.h>
 
 #include "common.cuh"
+#include "tma.cuh"
 
 namespace lr {
 namespace {
@@ -379,6 +380,8 @@ __global__ void reduce_slices_f32(int64_t M, int64_t N, int S, const float* __re
   }
 }
 
+}  // namespace
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -406,7 +409,6 @@ CUtensorMap make_map_2d(CUtensorMapDataType dt, const void* ptr, uint64_t inner,
   return m;
 }
 
-}  // namespace
 
 bool gemm_f32_tc_supported(bool transA, int64_t N, const float* A, int64_t lda) {
   return N >= 1 && N <= 256 && (lda % 4) == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0;
