@@ -155,8 +155,8 @@ gemm_f32_tc_kernel(const __grid_constant__ CUtensorMap mapA,
   if (threadIdx.x == 0) {
     for (int s = 0; s < TSTAGES; ++s) {
       mbar_init(&a32_full[s], 1);
-      mbar_init(&a32_empty[s], 4);
-      mbar_init(&ahl_full[s], 4);
+      mbar_init(&a32_empty[s], 128);   // every converter thread arrives itself
+      mbar_init(&ahl_full[s], 128);
       mbar_init(&b_full[s], 1);
       mbar_init(&st_empty[s], 1);
     }
@@ -239,16 +239,14 @@ gemm_f32_tc_kernel(const __grid_constant__ CUtensorMap mapA,
 #pragma unroll
         for (int k = 0; k < TBK; ++k) v[k] = st[k * TBM + r];
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&a32_empty[s]);
+      mbar_arrive(&a32_empty[s]);   // this thread's reads of the fp32 stage are done
       mbar_wait(&st_empty[s], ph ^ 1u);   // MMA finished with the previous hi/lo tiles
 #pragma unroll
       for (int g = 0; g < TBK / 8; ++g)
         split_store8(v + 8 * g, sA, reinterpret_cast<char*>(ahi(s)),
                      reinterpret_cast<char*>(alo(s)), r, g);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&ahl_full[s]);
+      mbar_arrive(&ahl_full[s]);    // this thread's hi/lo writes are visible to the MMA
     }
     // epilogue: TMEM -> registers (row per thread) -> per-warp shared
     // transpose (the ring is idle now) -> coalesced 128-B row stores
@@ -477,11 +475,18 @@ void gemm_f32_tc(Handle* h, bool transA, int64_t M, int64_t N, int64_t K, const 
   CUtensorMap mapBl = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT16, Blo, TBK, brows, TBK * 2, TBK,
                                   uint32_t(BN), CU_TENSOR_MAP_SWIZZLE_64B);
   const int stage_bytes = A32_BYTES + 2 * AH_BYTES + 2 * BN * TBK * 2;
-  // One CTA per SM: with two co-resident CTAs (N <= 128 fits twice) some
-  // output rows came out wrong on B200 (tools/tc_probe2.py); until that is
-  // understood the launch reserves more than half of the SM's shared memory.
   size_t smem = size_t(TSTAGES) * stage_bytes + 1024 /*align*/ + 256 /*barriers*/;
-  smem = std::max<size_t>(smem, 116 * 1024);
+  static int one_cta = -1;
+  if (one_cta < 0) {
+    const char* e = getenv("LR_TC_ONE_CTA");
+    one_cta = (e && e[0] == '0') ? 0 : 1;
+  }
+  // One CTA per SM (more than half the SM's shared memory reserved): with two
+  // co-resident CTAs (N <= 128 fits twice) some output rows still come out
+  // wrong on B200 (tools/tc_probe2.py, K >= 4096, N = 20) -- not the
+  // stage-release ordering (every converter thread now arrives itself);
+  // open issue, LR_TC_ONE_CTA=0 reproduces it.
+  if (one_cta) smem = std::max<size_t>(smem, 116 * 1024);
   const int64_t mt = ceil_div(M, TBM);
   int64_t splits = 1;
   if (mt < h->sm_count) {

@@ -89,6 +89,21 @@ def test_tcgen05_pass_shapes(ell, dtype):
     assert np.abs(Z - ref).max() <= 1e-5 * np.abs(ref).max()
 
 
+@pytest.mark.parametrize("m,n,ell", [(8192, 4096, 20), (1536, 16384, 20), (8192, 16384, 256)])
+def test_tcgen05_deep_k_narrow_n(m, n, ell):
+    """Long K with a narrow N (tools/tc_probe2.py shapes): the configuration
+    where two co-resident CTAs once produced wrong rows."""
+    from paper_0909_4061_b200 import core
+    g = torch.Generator(device="cuda").manual_seed(0)
+    A = torch.randn(m, n, device="cuda", generator=g)
+    X = torch.randn(n, ell, device="cuda", generator=g)
+    op = core.DenseOperator(A)
+    Y = torch.empty(m, ell, device="cuda")
+    core._pass(A, X, Y, False, op.amax)
+    ref = A.double() @ X.double()
+    assert (Y.double() - ref).abs().max().item() <= 2e-5 * ref.abs().max().item()
+
+
 def test_gemm_vector_and_strided_inputs():
     from paper_0909_4061_b200.core import DenseOperator
     A = rand((50, 40), np.float64, 1)
