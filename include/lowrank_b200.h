@@ -113,6 +113,17 @@ int lr_chol_drop(lr_handle_t h, int dtype, int64_t ell, const void* G,
                  double drop_tol, double unres_rel, double shift_coef,
                  void* P, void* R, int32_t* info);
 
+/* Host-sync-free lr_chol_drop for pipelines that decide later (the
+ * row-sharded orthonormalization, dist.py): flags as lr_orth_fast are ORed
+ * into *status (device int32): 1 = unresolved pivot, 2 = column dropped,
+ * 4 = non-finite.  near_thr > 0 (with shift_coef == 0) takes the first-order
+ * factor of a near-identity Gram (second CholeskyQR pass) when
+ * max |G - I| <= near_thr, the exact factorization otherwise -- decided on
+ * the device. */
+int lr_chol_drop_fast(lr_handle_t h, int dtype, int64_t ell, const void* G,
+                      double drop_tol, double unres_rel, double shift_coef, double near_thr,
+                      void* P, void* R, int32_t* info, int32_t* status);
+
 /* Orthonormalize the columns of Y (m x ell) -- replaces
  * orthonormalize_double_gs (reference core.py:84-115).  CholeskyQR2 with a
  * fp64 Gram; guarded fallbacks (shifted CholeskyQR3, then column-wise CGS2

@@ -49,6 +49,15 @@ thread_local std::string g_err;
 constexpr double U64 = 1.1102230246251565e-16;
 
 int wide_of(int dtype) { return is_complex(dtype) ? LR_C128 : LR_F64; }
+// LR_JACOBI_RH=0: one-sided Jacobi on R instead of R^H in the fast small SVD
+bool jacobi_on_rh() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("LR_JACOBI_RH");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
 // max |G - I| for the first-order second CholeskyQR pass (chol_near_identity)
 double near_id_thr(int dtype) { return (dtype == LR_F32 || dtype == LR_C64) ? 1e-4 : 1e-8; }
 size_t wide_size(int dtype) { return is_complex(dtype) ? 16 : 8; }
@@ -251,19 +260,40 @@ void small_svd_fast_impl(Handle* h, int dtype, int64_t r, int64_t c, const void*
   apply_right(h, dtype, c, r, r, Q1, r, P, r, Q2, r);
   trmm_upper(h, wd, r, R2, R1, R);
   if (jacobi_reg_supported(r, is_complex(dtype))) {
-    // register-resident Jacobi: R J = M; then J = R^{-1} M with R^{-1} = P1 P2
     void* Mun = pool_alloc(h, size_t(r) * r * ws);
     void* Jun = pool_alloc(h, size_t(r) * r * ws);
     void* Rinv = pool_alloc(h, size_t(r) * r * ws);
     void* Ut = pool_alloc(h, size_t(r) * r * ws);
     double* sig = pool_alloc_t<double>(h, size_t(r));
+    gemm_any(h, wd, false, false, r, r, r, P1, r, P, r, Rinv, r);   // R^{-1} = P1 P2
+    if (jacobi_on_rh()) {
+      // Jacobi on X = R^H (R R^H is one QR step closer to diagonal than R^H R:
+      // fewer sweeps): X J = M, B = U~ S V^H with U~ = M / S directly and
+      // V = Q2 J, J = R^{-H} M (one Newton-Schulz step restores orthonormality)
+      void* X = pool_alloc(h, size_t(r) * r * ws);
+      cast_copy(h, wd, R, r, wd, X, r, r, r, true);
+      if (is_complex(dtype))
+        jacobi_reg_c128(h, r, static_cast<const double2*>(X), static_cast<double2*>(Mun), sig,
+                        h->d_info);
+      else
+        jacobi_reg_f64(h, r, static_cast<const double*>(X), static_cast<double*>(Mun), sig,
+                       h->d_info);
+      gemm_any(h, wd, true, true, r, r, r, Rinv, r, Mun, r, Jun, r);
+      svd_finalize(h, wd, r, Jun, Mun, sig, Ut, S, Wr, true);
+      gemm_any(h, wd, true, true, r, r, r, Wr, r, Wr, r, G, r);
+      ns_coef(h, wd, r, G);
+      gemm_any(h, wd, false, false, r, r, r, Wr, r, G, r, J, r);
+      cast_copy(h, wd, Ut, r, dtype, U, r, r, r, false);
+      apply_right(h, dtype, c, r, r, Q2, r, J, r, V, r);
+      return;
+    }
+    // register-resident Jacobi on R: R J = M; then J = R^{-1} M
     if (is_complex(dtype))
       jacobi_reg_c128(h, r, static_cast<const double2*>(R), static_cast<double2*>(Mun), sig,
                       h->d_info);
     else
       jacobi_reg_f64(h, r, static_cast<const double*>(R), static_cast<double*>(Mun), sig,
                      h->d_info);
-    gemm_any(h, wd, false, false, r, r, r, P1, r, P, r, Rinv, r);
     gemm_any(h, wd, false, false, r, r, r, Rinv, r, Mun, r, Jun, r);
     svd_finalize(h, wd, r, Jun, Mun, sig, Ut, S, Wr);
     // one Newton-Schulz step restores orthonormality of J to roundoff:
@@ -648,6 +678,29 @@ int lr_chol_drop(lr_handle_t hh, int dtype, int64_t ell, const void* G, double d
   check_dtype(dtype);
   lr::pool_reset(h);
   lr::chol_any(h, dtype, ell, G, drop_tol, unres_rel, shift_coef, P, R, info);
+  API_END
+}
+
+int lr_chol_drop_fast(lr_handle_t hh, int dtype, int64_t ell, const void* G, double drop_tol,
+                      double unres_rel, double shift_coef, double near_thr, void* P, void* R,
+                      int32_t* info, int32_t* status) {
+  API_BEGIN
+  Handle* h = H(hh);
+  check_dtype(dtype);
+  lr::pool_reset(h);
+  int32_t* saved = h->status;
+  h->status = status;
+  try {
+    if (near_thr > 0.0 && shift_coef == 0.0)
+      lr::chol_near_identity(h, lr::wide_of(dtype), ell, G, drop_tol, unres_rel, P, R, info,
+                             near_thr);
+    else
+      lr::chol_any(h, dtype, ell, G, drop_tol, unres_rel, shift_coef, P, R, info);
+  } catch (...) {
+    h->status = saved;
+    throw;
+  }
+  h->status = saved;
   API_END
 }
 

@@ -133,6 +133,9 @@ void gemm_c64_hint(Handle* h, bool transA, bool conjA, int64_t M, int64_t N, int
                    float2* C, int64_t ldc);
 // fp64-accumulated Gram of fp32 / complex64 panels
 void gram_f32(Handle* h, int64_t m, int64_t ell, const float* Y, int64_t ldy, double* G);
+// C (M x N, ldc) = sum over S dense M x N partials, fixed order
+void splitk_reduce(Handle* h, int64_t M, int64_t N, int S, const double* part, double* C,
+                   int64_t ldc);
 bool gemm_f64_tma_ok(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
                      const double* B, int64_t ldb);
 bool gemm_f64_tma_pick(bool transA, int64_t N, int64_t K);
@@ -192,7 +195,7 @@ void jacobi_reg_f64(Handle* h, int64_t n, const double* R, double* Mout, double*
 void jacobi_reg_c128(Handle* h, int64_t n, const double2* R, double2* Mout, double* sig,
                      int32_t* info);
 void svd_finalize(Handle* h, int dtype_wide, int64_t n, const void* Jun, const void* Mun,
-                  const double* sig, void* U, double* S, void* W);
+                  const double* sig, void* U, double* S, void* W, bool swap = false);
 
 // misc.cu ---------------------------------------------------------------------
 // G <- 1.5 I - 0.5 G  (Newton-Schulz coefficient matrix, n x n wide dtype)

@@ -216,6 +216,45 @@ __global__ void splitk_reduce_f64(int64_t M, int64_t N, int S, const double* __r
   }
 }
 
+// Many splits (one-tile Grams: up to one per SM) over few outputs: 8 threads
+// per output element each sum a fixed stride of the partials, then a fixed
+// order combine in shared memory (deterministic, 8x the parallelism of the
+// one-thread-per-element sum whose 148 dependent loads were latency-bound).
+__global__ void splitk_reduce_wide(int64_t M, int64_t N, int S, const double* __restrict__ part,
+                                   double* __restrict__ out, int64_t ldo) {
+  __shared__ double red[8][33];
+  const int64_t total = M * N;
+  const int64_t i = int64_t(blockIdx.x) * 32 + threadIdx.x;
+  double s = 0.0;
+  if (i < total)
+    for (int k = threadIdx.y; k < S; k += 8) s += part[int64_t(k) * total + i];
+  red[threadIdx.y][threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.y == 0 && i < total) {
+    double t = 0.0;
+#pragma unroll
+    for (int y = 0; y < 8; ++y) t += red[y][threadIdx.x];
+    out[(i / N) * ldo + (i % N)] = t;
+  }
+}
+
+}  // namespace
+
+void splitk_reduce(Handle* h, int64_t M, int64_t N, int S, const double* part, double* C,
+                   int64_t ldc) {
+  const int64_t total = M * N;
+  if (S >= 16) {
+    splitk_reduce_wide<<<unsigned(ceil_div(total, 32)), dim3(32, 8), 0, h->stream>>>(
+        M, N, S, part, C, ldc);
+  } else {
+    const int blocks = int(std::min<int64_t>(ceil_div(total, 256), int64_t(h->sm_count) * 8));
+    splitk_reduce_f64<<<blocks, 256, 0, h->stream>>>(M, N, S, part, C, ldc);
+  }
+  LR_CHECK_LAUNCH();
+}
+
+namespace {
+
 template <bool TRANS, int NF, typename TIN>
 void launch_nf(Handle* h, int64_t M, int64_t N, int64_t K, const TIN* A, int64_t lda,
                const TIN* B, int64_t ldb, double* C, int64_t ldc) {
@@ -245,10 +284,7 @@ void launch_nf(Handle* h, int64_t M, int64_t N, int64_t K, const TIN* A, int64_t
   kern<<<grid, THREADS, S::bytes, h->stream>>>(M, N, K, A, lda, B, ldb, part, N, kchunk, M * N,
                                                  a16, b16);
   LR_CHECK_LAUNCH();
-  const int64_t total = M * N;
-  int blocks = int(std::min<int64_t>(ceil_div(total, 256), int64_t(h->sm_count) * 8));
-  splitk_reduce_f64<<<blocks, 256, 0, h->stream>>>(M, N, int(splits), part, C, ldc);
-  LR_CHECK_LAUNCH();
+  splitk_reduce(h, M, N, int(splits), part, C, ldc);
 }
 
 template <bool TRANS, typename TIN>

@@ -186,17 +186,6 @@ gemm_f64_tma_kernel(const __grid_constant__ CUtensorMap mapA,
   }
 }
 
-__global__ void splitk_sum(int64_t M, int64_t N, int S, const double* __restrict__ part,
-                           double* __restrict__ out, int64_t ldo) {
-  const int64_t total = M * N;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
-       i += int64_t(gridDim.x) * blockDim.x) {
-    double s = 0.0;
-    for (int k = 0; k < S; ++k) s += part[int64_t(k) * total + i];
-    out[(i / N) * ldo + (i % N)] = s;
-  }
-}
-
 template <bool TRANS, int NF>
 void launch(Handle* h, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
             const double* B, int64_t ldb, double* C, int64_t ldc) {
@@ -229,9 +218,7 @@ void launch(Handle* h, int64_t M, int64_t N, int64_t K, const double* A, int64_t
   double* part = pool_alloc_t<double>(h, size_t(splits) * M * N);
   kern<<<grid, THREADS, G::SMEM, h->stream>>>(mapA, mapB, M, N, K, part, N, kchunk, M * N);
   LR_CHECK_LAUNCH();
-  const int blocks = int(std::min<int64_t>(ceil_div(M * N, 256), int64_t(h->sm_count) * 8));
-  splitk_sum<<<blocks, 256, 0, h->stream>>>(M, N, int(splits), part, C, ldc);
-  LR_CHECK_LAUNCH();
+  splitk_reduce(h, M, N, int(splits), part, C, ldc);
 }
 
 template <bool TRANS>

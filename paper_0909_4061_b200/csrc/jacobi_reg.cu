@@ -204,10 +204,13 @@ jacobi_reg_kernel(int n, const T* __restrict__ R, T* __restrict__ Mout, double* 
 
 // sort by sigma (desc, ties by index), sign-fix J's columns (reference
 // core.py:221-229), W = M / sigma with the same phase.  One CTA.
+// swap: U = M / sigma (sign-fixed) and W = J (same phase) -- the Jacobi on R^H
+// variant, where the orthogonal-columns factor M gives the left vectors.
 template <typename T>
 __global__ void svd_finalize_kernel(int n, const T* __restrict__ Jun, const T* __restrict__ Mun,
                                     const double* __restrict__ sig, T* __restrict__ U,
-                                    double* __restrict__ S_out, T* __restrict__ Wout) {
+                                    double* __restrict__ S_out, T* __restrict__ Wout,
+                                    bool swap) {
   using S = Sc<T>;
   extern __shared__ int order[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
@@ -218,6 +221,11 @@ __global__ void svd_finalize_kernel(int n, const T* __restrict__ Jun, const T* _
     order[rk] = j;
   }
   __syncthreads();
+  if (swap) {   // the sign convention applies to U = M / sigma: use M's columns
+    const T* t = Jun;
+    Jun = Mun;
+    Mun = t;
+  }
   for (int o = warp; o < n; o += nw) {
     const int j = order[o];
     double mx = 0.0;
@@ -238,8 +246,13 @@ __global__ void svd_finalize_kernel(int n, const T* __restrict__ Jun, const T* _
     const double sj = sig[j];
     const double inv = sj > 0.0 ? 1.0 / sj : 0.0;
     for (int i = lane; i < n; i += 32) {
-      U[size_t(i) * n + o] = S::mul(Jun[size_t(i) * n + j], ph);
-      Wout[size_t(i) * n + o] = S::mul(S::scale(Mun[size_t(i) * n + j], inv), ph);
+      if (!swap) {
+        U[size_t(i) * n + o] = S::mul(Jun[size_t(i) * n + j], ph);
+        Wout[size_t(i) * n + o] = S::mul(S::scale(Mun[size_t(i) * n + j], inv), ph);
+      } else {   // Jun holds M here: U = M / sigma, W = J
+        U[size_t(i) * n + o] = S::mul(S::scale(Jun[size_t(i) * n + j], inv), ph);
+        Wout[size_t(i) * n + o] = S::mul(Mun[size_t(i) * n + j], ph);
+      }
     }
     if (lane == 0) S_out[o] = sj;
   }
@@ -303,16 +316,16 @@ void jacobi_reg_c128(Handle* h, int64_t n, const double2* R, double2* Mout, doub
 }
 
 void svd_finalize(Handle* h, int dtype_wide, int64_t n, const void* Jun, const void* Mun,
-                  const double* sig, void* U, double* S, void* W) {
+                  const double* sig, void* U, double* S, void* W, bool swap) {
   const size_t smem = size_t(n) * sizeof(int);
   if (dtype_wide == LR_C128)
     svd_finalize_kernel<double2><<<1, 1024, smem, h->stream>>>(
         int(n), static_cast<const double2*>(Jun), static_cast<const double2*>(Mun), sig,
-        static_cast<double2*>(U), S, static_cast<double2*>(W));
+        static_cast<double2*>(U), S, static_cast<double2*>(W), swap);
   else
     svd_finalize_kernel<double><<<1, 1024, smem, h->stream>>>(
         int(n), static_cast<const double*>(Jun), static_cast<const double*>(Mun), sig,
-        static_cast<double*>(U), S, static_cast<double*>(W));
+        static_cast<double*>(U), S, static_cast<double*>(W), swap);
   LR_CHECK_LAUNCH();
 }
 

@@ -98,6 +98,30 @@ class GpuBackend:
         inf = info.cpu().tolist()
         return P, R, inf[0], inf[1], inf[2]
 
+    def chol_fast(self, G, drop_tol, unres_rel, near_thr, status):
+        """Host-sync-free Cholesky: P only; decisions ORed into `status`
+        (device int32: 1 unresolved, 2 dropped, 4 non-finite)."""
+        torch = self.torch
+        ell = G.shape[0]
+        P = torch.empty_like(G)
+        R = torch.empty_like(G)
+        info = torch.zeros(4, dtype=torch.int32, device=G.device)
+        code = _lib.C128 if G.is_complex() else _lib.F64
+        _lib.call("lr_chol_drop_fast", _lib.handle(G.device.index), code, ell, _lib.ptr(G),
+                  float(drop_tol), float(unres_rel), 0.0, float(near_thr), _lib.ptr(P),
+                  _lib.ptr(R), _lib.ptr(info), _lib.ptr(status))
+        return P
+
+    def new_status(self, like):
+        return self.torch.zeros(1, dtype=self.torch.int32, device=like.device)
+
+    def status_value(self, status):
+        return int(status.item())
+
+    def speculate(self, status):
+        from .core import speculate
+        return speculate(status)
+
     def apply(self, Y, P, ncols):
         """Y @ P[:, :ncols] in the panel precision."""
         from .core import cast_dev, gemm_dev
@@ -201,6 +225,21 @@ def dist_orth(Y, comm, be, tol=config.GS_DROP_TOL):
     return dist_cgs2(Y, comm, be, tol, math.sqrt(be.trace(G)))
 
 
+def dist_orth_fast(Y, comm, be, status, tol=config.GS_DROP_TOL):
+    """Speculative row-sharded CholeskyQR2 (no host synchronization): the
+    drop / resolvability decisions of the exact path are evaluated on the
+    device (identically on every rank -- the Gram is all-reduced) and ORed
+    into `status`; a nonzero status at the end of the step sends every rank
+    back to the exact path (dist_orth)."""
+    ell = Y.shape[1]
+    unres = 4.0 * ell * U64
+    G = comm.allreduce(be.gram(Y))
+    Q1 = be.apply(Y, be.chol_fast(G, tol, unres, 0.0, status), ell)
+    G2 = comm.allreduce(be.gram(Q1))
+    near = 1e-4 if str(Y.dtype).endswith(("float32", "complex64")) else 1e-8
+    return be.apply(Q1, be.chol_fast(G2, tol, unres, near, status), ell)
+
+
 def dist_cgs2(Y, comm, be, tol, fro):
     """Column-wise classical Gram-Schmidt with one re-orthogonalization
     (reference core.py:99-114) on a row-sharded panel."""
@@ -244,50 +283,83 @@ class DistResult:
 
 def dist_randomized_svd(A_local, n, k, p, q, seed, comm, be, amax=None, estimate=True,
                         probes=config.DEFAULT_PROBES, alpha=config.DEFAULT_ALPHA,
-                        truncate=False, sketch="gauss"):
+                        truncate=False, sketch="gauss", speculative=True):
     """Alg 4.4 (q > 0) / 4.1 (q = 0) / 4.5 (sketch="srft") + Alg 5.1 +
     posterior estimate (reference rangefinder.py:49-82,221-265;
     factor.py:154-165; composition of cli.py:128-173,222-262) with A split by
     rows over `comm`.  Every rank returns its rows of Q and U and the
     replicated sigma, V and estimate.  `amax` is the global max|A| (fp32 /
-    complex64 pass scaling)."""
+    complex64 pass scaling).
+
+    speculative: run the step without host synchronization (device-side
+    decisions, one status all-reduce at the end) and fall back to the exact
+    synchronous path on every rank if any rank flagged a rank drop or an
+    unresolved pivot -- the single-GPU randomized_svd strategy."""
     ell = int(k) + int(p)
     if ell < 1 or ell > n:
         raise ValueError(f"rank+oversample {ell} must be in [1, {n}]")
+    if sketch not in ("srft", "gauss", "gaussian"):
+        raise ValueError(f"unknown sketch {sketch!r}")
     if sketch == "srft":
         if q > 0:
             raise ValueError("power iterations are not available with structured sketches")
         if not A_local.is_complex():
             raise NotImplementedError("row-sharded SRFT needs a complex A")
-        # the SRFT acts on the columns of A: every row block is sketched locally
-        Q = dist_orth(be.srft(A_local, ell, seed), comm, be)
-    elif sketch in ("gauss", "gaussian"):
-        Om = be.gaussian(n, ell, seed, _STREAM_GAUSS, A_local)
-        Q = dist_orth(be.pass_n(A_local, Om, amax), comm, be)
-    else:
-        raise ValueError(f"unknown sketch {sketch!r}")
-    for _ in range(q):
+    args = (A_local, n, k, p, q, seed, comm, be, amax, estimate, probes, alpha, truncate, sketch)
+    if speculative and hasattr(be, "chol_fast"):
+        status = be.new_status(A_local)
+        res = _dist_step(*args, status=status)
+        flag = comm.allreduce_max(status.to(dtype=_float_of(status)))
+        if be.status_value(flag) == 0:
+            return res
+    return _dist_step(*args, status=None)
+
+
+def _float_of(t):
+    import torch
+    return torch.float64
+
+
+def _dist_step(A_local, n, k, p, q, seed, comm, be, amax, estimate, probes, alpha, truncate,
+               sketch, status):
+    import contextlib
+    ell = int(k) + int(p)
+    spec = be.speculate(status) if status is not None else contextlib.nullcontext()
+
+    def orth_m(Y):
+        return dist_orth_fast(Y, comm, be, status) if status is not None else \
+            dist_orth(Y, comm, be)
+
+    with spec:
+        if sketch == "srft":
+            # the SRFT acts on the columns of A: every row block is sketched locally
+            Q = orth_m(be.srft(A_local, ell, seed))
+        else:
+            Om = be.gaussian(n, ell, seed, _STREAM_GAUSS, A_local)
+            Q = orth_m(be.pass_n(A_local, Om, amax))
+        for _ in range(q):
+            if Q.shape[1] == 0:
+                break
+            Z = comm.allreduce(be.pass_t(A_local, Q, amax))          # n x ell, replicated
+            Qt = _replicated_orth(Z, be)
+            Q = orth_m(be.pass_n(A_local, Qt, amax))
         if Q.shape[1] == 0:
-            break
-        Z = comm.allreduce(be.pass_t(A_local, Q, amax))          # n x ell, replicated
-        Qt = _replicated_orth(Z, be)
-        Q = dist_orth(be.pass_n(A_local, Qt, amax), comm, be)
-    if Q.shape[1] == 0:
-        z = be.zeros_like_rows(A_local, 0)
-        return DistResult(Q=Q, U=z, sigma=be.empty_sigma(A_local), V=be.zeros_rows(n, 0, A_local),
-                          est=0.0, passes=2 * q + 2 if q else 1)
-    # Alg 5.1: Z = A^H Q (all-reduce), small SVD replicated, U_r = Q_r U~
-    Z = comm.allreduce(be.pass_t(A_local, Q, amax))
-    Ub, S, V = be.small_svd(Z)
-    U = be.matmul(Q, Ub)
-    est = None
-    if estimate:
-        W = be.gaussian(n, probes, seed + 13, _STREAM_PROBE, A_local)
-        Zl = be.pass_n(A_local, W, amax)
-        C = comm.allreduce(be.adj_matmul(Q, Zl))                 # Q^H Z, ell x r
-        be.sub_(Zl, be.matmul(Q, C))
-        ss = comm.allreduce(be.colsumsq(Zl))
-        est = alpha * math.sqrt(2.0 / math.pi) * math.sqrt(be.to_scalar(ss))
+            z = be.zeros_like_rows(A_local, 0)
+            return DistResult(Q=Q, U=z, sigma=be.empty_sigma(A_local),
+                              V=be.zeros_rows(n, 0, A_local), est=0.0,
+                              passes=2 * q + 2 if q else 1)
+        # Alg 5.1: Z = A^H Q (all-reduce), small SVD replicated, U_r = Q_r U~
+        Z = comm.allreduce(be.pass_t(A_local, Q, amax))
+        Ub, S, V = be.small_svd(Z)
+        U = be.matmul(Q, Ub)
+        est = None
+        if estimate:
+            W = be.gaussian(n, probes, seed + 13, _STREAM_PROBE, A_local)
+            Zl = be.pass_n(A_local, W, amax)
+            C = comm.allreduce(be.adj_matmul(Q, Zl))                 # Q^H Z, ell x r
+            be.sub_(Zl, be.matmul(Q, C))
+            ss = comm.allreduce(be.colsumsq(Zl))
+            est = alpha * math.sqrt(2.0 / math.pi) * math.sqrt(be.to_scalar(ss))
     if truncate:
         kk = min(int(k), U.shape[1])
         U, S, V = U[:, :kk], S[:kk], V[:, :kk]

@@ -60,6 +60,22 @@ class TorchCpuBackend:
             P[np.ix_(kept, list(range(len(kept))))] = np.linalg.inv(Rk)
         return torch.from_numpy(P), torch.from_numpy(R), len(kept), unres, bad
 
+    def chol_fast(self, G, drop_tol, unres_rel, near_thr, status):
+        P, _, rank, unres, bad = self.chol(G, drop_tol, unres_rel, 0.0)
+        bits = (1 if unres else 0) | (2 if rank < G.shape[0] else 0) | (4 if bad else 0)
+        status |= bits
+        return P
+
+    def new_status(self, like):
+        return torch.zeros(1, dtype=torch.int32)
+
+    def status_value(self, status):
+        return int(status.item())
+
+    def speculate(self, status):
+        import contextlib
+        return contextlib.nullcontext()
+
     def apply(self, Y, P, ncols):
         return Y @ P[:, :ncols].to(Y.dtype)
 

@@ -37,9 +37,18 @@ rng = np.random.default_rng(0)
 for ell, ncols, cplx in [(30, 2048, False), (48, 4096, False), (110, 8192, False), (120, 8192, True),
                          (64, 4096, True), (128, 4096, False), (256, 4096, False)]:
     dt = torch.complex128 if cplx else torch.float64
-    B = rng.standard_normal((ell, ncols)) * np.exp(-np.arange(ell) / 30.0)[:, None]
-    if cplx:
-        B = B + 1j * rng.standard_normal((ell, ncols)) * np.exp(-np.arange(ell) / 30.0)[:, None]
+    if os.environ.get("MIXED"):
+        # B = W diag(s) V^T with random orthogonal W: rows of B are not graded
+        # (like B = Q^T A with a range basis Q from CholeskyQR)
+        W = np.linalg.qr(rng.standard_normal((ell, ell)))[0]
+        V = np.linalg.qr(rng.standard_normal((ncols, ell)))[0]
+        B = (W * (np.arange(1, ell + 1) ** -0.5)) @ V.T
+        if cplx:
+            B = B + 1j * ((np.linalg.qr(rng.standard_normal((ell, ell)))[0] * 0.5) @ V.T)
+    else:
+        B = rng.standard_normal((ell, ncols)) * np.exp(-np.arange(ell) / 30.0)[:, None]
+        if cplx:
+            B = B + 1j * rng.standard_normal((ell, ncols)) * np.exp(-np.arange(ell) / 30.0)[:, None]
     Bd = torch.from_numpy(B).cuda()
     Z = Bd.conj().T.contiguous()
     G = (Z.conj().T @ Z).contiguous()
