@@ -139,6 +139,10 @@ void splitk_reduce(Handle* h, int64_t M, int64_t N, int S, const double* part, d
 bool gemm_f64_tma_ok(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
                      const double* B, int64_t ldb);
 bool gemm_f64_tma_pick(bool transA, int64_t N, int64_t K);
+bool gemm_f64_tma_f32_ok(bool transA, int64_t M, int64_t N, int64_t K, const float* A,
+                         int64_t lda, const float* B, int64_t ldb);
+void gemm_f64_tma_f32(Handle* h, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
+                      const float* B, int64_t ldb, double* C, int64_t ldc);
 void gemm_f64_tma(Handle* h, bool transA, int64_t M, int64_t N, int64_t K, const double* A,
                   int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc);
 void gemm_f64_from_f32(Handle* h, bool transA, int64_t M, int64_t N, int64_t K, const float* A,

@@ -296,9 +296,22 @@ gemm_f32_tc_kernel(const __grid_constant__ CUtensorMap mapA,
 __global__ void amax_f32_kernel(int64_t rows, int64_t cols, const float* __restrict__ X,
                                 int64_t ld, unsigned int* __restrict__ out_bits) {
   float mx = 0.f;
-  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < rows * cols;
-       e += int64_t(gridDim.x) * blockDim.x)
-    mx = fmaxf(mx, fabsf(X[(e / cols) * ld + (e % cols)]));
+  if (ld == cols && (reinterpret_cast<uintptr_t>(X) & 15) == 0) {
+    // contiguous: float4 grid-stride sweep (no per-element index division)
+    const int64_t total = rows * cols, n4 = total / 4;
+    const float4* X4 = reinterpret_cast<const float4*>(X);
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n4;
+         e += int64_t(gridDim.x) * blockDim.x) {
+      const float4 v = X4[e];
+      mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+    }
+    for (int64_t e = n4 * 4 + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+         e += int64_t(gridDim.x) * blockDim.x)
+      mx = fmaxf(mx, fabsf(X[e]));
+  } else {
+    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x)
+      for (int64_t c = threadIdx.x; c < cols; c += blockDim.x) mx = fmaxf(mx, fabsf(X[r * ld + c]));
+  }
   for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   if ((threadIdx.x & 31) == 0) atomicMax(out_bits, __float_as_uint(mx));
 }

@@ -387,6 +387,10 @@ void gemm_f64_from_f32(Handle* h, bool transA, int64_t M, int64_t N, int64_t K, 
       LR_CUDA(cudaMemsetAsync(C + r * ldc, 0, N * sizeof(double), h->stream));
     return;
   }
+  if (gemm_f64_tma_f32_ok(transA, M, N, K, A, lda, B, ldb)) {
+    gemm_f64_tma_f32(h, M, N, K, A, lda, B, ldb, C, ldc);
+    return;
+  }
   if (transA) launch_trans<true, float>(h, M, N, K, A, lda, B, ldb, C, ldc);
   else        launch_trans<false, float>(h, M, N, K, A, lda, B, ldb, C, ldc);
 }

@@ -66,21 +66,27 @@ __device__ __forceinline__ void dmma(double (&c)[4], double a0, double a1, doubl
       : "d"(a0), "d"(a1), "d"(b0));
 }
 
-template <int NF>
+template <int NF, typename TIN = double>
 struct Cfg {
   static constexpr int BN = 16 * NF;
-  static constexpr int A_BYTES = BM * BK * 8;          // 16 KB
-  static constexpr int B_BYTES = BK * BN * 8;
-  static constexpr int STAGE = A_BYTES + B_BYTES;      // multiple of 1024
+  static constexpr int A_BYTES = BM * BK * int(sizeof(TIN));   // 16 KB (fp64)
+  static constexpr int B_BYTES = BK * BN * int(sizeof(TIN));
+  static constexpr int STAGE = A_BYTES + B_BYTES;              // multiple of 1024
   static constexpr size_t SMEM = size_t(ST) * STAGE + 1024 + 2 * ST * 8;
 };
 
-template <bool TRANS, int NF>
+// TIN = float: fp32 operands (the Gram of an fp32 / complex64 panel) staged
+// as fp32 and widened to fp64 at fragment load (exact products).  sym: C is
+// the Gram of one operand (A == B, M == N): CTA tiles strictly below the
+// diagonal are skipped and mirrored afterwards.
+template <bool TRANS, int NF, typename TIN = double>
 __global__ void __launch_bounds__(THREADS, 1)
 gemm_f64_tma_kernel(const __grid_constant__ CUtensorMap mapA,
                     const __grid_constant__ CUtensorMap mapB, int64_t M, int64_t N, int64_t K,
-                    double* __restrict__ C, int64_t ldc, int64_t kchunk, int64_t cstride) {
-  using G = Cfg<NF>;
+                    double* __restrict__ C, int64_t ldc, int64_t kchunk, int64_t cstride,
+                    bool sym) {
+  using G = Cfg<NF, TIN>;
+  if (sym && int64_t(blockIdx.y + 1) * G::BN <= int64_t(blockIdx.x) * BM) return;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* base = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -135,8 +141,8 @@ gemm_f64_tma_kernel(const __grid_constant__ CUtensorMap mapA,
   for (int kt = 0; kt < nk; ++kt) {
     const int s = kt % ST;
     bar_wait(&full[s], uint32_t(kt / ST) & 1u);
-    const double* as = reinterpret_cast<const double*>(base + s * G::STAGE);
-    const double* bs = reinterpret_cast<const double*>(base + s * G::STAGE + G::A_BYTES);
+    const TIN* as = reinterpret_cast<const TIN*>(base + s * G::STAGE);
+    const TIN* bs = reinterpret_cast<const TIN*>(base + s * G::STAGE + G::A_BYTES);
 #pragma unroll
     for (int kk = 0; kk < BK / 4; ++kk) {
       const int k = kk * 4 + t;
@@ -146,17 +152,18 @@ gemm_f64_tma_kernel(const __grid_constant__ CUtensorMap mapA,
         const int r = wm * 32 + mf * 16 + g;
         if (!TRANS) {
           // 128-B swizzle: 16-B chunk c of row r lives at chunk c ^ (r & 7)
+          // (fp64 only: the fp32 path is transposed-only)
           const int c = k >> 1, w = k & 1;
-          a[mf][0] = as[r * 16 + ((c ^ (r & 7)) << 1) + w];
-          a[mf][1] = as[(r + 8) * 16 + ((c ^ ((r + 8) & 7)) << 1) + w];
+          a[mf][0] = double(as[r * 16 + ((c ^ (r & 7)) << 1) + w]);
+          a[mf][1] = double(as[(r + 8) * 16 + ((c ^ ((r + 8) & 7)) << 1) + w]);
         } else {
-          a[mf][0] = as[k * BM + r];
-          a[mf][1] = as[k * BM + r + 8];
+          a[mf][0] = double(as[k * BM + r]);
+          a[mf][1] = double(as[k * BM + r + 8]);
         }
       }
 #pragma unroll
       for (int nf = 0; nf < NF; ++nf) {
-        const double b = bs[k * G::BN + wn * NF * 8 + nf * 8 + g];
+        const double b = double(bs[k * G::BN + wn * NF * 8 + nf * 8 + g]);
         dmma(acc[0][nf], a[0][0], a[0][1], b);
         dmma(acc[1][nf], a[1][0], a[1][1], b);
       }
@@ -186,54 +193,71 @@ gemm_f64_tma_kernel(const __grid_constant__ CUtensorMap mapA,
   }
 }
 
-template <bool TRANS, int NF>
-void launch(Handle* h, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
-            const double* B, int64_t ldb, double* C, int64_t ldc) {
-  using G = Cfg<NF>;
-  auto kern = gemm_f64_tma_kernel<TRANS, NF>;
+// strictly-lower tiles of a symmetric result <- transposed upper entries
+__global__ void mirror_lower(int64_t n, int bm, int bn, double* __restrict__ C, int64_t ldc) {
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n * n;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e / n, j = e - i * n;
+    if ((j / bn + 1) * bn <= (i / bm) * bm) C[i * ldc + j] = C[j * ldc + i];
+  }
+}
+
+template <bool TRANS, int NF, typename TIN = double>
+void launch(Handle* h, int64_t M, int64_t N, int64_t K, const TIN* A, int64_t lda,
+            const TIN* B, int64_t ldb, double* C, int64_t ldc, bool sym = false) {
+  using G = Cfg<NF, TIN>;
+  auto kern = gemm_f64_tma_kernel<TRANS, NF, TIN>;
+  constexpr CUtensorMapDataType DT =
+      sizeof(TIN) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
   static bool attr = false;
   if (!attr) {
     LR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(G::SMEM)));
     attr = true;
   }
+  constexpr uint64_t ES = sizeof(TIN);
   const CUtensorMap mapA =
-      !TRANS ? make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT64, A, uint64_t(K), uint64_t(M),
-                           uint64_t(lda) * 8, BK, BM, CU_TENSOR_MAP_SWIZZLE_128B)
-             : make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT64, A, uint64_t(M), uint64_t(K),
-                           uint64_t(lda) * 8, BM, BK, CU_TENSOR_MAP_SWIZZLE_NONE);
-  const CUtensorMap mapB = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT64, B, uint64_t(N),
-                                       uint64_t(K), uint64_t(ldb) * 8, G::BN, BK,
-                                       CU_TENSOR_MAP_SWIZZLE_NONE);
+      !TRANS ? make_map_2d(DT, A, uint64_t(K), uint64_t(M), uint64_t(lda) * ES, BK, BM,
+                           CU_TENSOR_MAP_SWIZZLE_128B)
+             : make_map_2d(DT, A, uint64_t(M), uint64_t(K), uint64_t(lda) * ES, BM, BK,
+                           CU_TENSOR_MAP_SWIZZLE_NONE);
+  const CUtensorMap mapB = make_map_2d(DT, B, uint64_t(N), uint64_t(K), uint64_t(ldb) * ES,
+                                       G::BN, BK, CU_TENSOR_MAP_SWIZZLE_NONE);
   const int64_t mt = ceil_div(M, BM), nt = ceil_div(N, G::BN);
   const int64_t want = choose_splits(h->sm_count, mt * nt, K);
   const int64_t kchunk = ceil_div(ceil_div(K, want), BK) * BK;
   const int64_t splits = std::max<int64_t>(1, ceil_div(K, kchunk));
   dim3 grid{unsigned(mt), unsigned(nt), unsigned(splits)};
   if (splits == 1) {
-    kern<<<grid, THREADS, G::SMEM, h->stream>>>(mapA, mapB, M, N, K, C, ldc, kchunk, 0);
+    kern<<<grid, THREADS, G::SMEM, h->stream>>>(mapA, mapB, M, N, K, C, ldc, kchunk, 0, sym);
     LR_CHECK_LAUNCH();
-    return;
+  } else {
+    double* part = pool_alloc_t<double>(h, size_t(splits) * M * N);
+    kern<<<grid, THREADS, G::SMEM, h->stream>>>(mapA, mapB, M, N, K, part, N, kchunk, M * N,
+                                                sym);
+    LR_CHECK_LAUNCH();
+    splitk_reduce(h, M, N, int(splits), part, C, ldc);
   }
-  double* part = pool_alloc_t<double>(h, size_t(splits) * M * N);
-  kern<<<grid, THREADS, G::SMEM, h->stream>>>(mapA, mapB, M, N, K, part, N, kchunk, M * N);
-  LR_CHECK_LAUNCH();
-  splitk_reduce(h, M, N, int(splits), part, C, ldc);
+  if (sym) {
+    mirror_lower<<<unsigned(std::min<int64_t>(ceil_div(M * N, 256), 4096)), 256, 0, h->stream>>>(
+        M, BM, G::BN, C, ldc);
+    LR_CHECK_LAUNCH();
+  }
 }
 
-template <bool TRANS>
-void launch_nf(Handle* h, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
-               const double* B, int64_t ldb, double* C, int64_t ldc) {
+template <bool TRANS, typename TIN = double>
+void launch_nf(Handle* h, int64_t M, int64_t N, int64_t K, const TIN* A, int64_t lda,
+               const TIN* B, int64_t ldb, double* C, int64_t ldc, bool sym = false) {
   const int nf = int(std::min<int64_t>(8, ceil_div(N, 16)));
   switch (nf) {
-    case 1: launch<TRANS, 1>(h, M, N, K, A, lda, B, ldb, C, ldc); break;
-    case 2: launch<TRANS, 2>(h, M, N, K, A, lda, B, ldb, C, ldc); break;
-    case 3: launch<TRANS, 3>(h, M, N, K, A, lda, B, ldb, C, ldc); break;
-    case 4: launch<TRANS, 4>(h, M, N, K, A, lda, B, ldb, C, ldc); break;
-    case 5: launch<TRANS, 5>(h, M, N, K, A, lda, B, ldb, C, ldc); break;
-    case 6: launch<TRANS, 6>(h, M, N, K, A, lda, B, ldb, C, ldc); break;
-    case 7: launch<TRANS, 7>(h, M, N, K, A, lda, B, ldb, C, ldc); break;
-    default: launch<TRANS, 8>(h, M, N, K, A, lda, B, ldb, C, ldc); break;
+    case 1: launch<TRANS, 1, TIN>(h, M, N, K, A, lda, B, ldb, C, ldc, sym); break;
+    case 2: launch<TRANS, 2, TIN>(h, M, N, K, A, lda, B, ldb, C, ldc, sym); break;
+    case 3: launch<TRANS, 3, TIN>(h, M, N, K, A, lda, B, ldb, C, ldc, sym); break;
+    case 4: launch<TRANS, 4, TIN>(h, M, N, K, A, lda, B, ldb, C, ldc, sym); break;
+    case 5: launch<TRANS, 5, TIN>(h, M, N, K, A, lda, B, ldb, C, ldc, sym); break;
+    case 6: launch<TRANS, 6, TIN>(h, M, N, K, A, lda, B, ldb, C, ldc, sym); break;
+    case 7: launch<TRANS, 7, TIN>(h, M, N, K, A, lda, B, ldb, C, ldc, sym); break;
+    default: launch<TRANS, 8, TIN>(h, M, N, K, A, lda, B, ldb, C, ldc, sym); break;
   }
 }
 
@@ -266,8 +290,30 @@ bool gemm_f64_tma_pick(bool transA, int64_t N, int64_t K) {
 
 void gemm_f64_tma(Handle* h, bool transA, int64_t M, int64_t N, int64_t K, const double* A,
                   int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc) {
-  if (transA) launch_nf<true>(h, M, N, K, A, lda, B, ldb, C, ldc);
+  const bool sym = transA && A == B && M == N && lda == ldb;
+  if (transA) launch_nf<true>(h, M, N, K, A, lda, B, ldb, C, ldc, sym);
   else        launch_nf<false>(h, M, N, K, A, lda, B, ldb, C, ldc);
+}
+
+// Gram-type products of fp32 panels (C = A^T B, fp64 out): TMA + DMMA with
+// fp32 staging; symmetric results computed on the upper tiles only.
+bool gemm_f64_tma_f32_ok(bool transA, int64_t M, int64_t N, int64_t K, const float* A,
+                         int64_t lda, const float* B, int64_t ldb) {
+  static int off = -1;
+  if (off < 0) {
+    const char* e = getenv("LR_DMMA_TMA");
+    off = (e && e[0] == '0') ? 1 : 0;
+  }
+  if (off || !transA || K < 512) return false;
+  const bool aligned = ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15) == 0 &&
+                       (lda % 4) == 0 && (ldb % 4) == 0;
+  return aligned && double(M) * double(N) * double(K) >= double(1 << 26);
+}
+
+void gemm_f64_tma_f32(Handle* h, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
+                      const float* B, int64_t ldb, double* C, int64_t ldc) {
+  const bool sym = A == B && M == N && lda == ldb;
+  launch_nf<true, float>(h, M, N, K, A, lda, B, ldb, C, ldc, sym);
 }
 
 }  // namespace lr
