@@ -808,9 +808,7 @@ int lr_srft_scaled(lr_handle_t hh, int dtype, int64_t m, int64_t n, int64_t ell,
   API_BEGIN
   Handle* h = H(hh);
   LR_REQUIRE(dtype == LR_C64 || dtype == LR_C128, LR_EINVAL, "lr_srft: complex dtypes only");
-  LR_REQUIRE(n >= 1 && (n & (n - 1)) == 0, LR_EUNSUPPORTED,
-             "lr_srft: n must be a power of two (Bluestein path not built)");
-  LR_REQUIRE(ell >= 1 && ell <= n, LR_EINVAL, "lr_srft: need 1 <= ell <= n");
+  LR_REQUIRE(n >= 1 && ell >= 1 && ell <= n, LR_EINVAL, "lr_srft: need 1 <= ell <= n");
   lr::pool_reset(h);
   if (dtype == LR_C64)
     lr::srft_c64(h, m, n, ell, static_cast<const float2*>(A), lda, static_cast<const float2*>(d),
@@ -831,8 +829,7 @@ int lr_dft_rows(lr_handle_t hh, int dtype, int64_t rows, int64_t n, void* X, int
   API_BEGIN
   Handle* h = H(hh);
   LR_REQUIRE(dtype == LR_C64 || dtype == LR_C128, LR_EINVAL, "lr_dft_rows: complex dtypes only");
-  LR_REQUIRE(n >= 1 && (n & (n - 1)) == 0, LR_EUNSUPPORTED,
-             "lr_dft_rows: n must be a power of two");
+  LR_REQUIRE(n >= 1, LR_EINVAL, "lr_dft_rows: n must be positive");
   lr::pool_reset(h);
   lr::dft_rows(h, dtype, rows, n, X, ldx);
   API_END

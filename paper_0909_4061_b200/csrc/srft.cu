@@ -114,22 +114,44 @@ namespace {
 
 // The SRFT restricted to its ell picked bins is the n x ell matrix
 //   X[k, t] = scale n^{-1/2} d_k exp(-2 pi i k picks_t / n),
-// so Y = A X is one more pass over A.  Entries in fp64 from the exact
-// residue (k picks_t) mod n, stored as complex64.
-__global__ void srft_matrix_kernel(int64_t n, int64_t ell, const float2* __restrict__ d,
+// so Y = A X is one more pass over A -- for ANY n (the FFT kernel needs a
+// power of two; the reference uses Bluestein there, sketch.py:155-176, which
+// is the same linear map).  Entries in fp64 from the exact residue
+// (k picks_t) mod n.  d == nullptr: d = 1; picks == nullptr: picks_t = t.
+template <typename C>
+__global__ void srft_matrix_kernel(int64_t n, int64_t ell, const C* __restrict__ d,
                                    const int32_t* __restrict__ picks, double scale,
-                                   float2* __restrict__ X) {
+                                   C* __restrict__ X) {
   const double sn = scale / sqrt(double(n));
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n * ell;
        e += int64_t(gridDim.x) * blockDim.x) {
     const int64_t k = e / ell, t = e - k * ell;
-    const int64_t r = (k * int64_t(picks[t])) % n;
+    const int64_t p = picks ? int64_t(picks[t]) : t;
+    const int64_t r = (k * p) % n;
     double sv, cv;
     sincospi(-2.0 * double(r) / double(n), &sv, &cv);
-    const double dr = d[k].x, di = d[k].y;
-    X[e] = make_float2(float(sn * (dr * cv - di * sv)), float(sn * (dr * sv + di * cv)));
+    const double dr = d ? double(d[k].x) : 1.0, di = d ? double(d[k].y) : 0.0;
+    using R = decltype(X[0].x);
+    X[e] = C{R(sn * (dr * cv - di * sv)), R(sn * (dr * sv + di * cv))};
   }
 }
+
+// Y (m x ell) = A (m x n) X with X the picked, D-scaled DFT columns.
+template <typename C>
+void srft_gemm(Handle* h, int64_t m, int64_t n, int64_t ell, const C* A, int64_t lda,
+               const C* d, const int32_t* picks, double scale, C* Y, int64_t ldy,
+               double a_amax) {
+  C* X = pool_alloc_t<C>(h, size_t(n) * ell);
+  const int blocks = int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n * ell, 256), 8192)));
+  srft_matrix_kernel<C><<<blocks, 256, 0, h->stream>>>(n, ell, d, picks, scale, X);
+  LR_CHECK_LAUNCH();
+  if constexpr (sizeof(C) == 8)
+    gemm_c64_hint(h, false, false, m, ell, n, A, lda, a_amax, X, ell, Y, ldy);
+  else
+    gemm_c128(h, false, false, m, ell, n, A, lda, X, ell, Y, ldy);
+}
+
+bool pow2(int64_t n) { return n >= 1 && (n & (n - 1)) == 0; }
 
 }  // namespace
 
@@ -137,7 +159,8 @@ __global__ void srft_matrix_kernel(int64_t n, int64_t ell, const float2* __restr
 // cores (Y = A X with the picked DFT columns, three-product split, the same
 // kernel as the Gaussian passes: ~0.15 ms for config 3 against ~1.7 ms for the
 // shared-memory FFT of all n bins, of which ell/n are kept); larger ell or
-// LR_SRFT=fft use the radix-2 FFT kernel.  a_amax < 0: unknown (computed).
+// LR_SRFT=fft use the radix-2 FFT kernel, non-power-of-two n always the GEMM.
+// a_amax < 0: unknown (computed).
 void srft_c64(Handle* h, int64_t m, int64_t n, int64_t ell, const float2* A, int64_t lda,
               const float2* d, const int32_t* picks, float scale, float2* Y, int64_t ldy,
               double a_amax) {
@@ -146,12 +169,9 @@ void srft_c64(Handle* h, int64_t m, int64_t n, int64_t ell, const float2* A, int
     const char* e = getenv("LR_SRFT");
     fft_only = (e && e[0] == 'f') ? 1 : 0;
   }
-  if (!fft_only && ell <= 128 && h->f32_mode == LR_F32_SPLIT3 && m >= 1024) {
-    float2* X = pool_alloc_t<float2>(h, size_t(n) * ell);
-    const int blocks = int(std::min<int64_t>(ceil_div(n * ell, 256), 8192));
-    srft_matrix_kernel<<<blocks, 256, 0, h->stream>>>(n, ell, d, picks, double(scale), X);
-    LR_CHECK_LAUNCH();
-    gemm_c64_hint(h, false, false, m, ell, n, A, lda, a_amax, X, ell, Y, ldy);
+  if (!pow2(n) ||
+      (!fft_only && ell <= 128 && h->f32_mode == LR_F32_SPLIT3 && m >= 1024)) {
+    srft_gemm<float2>(h, m, n, ell, A, lda, d, picks, double(scale), Y, ldy, a_amax);
     return;
   }
   launch_srft<float2>(h, m, n, ell, A, lda, d, picks, double(scale), Y, ldy);
@@ -159,11 +179,28 @@ void srft_c64(Handle* h, int64_t m, int64_t n, int64_t ell, const float2* A, int
 
 void srft_c128(Handle* h, int64_t m, int64_t n, int64_t ell, const double2* A, int64_t lda,
                const double2* d, const int32_t* picks, double scale, double2* Y, int64_t ldy) {
+  if (!pow2(n)) {
+    srft_gemm<double2>(h, m, n, ell, A, lda, d, picks, scale, Y, ldy, -1.0);
+    return;
+  }
   launch_srft<double2>(h, m, n, ell, A, lda, d, picks, scale, Y, ldy);
 }
 
 void dft_rows(Handle* h, int dtype, int64_t rows, int64_t n, void* X, int64_t ldx) {
   // unitary DFT of every row, in place: picks = identity, d = 1, scale = 1
+  if (!pow2(n)) {   // dense DFT matrix product (any n), through a scratch copy
+    const size_t es = dtype == LR_C64 ? sizeof(float2) : sizeof(double2);
+    void* T = pool_alloc(h, size_t(rows) * n * es);
+    if (dtype == LR_C64)
+      srft_gemm<float2>(h, rows, n, n, static_cast<const float2*>(X), ldx, nullptr, nullptr, 1.0,
+                        static_cast<float2*>(T), n, -1.0);
+    else
+      srft_gemm<double2>(h, rows, n, n, static_cast<const double2*>(X), ldx, nullptr, nullptr,
+                         1.0, static_cast<double2*>(T), n, -1.0);
+    LR_CUDA(cudaMemcpy2DAsync(X, ldx * es, T, n * es, n * es, rows, cudaMemcpyDeviceToDevice,
+                              h->stream));
+    return;
+  }
   if (dtype == LR_C64)
     launch_srft<float2>(h, rows, n, n, static_cast<const float2*>(X), ldx, nullptr, nullptr, 1.0,
                         static_cast<float2*>(X), ldx);

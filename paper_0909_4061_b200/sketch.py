@@ -1,13 +1,16 @@
 """Random test matrices and the SRFT fast apply.
 
 Mirrors the hot-path part of the reference's ``lowrank.sketch``
-(/root/reference/pkg/src/lowrank/sketch.py).  Every random draw is made on
-the host with the reference's counter-based Philox keying (sketch.py:32-42)
-so the same (dimensions, seed) give bitwise the same Omega / D / R as the
-reference; the draws are uploaded and all arithmetic runs on the GPU
-(K5 SRFT kernel, K1 GEMM).  The Givens-chain variant (GSRFT) and the
-Bluestein path for non-power-of-two lengths are outside this build's scope
- and raise NotImplementedError.
+(/root/reference/pkg/src/lowrank/sketch.py).  Random draws follow the
+reference's counter-based Philox keying (sketch.py:32-42) so the same
+(dimensions, seed) give bitwise the same Omega / D / R as the reference:
+Gaussian matrices are drawn on the device (lr_gaussian), the SRFT's D and R on
+the host (the permutation is sequential) and uploaded.  The SRFT runs as the
+shared-memory FFT (power-of-two n) or as a pass over A against the picked,
+D-scaled DFT columns (any n -- the linear map the reference evaluates with
+Bluestein for non-power-of-two lengths, sketch.py:155-176).  The
+Givens-chain variant (GSRFT) is outside this build's scope
+and raises NotImplementedError.
 """
 
 from __future__ import annotations
@@ -142,9 +145,6 @@ def srft_dev(A, op, amax=None):
     tensor-core pass over A (lr_srft_scaled)."""
     torch = _torch()
     m, n = A.shape
-    if n & (n - 1):
-        raise NotImplementedError(
-            "SRFT for non-power-of-two n needs the Bluestein path (SURVEY.md §8f #3)")
     cdt = _complex_of(A)
     code = _lib.dtype_code(cdt)
     h = _lib.handle(A.device.index)
@@ -177,7 +177,7 @@ def srft_apply(A, spec_or_op):
 
 def dft(v, axis=-1):
     """Unitary DFT along `axis`, f_pq = n^-1/2 exp(-2 pi i pq / n)
-    (sketch.py:179-200); power-of-two lengths only in this build."""
+    (sketch.py:179-200), any length."""
     torch = _torch()
     host = not is_device_array(v)
     t = to_device(v)
@@ -189,9 +189,8 @@ def dft(v, axis=-1):
     cdt = _complex_of(t)
     X = t.to(cdt).reshape(-1, n).contiguous()
     if n > 1:
-        if n & (n - 1):
-            raise NotImplementedError(
-                "dft for non-power-of-two n needs the Bluestein path (SURVEY.md §8f #3)")
+        # power of two: shared-memory radix-2 FFT; otherwise the dense DFT
+        # matrix product (same linear map as the reference's Bluestein path)
         _lib.call("lr_dft_rows", _lib.handle(X.device.index), _lib.dtype_code(cdt), X.shape[0], n,
                   _lib.ptr(X), _lib.ld(X))
     out = torch.movedim(X.reshape(shape), -1, axis)

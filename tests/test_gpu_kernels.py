@@ -298,20 +298,21 @@ def test_dft_and_srft_golden(golden):
     assert np.abs(m.dft(g["dft16_in"], axis=1) - g["dft16_out"]).max() <= 1e-13
     Y = m.srft_apply(g["srft_A"], m.srft_operator(16, 4, 1))
     assert np.abs(Y - g["srft_Y"]).max() <= 1e-13
-    with pytest.raises(NotImplementedError):
-        m.dft(g["dft12_in"], axis=1)
+    # non-power-of-two length (the reference's Bluestein path)
+    assert np.abs(m.dft(g["dft12_in"], axis=1) - g["dft12_out"]).max() <= 1e-13
 
 
-@pytest.mark.parametrize("n", [64, 1024, 8192])
+@pytest.mark.parametrize("n", [64, 1024, 8192, 12, 1000, 6000])
 def test_srft_vs_oracle(n):
     from oracle import lowrank_oracle as O
     A = rand((33, n), np.complex128, n)
-    op = O.srft_operator(n, 17, 9)
-    Y = lr().srft_apply(A, lr().srft_operator(n, 17, 9))
+    ell = min(17, n)
+    op = O.srft_operator(n, ell, 9)
+    Y = lr().srft_apply(A, lr().srft_operator(n, ell, 9))
     Yo = O.srft_apply(A, op)
     assert np.abs(Y - Yo).max() <= 1e-12 * np.abs(Yo).max()
     A32 = A.astype(np.complex64)
-    Y32 = lr().srft_apply(A32, lr().srft_operator(n, 17, 9))
+    Y32 = lr().srft_apply(A32, lr().srft_operator(n, ell, 9))
     assert np.abs(Y32 - Yo).max() <= 2e-5 * np.abs(Yo).max()
 
 
