@@ -172,8 +172,8 @@ int lr_estimate_tail(lr_handle_t h, int dtype, int64_t m, int64_t k, int64_t r,
                      const void* Q, int64_t ldq, void* Z, int64_t ldz,
                      double alpha, double* est);
 
-/* SRFT sketch (reference sketch.py:306-320): for complex A (m x n, n a
- * power of two), Y[:, t] = scale * (F_unitary (A_i * d))[picks[t]]. */
+/* SRFT sketch (reference sketch.py:306-320): for complex A (m x n, any n),
+ * Y[:, t] = scale * (F_unitary (A_i * d))[picks[t]]. */
 int lr_srft(lr_handle_t h, int dtype, int64_t m, int64_t n, int64_t ell,
             const void* A, int64_t lda, const void* d, const int32_t* picks,
             double scale, void* Y, int64_t ldy);
@@ -186,8 +186,22 @@ int lr_srft_scaled(lr_handle_t h, int dtype, int64_t m, int64_t n, int64_t ell,
                    const void* A, int64_t lda, double a_amax, const void* d,
                    const int32_t* picks, double scale, void* Y, int64_t ldy);
 
-/* Unitary DFT of each row of X (rows x n, n a power of two), in place
- * (reference sketch.py:179-200). */
+/* The ell picked columns of the Givens-chain SRFT (reference
+ * sketch.py:221-337, gsrft_operator / gsrft_apply):
+ *   Omega = D_outer Theta_outer D_mid Theta_inner D_inner F R scale,
+ *   Theta = P G_0 ... G_{n-2} (row-vector convention: x -> x[:, perm], then
+ *   column pairs (i, i+1) rotated by [[cos t_i, sin t_i], [-sin t_i, cos t_i]]).
+ * Inputs (device): d_* complex128 (n), perm_* int32 (n), thetas_* double
+ * (n-1), picks int32 (ell).  Output X (n x ell, row-major, dtype LR_C64 or
+ * LR_C128) such that gsrft_apply(A) = A X (one lr_gemm_scaled pass). */
+int lr_gsrft_matrix(lr_handle_t h, int dtype, int64_t n, int64_t ell, const void* d_outer,
+                    const int32_t* perm_outer, const double* thetas_outer, const void* d_mid,
+                    const int32_t* perm_inner, const double* thetas_inner, const void* d_inner,
+                    const int32_t* picks, double scale, void* X);
+
+/* Unitary DFT of each row of X (rows x n, any n), in place (reference
+ * sketch.py:179-200; radix-2 FFT for powers of two, the dense DFT product
+ * otherwise -- the linear map of the reference's Bluestein path). */
 int lr_dft_rows(lr_handle_t h, int dtype, int64_t rows, int64_t n, void* X, int64_t ldx);
 
 /* CSR SpMM (config 5): Y (m x ell) = S . X (n x ell) with int64 row

@@ -30,6 +30,7 @@ DEFAULT_ALPHA = 10.0
 # Philox stream tags, reference sketch.py:26-29 and rangefinder.py:78
 STREAM_GAUSS = 0x67617573      # "gaus"
 STREAM_SRFT = 0x73726674       # "srft"
+STREAM_GSRFT = 0x67737266      # "gsrf"  (sketch.py:28)
 STREAM_PROBE = 0x70726F62      # "prob"
 STREAM_SYNTH = 0x73796E74      # "synt"  (oracle.py:120)
 
@@ -154,6 +155,66 @@ def srft_apply(A, draw):
     if draw.n != A.shape[1]:
         raise ValueError("operator dimension does not match matrix columns")
     return dft(A * draw.d[None, :], axis=1)[:, draw.picks] * draw.scale
+
+
+@dataclass
+class GsrftDraw:
+    """Givens-chain SRFT draw (sketch.py:221-243): x -> x D'' Theta' D' Theta D F R."""
+    n: int
+    ell: int
+    d_outer: np.ndarray
+    perm_outer: np.ndarray
+    thetas_outer: np.ndarray
+    d_mid: np.ndarray
+    perm_inner: np.ndarray
+    thetas_inner: np.ndarray
+    d_inner: np.ndarray
+    picks: np.ndarray
+    scale: float
+
+
+def gsrft_operator(n, ell, seed):
+    """Draw order of sketch.py:259-275: d_outer, perm_outer, thetas_outer,
+    d_mid, perm_inner, thetas_inner, d_inner, picks -- one stream."""
+    if ell > n:
+        raise ValueError("sample count exceeds dimension")
+    g = rng_for(seed, STREAM_GSRFT)
+    d_outer = np.exp(2j * np.pi * g.random(n))
+    perm_outer = g.permutation(n)
+    thetas_outer = g.uniform(0.0, 2.0 * np.pi, max(n - 1, 0))
+    d_mid = np.exp(2j * np.pi * g.random(n))
+    perm_inner = g.permutation(n)
+    thetas_inner = g.uniform(0.0, 2.0 * np.pi, max(n - 1, 0))
+    d_inner = np.exp(2j * np.pi * g.random(n))
+    picks = g.permutation(n)[:ell]
+    return GsrftDraw(n, ell, d_outer, perm_outer, thetas_outer, d_mid, perm_inner,
+                     thetas_inner, d_inner, picks, float(np.sqrt(n / ell)))
+
+
+def givens_chain(X, perm, thetas):
+    """X[:, perm] then the ascending plane rotations on column pairs
+    (i, i+1): [a, b] <- [c a - s b, s a + c b]  (sketch.py:278-291)."""
+    Y = X[:, perm].astype(np.complex128, copy=True)
+    c, s = np.cos(thetas), np.sin(thetas)
+    for i in range(len(thetas)):
+        a = Y[:, i].copy()
+        b = Y[:, i + 1].copy()
+        Y[:, i] = c[i] * a - s[i] * b
+        Y[:, i + 1] = s[i] * a + c[i] * b
+    return Y
+
+
+def gsrft_apply(A, draw):
+    """Y = A Omega for the Givens-chain SRFT (sketch.py:323-337)."""
+    A = np.asarray(A)
+    if draw.n != A.shape[1]:
+        raise ValueError("operator dimension does not match matrix columns")
+    Y = A * draw.d_outer[None, :]
+    Y = givens_chain(Y, draw.perm_outer, draw.thetas_outer)
+    Y = Y * draw.d_mid[None, :]
+    Y = givens_chain(Y, draw.perm_inner, draw.thetas_inner)
+    Y = Y * draw.d_inner[None, :]
+    return dft(Y, axis=1)[:, draw.picks] * draw.scale
 
 
 # ---------------------------------------------------------------------------
@@ -374,6 +435,8 @@ class RangeBasis:
     power_q: int = 0
     seed: int = 0
     diagnostics: dict = field(default_factory=dict)
+    saturated: bool = False
+    probe_matvecs: int = 0
 
 
 def _check_ell(op, ell):
@@ -421,16 +484,71 @@ def subspace_iteration_range(A, ell, q, seed, ortho_tol=GS_DROP_TOL):
                       power_q=q, seed=seed)
 
 
-def fast_range_finder(A, ell, seed, ortho_tol=GS_DROP_TOL):
-    """Alg 4.5 with the SRFT (rangefinder.py:246-266)."""
+STREAM_ADAPT = 0x61646170      # "adap" (rangefinder.py:121)
+
+
+def adaptive_range_finder(A, eps, r=DEFAULT_PROBES, seed=0, alpha=DEFAULT_ALPHA, block=1):
+    """Alg 4.2 (rangefinder.py:89-159): grow the basis one vector at a time
+    from probe residuals y = (I - QQ*) A w; batch b of `block` probes is
+    drawn from Philox(seed, "adap", index = draws so far); stop once the r
+    oldest pending residual norms are <= eps / (alpha sqrt(2/pi))."""
+    if eps <= 0:
+        raise ValueError("eps must be positive")
+    if r < 1:
+        raise ValueError("r must be >= 1")
+    block = max(int(block), 1)
+    op = as_operator(A)
+    m, n = op.shape
+    threshold = eps / (alpha * math.sqrt(2.0 / math.pi))
+    draws = 0
+    pending, cols = [], []
+    saturated = False
+    while True:
+        while len(pending) < r:
+            W = rng_for(seed, STREAM_ADAPT, draws).standard_normal((n, block))
+            draws += block
+            fresh = op.apply(W)
+            if cols:
+                Qc = np.column_stack(cols)
+                fresh = fresh - Qc @ (Qc.conj().T @ fresh)
+            pending.extend(fresh[:, i] for i in range(fresh.shape[1]))
+        if max(np.linalg.norm(y) for y in pending[:r]) <= threshold:
+            break
+        y = pending.pop(0)
+        Q = np.column_stack(cols) if cols else np.zeros((m, 0))
+        y = y - Q @ (Q.conj().T @ y)
+        nrm = np.linalg.norm(y)
+        if nrm == 0.0:
+            continue
+        q = y / nrm
+        cols.append(q)
+        if len(cols) >= min(m, n):
+            saturated = True
+            break
+        for i in range(len(pending)):
+            pending[i] = pending[i] - q * np.vdot(q, pending[i])
+    Q = np.column_stack(cols) if cols else np.zeros((m, 0))
+    est = (alpha * math.sqrt(2.0 / math.pi) * max(np.linalg.norm(y) for y in pending[:r])
+           if pending else 0.0)
+    return RangeBasis(Q=Q, samples_used=draws, passes=1, est_error=float(est), kind="gaussian",
+                      ell=1, seed=seed, saturated=saturated, probe_matvecs=r)
+
+
+def fast_range_finder(A, ell, seed, ortho_tol=GS_DROP_TOL, kind="srft"):
+    """Alg 4.5 with the SRFT or its Givens-chain variant (rangefinder.py:246-266)."""
     A = np.asarray(A)
-    Y = srft_apply(A, srft_operator(A.shape[1], ell, seed))
+    if kind not in ("srft", "gsrft"):
+        raise ValueError("kind must be 'srft' or 'gsrft'")
+    if kind == "srft":
+        Y = srft_apply(A, srft_operator(A.shape[1], ell, seed))
+    else:
+        Y = gsrft_apply(A, gsrft_operator(A.shape[1], ell, seed))
     diag = {}
     if not np.iscomplexobj(A):
         diag["max_imag_sample"] = float(np.abs(Y.imag).max())
     Q = orthonormalize_double_gs(Y, tol=ortho_tol)
     return RangeBasis(Q=Q, samples_used=ell, passes=1,
-                      est_error=0.0 if Q.shape[1] == 0 else None, kind="srft",
+                      est_error=0.0 if Q.shape[1] == 0 else None, kind=kind,
                       ell=ell, seed=seed, diagnostics=diag)
 
 
@@ -537,7 +655,7 @@ def rsvd(A, k, p, q, seed, sketch="gauss", probes=DEFAULT_PROBES, alpha=DEFAULT_
     else:
         if q > 0:
             raise ValueError("power iterations are not available with structured sketches")
-        basis = fast_range_finder(op.array, ell, seed)
+        basis = fast_range_finder(op.array, ell, seed, kind=sketch)
     f = direct_svd(op, basis.Q)
     est = basis.est_error
     if est is None and estimate:

@@ -21,7 +21,7 @@ from .factor import PartialSVD, direct_svd, randomized_svd, truncate_rank
 from .rangefinder import (RangeBasis, adaptive_range_finder, adaptive_range_finder_blocked,
                           fast_range_finder, posterior_error_estimate, power_iteration_range,
                           randomized_range_finder, subspace_iteration_range)
-from .sketch import (SketchSpec, SrftOperator, dft, gaussian_matrix, gsrft_apply,
+from .sketch import (GsrftOperator, SketchSpec, SrftOperator, dft, gaussian_matrix, gsrft_apply,
                      gsrft_operator, rng_for, srft_apply, srft_operator)
 from .sparse import CudaCsrOperator
 

@@ -64,6 +64,8 @@ _SIGS = {
     "lr_srft_scaled": [_vp, _int, _i64, _i64, _i64, _vp, _i64, C.c_double, _vp, _vp, C.c_double,
                        _vp, _i64],
     "lr_dft_rows": [_vp, _int, _i64, _i64, _vp, _i64],
+    "lr_gsrft_matrix": [_vp, _int, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                        C.c_double, _vp],
     "lr_csr_spmm": [_vp, _int, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _i64, _vp, _i64, _int],
     "lr_check_finite": [_vp, _int, _i64, _i64, _vp, _i64, _vp, _vp],
     "lr_copy": [_vp, _int, _vp, _i64, _int, _vp, _i64, _i64, _i64, _int],

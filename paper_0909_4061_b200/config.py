@@ -1,4 +1,4 @@
-"""Numerical defaults of the hot path (reference config.py:9,19,22-23)."""
+"""Numerical defaults of the hot path (reference config.py:9,19,22-23,26)."""
 
 # Gram-Schmidt drop tolerance relative to ||Y||_F (orthonormalize_double_gs).
 GS_DROP_TOL = 1e-10
@@ -9,3 +9,6 @@ DEFAULT_OVERSAMPLE = 5
 # Posterior error estimator: probe count and inflation factor.
 DEFAULT_PROBES = 10
 DEFAULT_ALPHA = 10.0
+
+# Probe batch of the blocked adaptive range finder.
+ADAPTIVE_BLOCK = 8

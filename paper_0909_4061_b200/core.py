@@ -222,28 +222,47 @@ class DenseOperator(MatVecOperator):
         return self.array.dtype
 
     def _prep(self, X):
+        torch = _torch()
         host = not is_device_array(X)
-        t = to_device(X, self.array.dtype, self.array.device.index)
+        dt = self.array.dtype
+        if not self.array.is_complex() and (np.iscomplexobj(X) if not torch.is_tensor(X)
+                                            else X.is_complex()):
+            # real A times a complex block (e.g. the complex SRFT basis of a
+            # real matrix): keep X complex, the pass runs on its real view
+            dt = torch.complex64 if dt == torch.float32 else torch.complex128
+        t = to_device(X, dt, self.array.device.index)
         t, vec = _as2d(t)
         return t, host, vec
 
-    def _apply(self, X):
+    def _run(self, t, adjoint):
+        """One pass; a complex t against a real A goes through the real view
+        (A^H [Re Im] interleaved == A^H X since A is real)."""
         torch = _torch()
+        rows = self.n if adjoint else self.m
+        if t.is_complex() and not self.array.is_complex():
+            tc = t.contiguous()
+            tr = torch.view_as_real(tc).reshape(tc.shape[0], 2 * tc.shape[1])
+            Yr = torch.empty((rows, 2 * tc.shape[1]), dtype=self.array.dtype,
+                             device=self.array.device)
+            _timed_pass(self.array, tr, Yr, adjoint, self.amax)
+            return torch.view_as_complex(Yr.reshape(rows, tc.shape[1], 2))
+        Y = torch.empty((rows, t.shape[1]), dtype=self.array.dtype, device=self.array.device)
+        _timed_pass(self.array, t, Y, adjoint, self.amax)
+        return Y
+
+    def _apply(self, X):
         t, host, vec = self._prep(X)
         if t.shape[0] != self.n:
             raise ValueError(f"dimension mismatch: A is {self.shape}, X has {t.shape[0]} rows")
-        Y = torch.empty((self.m, t.shape[1]), dtype=self.array.dtype, device=self.array.device)
-        _timed_pass(self.array, t, Y, False, self.amax)
+        Y = self._run(t, False)
         Y = Y.reshape(-1) if vec else Y
         return _out(Y, host)
 
     def _apply_adjoint(self, Y):
-        torch = _torch()
         t, host, vec = self._prep(Y)
         if t.shape[0] != self.m:
             raise ValueError(f"dimension mismatch: A is {self.shape}, Y has {t.shape[0]} rows")
-        Z = torch.empty((self.n, t.shape[1]), dtype=self.array.dtype, device=self.array.device)
-        _timed_pass(self.array, t, Z, True, self.amax)
+        Z = self._run(t, True)
         Z = Z.reshape(-1) if vec else Z
         return _out(Z, host)
 

@@ -825,6 +825,21 @@ int lr_srft(lr_handle_t hh, int dtype, int64_t m, int64_t n, int64_t ell, const 
   return lr_srft_scaled(hh, dtype, m, n, ell, A, lda, -1.0, d, picks, scale, Y, ldy);
 }
 
+int lr_gsrft_matrix(lr_handle_t hh, int dtype, int64_t n, int64_t ell, const void* d_outer,
+                    const int32_t* perm_outer, const double* thetas_outer, const void* d_mid,
+                    const int32_t* perm_inner, const double* thetas_inner, const void* d_inner,
+                    const int32_t* picks, double scale, void* X) {
+  API_BEGIN
+  Handle* h = H(hh);
+  LR_REQUIRE(dtype == LR_C64 || dtype == LR_C128, LR_EINVAL, "lr_gsrft_matrix: complex only");
+  LR_REQUIRE(n >= 1 && ell >= 1 && ell <= n, LR_EINVAL, "lr_gsrft_matrix: need 1 <= ell <= n");
+  lr::pool_reset(h);
+  lr::gsrft_matrix(h, dtype, n, ell, static_cast<const double2*>(d_outer), perm_outer,
+                   thetas_outer, static_cast<const double2*>(d_mid), perm_inner, thetas_inner,
+                   static_cast<const double2*>(d_inner), picks, scale, X);
+  API_END
+}
+
 int lr_dft_rows(lr_handle_t hh, int dtype, int64_t rows, int64_t n, void* X, int64_t ldx) {
   API_BEGIN
   Handle* h = H(hh);

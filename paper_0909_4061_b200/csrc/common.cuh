@@ -223,6 +223,11 @@ void scale_col(Handle* h, int dtype, int64_t rows, const void* src, int64_t lds,
                void* dst, int64_t ldd);
 
 // srft.cu ---------------------------------------------------------------------
+// n x ell picked columns of the Givens-chain SRFT (c64 or c128 output)
+void gsrft_matrix(Handle* h, int dtype, int64_t n, int64_t ell, const double2* d_outer,
+                  const int32_t* perm_outer, const double* thetas_outer, const double2* d_mid,
+                  const int32_t* perm_inner, const double* thetas_inner, const double2* d_inner,
+                  const int32_t* picks, double scale, void* Xout);
 void srft_c64(Handle* h, int64_t m, int64_t n, int64_t ell, const float2* A, int64_t lda,
               const float2* d, const int32_t* picks, float scale, float2* Y, int64_t ldy,
               double a_amax = -1.0);

@@ -153,7 +153,79 @@ void srft_gemm(Handle* h, int64_t m, int64_t n, int64_t ell, const C* A, int64_t
 
 bool pow2(int64_t n) { return n >= 1 && (n & (n - 1)) == 0; }
 
+// ---- Givens-chain SRFT (reference sketch.py:221-337) -----------------------
+// Omega = D'' Theta' D' Theta D F R with Theta = P G_0 ... G_{n-2} acting on
+// row vectors (x -> x P: x[:, perm]; G_i rotates columns (i, i+1) by
+// [[c, s], [-s, c]]).  Its ell picked columns are built right to left on the
+// device -- X = D F_R, then X <- G_0 ... G_{n-2} X, X <- P X, X <- D' X, ... --
+// after which Y = A X is one pass over A.
+
+// X <- G_0 G_1 ... G_{n-2} X (G_{n-2} applied first): one thread per column,
+// the carried row i is the only state between consecutive rotations.
+__global__ void givens_rows_kernel(int64_t n, int64_t ell, const double* __restrict__ thetas,
+                                   double2* __restrict__ X) {
+  const int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (t >= ell || n < 2) return;
+  double2 hi = X[(n - 1) * ell + t];              // row i+1, updated in place
+  for (int64_t i = n - 2; i >= 0; --i) {
+    const double2 lo = X[i * ell + t];
+    double sv, cv;
+    sincos(thetas[i], &sv, &cv);
+    // (G_i X)[i] = c x_i + s x_{i+1};  (G_i X)[i+1] = -s x_i + c x_{i+1}
+    const double2 ni = make_double2(cv * lo.x + sv * hi.x, cv * lo.y + sv * hi.y);
+    const double2 nh = make_double2(-sv * lo.x + cv * hi.x, -sv * lo.y + cv * hi.y);
+    X[(i + 1) * ell + t] = nh;
+    hi = ni;
+  }
+  X[t] = hi;
+}
+
+// Y[perm[j], :] = d[perm[j]] * X[j, :]   (P X, then the diagonal D)
+__global__ void permute_scale_rows(int64_t n, int64_t ell, const int32_t* __restrict__ perm,
+                                   const double2* __restrict__ d, const double2* __restrict__ X,
+                                   double2* __restrict__ Y) {
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n * ell;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t j = e / ell, t = e - j * ell;
+    const int64_t r = perm[j];
+    const double2 x = X[e], w = d[r];
+    Y[r * ell + t] = make_double2(w.x * x.x - w.y * x.y, w.x * x.y + w.y * x.x);
+  }
+}
+
+__global__ void to_c64(int64_t count, const double2* __restrict__ X, float2* __restrict__ Y) {
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < count;
+       e += int64_t(gridDim.x) * blockDim.x)
+    Y[e] = make_float2(float(X[e].x), float(X[e].y));
+}
+
 }  // namespace
+
+void gsrft_matrix(Handle* h, int dtype, int64_t n, int64_t ell, const double2* d_outer,
+                  const int32_t* perm_outer, const double* thetas_outer, const double2* d_mid,
+                  const int32_t* perm_inner, const double* thetas_inner, const double2* d_inner,
+                  const int32_t* picks, double scale, void* Xout) {
+  const size_t cnt = size_t(n) * ell;
+  double2* X = pool_alloc_t<double2>(h, cnt);
+  double2* T = pool_alloc_t<double2>(h, cnt);
+  const int blocks = int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(int64_t(cnt), 256), 8192)));
+  const int cb = int(ceil_div(ell, 128));
+  srft_matrix_kernel<double2><<<blocks, 256, 0, h->stream>>>(n, ell, d_inner, picks, scale, X);
+  LR_CHECK_LAUNCH();
+  givens_rows_kernel<<<cb, 128, 0, h->stream>>>(n, ell, thetas_inner, X);
+  LR_CHECK_LAUNCH();
+  permute_scale_rows<<<blocks, 256, 0, h->stream>>>(n, ell, perm_inner, d_mid, X, T);
+  LR_CHECK_LAUNCH();
+  givens_rows_kernel<<<cb, 128, 0, h->stream>>>(n, ell, thetas_outer, T);
+  LR_CHECK_LAUNCH();
+  double2* out = dtype == LR_C128 ? static_cast<double2*>(Xout) : X;
+  permute_scale_rows<<<blocks, 256, 0, h->stream>>>(n, ell, perm_outer, d_outer, T, out);
+  LR_CHECK_LAUNCH();
+  if (dtype == LR_C64) {
+    to_c64<<<blocks, 256, 0, h->stream>>>(int64_t(cnt), X, static_cast<float2*>(Xout));
+    LR_CHECK_LAUNCH();
+  }
+}
 
 // complex64 SRFT: for ell <= 128 as a pass over A on the tcgen05 tensor
 // cores (Y = A X with the picked DFT columns, three-product split, the same

@@ -19,7 +19,7 @@ from .core import (_out, _torch, apply_dev, as_operator, gemm_dev, is_device_arr
 from .rangefinder import (RangeBasis, SketchSpec, _cast_like_op, _check_ell, _host_io,
                           _sketch_dev, orth_dev, posterior_error_estimate_dev, probes_dev,
                           subspace_iteration_range_dev)
-from .sketch import srft_dev, srft_operator
+from .sketch import gsrft_dev, gsrft_operator, srft_dev, srft_operator
 
 
 @dataclass
@@ -93,7 +93,7 @@ def randomized_svd(A, k, p=config.DEFAULT_OVERSAMPLE, q=0, seed=0, sketch="gauss
         _check_ell(op, ell)
         passes = 2 * q + 2 if q > 0 else 1
         spec = SketchSpec(kind="gaussian", ell=ell, power_q=q, seed=seed)
-    elif sketch == "srft":
+    elif sketch in ("srft", "gsrft"):
         if q > 0:
             raise ValueError("power iterations are not available with structured sketches")
         if ell > op.n:
@@ -101,13 +101,14 @@ def randomized_svd(A, k, p=config.DEFAULT_OVERSAMPLE, q=0, seed=0, sketch="gauss
         if not hasattr(op, "array"):
             raise TypeError("the SRFT sketch needs a dense matrix")
         passes = 1
-        spec = SketchSpec(kind="srft", ell=ell, seed=seed)
+        spec = SketchSpec(kind=sketch, ell=ell, seed=seed)
     else:
         raise ValueError(f"unknown sketch {sketch!r}")
 
     # SRFT draws (d, picks) come from the host Philox stream (permutation is
     # sequential); Gaussian Omega / probes are drawn on the device in body().
-    srft = srft_operator(op.n, ell, seed) if spec.kind == "srft" else None
+    srft = (srft_operator(op.n, ell, seed) if spec.kind == "srft" else
+            gsrft_operator(op.n, ell, seed) if spec.kind == "gsrft" else None)
 
     def body():
         W = probes_dev(op, probes, seed + 13) if estimate else None
@@ -117,8 +118,10 @@ def randomized_svd(A, k, p=config.DEFAULT_OVERSAMPLE, q=0, seed=0, sketch="gauss
                 Q = subspace_iteration_range_dev(op, ell, q, seed, omega=omega)
             else:
                 Q = orth_dev(apply_dev(op, omega))
-        else:
+        elif spec.kind == "srft":
             Q = orth_dev(srft_dev(op.array, srft, amax=getattr(op, "amax", None)))
+        else:
+            Q = orth_dev(gsrft_dev(op.array, srft, amax=getattr(op, "amax", None)))
         U, S, V = direct_svd_dev(op, Q)
         est_dev = None
         if estimate and Q.shape[1]:

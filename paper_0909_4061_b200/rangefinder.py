@@ -18,9 +18,10 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib, config
-from .core import (MatVecOperator, _out, _torch, apply_dev, as_operator, cast_dev,
+from .core import (MatVecOperator, _out, _torch, apply_dev, as_operator, cast_dev, gemm,
                    is_device_array, orth_dev, to_device)
-from .sketch import SketchSpec, gaussian_dev, srft_dev, srft_operator
+from .sketch import (SketchSpec, gaussian_dev, gsrft_dev, gsrft_operator, srft_dev,
+                     srft_operator)
 
 _STREAM_PROBE = 0x70726F62
 
@@ -172,8 +173,6 @@ def fast_range_finder(A, ell, seed, kind="srft", ortho_tol=config.GS_DROP_TOL):
     torch = _torch()
     if kind not in ("srft", "gsrft"):
         raise ValueError("kind must be 'srft' or 'gsrft'")
-    if kind == "gsrft":
-        raise NotImplementedError("GSRFT is outside this build's scope (SURVEY.md §8f #3)")
     if isinstance(A, MatVecOperator):
         if not hasattr(A, "array"):
             raise TypeError("fast_range_finder needs a dense matrix")
@@ -183,8 +182,10 @@ def fast_range_finder(A, ell, seed, kind="srft", ortho_tol=config.GS_DROP_TOL):
         t = to_device(A)
         amax = None
     spec = SketchSpec(kind=kind, ell=ell, seed=seed)
-    op = srft_operator(t.shape[1], ell, seed)
-    Y = srft_dev(t, op, amax=amax)
+    if kind == "srft":
+        Y = srft_dev(t, srft_operator(t.shape[1], ell, seed), amax=amax)
+    else:
+        Y = gsrft_dev(t, gsrft_operator(t.shape[1], ell, seed), amax=amax)
     diagnostics = {}
     if not t.is_complex():
         out = torch.empty(1, dtype=torch.float64, device=Y.device)
@@ -212,7 +213,11 @@ def posterior_error_estimate_dev(op, Q, r=config.DEFAULT_PROBES, alpha=config.DE
     Z = apply_dev(op, W)
     Z = Z.contiguous() if Z.stride(-1) != 1 else Z
     est = torch.empty(1, dtype=torch.float64, device=Z.device)
-    Qd = cast_dev(Q if is_device_array(Q) else to_device(Q), Z.dtype)
+    Qd = Q if is_device_array(Q) else to_device(Q)
+    if Qd.is_complex() and not Z.is_complex():
+        # complex (SRFT) basis of a real operator: project in complex
+        Z = cast_dev(Z, torch.complex64 if Z.dtype == torch.float32 else torch.complex128)
+    Qd = cast_dev(Qd, Z.dtype)
     k = Qd.shape[1] if Qd.dim() == 2 else 0
     _lib.call("lr_estimate_tail", _lib.handle(Z.device.index), _lib.dtype_code(Z.dtype),
               Z.shape[0], k, r, _lib.ptr(Qd) if k else _lib.ptr(None), _lib.ld(Qd) if k else 1,
@@ -231,9 +236,116 @@ def posterior_error_estimate(A, Q, r=config.DEFAULT_PROBES, alpha=config.DEFAULT
     return float(posterior_error_estimate_dev(op, Q, r, alpha, seed).item())
 
 
-def adaptive_range_finder(*args, **kwargs):
-    raise NotImplementedError(
-        "the adaptive (fixed-precision) finder is outside this build's scope (SURVEY.md §8f #1)")
+_STREAM_ADAPT = 0x61646170      # "adap" (rangefinder.py:121)
 
 
-adaptive_range_finder_blocked = adaptive_range_finder
+def adaptive_range_finder(A, eps, r=config.DEFAULT_PROBES, seed=0, alpha=config.DEFAULT_ALPHA,
+                          block=1):
+    """Alg 4.2 fixed-precision range finder (rangefinder.py:89-159) on the
+    GPU: the basis grows one vector at a time from probe residuals
+    y = (I - QQ*) A w, probes drawn in batches of `block` from
+    Philox(seed, "adap", index = draws so far); the loop stops once the r
+    oldest pending residual norms are <= eps / (alpha sqrt(2/pi)), or with
+    `saturated` when the basis reaches min(m, n) columns.  Same reprojection
+    (double orthogonalization) and incremental downdate of the pending probes
+    as the reference; Q, the pending block and all products stay on the
+    device, and each step reads two norms back (the stopping test and the
+    new vector's norm)."""
+    if eps <= 0:
+        raise ValueError("eps must be positive")
+    if r < 1:
+        raise ValueError("r must be >= 1")
+    block = max(int(block), 1)
+    torch = _torch()
+    op = as_operator(A)
+    host = _host_io(A, op)
+    m, n = op.shape
+    threshold = eps / (alpha * math.sqrt(2.0 / math.pi))
+    dt = _op_dtype(op)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    kmax = min(m, n)
+    Qb = torch.empty((m, kmax), dtype=dt, device=dev)
+    k = 0
+    cap = r + block + 32
+    Pm = torch.empty((m, cap), dtype=dt, device=dev)
+    head = cnt = 0
+    draws = 0
+    saturated = False
+    code = _lib.dtype_code(dt)
+    h = _lib.handle()
+
+    def project(X):
+        """X <- X - Q (Q^H X) for the current basis."""
+        if k:
+            Qk = Qb[:, :k]
+            C = torch.empty((k, X.shape[1]), dtype=dt, device=dev)
+            gemm(Qk, X, C, adjoint=True)
+            T = torch.empty_like(X)
+            gemm(Qk, C, T)
+            _lib.call("lr_axpy_sub", h, code, X.shape[0], X.shape[1], _lib.ptr(T), _lib.ld(T),
+                      _lib.ptr(X), _lib.ld(X))
+
+    def norms(X):
+        out = torch.empty(X.shape[1], dtype=torch.float64, device=dev)
+        _lib.call("lr_col_sumsq", h, code, X.shape[0], X.shape[1], _lib.ptr(X), _lib.ld(X),
+                  _lib.ptr(out))
+        return torch.sqrt(out)
+
+    while True:
+        while cnt < r:
+            W = cast_dev(gaussian_dev(n, block, seed, stream=_STREAM_ADAPT, index=draws,
+                                      dtype=_real_of(dt)), dt)
+            draws += block
+            fresh = apply_dev(op, W)
+            if fresh.dim() == 1:
+                fresh = fresh.reshape(-1, 1)
+            fresh = fresh.contiguous()
+            project(fresh)
+            if head + cnt + block > cap:                    # compact the pending block
+                Pm[:, :cnt] = Pm[:, head:head + cnt].clone()
+                head = 0
+                if cnt + block > cap:
+                    cap = 2 * (cnt + block)
+                    P2 = torch.empty((m, cap), dtype=dt, device=dev)
+                    P2[:, :cnt] = Pm[:, :cnt]
+                    Pm = P2
+            Pm[:, head + cnt:head + cnt + block] = fresh
+            cnt += block
+        if float(norms(Pm[:, head:head + r]).max().item()) <= threshold:
+            break
+        y = Pm[:, head:head + 1].clone()
+        head += 1
+        cnt -= 1
+        project(y)
+        nrm = float(norms(y)[0].item())
+        if nrm == 0.0:
+            continue
+        qk = Qb[:, k:k + 1]
+        _lib.call("lr_scale_col", h, code, m, _lib.ptr(y), _lib.ld(y), 1.0 / nrm, _lib.ptr(qk),
+                  _lib.ld(qk))
+        k += 1
+        if k >= kmax:
+            saturated = True
+            break
+        if cnt:
+            # pending_i <- pending_i - q (q^H pending_i)
+            act = Pm[:, head:head + cnt]
+            c = torch.empty((1, cnt), dtype=dt, device=dev)
+            gemm(qk, act, c, adjoint=True)
+            T = torch.empty((m, cnt), dtype=dt, device=dev)
+            gemm(qk, c, T)
+            _lib.call("lr_axpy_sub", h, code, m, cnt, _lib.ptr(T), _lib.ld(T), _lib.ptr(act),
+                      _lib.ld(act))
+    Q = Qb[:, :k].contiguous()
+    est = (alpha * math.sqrt(2.0 / math.pi) * float(norms(Pm[:, head:head + min(r, cnt)]).max().item())
+           if cnt else 0.0)
+    spec = SketchSpec(kind="gaussian", ell=1, seed=seed)
+    return RangeBasis(Q=_out(Q, host), samples_used=draws, passes=1, est_error=float(est),
+                      spec=spec, saturated=saturated, probe_matvecs=r)
+
+
+def adaptive_range_finder_blocked(A, eps, r=config.DEFAULT_PROBES, seed=0,
+                                  alpha=config.DEFAULT_ALPHA, block=config.ADAPTIVE_BLOCK):
+    """Blocked adaptive finder: draws probes in batches of `block`
+    (rangefinder.py:162-166)."""
+    return adaptive_range_finder(A, eps, r=r, seed=seed, alpha=alpha, block=block)

@@ -9,8 +9,9 @@ the host (the permutation is sequential) and uploaded.  The SRFT runs as the
 shared-memory FFT (power-of-two n) or as a pass over A against the picked,
 D-scaled DFT columns (any n -- the linear map the reference evaluates with
 Bluestein for non-power-of-two lengths, sketch.py:155-176).  The
-Givens-chain variant (GSRFT) is outside this build's scope
-and raises NotImplementedError.
+Givens-chain variant (GSRFT) builds the ell picked columns of its Omega on
+the device (two rotation chains, permutations and diagonals applied to the
+picked DFT columns) and is then one pass over A as well.
 """
 
 from __future__ import annotations
@@ -116,13 +117,15 @@ def srft_operator(n, ell, seed):
     return SrftOperator(n=n, ell=ell, d=d, picks=picks, scale=float(np.sqrt(n / ell)))
 
 
-def _resolve(spec_or_op, n):
-    if isinstance(spec_or_op, SrftOperator):
+def _resolve(spec_or_op, n, op_type=None, builder=None):
+    """Materialize a SketchSpec (or pass an operator through), as the
+    reference's _resolve (sketch.py:294-303)."""
+    op_type = op_type or SrftOperator
+    builder = builder or srft_operator
+    if isinstance(spec_or_op, op_type):
         op = spec_or_op
     elif isinstance(spec_or_op, SketchSpec):
-        if spec_or_op.kind == "gsrft":
-            raise NotImplementedError("GSRFT is outside this build's scope (SURVEY.md §8f #3)")
-        op = srft_operator(n, spec_or_op.ell, spec_or_op.seed)
+        op = builder(n, spec_or_op.ell, spec_or_op.seed)
     else:
         raise TypeError("expected a SketchSpec or a materialized operator")
     if op.n != n:
@@ -197,9 +200,98 @@ def dft(v, axis=-1):
     return _out(out, host)
 
 
+@dataclass
+class GsrftOperator:
+    """Givens-chain SRFT draw (sketch.py:221-243): applied to a row vector x
+    as x D'' Theta' D' Theta D F R, each Theta a random permutation followed
+    by the ascending chain of plane rotations G(i, i+1; theta_i)."""
+
+    n: int
+    ell: int
+    d_outer: np.ndarray
+    perm_outer: np.ndarray
+    thetas_outer: np.ndarray
+    d_mid: np.ndarray
+    perm_inner: np.ndarray
+    thetas_inner: np.ndarray
+    d_inner: np.ndarray
+    picks: np.ndarray
+    scale: float
+
+    def to_dense(self):
+        return gsrft_apply(np.eye(self.n), self)
+
+
 def gsrft_operator(n, ell, seed):
-    raise NotImplementedError("GSRFT is outside this build's scope (SURVEY.md §8f #3)")
+    """Draw order of sketch.py:259-275 (one Philox stream, host side)."""
+    if ell > n:
+        raise ValueError("sample count exceeds dimension")
+    rng = rng_for(seed, _STREAM_GSRFT)
+
+    def unimodular():
+        return np.exp(2j * np.pi * rng.random(n))
+
+    d_outer = unimodular()
+    perm_outer = rng.permutation(n)
+    thetas_outer = rng.uniform(0.0, 2.0 * np.pi, max(n - 1, 0))
+    d_mid = unimodular()
+    perm_inner = rng.permutation(n)
+    thetas_inner = rng.uniform(0.0, 2.0 * np.pi, max(n - 1, 0))
+    d_inner = unimodular()
+    picks = rng.permutation(n)[:ell]
+    return GsrftOperator(n=n, ell=ell, d_outer=d_outer, perm_outer=perm_outer,
+                         thetas_outer=thetas_outer, d_mid=d_mid, perm_inner=perm_inner,
+                         thetas_inner=thetas_inner, d_inner=d_inner, picks=picks,
+                         scale=float(np.sqrt(n / ell)))
+
+
+def gsrft_matrix_dev(op, dtype, device):
+    """The ell picked columns of the GSRFT (n x ell, complex) built on the
+    device (lr_gsrft_matrix): gsrft_apply(A) = A @ this."""
+    torch = _torch()
+    dev = torch.device("cuda", device)
+
+    def c(x):
+        return torch.from_numpy(np.ascontiguousarray(x, dtype=np.complex128)).to(dev)
+
+    def i32(x):
+        return torch.from_numpy(np.ascontiguousarray(x, dtype=np.int32)).to(dev)
+
+    def f64(x):
+        return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).to(dev)
+
+    arrs = (c(op.d_outer), i32(op.perm_outer), f64(op.thetas_outer), c(op.d_mid),
+            i32(op.perm_inner), f64(op.thetas_inner), c(op.d_inner), i32(op.picks))
+    X = torch.empty((op.n, op.ell), dtype=dtype, device=dev)
+    _lib.call("lr_gsrft_matrix", _lib.handle(device), _lib.dtype_code(dtype), op.n, op.ell,
+              *[_lib.ptr(a) for a in arrs], float(op.scale), _lib.ptr(X))
+    return X
+
+
+def gsrft_dev(A, op, amax=None):
+    """Y = A Omega_gsrft for a device matrix A: the picked columns of Omega
+    are built on the device, then one pass over A (lr_gemm_scaled)."""
+    from .core import _pass
+    torch = _torch()
+    m, n = A.shape
+    cdt = _complex_of(A)
+    if A.dtype != cdt:
+        Ac = torch.empty((m, n), dtype=cdt, device=A.device)
+        _lib.call("lr_copy", _lib.handle(A.device.index), _lib.dtype_code(A.dtype), _lib.ptr(A),
+                  _lib.ld(A), _lib.dtype_code(cdt), _lib.ptr(Ac), _lib.ld(Ac), m, n, 0)
+        A = Ac
+    X = gsrft_matrix_dev(op, cdt, A.device.index)
+    Y = torch.empty((m, op.ell), dtype=cdt, device=A.device)
+    _pass(A, X, Y, False, amax)
+    return Y
 
 
 def gsrft_apply(A, spec_or_op):
-    raise NotImplementedError("GSRFT is outside this build's scope (SURVEY.md §8f #3)")
+    """Y = A @ Omega for a Givens-chain SRFT Omega (sketch.py:323-337), on the
+    GPU; same contract as srft_apply."""
+    host = not is_device_array(A)
+    t = to_device(A)
+    if t.dim() != 2:
+        raise ValueError("A must be 2-D")
+    op = _resolve(spec_or_op, t.shape[1], GsrftOperator, gsrft_operator)
+    return _out(gsrft_dev(t, op), host)

@@ -101,6 +101,35 @@ def g_kats():
     b = rangefinder.fast_range_finder(A[:, :16], 5, 4)
     out["rf_fast_Q"] = b.Q
     out["rf_fast_maximag"] = np.array([b.diagnostics["max_imag_sample"]])
+    # Givens-chain SRFT (sketch.py:221-337): draws, apply (power-of-two and
+    # not), and the fast range finder with kind="gsrft"
+    g = sketch.gsrft_operator(16, 4, 2)
+    for f in ("d_outer", "perm_outer", "thetas_outer", "d_mid", "perm_inner", "thetas_inner",
+              "d_inner", "picks"):
+        out[f"gsrft16_{f}"] = getattr(g, f)
+    rng = np.random.default_rng(12)
+    A = rng.standard_normal((5, 16)) + 1j * rng.standard_normal((5, 16))
+    out["gsrft_A"], out["gsrft_Y"] = A, sketch.gsrft_apply(A, g)
+    A = rng.standard_normal((4, 12))
+    out["gsrft12_A"], out["gsrft12_Y"] = A, sketch.gsrft_apply(A, sketch.gsrft_operator(12, 5, 7))
+    b = rangefinder.fast_range_finder(out["rf_A"][:, :16], 5, 4, kind="gsrft")
+    out["rf_gsrft_Q"] = b.Q
+    # adaptive fixed-precision range finder (rangefinder.py:89-166), single and
+    # blocked draws, on a matrix with a decaying spectrum
+    rng = np.random.default_rng(13)
+    U = np.linalg.qr(rng.standard_normal((60, 40)))[0]
+    V = np.linalg.qr(rng.standard_normal((50, 40)))[0]
+    A = (U * np.exp(-np.arange(40) / 3.0)) @ V.T
+    out["ad_A"] = A
+    for blk in (1, 4):
+        b = rangefinder.adaptive_range_finder(A, 1e-3, r=10, seed=5, block=blk)
+        out[f"ad{blk}_Q"] = b.Q
+        out[f"ad{blk}_meta"] = np.array([b.samples_used, b.passes, b.est_error,
+                                         float(b.saturated), b.probe_matvecs])
+    b = rangefinder.adaptive_range_finder(A[:, :8], 1e-12, r=4, seed=2)
+    out["ad_sat_Q"] = b.Q
+    out["ad_sat_meta"] = np.array([b.samples_used, b.passes, b.est_error, float(b.saturated),
+                                   b.probe_matvecs])
     save("kats", **out)
 
 

@@ -316,6 +316,26 @@ def test_srft_vs_oracle(n):
     assert np.abs(Y32 - Yo).max() <= 2e-5 * np.abs(Yo).max()
 
 
+def test_gsrft_golden_and_oracle(golden):
+    """Givens-chain SRFT (reference sketch.py:221-337) on the device: the
+    reference's own outputs (power-of-two and not) and the oracle at size."""
+    from oracle import lowrank_oracle as O
+    g = golden("kats")
+    m = lr()
+    Y = m.gsrft_apply(g["gsrft_A"], m.gsrft_operator(16, 4, 2))
+    assert np.abs(Y - g["gsrft_Y"]).max() <= 1e-12
+    Y = m.gsrft_apply(g["gsrft12_A"], m.gsrft_operator(12, 5, 7))
+    assert np.abs(Y - g["gsrft12_Y"]).max() <= 1e-12
+    b = m.fast_range_finder(g["rf_A"][:, :16], 5, 4, kind="gsrft")
+    assert np.abs(b.Q - g["rf_gsrft_Q"]).max() <= 1e-10
+    for n, dt, tol in [(1024, np.complex128, 1e-11), (1000, np.complex128, 1e-11),
+                       (2048, np.complex64, 2e-5)]:
+        A = rand((300, n), dt, n + 1)
+        Yd = m.gsrft_apply(A, m.gsrft_operator(n, 40, 3))
+        Yo = O.gsrft_apply(A.astype(np.complex128), O.gsrft_operator(n, 40, 3))
+        assert np.abs(Yd - Yo).max() <= tol * np.abs(Yo).max()
+
+
 def test_csr_spmm_vs_scipy():
     import scipy.sparse as sp
     from paper_0909_4061_b200.sparse import CudaCsrOperator

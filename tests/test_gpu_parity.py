@@ -209,3 +209,41 @@ def test_cfg5_reduced(golden):
     op = lr().CudaCsrOperator(S, L, R, host_io=True)
     basis, f, est = lr().randomized_svd(op, c.k, c.p, c.q, c.seed)
     check_against_golden(g, f, basis, est, 1e-10, floor=1e-6)
+
+
+def test_adaptive_range_finder_vs_reference(golden):
+    """Alg 4.2 (reference rangefinder.py:89-166) on the device against the
+    reference's own runs: same basis size, probe draws and stopping point."""
+    g = golden("kats")
+    m = lr()
+    for blk, fn in ((1, m.adaptive_range_finder), (4, m.adaptive_range_finder)):
+        b = fn(g["ad_A"], 1e-3, r=10, seed=5, block=blk)
+        meta = g[f"ad{blk}_meta"]
+        assert b.Q.shape == g[f"ad{blk}_Q"].shape
+        assert np.abs(b.Q - g[f"ad{blk}_Q"]).max() <= 1e-9
+        assert [b.samples_used, b.passes, float(b.saturated), b.probe_matvecs] == \
+            [meta[0], meta[1], meta[3], meta[4]]
+        assert b.est_error == pytest.approx(meta[2], rel=1e-8)
+    b = m.adaptive_range_finder(g["ad_A"][:, :8], 1e-12, r=4, seed=2)
+    assert b.saturated and b.Q.shape == g["ad_sat_Q"].shape
+    assert np.abs(b.Q - g["ad_sat_Q"]).max() <= 1e-9
+    b = m.adaptive_range_finder_blocked(g["ad_A"], 1e-3, r=10, seed=5)
+    bo = __import__("oracle.lowrank_oracle", fromlist=["x"]).adaptive_range_finder(
+        g["ad_A"], 1e-3, r=10, seed=5, block=8)
+    assert b.Q.shape == bo.Q.shape and np.abs(b.Q - bo.Q).max() <= 1e-9
+    with pytest.raises(ValueError):
+        m.adaptive_range_finder(g["ad_A"], 0.0)
+
+
+def test_gsrft_randomized_svd_vs_oracle():
+    """randomized_svd with the Givens-chain sketch (the CLI's --sketch gsrft)."""
+    from oracle import lowrank_oracle as O
+    g = np.random.default_rng(3)
+    m_, n_ = 600, 512
+    U = np.linalg.qr(g.standard_normal((m_, 60)))[0]
+    V = np.linalg.qr(g.standard_normal((n_, 60)))[0]
+    A = (U * np.exp(-np.arange(60) / 6.0)) @ V.T
+    _, f, est = lr().randomized_svd(A, 20, 10, 0, 7, sketch="gsrft")
+    _, fo, esto = O.rsvd(A, 20, 10, 0, 7, sketch="gsrft")
+    assert np.max(np.abs(f.sigma - fo.sigma) / fo.sigma[0]) <= 1e-10
+    assert est == pytest.approx(esto, rel=1e-2)

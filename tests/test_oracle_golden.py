@@ -101,3 +101,34 @@ def test_cfg5_reduced_oracle_matches_reference(golden):
     assert np.all(np.abs(f.sigma - g["sigma"])[top] <= 1e-10 * g["sigma"][top])
     assert est == pytest.approx(g["est"][0], rel=1e-6)
     assert basis.passes == g["passes"][0]
+
+
+def test_gsrft_oracle_matches_reference(golden):
+    """Givens-chain SRFT (reference sketch.py:221-337): draws bitwise, the
+    apply (power-of-two and not) and the gsrft range finder."""
+    g = golden("kats")
+    d = O.gsrft_operator(16, 4, 2)
+    for f in ("d_outer", "perm_outer", "thetas_outer", "d_mid", "perm_inner", "thetas_inner",
+              "d_inner", "picks"):
+        assert np.array_equal(getattr(d, f), g[f"gsrft16_{f}"]), f
+    assert np.abs(O.gsrft_apply(g["gsrft_A"], d) - g["gsrft_Y"]).max() <= 1e-13
+    Y = O.gsrft_apply(g["gsrft12_A"], O.gsrft_operator(12, 5, 7))
+    assert np.abs(Y - g["gsrft12_Y"]).max() <= 1e-13
+    b = O.fast_range_finder(g["rf_A"][:, :16], 5, 4, kind="gsrft")
+    assert np.abs(b.Q - g["rf_gsrft_Q"]).max() <= 1e-12
+
+
+def test_adaptive_oracle_matches_reference(golden):
+    """Alg 4.2 fixed-precision finder (reference rangefinder.py:89-166)."""
+    g = golden("kats")
+    for blk in (1, 4):
+        b = O.adaptive_range_finder(g["ad_A"], 1e-3, r=10, seed=5, block=blk)
+        meta = g[f"ad{blk}_meta"]
+        assert b.Q.shape == g[f"ad{blk}_Q"].shape
+        assert np.abs(b.Q - g[f"ad{blk}_Q"]).max() <= 1e-12
+        assert [b.samples_used, b.passes, float(b.saturated), b.probe_matvecs] == \
+            [meta[0], meta[1], meta[3], meta[4]]
+        assert b.est_error == pytest.approx(meta[2], rel=1e-10)
+    b = O.adaptive_range_finder(g["ad_A"][:, :8], 1e-12, r=4, seed=2)
+    assert b.saturated and b.Q.shape == g["ad_sat_Q"].shape
+    assert np.abs(b.Q - g["ad_sat_Q"]).max() <= 1e-12
