@@ -72,91 +72,132 @@ __device__ __forceinline__ double next_double(uint64_t u) {
 
 // flags byte: bit7 yields a normal, bit6 continuation draw (set by pass B),
 // bits0-5 draws consumed by an attempt starting here (0x3f without bit7 = cap overflow)
-// pass A: one thread per Philox block (4 positions)
-__global__ void gauss_eval(PhiloxKey key, int64_t L, double* __restrict__ val,
-                           uint8_t* __restrict__ flags) {
+__device__ __forceinline__ bool is_special(uint8_t f) { return (f & 0x3f) != 1 || !(f & 0x80); }
+
+// pass A: one thread per Philox block (4 positions), a warp per 128
+// positions; besides value and flags it writes the bitmask of "special"
+// positions (one uint32 per 32 positions) that pass B scans.  The ziggurat
+// tables are indexed by random bytes: staged in shared memory (a __constant__
+// lookup with 32 different addresses per warp serializes 32-fold).
+__global__ void __launch_bounds__(256)
+gauss_eval(PhiloxKey key, int64_t L, double* __restrict__ val, uint8_t* __restrict__ flags,
+           uint32_t* __restrict__ smask) {
+  __shared__ uint64_t ki[256];
+  __shared__ double wi[256], fi[256];
+  ki[threadIdx.x] = kZigKi[threadIdx.x];
+  wi[threadIdx.x] = kZigWi[threadIdx.x];
+  fi[threadIdx.x] = kZigFi[threadIdx.x];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
   const int64_t blocks = (L + 3) >> 2;
-  for (int64_t b = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; b < blocks;
-       b += int64_t(gridDim.x) * blockDim.x) {
-    uint64_t o[4];
-    philox4x64_10(uint64_t(b) + 1, key, o);
+  const int64_t wstride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t bw = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) - lane; bw < blocks;
+       bw += wstride) {
+    const int64_t b = bw + lane;
+    uint32_t nib = 0;
+    if (b < blocks) {
+      uint64_t o[4];
+      philox4x64_10(uint64_t(b) + 1, key, o);
 #pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      const int64_t t = b * 4 + w;
-      if (t >= L) break;
-      const uint64_t u = o[w];
-      const int idx = int(u & 0xff);
-      const uint64_t r = u >> 8;
-      const uint64_t rabs = (r >> 1) & 0x000fffffffffffffULL;
-      double x = double(rabs) * kZigWi[idx];
-      if (r & 1) x = -x;
-      uint8_t f;
-      if (rabs < kZigKi[idx]) {
-        f = 0x80 | 1;
-      } else if (idx != 0) {
-        const double nd = next_double(raw_at(key, t + 1));
-        const bool yes = ((kZigFi[idx - 1] - kZigFi[idx]) * nd + kZigFi[idx]) < exp(-0.5 * x * x);
-        f = uint8_t((yes ? 0x80 : 0) | 2);
-      } else {
-        int64_t j = t + 1;
-        int used = 1;
-        f = 0x3f;   // overflow marker (c = 63, no yield) unless accepted within the cap
-        while (used + 2 < MAXC) {
-          const double xx = -ZIG_INV_R * log1p(-next_double(raw_at(key, j)));
-          const double yy = -log1p(-next_double(raw_at(key, j + 1)));
-          j += 2;
-          used += 2;
-          if (yy + yy > xx * xx) {
-            x = ((rabs >> 8) & 1) ? -(ZIG_R + xx) : ZIG_R + xx;
-            f = uint8_t(0x80 | used);
-            break;
+      for (int w = 0; w < 4; ++w) {
+        const int64_t t = b * 4 + w;
+        if (t >= L) break;
+        const uint64_t u = o[w];
+        const int idx = int(u & 0xff);
+        const uint64_t r = u >> 8;
+        const uint64_t rabs = (r >> 1) & 0x000fffffffffffffULL;
+        double x = double(rabs) * wi[idx];
+        if (r & 1) x = -x;
+        uint8_t f;
+        if (rabs < ki[idx]) {
+          f = 0x80 | 1;
+        } else if (idx != 0) {
+          const double nd = next_double(raw_at(key, t + 1));
+          const bool yes = ((fi[idx - 1] - fi[idx]) * nd + fi[idx]) < exp(-0.5 * x * x);
+          f = uint8_t((yes ? 0x80 : 0) | 2);
+        } else {
+          int64_t j = t + 1;
+          int used = 1;
+          f = 0x3f;   // overflow marker (c = 63, no yield) unless accepted within the cap
+          while (used + 2 < MAXC) {
+            const double xx = -ZIG_INV_R * log1p(-next_double(raw_at(key, j)));
+            const double yy = -log1p(-next_double(raw_at(key, j + 1)));
+            j += 2;
+            used += 2;
+            if (yy + yy > xx * xx) {
+              x = ((rabs >> 8) & 1) ? -(ZIG_R + xx) : ZIG_R + xx;
+              f = uint8_t(0x80 | used);
+              break;
+            }
           }
         }
+        val[t] = x;
+        flags[t] = f;
+        if (is_special(f)) nib |= 1u << w;
       }
-      val[t] = x;
-      flags[t] = f;
     }
+    // lanes 8k..8k+7 hold positions 32k..32k+31 of this warp's 128
+    uint32_t word = nib << (4 * (lane & 7));
+    word |= __shfl_xor_sync(0xffffffffu, word, 1);
+    word |= __shfl_xor_sync(0xffffffffu, word, 2);
+    word |= __shfl_xor_sync(0xffffffffu, word, 4);
+    const int64_t wi32 = (bw >> 3) + (lane >> 3);   // (bw * 4) / 32 + k
+    if ((lane & 7) == 0 && wi32 * 32 < L) smask[wi32] = word;
   }
 }
 
-// pass B: mark continuation draws (bit6 of flags) by walking from each head
-__global__ void gauss_fixup(int64_t L, uint8_t* __restrict__ flags, int32_t* status) {
-  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < L;
-       t += int64_t(gridDim.x) * blockDim.x) {
-    const uint8_t f = flags[t];
-    const bool special = (f & 0x3f) != 1 || !(f & 0x80);
-    if (!special) continue;
-    bool head = true;
-    for (int64_t s = t - 1; s >= 0 && s > t - MAXC; --s) {
-      const uint8_t g = flags[s];
-      if ((g & 0x3f) != 1 || !(g & 0x80)) { head = false; break; }
+__device__ __forceinline__ uint32_t mask_word(const uint32_t* smask, int64_t k, int64_t W) {
+  return (k >= 0 && k < W) ? smask[k] : 0u;
+}
+
+// first special position in [p, min(p + 64, L)), or -1
+__device__ __forceinline__ int64_t next_special(const uint32_t* smask, int64_t W, int64_t L,
+                                                int64_t p) {
+  const int64_t end = min(p + MAXC, L);
+  for (int64_t q = p; q < end;) {
+    const int64_t k = q >> 5;
+    const uint32_t m = mask_word(smask, k, W) >> (q & 31);
+    if (m) {
+      const int64_t r = q + __ffs(m) - 1;
+      return r < end ? r : -1;
     }
-    if (!head) continue;
-    // walk the cluster: p is always an attempt start here
-    int64_t p = t;
-    for (;;) {
-      const uint8_t g = flags[p];
-      const int c = g & 0x3f;
-      if (c == 0x3f && !(g & 0x80)) {   // cap exceeded
-        if (status) atomicOr(status, 16);
-        break;
+    q = (k + 1) << 5;
+  }
+  return -1;
+}
+
+// pass B: mark continuation draws (bit6 of flags) by walking from each head.
+// One thread per 32 positions; a special position is a head iff the 63
+// positions before it hold no special (read off the bitmask, not the bytes).
+__global__ void gauss_fixup(int64_t L, uint8_t* __restrict__ flags,
+                            const uint32_t* __restrict__ smask, int32_t* status) {
+  const int64_t W = (L + 31) >> 5;
+  for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < W;
+       k += int64_t(gridDim.x) * blockDim.x) {
+    uint32_t m = smask[k];
+    if (!m) continue;
+    const uint64_t lo = (uint64_t(mask_word(smask, k - 1, W)) << 32) | mask_word(smask, k - 2, W);
+    while (m) {
+      const int i = __ffs(m) - 1;
+      m &= m - 1;
+      // bits of positions t-63 .. t-1 (t = 32k + i at bit 64 + i of m:lo)
+      const uint64_t win =
+          ((lo >> (i + 1)) | (uint64_t(smask[k]) << (63 - i))) & 0x7fffffffffffffffULL;
+      if (win) continue;
+      int64_t p = k * 32 + i;
+      for (;;) {   // walk the cluster: p is always an attempt start here
+        const uint8_t g = flags[p];
+        const int c = g & 0x3f;
+        if (c == 0x3f && !(g & 0x80)) {   // cap exceeded
+          if (status) atomicOr(status, 16);
+          break;
+        }
+        for (int j = 1; j < c && p + j < L; ++j) flags[p + j] |= 0x40;
+        p += c;
+        if (p >= L) break;
+        p = next_special(smask, W, L, p);   // fast starts in between
+        if (p < 0) break;
       }
-      for (int k = 1; k < c && p + k < L; ++k) flags[p + k] |= 0x40;
-      p += c;
-      // stop once no special lies within reach of the next start
-      bool more = false;
-      for (int64_t q = p; q < L && q < p + MAXC; ++q) {
-        const uint8_t h = flags[q];
-        if ((h & 0x3f) != 1 || !(h & 0x80)) { more = true; break; }
-      }
-      if (!more || p >= L) break;
-      // advance over fast starts to the next special
-      while (p < L) {
-        const uint8_t h = flags[p];
-        if ((h & 0x3f) != 1 || !(h & 0x80)) break;
-        ++p;
-      }
-      if (p >= L) break;
     }
   }
 }
@@ -264,12 +305,13 @@ void gaussian_stream(Handle* h, uint64_t key_lo, uint64_t key_hi, int64_t count,
   const int64_t nb = ceil_div(L, SCAN_B);
   int32_t* bsum = pool_alloc_t<int32_t>(h, size_t(nb));
   int64_t* boff = pool_alloc_t<int64_t>(h, size_t(nb));
+  uint32_t* smask = pool_alloc_t<uint32_t>(h, size_t((L + 31) / 32));
   PhiloxKey key{key_lo, key_hi};
   const int grid = int(std::min<int64_t>(ceil_div(ceil_div(L, 4), 256), int64_t(h->sm_count) * 32));
-  gauss_eval<<<grid, 256, 0, h->stream>>>(key, L, val, flags);
+  gauss_eval<<<grid, 256, 0, h->stream>>>(key, L, val, flags, smask);
   LR_CHECK_LAUNCH();
-  const int grid2 = int(std::min<int64_t>(ceil_div(L, 256), int64_t(h->sm_count) * 32));
-  gauss_fixup<<<grid2, 256, 0, h->stream>>>(L, flags, h->status);
+  const int grid2 = int(std::min<int64_t>(ceil_div(ceil_div(L, 32), 256), int64_t(h->sm_count) * 8));
+  gauss_fixup<<<grid2, 256, 0, h->stream>>>(L, flags, smask, h->status);
   LR_CHECK_LAUNCH();
   gauss_count<<<unsigned(nb), SCAN_T, 0, h->stream>>>(L, flags, bsum);
   LR_CHECK_LAUNCH();
