@@ -280,6 +280,11 @@ bool chol_blocked_launch(Handle* h, int64_t ell, const T* G, double drop_tol, do
 void chol_drop_f64(Handle* h, int64_t ell, const double* G, double drop_tol, double unres_rel,
                    double shift_coef, double* P, double* R, int32_t* info) {
   LR_REQUIRE(ell >= 1 && ell <= 4096, LR_EINVAL, "chol_drop: ell out of range [1, 4096]");
+  if (chol_panel_supported(ell, false)) {
+    chol_panel_f64(h, ell, G, ell, drop_tol, unres_rel, shift_coef, P, R, info, nullptr, nullptr,
+                   0, true);
+    return;
+  }
   if (chol_tiled_supported(ell, false)) {
     chol_tiled_f64(h, ell, G, drop_tol, unres_rel, shift_coef, P, R, info);
     return;
@@ -295,6 +300,11 @@ void chol_drop_c128(Handle* h, int64_t ell, const double2* G, double drop_tol,
                     double unres_rel, double shift_coef, double2* P, double2* R,
                     int32_t* info) {
   LR_REQUIRE(ell >= 1 && ell <= 4096, LR_EINVAL, "chol_drop: ell out of range [1, 4096]");
+  if (chol_panel_supported(ell, true)) {
+    chol_panel_c128(h, ell, G, ell, drop_tol, unres_rel, shift_coef, P, R, info, nullptr,
+                    nullptr, 0, true);
+    return;
+  }
   if (chol_tiled_supported(ell, true)) {
     chol_tiled_c128(h, ell, G, drop_tol, unres_rel, shift_coef, P, R, info);
     return;

@@ -1,0 +1,484 @@
+// K3 core, panel-blocked variant (default for ell <= 200 real / 140 complex):
+// Cholesky with column deletion of a Gram matrix + the inverse of the kept
+// triangle, same contract and arithmetic decisions as chol_drop_kernel
+// (chol.cu) -- the rank decision of orthonormalize_double_gs, reference
+// core.py:84-115.
+//
+// The unblocked kernels pay one CTA barrier AND a rank-1 update of the whole
+// trailing matrix per column (chol_tiled: ~2500 cycles per column, issue
+// bound).  Here the factorization is right-looking over panels of NB = 16
+// rows, the packed upper triangle resident in shared memory:
+//   (a) one warp factors the 16 x 16 diagonal block (warp barriers only),
+//   (b) every thread forward-substitutes one column of the panel rows
+//       (R12 = R11^{-H} G12),
+//   (c) the trailing matrix takes one rank-16 update, register-blocked
+//       micro-tiles (4 x 4 real, 2 x 4 complex).
+// Three CTA barriers per panel instead of sixteen.  The inverse X = R~^{-1}
+// (R~: dropped rows/cols replaced by the identity) is formed in place by
+// blocks: every warp inverts diagonal blocks, then block column J is
+// X[:J, J] = -X[:J, :J] (R[:J, J] X_JJ), two barriers per block column.
+//
+// Pivot decisions are those of the unblocked algorithm: pivot j is the
+// Schur complement G_jj - sum_{i<j kept} |r_ij|^2, compared with
+// drop_tol^2 trace(G) (drop) and unres_rel * G_jj (unresolved); a dropped
+// pivot leaves a zero row of R and takes no part in later updates.
+#include <cstdio>
+#include <cstdlib>
+
+#include "common.cuh"
+#include "scalar.cuh"
+
+namespace lr {
+namespace {
+
+constexpr int NB = 16;     // panel width
+constexpr int NT = 512;    // threads per CTA
+constexpr int NW = NT / 32;
+
+// fp64 1/sqrt: MUFU seed + ITER Newton steps (2 give full precision)
+template <int ITER>
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+#pragma unroll
+  for (int i = 0; i < ITER; ++i) y = y * fma(-0.5 * x, y * y, 1.5);
+  return y;
+}
+
+template <int ITER>
+__device__ __forceinline__ double rcp_nr(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+#pragma unroll
+  for (int i = 0; i < ITER; ++i) y = y * fma(-x, y, 2.0);
+  return y;
+}
+
+template <typename T>
+constexpr int panel_maxn() { return sizeof(T) == 8 ? 200 : 140; }
+
+// packed upper triangle: row i holds columns i..n-1
+__device__ __forceinline__ int poff(int n, int i) { return i * n - (i * (i - 1)) / 2; }
+
+template <typename T>
+__host__ __device__ constexpr int tile_i() { return sizeof(T) == 8 ? 4 : 2; }
+constexpr int TK = 4;
+
+template <typename T>
+size_t panel_smem_bytes(int n) {
+  return size_t(n) * (n + 1) / 2 * sizeof(T)       // W
+         + size_t(n) * NB * sizeof(T)              // T buffer (inverse)
+         + size_t(n) * 4 * sizeof(double)          // d0, rd, ri, rti
+         + size_t(n) * 2 * sizeof(int) + 64;       // pos, kidx
+}
+
+template <typename T>
+__global__ void __launch_bounds__(NT, 1)
+chol_panel_kernel(int n, const T* __restrict__ G, int64_t ldg, double drop_tol, double unres_rel,
+                  double shift_coef, T* __restrict__ P, T* __restrict__ Rout,
+                  int32_t* __restrict__ info, int32_t* status, const double* __restrict__ trace_dev,
+                  const T* __restrict__ diag_src, int64_t diag_stride, bool compact,
+                  const int32_t* __restrict__ gate, long long* prof) {
+  if (gate && *gate == 0) return;
+  using S = Sc<T>;
+  int np = 0;   // LR_CHOL_PROF: phase timestamps of thread 0
+#define PROF_MARK() \
+  do { if (prof && threadIdx.x == 0 && np < 64) prof[np++] = clock64(); } while (0)
+  PROF_MARK();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* W = reinterpret_cast<T*>(smem_raw);
+  T* Tb = W + size_t(n) * (n + 1) / 2;
+  double* d0 = reinterpret_cast<double*>(Tb + size_t(n) * NB);
+  double* rd = d0 + n;
+  double* ri = rd + n;
+  double* rti = ri + n;
+  int* pos = reinterpret_cast<int*>(rti + n);
+  int* kidx = pos + n;
+  __shared__ double s_trace;
+  __shared__ int s_unres, s_bad, s_rank;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  auto at = [&](int i, int k) -> T& { return W[poff(n, i) + (k - i)]; };
+
+  // ---- load the upper triangle, trace, shift ----
+  if (warp == 0) {
+    double tr = 0.0;
+    if (!trace_dev)
+      for (int i = lane; i < n; i += 32) tr += S::re(G[size_t(i) * ldg + i]);
+#pragma unroll
+    for (int m = 16; m > 0; m >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, m);
+    if (lane == 0) { s_trace = trace_dev ? *trace_dev : tr; s_unres = 0; s_bad = 0; }
+  }
+  __syncthreads();
+  const double trace = s_trace;
+  const double thr2 = drop_tol * drop_tol * trace;
+  const double shift = shift_coef * trace;
+  // elements of the upper triangle, several loads in flight per thread
+  for (int e0 = tid; e0 < n * n; e0 += 4 * NT) {
+    T v[4];
+    int ii[4], kk[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = e0 + u * NT;
+      ii[u] = e / n;
+      kk[u] = e - ii[u] * n;
+      v[u] = (e < n * n && kk[u] >= ii[u]) ? G[size_t(ii[u]) * ldg + kk[u]] : S::zero();
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = ii[u], k = kk[u];
+      if (e0 + u * NT < n * n && k >= i) {
+        T x = v[u];
+        if (k == i) {
+          x = S::make(S::re(x) + shift, 0.0);
+          d0[i] = diag_src ? S::re(diag_src[size_t(i) * diag_stride]) + shift : S::re(x);
+        }
+        W[poff(n, i) + (k - i)] = x;
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- right-looking panel factorization ----
+  int my_unres = 0, my_bad = 0;   // warp 0, lane 0
+  for (int j0 = 0; j0 < n; j0 += NB) {
+    const int nb = min(NB, n - j0), j1 = j0 + nb;
+    // (a) diagonal block, one warp, in registers: lane l holds column
+    // b = l & 15 of rows 8h..8h+7 (h = l >> 4).  Step s broadcasts the pivot
+    // row with shuffles; updates use the unscaled pivot row times 1/d.
+    if (warp == 0) {
+      const int b = lane & 15, h = lane >> 4;
+      T w[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const int a = 8 * h + r;
+        w[r] = (a < nb && b < nb && b >= a) ? at(j0 + a, j0 + b) : S::zero();
+      }
+      PROF_MARK();
+      double myd = 0.0;   // lane s keeps pivot s (no branches in the chain)
+#pragma unroll 1
+      for (int hs = 0; hs < 2; ++hs) {        // pivot rows 8 hs .. 8 hs + 7
+        const int src = 16 * hs;
+#pragma unroll
+        for (int s2 = 0; s2 < 8; ++s2) {
+          const int s = 8 * hs + s2;   // s >= nb: zero pivot row, no update
+          {
+            const T ps = S::shfl_idx(w[s2], src + b);              // W(s, b)
+            const double d = S::re(S::shfl_idx(w[s2], src + s));   // W(s, s)
+            T t[8];
+#pragma unroll
+            for (int r = 0; r < 8; ++r)   // conj(W(s, a)) W(s, b), off the 1/d chain
+              t[r] = S::mul(S::conj(S::shfl_idx(w[s2], src + 8 * h + r)), ps);
+            const bool keep = isfinite(d) && d > thr2 && d > 0.0;
+            const double invd = keep ? 1.0 / d : 0.0;
+            myd = (lane == s) ? d : myd;
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+              const int a = 8 * h + r;
+              if (a > s && b >= a) w[r] = S::sub(w[r], S::scale(t[r], invd));
+            }
+          }
+        }
+      }
+      if (lane < nb) {
+        const int j = j0 + lane;
+        const bool fin = isfinite(myd);
+        const bool keep = fin && myd > thr2 && myd > 0.0;
+        const double r = keep ? sqrt(myd) : 0.0;
+        rd[j] = r;
+        ri[j] = keep ? 1.0 / r : 0.0;
+        const unsigned msk = (1u << nb) - 1u;   // lanes 0 .. nb-1 (nb <= 16)
+        const unsigned un = __ballot_sync(msk, keep && myd <= unres_rel * d0[j]);
+        const unsigned bd = __ballot_sync(msk, !fin);
+        if (lane == 0) { my_unres += __popc(un); my_bad += __popc(bd); }
+      }
+      __syncwarp();
+      PROF_MARK();
+      // R rows of the block: R_ab = W_ab / R_aa (zero row for a dropped pivot)
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const int a = 8 * h + r;
+        if (a < nb && b < nb && b >= a)
+          at(j0 + a, j0 + b) = (b == a) ? S::make(rd[j0 + a], 0.0) : S::scale(w[r], ri[j0 + a]);
+      }
+    }
+    __syncthreads();
+    PROF_MARK();
+    if (j1 >= n) break;
+    // (b) panel rows right of the block: R12 = R11^{-H} G12, one column per thread
+    for (int k = j1 + tid; k < n; k += NT) {
+      T x[NB];
+#pragma unroll
+      for (int u = 0; u < NB; ++u) x[u] = u < nb ? at(j0 + u, k) : S::zero();
+#pragma unroll
+      for (int s = 0; s < NB; ++s) {
+        if (s < nb) {
+          const T xs = S::scale(x[s], ri[j0 + s]);
+          x[s] = xs;
+#pragma unroll
+          for (int u = s + 1; u < NB; ++u)
+            if (u < nb) x[u] = S::sub(x[u], S::mul(S::conj(at(j0 + s, j0 + u)), xs));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < NB; ++u)
+        if (u < nb) at(j0 + u, k) = x[u];
+    }
+    __syncthreads();
+    PROF_MARK();
+    // (c) trailing update W(i, k) -= sum_s conj(R(s, i)) R(s, k), j1 <= i <= k.
+    // Warp tiles of (4 TI) x 32: lane (ly, lx) = (lane >> 3, lane & 7) owns
+    // rows ly + 4a and columns lx + 8b -- the row loads are 8 consecutive
+    // elements (one wavefront), the column loads 4 broadcasts.
+    {
+      constexpr int TI = tile_i<T>();
+      const int m = n - j1;
+      const int wr = 4 * TI;                  // rows per warp tile
+      const int nti = (m + wr - 1) / wr, ntk = (m + 31) / 32;
+      const int ly = lane >> 3, lx = lane & 7;
+      for (int e = warp; e < nti * ntk; e += NW) {
+        const int ti = e / ntk, tk = e - ti * ntk;
+        const int i0 = j1 + ti * wr, k0 = j1 + tk * 32;
+        if (k0 + 31 < i0) continue;           // entirely below the diagonal
+        T acc[TI][4];
+#pragma unroll
+        for (int a = 0; a < TI; ++a)
+#pragma unroll
+          for (int bb = 0; bb < 4; ++bb) acc[a][bb] = S::zero();
+        const T* row = W + poff(n, j0) - j0;  // row[c] = R(r, c), c >= r
+        for (int s = 0; s < nb; ++s) {
+          T av[TI], bv[4];
+#pragma unroll
+          for (int a = 0; a < TI; ++a) {
+            const int i = i0 + ly + 4 * a;
+            av[a] = i < n ? S::conj(row[i]) : S::zero();
+          }
+#pragma unroll
+          for (int bb = 0; bb < 4; ++bb) {
+            const int k = k0 + lx + 8 * bb;
+            bv[bb] = k < n ? row[k] : S::zero();
+          }
+#pragma unroll
+          for (int a = 0; a < TI; ++a)
+#pragma unroll
+            for (int bb = 0; bb < 4; ++bb) acc[a][bb] = S::add(acc[a][bb], S::mul(av[a], bv[bb]));
+          row += n - (j0 + s) - 1;            // next row: poff(r + 1) - (r + 1)
+        }
+#pragma unroll
+        for (int a = 0; a < TI; ++a) {
+          const int i = i0 + ly + 4 * a;
+          if (i < n) {
+            T* rowi = W + poff(n, i) - i;
+#pragma unroll
+            for (int bb = 0; bb < 4; ++bb) {
+              const int k = k0 + lx + 8 * bb;
+              if (k < n && k >= i) rowi[k] = S::sub(rowi[k], acc[a][bb]);
+            }
+          }
+        }
+      }
+    }
+    PROF_MARK();
+    __syncthreads();
+  }
+
+  PROF_MARK();
+  // ---- compaction of the kept pivots ----
+  if (warp == 0) {
+    if (lane == 0) { s_unres = my_unres; s_bad = my_bad; }
+    int base = 0;
+    for (int jj = 0; jj < n; jj += 32) {
+      const int j = jj + lane;
+      const bool k = j < n && rd[j] > 0.0;
+      const unsigned bal = __ballot_sync(0xffffffffu, k);
+      const int p = base + __popc(bal & ((1u << lane) - 1u));
+      if (j < n) {
+        pos[j] = k ? p : -1;
+        if (k) kidx[p] = j;
+        rti[j] = k ? ri[j] : 1.0;
+      }
+      base += __popc(bal);
+    }
+    if (lane == 0) s_rank = base;
+  }
+  __syncthreads();
+  const int rank = s_rank;
+
+  // ---- R output (kept rows/cols), then R~ in place ----
+  for (int i = warp; i < n; i += NW) {
+    const T* rowi = W + poff(n, i) - i;
+    const bool ki = pos[i] >= 0;
+    for (int k = lane; k < n; k += 32)
+      Rout[size_t(i) * n + k] = (k >= i && ki && pos[k] >= 0) ? rowi[k] : S::zero();
+  }
+  __syncthreads();
+  if (rank < n) {
+    for (int i = warp; i < n; i += NW) {
+      T* rowi = W + poff(n, i) - i;
+      for (int k = i + lane; k < n; k += 32)   // column k dropped: identity column
+        if (pos[k] < 0) rowi[k] = (i == k) ? S::one() : S::zero();
+    }
+    __syncthreads();
+  }
+  PROF_MARK();
+
+  // ---- X = R~^{-1} in place: diagonal blocks (one warp each) ----
+  const int nbk = (n + NB - 1) / NB;
+  for (int J = warp; J < nbk; J += NW) {
+    const int j0 = J * NB, nb = min(NB, n - j0);
+    const int c = lane;
+    T x[NB];
+#pragma unroll
+    for (int i = 0; i < NB; ++i) x[i] = (i == c) ? S::one() : S::zero();
+#pragma unroll
+    for (int k = NB - 1; k >= 0; --k) {
+      if (k <= c && c < nb) {
+        const T xk = S::scale(x[k], rti[j0 + k]);
+        x[k] = xk;
+#pragma unroll
+        for (int i = 0; i < k; ++i) x[i] = S::sub(x[i], S::mul(at(j0 + i, j0 + k), xk));
+      }
+    }
+    __syncwarp();
+    if (c < nb) {
+#pragma unroll
+      for (int i = 0; i < NB; ++i)
+        if (i <= c) at(j0 + i, j0 + c) = x[i];
+    }
+  }
+  __syncthreads();
+  PROF_MARK();
+  // ---- block columns: X[:j0, J] = -X[:j0, :j0] (R[:j0, J] X_JJ) ----
+  // lane = (half, c): column c of the block, rows i0 + half + 2a; the block
+  // row loads are 16 consecutive elements, the row-i loads broadcasts.
+  {
+    constexpr int RA = sizeof(T) == 8 ? 4 : 2;   // rows per thread
+    constexpr int WROWS = 2 * RA;                // rows per warp chunk
+    const int c = lane & 15, half = lane >> 4;
+    for (int J = 1; J < nbk; ++J) {
+      const int j0 = J * NB, nb = min(NB, n - j0);
+      const T* bJ = W;                           // rows of X_JJ: poff(j0 + k) - j0
+      for (int ib = warp * WROWS; ib < j0; ib += NW * WROWS) {
+        T acc[RA];
+#pragma unroll
+        for (int a = 0; a < RA; ++a) acc[a] = S::zero();
+        for (int k = 0; k < nb; ++k) {
+          const T* rowk = bJ + poff(n, j0 + k) - (j0 + k);
+          const T xk = (k <= c && c < nb) ? rowk[j0 + c] : S::zero();
+#pragma unroll
+          for (int a = 0; a < RA; ++a) {
+            const int i = ib + half + 2 * a;
+            if (i < j0) acc[a] = S::add(acc[a], S::mul(at(i, j0 + k), xk));
+          }
+        }
+#pragma unroll
+        for (int a = 0; a < RA; ++a) {
+          const int i = ib + half + 2 * a;
+          if (i < j0) Tb[i * NB + c] = acc[a];
+        }
+      }
+      __syncthreads();
+      for (int ib = warp * WROWS; ib < j0; ib += NW * WROWS) {
+        T acc[RA];
+#pragma unroll
+        for (int a = 0; a < RA; ++a) acc[a] = S::zero();
+        for (int k = ib; k < j0; ++k) {
+          const T tk = Tb[k * NB + c];
+#pragma unroll
+          for (int a = 0; a < RA; ++a) {
+            const int i = ib + half + 2 * a;
+            if (k >= i && i < j0) acc[a] = S::add(acc[a], S::mul(at(i, k), tk));
+          }
+        }
+#pragma unroll
+        for (int a = 0; a < RA; ++a) {
+          const int i = ib + half + 2 * a;
+          if (i < j0 && c < nb) at(i, j0 + c) = S::scale(acc[a], -1.0);
+        }
+      }
+      __syncthreads();
+    }
+  }
+
+  PROF_MARK();
+  // ---- P: kept columns (compacted or in place), zero elsewhere ----
+  for (int i = warp; i < n; i += NW) {
+    const T* rowi = W + poff(n, i) - i;
+    const bool ki = pos[i] >= 0;
+    for (int q = lane; q < n; q += 32) {
+      const int c = compact ? (q < rank ? kidx[q] : -1) : (pos[q] >= 0 ? q : -1);
+      P[size_t(i) * n + q] = (ki && c >= i) ? rowi[c] : S::zero();
+    }
+  }
+  __syncthreads();
+  PROF_MARK();
+  if (prof && tid == 0) prof[63] = np;
+#undef PROF_MARK
+  if (tid == 0) {
+    info[0] = rank;
+    info[1] = s_unres;
+    info[2] = s_bad;
+    if (status) {
+      const int bits = (s_unres ? 1 : 0) | (rank < n ? 2 : 0) | (s_bad ? 4 : 0);
+      if (bits) atomicOr(status, bits);
+    }
+  }
+}
+
+template <typename T>
+void launch_panel(Handle* h, int n, const T* G, int64_t ldg, double drop_tol, double unres_rel,
+                  double shift_coef, T* P, T* R, int32_t* info, const double* trace_dev,
+                  const T* diag_src, int64_t diag_stride, bool compact) {
+  const size_t smem = panel_smem_bytes<T>(n);
+  auto kern = chol_panel_kernel<T>;
+  LR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  static int prof_on = -1;
+  if (prof_on < 0) prof_on = getenv("LR_CHOL_PROF") ? 1 : 0;
+  long long* prof = prof_on ? pool_alloc_t<long long>(h, 64) : nullptr;
+  kern<<<1, NT, smem, h->stream>>>(n, G, ldg, drop_tol, unres_rel, shift_coef, P, R, info,
+                                   h->status, trace_dev, diag_src, diag_stride, compact, h->gate,
+                                   prof);
+  LR_CHECK_LAUNCH();
+  if (prof) {   // development only: synchronizes
+    long long hp[64];
+    LR_CUDA(cudaMemcpyAsync(hp, prof, sizeof(hp), cudaMemcpyDeviceToHost, h->stream));
+    LR_CUDA(cudaStreamSynchronize(h->stream));
+    fprintf(stderr, "[lr] chol_panel n=%d cycles:", n);
+    for (int i = 1; i < int(hp[63]); ++i) fprintf(stderr, " %lld", hp[i] - hp[i - 1]);
+    fprintf(stderr, " | total %lld\n", hp[int(hp[63]) - 1] - hp[0]);
+  }
+}
+
+}  // namespace
+
+// LR_CHOL=panel (default) | tiled | smem selects the Cholesky kernel family
+int chol_mode() {
+  static int mode = -1;
+  if (mode < 0) {
+    const char* e = getenv("LR_CHOL");
+    mode = !e ? 0 : (e[0] == 's' ? 1 : e[0] == 't' ? 2 : 0);
+  }
+  return mode;
+}
+
+bool chol_panel_supported(int64_t n, bool cplx) {
+  return chol_mode() == 0 && n >= 1 && n <= (cplx ? panel_maxn<double2>() : panel_maxn<double>());
+}
+
+void chol_panel_f64(Handle* h, int64_t n, const double* G, int64_t ldg, double drop_tol,
+                    double unres_rel, double shift_coef, double* P, double* R, int32_t* info,
+                    const double* trace_dev, const double* diag_src, int64_t diag_stride,
+                    bool compact) {
+  launch_panel<double>(h, int(n), G, ldg, drop_tol, unres_rel, shift_coef, P, R, info,
+                       trace_dev, diag_src, diag_stride, compact);
+}
+
+void chol_panel_c128(Handle* h, int64_t n, const double2* G, int64_t ldg, double drop_tol,
+                     double unres_rel, double shift_coef, double2* P, double2* R, int32_t* info,
+                     const double* trace_dev, const double2* diag_src, int64_t diag_stride,
+                     bool compact) {
+  launch_panel<double2>(h, int(n), G, ldg, drop_tol, unres_rel, shift_coef, P, R, info,
+                        trace_dev, diag_src, diag_stride, compact);
+}
+
+}  // namespace lr

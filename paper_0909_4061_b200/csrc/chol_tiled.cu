@@ -363,6 +363,24 @@ __global__ void assemble_kernel(int n, int n1, const T* __restrict__ X11, const 
   }
 }
 
+// the 2 x 2 driver's block factorizations: the panel kernel when selected
+template <typename T>
+void block_chol(Handle* h, int n, const T* G, int64_t ldg, double drop_tol, double unres_rel,
+                double shift_coef, T* P, T* R, int32_t* info, const double* trace_dev,
+                const T* diag_src, int64_t diag_stride) {
+  if (chol_mode() == 0) {
+    if constexpr (sizeof(T) == 8)
+      chol_panel_f64(h, n, G, ldg, drop_tol, unres_rel, shift_coef, P, R, info, trace_dev,
+                     diag_src, diag_stride, false);
+    else
+      chol_panel_c128(h, n, G, ldg, drop_tol, unres_rel, shift_coef, P, R, info, trace_dev,
+                      diag_src, diag_stride, false);
+    return;
+  }
+  launch<T>(h, n, G, ldg, drop_tol, unres_rel, shift_coef, P, R, info, trace_dev, diag_src,
+            diag_stride, false);
+}
+
 template <typename T>
 void chol_blocked(Handle* h, int dtype, int n, const T* G, double drop_tol, double unres_rel,
                   double shift_coef, T* P, T* R, int32_t* info) {
@@ -380,15 +398,15 @@ void chol_blocked(Handle* h, int dtype, int n, const T* G, double drop_tol, doub
   T* X12 = pool_alloc_t<T>(h, size_t(n1) * n2);
   trace_kernel<T><<<1, 256, 0, h->stream>>>(n, G, tr);
   LR_CHECK_LAUNCH();
-  launch<T>(h, n1, G, n, drop_tol, unres_rel, shift_coef, X11, R11, inf, tr, nullptr, 0, false);
+  block_chol<T>(h, n1, G, n, drop_tol, unres_rel, shift_coef, X11, R11, inf, tr, nullptr, 0);
   // R12 = X11^H G12
   gemm_any(h, dtype, true, true, n1, n2, n1, X11, n1, G + n1, n, R12, n2);
   // S = G22 - R12^H R12
   gemm_any(h, dtype, true, true, n2, n2, n1, R12, n2, R12, n2, Tm, n2);
   schur_kernel<T><<<64, 256, 0, h->stream>>>(n2, G + size_t(n1) * n + n1, n, Tm, Sm);
   LR_CHECK_LAUNCH();
-  launch<T>(h, n2, Sm, n2, drop_tol, unres_rel, shift_coef, X22, R22, inf + 4, tr,
-            G + size_t(n1) * n + n1, n + 1, false);
+  block_chol<T>(h, n2, Sm, n2, drop_tol, unres_rel, shift_coef, X22, R22, inf + 4, tr,
+                G + size_t(n1) * n + n1, n + 1);
   mask_cols_kernel<T><<<64, 256, 0, h->stream>>>(n1, n2, R12, R22);
   LR_CHECK_LAUNCH();
   // X12 = -(X11 R12) X22 (sign applied in the assembly)
@@ -473,7 +491,7 @@ void chol_near_identity(Handle* h, int dtype, int64_t n, const void* G, double d
     const char* e = getenv("LR_CHOL_NEARID");
     mode = (e && e[0] == '0') ? 0 : 1;
   }
-  if (!mode || n > MAXN) {   // exact (the blocked path is not gated)
+  if (!mode || (n > MAXN && !chol_panel_supported(n, cplx))) {   // exact (blocked: not gated)
     if (cplx) chol_drop_c128(h, n, static_cast<const double2*>(G), drop_tol, unres_rel, 0.0,
                              static_cast<double2*>(P), static_cast<double2*>(R), info);
     else chol_drop_f64(h, n, static_cast<const double*>(G), drop_tol, unres_rel, 0.0,
@@ -509,11 +527,7 @@ void chol_near_identity(Handle* h, int dtype, int64_t n, const void* G, double d
 // 128) and for complex above 64 (336 vs 443 us at 120); below that the
 // 1024-thread shared-memory kernel is faster.
 bool chol_tiled_supported(int64_t n, bool cplx) {
-  static int mode = -1;
-  if (mode < 0) {
-    const char* e = getenv("LR_CHOL");   // smem | tiled | (unset: by size)
-    mode = !e ? 0 : (e[0] == 's' ? 1 : 2);
-  }
+  const int mode = chol_mode();   // LR_CHOL: panel (default) | tiled | smem
   if (n < 1 || n > MAXN || mode == 1) return false;
   return mode == 2 || n >= (cplx ? 65 : 80);
 }

@@ -167,6 +167,17 @@ void jacobi_svd_c128(Handle* h, int64_t rows, int64_t n, const double2* M, doubl
 // chol_tiled.cu: register-tiled Cholesky with deletion for ell <= 128
 // (by size; LR_CHOL=smem|tiled forces one kernel)
 bool chol_tiled_supported(int64_t n, bool cplx);
+// chol_panel.cu: panel-blocked Cholesky with deletion (default, ell <= 200 / 140)
+int chol_mode();
+bool chol_panel_supported(int64_t n, bool cplx);
+void chol_panel_f64(Handle* h, int64_t n, const double* G, int64_t ldg, double drop_tol,
+                    double unres_rel, double shift_coef, double* P, double* R, int32_t* info,
+                    const double* trace_dev, const double* diag_src, int64_t diag_stride,
+                    bool compact);
+void chol_panel_c128(Handle* h, int64_t n, const double2* G, int64_t ldg, double drop_tol,
+                     double unres_rel, double shift_coef, double2* P, double2* R, int32_t* info,
+                     const double* trace_dev, const double2* diag_src, int64_t diag_stride,
+                     bool compact);
 bool chol_blocked_supported(int64_t n);
 // Cholesky-with-deletion of a Gram that is expected to be I + E (second
 // CholeskyQR pass): first-order factor when max|E| <= thr (its O(E^2) error

@@ -199,6 +199,47 @@ def test_chol_drop_sizes(ell, cplx, rank):
         assert np.abs(P[:, r:].cpu().numpy()).max() == 0.0
 
 
+@pytest.mark.parametrize("ell,cplx", [(17, False), (47, False), (110, False), (199, False),
+                                      (230, False), (33, True), (120, True), (140, True),
+                                      (150, True)])
+@pytest.mark.parametrize("shift", [0.0, 1e-14])   # shift < drop_tol^2: drops stay
+def test_chol_drop_interleaved(ell, cplx, shift):
+    """Dropped columns scattered through the panel (duplicates of earlier
+    columns at panel boundaries and inside panels) and a diagonal shift:
+    rank decision, R on the kept rows/cols, and P = R~^{-1} compacted."""
+    from paper_0909_4061_b200 import _lib
+    g = np.random.default_rng(1000 + ell)
+    m = 2 * ell + 5
+    Y = g.standard_normal((m, ell)) + (1j * g.standard_normal((m, ell)) if cplx else 0)
+    dup = sorted(set(int(x) for x in g.choice(np.arange(1, ell), size=max(1, ell // 9),
+                                               replace=False)) | {min(16, ell - 1)})
+    for j in dup:       # column j = combination of two earlier columns
+        a, b = g.integers(0, j, size=2)
+        Y[:, j] = 0.5 * Y[:, a] - 2.0 * Y[:, b]
+    Yd = torch.from_numpy(Y).cuda()
+    G = (Yd.conj().T @ Yd).contiguous()
+    P, R = torch.empty_like(G), torch.empty_like(G)
+    info = torch.zeros(4, dtype=torch.int32, device="cuda")
+    code = _lib.C128 if cplx else _lib.F64
+    _lib.call("lr_chol_drop", _lib.handle(), code, ell, _lib.ptr(G), 1e-6, 4 * ell * 1.1e-16,
+              shift, _lib.ptr(P), _lib.ptr(R), _lib.ptr(info))
+    torch.cuda.synchronize()
+    Gh = G.cpu().numpy()
+    Rref, kept = _chol_drop_ref(Gh, 1e-6, shift)
+    r = int(info[0].item())
+    assert r == len(kept) == ell - len(dup)
+    assert [j for j in range(ell) if j not in kept] == dup
+    Rg = R.cpu().numpy()
+    assert np.abs(Rg - Rref).max() <= 1e-9 * np.abs(Rref).max()
+    Pg = P.cpu().numpy()
+    Rk = Rref[np.ix_(kept, kept)]
+    Pk = Pg[np.ix_(kept, np.arange(r))]
+    assert np.abs(Rk @ Pk - np.eye(r)).max() <= 1e-8
+    assert np.abs(np.delete(Pg, kept, axis=0)).max() == 0.0
+    if r < ell:
+        assert np.abs(Pg[:, r:]).max() == 0.0
+
+
 def test_orth_ill_conditioned_panel():
     """kappa(Y) ~ 1e7 (cfg5-like): fp64 Gram CholQR2 cannot resolve it; the
     guarded fallback must still give the reference's Q."""
