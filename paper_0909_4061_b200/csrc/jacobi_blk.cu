@@ -27,6 +27,13 @@ namespace lr {
 namespace {
 
 constexpr int BW = 4;        // columns per block
+// Early exit: once every rotation of a sweep had |m_p^H m_q| <= 1e-9
+// ||m_p|| ||m_q||, the sweep's own rotations leave off-diagonal terms of
+// order 1e-18 / (relative gap) (quadratic convergence of cyclic Jacobi), far
+// below the test tolerance -- the confirming sweep that would find nothing
+// to rotate is skipped.  sigma = ||m_j|| is second-order in the remaining
+// off-diagonal terms.
+constexpr double kTQ2 = 1e-18;
 constexpr int WC = 2 * BW;   // columns held by one warp
 
 // call-free fp64 rsqrt / reciprocal (MUFU approximation + Newton steps):
@@ -140,7 +147,8 @@ __device__ __forceinline__ void subround(T (&x)[WC][R], double& nrmv, int lane, 
   double c, tg;
   T se;
   const bool rot = rot_params(a, b, v, tol, c, se, tg);
-  did |= rot ? 1 : 0;
+  // bit 1: a rotation above the quadratic-phase threshold (see kTQ2)
+  did |= (rot ? 1 : 0) | ((rot && S::abs2(v) > kTQ2 * a * b) ? 2 : 0);
   const double an = a - tg, bn = b + tg;
   // apply the four rotations (identity for pairs below the threshold)
 #pragma unroll
@@ -260,7 +268,7 @@ jacobi_blk_kernel(int n, const T* __restrict__ Rin, T* __restrict__ Mout, double
         if (lane >= BW && lane < WC) nrmv = nbuf[(P + w) * BW + lane - BW];
       }
     }
-    converged = !__syncthreads_or(did);
+    converged = !__syncthreads_or(did & 2);
   }
 
   // M (row-major, column = original column id) and the column norms
@@ -409,7 +417,7 @@ jacobi_cl_kernel(int n, const T* __restrict__ Rin, T* __restrict__ Mout, double*
       }
     }
     // cluster-wide "any rotation": per-CTA OR, gathered in rank 0
-    const int any_cta = __syncthreads_or(did);
+    const int any_cta = __syncthreads_or(did & 2);
     int* flags = cflag + (sweep & 1) * CL;
     if (threadIdx.x == 0) cluster.map_shared_rank(flags, 0)[rank] = any_cta;
     cluster.sync();
