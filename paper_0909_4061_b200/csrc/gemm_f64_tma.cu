@@ -224,7 +224,15 @@ void launch(Handle* h, int64_t M, int64_t N, int64_t K, const TIN* A, int64_t ld
   const CUtensorMap mapB = make_map_2d(DT, B, uint64_t(N), uint64_t(K), uint64_t(ldb) * ES,
                                        G::BN, BK, CU_TENSOR_MAP_SWIZZLE_NONE);
   const int64_t mt = ceil_div(M, BM), nt = ceil_div(N, G::BN);
-  const int64_t want = choose_splits(h->sm_count, mt * nt, K);
+  // a symmetric result computes only the tiles reaching the diagonal: size
+  // the split-K waves for those (the others exit at entry)
+  int64_t live = mt * nt;
+  if (sym) {
+    live = 0;
+    for (int64_t x = 0; x < mt; ++x)
+      for (int64_t y = 0; y < nt; ++y) live += ((y + 1) * G::BN > x * BM) ? 1 : 0;
+  }
+  const int64_t want = choose_splits(h->sm_count, live, K);
   const int64_t kchunk = ceil_div(ceil_div(K, want), BK) * BK;
   const int64_t splits = std::max<int64_t>(1, ceil_div(K, kchunk));
   dim3 grid{unsigned(mt), unsigned(nt), unsigned(splits)};
