@@ -11,8 +11,11 @@
 // All three products accumulate into ONE fp32 TMEM accumulator.
 //
 // CTA = 128 rows of op(A) x all N <= 256 columns (one UMMA 128 x N x 16 per
-// k-substep), k-stage 32, 3-stage ring, 256 threads:
-//   warp 0  TMA producer: fp32 A tile (16 KB) and fp16 X_hi/X_lo tiles
+// k-substep), k-stage 32, 256 threads, two rings: a 5-deep fp32 A ring
+// (TMA -> converters; deep enough to keep ~64 KB of A in flight per SM) and
+// a 3-deep operand ring (A hi/lo + X hi/lo -> MMA):
+//   warp 0  TMA producer: fp32 A tiles (16 KB, TS1 - 1 stages ahead) and
+//           fp16 X_hi/X_lo tiles
 //   warp 1  MMA issuer (one lane): 6 x tcgen05.mma kind::f16 per stage
 //   warp 2  TMEM allocator
 //   warps 4-7  converters: fp32 A tile -> scaled fp16 hi/lo in the canonical
@@ -33,7 +36,14 @@ namespace {
 
 constexpr int TBM = 128;          // UMMA M
 constexpr int TBK = 32;           // k per stage (64 B of fp16 per row)
-constexpr int TSTAGES = 3;
+#ifndef LR_TC_TS1
+#define LR_TC_TS1 5
+#endif
+#ifndef LR_TC_TS2
+#define LR_TC_TS2 3
+#endif
+constexpr int TS1 = LR_TC_TS1;    // fp32 A ring (TMA -> converters): deep, hides HBM latency
+constexpr int TS2 = LR_TC_TS2;    // operand ring (A hi/lo + X hi/lo -> MMA)
 constexpr int TTHREADS = 256;
 constexpr int A32_BYTES = TBM * TBK * 4;    // 16 KB
 constexpr int AH_BYTES = TBM * TBK * 2;     // 8 KB
@@ -100,8 +110,8 @@ __device__ __forceinline__ int sw64_off(int r, int chunk) {
   return r * 64 + ((chunk ^ ((r >> 1) & 3)) << 4);
 }
 
-__device__ __forceinline__ void split_store8(const float* v, float s, char* hi_row_base,
-                                             char* lo_row_base, int r, int g) {
+// 8 scaled fp32 values -> packed fp16 hi and lo pieces
+__device__ __forceinline__ void split8(const float* v, float s, uint4& hi, uint4& lo) {
   __half2 h[4], l[4];
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
@@ -111,9 +121,8 @@ __device__ __forceinline__ void split_store8(const float* v, float s, char* hi_r
     l[e] = __halves2half2(__float2half_rn(x0 - __half2float(h0)),
                           __float2half_rn(x1 - __half2float(h1)));
   }
-  const int off = sw64_off(r, g);
-  *reinterpret_cast<uint4*>(hi_row_base + off) = *reinterpret_cast<uint4*>(h);
-  *reinterpret_cast<uint4*>(lo_row_base + off) = *reinterpret_cast<uint4*>(l);
+  hi = *reinterpret_cast<uint4*>(h);
+  lo = *reinterpret_cast<uint4*>(l);
 }
 
 template <bool TRANS>
@@ -129,21 +138,22 @@ gemm_f32_tc_kernel(const __grid_constant__ CUtensorMap mapA,
   unsigned char* base = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int B_BYTES = BN * TBK * 2;
-  const int stage_bytes = A32_BYTES + 2 * AH_BYTES + 2 * B_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(base + TSTAGES * stage_bytes);
+  const int op_bytes = 2 * AH_BYTES + 2 * B_BYTES;
+  unsigned char* ring2 = base + TS1 * A32_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring2 + TS2 * op_bytes);
   uint64_t* a32_full = bars;
-  uint64_t* a32_empty = bars + TSTAGES;
-  uint64_t* ahl_full = bars + 2 * TSTAGES;
-  uint64_t* b_full = bars + 3 * TSTAGES;
-  uint64_t* st_empty = bars + 4 * TSTAGES;
-  uint64_t* acc_full = bars + 5 * TSTAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 5 * TSTAGES + 1);
+  uint64_t* a32_empty = bars + TS1;
+  uint64_t* ahl_full = bars + 2 * TS1;
+  uint64_t* b_full = ahl_full + TS2;
+  uint64_t* st_empty = b_full + TS2;
+  uint64_t* acc_full = st_empty + TS2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
 
-  auto a32 = [&](int s) { return base + s * stage_bytes; };
-  auto ahi = [&](int s) { return base + s * stage_bytes + A32_BYTES; };
-  auto alo = [&](int s) { return base + s * stage_bytes + A32_BYTES + AH_BYTES; };
-  auto bhi = [&](int s) { return base + s * stage_bytes + A32_BYTES + 2 * AH_BYTES; };
-  auto blo = [&](int s) { return base + s * stage_bytes + A32_BYTES + 2 * AH_BYTES + B_BYTES; };
+  auto a32 = [&](int s) { return base + s * A32_BYTES; };
+  auto ahi = [&](int s) { return ring2 + s * op_bytes; };
+  auto alo = [&](int s) { return ring2 + s * op_bytes + AH_BYTES; };
+  auto bhi = [&](int s) { return ring2 + s * op_bytes + 2 * AH_BYTES; };
+  auto blo = [&](int s) { return ring2 + s * op_bytes + 2 * AH_BYTES + B_BYTES; };
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const float sA = sA_dev ? *sA_dev : sA_host;
@@ -153,9 +163,11 @@ gemm_f32_tc_kernel(const __grid_constant__ CUtensorMap mapA,
   const int nk = int((kend - kbeg + TBK - 1) / TBK);
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < TSTAGES; ++s) {
+    for (int s = 0; s < TS1; ++s) {
       mbar_init(&a32_full[s], 1);
       mbar_init(&a32_empty[s], 128);   // every converter thread arrives itself
+    }
+    for (int s = 0; s < TS2; ++s) {
       mbar_init(&ahl_full[s], 128);
       mbar_init(&b_full[s], 1);
       mbar_init(&st_empty[s], 1);
@@ -177,21 +189,31 @@ gemm_f32_tc_kernel(const __grid_constant__ CUtensorMap mapA,
 
   if (warp == 0) {
     if (lane == 0) {
-      // ---------------- TMA producer
+      // ---------------- TMA producer.  The fp32 A tiles run TS1 - 1 stages
+      // ahead of the X tiles (whose slots free up only as the MMA retires);
+      // one thread issues both (a separate X producer warp raced: wrong rows).
       const uint32_t bbytes = uint32_t(2 * B_BYTES);
-      for (int kt = 0; kt < nk; ++kt) {
-        const int s = kt % TSTAGES;
-        const uint32_t ph = uint32_t(kt / TSTAGES) & 1u;
+      constexpr int D = TS1 - 1;
+      auto issue_a = [&](int kt) {
+        const int s = kt % TS1;
+        const uint32_t ph = uint32_t(kt / TS1) & 1u;
         const int kc = int(kbeg + int64_t(kt) * TBK);
         mbar_wait(&a32_empty[s], ph ^ 1u);
         mbar_expect_tx(&a32_full[s], A32_BYTES);
         if (!TRANS) tma_load_2d(a32(s), &mapA, &a32_full[s], kc, m0);
         else        tma_load_2d(a32(s), &mapA, &a32_full[s], m0, kc);
-        mbar_wait(&st_empty[s], ph ^ 1u);
-        mbar_expect_tx(&b_full[s], bbytes);
+      };
+      for (int kt = 0; kt < D && kt < nk; ++kt) issue_a(kt);
+      for (int kt = 0; kt < nk; ++kt) {
+        if (kt + D < nk) issue_a(kt + D);
+        const int s2 = kt % TS2;
+        const uint32_t ph2 = uint32_t(kt / TS2) & 1u;
+        const int kc = int(kbeg + int64_t(kt) * TBK);
+        mbar_wait(&st_empty[s2], ph2 ^ 1u);
+        mbar_expect_tx(&b_full[s2], bbytes);
         // X hi/lo are K-blocked: block kb = kc / 32 is BN contiguous rows of 64 B
-        tma_load_2d(bhi(s), &mapBhi, &b_full[s], 0, (kc / TBK) * BN);
-        tma_load_2d(blo(s), &mapBlo, &b_full[s], 0, (kc / TBK) * BN);
+        tma_load_2d(bhi(s2), &mapBhi, &b_full[s2], 0, (kc / TBK) * BN);
+        tma_load_2d(blo(s2), &mapBlo, &b_full[s2], 0, (kc / TBK) * BN);
       }
     }
   } else if (warp == 1) {
@@ -199,8 +221,8 @@ gemm_f32_tc_kernel(const __grid_constant__ CUtensorMap mapA,
       // ---------------- MMA issuer
       const uint32_t idesc = (1u << 4) | (uint32_t(BN >> 3) << 17) | (uint32_t(TBM >> 4) << 24);
       for (int kt = 0; kt < nk; ++kt) {
-        const int s = kt % TSTAGES;
-        const uint32_t ph = uint32_t(kt / TSTAGES) & 1u;
+        const int s = kt % TS2;
+        const uint32_t ph = uint32_t(kt / TS2) & 1u;
         mbar_wait(&ahl_full[s], ph);
         mbar_wait(&b_full[s], ph);
         asm volatile("tcgen05.fence::after_thread_sync;");
@@ -221,8 +243,10 @@ gemm_f32_tc_kernel(const __grid_constant__ CUtensorMap mapA,
     // ---------------- converters (one A row per thread), then epilogue
     const int r = threadIdx.x - 128;
     for (int kt = 0; kt < nk; ++kt) {
-      const int s = kt % TSTAGES;
-      const uint32_t ph = uint32_t(kt / TSTAGES) & 1u;
+      const int s = kt % TS1;
+      const uint32_t ph = uint32_t(kt / TS1) & 1u;
+      const int s2 = kt % TS2;
+      const uint32_t ph2 = uint32_t(kt / TS2) & 1u;
       mbar_wait(&a32_full[s], ph);
       float v[TBK];
       if (!TRANS) {
@@ -239,14 +263,23 @@ gemm_f32_tc_kernel(const __grid_constant__ CUtensorMap mapA,
 #pragma unroll
         for (int k = 0; k < TBK; ++k) v[k] = st[k * TBM + r];
       }
-      mbar_arrive(&a32_empty[s]);   // this thread's reads of the fp32 stage are done
-      mbar_wait(&st_empty[s], ph ^ 1u);   // MMA finished with the previous hi/lo tiles
+      // convert first: the fp32 values are consumed (the shared loads have
+      // landed) before the slot is handed back to the TMA engine -- an
+      // async-proxy overwrite is not ordered after generic loads still in flight
+      uint4 hv[TBK / 8], lv[TBK / 8];
 #pragma unroll
-      for (int g = 0; g < TBK / 8; ++g)
-        split_store8(v + 8 * g, sA, reinterpret_cast<char*>(ahi(s)),
-                     reinterpret_cast<char*>(alo(s)), r, g);
+      for (int g = 0; g < TBK / 8; ++g) split8(v + 8 * g, sA, hv[g], lv[g]);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive(&ahl_full[s]);    // this thread's hi/lo writes are visible to the MMA
+      mbar_arrive(&a32_empty[s]);   // this thread's reads of the fp32 stage are done
+      mbar_wait(&st_empty[s2], ph2 ^ 1u);   // MMA finished with the previous hi/lo tiles
+#pragma unroll
+      for (int g = 0; g < TBK / 8; ++g) {
+        const int off = sw64_off(r, g);
+        *reinterpret_cast<uint4*>(reinterpret_cast<char*>(ahi(s2)) + off) = hv[g];
+        *reinterpret_cast<uint4*>(reinterpret_cast<char*>(alo(s2)) + off) = lv[g];
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(&ahl_full[s2]);   // this thread's hi/lo writes are visible to the MMA
     }
     // epilogue: TMEM -> registers (row per thread) -> per-warp shared
     // transpose (the ring is idle now) -> coalesced 128-B row stores
@@ -487,8 +520,8 @@ void gemm_f32_tc(Handle* h, bool transA, int64_t M, int64_t N, int64_t K, const 
                                   uint32_t(BN), CU_TENSOR_MAP_SWIZZLE_64B);
   CUtensorMap mapBl = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT16, Blo, TBK, brows, TBK * 2, TBK,
                                   uint32_t(BN), CU_TENSOR_MAP_SWIZZLE_64B);
-  const int stage_bytes = A32_BYTES + 2 * AH_BYTES + 2 * BN * TBK * 2;
-  size_t smem = size_t(TSTAGES) * stage_bytes + 1024 /*align*/ + 256 /*barriers*/;
+  size_t smem = size_t(TS1) * A32_BYTES + size_t(TS2) * (2 * AH_BYTES + 2 * BN * TBK * 2) +
+                1024 /*align*/ + 256 /*barriers*/;
   static int one_cta = -1;
   if (one_cta < 0) {
     const char* e = getenv("LR_TC_ONE_CTA");
