@@ -113,6 +113,33 @@ int lr_chol_drop(lr_handle_t h, int dtype, int64_t ell, const void* G,
                  double drop_tol, double unres_rel, double shift_coef,
                  void* P, void* R, int32_t* info);
 
+/* PSD Cholesky of the reference (cholesky, core.py:249-272) as used by
+ * eig_nystrom (factor.py:300-335): G (ell x ell, fp64/complex128, Hermitian)
+ * = C^H C with pivots in [-neg_tol, 0] clamped to zero (zero row of C) and
+ * positive pivots kept; info[3] = number of pivots below -neg_tol (the
+ * caller raises NotPSDError / takes the eigen fallback).  P = C~^{-1}
+ * uncompacted: column j zero for a clamped pivot j, so A Q P is the
+ * reference's F = B1 C^{-1} with solve_triangular_trunc's zero components.
+ * info: {rank, 0, non-finite pivots, pivots < -neg_tol}.  ell <= 200 real /
+ * 140 complex (LR_EUNSUPPORTED above). */
+int lr_chol_psd(lr_handle_t h, int dtype, int64_t ell, const void* G, double neg_tol,
+                void* P, void* R, int32_t* info);
+
+/* Hermitian part of a small matrix (small_eig_hermitian symmetrizes,
+ * core.py:239-240): H = (B + B^H)/2 + s I with s = shift_mult ||(B+B^H)/2||_F
+ * (s = 1 for a zero matrix when shift_mult > 0); out2[0] = s, and with
+ * power_iters > 0 out2[1] = ||(B+B^H)/2||_2 by power iteration (the scale of
+ * the reference's PSD tolerance, core.py:259).  fp64 / complex128. */
+int lr_herm_prep(lr_handle_t h, int dtype, int64_t n, const void* B, int64_t ldb, void* H,
+                 double shift_mult, int power_iters, double* out2);
+
+/* Eigenpairs from the SVD of the shifted SPD matrix H = U diag(S) U^H:
+ * lam = S - *shift ordered as the reference's small_eig_hermitian
+ * (core.py:245: descending |lam|, ties descending lam), V the matching
+ * columns of U.  fp64 / complex128. */
+int lr_eig_finish(lr_handle_t h, int dtype, int64_t n, const double* S, const double* shift,
+                  const void* U, double* lam, void* V);
+
 /* Host-sync-free lr_chol_drop for pipelines that decide later (the
  * row-sharded orthonormalization, dist.py): flags as lr_orth_fast are ORed
  * into *status (device int32): 1 = unresolved pivot, 2 = column dropped,

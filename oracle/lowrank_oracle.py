@@ -595,6 +595,122 @@ def truncate_rank(f, k):
 
 
 # ---------------------------------------------------------------------------
+# Hermitian Stage-B routes (reference factor.py:168-191,300-335, core.py:233-294)
+
+PSD_TOL = 1e-12                 # reference config.py:16
+TRIANGULAR_TRUNC_TOL = 1e-12    # reference config.py:12
+
+
+class NotPSDError(ValueError):
+    """reference core.py:29-30"""
+
+
+def small_eig_hermitian(B):
+    """Symmetrize, LAPACK eigh, order by descending |lam| then descending lam
+    (core.py:233-246)."""
+    B = np.asarray(B)
+    H = 0.5 * (B + B.conj().T)
+    lam, V = np.linalg.eigh(H)
+    order = np.lexsort((-lam, -np.abs(lam)))
+    return V[:, order], lam[order].astype(np.float64)
+
+
+def cholesky_psd(B, tol=PSD_TOL):
+    """Upper C with B = C* C; pivots in [-tol ||B||_2, 0] clamp to zero, below
+    raise NotPSDError (core.py:249-272)."""
+    B = np.asarray(B)
+    n = B.shape[0]
+    scale = np.linalg.norm(B, 2) if n else 0.0
+    C = np.zeros_like(B, dtype=np.complex128 if np.iscomplexobj(B) else np.float64)
+    for i in range(n):
+        d = B[i, i].real - np.real(C[:i, i].conj() @ C[:i, i])
+        if d < -tol * scale:
+            raise NotPSDError(f"matrix is not PSD: pivot {d:.3e} at index {i}")
+        d = max(d, 0.0)
+        C[i, i] = np.sqrt(d)
+        if i + 1 < n:
+            if C[i, i] > 0:
+                C[i, i + 1:] = (B[i, i + 1:] - C[:i, i].conj() @ C[:i, i + 1:]) / C[i, i]
+            else:
+                C[i, i + 1:] = 0.0
+    return C
+
+
+def solve_triangular_trunc(R, B, trunc_tol=TRIANGULAR_TRUNC_TOL):
+    """Back substitution with zero components for diagonals <= trunc_tol
+    |r|_max (core.py:275-294)."""
+    R = np.asarray(R)
+    B = np.asarray(B)
+    k = R.shape[0]
+    X = np.zeros((k,) + B.shape[1:], dtype=np.promote_types(R.dtype, B.dtype))
+    diag = np.abs(np.diagonal(R))
+    cutoff = trunc_tol * (diag.max() if k else 0.0)
+    for i in range(k - 1, -1, -1):
+        if diag[i] <= cutoff:
+            continue
+        X[i] = (B[i] - R[i, i + 1:] @ X[i + 1:]) / R[i, i]
+    return X
+
+
+@dataclass
+class PartialEig:
+    U: np.ndarray
+    lam: np.ndarray
+    diagnostics: dict = field(default_factory=dict)
+
+    def compose(self):
+        return (self.U * self.lam) @ self.U.conj().T
+
+
+def hermitian_probe(op, seed=0, tol=1e-8):
+    """factor.py:168-178 (numpy default_rng draws, two applications)."""
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal(op.n)
+    y = rng.standard_normal(op.n)
+    ax = op.apply(x)
+    ay = op.apply(y)
+    lhs, rhs = np.vdot(y, ax), np.vdot(ay, x)
+    denom = max(abs(lhs), abs(rhs), 1e-300)
+    if abs(lhs - rhs) / denom > tol:
+        raise ValueError("operator failed the Hermitian probe")
+
+
+def direct_eig_hermitian(A, Q):
+    """factor.py:181-191: B = Q* A Q, eigenpairs of B, U = Q V."""
+    op = as_operator(A)
+    hermitian_probe(op)
+    B = Q.conj().T @ op.apply(Q)
+    V, lam = small_eig_hermitian(B)
+    return PartialEig(U=Q @ V, lam=lam)
+
+
+def eig_nystrom(A, Q):
+    """factor.py:300-335: F = (AQ) C^{-1} with B2 = Q*AQ = C*C (PSD
+    Cholesky), eigen fallback with clamping when B2 is not PSD; lam =
+    sigma(F)^2.  Returns (PartialEig, F)."""
+    op = as_operator(A)
+    B1 = op.apply(Q)
+    B2 = Q.conj().T @ B1
+    B2 = 0.5 * (B2 + B2.conj().T)
+    diagnostics = {}
+    try:
+        C = cholesky_psd(B2)
+        Ft = solve_triangular_trunc(C.conj().T[::-1, ::-1], B1.conj().T[::-1])[::-1]
+        F = Ft.conj().T
+    except NotPSDError as exc:
+        V, lam = small_eig_hermitian(B2)
+        diagnostics["not_psd_fallback"] = True
+        diagnostics["min_projected_eigenvalue"] = float(lam.min())
+        diagnostics["detail"] = str(exc)
+        lam_c = np.clip(lam, 0.0, None)
+        inv_root = np.where(lam_c > 1e-15 * max(lam_c.max(), 1e-300),
+                            1.0 / np.sqrt(np.where(lam_c > 0, lam_c, 1.0)), 0.0)
+        F = B1 @ (V * inv_root)
+    f = small_svd(F)
+    return PartialEig(U=f.U, lam=f.sigma ** 2, diagnostics=diagnostics), F
+
+
+# ---------------------------------------------------------------------------
 # Verification helpers (reference oracle.py)
 
 def exact_projection_error(A, Q, norm="spectral"):

@@ -16,8 +16,9 @@ include/lowrank_b200.h); there is no CPU fallback.
 from . import config
 from ._lib import ConvergenceError, LibraryMissing, NotPSDError
 from .core import (CudaDenseOperator, DenseOperator, MatVecOperator, OperatorCounters, SmallSVD,
-                   as_operator, orthonormalize_double_gs, small_svd)
-from .factor import PartialSVD, direct_svd, randomized_svd, truncate_rank
+                   as_operator, orthonormalize_double_gs, small_eig_hermitian, small_svd)
+from .factor import (NystromFactors, PartialEig, PartialSVD, direct_eig_hermitian, direct_svd,
+                     eig_nystrom, randomized_svd, truncate_rank)
 from .rangefinder import (RangeBasis, adaptive_range_finder, adaptive_range_finder_blocked,
                           fast_range_finder, posterior_error_estimate, power_iteration_range,
                           randomized_range_finder, subspace_iteration_range)

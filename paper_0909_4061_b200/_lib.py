@@ -52,6 +52,9 @@ _SIGS = {
                        _i64],
     "lr_gram": [_vp, _int, _i64, _i64, _vp, _i64, _vp],
     "lr_chol_drop": [_vp, _int, _i64, _vp, C.c_double, C.c_double, C.c_double, _vp, _vp, _vp],
+    "lr_chol_psd": [_vp, _int, _i64, _vp, C.c_double, _vp, _vp, _vp],
+    "lr_herm_prep": [_vp, _int, _i64, _vp, _i64, _vp, C.c_double, _int, _vp],
+    "lr_eig_finish": [_vp, _int, _i64, _vp, _vp, _vp, _vp, _vp],
     "lr_chol_drop_fast": [_vp, _int, _i64, _vp, C.c_double, C.c_double, C.c_double, C.c_double,
                           _vp, _vp, _vp, _vp],
     "lr_orth": [_vp, _int, _i64, _i64, _vp, _i64, _vp, _i64, C.c_double, C.POINTER(_i64)],

@@ -12,3 +12,7 @@ DEFAULT_ALPHA = 10.0
 
 # Probe batch of the blocked adaptive range finder.
 ADAPTIVE_BLOCK = 8
+
+# Semidefinite tolerance of the PSD Cholesky (pivots in [-PSD_TOL ||B||_2, 0]
+# clamp to zero), reference config.py:16.
+PSD_TOL = 1e-12

@@ -495,3 +495,54 @@ def small_svd(B):
         raise ValueError("B must be 2-D")
     U, S, V = small_svd_dev(t)
     return SmallSVD(U=_out(U, host), sigma=_out(S, host), V=_out(V, host))
+
+
+# ---------------------------------------------------------------------------
+# small Hermitian eigendecomposition (reference core.py:233-246)
+
+def _wide(dtype):
+    torch = _torch()
+    return torch.complex128 if dtype in (torch.complex64, torch.complex128) else torch.float64
+
+
+def small_eig_hermitian_dev(B):
+    """Eigenpairs of the Hermitian part of a device matrix B (k x k):
+    (V, lam), lam float64 ordered by descending |lam| (ties: descending lam).
+
+    Computed as the SVD of the shifted SPD matrix (B + B^H)/2 + s I,
+    s = 2 ||(B + B^H)/2||_F (condition number <= 3), by the K4 small-SVD
+    kernels: lam = sigma - s, absolute accuracy O(u ||B||) like LAPACK eigh."""
+    torch = _torch()
+    k = B.shape[0]
+    if B.dim() != 2 or B.shape[1] != k:
+        raise ValueError("small_eig_hermitian requires a square matrix")
+    wd = _wide(B.dtype)
+    if k == 0:
+        return (torch.zeros((0, 0), dtype=wd, device=B.device),
+                torch.zeros(0, dtype=torch.float64, device=B.device))
+    Bw = cast_dev(B, wd).contiguous()
+    code = _lib.dtype_code(wd)
+    h = _lib.handle(B.device.index)
+    H = torch.empty((k, k), dtype=wd, device=B.device)
+    out2 = torch.zeros(2, dtype=torch.float64, device=B.device)
+    _lib.call("lr_herm_prep", h, code, k, _lib.ptr(Bw), _lib.ld(Bw), _lib.ptr(H), 2.0, 0,
+              _lib.ptr(out2))
+    U, S, _ = small_svd_dev(H)
+    lam = torch.empty(k, dtype=torch.float64, device=B.device)
+    V = torch.empty((k, k), dtype=wd, device=B.device)
+    _lib.call("lr_eig_finish", h, code, k, _lib.ptr(S), _lib.ptr(out2), _lib.ptr(U.contiguous()),
+              _lib.ptr(lam), _lib.ptr(V))
+    return V, lam
+
+
+def small_eig_hermitian(B):
+    """Eigendecomposition of a Hermitian matrix, symmetrized internally
+    (replaces reference core.py:233-246).  Returns (V, lam): real lam by
+    descending magnitude (equal magnitudes in descending value), orthonormal
+    V."""
+    host = not is_device_array(B)
+    t = to_device(B)
+    if t.dim() != 2 or t.shape[0] != t.shape[1]:
+        raise ValueError("small_eig_hermitian requires a square matrix")
+    V, lam = small_eig_hermitian_dev(t)
+    return _out(V, host), _out(lam, host)

@@ -681,6 +681,49 @@ int lr_chol_drop(lr_handle_t hh, int dtype, int64_t ell, const void* G, double d
   API_END
 }
 
+int lr_chol_psd(lr_handle_t hh, int dtype, int64_t ell, const void* G, double neg_tol,
+                void* P, void* R, int32_t* info) {
+  API_BEGIN
+  Handle* h = H(hh);
+  check_dtype(dtype);
+  LR_REQUIRE(dtype == LR_F64 || dtype == LR_C128, LR_EINVAL, "chol_psd: wide dtypes only");
+  LR_REQUIRE(lr::chol_panel_supported(ell, dtype == LR_C128), LR_EUNSUPPORTED,
+             "chol_psd: ell above the panel kernel's range (200 real / 140 complex)");
+  LR_REQUIRE(neg_tol >= 0.0, LR_EINVAL, "chol_psd: neg_tol must be >= 0");
+  lr::pool_reset(h);
+  if (dtype == LR_C128)
+    lr::chol_panel_c128(h, ell, static_cast<const double2*>(G), ell, 0.0, 0.0, 0.0,
+                        static_cast<double2*>(P), static_cast<double2*>(R), info, nullptr,
+                        nullptr, 0, false, neg_tol);
+  else
+    lr::chol_panel_f64(h, ell, static_cast<const double*>(G), ell, 0.0, 0.0, 0.0,
+                       static_cast<double*>(P), static_cast<double*>(R), info, nullptr, nullptr,
+                       0, false, neg_tol);
+  API_END
+}
+
+int lr_herm_prep(lr_handle_t hh, int dtype, int64_t n, const void* B, int64_t ldb, void* Hout,
+                 double shift_mult, int power_iters, double* out2) {
+  API_BEGIN
+  Handle* h = H(hh);
+  check_dtype(dtype);
+  LR_REQUIRE(dtype == LR_F64 || dtype == LR_C128, LR_EINVAL, "herm_prep: wide dtypes only");
+  LR_REQUIRE(n >= 1 && n <= 4096, LR_EINVAL, "herm_prep: n out of range");
+  lr::herm_prep(h, dtype, n, B, ldb, Hout, shift_mult, power_iters, out2);
+  API_END
+}
+
+int lr_eig_finish(lr_handle_t hh, int dtype, int64_t n, const double* S, const double* shift,
+                  const void* U, double* lam, void* V) {
+  API_BEGIN
+  Handle* h = H(hh);
+  check_dtype(dtype);
+  LR_REQUIRE(dtype == LR_F64 || dtype == LR_C128, LR_EINVAL, "eig_finish: wide dtypes only");
+  LR_REQUIRE(n >= 1 && n <= 4096, LR_EINVAL, "eig_finish: n out of range");
+  lr::eig_finish(h, dtype, n, S, shift, U, lam, V);
+  API_END
+}
+
 int lr_chol_drop_fast(lr_handle_t hh, int dtype, int64_t ell, const void* G, double drop_tol,
                       double unres_rel, double shift_coef, double near_thr, void* P, void* R,
                       int32_t* info, int32_t* status) {

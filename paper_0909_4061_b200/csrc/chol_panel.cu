@@ -78,7 +78,7 @@ chol_panel_kernel(int n, const T* __restrict__ G, int64_t ldg, double drop_tol, 
                   double shift_coef, T* __restrict__ P, T* __restrict__ Rout,
                   int32_t* __restrict__ info, int32_t* status, const double* __restrict__ trace_dev,
                   const T* __restrict__ diag_src, int64_t diag_stride, bool compact,
-                  const int32_t* __restrict__ gate, long long* prof) {
+                  const int32_t* __restrict__ gate, double psd_neg, long long* prof) {
   if (gate && *gate == 0) return;
   using S = Sc<T>;
   int np = 0;   // LR_CHOL_PROF: phase timestamps of thread 0
@@ -95,7 +95,7 @@ chol_panel_kernel(int n, const T* __restrict__ G, int64_t ldg, double drop_tol, 
   int* pos = reinterpret_cast<int*>(rti + n);
   int* kidx = pos + n;
   __shared__ double s_trace;
-  __shared__ int s_unres, s_bad, s_rank;
+  __shared__ int s_unres, s_bad, s_rank, s_npsd;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   auto at = [&](int i, int k) -> T& { return W[poff(n, i) + (k - i)]; };
@@ -140,7 +140,7 @@ chol_panel_kernel(int n, const T* __restrict__ G, int64_t ldg, double drop_tol, 
   __syncthreads();
 
   // ---- right-looking panel factorization ----
-  int my_unres = 0, my_bad = 0;   // warp 0, lane 0
+  int my_unres = 0, my_bad = 0, my_npsd = 0;   // warp 0, lane 0
   for (int j0 = 0; j0 < n; j0 += NB) {
     const int nb = min(NB, n - j0), j1 = j0 + nb;
     // (a) diagonal block, one warp, in registers: lane l holds column
@@ -190,7 +190,10 @@ chol_panel_kernel(int n, const T* __restrict__ G, int64_t ldg, double drop_tol, 
         const unsigned msk = (1u << nb) - 1u;   // lanes 0 .. nb-1 (nb <= 16)
         const unsigned un = __ballot_sync(msk, keep && myd <= unres_rel * d0[j]);
         const unsigned bd = __ballot_sync(msk, !fin);
-        if (lane == 0) { my_unres += __popc(un); my_bad += __popc(bd); }
+        // PSD mode (cholesky of the reference, core.py:249-272): pivots below
+        // -psd_neg are a NotPSDError; those in [-psd_neg, 0] are clamped (dropped)
+        const unsigned ng = __ballot_sync(msk, psd_neg >= 0.0 && myd < -psd_neg);
+        if (lane == 0) { my_unres += __popc(un); my_bad += __popc(bd); my_npsd += __popc(ng); }
       }
       __syncwarp();
       PROF_MARK();
@@ -285,7 +288,7 @@ chol_panel_kernel(int n, const T* __restrict__ G, int64_t ldg, double drop_tol, 
   PROF_MARK();
   // ---- compaction of the kept pivots ----
   if (warp == 0) {
-    if (lane == 0) { s_unres = my_unres; s_bad = my_bad; }
+    if (lane == 0) { s_unres = my_unres; s_bad = my_bad; s_npsd = my_npsd; }
     int base = 0;
     for (int jj = 0; jj < n; jj += 32) {
       const int j = jj + lane;
@@ -418,6 +421,7 @@ chol_panel_kernel(int n, const T* __restrict__ G, int64_t ldg, double drop_tol, 
     info[0] = rank;
     info[1] = s_unres;
     info[2] = s_bad;
+    if (psd_neg >= 0.0) info[3] = s_npsd;
     if (status) {
       const int bits = (s_unres ? 1 : 0) | (rank < n ? 2 : 0) | (s_bad ? 4 : 0);
       if (bits) atomicOr(status, bits);
@@ -428,7 +432,7 @@ chol_panel_kernel(int n, const T* __restrict__ G, int64_t ldg, double drop_tol, 
 template <typename T>
 void launch_panel(Handle* h, int n, const T* G, int64_t ldg, double drop_tol, double unres_rel,
                   double shift_coef, T* P, T* R, int32_t* info, const double* trace_dev,
-                  const T* diag_src, int64_t diag_stride, bool compact) {
+                  const T* diag_src, int64_t diag_stride, bool compact, double psd_neg) {
   const size_t smem = panel_smem_bytes<T>(n);
   auto kern = chol_panel_kernel<T>;
   LR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -437,7 +441,7 @@ void launch_panel(Handle* h, int n, const T* G, int64_t ldg, double drop_tol, do
   long long* prof = prof_on ? pool_alloc_t<long long>(h, 64) : nullptr;
   kern<<<1, NT, smem, h->stream>>>(n, G, ldg, drop_tol, unres_rel, shift_coef, P, R, info,
                                    h->status, trace_dev, diag_src, diag_stride, compact, h->gate,
-                                   prof);
+                                   psd_neg, prof);
   LR_CHECK_LAUNCH();
   if (prof) {   // development only: synchronizes
     long long hp[64];
@@ -468,17 +472,17 @@ bool chol_panel_supported(int64_t n, bool cplx) {
 void chol_panel_f64(Handle* h, int64_t n, const double* G, int64_t ldg, double drop_tol,
                     double unres_rel, double shift_coef, double* P, double* R, int32_t* info,
                     const double* trace_dev, const double* diag_src, int64_t diag_stride,
-                    bool compact) {
+                    bool compact, double psd_neg) {
   launch_panel<double>(h, int(n), G, ldg, drop_tol, unres_rel, shift_coef, P, R, info,
-                       trace_dev, diag_src, diag_stride, compact);
+                       trace_dev, diag_src, diag_stride, compact, psd_neg);
 }
 
 void chol_panel_c128(Handle* h, int64_t n, const double2* G, int64_t ldg, double drop_tol,
                      double unres_rel, double shift_coef, double2* P, double2* R, int32_t* info,
                      const double* trace_dev, const double2* diag_src, int64_t diag_stride,
-                     bool compact) {
+                     bool compact, double psd_neg) {
   launch_panel<double2>(h, int(n), G, ldg, drop_tol, unres_rel, shift_coef, P, R, info,
-                        trace_dev, diag_src, diag_stride, compact);
+                        trace_dev, diag_src, diag_stride, compact, psd_neg);
 }
 
 }  // namespace lr

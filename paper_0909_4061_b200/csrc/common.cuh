@@ -173,11 +173,16 @@ bool chol_panel_supported(int64_t n, bool cplx);
 void chol_panel_f64(Handle* h, int64_t n, const double* G, int64_t ldg, double drop_tol,
                     double unres_rel, double shift_coef, double* P, double* R, int32_t* info,
                     const double* trace_dev, const double* diag_src, int64_t diag_stride,
-                    bool compact);
+                    bool compact, double psd_neg = -1.0);
 void chol_panel_c128(Handle* h, int64_t n, const double2* G, int64_t ldg, double drop_tol,
                      double unres_rel, double shift_coef, double2* P, double2* R, int32_t* info,
                      const double* trace_dev, const double2* diag_src, int64_t diag_stride,
-                     bool compact);
+                     bool compact, double psd_neg = -1.0);
+// stageb.cu: Hermitian helpers of the Stage-B variants (factor.py:168-335)
+void herm_prep(Handle* h, int dtype_wide, int64_t n, const void* B, int64_t ldb, void* H,
+               double shift_mult, int power_iters, double* out2);
+void eig_finish(Handle* h, int dtype_wide, int64_t n, const double* S, const double* shift,
+                const void* U, double* lam, void* V);
 bool chol_blocked_supported(int64_t n);
 // Cholesky-with-deletion of a Gram that is expected to be I + E (second
 // CholeskyQR pass): first-order factor when max|E| <= thr (its O(E^2) error

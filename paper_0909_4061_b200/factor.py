@@ -1,21 +1,28 @@
-"""Stage B on the GPU: the direct SVD (Alg 5.1) and the rSVD composition.
+"""Stage B on the GPU: the direct SVD (Alg 5.1), the rSVD composition and the
+Hermitian routes (direct eigendecomposition, Nystrom).
 
 Mirrors ``direct_svd`` / ``PartialSVD`` / ``truncate_rank`` of the
 reference's ``lowrank.factor`` (factor.py:41-50,154-165,408-426), and the
 CLI's "randomized SVD" composition (cli.py:128-173 Stage-A dispatch +
 direct_svd + posterior estimate with seed + 13, cli.py:222-262) as
 ``randomized_svd``, which keeps every intermediate in HBM and only copies
-the final factors back.  Other Stage-B routes (ID / row extraction,
-Nystrom, one-pass) are outside this build's scope.
+the final factors back.  ``direct_eig_hermitian`` (factor.py:168-191) and
+``eig_nystrom`` (factor.py:300-335) reuse the passes, the Cholesky kernel in
+its PSD mode and the small SVD.  ID / row extraction and
+the one-pass sketches are outside this build's scope.
 """
 
 from __future__ import annotations
 
-from dataclasses import dataclass
+from dataclasses import dataclass, field
+
+import numpy as np
 
 from . import config
-from .core import (_out, _torch, apply_dev, as_operator, gemm_dev, is_device_array,
-                   small_svd_from_adjoint, speculate, to_device)
+from . import _lib
+from .core import (_out, _torch, _wide, apply_dev, as_operator, cast_dev, gemm, gemm_dev,
+                   is_device_array, small_eig_hermitian_dev, small_svd_from_adjoint, speculate,
+                   to_device)
 from .rangefinder import (RangeBasis, SketchSpec, _cast_like_op, _check_ell, _host_io,
                           _sketch_dev, orth_dev, posterior_error_estimate_dev, probes_dev,
                           subspace_iteration_range_dev)
@@ -63,6 +70,169 @@ def direct_svd(A, Q):
     Qd = to_device(Q, dt if op.device_native else None)
     U, S, V = direct_svd_dev(op, Qd)
     return PartialSVD(U=_out(U, host), sigma=_out(S, host), V=_out(V, host))
+
+
+@dataclass
+class PartialEig:
+    """Hermitian A ~= U @ diag(lam) @ U*; lam real, descending magnitude
+    (reference factor.py:54-62)."""
+
+    U: object
+    lam: object
+    diagnostics: dict = field(default_factory=dict)
+
+    def compose(self):
+        if is_device_array(self.U):
+            return (self.U * self.lam.to(self.U.dtype)) @ self.U.conj().T
+        return (self.U * self.lam) @ self.U.conj().T
+
+
+@dataclass
+class NystromFactors:
+    """PSD approximation A ~= F @ F* (reference factor.py:87-91)."""
+
+    F: object
+
+
+def _vdot_dev(x, y):
+    """conj(x) . y of two device vectors, in fp64 / complex128 (one K1-type
+    product on the library's GEMM)."""
+    torch = _torch()
+    wd = torch.complex128 if (x.is_complex() or y.is_complex()) else torch.float64
+    xw = cast_dev(x, wd).reshape(-1, 1)
+    yw = cast_dev(y, wd).reshape(-1, 1)
+    out = torch.empty((1, 1), dtype=wd, device=x.device)
+    gemm(xw, yw, out, adjoint=True)
+    return out
+
+
+def _hermitian_probe(op, seed=0, tol=1e-8):
+    """Reject non-Hermitian operators: |<y, Ax> - <Ay, x>| <= tol max(...)
+    with x, y ~ N(0, 1) from numpy's default_rng(seed) (reference
+    factor.py:168-178; the draws are the reference's, uploaded).  The two
+    probe applications count in the operator's counters, as there."""
+    if op.m != op.n:
+        raise ValueError("operator failed the Hermitian probe (not square)")
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal(op.n)
+    y = rng.standard_normal(op.n)
+    dt = getattr(op, "dtype", None)
+    xd, yd = to_device(x, dt if op.device_native else None), to_device(y, dt if op.device_native else None)
+    ax = apply_dev(op, xd.reshape(-1, 1)).reshape(-1)
+    ay = apply_dev(op, yd.reshape(-1, 1)).reshape(-1)
+    lhs = complex(_vdot_dev(yd, ax).cpu().reshape(-1)[0].item())
+    rhs = complex(_vdot_dev(ay, xd).cpu().reshape(-1)[0].item())
+    denom = max(abs(lhs), abs(rhs), 1e-300)
+    torch = _torch()
+    if op.device_native and dt in (torch.float32, torch.complex64):
+        # fp32 operators: the passes carry ~1e-7 relative error (the reference
+        # upcasts to fp64, core.py:44-47), so the probe tolerance is widened to
+        # 1e-5 -- asymmetry between 1e-8 and 1e-5 relative passes here
+        tol = max(tol, 1e-5)
+    if abs(lhs - rhs) / denom > tol:
+        raise ValueError("operator failed the Hermitian probe")
+
+
+def direct_eig_hermitian_dev(op, Q):
+    """B = Q* (A Q) (one pass + one m-side product), eigenpairs of B on the
+    device, U = Q V.  Returns device (U, lam)."""
+    torch = _torch()
+    k = Q.shape[1]
+    Y = apply_dev(op, Q)
+    B = torch.empty((k, k), dtype=Q.dtype, device=Q.device)
+    gemm(Q, Y, B, adjoint=True)
+    V, lam = small_eig_hermitian_dev(B)
+    U = torch.empty((Q.shape[0], k), dtype=Q.dtype, device=Q.device)
+    gemm_dev(Q, cast_dev(V, Q.dtype), U)
+    return U, lam
+
+
+def direct_eig_hermitian(A, Q):
+    """Partial eigendecomposition of a Hermitian matrix via B = Q*AQ
+    (reference factor.py:181-191): the error is at most twice the basis
+    residual; a seeded probe rejects non-Hermitian operators."""
+    op = as_operator(A)
+    _hermitian_probe(op)
+    if Q.shape[0] != op.m:
+        raise ValueError("basis rows must match matrix rows")
+    host = _host_io(A, op) and not is_device_array(Q)
+    dt = getattr(op, "dtype", None)
+    Qd = to_device(Q, dt if op.device_native else None)
+    if Qd.dim() == 1:
+        Qd = Qd.reshape(-1, 1)
+    U, lam = direct_eig_hermitian_dev(op, Qd)
+    return PartialEig(U=_out(U, host), lam=_out(lam, host))
+
+
+def eig_nystrom(A, Q, psd_tol=config.PSD_TOL):
+    """Nystrom eigendecomposition of a PSD matrix (reference factor.py:300-335).
+
+    B1 = A Q (one pass), B2 = Q* B1 symmetrized, B2 = C* C by the PSD
+    Cholesky (pivots in [-psd_tol ||B2||_2, 0] clamped, core.py:249-272; the
+    panel kernel in PSD mode), F = B1 C^{-1} with zero columns for clamped
+    pivots (solve_triangular_trunc's zero components), then the small SVD of
+    F: lam = sigma^2.  A pivot below the tolerance takes the reference's
+    fallback: eigenpairs of B2 clamped at zero, F = B1 V diag(lam^-1/2), and
+    diagnostics["not_psd_fallback"] = True.  Returns (PartialEig,
+    NystromFactors)."""
+    torch = _torch()
+    op = as_operator(A)
+    if Q.shape[0] != op.m or op.m != op.n:
+        raise ValueError("eig_nystrom needs a square operator and a basis with matching rows")
+    host = _host_io(A, op) and not is_device_array(Q)
+    dt = getattr(op, "dtype", None)
+    Qd = to_device(Q, dt if op.device_native else None)
+    if Qd.dim() == 1:
+        Qd = Qd.reshape(-1, 1)
+    m, k = Qd.shape
+    dev = Qd.device
+    B1 = apply_dev(op, Qd)
+    B2 = torch.empty((k, k), dtype=Qd.dtype, device=dev)
+    gemm(Qd, B1, B2, adjoint=True)
+    wd = _wide(Qd.dtype)
+    code = _lib.dtype_code(wd)
+    h = _lib.handle(dev.index)
+    B2w = cast_dev(B2, wd).contiguous()
+    Hs = torch.empty((k, k), dtype=wd, device=dev)
+    out2 = torch.zeros(2, dtype=torch.float64, device=dev)
+    _lib.call("lr_herm_prep", h, code, k, _lib.ptr(B2w), _lib.ld(B2w), _lib.ptr(Hs), 0.0, 64,
+              _lib.ptr(out2))
+    scale = float(out2[1].item())
+    P = torch.empty((k, k), dtype=wd, device=dev)
+    R = torch.empty((k, k), dtype=wd, device=dev)
+    info = torch.zeros(4, dtype=torch.int32, device=dev)
+    _lib.call("lr_chol_psd", h, code, k, _lib.ptr(Hs), float(psd_tol * scale), _lib.ptr(P),
+              _lib.ptr(R), _lib.ptr(info))
+    inf = info.cpu().tolist()
+    diagnostics = {}
+    if inf[3] > 0 or inf[2] > 0:
+        # clamp the projected block at zero and pseudo-invert its square root
+        V, lam = small_eig_hermitian_dev(Hs)
+        lam_h = lam.cpu().numpy()
+        diagnostics["not_psd_fallback"] = True
+        diagnostics["min_projected_eigenvalue"] = float(lam_h.min())
+        diagnostics["detail"] = f"matrix is not PSD: {inf[3]} pivot(s) below -{psd_tol:g}*||B||"
+        lam_c = np.clip(lam_h, 0.0, None)
+        inv_root = np.where(lam_c > 1e-15 * max(lam_c.max(), 1e-300),
+                            1.0 / np.sqrt(np.where(lam_c > 0, lam_c, 1.0)), 0.0)
+        D = to_device(np.diag(inv_root).astype(np.complex128 if wd == torch.complex128
+                                                else np.float64), wd, dev.index)
+        W = torch.empty((k, k), dtype=wd, device=dev)
+        gemm_dev(V, D, W)
+        Pm = cast_dev(W, Qd.dtype)
+    else:
+        Pm = cast_dev(P, Qd.dtype)
+    F = torch.empty((m, k), dtype=Qd.dtype, device=dev)
+    gemm_dev(B1, Pm, F)
+    # SVD of the tall F: B = F^H = Ub S Vb^H, so F = Vb S Ub^H (U_F = Vb)
+    Z = F.clone()
+    Ub, S, Vb = small_svd_from_adjoint(Z)
+    UF, VF = Vb, Ub
+    _lib.call("lr_sign_fix", h, _lib.dtype_code(UF.dtype), m, k, k, _lib.ptr(UF), _lib.ld(UF),
+              _lib.ptr(VF), _lib.ld(VF))
+    lam = S * S
+    f = PartialEig(U=_out(UF, host), lam=_out(lam, host), diagnostics=diagnostics)
+    return f, NystromFactors(F=_out(F, host))
 
 
 def truncate_rank(f, k):

@@ -211,7 +211,42 @@ def g_cfg5s():
     save("cfg5s", **run_cfg(op, c.k, c.p, c.q, c.seed), nnz=np.array([S.nnz]))
 
 
-ALL = {"kats": g_kats, "cfg1": g_cfg1, "cfg3": g_cfg3, "cfg4s": g_cfg4s, "cfg5s": g_cfg5s,
+def g_stageb():
+    """Hermitian Stage-B routes (factor.py:168-191,300-335) on small inputs;
+    the matrices are stored (they are tiny)."""
+    from lowrank.oracle import synthetic_psd
+    out = {}
+    rng = np.random.default_rng(12)
+    G = rng.standard_normal((18, 18))
+    A = 0.5 * (G + G.T)
+    b = rangefinder.randomized_range_finder(core.DenseOperator(A), 6, seed=0)
+    f = factor.direct_eig_hermitian(core.DenseOperator(A), b.Q)
+    out.update(eig_A=A, eig_Q=b.Q, eig_lam=f.lam, eig_comp=f.compose())
+    f = factor.direct_eig_hermitian(core.DenseOperator(np.diag([3.0, -2.0, 1.0])), np.eye(3))
+    out["eig_diag_lam"] = f.lam
+    Gc = rng.standard_normal((16, 16)) + 1j * rng.standard_normal((16, 16))
+    Ac = 0.5 * (Gc + Gc.conj().T)
+    b = rangefinder.randomized_range_finder(core.DenseOperator(Ac), 5, seed=1)
+    f = factor.direct_eig_hermitian(core.DenseOperator(Ac), b.Q)
+    out.update(eigc_A=Ac, eigc_Q=b.Q, eigc_lam=f.lam, eigc_comp=f.compose())
+    out["seig_B"] = rng.standard_normal((9, 9))
+    V, lam = core.small_eig_hermitian(out["seig_B"])
+    out["seig_lam"] = lam
+    for tag, (kind, par, sd, ell, qs) in {"nys_rank": ("exact_rank", 4, 17, 6, 1),
+                                         "nys_exp": ("exp_decay", 0.7, 18, 6, 4),
+                                         "nys_pow": ("power_decay", 1.5, 3, 7, 3)}.items():
+        H, _ = synthetic_psd(25 if tag != "nys_pow" else 24, kind, par, seed=sd)
+        b = rangefinder.randomized_range_finder(core.DenseOperator(H), ell, seed=qs)
+        f, fac = factor.eig_nystrom(core.DenseOperator(H), b.Q)
+        out.update({f"{tag}_H": H, f"{tag}_Q": b.Q, f"{tag}_lam": f.lam,
+                    f"{tag}_comp": f.compose(), f"{tag}_FF": fac.F @ fac.F.conj().T})
+    f, fac = factor.eig_nystrom(core.DenseOperator(np.diag([1.0, 0.5, -0.8])), np.eye(3))
+    out["nys_fb_lam"] = f.lam
+    out["nys_fb_flag"] = np.array([float(bool(f.diagnostics.get("not_psd_fallback")))])
+    save("stageb", **out)
+
+
+ALL = {"kats": g_kats, "stageb": g_stageb, "cfg1": g_cfg1, "cfg3": g_cfg3, "cfg4s": g_cfg4s, "cfg5s": g_cfg5s,
        "cfg2": g_cfg2}
 
 if __name__ == "__main__":

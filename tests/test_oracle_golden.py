@@ -132,3 +132,31 @@ def test_adaptive_oracle_matches_reference(golden):
     b = O.adaptive_range_finder(g["ad_A"][:, :8], 1e-12, r=4, seed=2)
     assert b.saturated and b.Q.shape == g["ad_sat_Q"].shape
     assert np.abs(b.Q - g["ad_sat_Q"]).max() <= 1e-12
+
+
+def test_stageb_hermitian_routes(golden):
+    """direct_eig_hermitian / small_eig_hermitian / eig_nystrom restatements
+    against the reference (factor.py:168-191,300-335, core.py:233-294)."""
+    g = golden("stageb")
+    f = O.direct_eig_hermitian(g["eig_A"], g["eig_Q"])
+    assert np.abs(f.lam - g["eig_lam"]).max() <= 1e-13 * np.abs(g["eig_lam"]).max()
+    assert np.abs(f.compose() - g["eig_comp"]).max() <= 1e-13
+    assert np.allclose(O.direct_eig_hermitian(np.diag([3.0, -2.0, 1.0]), np.eye(3)).lam,
+                       g["eig_diag_lam"], rtol=0, atol=1e-15)
+    f = O.direct_eig_hermitian(g["eigc_A"], g["eigc_Q"])
+    assert np.abs(f.lam - g["eigc_lam"]).max() <= 1e-13 * np.abs(g["eigc_lam"]).max()
+    assert np.abs(f.compose() - g["eigc_comp"]).max() <= 1e-13
+    _, lam = O.small_eig_hermitian(g["seig_B"])
+    assert np.abs(lam - g["seig_lam"]).max() <= 1e-13
+    for tag in ("nys_rank", "nys_exp", "nys_pow"):
+        f, F = O.eig_nystrom(g[f"{tag}_H"], g[f"{tag}_Q"])
+        scale = np.abs(g[f"{tag}_lam"]).max()
+        assert np.abs(f.lam - g[f"{tag}_lam"]).max() <= 1e-12 * scale
+        assert np.abs(f.compose() - g[f"{tag}_comp"]).max() <= 1e-12 * scale
+        assert np.abs(F @ F.conj().T - g[f"{tag}_FF"]).max() <= 1e-12 * scale
+    f, _ = O.eig_nystrom(np.diag([1.0, 0.5, -0.8]), np.eye(3))
+    assert f.diagnostics.get("not_psd_fallback") and g["nys_fb_flag"][0] == 1.0
+    assert np.allclose(f.lam, g["nys_fb_lam"], rtol=0, atol=1e-15)
+    with pytest.raises(ValueError):
+        O.direct_eig_hermitian(np.random.default_rng(13).standard_normal((10, 10)),
+                               np.eye(10)[:, :3])
