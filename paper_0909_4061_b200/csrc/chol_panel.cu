@@ -62,7 +62,6 @@ __device__ __forceinline__ int poff(int n, int i) { return i * n - (i * (i - 1))
 
 template <typename T>
 __host__ __device__ constexpr int tile_i() { return sizeof(T) == 8 ? 4 : 2; }
-constexpr int TK = 4;
 
 template <typename T>
 size_t panel_smem_bytes(int n) {
@@ -352,51 +351,101 @@ chol_panel_kernel(int n, const T* __restrict__ G, int64_t ldg, double drop_tol, 
   __syncthreads();
   PROF_MARK();
   // ---- block columns: X[:j0, J] = -X[:j0, :j0] (R[:j0, J] X_JJ) ----
-  // lane = (half, c): column c of the block, rows i0 + half + 2a; the block
-  // row loads are 16 consecutive elements, the row-i loads broadcasts.
+  // Register-blocked: a thread owns RB consecutive rows x 4 consecutive
+  // columns (RB = 4 real, 2 complex), row pointers hoisted -- the per-element
+  // version was instruction-issue bound (~35 instructions per 4 FMAs).
   {
-    constexpr int RA = sizeof(T) == 8 ? 4 : 2;   // rows per thread
-    constexpr int WROWS = 2 * RA;                // rows per warp chunk
-    const int c = lane & 15, half = lane >> 4;
+    constexpr int RB = sizeof(T) == 8 ? 4 : 2;
     for (int J = 1; J < nbk; ++J) {
       const int j0 = J * NB, nb = min(NB, n - j0);
-      const T* bJ = W;                           // rows of X_JJ: poff(j0 + k) - j0
-      for (int ib = warp * WROWS; ib < j0; ib += NW * WROWS) {
-        T acc[RA];
+      const int nq = (nb + 3) / 4, nr = (j0 + RB - 1) / RB;
+      // T = R[:j0, J] X_JJ  (X_JJ upper: entry (k, c) nonzero for k <= c)
+      for (int e = tid; e < nr * nq; e += NT) {
+        const int rq = e / nq, c0 = 4 * (e - rq * nq);
+        const int i0 = RB * rq;
+        const T* rr[RB];
 #pragma unroll
-        for (int a = 0; a < RA; ++a) acc[a] = S::zero();
-        for (int k = 0; k < nb; ++k) {
-          const T* rowk = bJ + poff(n, j0 + k) - (j0 + k);
-          const T xk = (k <= c && c < nb) ? rowk[j0 + c] : S::zero();
+        for (int a = 0; a < RB; ++a) {
+          const int i = min(i0 + a, j0 - 1);
+          rr[a] = W + poff(n, i) - i + j0;          // rr[a][k] = R(i, j0 + k)
+        }
+        T acc[RB][4];
 #pragma unroll
-          for (int a = 0; a < RA; ++a) {
-            const int i = ib + half + 2 * a;
-            if (i < j0) acc[a] = S::add(acc[a], S::mul(at(i, j0 + k), xk));
+        for (int a = 0; a < RB; ++a)
+#pragma unroll
+          for (int t = 0; t < 4; ++t) acc[a][t] = S::zero();
+        const int kmax = min(c0 + 3, nb - 1);
+        for (int k = 0; k <= kmax; ++k) {
+          const T* xk = W + poff(n, j0 + k) - (j0 + k) + j0;   // xk[c] = X_JJ(k, c)
+          T xv[4];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) xv[t] = (c0 + t >= k && c0 + t < nb) ? xk[c0 + t] : S::zero();
+#pragma unroll
+          for (int a = 0; a < RB; ++a) {
+            const T r = rr[a][k];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) acc[a][t] = S::add(acc[a][t], S::mul(r, xv[t]));
           }
         }
 #pragma unroll
-        for (int a = 0; a < RA; ++a) {
-          const int i = ib + half + 2 * a;
-          if (i < j0) Tb[i * NB + c] = acc[a];
-        }
+        for (int a = 0; a < RB; ++a)
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+            if (i0 + a < j0) Tb[(i0 + a) * NB + c0 + t] = acc[a][t];
       }
       __syncthreads();
-      for (int ib = warp * WROWS; ib < j0; ib += NW * WROWS) {
-        T acc[RA];
+      // X(i, j0 + c) = -sum_{k >= i} X(i, k) T(k, c)
+      for (int e = tid; e < nr * nq; e += NT) {
+        const int rq = e / nq, c0 = 4 * (e - rq * nq);
+        const int i0 = RB * rq;
+        const T* xr[RB];
 #pragma unroll
-        for (int a = 0; a < RA; ++a) acc[a] = S::zero();
-        for (int k = ib; k < j0; ++k) {
-          const T tk = Tb[k * NB + c];
+        for (int a = 0; a < RB; ++a) {
+          const int i = min(i0 + a, j0 - 1);
+          xr[a] = W + poff(n, i) - i;                // xr[a][k] = X(i, k), k >= i
+        }
+        T acc[RB][4];
 #pragma unroll
-          for (int a = 0; a < RA; ++a) {
-            const int i = ib + half + 2 * a;
-            if (k >= i && i < j0) acc[a] = S::add(acc[a], S::mul(at(i, k), tk));
+        for (int a = 0; a < RB; ++a)
+#pragma unroll
+          for (int t = 0; t < 4; ++t) acc[a][t] = S::zero();
+        // the first RB - 1 columns k are inside the row block's triangle
+#pragma unroll
+        for (int kk = 0; kk < RB - 1; ++kk) {
+          const int k = i0 + kk;
+          if (k < j0) {
+            const T* tb = Tb + k * NB + c0;
+#pragma unroll
+            for (int a = 0; a < RB; ++a) {
+              if (a <= kk) {
+                const T x = xr[a][k];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) acc[a][t] = S::add(acc[a][t], S::mul(x, tb[t]));
+              }
+            }
+          }
+        }
+#pragma unroll 2
+        for (int k = i0 + RB - 1; k < j0; ++k) {
+          const T* tb = Tb + k * NB + c0;
+          T tv[4];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) tv[t] = tb[t];
+#pragma unroll
+          for (int a = 0; a < RB; ++a) {
+            const T x = xr[a][k];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) acc[a][t] = S::add(acc[a][t], S::mul(x, tv[t]));
           }
         }
 #pragma unroll
-        for (int a = 0; a < RA; ++a) {
-          const int i = ib + half + 2 * a;
-          if (i < j0 && c < nb) at(i, j0 + c) = S::scale(acc[a], -1.0);
+        for (int a = 0; a < RB; ++a) {
+          if (i0 + a < j0) {
+            T* row = W + poff(n, i0 + a) - (i0 + a) + j0;
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+              if (c0 + t < nb) row[c0 + t] = S::scale(acc[a][t], -1.0);
+          }
         }
       }
       __syncthreads();

@@ -170,7 +170,11 @@ gemm_f64_tma_kernel(const __grid_constant__ CUtensorMap mapA,
     }
     // every consumer thread releases the stage itself: an arrive by lane 0
     // after __syncwarp let the TMA overwrite a stage while loads of other lanes
-    // were still reading it (intermittent wrong rows, tools/flaky_probe.py)
+    // were still reading it (intermittent wrong rows, tools/flaky_probe.py).
+    // The release must also order this thread's own shared loads (generic
+    // proxy, possibly still in flight: the arrive does not depend on them)
+    // before the TMA refill (async proxy): proxy fence first.
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     bar_arrive(&empty[s]);
   }
 
