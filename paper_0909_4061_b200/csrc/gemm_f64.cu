@@ -369,6 +369,10 @@ void gemm_f64(Handle* h, bool transA, int64_t M, int64_t N, int64_t K, const dou
       LR_CUDA(cudaMemsetAsync(C + r * ldc, 0, N * sizeof(double), h->stream));
     return;
   }
+  if (gemm_skinny_ok(transA, M, N, K)) {
+    gemm_skinny_tn(h, M, N, K, A, lda, B, ldb, C, ldc);
+    return;
+  }
   if (gemm_f64_tma_ok(M, N, K, A, lda, B, ldb) && gemm_f64_tma_pick(transA, N, K)) {
     gemm_f64_tma(h, transA, M, N, K, A, lda, B, ldb, C, ldc);
     return;

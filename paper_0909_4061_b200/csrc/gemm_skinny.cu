@@ -1,0 +1,155 @@
+// C (M x N) = A^T B for tall, narrow fp64 panels: K >> M, N <= 64 -- the
+// Grams of an m x ell panel with ell <= 64 and the R^T X / L^T Y products of
+// config 5's implicit low-rank term (reference: the DenseOperator products
+// of core.py:391-395 and the Gram inside orthonormalize_double_gs' role,
+// core.py:84-115).
+//
+// The 128-row tiles of the pass kernels compute on padding here (M = 32 or
+// 48 of 128 rows: 62-75 % of the DMMA work wasted, 1.05 ms for a 2^21 x 48
+// Gram, ncu launch list of config 5).  This kernel gives every warp a run of
+// rows of A and B: per 4 rows it loads its m16n8k4 fragments straight from
+// global memory (8 consecutive doubles per fragment row, several k-steps in
+// flight) and issues MF x NF8 DMMAs on exactly the M x N output; the 8 warp
+// partials are summed in shared memory in a fixed order, one partial per CTA
+// goes to the split-K buffer, and splitk_reduce sums the CTAs in a fixed
+// order (deterministic).  Bound: HBM (K (M + N) 8 bytes) or the DMMA pipe on
+// M x N x K useful FMAs, whichever is larger.
+#include "common.cuh"
+
+namespace lr {
+namespace {
+
+constexpr int SK_THREADS = 256;
+constexpr int SK_WARPS = SK_THREADS / 32;
+// k4 steps with loads in flight: as many as the register file allows
+// (accumulators MF x NF8 x 4 doubles + U x (2 MF + NF8) operands)
+template <int MF, int NF8>
+__host__ __device__ constexpr int sk_unroll() { return MF * NF8 <= 12 ? 4 : 2; }
+
+__device__ __forceinline__ void dmma_sk(double (&c)[4], double a0, double a1, double b0) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
+      "{%0,%1,%2,%3};\n"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a0), "d"(a1), "d"(b0));
+}
+
+// grid.x = CTAs, each owns rows [blockIdx.x * rows_per, ...) of A and B
+template <int MF, int NF8>
+__global__ void __launch_bounds__(SK_THREADS)
+skinny_tn_kernel(int64_t M, int64_t N, int64_t K, const double* __restrict__ A, int64_t lda,
+                 const double* __restrict__ B, int64_t ldb, double* __restrict__ part,
+                 int64_t rows_per) {
+  __shared__ double red[MF * 16][NF8 * 8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int64_t r0 = int64_t(blockIdx.x) * rows_per;
+  const int64_t r1 = min(K, r0 + rows_per);
+  double acc[MF][NF8][4];
+#pragma unroll
+  for (int i = 0; i < MF; ++i)
+#pragma unroll
+    for (int j = 0; j < NF8; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[i][j][e] = 0.0;
+
+  constexpr int SK_UNROLL = sk_unroll<MF, NF8>();
+  // warp w takes k4-steps w, w + 8, ... of the CTA's rows, SK_UNROLL at a time
+  const int64_t nsteps = (r1 - r0 + 3) / 4;
+  for (int64_t s0 = int64_t(warp) * SK_UNROLL; s0 < nsteps; s0 += int64_t(SK_WARPS) * SK_UNROLL) {
+    double a[SK_UNROLL][MF][2], b[SK_UNROLL][NF8];
+#pragma unroll
+    for (int u = 0; u < SK_UNROLL; ++u) {
+      const int64_t k = r0 + (s0 + u) * 4 + t;
+      const bool kin = (s0 + u) < nsteps && k < r1;
+      const double* ar = A + k * lda;
+      const double* br = B + k * ldb;
+#pragma unroll
+      for (int mf = 0; mf < MF; ++mf) {
+        const int i0 = mf * 16 + g, i1 = i0 + 8;
+        a[u][mf][0] = (kin && i0 < M) ? __ldg(ar + i0) : 0.0;
+        a[u][mf][1] = (kin && i1 < M) ? __ldg(ar + i1) : 0.0;
+      }
+#pragma unroll
+      for (int nf = 0; nf < NF8; ++nf) {
+        const int j = nf * 8 + g;
+        b[u][nf] = (kin && j < N) ? __ldg(br + j) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < SK_UNROLL; ++u)
+#pragma unroll
+      for (int nf = 0; nf < NF8; ++nf)
+#pragma unroll
+        for (int mf = 0; mf < MF; ++mf) dmma_sk(acc[mf][nf], a[u][mf][0], a[u][mf][1], b[u][nf]);
+  }
+  // accumulator layout (m16n8 fp64): c0,c1 at (g, 2t..2t+1), c2,c3 at (g+8, 2t..2t+1);
+  // warps add their partials in a fixed order (deterministic)
+  for (int w = 0; w < SK_WARPS; ++w) {
+    if (warp == w) {
+#pragma unroll
+      for (int mf = 0; mf < MF; ++mf)
+#pragma unroll
+        for (int nf = 0; nf < NF8; ++nf) {
+          const int i = mf * 16 + g, j = nf * 8 + 2 * t;
+          if (w == 0) {
+            red[i][j] = acc[mf][nf][0];
+            red[i][j + 1] = acc[mf][nf][1];
+            red[i + 8][j] = acc[mf][nf][2];
+            red[i + 8][j + 1] = acc[mf][nf][3];
+          } else {
+            red[i][j] += acc[mf][nf][0];
+            red[i][j + 1] += acc[mf][nf][1];
+            red[i + 8][j] += acc[mf][nf][2];
+            red[i + 8][j + 1] += acc[mf][nf][3];
+          }
+        }
+    }
+    __syncthreads();
+  }
+  double* out = part + int64_t(blockIdx.x) * M * N;
+  for (int e = threadIdx.x; e < M * N; e += SK_THREADS) {
+    const int i = e / int(N), j = e - i * int(N);
+    out[e] = red[i][j];
+  }
+}
+
+template <int MF, int NF8>
+void launch_skinny(Handle* h, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
+                   const double* B, int64_t ldb, double* C, int64_t ldc) {
+  // one CTA per SM (up to 232 registers per thread), each a run of >= 1024 rows
+  int64_t ctas = std::min<int64_t>(h->sm_count, std::max<int64_t>(1, K / 1024));
+  const int64_t rows_per = ((ceil_div(K, ctas) + 3) / 4) * 4;
+  ctas = ceil_div(K, rows_per);
+  double* part = pool_alloc_t<double>(h, size_t(ctas) * M * N);
+  skinny_tn_kernel<MF, NF8><<<unsigned(ctas), SK_THREADS, 0, h->stream>>>(M, N, K, A, lda, B, ldb,
+                                                                          part, rows_per);
+  LR_CHECK_LAUNCH();
+  splitk_reduce(h, M, N, int(ctas), part, C, ldc);
+}
+
+}  // namespace
+
+// LR_SKINNY=0 disables (A/B against the tiled DMMA kernels)
+bool gemm_skinny_ok(bool transA, int64_t M, int64_t N, int64_t K) {
+  static int off = -1;
+  if (off < 0) {
+    const char* e = getenv("LR_SKINNY");
+    off = (e && e[0] == '0') ? 1 : 0;
+  }
+  return !off && transA && ceil_div(M, 16) * ceil_div(N, 8) <= 18 && M <= 48 && N <= 64 &&
+         K >= 16384;
+}
+
+void gemm_skinny_tn(Handle* h, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
+                    const double* B, int64_t ldb, double* C, int64_t ldc) {
+  const int mf = int(ceil_div(M, 16)), nf = int(ceil_div(N, 8));
+  // instantiate the shapes the configurations use; round up the others
+  if (mf <= 1 && nf <= 2) launch_skinny<1, 2>(h, M, N, K, A, lda, B, ldb, C, ldc);
+  else if (mf <= 2 && nf <= 4) launch_skinny<2, 4>(h, M, N, K, A, lda, B, ldb, C, ldc);
+  else if (mf <= 2 && nf <= 6) launch_skinny<2, 6>(h, M, N, K, A, lda, B, ldb, C, ldc);
+  else if (mf <= 3 && nf <= 6) launch_skinny<3, 6>(h, M, N, K, A, lda, B, ldb, C, ldc);
+  else launch_skinny<2, 8>(h, M, N, K, A, lda, B, ldb, C, ldc);   // M <= 32, N <= 64
+}
+
+}  // namespace lr

@@ -440,3 +440,25 @@ def test_passes_deterministic(dtype):
     Qs = [m.randomized_range_finder(A, 40, seed=3).Q for _ in range(6)]
     for Q in Qs[1:]:
         assert np.array_equal(Q, Qs[0])
+
+
+@pytest.mark.parametrize("M,N,K", [(32, 48, 2 ** 18), (48, 48, 20000), (10, 30, 16384),
+                                   (30, 30, 70001), (32, 64, 40000), (1, 1, 16384)])
+def test_skinny_tn(M, N, K):
+    """A^T B with K >> M, N (the Grams of narrow panels and config 5's R^T X):
+    the skinny kernel against numpy, and symmetric when A is B."""
+    from paper_0909_4061_b200 import _lib
+    g = np.random.default_rng(M * N + K)
+    A = torch.from_numpy(g.standard_normal((K, M))).cuda()
+    B = torch.from_numpy(g.standard_normal((K, N))).cuda()
+    C = torch.empty((M, N), dtype=torch.float64, device="cuda")
+    _lib.call("lr_gemm", _lib.handle(), _lib.F64, _lib.OP_T, K, M, N, _lib.ptr(A), _lib.ld(A),
+              _lib.ptr(B), _lib.ld(B), _lib.ptr(C), _lib.ld(C))
+    ref = A.cpu().numpy().T @ B.cpu().numpy()
+    assert np.abs(C.cpu().numpy() - ref).max() <= 1e-12 * np.sqrt(K) * 4
+    G = torch.empty((M, M), dtype=torch.float64, device="cuda")
+    _lib.call("lr_gemm", _lib.handle(), _lib.F64, _lib.OP_T, K, M, M, _lib.ptr(A), _lib.ld(A),
+              _lib.ptr(A), _lib.ld(A), _lib.ptr(G), _lib.ld(G))
+    Gh = G.cpu().numpy()
+    assert np.array_equal(Gh, Gh.T) or np.abs(Gh - Gh.T).max() <= 1e-12 * np.abs(Gh).max()
+    assert np.abs(Gh - A.cpu().numpy().T @ A.cpu().numpy()).max() <= 1e-12 * np.sqrt(K) * 4
