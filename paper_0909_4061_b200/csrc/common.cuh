@@ -140,6 +140,10 @@ void splitk_reduce(Handle* h, int64_t M, int64_t N, int S, const double* part, d
 bool gemm_skinny_ok(bool transA, int64_t M, int64_t N, int64_t K);
 void gemm_skinny_tn(Handle* h, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
                     const double* B, int64_t ldb, double* C, int64_t ldc);
+bool gemm_skinny_nn_ok(bool transA, int64_t M, int64_t N, int64_t K, const double* C,
+                       int64_t ldc);
+void gemm_skinny_nn(Handle* h, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
+                    const double* B, int64_t ldb, double* C, int64_t ldc);
 bool gemm_f64_tma_ok(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
                      const double* B, int64_t ldb);
 bool gemm_f64_tma_pick(bool transA, int64_t N, int64_t K);

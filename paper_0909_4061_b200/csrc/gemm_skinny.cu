@@ -128,6 +128,83 @@ void launch_skinny(Handle* h, int64_t M, int64_t N, int64_t K, const double* A, 
   splitk_reduce(h, M, N, int(ctas), part, C, ldc);
 }
 
+// C (M x N) = A (M x K) B (K x N) for M >> K, N <= 64 (the applies Y P of a
+// narrow panel and config 5's L Z): B staged in shared memory once per CTA,
+// every warp streams 16-row tiles of A (fragments straight from global),
+// K/4 x NF8 DMMAs per tile, 16-byte stores of the accumulator pairs.
+template <int NF8, int KS>   // KS = k4 steps (K <= 4 KS)
+__global__ void __launch_bounds__(SK_THREADS)
+skinny_nn_kernel(int64_t M, int64_t N, int64_t K, const double* __restrict__ A, int64_t lda,
+                 const double* __restrict__ B, int64_t ldb, double* __restrict__ C,
+                 int64_t ldc) {
+  __shared__ double bs[4 * KS][NF8 * 8 + 1];
+  for (int e = threadIdx.x; e < 4 * KS * NF8 * 8; e += SK_THREADS) {
+    const int k = e / (NF8 * 8), j = e - k * (NF8 * 8);
+    bs[k][j] = (k < K && j < N) ? B[int64_t(k) * ldb + j] : 0.0;
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int64_t ntiles = (M + 15) / 16;
+  const int64_t stride = int64_t(gridDim.x) * SK_WARPS;
+  // software pipeline: the next tile's A fragments are in flight while the
+  // current tile's DMMAs and stores run (the loop is latency-bound otherwise)
+  auto load = [&](int64_t tile, double (&a)[KS][2]) {
+    const int64_t r0 = tile * 16 + g, r1 = r0 + 8;
+    const double* a0p = A + r0 * lda;
+    const double* a1p = A + r1 * lda;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const int k = 4 * ks + t;
+      a[ks][0] = (tile < ntiles && r0 < M && k < K) ? __ldg(a0p + k) : 0.0;
+      a[ks][1] = (tile < ntiles && r1 < M && k < K) ? __ldg(a1p + k) : 0.0;
+    }
+  };
+  int64_t tile = int64_t(blockIdx.x) * SK_WARPS + warp;
+  double a[KS][2], an[KS][2];
+  load(tile, a);
+  for (; tile < ntiles; tile += stride) {
+    load(tile + stride, an);
+    const int64_t r0 = tile * 16 + g, r1 = r0 + 8;
+    double acc[NF8][4];
+#pragma unroll
+    for (int nf = 0; nf < NF8; ++nf)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[nf][e] = 0.0;
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+      for (int nf = 0; nf < NF8; ++nf)
+        dmma_sk(acc[nf], a[ks][0], a[ks][1], bs[4 * ks + t][nf * 8 + g]);
+#pragma unroll
+    for (int nf = 0; nf < NF8; ++nf) {
+      const int64_t j = nf * 8 + 2 * t;
+      if (j + 1 < N) {
+        if (r0 < M) *reinterpret_cast<double2*>(C + r0 * ldc + j) = make_double2(acc[nf][0], acc[nf][1]);
+        if (r1 < M) *reinterpret_cast<double2*>(C + r1 * ldc + j) = make_double2(acc[nf][2], acc[nf][3]);
+      } else if (j < N) {
+        if (r0 < M) C[r0 * ldc + j] = acc[nf][0];
+        if (r1 < M) C[r1 * ldc + j] = acc[nf][2];
+      }
+    }
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      a[ks][0] = an[ks][0];
+      a[ks][1] = an[ks][1];
+    }
+  }
+}
+
+template <int NF8, int KS>
+void launch_skinny_nn(Handle* h, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
+                      const double* B, int64_t ldb, double* C, int64_t ldc) {
+  const int64_t ntiles = ceil_div(M, 16);
+  const int64_t ctas = std::min<int64_t>(4 * h->sm_count, ceil_div(ntiles, SK_WARPS));
+  skinny_nn_kernel<NF8, KS><<<unsigned(ctas), SK_THREADS, 0, h->stream>>>(M, N, K, A, lda, B, ldb,
+                                                                          C, ldc);
+  LR_CHECK_LAUNCH();
+}
+
 }  // namespace
 
 // LR_SKINNY=0 disables (A/B against the tiled DMMA kernels)
@@ -150,6 +227,32 @@ void gemm_skinny_tn(Handle* h, int64_t M, int64_t N, int64_t K, const double* A,
   else if (mf <= 2 && nf <= 6) launch_skinny<2, 6>(h, M, N, K, A, lda, B, ldb, C, ldc);
   else if (mf <= 3 && nf <= 6) launch_skinny<3, 6>(h, M, N, K, A, lda, B, ldb, C, ldc);
   else launch_skinny<2, 8>(h, M, N, K, A, lda, B, ldb, C, ldc);   // M <= 32, N <= 64
+}
+
+}  // namespace lr
+
+namespace lr {
+
+// M >> K, N: 16-byte aligned C rows for the paired stores
+bool gemm_skinny_nn_ok(bool transA, int64_t M, int64_t N, int64_t K, const double* C,
+                       int64_t ldc) {
+  static int off = -1;
+  if (off < 0) {
+    const char* e = getenv("LR_SKINNY");
+    off = (e && e[0] == '0') ? 1 : 0;
+  }
+  // measured (config 5 launch lists): 328 vs 394 us at K = 32, but 453 vs 394
+  // at K = 48 where the tiled kernel's larger warp tile wins -- K <= 32 only
+  return !off && !transA && K <= 32 && N <= 64 && M >= 65536 && (ldc % 2) == 0 &&
+         (reinterpret_cast<uintptr_t>(C) & 15) == 0;
+}
+
+void gemm_skinny_nn(Handle* h, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
+                    const double* B, int64_t ldb, double* C, int64_t ldc) {
+  const int nf = int(ceil_div(N, 8));
+  if (nf <= 4) launch_skinny_nn<4, 8>(h, M, N, K, A, lda, B, ldb, C, ldc);
+  else if (nf <= 6) launch_skinny_nn<6, 8>(h, M, N, K, A, lda, B, ldb, C, ldc);
+  else launch_skinny_nn<8, 8>(h, M, N, K, A, lda, B, ldb, C, ldc);
 }
 
 }  // namespace lr

@@ -462,3 +462,19 @@ def test_skinny_tn(M, N, K):
     Gh = G.cpu().numpy()
     assert np.array_equal(Gh, Gh.T) or np.abs(Gh - Gh.T).max() <= 1e-12 * np.abs(Gh).max()
     assert np.abs(Gh - A.cpu().numpy().T @ A.cpu().numpy()).max() <= 1e-12 * np.sqrt(K) * 4
+
+
+@pytest.mark.parametrize("M,N,K", [(2 ** 18, 48, 32), (100003, 48, 48), (70000, 30, 30),
+                                   (65536, 64, 32), (65537, 1, 1), (131072, 10, 20)])
+def test_skinny_nn(M, N, K):
+    """A B with M >> K, N (the applies Y P of narrow panels, config 5's L Z):
+    the skinny NN kernel against numpy, including ragged last tiles."""
+    from paper_0909_4061_b200 import _lib
+    g = np.random.default_rng(M + N + K)
+    A = torch.from_numpy(g.standard_normal((M, K))).cuda()
+    B = torch.from_numpy(g.standard_normal((K, N))).cuda()
+    C = torch.empty((M, N + (N % 2)), dtype=torch.float64, device="cuda")[:, :N]
+    _lib.call("lr_gemm", _lib.handle(), _lib.F64, _lib.OP_N, M, K, N, _lib.ptr(A), _lib.ld(A),
+              _lib.ptr(B), _lib.ld(B), _lib.ptr(C), _lib.ld(C))
+    ref = A.cpu().numpy() @ B.cpu().numpy()
+    assert np.abs(C.cpu().numpy() - ref).max() <= 1e-13 * K
