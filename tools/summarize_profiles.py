@@ -68,15 +68,17 @@ def main(src, tag):
         cfg = os.path.basename(lf)[len("launches_"):-4]
         shutil.copy(lf, os.path.join(prof, f"{tag}_{cfg}_launches.csv"))
         bj = os.path.join(src, f"bench_{cfg}.json")
+        steps = 2
         if os.path.exists(bj):
             txt = open(bj).read().strip().splitlines()
             if txt:
                 b = json.loads(txt[-1])
+                steps = int(b.get("steps", 2))
                 lines += [f"## {cfg}: {b['config']['workload']}", "",
-                          f"bench (2 steps, no ncu): {b['ms_per_step']} ms/step, "
+                          f"bench ({steps} steps, no ncu): {b['ms_per_step']} ms/step, "
                           f"{b['value']} {b['unit']}; roofline kernel frac "
                           f"{b['roofline']['frac']}", ""]
-        lines += ["```", summarize(lf, 2), "```", ""]
+        lines += ["```", summarize(lf, steps), "```", ""]
         for kind in ("pass", "small"):
             rep = os.path.join(src, f"full_{cfg}_{kind}.ncu-rep")
             if not os.path.exists(rep):
@@ -96,8 +98,12 @@ def main(src, tag):
                     f"{d.get('sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active', 0):.1f} |")
             lines.append("")
             if kind == "pass" and ms:
+                # the pass launches proper (a capture may include shorter
+                # products of the same kernel, e.g. cfg4's Y P applies)
+                tmax = max(d.get("gpu__time_duration.sum", 0) for d in ms)
+                big = [d for d in ms if d.get("gpu__time_duration.sum", 0) >= 0.5 * tmax]
                 tb = [d.get("dram__bytes_read.sum", 0) + d.get("dram__bytes_write.sum", 0)
-                      for d in ms]
+                      for d in big]
                 traffic[cfg] = int(sum(tb) / len(tb))
     json.dump(traffic, open(traffic_path, "w"), indent=1)
     open(os.path.join(prof, f"{tag}_summary.md"), "w").write("\n".join(lines) + "\n")
