@@ -117,6 +117,24 @@ struct Pairs {
     return (c == P0 || c == Q0) ? 0 : (c == P1 || c == Q1) ? 1 : (c == P2 || c == Q2) ? 2 : 3;
   }
   __device__ static constexpr bool first(int c) { return c == P0 || c == P1 || c == P2 || c == P3; }
+  // lane-dependent lookups as shifts of compile-time packed tables (the
+  // select chains of p()/q()/of() on runtime indices cost ~10% of a subround)
+  static constexpr unsigned PT = unsigned(P0) | unsigned(P1) << 4 | unsigned(P2) << 8 | unsigned(P3) << 12;
+  static constexpr unsigned QT = unsigned(Q0) | unsigned(Q1) << 4 | unsigned(Q2) << 8 | unsigned(Q3) << 12;
+  __device__ static constexpr unsigned of_tab() {
+    unsigned t = 0;
+    for (int c = 0; c < 8; ++c) t |= unsigned(of(c)) << (2 * c);
+    return t;
+  }
+  __device__ static constexpr unsigned first_tab() {
+    unsigned t = 0;
+    for (int c = 0; c < 8; ++c) t |= (first(c) ? 1u : 0u) << c;
+    return t;
+  }
+  __device__ static __forceinline__ int p_rt(int k) { return int((PT >> (4 * k)) & 15u); }
+  __device__ static __forceinline__ int q_rt(int k) { return int((QT >> (4 * k)) & 15u); }
+  __device__ static __forceinline__ int of_rt(int c) { return int((of_tab() >> (2 * c)) & 3u); }
+  __device__ static __forceinline__ bool first_rt(int c) { return (first_tab() >> c) & 1u; }
 };
 
 template <typename T, int R, int P0, int Q0, int P1, int Q1, int P2, int Q2, int P3, int Q3>
@@ -142,8 +160,8 @@ __device__ __forceinline__ void subround(T (&x)[WC][R], double& nrmv, int lane, 
   v = S::add(v, S::shfl_xor(v, 2));
   v = S::add(v, S::shfl_xor(v, 1));
   const int kk = (lane >> 3) & 3;   // = 2 b4 + b3: the pair whose sum this lane holds
-  const double a = __shfl_sync(0xffffffffu, nrmv, PR::p(kk));
-  const double b = __shfl_sync(0xffffffffu, nrmv, PR::q(kk));
+  const double a = __shfl_sync(0xffffffffu, nrmv, PR::p_rt(kk));
+  const double b = __shfl_sync(0xffffffffu, nrmv, PR::q_rt(kk));
   double c, tg;
   T se;
   const bool rot = rot_params(a, b, v, tol, c, se, tg);
@@ -165,10 +183,10 @@ __device__ __forceinline__ void subround(T (&x)[WC][R], double& nrmv, int lane, 
   }
   // new norms: lane c < WC fetches its column's from lane 8 * pair(c)
   const int lc = lane & (WC - 1);
-  const int src = 8 * PR::of(lc);
+  const int src = 8 * PR::of_rt(lc);
   const double na = __shfl_sync(0xffffffffu, an, src);
   const double nb = __shfl_sync(0xffffffffu, bn, src);
-  if (lane < WC) nrmv = PR::first(lc) ? na : nb;
+  if (lane < WC) nrmv = PR::first_rt(lc) ? na : nb;
   // cancellation guard (rare, warp-uniform)
   const unsigned need = __ballot_sync(0xffffffffu, (lane & 7) == 0 && rot && an < 0.1 * a);
   if (need) {
