@@ -104,12 +104,41 @@ def cast_dev(t, dtype):
     return out.reshape(-1) if vec else out
 
 
+def _stage_host(t):
+    """Enqueue the D2H copy of a device tensor into a pinned host buffer
+    (torch's caching host allocator: repeated calls reuse the blocks) on the
+    current stream; the caller synchronizes once for a batch.  A pageable
+    .cpu() runs at a third of the link rate and page-faults a fresh buffer
+    every call (13.6 ms for config 2's four factors vs 0.7 ms pinned)."""
+    torch = _torch()
+    t = t.detach()
+    if not t.is_cuda:
+        return t
+    h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    if t.numel():
+        h.copy_(t, non_blocking=True)
+    return h
+
+
 def to_host(t):
-    return t.detach().cpu().numpy()
+    return to_hosts(t)[0]
+
+
+def to_hosts(*ts):
+    """Several device tensors -> numpy arrays with one synchronization."""
+    torch = _torch()
+    hs = [_stage_host(t) for t in ts]
+    if any(t.is_cuda for t in ts):
+        torch.cuda.current_stream().synchronize()
+    return [h.numpy() for h in hs]
 
 
 def _out(t, host):
     return to_host(t) if host else t
+
+
+def _outs(host, *ts):
+    return to_hosts(*ts) if host else list(ts)
 
 
 def _as2d(t):
@@ -189,6 +218,12 @@ class DenseOperator(MatVecOperator):
 
     device_native = True
 
+    # pinned host inputs at least this large are uploaded in row chunks on a
+    # copy stream, and the validation and the first pass A*X run chunk by
+    # chunk behind the copy (fp64 / complex128: no max|A| needed up front)
+    STREAM_MIN_BYTES = 256 << 20
+    STREAM_CHUNK_BYTES = 64 << 20
+
     def __init__(self, A, device=None, validate=True):
         torch = _torch()
         host = not is_device_array(A)
@@ -197,14 +232,83 @@ class DenseOperator(MatVecOperator):
             raise ValueError(f"matrix must be 2-D, got shape {shape}")
         if shape[0] == 0 or shape[1] == 0:
             raise ValueError("matrix must be nonempty")
+        self._pending = None
+        self.amax = None
+        self.host_io = host
+        if validate and self._streamable(A):
+            super().__init__(*shape)
+            self._upload_streamed(A, device)
+            if self._array.dtype not in (torch.float64, torch.complex128):
+                self._finalize()       # the scaled passes need max|A| first
+            return
         t = to_device(A, _torch_compute_dtype(A) if torch.is_tensor(A) else None, device)
         super().__init__(*t.shape)
-        self.array = t
+        self._array = t
         self.code = _lib.dtype_code(t.dtype)
-        self.host_io = host
-        self.amax = None
         if validate:
             self.validate()
+
+    @staticmethod
+    def _streamable(A):
+        torch = _torch()
+        return (torch.is_tensor(A) and not A.is_cuda and A.is_pinned() and A.is_contiguous()
+                and A.dtype in (torch.float32, torch.float64, torch.complex64, torch.complex128)
+                and A.numel() * A.element_size() >= DenseOperator.STREAM_MIN_BYTES)
+
+    def _upload_streamed(self, A, device):
+        """H2D in row chunks on a side stream (one event per chunk); the
+        as_matrix check of each chunk is enqueued on the current stream
+        behind its event, into per-chunk slots read by _finalize()."""
+        torch = _torch()
+        dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        t = torch.empty(A.shape, dtype=A.dtype, device=dev)
+        self._array = t
+        self.code = _lib.dtype_code(t.dtype)
+        m, n = A.shape
+        rows = max(128, (self.STREAM_CHUNK_BYTES // (n * A.element_size())) // 128 * 128)
+        bounds = [(r, min(m, r + rows)) for r in range(0, m, rows)]
+        bad = torch.empty(len(bounds), dtype=torch.int64, device=dev)
+        res = torch.empty((len(bounds), 2), dtype=torch.float64, device=dev)
+        cur = torch.cuda.current_stream(dev)
+        side = _copy_stream(dev)
+        side.wait_stream(cur)          # t's allocation is ordered before the copies
+        chunks = []
+        h = _lib.handle(dev.index)
+        for i, (r0, r1) in enumerate(bounds):
+            with torch.cuda.stream(side):
+                t[r0:r1].copy_(A[r0:r1], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(side)
+            cur.wait_event(ev)
+            _lib.call("lr_check_finite", h, self.code, r1 - r0, n, _lib.ptr(t[r0:r1]), n,
+                      _lib.ptr(bad[i:i + 1]), _lib.ptr(res[i]))
+            chunks.append((r0, r1, ev))
+        t.record_stream(side)
+        self._pending = chunks
+        self._checks = (bad, res, A)   # A stays referenced until the copies are done
+
+    def _finalize(self):
+        """Join the upload: the current stream waits for the last chunk, and
+        the deferred as_matrix result is read (one synchronization)."""
+        torch = _torch()
+        chunks, self._pending = self._pending, None
+        torch.cuda.current_stream(self._array.device).wait_event(chunks[-1][2])
+        bad, res, _ = self._checks
+        self._checks = None
+        nb, amax = to_hosts(bad, res[:, 0])
+        if int(nb.sum()):
+            raise ValueError("matrix contains non-finite entries")
+        self.amax = float(amax.max())
+
+    @property
+    def array(self):
+        if self._pending is not None:
+            self._finalize()
+        return self._array
+
+    @property
+    def device(self):
+        return self._array.device
 
     def validate(self):
         torch = _torch()
@@ -219,18 +323,18 @@ class DenseOperator(MatVecOperator):
 
     @property
     def dtype(self):
-        return self.array.dtype
+        return self._array.dtype
 
     def _prep(self, X):
         torch = _torch()
         host = not is_device_array(X)
-        dt = self.array.dtype
-        if not self.array.is_complex() and (np.iscomplexobj(X) if not torch.is_tensor(X)
+        dt = self._array.dtype
+        if not self._array.is_complex() and (np.iscomplexobj(X) if not torch.is_tensor(X)
                                             else X.is_complex()):
             # real A times a complex block (e.g. the complex SRFT basis of a
             # real matrix): keep X complex, the pass runs on its real view
             dt = torch.complex64 if dt == torch.float32 else torch.complex128
-        t = to_device(X, dt, self.array.device.index)
+        t = to_device(X, dt, self._array.device.index)
         t, vec = _as2d(t)
         return t, host, vec
 
@@ -239,6 +343,16 @@ class DenseOperator(MatVecOperator):
         (A^H [Re Im] interleaved == A^H X since A is real)."""
         torch = _torch()
         rows = self.n if adjoint else self.m
+        if self._pending is not None and not adjoint and t.dtype == self._array.dtype:
+            # first pass of a streamed upload: chunk by chunk behind the copy
+            chunks = self._pending
+            Y = torch.empty((rows, t.shape[1]), dtype=self._array.dtype, device=t.device)
+            cur = torch.cuda.current_stream(t.device)
+            for r0, r1, ev in chunks:
+                cur.wait_event(ev)
+                _pass(self._array[r0:r1], t, Y[r0:r1], False, self.amax)
+            self._finalize()
+            return Y
         if t.is_complex() and not self.array.is_complex():
             tc = t.contiguous()
             tr = torch.view_as_real(tc).reshape(tc.shape[0], 2 * tc.shape[1])
@@ -273,6 +387,17 @@ CudaDenseOperator = DenseOperator
 # (start_event, end_event, algorithmic_flops, a_bytes, cols) for every pass
 # over a dense A, recorded on the launching stream.
 PASS_EVENTS = None
+
+
+_COPY_STREAMS = {}
+
+
+def _copy_stream(dev):
+    torch = _torch()
+    st = _COPY_STREAMS.get(dev.index)
+    if st is None:
+        st = _COPY_STREAMS[dev.index] = torch.cuda.Stream(dev)
+    return st
 
 
 def _pass(A, X, Y, adjoint, amax):
@@ -494,7 +619,8 @@ def small_svd(B):
     if t.dim() != 2:
         raise ValueError("B must be 2-D")
     U, S, V = small_svd_dev(t)
-    return SmallSVD(U=_out(U, host), sigma=_out(S, host), V=_out(V, host))
+    U, S, V = _outs(host, U, S, V)
+    return SmallSVD(U=U, sigma=S, V=V)
 
 
 # ---------------------------------------------------------------------------

@@ -381,7 +381,7 @@ def sharded_randomized_svd(A_rows, k, p=config.DEFAULT_OVERSAMPLE, q=0, seed=0, 
     Returns (U_rows, sigma, V, est) -- the same factors as randomized_svd
     (factor.py) on the stacked matrix."""
     import torch
-    from .core import DenseOperator, is_device_array, to_host
+    from .core import DenseOperator, is_device_array, to_hosts
     host = not is_device_array(A_rows)
     comm = Comm(group)
     # upload, finiteness check and local max|A|; the verdict is agreed on by
@@ -404,7 +404,7 @@ def sharded_randomized_svd(A_rows, k, p=config.DEFAULT_OVERSAMPLE, q=0, seed=0, 
                               estimate=estimate, probes=probes, alpha=alpha, truncate=truncate,
                               sketch=sketch)
     if host:
-        return to_host(res.U), to_host(res.sigma), to_host(res.V), res.est
+        return (*to_hosts(res.U, res.sigma, res.V), res.est)
     return res.U, res.sigma, res.V, res.est
 
 

@@ -20,7 +20,7 @@ import numpy as np
 
 from . import config
 from . import _lib
-from .core import (_out, _torch, _wide, apply_dev, as_operator, cast_dev, gemm, gemm_dev,
+from .core import (_out, _outs, _torch, _wide, apply_dev, as_operator, cast_dev, gemm, gemm_dev,
                    is_device_array, small_eig_hermitian_dev, small_svd_from_adjoint, speculate,
                    to_device)
 from .rangefinder import (RangeBasis, SketchSpec, _cast_like_op, _check_ell, _host_io,
@@ -69,7 +69,8 @@ def direct_svd(A, Q):
     dt = getattr(op, "dtype", None)
     Qd = to_device(Q, dt if op.device_native else None)
     U, S, V = direct_svd_dev(op, Qd)
-    return PartialSVD(U=_out(U, host), sigma=_out(S, host), V=_out(V, host))
+    U, S, V = _outs(host, U, S, V)
+    return PartialSVD(U=U, sigma=S, V=V)
 
 
 @dataclass
@@ -304,9 +305,9 @@ def randomized_svd(A, k, p=config.DEFAULT_OVERSAMPLE, q=0, seed=0, sketch="gauss
     if truncate:
         kk = min(int(k), U.shape[1])
         U, S, V = U[:, :kk], S[:kk], V[:, :kk]
-    basis = RangeBasis(Q=_out(Q, host), samples_used=ell, passes=passes, est_error=est,
-                       spec=spec)
-    return basis, PartialSVD(U=_out(U, host), sigma=_out(S, host), V=_out(V, host)), est
+    Q, U, S, V = _outs(host, Q, U, S, V)
+    basis = RangeBasis(Q=Q, samples_used=ell, passes=passes, est_error=est, spec=spec)
+    return basis, PartialSVD(U=U, sigma=S, V=V), est
 
 
 # ---------------------------------------------------------------------------
@@ -326,7 +327,10 @@ def _graph_enabled():
 def _run_step(op, body, key):
     torch = _torch()
     counters = _snapshot(op)
-    dense = getattr(op, "device_native", False) and hasattr(op, "array")
+    # a streamed upload still in flight (_pending) runs eagerly: its first
+    # pass overlaps the copy; touching op.array here would join the upload
+    dense = (getattr(op, "device_native", False) and getattr(op, "_pending", None) is None
+             and hasattr(op, "array"))
     graphable = dense and _graph_enabled() and key[4] == "gaussian"
     if graphable:
         gkey = (id(op), op.array.data_ptr(), tuple(op.array.shape), op.array.dtype,
@@ -343,8 +347,8 @@ def _run_step(op, body, key):
     result = None
     if getattr(op, "device_native", False):
         # speculative pass: no host synchronization until the flags are read
-        dev = op.array.device if hasattr(op, "array") else torch.device(
-            "cuda", torch.cuda.current_device())
+        dev = op.device if isinstance(getattr(op, "device", None), torch.device) else \
+            torch.device("cuda", torch.cuda.current_device())
         status = torch.zeros(1, dtype=torch.int32, device=dev)
         with speculate(status):
             result = body()

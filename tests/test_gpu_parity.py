@@ -247,3 +247,32 @@ def test_gsrft_randomized_svd_vs_oracle():
     _, fo, esto = O.rsvd(A, 20, 10, 0, 7, sketch="gsrft")
     assert np.max(np.abs(f.sigma - fo.sigma) / fo.sigma[0]) <= 1e-10
     assert est == pytest.approx(esto, rel=1e-2)
+
+
+@pytest.mark.parametrize("dtype", ["float64", "complex128", "float32"])
+def test_streamed_host_upload(dtype, monkeypatch):
+    """A pinned host A above DenseOperator.STREAM_MIN_BYTES is uploaded in
+    row chunks with the as_matrix check and (fp64 / complex128) the first
+    pass overlapped: same factors as the device-resident path, numpy out,
+    and a non-finite entry in the last chunk still raises ValueError."""
+    m = lr()
+    monkeypatch.setattr(m.DenseOperator, "STREAM_MIN_BYTES", 1 << 16)
+    monkeypatch.setattr(m.DenseOperator, "STREAM_CHUNK_BYTES", 1 << 15)
+    rng = np.random.default_rng(4)
+    An = rng.standard_normal((1000, 96)) * np.exp(-np.arange(96) / 8.0)
+    if dtype == "complex128":
+        An = An + 1j * rng.standard_normal((1000, 96)) * np.exp(-np.arange(96) / 8.0)
+    An = An.astype(dtype)
+    host = torch.from_numpy(An).pin_memory()
+    op = m.DenseOperator(host)
+    assert (op._pending is not None) == (dtype != "float32")
+    b, f, _ = m.randomized_svd(host, 10, 6, 1, 3, estimate=False)
+    assert isinstance(f.sigma, np.ndarray)
+    bd, fd, _ = m.randomized_svd(host.cuda(), 10, 6, 1, 3, estimate=False)
+    tol = 1e-12 if dtype != "float32" else 1e-5
+    s = fd.sigma.cpu().numpy()
+    assert np.abs(f.sigma - s).max() <= tol * s[0]
+    bad = An.copy()
+    bad[-1, -1] = np.nan
+    with pytest.raises(ValueError):
+        m.randomized_svd(torch.from_numpy(bad).pin_memory(), 10, 6, 1, 3, estimate=False)
