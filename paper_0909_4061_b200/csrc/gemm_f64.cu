@@ -344,7 +344,11 @@ int64_t choose_splits(int sm_count, int64_t tiles, int64_t K) {
   // k-tiles; each extra wave costs a little (split-K partial traffic).  Few
   // tiles (Gram / Q^T Z of a tall panel: one or two tiles) take up to one
   // split per SM.
-  const int64_t max_s = std::max<int64_t>(1, std::min<int64_t>(4096, K / (4 * BK)));
+  // A product of only a few tiles with a short K (the ell x ell x ell
+  // products of the small SVD: one CTA, 24 us at ell = 110) splits down to
+  // 2 k-tiles per CTA.
+  const int64_t min_k = (tiles <= 4 && K < 1024) ? 2 * BK : 4 * BK;
+  const int64_t max_s = std::max<int64_t>(1, std::min<int64_t>(4096, K / min_k));
   int64_t best_s = 1;
   double best = -1.0;
   for (int64_t s = 1; s <= max_s; ++s) {

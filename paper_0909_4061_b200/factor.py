@@ -26,7 +26,7 @@ from .core import (_out, _outs, _torch, _wide, apply_dev, as_operator, cast_dev,
 from .rangefinder import (RangeBasis, SketchSpec, _cast_like_op, _check_ell, _host_io,
                           _sketch_dev, orth_dev, posterior_error_estimate_dev, probes_dev,
                           subspace_iteration_range_dev)
-from .sketch import gsrft_dev, gsrft_operator, srft_dev, srft_operator
+from .sketch import cached_operator, gsrft_dev, srft_dev
 
 
 @dataclass
@@ -278,8 +278,7 @@ def randomized_svd(A, k, p=config.DEFAULT_OVERSAMPLE, q=0, seed=0, sketch="gauss
 
     # SRFT draws (d, picks) come from the host Philox stream (permutation is
     # sequential); Gaussian Omega / probes are drawn on the device in body().
-    srft = (srft_operator(op.n, ell, seed) if spec.kind == "srft" else
-            gsrft_operator(op.n, ell, seed) if spec.kind == "gsrft" else None)
+    srft = cached_operator(spec.kind, op.n, ell, seed) if spec.kind in ("srft", "gsrft") else None
 
     def body():
         W = probes_dev(op, probes, seed + 13) if estimate else None
@@ -331,7 +330,7 @@ def _run_step(op, body, key):
     # pass overlaps the copy; touching op.array here would join the upload
     dense = (getattr(op, "device_native", False) and getattr(op, "_pending", None) is None
              and hasattr(op, "array"))
-    graphable = dense and _graph_enabled() and key[4] == "gaussian"
+    graphable = dense and _graph_enabled() and key[4] in ("gaussian", "srft", "gsrft")
     if graphable:
         gkey = (id(op), op.array.data_ptr(), tuple(op.array.shape), op.array.dtype,
                 getattr(op, "amax", None), torch.cuda.current_device()) + tuple(key)

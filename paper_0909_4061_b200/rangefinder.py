@@ -20,8 +20,7 @@ import numpy as np
 from . import _lib, config
 from .core import (MatVecOperator, _out, _torch, apply_dev, as_operator, cast_dev, gemm,
                    is_device_array, orth_dev, to_device)
-from .sketch import (SketchSpec, gaussian_dev, gsrft_dev, gsrft_operator, srft_dev,
-                     srft_operator)
+from .sketch import SketchSpec, cached_operator, gaussian_dev, gsrft_dev, srft_dev
 
 _STREAM_PROBE = 0x70726F62
 
@@ -183,9 +182,9 @@ def fast_range_finder(A, ell, seed, kind="srft", ortho_tol=config.GS_DROP_TOL):
         amax = None
     spec = SketchSpec(kind=kind, ell=ell, seed=seed)
     if kind == "srft":
-        Y = srft_dev(t, srft_operator(t.shape[1], ell, seed), amax=amax)
+        Y = srft_dev(t, cached_operator("srft", t.shape[1], ell, seed), amax=amax)
     else:
-        Y = gsrft_dev(t, gsrft_operator(t.shape[1], ell, seed), amax=amax)
+        Y = gsrft_dev(t, cached_operator("gsrft", t.shape[1], ell, seed), amax=amax)
     diagnostics = {}
     if not t.is_complex():
         out = torch.empty(1, dtype=torch.float64, device=Y.device)

@@ -142,6 +142,34 @@ def _complex_of(t):
     return torch.complex128
 
 
+def _device_cached(op, key, make):
+    """Device copies derived from a (host-drawn) sketch operator, kept on the
+    operator object: a repeated randomized SVD with the same draw uploads
+    nothing, so its step has no host->device copy (which would synchronize
+    the stream) and can be captured as a CUDA graph."""
+    cache = op.__dict__.setdefault("_dev_cache", {})
+    val = cache.get(key)
+    if val is None:
+        val = cache[key] = make()
+    return val
+
+
+_OPERATORS = {}
+
+
+def cached_operator(kind, n, ell, seed):
+    """srft_operator / gsrft_operator(n, ell, seed), memoized (the draws are
+    a pure function of the arguments; bounded cache)."""
+    key = (kind, int(n), int(ell), int(seed))
+    op = _OPERATORS.get(key)
+    if op is None:
+        op = (srft_operator if kind == "srft" else gsrft_operator)(n, ell, seed)
+        if len(_OPERATORS) >= 16:
+            _OPERATORS.pop(next(iter(_OPERATORS)))
+        _OPERATORS[key] = op
+    return op
+
+
 def srft_dev(A, op, amax=None):
     """Y = scale * dft(A o d)[:, picks] for a device matrix A (K5).  amax:
     max |A| when known (DenseOperator.amax) -- complex64 runs as one
@@ -156,8 +184,9 @@ def srft_dev(A, op, amax=None):
         _lib.call("lr_copy", h, _lib.dtype_code(A.dtype), _lib.ptr(A), _lib.ld(A), code,
                   _lib.ptr(Ac), _lib.ld(Ac), m, n, 0)
         A = Ac
-    d = torch.from_numpy(np.ascontiguousarray(op.d)).to(device=A.device, dtype=cdt)
-    picks = torch.from_numpy(np.ascontiguousarray(op.picks, dtype=np.int32)).to(A.device)
+    d, picks = _device_cached(op, ("srft", cdt, A.device.index), lambda: (
+        torch.from_numpy(np.ascontiguousarray(op.d)).to(device=A.device, dtype=cdt),
+        torch.from_numpy(np.ascontiguousarray(op.picks, dtype=np.int32)).to(A.device)))
     Y = torch.empty((m, op.ell), dtype=cdt, device=A.device)
     _lib.call("lr_srft_scaled", h, code, m, n, op.ell, _lib.ptr(A), _lib.ld(A),
               float(-1.0 if amax is None else amax), _lib.ptr(d), _lib.ptr(picks),
@@ -280,7 +309,8 @@ def gsrft_dev(A, op, amax=None):
         _lib.call("lr_copy", _lib.handle(A.device.index), _lib.dtype_code(A.dtype), _lib.ptr(A),
                   _lib.ld(A), _lib.dtype_code(cdt), _lib.ptr(Ac), _lib.ld(Ac), m, n, 0)
         A = Ac
-    X = gsrft_matrix_dev(op, cdt, A.device.index)
+    X = _device_cached(op, ("gsrft", cdt, A.device.index),
+                       lambda: gsrft_matrix_dev(op, cdt, A.device.index))
     Y = torch.empty((m, op.ell), dtype=cdt, device=A.device)
     _pass(A, X, Y, False, amax)
     return Y
