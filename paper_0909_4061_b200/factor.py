@@ -323,17 +323,28 @@ def _graph_enabled():
     return os.environ.get("LR_GRAPH", "1") != "0"
 
 
+def _graph_key(op):
+    """Identity of a device operator's data for the CUDA-graph cache, or None
+    when its steps must run eagerly (host operators; a streamed upload still
+    in flight, whose first pass overlaps the copy -- touching op.array
+    would join the upload)."""
+    if not getattr(op, "device_native", False) or getattr(op, "_pending", None) is not None:
+        return None
+    if hasattr(op, "graph_key"):
+        return tuple(op.graph_key())
+    if hasattr(op, "array"):
+        a = op.array
+        return (a.data_ptr(), tuple(a.shape), a.dtype, getattr(op, "amax", None))
+    return None
+
+
 def _run_step(op, body, key):
     torch = _torch()
     counters = _snapshot(op)
-    # a streamed upload still in flight (_pending) runs eagerly: its first
-    # pass overlaps the copy; touching op.array here would join the upload
-    dense = (getattr(op, "device_native", False) and getattr(op, "_pending", None) is None
-             and hasattr(op, "array"))
-    graphable = dense and _graph_enabled() and key[4] in ("gaussian", "srft", "gsrft")
+    gk = _graph_key(op)
+    graphable = gk is not None and _graph_enabled() and key[4] in ("gaussian", "srft", "gsrft")
     if graphable:
-        gkey = (id(op), op.array.data_ptr(), tuple(op.array.shape), op.array.dtype,
-                getattr(op, "amax", None), torch.cuda.current_device()) + tuple(key)
+        gkey = (id(op),) + gk + (torch.cuda.current_device(),) + tuple(key)
         entry = _GRAPHS.get(gkey)
         if entry is not None and entry.get("op") is not None and entry["op"]() is not op:
             _GRAPHS.pop(gkey, None)               # a different operator reused the id

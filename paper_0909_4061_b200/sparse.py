@@ -58,6 +58,13 @@ class CudaCsrOperator(MatVecOperator):
         self.host_io = bool(host_io)
         self.dtype = torch.float64
 
+    def graph_key(self):
+        """Data identity for the CUDA-graph cache of repeated steps (factor._run_step)."""
+        ptrs = [t.data_ptr() for t in self.S + self.St]
+        if self.L is not None:
+            ptrs += [self.L.data_ptr(), self.R.data_ptr(), self.L.shape[1]]
+        return (self.m, self.n, self.nnz, *ptrs)
+
     def csr_bytes(self):
         """Bytes of one pass over the CSR data (values, column indices, row pointers)."""
         return self.nnz * (8 + 4) + (self.m + 1) * 8

@@ -22,8 +22,10 @@ import paper_0909_4061_b200 as lr  # noqa: E402
 
 def main():
     cfg = workloads.CONFIGS[int(sys.argv[1]) if len(sys.argv) > 1 else 2]
-    A = bench.build_input(cfg)
-    op = lr.DenseOperator(A)
+    if cfg.idx == 5:
+        op = lr.CudaCsrOperator(*workloads.build_cfg5())
+    else:
+        op = lr.DenseOperator(bench.build_input(cfg))
 
     def step():
         return lr.randomized_svd(op, cfg.k, cfg.p, cfg.q, cfg.seed, sketch=cfg.sketch,
@@ -51,7 +53,8 @@ def main():
           f"gaps {span - busy:.1f} us (median gap {gaps_sorted[len(gaps) // 2]:.2f} us)")
     agg = {}
     for e in ks:
-        nm = e.name.split("(")[0].split("<")[0].split("::")[-1]
+        nm = e.name.replace("(anonymous namespace)::", "").split("(")[0].split("<")[0]
+        nm = nm.replace("void ", "").split("::")[-1]
         d = e.time_range.end - e.time_range.start
         a = agg.setdefault(nm, [0, 0.0])
         a[0] += 1
