@@ -148,6 +148,27 @@ def measured_fp64_peak():
     return 2.0 * n ** 3 / best / 1e12
 
 
+def measured_int8_peak():
+    """cuBLASLt int8 GEMM 8192^3 (torch._int_mm, best of 5) in TOP/s -- the
+    int8 tensor peak of the emulated fp64 passes (not in MEASURED_PEAKS.json)."""
+    import torch
+    n = 8192
+    a = torch.randint(-64, 64, (n, n), dtype=torch.int8, device="cuda")
+    b = torch.randint(-64, 64, (n, n), dtype=torch.int8, device="cuda")
+    for _ in range(2):
+        torch._int_mm(a, b)
+    best = 1e9
+    for _ in range(5):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        torch._int_mm(a, b)
+        e.record()
+        torch.cuda.synchronize()
+        best = min(best, s.elapsed_time(e) / 1e3)
+    del a, b
+    return 2.0 * n ** 3 / best / 1e12
+
+
 def peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
@@ -299,6 +320,9 @@ def roofline(A, cfg, pev, ms, steps, passes, a_bytes):
     avg_pass_ms = sum(pass_ms) / len(pass_ms)
     avg_flops = sum(flops_per) / len(flops_per)
     pk, src = peaks()
+    from paper_0909_4061_b200 import core as lrcore
+    ozaki = A.dtype == torch.float64 and lrcore._ozaki_wanted(
+        A, torch.empty((1, cfg.ell), dtype=A.dtype, device=A.device))
     if A.dtype in (torch.float64, torch.complex128):
         peak_tf = measured_fp64_peak()
         peak_src = "measured in-run: cuBLAS DGEMM 8192^3 (torch.matmul)"
@@ -314,6 +338,36 @@ def roofline(A, cfg, pev, ms, steps, passes, a_bytes):
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         traffic = json.load(open(tpath)).get(f"cfg{cfg.idx}")
+    if ozaki:
+        # fp64 passes emulated on the int8 tensor cores (lr_gemm_ozaki): the
+        # kernel's own bound is int8 work -- 36 digit-plane products over
+        # 64-column tiles -- against the measured int8 peak; the fp64-DMMA
+        # roofline (the native fp64 bound) is kept beside it
+        i8_peak = measured_int8_peak()
+        m, n = A.shape
+        ntile = -(-cfg.ell // 64) * 64 if cfg.ell > 32 else 32
+        i8_ops = 36 * 2.0 * m * n * ntile
+        achieved_i8 = i8_ops / (avg_pass_ms / 1e3) / 1e12
+        roof_i8_s = max(i8_ops / (i8_peak * 1e12), a_bytes / (hbm * 1e9))
+        return {"bound": "tensor", "achieved": round(achieved_i8, 1), "peak": round(i8_peak, 1),
+                "unit": "TOP/s (int8)", "frac": round(achieved_i8 / i8_peak, 4),
+                "traffic": traffic,
+                "kernel": "ozaki_gemm_kernel: fp64 pass over A as 36 exact int8 digit-plane "
+                          "products on tcgen05 (lr_gemm_ozaki)",
+                "peak_source": "measured in-run: cuBLASLt int8 GEMM 8192^3 (torch._int_mm)",
+                "int8_ops_per_pass": i8_ops,
+                "avg_pass_ms": round(avg_pass_ms, 4),
+                "fp64_equiv_tflops": round(achieved_tf, 3),
+                "fp64_dmma_peak_tflops": round(peak_tf, 3),
+                "fp64_equiv_frac_of_dmma_peak": round(achieved_tf / peak_tf, 4),
+                "pass_a_gbs": round(a_bytes / (avg_pass_ms / 1e3) / 1e9, 1),
+                "hbm_frac": round(a_bytes / (avg_pass_ms / 1e3) / 1e9 / hbm, 4),
+                "step_roofline_ms": round(roof_step_ms, 4),
+                "step_roofline_frac": round(roof_step_ms / ms, 4),
+                "step_roofline_basis": "fp64 flops at the DMMA peak vs A bytes at HBM, per pass",
+                "step_roofline_int8_ms": round(passes * roof_i8_s * 1e3, 4),
+                "step_roofline_int8_frac": round(passes * roof_i8_s * 1e3 / ms, 4),
+                "pass_share_of_step": round(sum(pass_ms) / (ms * steps), 4)}
     return {"bound": "tensor", "achieved": round(achieved_tf, 3), "peak": round(peak_tf, 3),
             "unit": "TFLOP/s", "frac": round(achieved_tf / peak_tf, 4),
             "traffic": traffic, "kernel": "lr_gemm pass over A (K1/K2)",

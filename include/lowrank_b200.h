@@ -89,6 +89,22 @@ int lr_gemm_scaled(lr_handle_t h, int dtype, int op, int64_t m, int64_t n, int64
                    const void* A, int64_t lda, double a_amax, const void* X, int64_t ldx,
                    void* Y, int64_t ldy);
 
+/* fp64 passes on the int8 tensor cores (Ozaki digit slicing, exact int32
+ * products; accuracy of an fp64 GEMM, bitwise deterministic).  Replaces the
+ * same reference call as lr_gemm (DenseOperator._apply / _apply_adjoint,
+ * core.py:391-395) for float64 A.  lr_ozaki_prepare builds, once per
+ * operator, the 8 int8 digit planes of A (planes: 8 x MP x ldp bytes in
+ * 128 x 128 blocks, MP = m and ldp = n rounded up to multiples of 128,
+ * device memory owned by the caller) and the
+ * row exponents (row_exp: m int32).  lr_gemm_ozaki then computes
+ * Y = A X (op N: X n x ell, Y m x ell) or Y = A^T X (op T: X m x ell,
+ * Y n x ell), ell <= 256, from the planes. */
+int lr_ozaki_prepare(lr_handle_t h, int64_t m, int64_t n, const double* A, int64_t lda,
+                     int8_t* planes, int64_t ldp, int32_t* row_exp);
+int lr_gemm_ozaki(lr_handle_t h, int op, int64_t m, int64_t n, int64_t ell,
+                  const int8_t* planes, int64_t ldp, const int32_t* row_exp, const double* X,
+                  int64_t ldx, double* Y, int64_t ldy);
+
 /* Gram matrix G = Y^H Y (ell x ell), accumulated in fp64 (real dtypes) or
  * complex128 (complex dtypes) regardless of the input precision.  G is
  * written as double / double2 row-major with leading dimension ell.  Used

@@ -350,7 +350,8 @@ class DenseOperator(MatVecOperator):
             cur = torch.cuda.current_stream(t.device)
             for r0, r1, ev in chunks:
                 cur.wait_event(ev)
-                _pass(self._array[r0:r1], t, Y[r0:r1], False, self.amax)
+                # (DMMA: digit planes of each chunk view would be rebuilt per call)
+                _pass(self._array[r0:r1], t, Y[r0:r1], False, self.amax, allow_ozaki=False)
             self._finalize()
             return Y
         if t.is_complex() and not self.array.is_complex():
@@ -400,9 +401,76 @@ def _copy_stream(dev):
     return st
 
 
-def _pass(A, X, Y, adjoint, amax):
+def ozaki_prepare(A):
+    """Digit planes of a float64 device matrix for the int8-tensor-core fp64
+    passes (lr_ozaki_prepare): (planes, ldp, row_exp); planes holds 8 x MP x
+    ldp bytes (m and n rounded up to 128, blocked layout)."""
+    torch = _torch()
+    m, n = A.shape
+    ldp = -(-n // 128) * 128          # blocked layout: 128 x 128 blocks per plane
+    mp = -(-m // 128) * 128
+    planes = torch.empty(8 * mp * ldp, dtype=torch.int8, device=A.device)
+    row_exp = torch.empty(m, dtype=torch.int32, device=A.device)
+    _lib.call("lr_ozaki_prepare", _lib.handle(A.device.index), m, n, _lib.ptr(A), _lib.ld(A),
+              _lib.ptr(planes), ldp, _lib.ptr(row_exp))
+    return planes, ldp, row_exp
+
+
+def ozaki_pass(oz, m, n, X, Y, adjoint):
+    """Y = A X (or A^T X) from A's digit planes (lr_gemm_ozaki)."""
+    planes, ldp, row_exp = oz
+    _lib.call("lr_gemm_ozaki", _lib.handle(X.device.index), _lib.OP_T if adjoint else _lib.OP_N,
+              m, n, X.shape[1], _lib.ptr(planes), ldp, _lib.ptr(row_exp), _lib.ptr(X), _lib.ld(X),
+              _lib.ptr(Y), _lib.ld(Y))
+    return Y
+
+
+# Digit planes of a float64 matrix for the int8-tensor-core passes are kept
+# on the tensor object itself (attribute _lr_ozaki with its version counter:
+# an in-place modification of A rebuilds them), so they live exactly as long
+# as A -- and as long as any CUDA graph that replays passes over it through
+# the operator holding A.
+
+
+def _ozaki_wanted(A, X):
+    """fp64 passes run on the int8 tensor cores (lr_gemm_ozaki) when that is
+    faster than DMMA: the emulated pass costs about the same per 64 output
+    columns (128-row x 64-column tiles, 36 digit products) whatever the
+    width, the DMMA pass grows with it -- measured crossover near 36
+    columns per 64-wide tile (tools/ozaki_probe.py).  LR_OZAKI=0 disables,
+    =1 forces it for every fp64 pass."""
+    import os
+    torch = _torch()
+    mode = os.environ.get("LR_OZAKI", "auto")
+    if mode == "0" or A.dtype != torch.float64 or A.dim() != 2:
+        return False
+    ell = X.shape[1]
+    if ell < 1 or ell > 256 or A.stride(1) != 1:
+        return False
+    if mode == "1":
+        return True
+    m, n = A.shape
+    return m >= 1024 and n >= 512 and ell / -(-ell // 64) >= 40
+
+
+def _ozaki_planes(A):
+    cached = getattr(A, "_lr_ozaki", None)
+    if cached is not None and cached[0] == A._version:
+        return cached[1]
+    oz = ozaki_prepare(A)
+    A._lr_ozaki = (A._version, oz)
+    return oz
+
+
+def _pass(A, X, Y, adjoint, amax, allow_ozaki=True):
     """One pass over A (K1/K2); fp32 / complex64 passes use the tcgen05
-    scaled-fp16 split with the operator's max|A| (lr_gemm_scaled)."""
+    scaled-fp16 split with the operator's max|A| (lr_gemm_scaled); fp64
+    passes of enough columns use the int8-tensor-core emulation
+    (lr_gemm_ozaki), the others DMMA."""
+    if allow_ozaki and _ozaki_wanted(A, X):
+        m, n = A.shape
+        ozaki_pass(_ozaki_planes(A), m, n, X, Y, adjoint)
+        return
     code = _lib.dtype_code(A.dtype)
     op = _lib.OP_N if not adjoint else (_lib.OP_C if A.is_complex() else _lib.OP_T)
     m, n = A.shape

@@ -636,6 +636,30 @@ int lr_gemm(lr_handle_t hh, int dtype, int op, int64_t m, int64_t n, int64_t ell
   API_END
 }
 
+int lr_ozaki_prepare(lr_handle_t hh, int64_t m, int64_t n, const double* A, int64_t lda,
+                     int8_t* planes, int64_t ldp, int32_t* row_exp) {
+  API_BEGIN
+  Handle* h = H(hh);
+  LR_REQUIRE(m >= 1 && n >= 1 && lda >= n, LR_EINVAL, "lr_ozaki_prepare: bad dimensions");
+  lr::pool_reset(h);
+  lr::ozaki_prepare(h, m, n, A, lda, planes, ldp, row_exp);
+  API_END
+}
+
+int lr_gemm_ozaki(lr_handle_t hh, int op, int64_t m, int64_t n, int64_t ell,
+                  const int8_t* planes, int64_t ldp, const int32_t* row_exp, const double* X,
+                  int64_t ldx, double* Y, int64_t ldy) {
+  API_BEGIN
+  Handle* h = H(hh);
+  LR_REQUIRE(m >= 0 && n >= 0 && ell >= 0 && ell <= 256, LR_EINVAL,
+             "lr_gemm_ozaki: bad dimensions (ell <= 256)");
+  LR_REQUIRE(op == LR_OP_N || op == LR_OP_T, LR_EINVAL, "lr_gemm_ozaki: op must be N or T");
+  LR_REQUIRE(ldx >= ell && ldy >= ell && ldp >= n, LR_EINVAL, "lr_gemm_ozaki: bad leading dims");
+  lr::pool_reset(h);
+  if (ell > 0) lr::ozaki_gemm(h, op != LR_OP_N, m, n, ell, planes, ldp, row_exp, X, ldx, Y, ldy);
+  API_END
+}
+
 int lr_gemm_scaled(lr_handle_t hh, int dtype, int op, int64_t m, int64_t n, int64_t ell,
                    const void* A, int64_t lda, double a_amax, const void* X, int64_t ldx, void* Y,
                    int64_t ldy) {

@@ -104,6 +104,12 @@ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 // gemm_f64.cu ---------------------------------------------------------------
 int64_t choose_splits(int sm_count, int64_t tiles, int64_t K);
+// gemm_f64_ozaki.cu: fp64 passes on the int8 tensor cores (digit planes of A)
+void ozaki_prepare(Handle* h, int64_t m, int64_t n, const double* A, int64_t lda, int8_t* planes,
+                   int64_t ldp, int32_t* row_exp);
+void ozaki_gemm(Handle* h, bool trans, int64_t m, int64_t n, int64_t N, const int8_t* planes,
+                int64_t ldp, const int32_t* row_exp, const double* X, int64_t ldx, double* C,
+                int64_t ldc);
 // C (M x N) = op(A) . B, op(A) = A (A M x K, lda) or A^T (A K x M, lda);
 // B is K x N (ldb); C M x N (ldc).  conjA applies for complex.
 void gemm_f64(Handle* h, bool transA, int64_t M, int64_t N, int64_t K, const double* A,

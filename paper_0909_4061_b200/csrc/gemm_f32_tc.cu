@@ -459,6 +459,37 @@ CUtensorMap make_map_2d(CUtensorMapDataType dt, const void* ptr, uint64_t inner,
   return m;
 }
 
+CUtensorMap make_map_nd(CUtensorMapDataType dt, const void* ptr, int rank, const uint64_t* dims,
+                        const uint64_t* strides, const uint32_t* box, CUtensorMapSwizzle swz) {
+  CUtensorMap m;
+  cuuint64_t d[5], st[4];
+  cuuint32_t bx[5], estr[5];
+  for (int i = 0; i < rank; ++i) {
+    d[i] = dims[i];
+    bx[i] = box[i];
+    estr[i] = 1;
+    if (i + 1 < rank) st[i] = strides[i];
+  }
+  CUresult r = encode_fn()(&m, dt, cuuint32_t(rank), const_cast<void*>(ptr), d, st, bx, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  LR_REQUIRE(r == CUDA_SUCCESS, LR_ECUDA, "cuTensorMapEncodeTiled (n-D) failed");
+  return m;
+}
+
+CUtensorMap make_map_3d(CUtensorMapDataType dt, const void* ptr, const uint64_t dims[3],
+                        const uint64_t strides[2], const uint32_t box[3], CUtensorMapSwizzle swz) {
+  CUtensorMap m;
+  const cuuint64_t d[3] = {dims[0], dims[1], dims[2]};
+  const cuuint64_t st[2] = {strides[0], strides[1]};
+  const cuuint32_t bx[3] = {box[0], box[1], box[2]};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode_fn()(&m, dt, 3, const_cast<void*>(ptr), d, st, bx, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  LR_REQUIRE(r == CUDA_SUCCESS, LR_ECUDA, "cuTensorMapEncodeTiled (3-D) failed");
+  return m;
+}
 
 bool gemm_f32_tc_supported(bool transA, int64_t N, const float* A, int64_t lda) {
   return N >= 1 && N <= 256 && (lda % 4) == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0;

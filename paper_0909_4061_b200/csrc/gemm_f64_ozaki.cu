@@ -1,0 +1,482 @@
+// K1/K2 in fp64 on the int8 tensor cores (tcgen05.mma kind::i8): the passes
+// over a float64 A (reference DenseOperator._apply / _apply_adjoint,
+// core.py:391-395) as an exact-integer emulation of the fp64 product (Ozaki
+// scheme, digit-sliced operands).
+//
+// B200's FP64 tensor pipe (DMMA) peaks near 36 TF/s, which makes a pass of
+// config 2 (16384 x 8192 x 110) compute-bound at ~0.9 ms against 0.16 ms of
+// HBM time.  The int8 pipe is ~100x faster, so the product is rebuilt from
+// exact integer products:
+//   A_ik = 2^eA_i * sum_{s=1..8} a_s,ik 2^-(6 + 7(s-1)),   |a_s| <= 64
+//   X_kj = 2^eX_j * sum_{t=1..8} x_t,kj 2^-(6 + 7(t-1))
+// (eA_i: exponent of row i's max, eX_j: of column j's max; the digits are
+// exact fp64 rint remainders, 55 bits of each entry relative to its row /
+// column maximum), and
+//   (A X)_ij = 2^(eA_i + eX_j) * sum_{d=2..9} 2^-(12 + 7(d-2)) acc_d,ij,
+//   acc_d = sum_{s+t=d} sum_k a_s,ik x_t,kj      (int32, exact)
+// The 36 digit-plane products with s + t <= 9 are the only ones whose
+// weight reaches fp64 resolution: the first dropped diagonal (d = 10) is
+// 2^-53 of the |A||X| bound, the same size as the rounding of one fp64
+// product -- the result has the accuracy of an fp64 GEMM (tests compare it
+// with the DMMA kernels), and it is bitwise deterministic (integer sums).
+//
+// Data: the 8 digit planes of A are built once per operator
+// (lr_ozaki_prepare, 8 bytes per entry like A itself) with row scaling; the
+// same planes serve A^T Y, whose summation index is the row index: the row
+// scales fold into Y (Y'_ik = 2^eA_i Y_ik, exact), and the A tile is read
+// MN-major.  X / Y' are sliced per pass (small).
+//
+// Kernel: CTA = 128 rows x BN (32 or 64) columns, 8 int32 TMEM accumulators
+// (one per diagonal d, 8 * BN <= 512 columns), k-stage = 32 (one UMMA K),
+// 4-deep TMA ring of {8 A planes, 8 X planes} (48 KB per stage at BN = 64),
+// warp-specialized: warp 0 TMA, warp 1 MMA issuer (36 UMMAs per stage),
+// warp 2 TMEM allocator, warps 4-7 epilogue (TMEM -> fp64 combine -> scaled
+// coalesced stores or a split-K slice).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+#include "tma.cuh"
+
+namespace lr {
+namespace {
+
+constexpr int OZ_S = 8;             // digit planes per operand
+constexpr int OZ_ND = 8;            // diagonals d = 2..9
+constexpr int OBM = 128;            // UMMA M
+constexpr int OBK = 32;             // k per stage (= UMMA K for kind::i8)
+#ifndef LR_OZ_ST
+#define LR_OZ_ST 4
+#endif
+constexpr int OST = LR_OZ_ST;       // ring depth
+constexpr int OTHREADS = 256;
+constexpr int A_PLANE = OBM * OBK;  // 4 KB
+constexpr int A_STAGE = OZ_S * A_PLANE;
+constexpr int64_t OZ_KMAX = 65536;  // int32 headroom: 8 pairs x 64^2 x K < 2^31
+
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mb_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n));
+}
+__device__ __forceinline__ void mb_expect(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mb_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "W%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra W%=;\n}" ::"r"(su32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                      int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(su32(dst)),
+      "l"(map), "r"(su32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tma5d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                      int c1, int c2, int c3, int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(su32(dst)),
+      "l"(map), "r"(su32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+      : "memory");
+}
+// K-major, 32-byte swizzle: rows of 32 B (one UMMA K of int8), 8-row groups 256 B apart
+__device__ __forceinline__ uint64_t desc_k_sw32(const void* p) {
+  return ((uint64_t(su32(p)) >> 4) & 0x3FFFull) | (1ull << 16) | (uint64_t(256 >> 4) << 32) |
+         (1ull << 46) | (6ull << 61);
+}
+// MN-major, 128-byte swizzle: 128 M-elements (bytes) per K-row, 8-row groups
+// 1024 B apart (one MN atom covers M = 128 int8)
+__device__ __forceinline__ uint64_t desc_mn_sw128(const void* p) {
+  return ((uint64_t(su32(p)) >> 4) & 0x3FFFull) | (1ull << 16) | (uint64_t(1024 >> 4) << 32) |
+         (1ull << 46) | (2ull << 61);
+}
+__device__ __forceinline__ void umma_i8(uint32_t tmem, uint64_t adesc, uint64_t bdesc,
+                                        uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   su32(bar))
+               : "memory");
+}
+
+// the 8 signed 7-bit digits of r in (-1, 1): r = sum_s d_s 2^-(6 + 7(s-1)) + O(2^-56)
+__device__ __forceinline__ void digits8(double r, int8_t (&d)[OZ_S]) {
+  double x = r * 64.0;
+#pragma unroll
+  for (int s = 0; s < OZ_S; ++s) {
+    const double q = rint(x);
+    d[s] = static_cast<int8_t>(static_cast<int>(q));
+    x = (x - q) * 128.0;
+  }
+}
+
+__device__ __forceinline__ int exp_of(double amax) {
+  if (!(amax > 0.0)) return 0;
+  int e;
+  frexp(amax, &e);   // amax = f 2^e, f in [0.5, 1): |v| 2^-e < 1
+  return e;
+}
+
+// ---------------------------------------------------------------------------
+// A planes (once per operator): row exponents, then digits
+
+__global__ void oz_row_exp_kernel(int64_t m, int64_t n, const double* __restrict__ A, int64_t lda,
+                                  int32_t* __restrict__ row_exp) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5); i < m; i += warps) {
+    double mx = 0.0;
+    const double* row = A + i * lda;
+    for (int64_t k = lane; k < n; k += 32) mx = fmax(mx, fabs(row[k]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) row_exp[i] = exp_of(mx);
+  }
+}
+
+// Blocked plane layout (both passes stream it with good DRAM locality):
+// 128 x 128 blocks of A, block (bi, bk) of plane s at
+// ((bi * NB + bk) * 8 + s) * 16 KB, row-major inside (128 B per row).  The
+// A X pass reads 128 rows x 32 B of a block per stage, the A^T Y pass 32 rows
+// x 128 B; a plain [plane][row][col] layout made every A X stage a gather of
+// 32-byte pieces 8 KB apart (~40 % of HBM bandwidth).  Padding is zero.
+constexpr int OZB = 128;
+constexpr int64_t OZ_BLOCK = int64_t(OZB) * OZB;   // bytes per plane block
+
+__global__ void oz_slice_a_kernel(int64_t m, int64_t n, const double* __restrict__ A, int64_t lda,
+                                  const int32_t* __restrict__ row_exp, int8_t* __restrict__ planes,
+                                  int64_t MP, int64_t NP) {
+  const int64_t groups = NP / 8, total = MP * groups, NB = NP / OZB;
+  for (int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; g < total;
+       g += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = g / groups, k0 = (g - i * groups) * 8;
+    const int e = i < m ? row_exp[i] : 0;
+    uint64_t packed[OZ_S];
+#pragma unroll
+    for (int s = 0; s < OZ_S; ++s) packed[s] = 0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t k = k0 + u;
+      int8_t d[OZ_S];
+      digits8((i < m && k < n) ? ldexp(A[i * lda + k], -e) : 0.0, d);
+#pragma unroll
+      for (int s = 0; s < OZ_S; ++s) packed[s] |= uint64_t(uint8_t(d[s])) << (8 * u);
+    }
+    const int64_t blk = (i / OZB) * NB + k0 / OZB;
+    int8_t* dst = planes + blk * OZ_S * OZ_BLOCK + (i % OZB) * OZB + (k0 % OZB);
+#pragma unroll
+    for (int s = 0; s < OZ_S; ++s) *reinterpret_cast<uint64_t*>(dst + s * OZ_BLOCK) = packed[s];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// X / Y' planes (per pass): column exponents of X' = diag(2^row_exp) X, then
+// the digits transposed to [t][j][k] (K-major B operand), rows j >= N zero
+
+__global__ void oz_col_max_kernel(int64_t K, int64_t N, const double* __restrict__ X, int64_t ldx,
+                                  const int32_t* __restrict__ row_exp,
+                                  unsigned long long* __restrict__ bits) {
+  const int64_t rows_per = (K + gridDim.x - 1) / gridDim.x;
+  const int64_t k0 = blockIdx.x * rows_per, k1 = min(K, k0 + rows_per);
+  for (int64_t j = threadIdx.x; j < N; j += blockDim.x) {
+    double mx = 0.0;
+    for (int64_t k = k0; k < k1; ++k) {
+      const double v = X[k * ldx + j];
+      mx = fmax(mx, fabs(row_exp ? ldexp(v, row_exp[k]) : v));
+    }
+    if (mx > 0.0) atomicMax(bits + j, static_cast<unsigned long long>(__double_as_longlong(mx)));
+  }
+}
+
+__global__ void oz_col_exp_kernel(int64_t N, const unsigned long long* __restrict__ bits,
+                                  int32_t* __restrict__ col_exp) {
+  for (int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; j < N;
+       j += int64_t(gridDim.x) * blockDim.x)
+    col_exp[j] = exp_of(__longlong_as_double(static_cast<long long>(bits[j])));
+}
+
+// 32 (k) x 32 (j) tiles through shared memory: coalesced reads of X rows,
+// coalesced 32-byte runs of k in each output plane row
+__global__ void oz_slice_b_kernel(int64_t K, int64_t N, int64_t Np, const double* __restrict__ X,
+                                  int64_t ldx, const int32_t* __restrict__ row_exp,
+                                  const int32_t* __restrict__ col_exp, int8_t* __restrict__ planes,
+                                  int64_t ldp) {
+  __shared__ int8_t t8[OZ_S][32][33];
+  const int64_t k0 = int64_t(blockIdx.x) * 32, j0 = int64_t(blockIdx.y) * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;   // 32 x 8
+  for (int r = ty; r < 32; r += 8) {
+    const int64_t k = k0 + r, j = j0 + tx;
+    double v = 0.0;
+    if (k < K && j < N) {
+      v = X[k * ldx + j];
+      if (row_exp) v = ldexp(v, row_exp[k]);
+      v = ldexp(v, -col_exp[j]);
+    }
+    int8_t d[OZ_S];
+    digits8(v, d);
+#pragma unroll
+    for (int s = 0; s < OZ_S; ++s) t8[s][tx][r] = d[s];
+  }
+  __syncthreads();
+  const int64_t plane = Np * ldp;
+  for (int r = ty; r < 32; r += 8) {
+    const int64_t j = j0 + r, k = k0 + tx;
+    if (j < Np && k < ldp) {
+#pragma unroll
+      for (int s = 0; s < OZ_S; ++s) planes[s * plane + j * ldp + k] = t8[s][r][tx];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// the pass kernel
+
+template <bool TRANS>
+__global__ void __launch_bounds__(OTHREADS, 1)
+ozaki_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                  int M, int N, int BN, int64_t k_per_split, int64_t K,
+                  const int32_t* __restrict__ row_exp, const int32_t* __restrict__ col_exp,
+                  double* __restrict__ C, int64_t ldc, int64_t cstride) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* base = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int b_plane = BN * OBK;
+  const int stage_bytes = A_STAGE + OZ_S * b_plane;
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + OST * stage_bytes);
+  uint64_t* empty = full + OST;
+  uint64_t* acc_full = empty + OST;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // N tile fastest in launch order: the CTAs sharing an A tile run together (L2 reuse)
+  const int m0 = blockIdx.y * OBM, n0 = blockIdx.x * BN;
+  const int64_t kbeg = int64_t(blockIdx.z) * k_per_split;
+  const int64_t kend = min(K, kbeg + k_per_split);
+  const int nk = int((kend - kbeg + OBK - 1) / OBK);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < OST; ++s) {
+      mb_init(&full[s], 1);
+      mb_init(&empty[s], 1);
+    }
+    mb_init(acc_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  const uint32_t tmem_cols = uint32_t(OZ_ND * BN);   // 256 or 512
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     su32(tmem_slot)),
+                 "r"(tmem_cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int kt = 0; kt < nk; ++kt) {
+        const int s = kt % OST;
+        const uint32_t ph = uint32_t(kt / OST) & 1u;
+        const int kc = int(kbeg + int64_t(kt) * OBK);
+        mb_wait(&empty[s], ph ^ 1u);
+        mb_expect(&full[s], uint32_t(stage_bytes));
+        unsigned char* st = base + s * stage_bytes;
+        // A map dims {col-in-block, row-in-block, plane, block col, block row}
+        if (!TRANS) tma5d(st, &mapA, &full[s], kc % OZB, 0, 0, kc / OZB, m0 / OZB);
+        else        tma5d(st, &mapA, &full[s], 0, kc % OZB, 0, m0 / OZB, kc / OZB);
+        tma3d(st + A_STAGE, &mapB, &full[s], kc, n0, 0);     // [plane][BN rows][32 k]
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // kind::i8: D = s32 (c_format 2), A/B signed int8 (format 1), A MN-major for A^T
+      const uint32_t idesc0 = (2u << 4) | (1u << 7) | (1u << 10) | ((TRANS ? 1u : 0u) << 15) |
+                              (uint32_t(OBM >> 4) << 24);
+      // X planes t = 1..8 are consecutive BN-row blocks of one K-major operand,
+      // and the accumulators of diagonals d = 2..9 consecutive BN-column blocks
+      // of TMEM: for A plane sa, the products with planes t = t0 .. t0+np-1
+      // land in diagonals sa+t0 .. sa+t0+np-1 -- ONE UMMA with N = np * BN.
+      // 12 UMMAs per stage instead of 36: each UMMA re-reads its A plane from
+      // shared memory, which bounded the 36-product version (~90 clk each).
+      const int cmax = 256 / BN;
+      for (int kt = 0; kt < nk; ++kt) {
+        const int s = kt % OST;
+        const uint32_t ph = uint32_t(kt / OST) & 1u;
+        mb_wait(&full[s], ph);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const unsigned char* st = base + s * stage_bytes;
+#pragma unroll
+        for (int sa = 1; sa <= OZ_S; ++sa) {
+          const uint64_t da = TRANS ? desc_mn_sw128(st + (sa - 1) * A_PLANE)
+                                    : desc_k_sw32(st + (sa - 1) * A_PLANE);
+          const int tmax = (OZ_ND + 1) - sa;   // t <= 9 - sa
+          for (int t0 = 1; t0 <= tmax; t0 += cmax) {
+            const int np = min(cmax, tmax - t0 + 1);
+            const uint32_t idesc = idesc0 | (uint32_t((np * BN) >> 3) << 17);
+            umma_i8(tmem + uint32_t((sa + t0 - 2) * BN),
+                    da, desc_k_sw32(st + A_STAGE + (t0 - 1) * b_plane), idesc,
+                    (kt > 0 || sa > 1) ? 1u : 0u);
+          }
+        }
+        umma_commit(&empty[s]);
+      }
+      umma_commit(acc_full);
+    }
+  } else if (warp >= 4) {
+    mb_wait(acc_full, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const int q = warp - 4;   // TMEM lane quarter: rows q*32 .. q*32+31
+    const int row = m0 + q * 32 + lane;
+    const int re = (row_exp && row < M) ? row_exp[row] : 0;
+    double* wbuf = reinterpret_cast<double*>(base) + q * (32 * 33);   // ring is idle now
+    double* cbase = C + int64_t(blockIdx.z) * cstride;
+    for (int c0 = 0; c0 < BN; c0 += 32) {
+      double acc[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) acc[j] = 0.0;
+#pragma unroll 1
+      for (int d = 9; d >= 2; --d) {   // smallest weights first
+        uint32_t v[32];
+        const uint32_t taddr = tmem + (uint32_t(q * 32) << 16) + uint32_t((d - 2) * BN + c0);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+            "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+              "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]),
+              "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]),
+              "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+              "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
+              "=r"(v[30]), "=r"(v[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        const double w = ldexp(1.0, -(12 + 7 * (d - 2)) + re);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc[j] = fma(double(int32_t(v[j])), w, acc[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < 32; ++j) wbuf[lane * 33 + j] = acc[j];
+      __syncwarp();
+      const int col = n0 + c0 + lane;
+      const int ce = col < N ? col_exp[col] : 0;
+      for (int rr = 0; rr < 32; ++rr) {
+        const int r = m0 + q * 32 + rr;
+        if (r < M && col < N) cbase[int64_t(r) * ldc + col] = ldexp(wbuf[rr * 33 + lane], ce);
+      }
+      __syncwarp();
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(tmem_cols));
+  }
+}
+
+}  // namespace
+
+// 8 digit planes of A in the blocked layout (ldp = NP: n rounded up to 128;
+// the buffer holds 8 * MP * NP bytes, MP = m rounded up to 128) + row exponents
+void ozaki_prepare(Handle* h, int64_t m, int64_t n, const double* A, int64_t lda, int8_t* planes,
+                   int64_t ldp, int32_t* row_exp) {
+  LR_REQUIRE(ldp >= n && ldp % OZB == 0, LR_EINVAL,
+             "ozaki_prepare: ldp must be n rounded up to a multiple of 128");
+  const int64_t MP = ceil_div(m, OZB) * OZB;
+  const int blocks = h->sm_count * 8;
+  oz_row_exp_kernel<<<blocks, 256, 0, h->stream>>>(m, n, A, lda, row_exp);
+  LR_CHECK_LAUNCH();
+  oz_slice_a_kernel<<<blocks, 256, 0, h->stream>>>(m, n, A, lda, row_exp, planes, MP, ldp);
+  LR_CHECK_LAUNCH();
+}
+
+// C = A X (trans = false: A m x n, X n x N, C m x N) or C = A^T X (trans:
+// X m x N, C n x N) from the prepared planes of A.
+void ozaki_gemm(Handle* h, bool trans, int64_t m, int64_t n, int64_t N, const int8_t* planes,
+                int64_t ldp, const int32_t* row_exp, const double* X, int64_t ldx, double* C,
+                int64_t ldc) {
+  const int64_t M = trans ? n : m;        // output rows
+  const int64_t K = trans ? m : n;        // summation length
+  if (M == 0 || N == 0) return;
+  LR_REQUIRE(N <= 256, LR_EUNSUPPORTED, "ozaki_gemm: more than 256 columns");
+  const int BN = N <= 32 ? 32 : 64;
+  const int64_t nt = ceil_div(N, BN), Np = nt * BN;
+  const int64_t ldb = ceil_div(K, 16) * 16;
+  // X' planes and column exponents
+  int8_t* bpl = pool_alloc_t<int8_t>(h, size_t(OZ_S) * Np * ldb);
+  unsigned long long* bits = pool_alloc_t<unsigned long long>(h, size_t(N));
+  int32_t* col_exp = pool_alloc_t<int32_t>(h, size_t(N));
+  LR_CUDA(cudaMemsetAsync(bits, 0, size_t(N) * sizeof(unsigned long long), h->stream));
+  const int32_t* rexp_b = trans ? row_exp : nullptr;   // A^T Y: row scales fold into Y
+  oz_col_max_kernel<<<unsigned(std::min<int64_t>(ceil_div(K, 64), int64_t(h->sm_count) * 4)), 128, 0,
+                      h->stream>>>(K, N, X, ldx, rexp_b, bits);
+  LR_CHECK_LAUNCH();
+  oz_col_exp_kernel<<<1, 256, 0, h->stream>>>(N, bits, col_exp);
+  LR_CHECK_LAUNCH();
+  {
+    dim3 grid(unsigned(ceil_div(ldb, 32)), unsigned(ceil_div(Np, 32)));
+    oz_slice_b_kernel<<<grid, dim3(32, 8), 0, h->stream>>>(K, N, Np, X, ldx, rexp_b, col_exp, bpl,
+                                                           ldb);
+    LR_CHECK_LAUNCH();
+  }
+  // tensor maps: A planes blocked (see oz_slice_a_kernel), B planes [8][Np][ldb]
+  CUtensorMap mapA, mapB;
+  {
+    const int64_t MB = ceil_div(m, OZB), NB = ldp / OZB;
+    const uint64_t dA[5] = {uint64_t(OZB), uint64_t(OZB), uint64_t(OZ_S), uint64_t(NB), uint64_t(MB)};
+    const uint64_t sA[4] = {uint64_t(OZB), uint64_t(OZ_BLOCK), uint64_t(OZ_S * OZ_BLOCK),
+                            uint64_t(NB * OZ_S * OZ_BLOCK)};
+    const uint32_t bA[5] = {trans ? uint32_t(OBM) : uint32_t(OBK),
+                            trans ? uint32_t(OBK) : uint32_t(OBM), uint32_t(OZ_S), 1, 1};
+    mapA = make_map_nd(CU_TENSOR_MAP_DATA_TYPE_UINT8, planes, 5, dA, sA, bA,
+                       trans ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_32B);
+    const uint64_t dB[3] = {uint64_t(ldb), uint64_t(Np), uint64_t(OZ_S)};
+    const uint64_t sB[2] = {uint64_t(ldb), uint64_t(Np) * ldb};
+    const uint32_t bB[3] = {uint32_t(OBK), uint32_t(BN), uint32_t(OZ_S)};
+    mapB = make_map_3d(CU_TENSOR_MAP_DATA_TYPE_UINT8, bpl, dB, sB, bB, CU_TENSOR_MAP_SWIZZLE_32B);
+  }
+  const int stage_bytes = A_STAGE + OZ_S * BN * OBK;
+  const size_t smem = size_t(OST) * stage_bytes + 1024 + 256;
+  auto kern = trans ? ozaki_gemm_kernel<true> : ozaki_gemm_kernel<false>;
+  static size_t attr[2] = {0, 0};
+  if (attr[trans] < smem) {
+    LR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    attr[trans] = smem;
+  }
+  const int64_t mt = ceil_div(M, OBM);
+  int64_t want = choose_splits(h->sm_count, mt * nt, K);
+  want = std::max<int64_t>(want, ceil_div(K, OZ_KMAX));
+  const int64_t kchunk = ceil_div(ceil_div(K, want), OBK) * OBK;
+  const int64_t splits = ceil_div(K, kchunk);
+  dim3 grid{unsigned(nt), unsigned(mt), unsigned(splits)};
+  const int32_t* rexp_c = trans ? nullptr : row_exp;
+  if (splits == 1) {
+    kern<<<grid, OTHREADS, smem, h->stream>>>(mapA, mapB, int(M), int(N), BN, kchunk, K, rexp_c,
+                                              col_exp, C, ldc, 0);
+    LR_CHECK_LAUNCH();
+    return;
+  }
+  double* part = pool_alloc_t<double>(h, size_t(splits) * M * N);
+  kern<<<grid, OTHREADS, smem, h->stream>>>(mapA, mapB, int(M), int(N), BN, kchunk, K, rexp_c,
+                                            col_exp, part, N, M * N);
+  LR_CHECK_LAUNCH();
+  splitk_reduce(h, M, N, int(splits), part, C, ldc);
+}
+
+}  // namespace lr

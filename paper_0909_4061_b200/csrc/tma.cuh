@@ -15,4 +15,12 @@ CUtensorMap make_map_2d(CUtensorMapDataType dt, const void* ptr, uint64_t inner,
                         uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer,
                         CUtensorMapSwizzle swz);
 
+// rank-D tensor map (rank <= 5): dims[0] contiguous, byte strides of dims
+// 1..rank-1, box sizes.
+CUtensorMap make_map_nd(CUtensorMapDataType dt, const void* ptr, int rank, const uint64_t* dims,
+                        const uint64_t* strides, const uint32_t* box, CUtensorMapSwizzle swz);
+// 3-D tensor map: dims[0] contiguous, byte strides of dims 1 and 2, box sizes.
+CUtensorMap make_map_3d(CUtensorMapDataType dt, const void* ptr, const uint64_t dims[3],
+                        const uint64_t strides[2], const uint32_t box[3], CUtensorMapSwizzle swz);
+
 }  // namespace lr

@@ -478,3 +478,31 @@ def test_skinny_nn(M, N, K):
               _lib.ptr(B), _lib.ld(B), _lib.ptr(C), _lib.ld(C))
     ref = A.cpu().numpy() @ B.cpu().numpy()
     assert np.abs(C.cpu().numpy() - ref).max() <= 1e-13 * K
+
+
+@pytest.mark.parametrize("m,n,ell", [(300, 257, 30), (129, 64, 110), (2048, 2048, 30),
+                                     (1000, 3000, 64), (513, 77, 128), (4096, 700, 200),
+                                     (37, 1, 3), (5000, 40, 7)])
+@pytest.mark.parametrize("adjoint", [False, True])
+def test_ozaki_fp64_pass(m, n, ell, adjoint):
+    """fp64 passes on the int8 tensor cores (lr_gemm_ozaki): every entry
+    within 2^-50 of the |A||X| bound of an fp64 GEMM (the reference's
+    OpenBLAS dgemm has the same bound), checked against an 80-bit product;
+    deterministic bit for bit."""
+    from paper_0909_4061_b200 import core
+    g = np.random.default_rng(m + n + ell)
+    A = g.standard_normal((m, n)) * np.exp(g.uniform(-3, 3, (m, 1)))   # rows of mixed scale
+    X = g.standard_normal((m if adjoint else n, ell)) * np.exp(g.uniform(-3, 3, (1, ell)))
+    Ad, Xd = torch.from_numpy(A).cuda(), torch.from_numpy(X).cuda()
+    oz = core.ozaki_prepare(Ad)
+    rows = n if adjoint else m
+    Y = torch.empty((rows, ell), dtype=torch.float64, device="cuda")
+    core.ozaki_pass(oz, m, n, Xd, Y, adjoint)
+    Y2 = torch.empty_like(Y)
+    core.ozaki_pass(oz, m, n, Xd, Y2, adjoint)
+    assert torch.equal(Y, Y2)
+    Al, Xl = A.astype(np.longdouble), X.astype(np.longdouble)
+    ref = (Al.T @ Xl) if adjoint else (Al @ Xl)
+    bound = (np.abs(A).T @ np.abs(X)) if adjoint else (np.abs(A) @ np.abs(X))
+    err = np.abs(Y.cpu().numpy().astype(np.longdouble) - ref)
+    assert float((err / np.maximum(bound, 1e-300)).max()) <= 2.0 ** -50
