@@ -93,9 +93,10 @@ int lr_gemm_scaled(lr_handle_t h, int dtype, int op, int64_t m, int64_t n, int64
  * products; accuracy of an fp64 GEMM, bitwise deterministic).  Replaces the
  * same reference call as lr_gemm (DenseOperator._apply / _apply_adjoint,
  * core.py:391-395) for float64 A.  lr_ozaki_prepare builds, once per
- * operator, the 8 int8 digit planes of A (planes: 8 x MP x ldp bytes in
- * 128 x 128 blocks, MP = m and ldp = n rounded up to multiples of 128,
- * device memory owned by the caller) and the
+ * operator, the 8 int8 digit planes of A as the two tiled shared-memory
+ * images the pass kernel streams (planes: 16 x MP x ldp bytes, MP = m and
+ * ldp = n rounded up to multiples of 128, device memory owned by the
+ * caller) and the
  * row exponents (row_exp: m int32).  lr_gemm_ozaki then computes
  * Y = A X (op N: X n x ell, Y m x ell) or Y = A^T X (op T: X m x ell,
  * Y n x ell), ell <= 256, from the planes. */

@@ -403,13 +403,14 @@ def _copy_stream(dev):
 
 def ozaki_prepare(A):
     """Digit planes of a float64 device matrix for the int8-tensor-core fp64
-    passes (lr_ozaki_prepare): (planes, ldp, row_exp); planes holds 8 x MP x
-    ldp bytes (m and n rounded up to 128, blocked layout)."""
+    passes (lr_ozaki_prepare): (planes, ldp, row_exp); planes holds the two
+    shared-memory images of the 8 digit planes (A X and A^T Y tiles),
+    16 x MP x ldp bytes (m and n rounded up to 128)."""
     torch = _torch()
     m, n = A.shape
     ldp = -(-n // 128) * 128          # blocked layout: 128 x 128 blocks per plane
     mp = -(-m // 128) * 128
-    planes = torch.empty(8 * mp * ldp, dtype=torch.int8, device=A.device)
+    planes = torch.empty(16 * mp * ldp, dtype=torch.int8, device=A.device)   # two images
     row_exp = torch.empty(m, dtype=torch.int32, device=A.device)
     _lib.call("lr_ozaki_prepare", _lib.handle(A.device.index), m, n, _lib.ptr(A), _lib.ld(A),
               _lib.ptr(planes), ldp, _lib.ptr(row_exp))

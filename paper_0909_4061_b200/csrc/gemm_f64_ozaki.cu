@@ -32,6 +32,8 @@
 // warp-specialized: warp 0 TMA, warp 1 MMA issuer (36 UMMAs per stage),
 // warp 2 TMEM allocator, warps 4-7 epilogue (TMEM -> fp64 combine -> scaled
 // coalesced stores or a split-K slice).
+#include <cstdlib>
+
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -73,22 +75,24 @@ __device__ __forceinline__ void mb_wait(uint64_t* b, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ void tma3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
-                                      int c1, int c2) {
+// 1-D bulk copy global -> shared (one request for a whole pre-swizzled tile)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(su32(dst)),
-      "l"(map), "r"(su32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          su32(dst)),
+      "l"(src), "r"(bytes), "r"(su32(bar))
       : "memory");
 }
-__device__ __forceinline__ void tma5d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
-                                      int c1, int c2, int c3, int c4) {
-  asm volatile(
-      "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(su32(dst)),
-      "l"(map), "r"(su32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
-      : "memory");
+// byte offsets inside the shared-memory images the UMMA descriptors read:
+// K-major SWIZZLE_32B (rows of 32 B; 16-B chunk c of row r at c ^ ((r >> 2) & 1))
+__host__ __device__ __forceinline__ int img_k32(int r, int k) {
+  return r * 32 + ((((k >> 4) ^ (r >> 2)) & 1) << 4) + (k & 15);
 }
+// MN-major SWIZZLE_128B (rows of 128 B along M, one row per k; chunk c at c ^ (k & 7))
+__host__ __device__ __forceinline__ int img_mn128(int k, int mm) {
+  return k * 128 + ((((mm >> 4) ^ k) & 7) << 4) + (mm & 15);
+}
+
 // K-major, 32-byte swizzle: rows of 32 B (one UMMA K of int8), 8-row groups 256 B apart
 __device__ __forceinline__ uint64_t desc_k_sw32(const void* p) {
   return ((uint64_t(su32(p)) >> 4) & 0x3FFFull) | (1ull << 16) | (uint64_t(256 >> 4) << 32) |
@@ -149,38 +153,52 @@ __global__ void oz_row_exp_kernel(int64_t m, int64_t n, const double* __restrict
   }
 }
 
-// Blocked plane layout (both passes stream it with good DRAM locality):
-// 128 x 128 blocks of A, block (bi, bk) of plane s at
-// ((bi * NB + bk) * 8 + s) * 16 KB, row-major inside (128 B per row).  The
-// A X pass reads 128 rows x 32 B of a block per stage, the A^T Y pass 32 rows
-// x 128 B; a plain [plane][row][col] layout made every A X stage a gather of
-// 32-byte pieces 8 KB apart (~40 % of HBM bandwidth).  Padding is zero.
+// The digit planes of A are stored as the exact shared-memory images the
+// pass kernel consumes, so every pipeline stage is ONE contiguous bulk copy
+// (a tensor-map box of 32-byte rows split each stage into ~1024 sector
+// requests, capping the A stream near 25 GB/s per SM):
+//   imgN (A X):   tile (mt = i / 128, kt = k / 32), plane s: 128 rows x 32 B,
+//                 K-major SWIZZLE_32B, at ((mt * KT + kt) * 8 + s) * 4 KB
+//   imgT (A^T Y): tile (jt = k / 128, it = i / 32), plane s: 32 rows (i) x
+//                 128 B (k), MN-major SWIZZLE_128B, at ((jt * IT + it) * 8 + s) * 4 KB
+// with m, n padded to multiples of 128 (KT = NP / 32, IT = MP / 32); padding
+// is zero.  Each image holds 8 * MP * NP bytes.
 constexpr int OZB = 128;
-constexpr int64_t OZ_BLOCK = int64_t(OZB) * OZB;   // bytes per plane block
+constexpr int64_t TILE = 4096;   // bytes of one plane of one stage tile
 
 __global__ void oz_slice_a_kernel(int64_t m, int64_t n, const double* __restrict__ A, int64_t lda,
-                                  const int32_t* __restrict__ row_exp, int8_t* __restrict__ planes,
-                                  int64_t MP, int64_t NP) {
-  const int64_t groups = NP / 8, total = MP * groups, NB = NP / OZB;
+                                  const int32_t* __restrict__ row_exp, int8_t* __restrict__ imgN,
+                                  int8_t* __restrict__ imgT, int64_t MP, int64_t NP) {
+  // one thread: 4 consecutive k of one row i (4-byte stores into imgN)
+  const int64_t groups = NP / 4, total = MP * groups;
+  const int64_t KT = NP / 32, IT = MP / 32;
   for (int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; g < total;
        g += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t i = g / groups, k0 = (g - i * groups) * 8;
+    const int64_t i = g / groups, k0 = (g - i * groups) * 4;
     const int e = i < m ? row_exp[i] : 0;
-    uint64_t packed[OZ_S];
+    uint32_t packed[OZ_S];
+    int8_t dd[4][OZ_S];
 #pragma unroll
     for (int s = 0; s < OZ_S; ++s) packed[s] = 0;
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < 4; ++u) {
       const int64_t k = k0 + u;
-      int8_t d[OZ_S];
-      digits8((i < m && k < n) ? ldexp(A[i * lda + k], -e) : 0.0, d);
+      digits8((i < m && k < n) ? ldexp(A[i * lda + k], -e) : 0.0, dd[u]);
 #pragma unroll
-      for (int s = 0; s < OZ_S; ++s) packed[s] |= uint64_t(uint8_t(d[s])) << (8 * u);
+      for (int s = 0; s < OZ_S; ++s) packed[s] |= uint32_t(uint8_t(dd[u][s])) << (8 * u);
     }
-    const int64_t blk = (i / OZB) * NB + k0 / OZB;
-    int8_t* dst = planes + blk * OZ_S * OZ_BLOCK + (i % OZB) * OZB + (k0 % OZB);
+    // imgN: 4 consecutive k stay inside one 16-B chunk
+    int8_t* tn = imgN + ((i / OZB) * KT + k0 / 32) * OZ_S * TILE + img_k32(int(i % OZB), int(k0 % 32));
 #pragma unroll
-    for (int s = 0; s < OZ_S; ++s) *reinterpret_cast<uint64_t*>(dst + s * OZ_BLOCK) = packed[s];
+    for (int s = 0; s < OZ_S; ++s) *reinterpret_cast<uint32_t*>(tn + s * TILE) = packed[s];
+    // imgT: byte (i, k) -> tile (k / 128, i / 32), row i % 32, column k % 128
+    int8_t* tt = imgT + ((k0 / OZB) * IT + i / 32) * OZ_S * TILE;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int off = img_mn128(int(i % 32), int((k0 + u) % OZB));
+#pragma unroll
+      for (int s = 0; s < OZ_S; ++s) tt[s * TILE + off] = dd[u][s];
+    }
   }
 }
 
@@ -210,12 +228,14 @@ __global__ void oz_col_exp_kernel(int64_t N, const unsigned long long* __restric
     col_exp[j] = exp_of(__longlong_as_double(static_cast<long long>(bits[j])));
 }
 
-// 32 (k) x 32 (j) tiles through shared memory: coalesced reads of X rows,
-// coalesced 32-byte runs of k in each output plane row
-__global__ void oz_slice_b_kernel(int64_t K, int64_t N, int64_t Np, const double* __restrict__ X,
-                                  int64_t ldx, const int32_t* __restrict__ row_exp,
-                                  const int32_t* __restrict__ col_exp, int8_t* __restrict__ planes,
-                                  int64_t ldp) {
+// digits of X' into the B-operand images: tile (nt = j / BN, kt = k / 32),
+// plane t: BN rows (j) x 32 B (k), K-major SWIZZLE_32B, at
+// ((nt * KTB + kt) * 8 + t) * BN * 32; j >= N and k >= K are zero.  One
+// block: 32 k x 32 j through shared memory (coalesced X reads).
+__global__ void oz_slice_b_kernel(int64_t K, int64_t N, int64_t Np, int BNmax, int64_t KTB,
+                                  const double* __restrict__ X, int64_t ldx,
+                                  const int32_t* __restrict__ row_exp,
+                                  const int32_t* __restrict__ col_exp, int8_t* __restrict__ img) {
   __shared__ int8_t t8[OZ_S][32][33];
   const int64_t k0 = int64_t(blockIdx.x) * 32, j0 = int64_t(blockIdx.y) * 32;
   const int tx = threadIdx.x, ty = threadIdx.y;   // 32 x 8
@@ -233,12 +253,17 @@ __global__ void oz_slice_b_kernel(int64_t K, int64_t N, int64_t Np, const double
     for (int s = 0; s < OZ_S; ++s) t8[s][tx][r] = d[s];
   }
   __syncthreads();
-  const int64_t plane = Np * ldp;
   for (int r = ty; r < 32; r += 8) {
     const int64_t j = j0 + r, k = k0 + tx;
-    if (j < Np && k < ldp) {
+    const int64_t nt = j / BNmax;
+    const int jj = int(j - nt * BNmax);
+    const int bnt = BNmax;
+    if (j < Np && jj < bnt && k < KTB * 32) {
+      const int64_t tile = int64_t(bnt) * 32;
+      int8_t* dst = img + nt * KTB * OZ_S * int64_t(BNmax) * 32 + (k / 32) * OZ_S * tile +
+                    img_k32(jj, int(k % 32));
 #pragma unroll
-      for (int s = 0; s < OZ_S; ++s) planes[s * plane + j * ldp + k] = t8[s][r][tx];
+      for (int s = 0; s < OZ_S; ++s) dst[s * tile] = t8[s][r][tx];
     }
   }
 }
@@ -248,23 +273,27 @@ __global__ void oz_slice_b_kernel(int64_t K, int64_t N, int64_t Np, const double
 
 template <bool TRANS>
 __global__ void __launch_bounds__(OTHREADS, 1)
-ozaki_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
-                  int M, int N, int BN, int64_t k_per_split, int64_t K,
+ozaki_gemm_kernel(const int8_t* __restrict__ imgA, const int8_t* __restrict__ imgB, int64_t KTA,
+                  int64_t KTB, int M, int N, int BNmax, int64_t k_per_split, int64_t K,
                   const int32_t* __restrict__ row_exp, const int32_t* __restrict__ col_exp,
-                  double* __restrict__ C, int64_t ldc, int64_t cstride) {
+                  double* __restrict__ C, int64_t ldc, int64_t cstride, int dbg) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* base = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // uniform tile width (a narrower last tile -- 64 + 48 for l = 110 -- measured
+  // no faster: the UMMA count per stage, not N, sets the time)
+  const int n0 = blockIdx.x * BNmax;
+  const int BN = BNmax;
   const int b_plane = BN * OBK;
   const int stage_bytes = A_STAGE + OZ_S * b_plane;
-  uint64_t* full = reinterpret_cast<uint64_t*>(base + OST * stage_bytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + OST * (A_STAGE + OZ_S * BNmax * OBK));
   uint64_t* empty = full + OST;
   uint64_t* acc_full = empty + OST;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // N tile fastest in launch order: the CTAs sharing an A tile run together (L2 reuse)
-  const int m0 = blockIdx.y * OBM, n0 = blockIdx.x * BN;
+  const int m0 = blockIdx.y * OBM;
   const int64_t kbeg = int64_t(blockIdx.z) * k_per_split;
   const int64_t kend = min(K, kbeg + k_per_split);
   const int nk = int((kend - kbeg + OBK - 1) / OBK);
@@ -277,7 +306,8 @@ ozaki_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
     mb_init(acc_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  const uint32_t tmem_cols = uint32_t(OZ_ND * BN);   // 256 or 512
+  uint32_t tmem_cols = 32;
+  while (tmem_cols < uint32_t(OZ_ND * BN)) tmem_cols <<= 1;   // power of two, <= 512
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      su32(tmem_slot)),
@@ -296,12 +326,18 @@ ozaki_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
         const uint32_t ph = uint32_t(kt / OST) & 1u;
         const int kc = int(kbeg + int64_t(kt) * OBK);
         mb_wait(&empty[s], ph ^ 1u);
-        mb_expect(&full[s], uint32_t(stage_bytes));
         unsigned char* st = base + s * stage_bytes;
-        // A map dims {col-in-block, row-in-block, plane, block col, block row}
-        if (!TRANS) tma5d(st, &mapA, &full[s], kc % OZB, 0, 0, kc / OZB, m0 / OZB);
-        else        tma5d(st, &mapA, &full[s], 0, kc % OZB, 0, m0 / OZB, kc / OZB);
-        tma3d(st + A_STAGE, &mapB, &full[s], kc, n0, 0);     // [plane][BN rows][32 k]
+        if (dbg == 2) {   // development: no loads (MMA throughput alone)
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&full[s])) : "memory");
+          continue;
+        }
+        mb_expect(&full[s], uint32_t(stage_bytes));
+        // stage images: A tile (m0 / 128, kc / 32), B tile (n0 / BN, kc / 32)
+        bulk_g2s(st, imgA + ((m0 / OZB) * KTA + kc / 32) * int64_t(A_STAGE), uint32_t(A_STAGE),
+                 &full[s]);
+        bulk_g2s(st + A_STAGE, imgB + (n0 / BNmax) * KTB * int64_t(OZ_S * BNmax * OBK) +
+                                   (kc / 32) * int64_t(OZ_S * b_plane),
+                 uint32_t(OZ_S * b_plane), &full[s]);
       }
     }
   } else if (warp == 1) {
@@ -323,7 +359,7 @@ ozaki_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
         asm volatile("tcgen05.fence::after_thread_sync;");
         const unsigned char* st = base + s * stage_bytes;
 #pragma unroll
-        for (int sa = 1; sa <= OZ_S; ++sa) {
+        for (int sa = 1; sa <= (dbg == 1 ? 0 : OZ_S); ++sa) {   // dbg 1: no MMA (loads alone)
           const uint64_t da = TRANS ? desc_mn_sw128(st + (sa - 1) * A_PLANE)
                                     : desc_k_sw32(st + (sa - 1) * A_PLANE);
           const int tmax = (OZ_ND + 1) - sa;   // t <= 9 - sa
@@ -390,10 +426,19 @@ ozaki_gemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constan
   }
 }
 
+int oz_dbg() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("LR_OZ_DEBUG");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
 }  // namespace
 
-// 8 digit planes of A in the blocked layout (ldp = NP: n rounded up to 128;
-// the buffer holds 8 * MP * NP bytes, MP = m rounded up to 128) + row exponents
+// the two digit-plane images of A (see oz_slice_a_kernel): planes holds
+// 16 * MP * NP bytes (imgN, then imgT), ldp = NP (n rounded up to 128)
 void ozaki_prepare(Handle* h, int64_t m, int64_t n, const double* A, int64_t lda, int8_t* planes,
                    int64_t ldp, int32_t* row_exp) {
   LR_REQUIRE(ldp >= n && ldp % OZB == 0, LR_EINVAL,
@@ -402,7 +447,8 @@ void ozaki_prepare(Handle* h, int64_t m, int64_t n, const double* A, int64_t lda
   const int blocks = h->sm_count * 8;
   oz_row_exp_kernel<<<blocks, 256, 0, h->stream>>>(m, n, A, lda, row_exp);
   LR_CHECK_LAUNCH();
-  oz_slice_a_kernel<<<blocks, 256, 0, h->stream>>>(m, n, A, lda, row_exp, planes, MP, ldp);
+  oz_slice_a_kernel<<<blocks, 256, 0, h->stream>>>(m, n, A, lda, row_exp, planes,
+                                                   planes + OZ_S * MP * ldp, MP, ldp);
   LR_CHECK_LAUNCH();
 }
 
@@ -417,9 +463,10 @@ void ozaki_gemm(Handle* h, bool trans, int64_t m, int64_t n, int64_t N, const in
   LR_REQUIRE(N <= 256, LR_EUNSUPPORTED, "ozaki_gemm: more than 256 columns");
   const int BN = N <= 32 ? 32 : 64;
   const int64_t nt = ceil_div(N, BN), Np = nt * BN;
-  const int64_t ldb = ceil_div(K, 16) * 16;
-  // X' planes and column exponents
-  int8_t* bpl = pool_alloc_t<int8_t>(h, size_t(OZ_S) * Np * ldb);
+  const int64_t KTB = ceil_div(K, 32);
+  const int64_t MP = ceil_div(m, OZB) * OZB;
+  // X' images and column exponents
+  int8_t* bpl = pool_alloc_t<int8_t>(h, size_t(OZ_S) * Np * KTB * 32);
   unsigned long long* bits = pool_alloc_t<unsigned long long>(h, size_t(N));
   int32_t* col_exp = pool_alloc_t<int32_t>(h, size_t(N));
   LR_CUDA(cudaMemsetAsync(bits, 0, size_t(N) * sizeof(unsigned long long), h->stream));
@@ -430,27 +477,14 @@ void ozaki_gemm(Handle* h, bool trans, int64_t m, int64_t n, int64_t N, const in
   oz_col_exp_kernel<<<1, 256, 0, h->stream>>>(N, bits, col_exp);
   LR_CHECK_LAUNCH();
   {
-    dim3 grid(unsigned(ceil_div(ldb, 32)), unsigned(ceil_div(Np, 32)));
-    oz_slice_b_kernel<<<grid, dim3(32, 8), 0, h->stream>>>(K, N, Np, X, ldx, rexp_b, col_exp, bpl,
-                                                           ldb);
+    dim3 grid(unsigned(KTB), unsigned(ceil_div(Np, 32)));
+    oz_slice_b_kernel<<<grid, dim3(32, 8), 0, h->stream>>>(K, N, Np, BN, KTB, X, ldx, rexp_b,
+                                                           col_exp, bpl);
     LR_CHECK_LAUNCH();
   }
-  // tensor maps: A planes blocked (see oz_slice_a_kernel), B planes [8][Np][ldb]
-  CUtensorMap mapA, mapB;
-  {
-    const int64_t MB = ceil_div(m, OZB), NB = ldp / OZB;
-    const uint64_t dA[5] = {uint64_t(OZB), uint64_t(OZB), uint64_t(OZ_S), uint64_t(NB), uint64_t(MB)};
-    const uint64_t sA[4] = {uint64_t(OZB), uint64_t(OZ_BLOCK), uint64_t(OZ_S * OZ_BLOCK),
-                            uint64_t(NB * OZ_S * OZ_BLOCK)};
-    const uint32_t bA[5] = {trans ? uint32_t(OBM) : uint32_t(OBK),
-                            trans ? uint32_t(OBK) : uint32_t(OBM), uint32_t(OZ_S), 1, 1};
-    mapA = make_map_nd(CU_TENSOR_MAP_DATA_TYPE_UINT8, planes, 5, dA, sA, bA,
-                       trans ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_32B);
-    const uint64_t dB[3] = {uint64_t(ldb), uint64_t(Np), uint64_t(OZ_S)};
-    const uint64_t sB[2] = {uint64_t(ldb), uint64_t(Np) * ldb};
-    const uint32_t bB[3] = {uint32_t(OBK), uint32_t(BN), uint32_t(OZ_S)};
-    mapB = make_map_3d(CU_TENSOR_MAP_DATA_TYPE_UINT8, bpl, dB, sB, bB, CU_TENSOR_MAP_SWIZZLE_32B);
-  }
+  // A images: imgN tiles (m/128, n/32) for A X, imgT tiles (n/128, m/32) for A^T Y
+  const int8_t* imgA = trans ? planes + OZ_S * MP * ldp : planes;
+  const int64_t KTA = trans ? MP / 32 : ldp / 32;
   const int stage_bytes = A_STAGE + OZ_S * BN * OBK;
   const size_t smem = size_t(OST) * stage_bytes + 1024 + 256;
   auto kern = trans ? ozaki_gemm_kernel<true> : ozaki_gemm_kernel<false>;
@@ -467,14 +501,14 @@ void ozaki_gemm(Handle* h, bool trans, int64_t m, int64_t n, int64_t N, const in
   dim3 grid{unsigned(nt), unsigned(mt), unsigned(splits)};
   const int32_t* rexp_c = trans ? nullptr : row_exp;
   if (splits == 1) {
-    kern<<<grid, OTHREADS, smem, h->stream>>>(mapA, mapB, int(M), int(N), BN, kchunk, K, rexp_c,
-                                              col_exp, C, ldc, 0);
+    kern<<<grid, OTHREADS, smem, h->stream>>>(imgA, bpl, KTA, KTB, int(M), int(N), BN, kchunk, K, rexp_c,
+                                              col_exp, C, ldc, 0, oz_dbg());
     LR_CHECK_LAUNCH();
     return;
   }
   double* part = pool_alloc_t<double>(h, size_t(splits) * M * N);
-  kern<<<grid, OTHREADS, smem, h->stream>>>(mapA, mapB, int(M), int(N), BN, kchunk, K, rexp_c,
-                                            col_exp, part, N, M * N);
+  kern<<<grid, OTHREADS, smem, h->stream>>>(imgA, bpl, KTA, KTB, int(M), int(N), BN, kchunk, K, rexp_c,
+                                            col_exp, part, N, M * N, oz_dbg());
   LR_CHECK_LAUNCH();
   splitk_reduce(h, M, N, int(splits), part, C, ldc);
 }
