@@ -102,6 +102,12 @@ int lr_gemm_scaled(lr_handle_t h, int dtype, int op, int64_t m, int64_t n, int64
  * Y n x ell), ell <= 256, from the planes. */
 int lr_ozaki_prepare(lr_handle_t h, int64_t m, int64_t n, const double* A, int64_t lda,
                      int8_t* planes, int64_t ldp, int32_t* row_exp);
+/* lr_ozaki_prepare for rows [i0, i1) only (A still points at row 0; i0 a
+ * multiple of 128, i1 a multiple of 32 or m): a row-chunked upload prepares
+ * each chunk as it arrives; the chunk ending at m also zero-fills the padding. */
+int lr_ozaki_prepare_rows(lr_handle_t h, int64_t m, int64_t n, int64_t i0, int64_t i1,
+                          const double* A, int64_t lda, int8_t* planes, int64_t ldp,
+                          int32_t* row_exp);
 int lr_gemm_ozaki(lr_handle_t h, int op, int64_t m, int64_t n, int64_t ell,
                   const int8_t* planes, int64_t ldp, const int32_t* row_exp, const double* X,
                   int64_t ldx, double* Y, int64_t ldy);

@@ -52,6 +52,7 @@ _SIGS = {
                        _i64],
     "lr_gram": [_vp, _int, _i64, _i64, _vp, _i64, _vp],
     "lr_ozaki_prepare": [_vp, _i64, _i64, _vp, _i64, _vp, _i64, _vp],
+    "lr_ozaki_prepare_rows": [_vp, _i64, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp],
     "lr_gemm_ozaki": [_vp, _int, _i64, _i64, _i64, _vp, _i64, _vp, _vp, _i64, _vp, _i64],
     "lr_chol_drop": [_vp, _int, _i64, _vp, C.c_double, C.c_double, C.c_double, _vp, _vp, _vp],
     "lr_chol_psd": [_vp, _int, _i64, _vp, C.c_double, _vp, _vp, _vp],

@@ -274,6 +274,13 @@ class DenseOperator(MatVecOperator):
         side.wait_stream(cur)          # t's allocation is ordered before the copies
         chunks = []
         h = _lib.handle(dev.index)
+        # float64: the int8-tensor-core digit planes are built chunk by chunk
+        # behind the copy too (the whole-matrix prepare would follow the upload)
+        oz = None
+        if t.dtype == torch.float64 and _ozaki_size_ok(m, n):
+            ldp, mp = -(-n // 128) * 128, -(-m // 128) * 128
+            oz = (torch.empty(16 * mp * ldp, dtype=torch.int8, device=dev), ldp,
+                  torch.empty(m, dtype=torch.int32, device=dev))
         for i, (r0, r1) in enumerate(bounds):
             with torch.cuda.stream(side):
                 t[r0:r1].copy_(A[r0:r1], non_blocking=True)
@@ -282,8 +289,13 @@ class DenseOperator(MatVecOperator):
             cur.wait_event(ev)
             _lib.call("lr_check_finite", h, self.code, r1 - r0, n, _lib.ptr(t[r0:r1]), n,
                       _lib.ptr(bad[i:i + 1]), _lib.ptr(res[i]))
+            if oz is not None:
+                _lib.call("lr_ozaki_prepare_rows", h, m, n, r0, r1, _lib.ptr(t), n,
+                          _lib.ptr(oz[0]), oz[1], _lib.ptr(oz[2]))
             chunks.append((r0, r1, ev))
         t.record_stream(side)
+        if oz is not None:
+            t._lr_ozaki = (t._version, oz)
         self._pending = chunks
         self._checks = (bad, res, A)   # A stays referenced until the copies are done
 
@@ -451,7 +463,12 @@ def _ozaki_wanted(A, X):
     if mode == "1":
         return True
     m, n = A.shape
-    return m >= 1024 and n >= 512 and ell / -(-ell // 64) >= 40
+    return _ozaki_size_ok(m, n) and ell / -(-ell // 64) >= 40
+
+
+def _ozaki_size_ok(m, n):
+    import os
+    return os.environ.get("LR_OZAKI", "auto") != "0" and m >= 1024 and n >= 512
 
 
 def _ozaki_planes(A):

@@ -646,6 +646,17 @@ int lr_ozaki_prepare(lr_handle_t hh, int64_t m, int64_t n, const double* A, int6
   API_END
 }
 
+int lr_ozaki_prepare_rows(lr_handle_t hh, int64_t m, int64_t n, int64_t i0, int64_t i1,
+                          const double* A, int64_t lda, int8_t* planes, int64_t ldp,
+                          int32_t* row_exp) {
+  API_BEGIN
+  Handle* h = H(hh);
+  LR_REQUIRE(m >= 1 && n >= 1 && lda >= n, LR_EINVAL, "lr_ozaki_prepare_rows: bad dimensions");
+  lr::pool_reset(h);
+  lr::ozaki_prepare_rows(h, m, n, i0, i1, A, lda, planes, ldp, row_exp);
+  API_END
+}
+
 int lr_gemm_ozaki(lr_handle_t hh, int op, int64_t m, int64_t n, int64_t ell,
                   const int8_t* planes, int64_t ldp, const int32_t* row_exp, const double* X,
                   int64_t ldx, double* Y, int64_t ldy) {

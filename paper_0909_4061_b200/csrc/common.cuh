@@ -107,6 +107,8 @@ int64_t choose_splits(int sm_count, int64_t tiles, int64_t K);
 // gemm_f64_ozaki.cu: fp64 passes on the int8 tensor cores (digit planes of A)
 void ozaki_prepare(Handle* h, int64_t m, int64_t n, const double* A, int64_t lda, int8_t* planes,
                    int64_t ldp, int32_t* row_exp);
+void ozaki_prepare_rows(Handle* h, int64_t m, int64_t n, int64_t i0, int64_t i1, const double* A,
+                        int64_t lda, int8_t* planes, int64_t ldp, int32_t* row_exp);
 void ozaki_gemm(Handle* h, bool trans, int64_t m, int64_t n, int64_t N, const int8_t* planes,
                 int64_t ldp, const int32_t* row_exp, const double* X, int64_t ldx, double* C,
                 int64_t ldc);

@@ -140,10 +140,11 @@ __device__ __forceinline__ int exp_of(double amax) {
 // A planes (once per operator): row exponents, then digits
 
 __global__ void oz_row_exp_kernel(int64_t m, int64_t n, const double* __restrict__ A, int64_t lda,
-                                  int32_t* __restrict__ row_exp) {
+                                  int32_t* __restrict__ row_exp, int64_t i0) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5); i < m; i += warps) {
+  for (int64_t i = i0 + blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5); i < m;
+       i += warps) {
     double mx = 0.0;
     const double* row = A + i * lda;
     for (int64_t k = lane; k < n; k += 32) mx = fmax(mx, fabs(row[k]));
@@ -168,13 +169,15 @@ constexpr int64_t TILE = 4096;   // bytes of one plane of one stage tile
 
 __global__ void oz_slice_a_kernel(int64_t m, int64_t n, const double* __restrict__ A, int64_t lda,
                                   const int32_t* __restrict__ row_exp, int8_t* __restrict__ imgN,
-                                  int8_t* __restrict__ imgT, int64_t MP, int64_t NP) {
-  // one thread: 4 consecutive k of one row i (4-byte stores into imgN)
-  const int64_t groups = NP / 4, total = MP * groups;
+                                  int8_t* __restrict__ imgT, int64_t MP, int64_t NP, int64_t i0,
+                                  int64_t i1) {
+  // rows [i0, i1) of the padded MP x NP matrix; one thread: 4 consecutive k of
+  // one row i (4-byte stores into imgN)
+  const int64_t groups = NP / 4, total = (i1 - i0) * groups;
   const int64_t KT = NP / 32, IT = MP / 32;
   for (int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; g < total;
        g += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t i = g / groups, k0 = (g - i * groups) * 4;
+    const int64_t i = i0 + g / groups, k0 = (g % groups) * 4;
     const int e = i < m ? row_exp[i] : 0;
     uint32_t packed[OZ_S];
     int8_t dd[4][OZ_S];
@@ -438,18 +441,29 @@ int oz_dbg() {
 }  // namespace
 
 // the two digit-plane images of A (see oz_slice_a_kernel): planes holds
-// 16 * MP * NP bytes (imgN, then imgT), ldp = NP (n rounded up to 128)
-void ozaki_prepare(Handle* h, int64_t m, int64_t n, const double* A, int64_t lda, int8_t* planes,
-                   int64_t ldp, int32_t* row_exp) {
+// 16 * MP * NP bytes (imgN, then imgT), ldp = NP (n rounded up to 128).
+// Rows [i0, i1) only (i0 a multiple of 128, i1 = m finishes the padding):
+// the streamed upload prepares each chunk as it lands.
+void ozaki_prepare_rows(Handle* h, int64_t m, int64_t n, int64_t i0, int64_t i1, const double* A,
+                        int64_t lda, int8_t* planes, int64_t ldp, int32_t* row_exp) {
   LR_REQUIRE(ldp >= n && ldp % OZB == 0, LR_EINVAL,
              "ozaki_prepare: ldp must be n rounded up to a multiple of 128");
+  LR_REQUIRE(i0 >= 0 && i0 % OZB == 0 && i1 > i0 && i1 <= m, LR_EINVAL,
+             "ozaki_prepare: row range must start at a multiple of 128");
   const int64_t MP = ceil_div(m, OZB) * OZB;
+  const int64_t iend = (i1 == m) ? MP : i1;
+  LR_REQUIRE(iend % 32 == 0, LR_EINVAL, "ozaki_prepare: row range end must be a multiple of 32");
   const int blocks = h->sm_count * 8;
-  oz_row_exp_kernel<<<blocks, 256, 0, h->stream>>>(m, n, A, lda, row_exp);
+  oz_row_exp_kernel<<<blocks, 256, 0, h->stream>>>(i1, n, A, lda, row_exp, i0);
   LR_CHECK_LAUNCH();
   oz_slice_a_kernel<<<blocks, 256, 0, h->stream>>>(m, n, A, lda, row_exp, planes,
-                                                   planes + OZ_S * MP * ldp, MP, ldp);
+                                                   planes + OZ_S * MP * ldp, MP, ldp, i0, iend);
   LR_CHECK_LAUNCH();
+}
+
+void ozaki_prepare(Handle* h, int64_t m, int64_t n, const double* A, int64_t lda, int8_t* planes,
+                   int64_t ldp, int32_t* row_exp) {
+  ozaki_prepare_rows(h, m, n, 0, m, A, lda, planes, ldp, row_exp);
 }
 
 // C = A X (trans = false: A m x n, X n x N, C m x N) or C = A^T X (trans:

@@ -276,3 +276,28 @@ def test_streamed_host_upload(dtype, monkeypatch):
     bad[-1, -1] = np.nan
     with pytest.raises(ValueError):
         m.randomized_svd(torch.from_numpy(bad).pin_memory(), 10, 6, 1, 3, estimate=False)
+
+
+def test_streamed_upload_prepares_digit_planes(monkeypatch):
+    """float64 host upload in chunks also builds the int8-tensor-core digit
+    planes chunk by chunk (lr_ozaki_prepare_rows); the passes that use them
+    give the same factors as planes built from the whole device matrix."""
+    m = lr()
+    from paper_0909_4061_b200 import core
+    monkeypatch.setattr(m.DenseOperator, "STREAM_MIN_BYTES", 1 << 16)
+    monkeypatch.setattr(m.DenseOperator, "STREAM_CHUNK_BYTES", 1 << 18)
+    monkeypatch.setenv("LR_OZAKI", "1")
+    rng = np.random.default_rng(8)
+    An = rng.standard_normal((2100, 640)) * np.exp(-np.arange(640) / 40.0)
+    host = torch.from_numpy(An).pin_memory()
+    op = m.DenseOperator(host)
+    assert op._pending is not None and hasattr(op._array, "_lr_ozaki")
+    chunked = op._array._lr_ozaki[1]
+    b, f, _ = m.randomized_svd(op, 40, 10, 1, 5, estimate=False)
+    dev = torch.from_numpy(An).cuda()
+    whole = core.ozaki_prepare(dev)
+    torch.cuda.synchronize()
+    assert torch.equal(chunked[0], whole[0]) and torch.equal(chunked[2], whole[2])
+    bd, fd, _ = m.randomized_svd(dev, 40, 10, 1, 5, estimate=False)
+    s = fd.sigma.cpu().numpy()
+    assert np.abs(f.sigma - s).max() <= 1e-12 * s[0]
