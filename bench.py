@@ -246,6 +246,8 @@ def run_ours(args, cfg):
     # estimator pass, timed separately
     est_s, est_e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     b, f, _ = step()
+    lr.posterior_error_estimate(op, b.Q, r=10, alpha=10.0, seed=cfg.seed + 13)   # warm-up
+    torch.cuda.synchronize()
     est_s.record()
     est = lr.posterior_error_estimate(op, b.Q, r=10, alpha=10.0, seed=cfg.seed + 13)
     est_e.record()

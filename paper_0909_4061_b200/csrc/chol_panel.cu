@@ -34,6 +34,7 @@ namespace {
 constexpr int NB = 16;     // panel width
 constexpr int NT = 512;    // threads per CTA
 constexpr int NW = NT / 32;
+constexpr int TBS = NB + 2;   // row stride of the inverse's T buffer (bank spread)
 
 // fp64 1/sqrt: MUFU seed + ITER Newton steps (2 give full precision)
 template <int ITER>
@@ -66,7 +67,7 @@ __host__ __device__ constexpr int tile_i() { return sizeof(T) == 8 ? 4 : 2; }
 template <typename T>
 size_t panel_smem_bytes(int n) {
   return size_t(n) * (n + 1) / 2 * sizeof(T)       // W
-         + size_t(n) * NB * sizeof(T)              // T buffer (inverse)
+         + size_t(n) * TBS * sizeof(T)             // T buffer (inverse)
          + size_t(n) * 4 * sizeof(double)          // d0, rd, ri, rti
          + size_t(n) * 2 * sizeof(int) + 64;       // pos, kidx
 }
@@ -87,7 +88,7 @@ chol_panel_kernel(int n, const T* __restrict__ G, int64_t ldg, double drop_tol, 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* W = reinterpret_cast<T*>(smem_raw);
   T* Tb = W + size_t(n) * (n + 1) / 2;
-  double* d0 = reinterpret_cast<double*>(Tb + size_t(n) * NB);
+  double* d0 = reinterpret_cast<double*>(Tb + size_t(n) * TBS);
   double* rd = d0 + n;
   double* ri = rd + n;
   double* rti = ri + n;
@@ -112,27 +113,35 @@ chol_panel_kernel(int n, const T* __restrict__ G, int64_t ldg, double drop_tol, 
   const double trace = s_trace;
   const double thr2 = drop_tol * drop_tol * trace;
   const double shift = shift_coef * trace;
-  // elements of the upper triangle, several loads in flight per thread
-  for (int e0 = tid; e0 < n * n; e0 += 4 * NT) {
-    T v[4];
-    int ii[4], kk[4];
+  // elements of the upper triangle: UL loads in flight per thread, the row
+  // index from a float quotient corrected by one step (no integer division)
+  {
+    constexpr int UL = 8;
+    const float inv_n = 1.0f / float(n);
+    for (int e0 = tid; e0 < n * n; e0 += UL * NT) {
+      T v[UL];
+      int ii[UL], kk[UL];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int e = e0 + u * NT;
-      ii[u] = e / n;
-      kk[u] = e - ii[u] * n;
-      v[u] = (e < n * n && kk[u] >= ii[u]) ? G[size_t(ii[u]) * ldg + kk[u]] : S::zero();
-    }
+      for (int u = 0; u < UL; ++u) {
+        const int e = e0 + u * NT;
+        int i = int(float(e) * inv_n);
+        i -= (i * n > e) ? 1 : 0;
+        i += ((i + 1) * n <= e) ? 1 : 0;
+        ii[u] = i;
+        kk[u] = e - i * n;
+        v[u] = (e < n * n && kk[u] >= i) ? G[size_t(i) * ldg + kk[u]] : S::zero();
+      }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int i = ii[u], k = kk[u];
-      if (e0 + u * NT < n * n && k >= i) {
-        T x = v[u];
-        if (k == i) {
-          x = S::make(S::re(x) + shift, 0.0);
-          d0[i] = diag_src ? S::re(diag_src[size_t(i) * diag_stride]) + shift : S::re(x);
+      for (int u = 0; u < UL; ++u) {
+        const int i = ii[u], k = kk[u];
+        if (e0 + u * NT < n * n && k >= i) {
+          T x = v[u];
+          if (k == i) {
+            x = S::make(S::re(x) + shift, 0.0);
+            d0[i] = diag_src ? S::re(diag_src[size_t(i) * diag_stride]) + shift : S::re(x);
+          }
+          W[poff(n, i) + (k - i)] = x;
         }
-        W[poff(n, i) + (k - i)] = x;
       }
     }
   }
@@ -307,11 +316,16 @@ chol_panel_kernel(int n, const T* __restrict__ G, int64_t ldg, double drop_tol, 
   const int rank = s_rank;
 
   // ---- R output (kept rows/cols), then R~ in place ----
-  for (int i = warp; i < n; i += NW) {
-    const T* rowi = W + poff(n, i) - i;
-    const bool ki = pos[i] >= 0;
-    for (int k = lane; k < n; k += 32)
-      Rout[size_t(i) * n + k] = (k >= i && ki && pos[k] >= 0) ? rowi[k] : S::zero();
+  {
+    const float inv_n = 1.0f / float(n);
+#pragma unroll 4
+    for (int e = tid; e < n * n; e += NT) {
+      int i = int(float(e) * inv_n);
+      i -= (i * n > e) ? 1 : 0;
+      i += ((i + 1) * n <= e) ? 1 : 0;
+      const int k = e - i * n;
+      Rout[e] = (k >= i && pos[i] >= 0 && pos[k] >= 0) ? W[poff(n, i) + (k - i)] : S::zero();
+    }
   }
   __syncthreads();
   if (rank < n) {
@@ -391,60 +405,82 @@ chol_panel_kernel(int n, const T* __restrict__ G, int64_t ldg, double drop_tol, 
         for (int a = 0; a < RB; ++a)
 #pragma unroll
           for (int t = 0; t < 4; ++t)
-            if (i0 + a < j0) Tb[(i0 + a) * NB + c0 + t] = acc[a][t];
+            if (i0 + a < j0) Tb[(i0 + a) * TBS + c0 + t] = acc[a][t];
       }
       __syncthreads();
-      // X(i, j0 + c) = -sum_{k >= i} X(i, k) T(k, c)
-      for (int e = tid; e < nr * nq; e += NT) {
-        const int rq = e / nq, c0 = 4 * (e - rq * nq);
-        const int i0 = RB * rq;
-        const T* xr[RB];
+      // X(i, j0 + c) = -sum_{k >= i} X(i, k) T(k, c): the k-sum of each
+      // RB x 4 output block is split over KS consecutive lanes (interleaved
+      // k) and reduced with shuffles (one thread per block ran chains of up
+      // to j0 dependent steps with most of the CTA idle)
+      {
+        constexpr int KS = 4;
+        const int tot = nr * nq * KS;
+        for (int eb = warp * 32; eb < tot; eb += NT) {
+          const int e = eb + lane;
+          const bool valid = e < tot;
+          const int sub = e & (KS - 1);
+          const int gi = valid ? e / KS : 0;
+          const int rq = gi / nq, c0 = 4 * (gi - rq * nq);
+          const int i0 = RB * rq;
+          const T* xr[RB];
 #pragma unroll
-        for (int a = 0; a < RB; ++a) {
-          const int i = min(i0 + a, j0 - 1);
-          xr[a] = W + poff(n, i) - i;                // xr[a][k] = X(i, k), k >= i
-        }
-        T acc[RB][4];
+          for (int a = 0; a < RB; ++a) {
+            const int i = min(i0 + a, j0 - 1);
+            xr[a] = W + poff(n, i) - i;                // xr[a][k] = X(i, k), k >= i
+          }
+          T acc[RB][4];
 #pragma unroll
-        for (int a = 0; a < RB; ++a)
+          for (int a = 0; a < RB; ++a)
 #pragma unroll
-          for (int t = 0; t < 4; ++t) acc[a][t] = S::zero();
-        // the first RB - 1 columns k are inside the row block's triangle
+            for (int t = 0; t < 4; ++t) acc[a][t] = S::zero();
+          if (valid && sub == 0) {
+            // the first RB - 1 columns k are inside the row block's triangle
 #pragma unroll
-        for (int kk = 0; kk < RB - 1; ++kk) {
-          const int k = i0 + kk;
-          if (k < j0) {
-            const T* tb = Tb + k * NB + c0;
+            for (int kk = 0; kk < RB - 1; ++kk) {
+              const int k = i0 + kk;
+              if (k < j0) {
+                const T* tb = Tb + k * TBS + c0;
 #pragma unroll
-            for (int a = 0; a < RB; ++a) {
-              if (a <= kk) {
-                const T x = xr[a][k];
+                for (int a = 0; a < RB; ++a) {
+                  if (a <= kk) {
+                    const T x = xr[a][k];
 #pragma unroll
-                for (int t = 0; t < 4; ++t) acc[a][t] = S::add(acc[a][t], S::mul(x, tb[t]));
+                    for (int t = 0; t < 4; ++t) acc[a][t] = S::add(acc[a][t], S::mul(x, tb[t]));
+                  }
+                }
               }
             }
           }
-        }
+          const int kend = valid ? j0 : 0;
 #pragma unroll 2
-        for (int k = i0 + RB - 1; k < j0; ++k) {
-          const T* tb = Tb + k * NB + c0;
-          T tv[4];
+          for (int k = i0 + RB - 1 + sub; k < kend; k += KS) {
+            const T* tb = Tb + k * TBS + c0;
+            T tv[4];
 #pragma unroll
-          for (int t = 0; t < 4; ++t) tv[t] = tb[t];
+            for (int t = 0; t < 4; ++t) tv[t] = tb[t];
 #pragma unroll
-          for (int a = 0; a < RB; ++a) {
-            const T x = xr[a][k];
+            for (int a = 0; a < RB; ++a) {
+              const T x = xr[a][k];
 #pragma unroll
-            for (int t = 0; t < 4; ++t) acc[a][t] = S::add(acc[a][t], S::mul(x, tv[t]));
+              for (int t = 0; t < 4; ++t) acc[a][t] = S::add(acc[a][t], S::mul(x, tv[t]));
+            }
           }
-        }
 #pragma unroll
-        for (int a = 0; a < RB; ++a) {
-          if (i0 + a < j0) {
-            T* row = W + poff(n, i0 + a) - (i0 + a) + j0;
+          for (int a = 0; a < RB; ++a)
 #pragma unroll
             for (int t = 0; t < 4; ++t)
-              if (c0 + t < nb) row[c0 + t] = S::scale(acc[a][t], -1.0);
+#pragma unroll
+              for (int o = 1; o < KS; o <<= 1) acc[a][t] = S::add(acc[a][t], S::shfl_xor(acc[a][t], o));
+          if (valid && sub == 0) {
+#pragma unroll
+            for (int a = 0; a < RB; ++a) {
+              if (i0 + a < j0) {
+                T* row = W + poff(n, i0 + a) - (i0 + a) + j0;
+#pragma unroll
+                for (int t = 0; t < 4; ++t)
+                  if (c0 + t < nb) row[c0 + t] = S::scale(acc[a][t], -1.0);
+              }
+            }
           }
         }
       }
@@ -454,12 +490,16 @@ chol_panel_kernel(int n, const T* __restrict__ G, int64_t ldg, double drop_tol, 
 
   PROF_MARK();
   // ---- P: kept columns (compacted or in place), zero elsewhere ----
-  for (int i = warp; i < n; i += NW) {
-    const T* rowi = W + poff(n, i) - i;
-    const bool ki = pos[i] >= 0;
-    for (int q = lane; q < n; q += 32) {
+  {
+    const float inv_n = 1.0f / float(n);
+#pragma unroll 4
+    for (int e = tid; e < n * n; e += NT) {
+      int i = int(float(e) * inv_n);
+      i -= (i * n > e) ? 1 : 0;
+      i += ((i + 1) * n <= e) ? 1 : 0;
+      const int q = e - i * n;
       const int c = compact ? (q < rank ? kidx[q] : -1) : (pos[q] >= 0 ? q : -1);
-      P[size_t(i) * n + q] = (ki && c >= i) ? rowi[c] : S::zero();
+      P[e] = (pos[i] >= 0 && c >= i) ? W[poff(n, i) + (c - i)] : S::zero();
     }
   }
   __syncthreads();

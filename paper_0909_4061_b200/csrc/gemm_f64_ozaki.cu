@@ -212,15 +212,30 @@ __global__ void oz_slice_a_kernel(int64_t m, int64_t n, const double* __restrict
 __global__ void oz_col_max_kernel(int64_t K, int64_t N, const double* __restrict__ X, int64_t ldx,
                                   const int32_t* __restrict__ row_exp,
                                   unsigned long long* __restrict__ bits) {
+  // block (32 x 8): columns tx + 32 c, rows ty + 8 r of the block's row range;
+  // the 8 row lanes combine through shared memory, one atomic per column
+  __shared__ double red[8][33];
   const int64_t rows_per = (K + gridDim.x - 1) / gridDim.x;
   const int64_t k0 = blockIdx.x * rows_per, k1 = min(K, k0 + rows_per);
-  for (int64_t j = threadIdx.x; j < N; j += blockDim.x) {
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  for (int64_t j0 = 0; j0 < N; j0 += 32) {
+    const int64_t j = j0 + tx;
     double mx = 0.0;
-    for (int64_t k = k0; k < k1; ++k) {
-      const double v = X[k * ldx + j];
-      mx = fmax(mx, fabs(row_exp ? ldexp(v, row_exp[k]) : v));
+    if (j < N) {
+#pragma unroll 4
+      for (int64_t k = k0 + ty; k < k1; k += 8) {
+        const double v = X[k * ldx + j];
+        mx = fmax(mx, fabs(row_exp ? ldexp(v, row_exp[k]) : v));
+      }
     }
-    if (mx > 0.0) atomicMax(bits + j, static_cast<unsigned long long>(__double_as_longlong(mx)));
+    red[ty][tx] = mx;
+    __syncthreads();
+    if (ty == 0 && j < N) {
+#pragma unroll
+      for (int r = 1; r < 8; ++r) mx = fmax(mx, red[r][tx]);
+      if (mx > 0.0) atomicMax(bits + j, static_cast<unsigned long long>(__double_as_longlong(mx)));
+    }
+    __syncthreads();
   }
 }
 
@@ -485,8 +500,8 @@ void ozaki_gemm(Handle* h, bool trans, int64_t m, int64_t n, int64_t N, const in
   int32_t* col_exp = pool_alloc_t<int32_t>(h, size_t(N));
   LR_CUDA(cudaMemsetAsync(bits, 0, size_t(N) * sizeof(unsigned long long), h->stream));
   const int32_t* rexp_b = trans ? row_exp : nullptr;   // A^T Y: row scales fold into Y
-  oz_col_max_kernel<<<unsigned(std::min<int64_t>(ceil_div(K, 64), int64_t(h->sm_count) * 4)), 128, 0,
-                      h->stream>>>(K, N, X, ldx, rexp_b, bits);
+  oz_col_max_kernel<<<unsigned(std::min<int64_t>(ceil_div(K, 64), int64_t(h->sm_count) * 4)),
+                      dim3(32, 8), 0, h->stream>>>(K, N, X, ldx, rexp_b, bits);
   LR_CHECK_LAUNCH();
   oz_col_exp_kernel<<<1, 256, 0, h->stream>>>(N, bits, col_exp);
   LR_CHECK_LAUNCH();
