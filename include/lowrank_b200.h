@@ -95,7 +95,7 @@ int lr_gemm_scaled(lr_handle_t h, int dtype, int op, int64_t m, int64_t n, int64
  * core.py:391-395) for float64 A.  lr_ozaki_prepare builds, once per
  * operator, the 8 int8 digit planes of A as the two tiled shared-memory
  * images the pass kernel streams (planes: 16 x MP x ldp bytes, MP = m and
- * ldp = n rounded up to multiples of 128, device memory owned by the
+ * ldp = n rounded up to multiples of 256, device memory owned by the
  * caller) and the
  * row exponents (row_exp: m int32).  lr_gemm_ozaki then computes
  * Y = A X (op N: X n x ell, Y m x ell) or Y = A^T X (op T: X m x ell,
@@ -103,7 +103,7 @@ int lr_gemm_scaled(lr_handle_t h, int dtype, int op, int64_t m, int64_t n, int64
 int lr_ozaki_prepare(lr_handle_t h, int64_t m, int64_t n, const double* A, int64_t lda,
                      int8_t* planes, int64_t ldp, int32_t* row_exp);
 /* lr_ozaki_prepare for rows [i0, i1) only (A still points at row 0; i0 a
- * multiple of 128, i1 a multiple of 32 or m): a row-chunked upload prepares
+ * multiple of 128, i1 a multiple of 128 or m): a row-chunked upload prepares
  * each chunk as it arrives; the chunk ending at m also zero-fills the padding. */
 int lr_ozaki_prepare_rows(lr_handle_t h, int64_t m, int64_t n, int64_t i0, int64_t i1,
                           const double* A, int64_t lda, int8_t* planes, int64_t ldp,

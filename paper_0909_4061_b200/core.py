@@ -278,7 +278,7 @@ class DenseOperator(MatVecOperator):
         # behind the copy too (the whole-matrix prepare would follow the upload)
         oz = None
         if t.dtype == torch.float64 and _ozaki_size_ok(m, n):
-            ldp, mp = -(-n // 128) * 128, -(-m // 128) * 128
+            ldp, mp = -(-n // 256) * 256, -(-m // 256) * 256
             oz = (torch.empty(16 * mp * ldp, dtype=torch.int8, device=dev), ldp,
                   torch.empty(m, dtype=torch.int32, device=dev))
         for i, (r0, r1) in enumerate(bounds):
@@ -417,11 +417,11 @@ def ozaki_prepare(A):
     """Digit planes of a float64 device matrix for the int8-tensor-core fp64
     passes (lr_ozaki_prepare): (planes, ldp, row_exp); planes holds the two
     shared-memory images of the 8 digit planes (A X and A^T Y tiles),
-    16 x MP x ldp bytes (m and n rounded up to 128)."""
+    16 x MP x ldp bytes (m and n rounded up to 256)."""
     torch = _torch()
     m, n = A.shape
-    ldp = -(-n // 128) * 128          # blocked layout: 128 x 128 blocks per plane
-    mp = -(-m // 128) * 128
+    ldp = -(-n // 256) * 256          # tiles of 128, padded to pairs (2-SM kernel)
+    mp = -(-m // 256) * 256
     planes = torch.empty(16 * mp * ldp, dtype=torch.int8, device=A.device)   # two images
     row_exp = torch.empty(m, dtype=torch.int32, device=A.device)
     _lib.call("lr_ozaki_prepare", _lib.handle(A.device.index), m, n, _lib.ptr(A), _lib.ld(A),

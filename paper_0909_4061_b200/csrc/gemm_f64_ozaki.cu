@@ -165,6 +165,7 @@ __global__ void oz_row_exp_kernel(int64_t m, int64_t n, const double* __restrict
 // with m, n padded to multiples of 128 (KT = NP / 32, IT = MP / 32); padding
 // is zero.  Each image holds 8 * MP * NP bytes.
 constexpr int OZB = 128;
+constexpr int OZP = 256;          // m, n padding (the 2-SM kernel pairs 128-row tiles)
 constexpr int64_t TILE = 4096;   // bytes of one plane of one stage tile
 
 __global__ void oz_slice_a_kernel(int64_t m, int64_t n, const double* __restrict__ A, int64_t lda,
@@ -444,6 +445,261 @@ ozaki_gemm_kernel(const int8_t* __restrict__ imgA, const int8_t* __restrict__ im
   }
 }
 
+// ---------------------------------------------------------------------------
+// 2-SM variant (tcgen05.mma.cta_group::2): a CTA pair computes 256 rows x 64
+// columns, one UMMA (issued by the even CTA) covering both SMs' 128-row A
+// tiles.  The B operand of a cta_group::2 UMMA with N columns is split: the
+// first N/2 rows come from the leader's shared memory, the last N/2 from the
+// peer's, at the same address.  Each UMMA here has N = 128 = two X planes, so
+// the peer keeps its X planes shifted by one slot: leader slot p = plane p,
+// peer slot p = plane p + 1, and slot 0 = {zeros | plane 1} starts the odd
+// counts.  For A plane s the planes t = 1..9-s then go in pairs (t, t+1) at
+// slot t (D columns of diagonals s+t, s+t+1), odd counts first through slot 0
+// (diagonals s, s+1, the zero half adding nothing): 20 UMMAs of
+// 256 x 128 x 32 per stage.  Stage readiness of the peer's copies is relayed
+// to the leader by a remote mbarrier arrive; the leader's commits multicast
+// to both CTAs' "empty" and "accumulator full" barriers.
+constexpr int B2_SLOTS = 9;
+constexpr int BN2 = 64;
+constexpr int B2_STAGE = B2_SLOTS * BN2 * OBK;   // 18 KB
+constexpr int ST2 = 4;
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mb_wait_cluster(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "W%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra W%=;\n}" ::"r"(su32(b)),
+      "r"(parity)
+      : "memory");
+}
+// arrive (release, cluster scope) on the barrier at the same offset in CTA `cta`
+__device__ __forceinline__ void mb_arrive_remote(uint64_t* b, uint32_t cta) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\t"
+      "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n\t}" ::"r"(su32(b)),
+      "r"(cta)
+      : "memory");
+}
+__device__ __forceinline__ void umma2_i8(uint32_t tmem, uint64_t adesc, uint64_t bdesc,
+                                         uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma2_commit_both(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          su32(bar)),
+      "h"(uint16_t(3))
+      : "memory");
+}
+
+template <bool TRANS>
+__global__ void __launch_bounds__(OTHREADS, 1)
+ozaki_gemm2_kernel(const int8_t* __restrict__ imgA, const int8_t* __restrict__ imgB, int64_t KTA,
+                   int64_t KTB, int nt, int M, int N, int64_t k_per_split, int64_t K,
+                   const int32_t* __restrict__ row_exp, const int32_t* __restrict__ col_exp,
+                   double* __restrict__ C, int64_t ldc, int64_t cstride) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* base = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr int stage_bytes = A_STAGE + B2_STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + ST2 * stage_bytes);
+  uint64_t* peer_full = full + ST2;
+  uint64_t* empty = peer_full + ST2;
+  uint64_t* acc_full = empty + ST2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int q = int(blockIdx.x >> 1);
+  const int ntile = q % nt, pair = q / nt;
+  const int m0 = (2 * pair + int(rank)) * OBM, n0 = ntile * BN2;
+  const int64_t kbeg = int64_t(blockIdx.z) * k_per_split;
+  const int64_t kend = min(K, kbeg + k_per_split);
+  const int nk = int((kend - kbeg + OBK - 1) / OBK);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < ST2; ++s) {
+      mb_init(&full[s], 1);
+      mb_init(&peer_full[s], 1);
+      mb_init(&empty[s], 1);
+    }
+    mb_init(acc_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     su32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  cluster_sync_all();   // both CTAs' barriers and TMEM exist before any cross-CTA traffic
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const int8_t* bsrc = imgB + (int64_t(ntile) * KTB * 2 + rank) * int64_t(B2_STAGE);
+      for (int kt = 0; kt < nk; ++kt) {
+        const int s = kt % ST2;
+        const uint32_t ph = uint32_t(kt / ST2) & 1u;
+        const int kc = int(kbeg + int64_t(kt) * OBK);
+        mb_wait(&empty[s], ph ^ 1u);
+        mb_expect(&full[s], uint32_t(stage_bytes));
+        unsigned char* st = base + s * stage_bytes;
+        bulk_g2s(st, imgA + ((m0 / OZB) * KTA + kc / 32) * int64_t(A_STAGE), uint32_t(A_STAGE),
+                 &full[s]);
+        bulk_g2s(st + A_STAGE, bsrc + int64_t(kc / 32) * 2 * B2_STAGE, uint32_t(B2_STAGE),
+                 &full[s]);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      if (rank != 0) {
+        // peer: relay "my stage landed" to the leader
+        for (int kt = 0; kt < nk; ++kt) {
+          const int s = kt % ST2;
+          mb_wait(&full[s], uint32_t(kt / ST2) & 1u);
+          mb_arrive_remote(&peer_full[s], 0);
+        }
+      } else {
+        const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((TRANS ? 1u : 0u) << 15) |
+                               (uint32_t(128 >> 3) << 17) | (uint32_t(256 >> 4) << 24);
+        for (int kt = 0; kt < nk; ++kt) {
+          const int s = kt % ST2;
+          const uint32_t ph = uint32_t(kt / ST2) & 1u;
+          mb_wait(&full[s], ph);
+          mb_wait_cluster(&peer_full[s], ph);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const unsigned char* st = base + s * stage_bytes;
+          const unsigned char* bs = st + A_STAGE;
+#pragma unroll
+          for (int sa = 1; sa <= OZ_S; ++sa) {
+            const uint64_t da = TRANS ? desc_mn_sw128(st + (sa - 1) * A_PLANE)
+                                      : desc_k_sw32(st + (sa - 1) * A_PLANE);
+            const int tmax = (OZ_ND + 1) - sa;
+            const uint32_t acc = (kt > 0 || sa > 1) ? 1u : 0u;
+            int t = 1;
+            if (tmax & 1) {   // slot 0: {zeros | plane 1} -> diagonals sa, sa + 1
+              umma2_i8(tmem + uint32_t((sa - 2) * BN2), da, desc_k_sw32(bs), idesc, acc);
+              t = 2;
+            }
+            for (; t < tmax; t += 2)   // slot t: {plane t | plane t + 1}
+              umma2_i8(tmem + uint32_t((sa + t - 2) * BN2), da,
+                       desc_k_sw32(bs + t * BN2 * OBK), idesc, acc);
+          }
+          umma2_commit_both(&empty[s]);
+        }
+        umma2_commit_both(acc_full);
+      }
+    }
+  } else if (warp >= 4) {
+    mb_wait(acc_full, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const int qq = warp - 4;
+    const int row = m0 + qq * 32 + lane;
+    const int re = (row_exp && row < M) ? row_exp[row] : 0;
+    double* wbuf = reinterpret_cast<double*>(base) + qq * (32 * 33);
+    double* cbase = C + int64_t(blockIdx.z) * cstride;
+    for (int c0 = 0; c0 < BN2; c0 += 32) {
+      double acc[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) acc[j] = 0.0;
+#pragma unroll 1
+      for (int d = 9; d >= 2; --d) {
+        uint32_t v[32];
+        const uint32_t taddr = tmem + (uint32_t(qq * 32) << 16) + uint32_t((d - 2) * BN2 + c0);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+            "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+              "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]),
+              "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]),
+              "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+              "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]),
+              "=r"(v[30]), "=r"(v[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        const double w = ldexp(1.0, -(12 + 7 * (d - 2)) + re);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc[j] = fma(double(int32_t(v[j])), w, acc[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < 32; ++j) wbuf[lane * 33 + j] = acc[j];
+      __syncwarp();
+      const int col = n0 + c0 + lane;
+      const int ce = col < N ? col_exp[col] : 0;
+      for (int rr = 0; rr < 32; ++rr) {
+        const int r = m0 + qq * 32 + rr;
+        if (r < M && col < N) cbase[int64_t(r) * ldc + col] = ldexp(wbuf[rr * 33 + lane], ce);
+      }
+      __syncwarp();
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  cluster_sync_all();   // the peer's smem / TMEM stay alive until the pair is done
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
+// X' digits into the 2-SM B images: tile (nt, kt) holds two variants
+// (leader, peer) of 9 slots x 64 rows x 32 B: leader slot p = plane p
+// (slot 0 zero), peer slot p = plane p + 1 (slot 8 zero).  The buffer is
+// zeroed first; each digit is written to its two places.
+__global__ void oz_slice_b2_kernel(int64_t K, int64_t N, int64_t Np, int64_t KTB,
+                                   const double* __restrict__ X, int64_t ldx,
+                                   const int32_t* __restrict__ row_exp,
+                                   const int32_t* __restrict__ col_exp, int8_t* __restrict__ img) {
+  __shared__ int8_t t8[OZ_S][32][33];
+  const int64_t k0 = int64_t(blockIdx.x) * 32, j0 = int64_t(blockIdx.y) * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  for (int r = ty; r < 32; r += 8) {
+    const int64_t k = k0 + r, j = j0 + tx;
+    double v = 0.0;
+    if (k < K && j < N) {
+      v = X[k * ldx + j];
+      if (row_exp) v = ldexp(v, row_exp[k]);
+      v = ldexp(v, -col_exp[j]);
+    }
+    int8_t d[OZ_S];
+    digits8(v, d);
+#pragma unroll
+    for (int s = 0; s < OZ_S; ++s) t8[s][tx][r] = d[s];
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const int64_t j = j0 + r, k = k0 + tx;
+    if (j < Np && k < KTB * 32) {
+      const int64_t nt = j / BN2;
+      int8_t* tile = img + ((nt * KTB + k / 32) * 2) * int64_t(B2_STAGE);
+      const int off = img_k32(int(j % BN2), int(k % 32));
+#pragma unroll
+      for (int s = 0; s < OZ_S; ++s) {
+        const int8_t v = t8[s][r][tx];
+        tile[(s + 1) * BN2 * OBK + off] = v;                        // leader slot s+1 = plane s+1
+        tile[B2_STAGE + s * BN2 * OBK + off] = v;                   // peer slot s = plane s+1
+      }
+    }
+  }
+}
+
 int oz_dbg() {
   static int v = -1;
   if (v < 0) {
@@ -461,11 +717,11 @@ int oz_dbg() {
 // the streamed upload prepares each chunk as it lands.
 void ozaki_prepare_rows(Handle* h, int64_t m, int64_t n, int64_t i0, int64_t i1, const double* A,
                         int64_t lda, int8_t* planes, int64_t ldp, int32_t* row_exp) {
-  LR_REQUIRE(ldp >= n && ldp % OZB == 0, LR_EINVAL,
-             "ozaki_prepare: ldp must be n rounded up to a multiple of 128");
+  LR_REQUIRE(ldp >= n && ldp % OZP == 0, LR_EINVAL,
+             "ozaki_prepare: ldp must be n rounded up to a multiple of 256");
   LR_REQUIRE(i0 >= 0 && i0 % OZB == 0 && i1 > i0 && i1 <= m, LR_EINVAL,
              "ozaki_prepare: row range must start at a multiple of 128");
-  const int64_t MP = ceil_div(m, OZB) * OZB;
+  const int64_t MP = ceil_div(m, OZP) * OZP;
   const int64_t iend = (i1 == m) ? MP : i1;
   LR_REQUIRE(iend % 32 == 0, LR_EINVAL, "ozaki_prepare: row range end must be a multiple of 32");
   const int blocks = h->sm_count * 8;
@@ -481,6 +737,71 @@ void ozaki_prepare(Handle* h, int64_t m, int64_t n, const double* A, int64_t lda
   ozaki_prepare_rows(h, m, n, 0, m, A, lda, planes, ldp, row_exp);
 }
 
+namespace {
+// LR_OZ_2SM=1 forces the CTA-pair kernel, =0 disables it; by default it runs
+// for >= 8192 output rows (config 2: 0.544 / 0.560 ms vs 0.58 / 0.59 ms for
+// A X / A^T Y; on a 4096-row A^T Y with K = 65536 it measured slower)
+bool oz_2sm(int64_t M) {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("LR_OZ_2SM");
+    v = !e ? 2 : (e[0] == '1' ? 1 : 0);
+  }
+  return v == 1 || (v == 2 && M >= 8192);
+}
+
+void ozaki_gemm_2sm(Handle* h, bool trans, int64_t M, int64_t N, int64_t K, const int8_t* imgA,
+                    int64_t KTA, const int32_t* row_exp, const double* X, int64_t ldx,
+                    const int32_t* rexp_b, const int32_t* col_exp, double* C, int64_t ldc) {
+  const int64_t nt = ceil_div(N, BN2), Np = nt * BN2;
+  const int64_t KTB = ceil_div(K, 32);
+  int8_t* bimg = pool_alloc_t<int8_t>(h, size_t(nt) * KTB * 2 * B2_STAGE);
+  LR_CUDA(cudaMemsetAsync(bimg, 0, size_t(nt) * KTB * 2 * B2_STAGE, h->stream));
+  {
+    dim3 grid(unsigned(KTB), unsigned(ceil_div(Np, 32)));
+    oz_slice_b2_kernel<<<grid, dim3(32, 8), 0, h->stream>>>(K, N, Np, KTB, X, ldx, rexp_b, col_exp,
+                                                            bimg);
+    LR_CHECK_LAUNCH();
+  }
+  const size_t smem = size_t(ST2) * (A_STAGE + B2_STAGE) + 1024 + 256;
+  auto kern = trans ? ozaki_gemm2_kernel<true> : ozaki_gemm2_kernel<false>;
+  static bool attr[2] = {false, false};
+  if (!attr[trans]) {
+    LR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    attr[trans] = true;
+  }
+  const int64_t pairs = ceil_div(ceil_div(M, OBM), 2);
+  int64_t want = choose_splits(h->sm_count, 2 * pairs * nt, K);
+  want = std::max<int64_t>(want, ceil_div(K, OZ_KMAX));
+  const int64_t kchunk = ceil_div(ceil_div(K, want), OBK) * OBK;
+  const int64_t splits = ceil_div(K, kchunk);
+  const int32_t* rexp_c = trans ? nullptr : row_exp;
+  double* out = C;
+  int64_t ldo = ldc, cstride = 0;
+  if (splits > 1) {
+    out = pool_alloc_t<double>(h, size_t(splits) * M * N);
+    ldo = N;
+    cstride = M * N;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(unsigned(2 * pairs * nt), 1, unsigned(splits));
+  cfg.blockDim = dim3(OTHREADS, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = h->stream;
+  cudaLaunchAttribute attr2[1];
+  attr2[0].id = cudaLaunchAttributeClusterDimension;
+  attr2[0].val.clusterDim.x = 2;
+  attr2[0].val.clusterDim.y = 1;
+  attr2[0].val.clusterDim.z = 1;
+  cfg.attrs = attr2;
+  cfg.numAttrs = 1;
+  LR_CUDA(cudaLaunchKernelEx(&cfg, kern, imgA, static_cast<const int8_t*>(bimg), KTA, KTB, int(nt),
+                             int(M), int(N), kchunk, K, rexp_c, col_exp, out, ldo, cstride));
+  LR_CHECK_LAUNCH();
+  if (splits > 1) splitk_reduce(h, M, N, int(splits), out, C, ldc);
+}
+}  // namespace
+
 // C = A X (trans = false: A m x n, X n x N, C m x N) or C = A^T X (trans:
 // X m x N, C n x N) from the prepared planes of A.
 void ozaki_gemm(Handle* h, bool trans, int64_t m, int64_t n, int64_t N, const int8_t* planes,
@@ -493,7 +814,7 @@ void ozaki_gemm(Handle* h, bool trans, int64_t m, int64_t n, int64_t N, const in
   const int BN = N <= 32 ? 32 : 64;
   const int64_t nt = ceil_div(N, BN), Np = nt * BN;
   const int64_t KTB = ceil_div(K, 32);
-  const int64_t MP = ceil_div(m, OZB) * OZB;
+  const int64_t MP = ceil_div(m, OZP) * OZP;
   // X' images and column exponents
   int8_t* bpl = pool_alloc_t<int8_t>(h, size_t(OZ_S) * Np * KTB * 32);
   unsigned long long* bits = pool_alloc_t<unsigned long long>(h, size_t(N));
@@ -505,15 +826,19 @@ void ozaki_gemm(Handle* h, bool trans, int64_t m, int64_t n, int64_t N, const in
   LR_CHECK_LAUNCH();
   oz_col_exp_kernel<<<1, 256, 0, h->stream>>>(N, bits, col_exp);
   LR_CHECK_LAUNCH();
+  // A images: imgN tiles (m/128, n/32) for A X, imgT tiles (n/128, m/32) for A^T Y
+  const int8_t* imgA = trans ? planes + OZ_S * MP * ldp : planes;
+  const int64_t KTA = trans ? MP / 32 : ldp / 32;
+  if (oz_2sm(M) && N > 32) {
+    ozaki_gemm_2sm(h, trans, M, N, K, imgA, KTA, row_exp, X, ldx, rexp_b, col_exp, C, ldc);
+    return;
+  }
   {
     dim3 grid(unsigned(KTB), unsigned(ceil_div(Np, 32)));
     oz_slice_b_kernel<<<grid, dim3(32, 8), 0, h->stream>>>(K, N, Np, BN, KTB, X, ldx, rexp_b,
                                                            col_exp, bpl);
     LR_CHECK_LAUNCH();
   }
-  // A images: imgN tiles (m/128, n/32) for A X, imgT tiles (n/128, m/32) for A^T Y
-  const int8_t* imgA = trans ? planes + OZ_S * MP * ldp : planes;
-  const int64_t KTA = trans ? MP / 32 : ldp / 32;
   const int stage_bytes = A_STAGE + OZ_S * BN * OBK;
   const size_t smem = size_t(OST) * stage_bytes + 1024 + 256;
   auto kern = trans ? ozaki_gemm_kernel<true> : ozaki_gemm_kernel<false>;
