@@ -661,13 +661,15 @@ ozaki_gemm2_kernel(const int8_t* __restrict__ imgA, const int8_t* __restrict__ i
 
 // X' digits into the 2-SM B images: tile (nt, kt) holds two variants
 // (leader, peer) of 9 slots x 64 rows x 32 B: leader slot p = plane p
-// (slot 0 zero), peer slot p = plane p + 1 (slot 8 zero).  The buffer is
-// zeroed first; each digit is written to its two places.
+// (slot 0 zero), peer slot p = plane p + 1 (slot 8 zero).  Block: 32 k x 32
+// j through shared memory; a thread then owns one row j and 4 consecutive k
+// (one 4-byte word of a 16-byte chunk in every slot, the zero slots included,
+// so the image needs no separate clearing).
 __global__ void oz_slice_b2_kernel(int64_t K, int64_t N, int64_t Np, int64_t KTB,
                                    const double* __restrict__ X, int64_t ldx,
                                    const int32_t* __restrict__ row_exp,
                                    const int32_t* __restrict__ col_exp, int8_t* __restrict__ img) {
-  __shared__ int8_t t8[OZ_S][32][33];
+  __shared__ __align__(16) int8_t t8[OZ_S][32][36];
   const int64_t k0 = int64_t(blockIdx.x) * 32, j0 = int64_t(blockIdx.y) * 32;
   const int tx = threadIdx.x, ty = threadIdx.y;
   for (int r = ty; r < 32; r += 8) {
@@ -684,18 +686,22 @@ __global__ void oz_slice_b2_kernel(int64_t K, int64_t N, int64_t Np, int64_t KTB
     for (int s = 0; s < OZ_S; ++s) t8[s][tx][r] = d[s];
   }
   __syncthreads();
-  for (int r = ty; r < 32; r += 8) {
-    const int64_t j = j0 + r, k = k0 + tx;
-    if (j < Np && k < KTB * 32) {
-      const int64_t nt = j / BN2;
-      int8_t* tile = img + ((nt * KTB + k / 32) * 2) * int64_t(B2_STAGE);
-      const int off = img_k32(int(j % BN2), int(k % 32));
+  const int t = ty * 32 + tx;           // 256 threads: (row jj, k group kg)
+  const int jj = t >> 3, kg = t & 7;
+  const int64_t j = j0 + jj;
+  if (j < Np && k0 < KTB * 32) {
+    const int64_t nt = j / BN2;
+    int8_t* tile = img + ((nt * KTB + k0 / 32) * 2) * int64_t(B2_STAGE);
+    const int off = img_k32(int(j % BN2), 4 * kg);
+    uint32_t w[OZ_S];
 #pragma unroll
-      for (int s = 0; s < OZ_S; ++s) {
-        const int8_t v = t8[s][r][tx];
-        tile[(s + 1) * BN2 * OBK + off] = v;                        // leader slot s+1 = plane s+1
-        tile[B2_STAGE + s * BN2 * OBK + off] = v;                   // peer slot s = plane s+1
-      }
+    for (int s = 0; s < OZ_S; ++s) w[s] = *reinterpret_cast<const uint32_t*>(&t8[s][jj][4 * kg]);
+    *reinterpret_cast<uint32_t*>(tile + off) = 0u;                                   // leader slot 0
+    *reinterpret_cast<uint32_t*>(tile + B2_STAGE + 8 * BN2 * OBK + off) = 0u;        // peer slot 8
+#pragma unroll
+    for (int s = 0; s < OZ_S; ++s) {
+      *reinterpret_cast<uint32_t*>(tile + (s + 1) * BN2 * OBK + off) = w[s];         // leader
+      *reinterpret_cast<uint32_t*>(tile + B2_STAGE + s * BN2 * OBK + off) = w[s];    // peer
     }
   }
 }
@@ -756,7 +762,6 @@ void ozaki_gemm_2sm(Handle* h, bool trans, int64_t M, int64_t N, int64_t K, cons
   const int64_t nt = ceil_div(N, BN2), Np = nt * BN2;
   const int64_t KTB = ceil_div(K, 32);
   int8_t* bimg = pool_alloc_t<int8_t>(h, size_t(nt) * KTB * 2 * B2_STAGE);
-  LR_CUDA(cudaMemsetAsync(bimg, 0, size_t(nt) * KTB * 2 * B2_STAGE, h->stream));
   {
     dim3 grid(unsigned(KTB), unsigned(ceil_div(Np, 32)));
     oz_slice_b2_kernel<<<grid, dim3(32, 8), 0, h->stream>>>(K, N, Np, KTB, X, ldx, rexp_b, col_exp,
