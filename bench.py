@@ -581,7 +581,8 @@ def e2e_measure(args, cfg, A, lr):
                                     estimate=False)
         return f
 
-    once()
+    for _ in range(3):          # warm-up: allocator / pinned-buffer caches settle by the 3rd call
+        once()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(steps):
