@@ -279,8 +279,11 @@ class DenseOperator(MatVecOperator):
         oz = None
         if t.dtype == torch.float64 and _ozaki_size_ok(m, n):
             ldp, mp = -(-n // 256) * 256, -(-m // 256) * 256
-            oz = (torch.empty(16 * mp * ldp, dtype=torch.int8, device=dev), ldp,
-                  torch.empty(m, dtype=torch.int32, device=dev))
+            try:
+                oz = (torch.empty(16 * mp * ldp, dtype=torch.int8, device=dev), ldp,
+                      torch.empty(m, dtype=torch.int32, device=dev))
+            except torch.cuda.OutOfMemoryError:
+                oz = None        # no room for the planes: DMMA passes
         for i, (r0, r1) in enumerate(bounds):
             with torch.cuda.stream(side):
                 t[r0:r1].copy_(A[r0:r1], non_blocking=True)
@@ -472,10 +475,16 @@ def _ozaki_size_ok(m, n):
 
 
 def _ozaki_planes(A):
+    """The digit planes of A (built on first use), or None when they do not
+    fit in device memory (2 x A's bytes): the passes then stay on DMMA."""
+    torch = _torch()
     cached = getattr(A, "_lr_ozaki", None)
     if cached is not None and cached[0] == A._version:
         return cached[1]
-    oz = ozaki_prepare(A)
+    try:
+        oz = ozaki_prepare(A)
+    except torch.cuda.OutOfMemoryError:
+        oz = None
     A._lr_ozaki = (A._version, oz)
     return oz
 
@@ -485,9 +494,10 @@ def _pass(A, X, Y, adjoint, amax, allow_ozaki=True):
     scaled-fp16 split with the operator's max|A| (lr_gemm_scaled); fp64
     passes of enough columns use the int8-tensor-core emulation
     (lr_gemm_ozaki), the others DMMA."""
-    if allow_ozaki and _ozaki_wanted(A, X):
+    oz = _ozaki_planes(A) if allow_ozaki and _ozaki_wanted(A, X) else None
+    if oz is not None:
         m, n = A.shape
-        ozaki_pass(_ozaki_planes(A), m, n, X, Y, adjoint)
+        ozaki_pass(oz, m, n, X, Y, adjoint)
         return
     code = _lib.dtype_code(A.dtype)
     op = _lib.OP_N if not adjoint else (_lib.OP_C if A.is_complex() else _lib.OP_T)

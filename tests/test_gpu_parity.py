@@ -301,3 +301,24 @@ def test_streamed_upload_prepares_digit_planes(monkeypatch):
     bd, fd, _ = m.randomized_svd(dev, 40, 10, 1, 5, estimate=False)
     s = fd.sigma.cpu().numpy()
     assert np.abs(f.sigma - s).max() <= 1e-12 * s[0]
+
+
+def test_int8_emulated_passes_match_dmma(monkeypatch):
+    """The fp64 passes on the int8 tensor cores (LR_OZAKI=1) and on DMMA
+    (LR_OZAKI=0) give the same randomized SVD to fp64 roundoff, through the
+    subspace-iteration path of config 2 (scaled down), for both the CTA-pair
+    (>= 8192 output rows) and single-CTA kernels."""
+    m = lr()
+    g = np.random.default_rng(21)
+    for rows in (9000, 3000):
+        A = g.standard_normal((rows, 1500)) * (np.arange(1, 1501) ** -0.5)
+        Ad = torch.from_numpy(A).cuda()
+        out = {}
+        for mode in ("1", "0"):
+            monkeypatch.setenv("LR_OZAKI", mode)
+            b, f, _ = m.randomized_svd(Ad.clone(), 60, 10, 2, 3, estimate=False)
+            out[mode] = (b.Q.cpu().numpy(), f.sigma.cpu().numpy(), f.U.cpu().numpy())
+        s1, s0 = out["1"][1], out["0"][1]
+        assert np.abs(s1 - s0).max() <= 1e-13 * s0[0]
+        assert np.abs(out["1"][0] - out["0"][0]).max() <= 1e-10
+        assert np.abs(out["1"][2] - out["0"][2]).max() <= 1e-10
