@@ -516,6 +516,20 @@ static bool cl_mid() {
   return v == 1;
 }
 
+// CTAs of the cluster Jacobi (warps spread over more SMs: fewer warps per SM
+// contending for the shuffle / FP64 pipes on the latency-bound subrounds).
+// Measured (tools/small_probe.py, MIXED): real 110: 2 CTAs 1252 us, 4: 1050,
+// 8: 1039; complex 120: 2416 / 1931 / 2058; real 256: 4 CTAs 4578 us, 8: 3622.
+// LR_JACOBI_CLN overrides (2 | 4 | 8 | 16).
+static int cln(int def) {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("LR_JACOBI_CLN");
+    v = e ? atoi(e) : 0;
+  }
+  return v ? v : def;
+}
+
 void jacobi_blk_f64(Handle* h, int64_t n, const double* R, double* Mout, double* sig,
                     int32_t* info) {
   // thread count = 32 * ceil(ceil(n/4)/2): the register budget per thread is
@@ -524,9 +538,13 @@ void jacobi_blk_f64(Handle* h, int64_t n, const double* R, double* Mout, double*
   else if (n <= 64) launch_blk<double, 2, 256>(h, int(n), R, Mout, sig, info);
   else if (n <= 80) launch_blk<double, 3, 320>(h, int(n), R, Mout, sig, info);
   else if (n <= 96) launch_blk<double, 3, 384>(h, int(n), R, Mout, sig, info);
+  else if (n <= 128 && cl_mid() && cln(8) == 8) launch_cl<double, 4, 8, 2>(h, int(n), R, Mout, sig, info);
+  else if (n <= 128 && cl_mid() && cln(8) == 4) launch_cl<double, 4, 4, 4>(h, int(n), R, Mout, sig, info);
   else if (n <= 128 && cl_mid()) launch_cl<double, 4, 2, 8>(h, int(n), R, Mout, sig, info);
   else if (n <= 112) launch_blk<double, 4, 448>(h, int(n), R, Mout, sig, info);
   else if (n <= 128) launch_blk<double, 4, 512>(h, int(n), R, Mout, sig, info);
+  else if (cln(8) == 16) launch_cl<double, 8, 16, 2>(h, int(n), R, Mout, sig, info);
+  else if (cln(8) == 8) launch_cl<double, 8, 8, 4>(h, int(n), R, Mout, sig, info);
   else launch_cl<double, 8, 4, 8>(h, int(n), R, Mout, sig, info);
 }
 
@@ -535,6 +553,8 @@ void jacobi_blk_c128(Handle* h, int64_t n, const double2* R, double2* Mout, doub
   if (n <= 32) launch_blk<double2, 1, 128>(h, int(n), R, Mout, sig, info);
   else if (n <= 48) launch_blk<double2, 2, 192>(h, int(n), R, Mout, sig, info);
   else if (n <= 64) launch_blk<double2, 2, 256>(h, int(n), R, Mout, sig, info);
+  else if (cln(4) == 8) launch_cl<double2, 4, 8, 2>(h, int(n), R, Mout, sig, info);
+  else if (cln(4) == 4) launch_cl<double2, 4, 4, 4>(h, int(n), R, Mout, sig, info);
   else launch_cl<double2, 4, 2, 8>(h, int(n), R, Mout, sig, info);
 }
 
