@@ -4,7 +4,7 @@
 set -u
 OUT=${OUT:-gpurun_out/prof}
 run() { OUT=$OUT CONFIGS="$1" PASS_KERNELS="$2" PASS_SKIP=${3:-6} bash tools/profile_round.sh; }
-run 2 "ozaki_gemm_kernel"
+run 2 "ozaki_gemm"
 run 1 "gemm_f64_kernel" 12
 run 3 "gemm_f32_tc_kernel"
 run 4 "gemm_f32_tc_kernel"
