@@ -354,7 +354,8 @@ def roofline(A, cfg, pev, ms, steps, passes, a_bytes):
         return {"bound": "tensor", "achieved": round(achieved_i8, 1), "peak": round(i8_peak, 1),
                 "unit": "TOP/s (int8)", "frac": round(achieved_i8 / i8_peak, 4),
                 "traffic": traffic,
-                "kernel": "ozaki_gemm_kernel: fp64 pass over A as 36 exact int8 digit-plane "
+                "kernel": "ozaki_gemm2_kernel (CTA pairs; ozaki_gemm_kernel below 8192 "
+                          "output rows): fp64 pass over A as 36 exact int8 digit-plane "
                           "products on tcgen05 (lr_gemm_ozaki)",
                 "peak_source": "measured in-run: cuBLASLt int8 GEMM 8192^3 (torch._int_mm)",
                 "int8_ops_per_pass": i8_ops,
