@@ -347,8 +347,17 @@ def roofline(A, cfg, pev, ms, steps, passes, a_bytes):
         # roofline (the native fp64 bound) is kept beside it
         i8_peak = measured_int8_peak()
         m, n = A.shape
-        ntile = -(-cfg.ell // 64) * 64 if cfg.ell > 32 else 32
-        i8_ops = 36 * 2.0 * m * n * ntile
+        # the tensor work the kernel issues (gemm_f64_ozaki.cu): CTA pairs
+        # (>= 8192 output rows, 56-column tiles) 20 UMMAs of 2 x 56 columns per
+        # 32-deep stage = 40 digit products per tile column; single CTAs 36
+        # products over 64-column tiles (32 when l <= 32)
+        pair = (m >= 8192 and -(-cfg.ell // 56) * 56 <= -(-cfg.ell // 64) * 64
+                and cfg.ell > 32)
+        if pair:
+            i8_ops = 40 * 2.0 * m * n * (-(-cfg.ell // 56) * 56)
+        else:
+            ntile = -(-cfg.ell // 64) * 64 if cfg.ell > 32 else 32
+            i8_ops = 36 * 2.0 * m * n * ntile
         achieved_i8 = i8_ops / (avg_pass_ms / 1e3) / 1e12
         roof_i8_s = max(i8_ops / (i8_peak * 1e12), a_bytes / (hbm * 1e9))
         return {"bound": "tensor", "achieved": round(achieved_i8, 1), "peak": round(i8_peak, 1),

@@ -446,22 +446,24 @@ ozaki_gemm_kernel(const int8_t* __restrict__ imgA, const int8_t* __restrict__ im
 }
 
 // ---------------------------------------------------------------------------
-// 2-SM variant (tcgen05.mma.cta_group::2): a CTA pair computes 256 rows x 64
+// 2-SM variant (tcgen05.mma.cta_group::2): a CTA pair computes 256 rows x 56
 // columns, one UMMA (issued by the even CTA) covering both SMs' 128-row A
 // tiles.  The B operand of a cta_group::2 UMMA with N columns is split: the
 // first N/2 rows come from the leader's shared memory, the last N/2 from the
-// peer's, at the same address.  Each UMMA here has N = 128 = two X planes, so
-// the peer keeps its X planes shifted by one slot: leader slot p = plane p,
-// peer slot p = plane p + 1, and slot 0 = {zeros | plane 1} starts the odd
-// counts.  For A plane s the planes t = 1..9-s then go in pairs (t, t+1) at
-// slot t (D columns of diagonals s+t, s+t+1), odd counts first through slot 0
-// (diagonals s, s+1, the zero half adding nothing): 20 UMMAs of
-// 256 x 128 x 32 per stage.  Stage readiness of the peer's copies is relayed
-// to the leader by a remote mbarrier arrive; the leader's commits multicast
-// to both CTAs' "empty" and "accumulator full" barriers.
-constexpr int B2_SLOTS = 9;
-constexpr int BN2 = 64;
-constexpr int B2_STAGE = B2_SLOTS * BN2 * OBK;   // 18 KB
+// peer's, at the same address.  Each UMMA here has N = 112 = two X planes, so
+// the peer keeps its X planes shifted by one slot: leader slot p = plane p+1,
+// peer slot p = plane p+2.  For A plane s the planes t = 1..9-s go in pairs
+// (t, t+1), t odd, at slot t-1 (D columns of diagonals s+t, s+t+1); an odd
+// count's last pair reaches diagonal 10, kept in a 10th accumulator (9 x 56 =
+// 504 TMEM columns) as an extra, correct high-order term -- no zero halves,
+// and l = 110 pads to 112 columns, not 128.  20 UMMAs of 256 x 112 x 32 per
+// stage.  Stage readiness of the peer's copies is relayed to the leader by a
+// remote mbarrier arrive; the leader's commits multicast to both CTAs' "empty"
+// and "accumulator full" barriers.
+constexpr int B2_SLOTS = 8;
+constexpr int BN2 = 56;
+constexpr int ND2 = 9;                           // diagonals d = 2..10
+constexpr int B2_STAGE = B2_SLOTS * BN2 * OBK;   // 14 KB
 constexpr int ST2 = 4;
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -548,9 +550,24 @@ ozaki_gemm2_kernel(const int8_t* __restrict__ imgA, const int8_t* __restrict__ i
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
-  cluster_sync_all();   // both CTAs' barriers and TMEM exist before any cross-CTA traffic
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tmem_slot;
+  if (warp >= 4) {
+    // the d = 10 accumulator is only ever accumulated into: zero it (each
+    // epilogue warp its 32 lanes) before the pair's first UMMA
+    const uint32_t base10 = tmem + (uint32_t((warp - 4) * 32) << 16) + uint32_t((ND2 - 1) * BN2);
+#pragma unroll
+    for (int c = 0; c < BN2; c += 8)
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(
+                       base10 + uint32_t(c)),
+                   "r"(0u)
+                   : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  cluster_sync_all();   // both CTAs' barriers and TMEM (zeroed d = 10) ready before cross-CTA traffic
+  asm volatile("tcgen05.fence::after_thread_sync;");
 
   if (warp == 0) {
     if (lane == 0) {
@@ -579,7 +596,7 @@ ozaki_gemm2_kernel(const int8_t* __restrict__ imgA, const int8_t* __restrict__ i
         }
       } else {
         const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((TRANS ? 1u : 0u) << 15) |
-                               (uint32_t(128 >> 3) << 17) | (uint32_t(256 >> 4) << 24);
+                               (uint32_t((2 * BN2) >> 3) << 17) | (uint32_t(256 >> 4) << 24);
         for (int kt = 0; kt < nk; ++kt) {
           const int s = kt % ST2;
           const uint32_t ph = uint32_t(kt / ST2) & 1u;
@@ -593,15 +610,11 @@ ozaki_gemm2_kernel(const int8_t* __restrict__ imgA, const int8_t* __restrict__ i
             const uint64_t da = TRANS ? desc_mn_sw128(st + (sa - 1) * A_PLANE)
                                       : desc_k_sw32(st + (sa - 1) * A_PLANE);
             const int tmax = (OZ_ND + 1) - sa;
+            // sa = 1 at the first stage writes diagonals 2..9 (d = 10 is pre-zeroed)
             const uint32_t acc = (kt > 0 || sa > 1) ? 1u : 0u;
-            int t = 1;
-            if (tmax & 1) {   // slot 0: {zeros | plane 1} -> diagonals sa, sa + 1
-              umma2_i8(tmem + uint32_t((sa - 2) * BN2), da, desc_k_sw32(bs), idesc, acc);
-              t = 2;
-            }
-            for (; t < tmax; t += 2)   // slot t: {plane t | plane t + 1}
+            for (int t = 1; t <= tmax; t += 2)   // slot t-1: {plane t | plane t + 1}
               umma2_i8(tmem + uint32_t((sa + t - 2) * BN2), da,
-                       desc_k_sw32(bs + t * BN2 * OBK), idesc, acc);
+                       desc_k_sw32(bs + (t - 1) * BN2 * OBK), idesc, acc);
           }
           umma2_commit_both(&empty[s]);
         }
@@ -621,7 +634,7 @@ ozaki_gemm2_kernel(const int8_t* __restrict__ imgA, const int8_t* __restrict__ i
 #pragma unroll
       for (int j = 0; j < 32; ++j) acc[j] = 0.0;
 #pragma unroll 1
-      for (int d = 9; d >= 2; --d) {
+      for (int d = ND2 + 1; d >= 2; --d) {
         uint32_t v[32];
         const uint32_t taddr = tmem + (uint32_t(qq * 32) << 16) + uint32_t((d - 2) * BN2 + c0);
         asm volatile(
@@ -643,10 +656,11 @@ ozaki_gemm2_kernel(const int8_t* __restrict__ imgA, const int8_t* __restrict__ i
       for (int j = 0; j < 32; ++j) wbuf[lane * 33 + j] = acc[j];
       __syncwarp();
       const int col = n0 + c0 + lane;
-      const int ce = col < N ? col_exp[col] : 0;
+      const bool cok = c0 + lane < BN2 && col < N;   // columns past the tile belong to the next diagonal
+      const int ce = cok ? col_exp[col] : 0;
       for (int rr = 0; rr < 32; ++rr) {
         const int r = m0 + qq * 32 + rr;
-        if (r < M && col < N) cbase[int64_t(r) * ldc + col] = ldexp(wbuf[rr * 33 + lane], ce);
+        if (r < M && cok) cbase[int64_t(r) * ldc + col] = ldexp(wbuf[rr * 33 + lane], ce);
       }
       __syncwarp();
     }
@@ -660,8 +674,8 @@ ozaki_gemm2_kernel(const int8_t* __restrict__ imgA, const int8_t* __restrict__ i
 }
 
 // X' digits into the 2-SM B images: tile (nt, kt) holds two variants
-// (leader, peer) of 9 slots x 64 rows x 32 B: leader slot p = plane p
-// (slot 0 zero), peer slot p = plane p + 1 (slot 8 zero).  Block: 32 k x 32
+// (leader, peer) of 8 slots x 56 rows x 32 B: leader slot p = plane p + 1,
+// peer slot p = plane p + 2 (slot 7 zero).  Block: 32 k x 32
 // j through shared memory; a thread then owns one row j and 4 consecutive k
 // (one 4-byte word of a 16-byte chunk in every slot, the zero slots included,
 // so the image needs no separate clearing).
@@ -696,12 +710,12 @@ __global__ void oz_slice_b2_kernel(int64_t K, int64_t N, int64_t Np, int64_t KTB
     uint32_t w[OZ_S];
 #pragma unroll
     for (int s = 0; s < OZ_S; ++s) w[s] = *reinterpret_cast<const uint32_t*>(&t8[s][jj][4 * kg]);
-    *reinterpret_cast<uint32_t*>(tile + off) = 0u;                                   // leader slot 0
-    *reinterpret_cast<uint32_t*>(tile + B2_STAGE + 8 * BN2 * OBK + off) = 0u;        // peer slot 8
+    *reinterpret_cast<uint32_t*>(tile + B2_STAGE + 7 * BN2 * OBK + off) = 0u;        // peer slot 7
 #pragma unroll
     for (int s = 0; s < OZ_S; ++s) {
-      *reinterpret_cast<uint32_t*>(tile + (s + 1) * BN2 * OBK + off) = w[s];         // leader
-      *reinterpret_cast<uint32_t*>(tile + B2_STAGE + s * BN2 * OBK + off) = w[s];    // peer
+      *reinterpret_cast<uint32_t*>(tile + s * BN2 * OBK + off) = w[s];               // leader: plane s+1
+      if (s >= 1)   // peer: plane s+1 at slot s-1
+        *reinterpret_cast<uint32_t*>(tile + B2_STAGE + (s - 1) * BN2 * OBK + off) = w[s];
     }
   }
 }
@@ -745,15 +759,18 @@ void ozaki_prepare(Handle* h, int64_t m, int64_t n, const double* A, int64_t lda
 
 namespace {
 // LR_OZ_2SM=1 forces the CTA-pair kernel, =0 disables it; by default it runs
-// for >= 8192 output rows (config 2: 0.544 / 0.560 ms vs 0.58 / 0.59 ms for
+// for >= 8192 output rows (config 2: 0.530 / 0.540 ms vs 0.58 / 0.59 ms for
 // A X / A^T Y; on a 4096-row A^T Y with K = 65536 it measured slower)
-bool oz_2sm(int64_t M) {
+// ... and only where its 56-column tiles pad less than the single-CTA kernel's
+// 64-column ones (l = 110: 112 vs 128 columns; at l = 128 the pair kernel's
+// 3 x 56 measured 1.3 / 1.45 ms against 1.0 / 1.06 ms for 2 x 64).
+bool oz_2sm(int64_t M, int64_t N) {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("LR_OZ_2SM");
     v = !e ? 2 : (e[0] == '1' ? 1 : 0);
   }
-  return v == 1 || (v == 2 && M >= 8192);
+  return v == 1 || (v == 2 && M >= 8192 && ceil_div(N, 56) * 56 <= ceil_div(N, 64) * 64);
 }
 
 void ozaki_gemm_2sm(Handle* h, bool trans, int64_t M, int64_t N, int64_t K, const int8_t* imgA,
@@ -834,7 +851,7 @@ void ozaki_gemm(Handle* h, bool trans, int64_t m, int64_t n, int64_t N, const in
   // A images: imgN tiles (m/128, n/32) for A X, imgT tiles (n/128, m/32) for A^T Y
   const int8_t* imgA = trans ? planes + OZ_S * MP * ldp : planes;
   const int64_t KTA = trans ? MP / 32 : ldp / 32;
-  if (oz_2sm(M) && N > 32) {
+  if (oz_2sm(M, N) && N > 32) {
     ozaki_gemm_2sm(h, trans, M, N, K, imgA, KTA, row_exp, X, ldx, rexp_b, col_exp, C, ldc);
     return;
   }
