@@ -44,7 +44,9 @@ def parse():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
-    p.add_argument("--config", type=int, default=2)
+    p.add_argument("--config", type=int, default=4,
+                   help="BASELINE.json config (default 4: the largest single-GPU config, "
+                        "north_star's row-sharded scaling config)")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
@@ -178,18 +180,31 @@ def peaks():
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
 
 
-def cpu_baseline(cfg, A_host, steps=1):
-    """The CPU oracle on the same A with all host threads (kind "port")."""
+def config_dict(cfg, world):
+    """The `config` object of every line (both arms, every N): identical
+    keys and values so the driver can match them."""
+    return {"workload": cfg.name, "config_index": cfg.idx, "m": cfg.m, "n": cfg.n,
+            "k": cfg.k, "ell": cfg.ell, "q": cfg.q, "sketch": cfg.sketch,
+            "passes": cfg.passes(), "a_bytes": cfg.a_bytes(),
+            "a_bytes_model": ("CSR values f64 + int32 cols + int64 rowptr" if cfg.idx == 5
+                              else "dense A in its storage dtype"),
+            "l2": "inputs larger than the 126 MB L2 (A >= 512 MiB per GPU), no flush",
+            "parallelism": f"row-sharded x{world}" if world > 1 else "single GPU"}
+
+
+def cpu_baseline(cfg, A_dev=None):
+    """The CPU oracle (kind "port": numpy/OpenBLAS with all host threads) on
+    a bounded sample of the same workload; returns the line's cpu_baseline
+    object (rate in A-GB/s = passes x sample bytes / seconds)."""
     from oracle import lowrank_oracle as O
-    cores = os.cpu_count()
-    op = O.Dense(A_host, promote=True)
-    best = None
-    for _ in range(steps):
-        t0 = time.perf_counter()
-        O.rsvd(op, cfg.k, cfg.p, cfg.q, cfg.seed, sketch=cfg.sketch, estimate=False)
-        dt = time.perf_counter() - t0
-        best = dt if best is None else min(best, dt)
-    return best, cores
+    op, a_bytes, sample = reference_sample(cfg, A_dev)
+    t0 = time.perf_counter()
+    O.rsvd(op, cfg.k, cfg.p, cfg.q, cfg.seed, sketch=cfg.sketch, estimate=False)
+    dt = time.perf_counter() - t0
+    return {"value": round(cfg.passes() * a_bytes / dt / 1e9, 4), "unit": "A-GB/s",
+            "cores": os.cpu_count(), "kind": "port",
+            "sample": f"{sample}: one rSVD (Stage A + direct SVD) by oracle/lowrank_oracle.py, "
+                      f"{dt:.2f} s", "seconds": round(dt, 3)}
 
 
 # ---------------------------------------------------------------------------
@@ -264,11 +279,7 @@ def run_ours(args, cfg):
         "dtype": {torch.float64: "f64", torch.float32: "f32", torch.complex64: "c64",
                   torch.complex128: "c128"}[A.dtype],
         "data": "synthetic (seeded, BASELINE.json config recipe; see workloads.py)",
-        "config": {"workload": cfg.name, "config_index": cfg.idx, "m": cfg.m, "n": cfg.n,
-                   "k": cfg.k, "ell": cfg.ell, "q": cfg.q, "sketch": cfg.sketch,
-                   "passes": passes, "a_bytes": a_bytes,
-                   "l2": "inputs larger than L2 (A >= 1 GiB), no flush",
-                   "parallelism": f"rows x{world}" if world > 1 else "single GPU"},
+        "config": config_dict(cfg, world),
         "roofline": roof,
         "estimator_ms": round(est_ms, 4),
         "gpu_launches": int(launches),
@@ -277,15 +288,21 @@ def run_ours(args, cfg):
 
     if not args.no_e2e and rank == 0:
         line["e2e"] = e2e_measure(args, cfg, A, lr)
+    if A.dtype == torch.float64 and lrcore._ozaki_wanted(
+            A, torch.empty((1, cfg.ell), dtype=A.dtype, device=A.device)):
+        # the int8 digit planes are built once per operator (cached on A) and
+        # are not part of the timed steps: their build time, reported here
+        ps, pe = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ps.record()
+        lrcore.ozaki_prepare(A)
+        pe.record()
+        torch.cuda.synchronize()
+        line["digit_plane_build_ms"] = round(ps.elapsed_time(pe), 4)
+        line["digit_plane_build_note"] = (
+            "once per operator (reads A, writes 2 x A's bytes); outside the timed steps, "
+            "inside every e2e step")
     if not args.no_cpu and rank == 0 and world == 1:
-        A_host = A.cpu().numpy()
-        t_cpu, cores = cpu_baseline(cfg, A_host)
-        line["cpu_baseline"] = {"value": round(passes * a_bytes / t_cpu / 1e9, 4),
-                                "unit": "A-GB/s", "cores": cores, "kind": "port",
-                                "sample": f"one full {cfg.name} rSVD (Stage A + direct SVD) "
-                                          f"by oracle/lowrank_oracle.py, "
-                                          f"{t_cpu:.2f} s",
-                                "seconds": round(t_cpu, 3)}
+        line["cpu_baseline"] = cpu_baseline(cfg, A)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -351,13 +368,10 @@ def roofline(A, cfg, pev, ms, steps, passes, a_bytes):
         # (>= 8192 output rows, 56-column tiles) 20 UMMAs of 2 x 56 columns per
         # 32-deep stage = 40 digit products per tile column; single CTAs 36
         # products over 64-column tiles (32 when l <= 32)
-        pair = (m >= 8192 and -(-cfg.ell // 56) * 56 <= -(-cfg.ell // 64) * 64
-                and cfg.ell > 32)
-        if pair:
-            i8_ops = 40 * 2.0 * m * n * (-(-cfg.ell // 56) * 56)
-        else:
-            ntile = -(-cfg.ell // 64) * 64 if cfg.ell > 32 else 32
-            i8_ops = 36 * 2.0 * m * n * ntile
+        # algorithmic int8 work only: the 36 digit products (s + t <= 9) over
+        # the ell real columns -- not the padded tile columns nor the extra
+        # 10th-diagonal products the CTA-pair kernel issues
+        i8_ops = 36 * 2.0 * m * n * cfg.ell
         achieved_i8 = i8_ops / (avg_pass_ms / 1e3) / 1e12
         roof_i8_s = max(i8_ops / (i8_peak * 1e12), a_bytes / (hbm * 1e9))
         return {"bound": "tensor", "achieved": round(achieved_i8, 1), "peak": round(i8_peak, 1),
@@ -379,6 +393,32 @@ def roofline(A, cfg, pev, ms, steps, passes, a_bytes):
                 "step_roofline_basis": "fp64 flops at the DMMA peak vs A bytes at HBM, per pass",
                 "step_roofline_int8_ms": round(passes * roof_i8_s * 1e3, 4),
                 "step_roofline_int8_frac": round(passes * roof_i8_s * 1e3 / ms, 4),
+                "pass_share_of_step": round(sum(pass_ms) / (ms * steps), 4)}
+    if A.dtype in (torch.float32, torch.complex64):
+        # the tcgen05 pass issues three fp16 products per algorithmic product
+        # (hi*hi + hi*lo + lo*hi): the kernel's own
+        # bound is that tensor work at the bf16/fp16 peak; the north_star step
+        # roofline (per pass max(2mnl at the 1x-TF32 rate, A bytes at HBM)) is
+        # HBM-bound for fp32 and is reported beside it
+        issued = 3.0 * avg_flops
+        ach3 = issued / (avg_pass_ms / 1e3) / 1e12
+        roof_pass_s = max(avg_flops / (0.5 * peak_tf * 1e12), a_bytes / (hbm * 1e9))
+        roof_step_ms = passes * roof_pass_s * 1e3
+        return {"bound": "tensor", "achieved": round(ach3, 3), "peak": round(peak_tf, 3),
+                "unit": "TFLOP/s (fp16 issued)", "frac": round(ach3 / peak_tf, 4),
+                "traffic": traffic,
+                "kernel": "gemm_f32_tc pass over A (tcgen05 kind::f16, 3-product split)",
+                "peak_source": peak_src, "avg_pass_ms": round(avg_pass_ms, 4),
+                "algorithmic_tflops": round(achieved_tf, 3),
+                "issued_flops_per_pass": issued,
+                "pass_a_gbs": round(a_bytes / (avg_pass_ms / 1e3) / 1e9, 1),
+                "hbm_frac": round(a_bytes / (avg_pass_ms / 1e3) / 1e9 / hbm, 4),
+                "step_roofline_ms": round(roof_step_ms, 4),
+                "step_roofline_frac": round(roof_step_ms / ms, 4),
+                "step_roofline_basis": "per pass max(2mnl at 1x TF32 = half the bf16 peak, "
+                                       "A bytes at HBM) -- HBM-bound",
+                "step_roofline_3product_ms": round(passes * max(
+                    issued / (peak_tf * 1e12), a_bytes / (hbm * 1e9)) * 1e3, 4),
                 "pass_share_of_step": round(sum(pass_ms) / (ms * steps), 4)}
     return {"bound": "tensor", "achieved": round(achieved_tf, 3), "peak": round(peak_tf, 3),
             "unit": "TFLOP/s", "frac": round(achieved_tf / peak_tf, 4),
@@ -430,11 +470,7 @@ def run_sparse(args, cfg):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded CSR + Gaussian low-rank factors, BASELINE.json config 5)",
-        "config": {"workload": cfg.name, "config_index": 5, "m": cfg.m, "n": cfg.n, "nnz": op.nnz,
-                   "k": cfg.k, "ell": cfg.ell, "q": cfg.q, "passes": passes,
-                   "a_bytes": a_bytes, "a_bytes_model": "CSR values + int32 cols + int64 rowptr",
-                   "l2": "inputs larger than L2 (CSR 0.4 GB, X 0.8 GB), no flush",
-                   "parallelism": "single GPU"},
+        "config": config_dict(cfg, world),
         "roofline": roofline_sparse(cfg, pev, ms, args.steps, passes),
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
@@ -442,20 +478,7 @@ def run_sparse(args, cfg):
                            "not measured for config 5 in this round"},
     }
     if not args.no_cpu and rank == 0:
-        # bounded CPU sample: the oracle (scipy CSR, single-threaded SpMM) on a
-        # 2^17-row instance of the same recipe, rate in A-GB/s
-        from oracle import lowrank_oracle as O
-        S2, L2, R2 = workloads.build_cfg5(n=1 << 17)
-        op2 = O.SparsePlusLowRank(S2, L2, R2)
-        t0 = time.perf_counter()
-        O.rsvd(op2, cfg.k, cfg.p, cfg.q, cfg.seed, estimate=False)
-        dt = time.perf_counter() - t0
-        b2 = S2.nnz * 12 + (S2.shape[0] + 1) * 8
-        line["cpu_baseline"] = {"value": round(passes * b2 / dt / 1e9, 4), "unit": "A-GB/s",
-                                "cores": os.cpu_count(), "kind": "port",
-                                "sample": f"config-5 recipe at n = 2^17 ({S2.nnz} nnz), one rSVD "
-                                          f"by oracle/lowrank_oracle.py (scipy CSR), {dt:.2f} s",
-                                "seconds": round(dt, 3)}
+        line["cpu_baseline"] = cpu_baseline(cfg)
     if rank == 0:
         print(json.dumps(line), flush=True)
 
@@ -472,6 +495,7 @@ def run_sharded(args, cfg):
     from paper_0909_4061_b200.dist import (Comm, GpuBackend, dist_randomized_svd, row_range,
                                            sharded_randomized_svd)
     rank, world, local = env_rank()
+    os.environ.setdefault("NCCL_DEBUG", "INFO")     # rank/NVLink setup in the log
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
@@ -539,12 +563,8 @@ def run_sharded(args, cfg):
         "dtype": {torch.float64: "f64", torch.float32: "f32", torch.complex64: "c64",
                   torch.complex128: "c128"}[A.dtype],
         "data": "synthetic (seeded, BASELINE.json config recipe; see workloads.py)",
-        "config": {"workload": cfg.name, "config_index": cfg.idx, "m": m_total, "n": n,
-                   "k": cfg.k, "ell": cfg.ell, "q": cfg.q, "sketch": cfg.sketch,
-                   "passes": passes, "a_bytes": a_bytes_total, "rows_per_rank": r1 - r0,
-                   "l2": "inputs larger than L2 (A shard >= 126 MB), no flush",
-                   "parallelism": f"row-sharded x{world} (NCCL all-reduce of Gram and "
-                                  "n x ell partials)"},
+        "config": config_dict(cfg, world),
+        "rows_per_rank": r1 - r0,
         "roofline": roof,
         "rsvd_plus_estimate_ms_rank0": round(est_s.elapsed_time(est_e), 4),
         "gpu_launches": int(launches),
@@ -605,14 +625,17 @@ def e2e_measure(args, cfg, A, lr):
             "d2h_bytes_per_step": int(d2h), "steps": steps}
 
 
-def reference_sample(cfg):
-    """(operator, A-bytes of one pass, sample description) for the reference
-    arm: the full matrix where one CPU rSVD takes seconds (configs 1, 2),
-    otherwise a bounded sample of the same recipe (rows / size reduced)."""
+def reference_sample(cfg, A_dev=None):
+    """(operator, A-bytes of one pass, sample description) for the CPU legs
+    (reference arm, cpu_baseline): the full matrix where one CPU rSVD takes
+    seconds (configs 1, 2), otherwise a bounded sample of the same recipe --
+    rows of the same matrix, so the A-GB/s rate is comparable."""
     from oracle import lowrank_oracle as O
     import torch
     if cfg.idx in (1, 2):
-        if torch.cuda.is_available():
+        if A_dev is not None:
+            A = A_dev.cpu().numpy()
+        elif torch.cuda.is_available():
             A = build_input(cfg).cpu().numpy()
             torch.cuda.empty_cache()
         else:
@@ -620,11 +643,15 @@ def reference_sample(cfg):
                                                 cfg.seed)
         return O.Dense(A), A.size * A.itemsize, f"full {cfg.name} matrix"
     if cfg.idx == 3:
-        A = workloads.build_cfg3()[:1024]
-        return O.Dense(A), A.size * A.itemsize, "config-3 recipe, first 1024 of 8192 rows"
+        A = A_dev[:1024].cpu().numpy() if A_dev is not None else workloads.build_cfg3()[:1024]
+        return O.Dense(A), A.size * A.itemsize, "config-3 matrix, first 1024 of 8192 rows"
     if cfg.idx == 4:
-        A, _ = workloads.build_cfg4_host(m=65536)
-        return O.Dense(A, promote=True), A.size * 4, "config-4 recipe at 65536 of 2^20 rows"
+        rows = 65536
+        A = (A_dev[:rows].cpu().numpy() if A_dev is not None
+             else workloads.cfg4_block_host(0))
+        return (O.Blockwise(A), A.size * 4,
+                f"config-4 matrix, first {rows} of 2^20 rows (recipe block 0), fp64 "
+                "row-block application (O.Blockwise)")
     S, L, R = workloads.build_cfg5(n=1 << 17)
     return (O.SparsePlusLowRank(S, L, R), S.nnz * 12 + (S.shape[0] + 1) * 8,
             "config-5 recipe at n = 2^17 (scipy CSR, single-threaded SpMM)")
@@ -657,8 +684,7 @@ def run_reference(args, cfg):
         "dtype": {"f64": "f64", "f32": "f64 (reference upcast)", "c64": "c128 (reference upcast)"
                   }.get(cfg.dtype, "f64"),
         "data": "synthetic (seeded, BASELINE.json config recipe; see workloads.py)",
-        "config": {"workload": cfg.name, "config_index": cfg.idx, "m": cfg.m, "n": cfg.n,
-                   "k": cfg.k, "ell": cfg.ell, "q": cfg.q, "passes": cfg.passes()},
+        "config": config_dict(cfg, world),
         "cpu_baseline": {"value": round(v, 4), "unit": "A-GB/s", "cores": os.cpu_count(),
                          "kind": "port",
                          "sample": f"{sample}: one rSVD (Stage A + direct SVD) per step by "
@@ -669,8 +695,26 @@ def run_reference(args, cfg):
     print(json.dumps(line), flush=True)
 
 
+def spawn_ranks(args):
+    """bench.py --gpus N run directly (not under torchrun): re-launch this
+    script as N ranks, one per GPU, with torch.distributed.run on 127.0.0.1
+    (NCCL_DEBUG=INFO so every rank's NCCL init is visible in the log)."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        sys.exit(spawn_ranks(args))
     cfg = workloads.CONFIGS[args.config]
     if args.impl == "reference":
         run_reference(args, cfg)

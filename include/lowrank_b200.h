@@ -67,6 +67,11 @@ int lr_set_stream(lr_handle_t h, void* stream);
 int lr_set_f32_mode(lr_handle_t h, int mode);
 /* Bytes currently reserved by the scratch pool. */
 int64_t lr_workspace_bytes(lr_handle_t h);
+/* Scratch-pool generation: incremented whenever pool chunks are freed
+ * (the pool merges its chunks after a call outgrew it).  Work captured in a
+ * CUDA graph holds raw pool addresses, so a graph recorded at generation g
+ * must not be replayed once the handle's generation differs. */
+uint64_t lr_pool_generation(lr_handle_t h);
 /* Pre-size the scratch pool (needed before CUDA-graph capture). */
 int lr_reserve(lr_handle_t h, int64_t bytes);
 
@@ -97,17 +102,22 @@ int lr_gemm_scaled(lr_handle_t h, int dtype, int op, int64_t m, int64_t n, int64
  * images the pass kernel streams (planes: 16 x MP x ldp bytes, MP = m and
  * ldp = n rounded up to multiples of 256, device memory owned by the
  * caller) and the
- * row exponents (row_exp: m int32).  lr_gemm_ozaki then computes
+ * row exponents (row_exp: m int32).  The digits are fixed-point relative to
+ * each row's maximum: |error_ij| <= 2^-50 max_k|A_ik| sum_k|X_kj| (fp64
+ * accuracy relative to the row scale).  wide_rows (device int32, nullable,
+ * accumulated with +=) counts rows whose nonzero entries span more than
+ * 2^32; for such a matrix the caller keeps the passes on lr_gemm (DMMA,
+ * error relative to |A||X| entrywise).  lr_gemm_ozaki then computes
  * Y = A X (op N: X n x ell, Y m x ell) or Y = A^T X (op T: X m x ell,
  * Y n x ell), ell <= 256, from the planes. */
 int lr_ozaki_prepare(lr_handle_t h, int64_t m, int64_t n, const double* A, int64_t lda,
-                     int8_t* planes, int64_t ldp, int32_t* row_exp);
+                     int8_t* planes, int64_t ldp, int32_t* row_exp, int32_t* wide_rows);
 /* lr_ozaki_prepare for rows [i0, i1) only (A still points at row 0; i0 a
  * multiple of 128, i1 a multiple of 128 or m): a row-chunked upload prepares
  * each chunk as it arrives; the chunk ending at m also zero-fills the padding. */
 int lr_ozaki_prepare_rows(lr_handle_t h, int64_t m, int64_t n, int64_t i0, int64_t i1,
                           const double* A, int64_t lda, int8_t* planes, int64_t ldp,
-                          int32_t* row_exp);
+                          int32_t* row_exp, int32_t* wide_rows);
 int lr_gemm_ozaki(lr_handle_t h, int op, int64_t m, int64_t n, int64_t ell,
                   const int8_t* planes, int64_t ldp, const int32_t* row_exp, const double* X,
                   int64_t ldx, double* Y, int64_t ldy);

@@ -51,8 +51,8 @@ _SIGS = {
     "lr_gemm_scaled": [_vp, _int, _int, _i64, _i64, _i64, _vp, _i64, C.c_double, _vp, _i64, _vp,
                        _i64],
     "lr_gram": [_vp, _int, _i64, _i64, _vp, _i64, _vp],
-    "lr_ozaki_prepare": [_vp, _i64, _i64, _vp, _i64, _vp, _i64, _vp],
-    "lr_ozaki_prepare_rows": [_vp, _i64, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp],
+    "lr_ozaki_prepare": [_vp, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp],
+    "lr_ozaki_prepare_rows": [_vp, _i64, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp],
     "lr_gemm_ozaki": [_vp, _int, _i64, _i64, _i64, _vp, _i64, _vp, _vp, _i64, _vp, _i64],
     "lr_chol_drop": [_vp, _int, _i64, _vp, C.c_double, C.c_double, C.c_double, _vp, _vp, _vp],
     "lr_chol_psd": [_vp, _int, _i64, _vp, C.c_double, _vp, _vp, _vp],
@@ -88,7 +88,8 @@ _lock = threading.Lock()
 
 
 def exported_symbols():
-    return sorted(_SIGS) + ["lr_last_error", "lr_workspace_bytes", "lr_launch_count"]
+    return sorted(_SIGS) + ["lr_last_error", "lr_workspace_bytes", "lr_launch_count",
+                            "lr_pool_generation"]
 
 
 # kernels launched through CUDA-graph replays (factor._replay): the C
@@ -124,6 +125,8 @@ def load():
         lib.lr_workspace_bytes.restype = _i64
         lib.lr_launch_count.argtypes = []
         lib.lr_launch_count.restype = C.c_uint64
+        lib.lr_pool_generation.argtypes = [_vp]
+        lib.lr_pool_generation.restype = C.c_uint64
         _lib = lib
     return _lib
 
@@ -186,6 +189,11 @@ def handle(device=None):
     else:
         check(lib.lr_set_stream(h, _vp(stream)))
     return h
+
+
+def pool_generation(h):
+    """Generation of handle h's scratch pool (lr_pool_generation)."""
+    return int(load().lr_pool_generation(h))
 
 
 def set_f32_mode(mode, device=None):

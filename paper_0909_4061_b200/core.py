@@ -281,7 +281,8 @@ class DenseOperator(MatVecOperator):
             ldp, mp = -(-n // 256) * 256, -(-m // 256) * 256
             try:
                 oz = (torch.empty(16 * mp * ldp, dtype=torch.int8, device=dev), ldp,
-                      torch.empty(m, dtype=torch.int32, device=dev))
+                      torch.empty(m, dtype=torch.int32, device=dev),
+                      torch.zeros(1, dtype=torch.int32, device=dev))
             except torch.cuda.OutOfMemoryError:
                 oz = None        # no room for the planes: DMMA passes
         for i, (r0, r1) in enumerate(bounds):
@@ -294,7 +295,7 @@ class DenseOperator(MatVecOperator):
                       _lib.ptr(bad[i:i + 1]), _lib.ptr(res[i]))
             if oz is not None:
                 _lib.call("lr_ozaki_prepare_rows", h, m, n, r0, r1, _lib.ptr(t), n,
-                          _lib.ptr(oz[0]), oz[1], _lib.ptr(oz[2]))
+                          _lib.ptr(oz[0]), oz[1], _lib.ptr(oz[2]), _lib.ptr(oz[3]))
             chunks.append((r0, r1, ev))
         t.record_stream(side)
         if oz is not None:
@@ -310,10 +311,16 @@ class DenseOperator(MatVecOperator):
         torch.cuda.current_stream(self._array.device).wait_event(chunks[-1][2])
         bad, res, _ = self._checks
         self._checks = None
-        nb, amax = to_hosts(bad, res[:, 0])
+        oz = getattr(self._array, "_lr_ozaki", None)
+        wide = oz[1][3] if oz is not None and oz[1] is not None else torch.zeros(
+            1, dtype=torch.int32, device=self._array.device)
+        nb, amax, nwide = to_hosts(bad, res[:, 0], wide)
         if int(nb.sum()):
             raise ValueError("matrix contains non-finite entries")
+        if oz is not None and int(nwide[0]):
+            self._array._lr_ozaki = (self._array._version, None)   # wide rows: DMMA
         self.amax = float(amax.max())
+        self._amax_version = self._array._version
 
     @property
     def array(self):
@@ -335,6 +342,15 @@ class DenseOperator(MatVecOperator):
         if nb:
             raise ValueError("matrix contains non-finite entries")
         self.amax = float(res[0].item())
+        self._amax_version = self._array._version
+
+    def _refresh(self):
+        """max|A| (the power-of-two scale of the fp32 / complex64 tensor-core
+        passes) follows in-place modifications of A: a changed version
+        counter re-runs the as_matrix check before the next pass."""
+        if (self._pending is None and self.amax is not None
+                and getattr(self, "_amax_version", self._array._version) != self._array._version):
+            self.validate()
 
     @property
     def dtype(self):
@@ -381,6 +397,7 @@ class DenseOperator(MatVecOperator):
         return Y
 
     def _apply(self, X):
+        self._refresh()
         t, host, vec = self._prep(X)
         if t.shape[0] != self.n:
             raise ValueError(f"dimension mismatch: A is {self.shape}, X has {t.shape[0]} rows")
@@ -389,6 +406,7 @@ class DenseOperator(MatVecOperator):
         return _out(Y, host)
 
     def _apply_adjoint(self, Y):
+        self._refresh()
         t, host, vec = self._prep(Y)
         if t.shape[0] != self.m:
             raise ValueError(f"dimension mismatch: A is {self.shape}, Y has {t.shape[0]} rows")
@@ -418,23 +436,25 @@ def _copy_stream(dev):
 
 def ozaki_prepare(A):
     """Digit planes of a float64 device matrix for the int8-tensor-core fp64
-    passes (lr_ozaki_prepare): (planes, ldp, row_exp); planes holds the two
-    shared-memory images of the 8 digit planes (A X and A^T Y tiles),
-    16 x MP x ldp bytes (m and n rounded up to 256)."""
+    passes (lr_ozaki_prepare): (planes, ldp, row_exp, wide_rows); planes holds
+    the two shared-memory images of the 8 digit planes (A X and A^T Y tiles),
+    16 x MP x ldp bytes (m and n rounded up to 256); wide_rows (device int32)
+    counts rows whose nonzero entries span more than 2^32."""
     torch = _torch()
     m, n = A.shape
     ldp = -(-n // 256) * 256          # tiles of 128, padded to pairs (2-SM kernel)
     mp = -(-m // 256) * 256
     planes = torch.empty(16 * mp * ldp, dtype=torch.int8, device=A.device)   # two images
     row_exp = torch.empty(m, dtype=torch.int32, device=A.device)
+    wide = torch.zeros(1, dtype=torch.int32, device=A.device)
     _lib.call("lr_ozaki_prepare", _lib.handle(A.device.index), m, n, _lib.ptr(A), _lib.ld(A),
-              _lib.ptr(planes), ldp, _lib.ptr(row_exp))
-    return planes, ldp, row_exp
+              _lib.ptr(planes), ldp, _lib.ptr(row_exp), _lib.ptr(wide))
+    return planes, ldp, row_exp, wide
 
 
 def ozaki_pass(oz, m, n, X, Y, adjoint):
     """Y = A X (or A^T X) from A's digit planes (lr_gemm_ozaki)."""
-    planes, ldp, row_exp = oz
+    planes, ldp, row_exp = oz[:3]
     _lib.call("lr_gemm_ozaki", _lib.handle(X.device.index), _lib.OP_T if adjoint else _lib.OP_N,
               m, n, X.shape[1], _lib.ptr(planes), ldp, _lib.ptr(row_exp), _lib.ptr(X), _lib.ld(X),
               _lib.ptr(Y), _lib.ld(Y))
@@ -484,6 +504,11 @@ def _ozaki_planes(A):
     try:
         oz = ozaki_prepare(A)
     except torch.cuda.OutOfMemoryError:
+        oz = None
+    if oz is not None and int(oz[3].item()):
+        # some row's nonzero entries span more than 2^32: the fixed-point
+        # digits (relative to the row maximum) would leave its small entries
+        # under fp32 precision -- this matrix stays on the DMMA passes
         oz = None
     A._lr_ozaki = (A._version, oz)
     return oz

@@ -486,7 +486,10 @@ const char* get_error() { return g_err.c_str(); }
 void pool_reset(Handle* h) {
   Pool& p = h->pool;
   if (p.chunks.size() > 1) {
-    LR_CUDA(cudaStreamSynchronize(h->stream));
+    // the chunks may still be in use by work on any stream (or referenced by
+    // a captured graph): drain the device, then invalidate via the generation
+    LR_CUDA(cudaDeviceSynchronize());
+    ++p.generation;
     for (auto& c : p.chunks) LR_CUDA(cudaFree(c.base));
     p.chunks.clear();
     const size_t sz = (p.peak + (size_t(1) << 20)) & ~((size_t(1) << 20) - 1);
@@ -580,6 +583,7 @@ int lr_create(int device, void* stream, lr_handle_t* out) {
 int lr_destroy(lr_handle_t hh) {
   API_BEGIN
   Handle* h = H(hh);
+  lr::DeviceGuard dg_(h->device);
   if (!h) return LR_OK;
   cudaStreamSynchronize(h->stream);
   for (auto& c : h->pool.chunks) cudaFree(c.base);
@@ -602,6 +606,8 @@ int lr_set_f32_mode(lr_handle_t h, int mode) {
   API_END
 }
 
+uint64_t lr_pool_generation(lr_handle_t h) { return h ? H(h)->pool.generation : 0; }
+
 int64_t lr_workspace_bytes(lr_handle_t h) {
   int64_t s = 0;
   for (auto& c : H(h)->pool.chunks) s += int64_t(c.size);
@@ -611,6 +617,7 @@ int64_t lr_workspace_bytes(lr_handle_t h) {
 int lr_reserve(lr_handle_t hh, int64_t bytes) {
   API_BEGIN
   Handle* h = H(hh);
+  lr::DeviceGuard dg_(h->device);
   lr::pool_reset(h);
   lr::pool_alloc(h, size_t(bytes));
   lr::pool_reset(h);
@@ -621,6 +628,7 @@ int lr_gemm(lr_handle_t hh, int dtype, int op, int64_t m, int64_t n, int64_t ell
             int64_t lda, const void* X, int64_t ldx, void* Y, int64_t ldy) {
   API_BEGIN
   Handle* h = H(hh);
+  lr::DeviceGuard dg_(h->device);
   check_dtype(dtype);
   LR_REQUIRE(m >= 0 && n >= 0 && ell >= 0, LR_EINVAL, "lr_gemm: negative dimension");
   LR_REQUIRE(op == LR_OP_N || op == LR_OP_T || op == LR_OP_C, LR_EINVAL, "lr_gemm: bad op");
@@ -637,23 +645,25 @@ int lr_gemm(lr_handle_t hh, int dtype, int op, int64_t m, int64_t n, int64_t ell
 }
 
 int lr_ozaki_prepare(lr_handle_t hh, int64_t m, int64_t n, const double* A, int64_t lda,
-                     int8_t* planes, int64_t ldp, int32_t* row_exp) {
+                     int8_t* planes, int64_t ldp, int32_t* row_exp, int32_t* wide_rows) {
   API_BEGIN
   Handle* h = H(hh);
+  lr::DeviceGuard dg_(h->device);
   LR_REQUIRE(m >= 1 && n >= 1 && lda >= n, LR_EINVAL, "lr_ozaki_prepare: bad dimensions");
   lr::pool_reset(h);
-  lr::ozaki_prepare(h, m, n, A, lda, planes, ldp, row_exp);
+  lr::ozaki_prepare(h, m, n, A, lda, planes, ldp, row_exp, wide_rows);
   API_END
 }
 
 int lr_ozaki_prepare_rows(lr_handle_t hh, int64_t m, int64_t n, int64_t i0, int64_t i1,
                           const double* A, int64_t lda, int8_t* planes, int64_t ldp,
-                          int32_t* row_exp) {
+                          int32_t* row_exp, int32_t* wide_rows) {
   API_BEGIN
   Handle* h = H(hh);
+  lr::DeviceGuard dg_(h->device);
   LR_REQUIRE(m >= 1 && n >= 1 && lda >= n, LR_EINVAL, "lr_ozaki_prepare_rows: bad dimensions");
   lr::pool_reset(h);
-  lr::ozaki_prepare_rows(h, m, n, i0, i1, A, lda, planes, ldp, row_exp);
+  lr::ozaki_prepare_rows(h, m, n, i0, i1, A, lda, planes, ldp, row_exp, wide_rows);
   API_END
 }
 
@@ -662,6 +672,7 @@ int lr_gemm_ozaki(lr_handle_t hh, int op, int64_t m, int64_t n, int64_t ell,
                   int64_t ldx, double* Y, int64_t ldy) {
   API_BEGIN
   Handle* h = H(hh);
+  lr::DeviceGuard dg_(h->device);
   LR_REQUIRE(m >= 0 && n >= 0 && ell >= 0 && ell <= 256, LR_EINVAL,
              "lr_gemm_ozaki: bad dimensions (ell <= 256)");
   LR_REQUIRE(op == LR_OP_N || op == LR_OP_T, LR_EINVAL, "lr_gemm_ozaki: op must be N or T");
@@ -676,6 +687,7 @@ int lr_gemm_scaled(lr_handle_t hh, int dtype, int op, int64_t m, int64_t n, int6
                    int64_t ldy) {
   API_BEGIN
   Handle* h = H(hh);
+  lr::DeviceGuard dg_(h->device);
   check_dtype(dtype);
   LR_REQUIRE(m >= 0 && n >= 0 && ell >= 0, LR_EINVAL, "lr_gemm_scaled: negative dimension");
   LR_REQUIRE(op == LR_OP_N || op == LR_OP_T || op == LR_OP_C, LR_EINVAL, "lr_gemm_scaled: bad op");
@@ -699,6 +711,7 @@ int lr_gram(lr_handle_t hh, int dtype, int64_t m, int64_t ell, const void* Y, in
             void* G) {
   API_BEGIN
   Handle* h = H(hh);
+  lr::DeviceGuard dg_(h->device);
   check_dtype(dtype);
   LR_REQUIRE(ldy >= ell, LR_EINVAL, "lr_gram: ldy < ell");
   lr::pool_reset(h);
@@ -710,6 +723,7 @@ int lr_chol_drop(lr_handle_t hh, int dtype, int64_t ell, const void* G, double d
                  double unres_rel, double shift_coef, void* P, void* R, int32_t* info) {
   API_BEGIN
   Handle* h = H(hh);
+  lr::DeviceGuard dg_(h->device);
   check_dtype(dtype);
   lr::pool_reset(h);
   lr::chol_any(h, dtype, ell, G, drop_tol, unres_rel, shift_coef, P, R, info);
@@ -720,6 +734,7 @@ int lr_chol_psd(lr_handle_t hh, int dtype, int64_t ell, const void* G, double ne
                 void* P, void* R, int32_t* info) {
   API_BEGIN
   Handle* h = H(hh);
+  lr::DeviceGuard dg_(h->device);
   check_dtype(dtype);
   LR_REQUIRE(dtype == LR_F64 || dtype == LR_C128, LR_EINVAL, "chol_psd: wide dtypes only");
   LR_REQUIRE(lr::chol_panel_supported(ell, dtype == LR_C128), LR_EUNSUPPORTED,
@@ -741,6 +756,7 @@ int lr_herm_prep(lr_handle_t hh, int dtype, int64_t n, const void* B, int64_t ld
                  double shift_mult, int power_iters, double* out2) {
   API_BEGIN
   Handle* h = H(hh);
+  lr::DeviceGuard dg_(h->device);
   check_dtype(dtype);
   LR_REQUIRE(dtype == LR_F64 || dtype == LR_C128, LR_EINVAL, "herm_prep: wide dtypes only");
   LR_REQUIRE(n >= 1 && n <= 4096, LR_EINVAL, "herm_prep: n out of range");
@@ -752,6 +768,7 @@ int lr_eig_finish(lr_handle_t hh, int dtype, int64_t n, const double* S, const d
                   const void* U, double* lam, void* V) {
   API_BEGIN
   Handle* h = H(hh);
+  lr::DeviceGuard dg_(h->device);
   check_dtype(dtype);
   LR_REQUIRE(dtype == LR_F64 || dtype == LR_C128, LR_EINVAL, "eig_finish: wide dtypes only");
   LR_REQUIRE(n >= 1 && n <= 4096, LR_EINVAL, "eig_finish: n out of range");
@@ -764,6 +781,7 @@ int lr_chol_drop_fast(lr_handle_t hh, int dtype, int64_t ell, const void* G, dou
                       int32_t* info, int32_t* status) {
   API_BEGIN
   Handle* h = H(hh);
+  lr::DeviceGuard dg_(h->device);
   check_dtype(dtype);
   lr::pool_reset(h);
   int32_t* saved = h->status;
@@ -786,6 +804,7 @@ int lr_orth(lr_handle_t hh, int dtype, int64_t m, int64_t ell, const void* Y, in
             void* Q, int64_t ldq, double tol, int64_t* rank_out) {
   API_BEGIN
   Handle* h = H(hh);
+  lr::DeviceGuard dg_(h->device);
   check_dtype(dtype);
   LR_REQUIRE(m >= 1 && ell >= 1 && ldy >= ell && ldq >= ell, LR_EINVAL, "lr_orth: bad shape");
   lr::pool_reset(h);
@@ -797,6 +816,7 @@ int lr_orth_fast(lr_handle_t hh, int dtype, int64_t m, int64_t ell, const void* 
                  void* Q, int64_t ldq, double tol, int32_t* status) {
   API_BEGIN
   Handle* h = H(hh);
+  lr::DeviceGuard dg_(h->device);
   check_dtype(dtype);
   LR_REQUIRE(m >= 1 && ell >= 1 && ldy >= ell && ldq >= ell && status, LR_EINVAL,
              "lr_orth_fast: bad arguments");
@@ -818,6 +838,7 @@ int lr_small_svd_fast(lr_handle_t hh, int dtype, int64_t ell, int64_t ncols, con
                       void* U, double* S, void* V, int32_t* status) {
   API_BEGIN
   Handle* h = H(hh);
+  lr::DeviceGuard dg_(h->device);
   check_dtype(dtype);
   LR_REQUIRE(ell >= 1 && ncols >= ell && status, LR_EINVAL, "lr_small_svd_fast: bad arguments");
   lr::pool_reset(h);
@@ -837,6 +858,7 @@ int lr_small_svd(lr_handle_t hh, int dtype, int64_t ell, int64_t ncols, void* Bh
                  double* S, void* V) {
   API_BEGIN
   Handle* h = H(hh);
+  lr::DeviceGuard dg_(h->device);
   check_dtype(dtype);
   LR_REQUIRE(ell >= 1 && ncols >= ell, LR_EINVAL, "lr_small_svd: need 1 <= ell <= ncols");
   lr::pool_reset(h);
@@ -848,6 +870,7 @@ int lr_jacobi_svd(lr_handle_t hh, int dtype, int64_t ell, const void* M, void* W
                   void* J, int32_t* info) {
   API_BEGIN
   Handle* h = H(hh);
+  lr::DeviceGuard dg_(h->device);
   LR_REQUIRE(dtype == LR_F64 || dtype == LR_C128, LR_EINVAL,
              "lr_jacobi_svd: fp64 / complex128 only");
   lr::pool_reset(h);
@@ -864,6 +887,7 @@ int lr_estimate_tail(lr_handle_t hh, int dtype, int64_t m, int64_t k, int64_t r,
                      int64_t ldq, void* Z, int64_t ldz, double alpha, double* est) {
   API_BEGIN
   Handle* h = H(hh);
+  lr::DeviceGuard dg_(h->device);
   check_dtype(dtype);
   lr::pool_reset(h);
   const size_t es = lr::elem_size(dtype);
@@ -885,6 +909,7 @@ int lr_srft_scaled(lr_handle_t hh, int dtype, int64_t m, int64_t n, int64_t ell,
                    void* Y, int64_t ldy) {
   API_BEGIN
   Handle* h = H(hh);
+  lr::DeviceGuard dg_(h->device);
   LR_REQUIRE(dtype == LR_C64 || dtype == LR_C128, LR_EINVAL, "lr_srft: complex dtypes only");
   LR_REQUIRE(n >= 1 && ell >= 1 && ell <= n, LR_EINVAL, "lr_srft: need 1 <= ell <= n");
   lr::pool_reset(h);
@@ -909,6 +934,7 @@ int lr_gsrft_matrix(lr_handle_t hh, int dtype, int64_t n, int64_t ell, const voi
                     const int32_t* picks, double scale, void* X) {
   API_BEGIN
   Handle* h = H(hh);
+  lr::DeviceGuard dg_(h->device);
   LR_REQUIRE(dtype == LR_C64 || dtype == LR_C128, LR_EINVAL, "lr_gsrft_matrix: complex only");
   LR_REQUIRE(n >= 1 && ell >= 1 && ell <= n, LR_EINVAL, "lr_gsrft_matrix: need 1 <= ell <= n");
   lr::pool_reset(h);
@@ -921,6 +947,7 @@ int lr_gsrft_matrix(lr_handle_t hh, int dtype, int64_t n, int64_t ell, const voi
 int lr_dft_rows(lr_handle_t hh, int dtype, int64_t rows, int64_t n, void* X, int64_t ldx) {
   API_BEGIN
   Handle* h = H(hh);
+  lr::DeviceGuard dg_(h->device);
   LR_REQUIRE(dtype == LR_C64 || dtype == LR_C128, LR_EINVAL, "lr_dft_rows: complex dtypes only");
   LR_REQUIRE(n >= 1, LR_EINVAL, "lr_dft_rows: n must be positive");
   lr::pool_reset(h);
@@ -933,6 +960,7 @@ int lr_csr_spmm(lr_handle_t hh, int dtype, int64_t m, int64_t n, int64_t ell,
                 int64_t ldx, void* Y, int64_t ldy, int accumulate) {
   API_BEGIN
   Handle* h = H(hh);
+  lr::DeviceGuard dg_(h->device);
   LR_REQUIRE(dtype == LR_F64, LR_EUNSUPPORTED, "lr_csr_spmm: fp64 only");
   (void)n;
   lr::pool_reset(h);
@@ -946,6 +974,7 @@ int lr_check_finite(lr_handle_t hh, int dtype, int64_t m, int64_t n, const void*
                     int64_t* nonfinite, double* amax) {
   API_BEGIN
   Handle* h = H(hh);
+  lr::DeviceGuard dg_(h->device);
   check_dtype(dtype);
   lr::pool_reset(h);
   lr::check_finite(h, dtype, m, n, A, lda, nonfinite, amax);
@@ -956,6 +985,7 @@ int lr_copy(lr_handle_t hh, int src_dtype, const void* src, int64_t lds, int dst
             void* dst, int64_t ldd, int64_t rows, int64_t cols, int conj_transpose) {
   API_BEGIN
   Handle* h = H(hh);
+  lr::DeviceGuard dg_(h->device);
   check_dtype(src_dtype);
   check_dtype(dst_dtype);
   lr::pool_reset(h);
@@ -967,6 +997,7 @@ int lr_sign_fix(lr_handle_t hh, int dtype, int64_t rows, int64_t vrows, int64_t 
                 int64_t ldu, void* V, int64_t ldv) {
   API_BEGIN
   Handle* h = H(hh);
+  lr::DeviceGuard dg_(h->device);
   check_dtype(dtype);
   lr::pool_reset(h);
   lr::sign_fix(h, dtype, rows, vrows, cols, U, ldu, V, ldv);
@@ -977,6 +1008,7 @@ int lr_max_abs_imag(lr_handle_t hh, int dtype, int64_t m, int64_t n, const void*
                     double* out) {
   API_BEGIN
   Handle* h = H(hh);
+  lr::DeviceGuard dg_(h->device);
   lr::pool_reset(h);
   lr::max_abs_imag(h, dtype, m, n, Y, ldy, out);
   API_END
@@ -986,6 +1018,7 @@ int lr_gaussian(lr_handle_t hh, uint64_t key_lo, uint64_t key_hi, int64_t count,
                 void* out, int32_t* status) {
   API_BEGIN
   Handle* h = H(hh);
+  lr::DeviceGuard dg_(h->device);
   LR_REQUIRE(dtype == LR_F32 || dtype == LR_F64, LR_EINVAL, "lr_gaussian: f32 or f64 output");
   LR_REQUIRE(count >= 0, LR_EINVAL, "lr_gaussian: negative count");
   lr::pool_reset(h);
@@ -1005,6 +1038,7 @@ int lr_axpy_sub(lr_handle_t hh, int dtype, int64_t rows, int64_t cols, const voi
                 int64_t ldt, void* Z, int64_t ldz) {
   API_BEGIN
   Handle* h = H(hh);
+  lr::DeviceGuard dg_(h->device);
   check_dtype(dtype);
   lr::pool_reset(h);
   lr::axpy_sub(h, dtype, rows, cols, T, ldt, Z, ldz);
@@ -1015,6 +1049,7 @@ int lr_col_sumsq(lr_handle_t hh, int dtype, int64_t m, int64_t r, const void* Z,
                  double* out) {
   API_BEGIN
   Handle* h = H(hh);
+  lr::DeviceGuard dg_(h->device);
   check_dtype(dtype);
   lr::pool_reset(h);
   lr::col_sumsq(h, dtype, m, r, Z, ldz, out);
@@ -1025,6 +1060,7 @@ int lr_scale_col(lr_handle_t hh, int dtype, int64_t rows, const void* src, int64
                  double inv, void* dst, int64_t ldd) {
   API_BEGIN
   Handle* h = H(hh);
+  lr::DeviceGuard dg_(h->device);
   check_dtype(dtype);
   lr::pool_reset(h);
   lr::scale_col(h, dtype, rows, src, lds, inv, dst, ldd);

@@ -273,10 +273,6 @@ void launch_chol(Handle* h, int64_t ell, const T* G, double drop_tol, double unr
 
 }  // namespace
 
-template <typename T>
-bool chol_blocked_launch(Handle* h, int64_t ell, const T* G, double drop_tol, double unres_rel,
-                         double shift_coef, T* P, T* R, int32_t* info);
-
 void chol_drop_f64(Handle* h, int64_t ell, const double* G, double drop_tol, double unres_rel,
                    double shift_coef, double* P, double* R, int32_t* info) {
   LR_REQUIRE(ell >= 1 && ell <= 4096, LR_EINVAL, "chol_drop: ell out of range [1, 4096]");

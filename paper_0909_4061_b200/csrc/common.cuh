@@ -61,6 +61,9 @@ struct Pool {
   size_t off = 0;     // bump offset within chunk
   size_t peak = 0;    // bytes needed by the largest call so far
   size_t used = 0;    // bytes handed out in this call
+  // bumped whenever chunks are freed (merge at reset): a CUDA graph captured
+  // over this pool's addresses is stale once the generation moves
+  uint64_t generation = 0;
 };
 
 struct Handle {
@@ -80,6 +83,41 @@ struct Handle {
 };
 
 void pool_reset(Handle* h);
+
+// Every API entry runs on the handle's device (restoring the caller's):
+// kernel attributes and the pool belong to that device.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) == cudaSuccess && prev != dev) {
+      cudaSetDevice(dev);
+    } else {
+      prev = -1;
+    }
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+// per-device "attribute already set" flags for kernels that raise their
+// dynamic shared-memory limit once (cudaFuncSetAttribute is per device)
+struct AttrOnce {
+  bool done[16] = {};
+  template <typename F>
+  void operator()(F&& set) {
+    int d = 0;
+    cudaGetDevice(&d);
+    if (d < 0 || d >= 16) {
+      set();
+      return;
+    }
+    if (!done[d]) {
+      set();
+      done[d] = true;
+    }
+  }
+};
 void* pool_alloc(Handle* h, size_t bytes);
 template <typename T>
 T* pool_alloc_t(Handle* h, size_t count) {
@@ -105,10 +143,13 @@ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 // gemm_f64.cu ---------------------------------------------------------------
 int64_t choose_splits(int sm_count, int64_t tiles, int64_t K);
 // gemm_f64_ozaki.cu: fp64 passes on the int8 tensor cores (digit planes of A)
+// wide_rows (nullable): += number of rows whose nonzero entries span more
+// than 2^32 (the caller keeps such a matrix on the DMMA passes)
 void ozaki_prepare(Handle* h, int64_t m, int64_t n, const double* A, int64_t lda, int8_t* planes,
-                   int64_t ldp, int32_t* row_exp);
+                   int64_t ldp, int32_t* row_exp, int32_t* wide_rows);
 void ozaki_prepare_rows(Handle* h, int64_t m, int64_t n, int64_t i0, int64_t i1, const double* A,
-                        int64_t lda, int8_t* planes, int64_t ldp, int32_t* row_exp);
+                        int64_t lda, int8_t* planes, int64_t ldp, int32_t* row_exp,
+                        int32_t* wide_rows);
 void ozaki_gemm(Handle* h, bool trans, int64_t m, int64_t n, int64_t N, const int8_t* planes,
                 int64_t ldp, const int32_t* row_exp, const double* X, int64_t ldx, double* C,
                 int64_t ldc);

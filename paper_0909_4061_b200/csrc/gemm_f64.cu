@@ -260,12 +260,11 @@ void launch_nf(Handle* h, int64_t M, int64_t N, int64_t K, const TIN* A, int64_t
                const TIN* B, int64_t ldb, double* C, int64_t ldc) {
   using S = Smem<NF, TIN>;
   auto kern = gemm_f64_kernel<TRANS, NF, TIN>;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static AttrOnce attr_once;
+  attr_once([&] {
     LR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(S::bytes)));
-    attr_set = true;
-  }
+  });
   const int64_t mt = ceil_div(M, BM), nt = ceil_div(N, S::BN);
   const int64_t splits_wanted = choose_splits(h->sm_count, mt * nt, K);
   const int64_t kchunk = ceil_div(ceil_div(K, splits_wanted), BK) * BK;

@@ -54,7 +54,9 @@ constexpr int OST = LR_OZ_ST;       // ring depth
 constexpr int OTHREADS = 256;
 constexpr int A_PLANE = OBM * OBK;  // 4 KB
 constexpr int A_STAGE = OZ_S * A_PLANE;
-constexpr int64_t OZ_KMAX = 65536;  // int32 headroom: 8 pairs x 64^2 x K < 2^31
+// int32 headroom: at most 8 digit pairs per diagonal, |digit| <= 64, so one
+// accumulator grows by <= 8 x 64^2 = 2^15 per k: K <= 2^15 keeps it < 2^30
+constexpr int64_t OZ_KMAX = 32768;
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -139,18 +141,36 @@ __device__ __forceinline__ int exp_of(double amax) {
 // ---------------------------------------------------------------------------
 // A planes (once per operator): row exponents, then digits
 
+// Digits are fixed-point relative to each row's maximum, so an entry 2^-e
+// below its row maximum keeps 55 - e bits.  Rows whose nonzero entries span
+// more than 2^OZ_RANGE (entries keeping < 23 bits, fp32 precision) are
+// counted in *wide_rows: the caller then keeps that matrix on the DMMA passes,
+// whose error is relative to each entry (|A||X|) rather than to the row scale.
+constexpr int OZ_RANGE = 32;
+
 __global__ void oz_row_exp_kernel(int64_t m, int64_t n, const double* __restrict__ A, int64_t lda,
-                                  int32_t* __restrict__ row_exp, int64_t i0) {
+                                  int32_t* __restrict__ row_exp, int64_t i0,
+                                  int32_t* __restrict__ wide_rows) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
   for (int64_t i = i0 + blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5); i < m;
        i += warps) {
-    double mx = 0.0;
+    double mx = 0.0, mn = INFINITY;
     const double* row = A + i * lda;
-    for (int64_t k = lane; k < n; k += 32) mx = fmax(mx, fabs(row[k]));
+    for (int64_t k = lane; k < n; k += 32) {
+      const double v = fabs(row[k]);
+      mx = fmax(mx, v);
+      if (v > 0.0) mn = fmin(mn, v);
+    }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if (lane == 0) row_exp[i] = exp_of(mx);
+    for (int o = 16; o > 0; o >>= 1) {
+      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    }
+    if (lane == 0) {
+      row_exp[i] = exp_of(mx);
+      if (wide_rows && mx > 0.0 && exp_of(mx) - exp_of(mn) > OZ_RANGE) atomicAdd(wide_rows, 1);
+    }
   }
 }
 
@@ -736,7 +756,8 @@ int oz_dbg() {
 // Rows [i0, i1) only (i0 a multiple of 128, i1 = m finishes the padding):
 // the streamed upload prepares each chunk as it lands.
 void ozaki_prepare_rows(Handle* h, int64_t m, int64_t n, int64_t i0, int64_t i1, const double* A,
-                        int64_t lda, int8_t* planes, int64_t ldp, int32_t* row_exp) {
+                        int64_t lda, int8_t* planes, int64_t ldp, int32_t* row_exp,
+                        int32_t* wide_rows) {
   LR_REQUIRE(ldp >= n && ldp % OZP == 0, LR_EINVAL,
              "ozaki_prepare: ldp must be n rounded up to a multiple of 256");
   LR_REQUIRE(i0 >= 0 && i0 % OZB == 0 && i1 > i0 && i1 <= m, LR_EINVAL,
@@ -745,7 +766,7 @@ void ozaki_prepare_rows(Handle* h, int64_t m, int64_t n, int64_t i0, int64_t i1,
   const int64_t iend = (i1 == m) ? MP : i1;
   LR_REQUIRE(iend % 32 == 0, LR_EINVAL, "ozaki_prepare: row range end must be a multiple of 32");
   const int blocks = h->sm_count * 8;
-  oz_row_exp_kernel<<<blocks, 256, 0, h->stream>>>(i1, n, A, lda, row_exp, i0);
+  oz_row_exp_kernel<<<blocks, 256, 0, h->stream>>>(i1, n, A, lda, row_exp, i0, wide_rows);
   LR_CHECK_LAUNCH();
   oz_slice_a_kernel<<<blocks, 256, 0, h->stream>>>(m, n, A, lda, row_exp, planes,
                                                    planes + OZ_S * MP * ldp, MP, ldp, i0, iend);
@@ -753,8 +774,8 @@ void ozaki_prepare_rows(Handle* h, int64_t m, int64_t n, int64_t i0, int64_t i1,
 }
 
 void ozaki_prepare(Handle* h, int64_t m, int64_t n, const double* A, int64_t lda, int8_t* planes,
-                   int64_t ldp, int32_t* row_exp) {
-  ozaki_prepare_rows(h, m, n, 0, m, A, lda, planes, ldp, row_exp);
+                   int64_t ldp, int32_t* row_exp, int32_t* wide_rows) {
+  ozaki_prepare_rows(h, m, n, 0, m, A, lda, planes, ldp, row_exp, wide_rows);
 }
 
 namespace {
@@ -787,11 +808,10 @@ void ozaki_gemm_2sm(Handle* h, bool trans, int64_t M, int64_t N, int64_t K, cons
   }
   const size_t smem = size_t(ST2) * (A_STAGE + B2_STAGE) + 1024 + 256;
   auto kern = trans ? ozaki_gemm2_kernel<true> : ozaki_gemm2_kernel<false>;
-  static bool attr[2] = {false, false};
-  if (!attr[trans]) {
+  static AttrOnce attr_once[2];
+  attr_once[trans]([&] {
     LR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    attr[trans] = true;
-  }
+  });
   const int64_t pairs = ceil_div(ceil_div(M, OBM), 2);
   int64_t want = choose_splits(h->sm_count, 2 * pairs * nt, K);
   want = std::max<int64_t>(want, ceil_div(K, OZ_KMAX));
@@ -864,11 +884,7 @@ void ozaki_gemm(Handle* h, bool trans, int64_t m, int64_t n, int64_t N, const in
   const int stage_bytes = A_STAGE + OZ_S * BN * OBK;
   const size_t smem = size_t(OST) * stage_bytes + 1024 + 256;
   auto kern = trans ? ozaki_gemm_kernel<true> : ozaki_gemm_kernel<false>;
-  static size_t attr[2] = {0, 0};
-  if (attr[trans] < smem) {
-    LR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    attr[trans] = smem;
-  }
+  LR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   const int64_t mt = ceil_div(M, OBM);
   int64_t want = choose_splits(h->sm_count, mt * nt, K);
   want = std::max<int64_t>(want, ceil_div(K, OZ_KMAX));

@@ -213,12 +213,11 @@ void launch(Handle* h, int64_t M, int64_t N, int64_t K, const TIN* A, int64_t ld
   auto kern = gemm_f64_tma_kernel<TRANS, NF, TIN>;
   constexpr CUtensorMapDataType DT =
       sizeof(TIN) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
-  static bool attr = false;
-  if (!attr) {
+  static AttrOnce attr_once;
+  attr_once([&] {
     LR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  int(G::SMEM)));
-    attr = true;
-  }
+  });
   constexpr uint64_t ES = sizeof(TIN);
   const CUtensorMap mapA =
       !TRANS ? make_map_2d(DT, A, uint64_t(K), uint64_t(M), uint64_t(lda) * ES, BK, BM,

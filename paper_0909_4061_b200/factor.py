@@ -334,7 +334,9 @@ def _graph_key(op):
         return tuple(op.graph_key())
     if hasattr(op, "array"):
         a = op.array
-        return (a.data_ptr(), tuple(a.shape), a.dtype, getattr(op, "amax", None))
+        # _version: an in-place change of A (new digit planes / max|A|) must
+        # not replay work captured against the old ones
+        return (a.data_ptr(), tuple(a.shape), a.dtype, a._version, getattr(op, "amax", None))
     return None
 
 
@@ -408,11 +410,21 @@ def _capture(op, body, entry, dev):
     after = _snapshot(op)
     entry["delta"] = tuple(a - b for a, b in zip(after, snap))
     _restore(op, snap)
-    entry.update(graph=g, status=status, out=out)
+    # the captured kernels hold raw addresses in this handle's scratch pool:
+    # remember its generation (a later pool merge frees those chunks)
+    h = _lib.handle(dev.index)
+    entry.update(graph=g, status=status, out=out, pool=(h, _lib.pool_generation(h)))
 
 
 def _replay(op, entry, counters):
     from . import core
+    from . import _lib
+    h, gen = entry["pool"]
+    if _lib.pool_generation(h) != gen:
+        # the scratch chunks this graph addresses were freed: drop it (it is
+        # re-captured after the next eager runs) and run eagerly
+        entry.update(graph=None, runs=0, out=None)
+        return None
     entry["graph"].replay()
     if core.PASS_EVENTS is not None:     # bench.py: the replay's pass timings
         core.PASS_EVENTS.extend(entry.get("pass_events", []))

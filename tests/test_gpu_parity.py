@@ -199,7 +199,66 @@ def test_cfg4_reduced_rows(golden):
     c = workloads.CONFIGS[4]
     A, _ = workloads.build_cfg4_host(m=65536)
     basis, f, est = lr().randomized_svd(A, c.k, c.p, c.q, c.seed)
-    check_against_golden(g, f, basis, est, 1e-4, floor=2e-5)
+    check_against_golden(g, f, basis, est, 1e-4, floor=2.2e-6)
+
+
+@pytest.mark.slow
+def test_cfg4_full_size():
+    """Config 4 at its full size (2^20 x 4096 fp32, 16 GiB) with the exact
+    BASELINE recipe (device-drawn reference Philox streams, fp64 QR), against
+    the CPU oracle -- the reference algorithm in fp64, applied by row blocks
+    (O.Blockwise, arithmetic-identical to the reference's upcast
+    DenseOperator) -- on the same A and the same Omega / probes.
+    Tolerances (north_star): sigma_j within 1e-4 relative
+    where sigma_j >= 2.2e-6 sigma_1 (the fp32 noise floor: j <= 124), the
+    normwise max |dsigma| / sigma_1 <= 1e-6 over all ell, the posterior
+    estimate within 1 %.  Block 3 of the device build is checked against the
+    host recipe (numpy QR) to one fp32 ulp."""
+    from oracle import lowrank_oracle as O
+    c = workloads.CONFIGS[4]
+    A, _ = workloads.build_cfg4_device()
+    blk = workloads.cfg4_block_host(3)
+    dev_blk = A[3 * 65536:4 * 65536].cpu().numpy()
+    ulp = np.spacing(np.abs(blk).astype(np.float32))
+    assert np.all(np.abs(dev_blk - blk) <= ulp)
+    assert np.mean(dev_blk != blk) <= 1e-3
+    del blk, dev_blk
+    basis, f, est = lr().randomized_svd(A, c.k, c.p, c.q, c.seed)
+    s = f.sigma.cpu().numpy()
+    assert basis.passes == 4 and basis.Q.shape == (c.m, c.ell)
+    A_h = A.cpu().numpy()
+    del A, basis, f
+    torch.cuda.empty_cache()
+    ob, of, oest = O.rsvd(O.Blockwise(A_h), c.k, c.p, c.q, c.seed)
+    assert ob.Q.shape[1] == c.ell
+    rel = np.abs(s - of.sigma) / of.sigma
+    mask = of.sigma >= 2.2e-6 * of.sigma[0]
+    assert mask.sum() >= 124
+    assert rel[mask].max() <= 1e-4, (rel[mask].max(), int(np.argmax(rel * mask)))
+    assert np.abs(s - of.sigma).max() / of.sigma[0] <= 1e-6
+    assert est == pytest.approx(oest, rel=1e-2)
+
+
+@pytest.mark.slow
+def test_cfg5_full_size():
+    """Config 5 at its full size (CSR 2^21 x 2^21, ~16 nnz/row, plus the
+    implicit rank-32 L R^T) against the CPU oracle (the reference's
+    subspace_iteration_range + direct_svd driven through a scipy-CSR operator,
+    SURVEY.md §8c): sigma_j within 1e-10 relative for sigma_j >= 1e-6 sigma_1,
+    the estimate within 1 %."""
+    from oracle import lowrank_oracle as O
+    c = workloads.CONFIGS[5]
+    S, L, R = workloads.build_cfg5()
+    op = lr().CudaCsrOperator(S, L, R, host_io=True)
+    basis, f, est = lr().randomized_svd(op, c.k, c.p, c.q, c.seed)
+    assert basis.passes == 8
+    ob, of, oest = O.rsvd(O.SparsePlusLowRank(S, L, R), c.k, c.p, c.q, c.seed)
+    s = np.asarray(f.sigma)
+    mask = of.sigma >= 1e-6 * of.sigma[0]
+    assert mask.sum() >= c.k
+    rel = np.abs(s - of.sigma) / of.sigma
+    assert rel[mask].max() <= 1e-10, rel[mask].max()
+    assert est == pytest.approx(oest, rel=1e-2)
 
 
 def test_cfg5_reduced(golden):

@@ -18,9 +18,8 @@ sketch.py:32-42, unless a builder says otherwise):
   cfg4  fp32 2^20 x 4096, A = U diag(s) V^T built in fp64, stored fp32:
         U = vstack_b haar(65536, 4096, rng(s, "Ublk", b)) / sqrt(#blocks),
         V = haar(4096, 4096, rng(s, "Vhar")), s_j = 0.9^(j-1) (j <= 200)
-        else 1e-6.  (The full-size device build draws its Gaussians from a
-        seeded torch generator instead -- host Philox for 4.3e9 draws takes
-        minutes -- and is used only for timing and size-independent checks.)
+        else 1e-6.  The full-size device build draws the same Philox streams
+        on the GPU (numpy-matching generator) and QR-factors them there.
   cfg5  fp64 CSR 2^21 x 2^21 with 16 uniform random columns per row
         (duplicates summed), values N(0,1) (stream "sprs"); plus implicit
         L R^T with L, R = 10 * Gaussian n x 32 (stream "lowr").
@@ -39,6 +38,9 @@ STREAM_UBLK = 0x55626C6B    # "Ublk"
 STREAM_VHAR = 0x56686172    # "Vhar"
 STREAM_SPRS = 0x73707273    # "sprs"
 STREAM_LOWR = 0x6C6F7772    # "lowr"
+
+# nonzeros of the cfg5 recipe at seed 5 (duplicates summed), SURVEY.md §8d
+CFG5_NNZ = 33554314
 
 
 def rng_for(seed, stream=0, index=0):
@@ -75,7 +77,9 @@ class Config:
 
     def a_bytes(self, nnz=None):
         if self.idx == 5:
-            return None
+            # CSR bytes model: f64 values + int32 columns + int64 row pointers
+            nnz = CFG5_NNZ if nnz is None else nnz
+            return nnz * 12 + (self.m + 1) * 8
         elem = {"f64": 8, "f32": 4, "c64": 8, "c128": 16}[self.dtype]
         return self.m * self.n * elem
 
@@ -212,18 +216,42 @@ def build_synthetic_device(m, n, s, seed, device="cuda", host_rng=True):
 
 
 def build_cfg4_device(seed=4, m=1 << 20, n=4096, block=65536, device="cuda"):
-    """Full-size cfg4 on the GPU (torch-generator Gaussians; see module doc)."""
+    """Full-size cfg4 on the GPU with the exact recipe of build_cfg4_host:
+    the Gaussian blocks are the reference's Philox streams rng_for(seed,
+    "Ublk", b) / rng_for(seed, "Vhar") drawn on the device by the library's
+    numpy-matching generator (lr_gaussian, checked against numpy in
+    tests/test_gpu_kernels.py), QR-factored in fp64 on the device (cuSOLVER
+    Householder, like numpy's LAPACK QR up to roundoff) and signed by diag R;
+    A = U diag(s) V^T in fp64, stored fp32.  Differs from the host build only
+    by fp64 QR rounding (~1e-15 relative), i.e. at most one fp32 ulp on rare
+    entries (tests/test_gpu_parity.py checks a block against the host)."""
     import torch
+    from paper_0909_4061_b200.sketch import gaussian_dev
     nb = m // block
-    s = torch.as_tensor(spectrum(4, n), dtype=torch.float64, device=device)
-    gen = torch.Generator(device=device).manual_seed(0x4C52 + seed)
-    V = _haar_torch(torch.randn((n, n), dtype=torch.float64, device=device, generator=gen), device)
+    dev = torch.device(device)
+    s = torch.as_tensor(spectrum(4, n), dtype=torch.float64, device=dev)
+    V = _haar_torch(gaussian_dev(n, n, seed, stream=STREAM_VHAR, dtype=torch.float64,
+                                 device=dev.index), device)
     W = (V * s).T.contiguous()
-    A = torch.empty((m, n), dtype=torch.float32, device=device)
+    del V
+    A = torch.empty((m, n), dtype=torch.float32, device=dev)
     for b in range(nb):
-        g = torch.randn((block, n), dtype=torch.float64, device=device, generator=gen)
+        g = gaussian_dev(block, n, seed, stream=STREAM_UBLK, index=b, dtype=torch.float64,
+                         device=dev.index)
         Ub = _haar_torch(g, device) / np.sqrt(nb)
         del g
         A[b * block:(b + 1) * block] = (Ub @ W).to(torch.float32)
         del Ub
+    torch.cuda.synchronize(dev)
     return A, s.cpu().numpy()
+
+
+def cfg4_block_host(b, seed=4, m=1 << 20, n=4096, block=65536):
+    """Block b (rows [b*block, (b+1)*block)) of the full-size cfg4 recipe on
+    the host (reference haar_basis via numpy QR) -- the recipe check for
+    build_cfg4_device."""
+    nb = m // block
+    s = spectrum(4, n)
+    V = haar_basis(n, n, rng_for(seed, STREAM_VHAR))
+    Ub = haar_basis(block, n, rng_for(seed, STREAM_UBLK, b)) / np.sqrt(nb)
+    return (Ub @ (V * s).T).astype(np.float32)
