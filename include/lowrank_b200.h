@@ -105,9 +105,9 @@ int lr_gemm_scaled(lr_handle_t h, int dtype, int op, int64_t m, int64_t n, int64
  * row exponents (row_exp: m int32).  The digits are fixed-point relative to
  * each row's maximum: |error_ij| <= 2^-50 max_k|A_ik| sum_k|X_kj| (fp64
  * accuracy relative to the row scale).  wide_rows (device int32, nullable,
- * accumulated with +=) counts rows whose nonzero entries span more than
- * 2^32; for such a matrix the caller keeps the passes on lr_gemm (DMMA,
- * error relative to |A||X| entrywise).  lr_gemm_ozaki then computes
+ * accumulated with +=) counts graded rows -- more than 1/8 of the nonzeros
+ * below 2^-32 of the row maximum; for such a matrix the caller keeps the
+ * passes on lr_gemm (DMMA, error relative to |A||X| entrywise).  lr_gemm_ozaki then computes
  * Y = A X (op N: X n x ell, Y m x ell) or Y = A^T X (op T: X m x ell,
  * Y n x ell), ell <= 256, from the planes. */
 int lr_ozaki_prepare(lr_handle_t h, int64_t m, int64_t n, const double* A, int64_t lda,
@@ -128,6 +128,16 @@ int lr_gemm_ozaki(lr_handle_t h, int op, int64_t m, int64_t n, int64_t ell,
  * by lr_orth and, between ranks, by the row-sharded path (all-reduce of G). */
 int lr_gram(lr_handle_t h, int dtype, int64_t m, int64_t ell,
             const void* Y, int64_t ldy, void* G);
+
+/* Gram of an fp32 panel on the tcgen05 tensor cores, G (ell x ell fp64,
+ * row-major) = Y^T Y, at fp32-level accuracy: Y scaled by 2^log2_scale and
+ * split into fp16 hi + lo, fp32 accumulation in TMEM per row block, the
+ * blocks summed in fp64.  Used for the second CholeskyQR pass of an fp32
+ * panel (reference orthonormalize_double_gs, core.py:84-115, whose second
+ * projection it replaces); an entry with |y| 2^log2_scale >= 2^15 sets bit 1
+ * of *status (device int32, nullable).  ell <= 256, m >= 4096. */
+int lr_gram_tc(lr_handle_t h, int64_t m, int64_t ell, const float* Y, int64_t ldy, double* G,
+               int log2_scale, int32_t* status);
 
 /* Cholesky with column deletion on a Gram matrix G = Y^H Y (fp64 / c128,
  * row-major) -- the rank decision of orthonormalize_double_gs (reference
@@ -303,6 +313,19 @@ int lr_max_abs_imag(lr_handle_t h, int dtype, int64_t m, int64_t n, const void* 
  * exceeded 63 draws, 32 = internal stream margin too short.  Async. */
 int lr_gaussian(lr_handle_t h, uint64_t key_lo, uint64_t key_hi, int64_t count, int dtype,
                 void* out, int32_t* status);
+
+/* One-pass sketches (reference io.py:364-388 accumulate_two_sided_samples,
+ * factor.py:364-401 svd_one_pass_general):
+ *   lr_axpy_add:      Z (rows x cols) += T    (fp64 / complex128) -- the
+ *                     row-block accumulation Y~ += block^H Omega~[rows];
+ *   lr_sylvester_div: C_ij /= (d2_i + d1_j), 0 where the sum <= floor -- the
+ *                     diagonalized normal equations B (P P^H) + (S S^H) B = C
+ *                     of the one-pass least-squares problem.
+ * d1, d2: device float64; C row-major k x kt (ldc). */
+int lr_axpy_add(lr_handle_t h, int dtype, int64_t rows, int64_t cols, const void* T,
+                int64_t ldt, void* Z, int64_t ldz);
+int lr_sylvester_div(lr_handle_t h, int dtype, int64_t k, int64_t kt, void* C, int64_t ldc,
+                     const double* d2, const double* d1, double floor);
 
 /* BLAS-1 helpers for the column-wise paths (device CGS2 / the unsafeguarded
  * Gram-Schmidt of power_iteration_range(safeguarded=False), reference

@@ -777,3 +777,184 @@ def rsvd(A, k, p, q, seed, sketch="gauss", probes=DEFAULT_PROBES, alpha=DEFAULT_
     if est is None and estimate:
         est = posterior_error_estimate(op, basis.Q, r=probes, alpha=alpha, seed=seed + 13)
     return basis, f, est
+
+
+# ---------------------------------------------------------------------------
+# One-pass sketches and row-block streaming (reference factor.py:95-147,
+# 338-401; io.py:35,178-204,319-430; core.py:133-186,297-325)
+
+ONE_PASS_DIM_CAP = 250_000       # reference config.py:31
+ONE_PASS_COND_WARN = 1e12        # reference config.py:34
+LRK_MAGIC = b"LRKMAT00"          # reference io.py:35
+
+
+def write_matrix_binary(A, path):
+    """io.py:178-188."""
+    A = as_matrix(A)
+    with open(path, "wb") as fh:
+        fh.write(LRK_MAGIC)
+        np.asarray([1 if np.iscomplexobj(A) else 0, A.shape[0], A.shape[1]],
+                   dtype="<i8").tofile(fh)
+        np.ascontiguousarray(A).astype("<c16" if np.iscomplexobj(A) else "<f8").tofile(fh)
+
+
+def stream_row_blocks(path, block_rows):
+    """io.py:319-356: (row, block) pairs of a LRKMAT00 file."""
+    with open(path, "rb") as fh:
+        if fh.read(8) != LRK_MAGIC:
+            raise ValueError(f"{path}: bad magic")
+        code, m, n = (int(x) for x in np.fromfile(fh, dtype="<i8", count=3))
+        dtype = "<c16" if code == 1 else "<f8"
+        row = 0
+        while row < m:
+            rows = min(block_rows, m - row)
+            data = np.fromfile(fh, dtype=dtype, count=rows * n)
+            if data.size != rows * n:
+                raise IOError(f"{path}: stream truncated at row block starting {row}")
+            yield row, data.reshape(rows, n)
+            row += rows
+
+
+def accumulate_two_sided_samples(blocks, m, n, ell, ell_tilde, seed):
+    """io.py:364-388."""
+    Omega = gaussian_matrix(n, ell, seed)
+    Omega_t = gaussian_matrix(m, ell_tilde, seed + 1)
+    Y = Yt = None
+    total = 0
+    for row, block in blocks:
+        if Y is None:
+            dt = np.promote_types(block.dtype, Omega.dtype)
+            Y = np.zeros((m, ell), dtype=dt)
+            Yt = np.zeros((n, ell_tilde), dtype=dt)
+        rows = block.shape[0]
+        Y[row:row + rows, :] = block @ Omega
+        Yt += block.conj().T @ Omega_t[row:row + rows, :]
+        total += rows
+    if total != m:
+        raise IOError(f"stream delivered {total} rows, expected {m}")
+    return Omega, Omega_t, Y, Yt
+
+
+@dataclass
+class SampleBundle:
+    """factor.py:95-113."""
+    Omega: np.ndarray
+    Y: np.ndarray
+    Q: np.ndarray
+    Omega_tilde: np.ndarray = None
+    Y_tilde: np.ndarray = None
+    Q_tilde: np.ndarray = None
+    q_choice: str = "gs"
+    seed: int = None
+
+
+def _basis_from_samples(Y, rank=None, ortho_tol=GS_DROP_TOL):
+    """factor.py:116-120."""
+    if rank is None:
+        return orthonormalize_double_gs(Y, tol=ortho_tol), "gs"
+    return small_svd(Y).U[:, :rank], "svd"
+
+
+def sample_bundle(A, ell, seed, rank=None):
+    """factor.py:123-133."""
+    op = as_operator(A)
+    Omega = gaussian_matrix(op.n, ell, seed)
+    Y = op.apply(Omega)
+    Q, choice = _basis_from_samples(Y, rank)
+    return SampleBundle(Omega=Omega, Y=Y, Q=Q, q_choice=choice, seed=seed)
+
+
+def sample_bundle_two_sided(A, ell, ell_tilde=None, seed=0, rank=None):
+    """factor.py:136-147."""
+    op = as_operator(A)
+    ell_tilde = ell if ell_tilde is None else ell_tilde
+    Omega = gaussian_matrix(op.n, ell, seed)
+    Omega_t = gaussian_matrix(op.m, ell_tilde, seed + 1)
+    Y = op.apply(Omega)
+    Yt = op.apply_adjoint(Omega_t)
+    Q, choice = _basis_from_samples(Y, rank)
+    Qt, _ = _basis_from_samples(Yt, rank)
+    return SampleBundle(Omega=Omega, Y=Y, Q=Q, Omega_tilde=Omega_t, Y_tilde=Yt, Q_tilde=Qt,
+                        q_choice=choice, seed=seed)
+
+
+def streamed_sample_bundle(path, block_rows, ell, ell_tilde=None, seed=0, rank=None):
+    """io.py:391-404 over a file."""
+    with open(path, "rb") as fh:
+        fh.read(8)
+        _, m, n = (int(x) for x in np.fromfile(fh, dtype="<i8", count=3))
+    ell_tilde = ell if ell_tilde is None else ell_tilde
+    Omega, Omega_t, Y, Yt = accumulate_two_sided_samples(stream_row_blocks(path, block_rows), m, n,
+                                                         ell, ell_tilde, seed)
+    Q, choice = _basis_from_samples(Y, rank)
+    Qt, _ = _basis_from_samples(Yt, rank)
+    return SampleBundle(Omega=Omega, Y=Y, Q=Q, Omega_tilde=Omega_t, Y_tilde=Yt, Q_tilde=Qt,
+                        q_choice=choice, seed=seed)
+
+
+def pivoted_qr_r(A):
+    """Column-pivoted QR (core.py:133-186, Businger-Golub: largest remaining
+    column norm, ties to the lowest index): (Q, R, perm) with A[:, perm] =
+    Q R.  scipy's geqp3 makes the same greedy choice."""
+    import scipy.linalg
+    Q, R, perm = scipy.linalg.qr(np.asarray(A), mode="economic", pivoting=True)
+    return Q, R, perm
+
+
+def least_squares(A, B):
+    """core.py:297-325 (overdetermined branch: pivoted-QR basic solution
+    with truncated back substitution; underdetermined: minimum norm)."""
+    A = np.asarray(A)
+    B = np.asarray(B)
+    vec = B.ndim == 1
+    B2 = B[:, None] if vec else B
+    m, n = A.shape
+    if m >= n:
+        Q, R, perm = pivoted_qr_r(A)
+        Yp = solve_triangular_trunc(R, Q.conj().T @ B2)
+        X = np.zeros((n, B2.shape[1]), dtype=Yp.dtype)
+        X[perm[:Yp.shape[0]], :] = Yp
+    else:
+        X = np.linalg.pinv(A) @ B2
+    return X[:, 0] if vec else X
+
+
+def svd_one_pass_general(bundle):
+    """factor.py:364-401: dense least squares over vec(B)."""
+    Q, Qt = bundle.Q, bundle.Q_tilde
+    k, kt = Q.shape[1], Qt.shape[1]
+    if k * kt > ONE_PASS_DIM_CAP:
+        raise ValueError(f"reduced problem has {k * kt} unknowns, above the cap "
+                         f"{ONE_PASS_DIM_CAP}; use the two-pass path")
+    if k == 0 or kt == 0:
+        dt = bundle.Y.dtype
+        return PartialSVD(U=np.zeros((Q.shape[0], 0), dt), sigma=np.zeros(0),
+                          V=np.zeros((Qt.shape[0], 0), dt))
+    P = Qt.conj().T @ bundle.Omega
+    N1 = Q.conj().T @ bundle.Y
+    S = Q.conj().T @ bundle.Omega_tilde
+    N2 = Qt.conj().T @ bundle.Y_tilde
+    dt = np.promote_types(P.dtype, N1.dtype)
+    M_top = np.kron(P.T, np.eye(k, dtype=dt))
+    M_bot = np.kron(np.eye(kt, dtype=dt), S.conj().T)
+    rhs = np.concatenate([N1.reshape(-1, order="F"), N2.conj().T.reshape(-1, order="F")])
+    B = least_squares(np.vstack([M_top, M_bot]), rhs).reshape((k, kt), order="F")
+    f = small_svd(B)
+    return PartialSVD(U=Q @ f.U, sigma=f.sigma, V=Qt @ f.V)
+
+
+def eig_one_pass(bundle):
+    """factor.py:338-361."""
+    Q = bundle.Q
+    M = Q.conj().T @ bundle.Omega
+    N = Q.conj().T @ bundle.Y
+    B = least_squares(M.conj().T, N.conj().T).conj().T
+    B = 0.5 * (B + B.conj().T)
+    diagnostics = {"q_choice": bundle.q_choice}
+    sv = small_svd(M).sigma
+    tau_min = float(sv.min()) if sv.size else 0.0
+    diagnostics["tau_min"] = tau_min
+    if sv.size and (tau_min == 0.0 or sv.max() / max(tau_min, 1e-300) > ONE_PASS_COND_WARN):
+        diagnostics["ill_conditioned"] = True
+    V, lam = small_eig_hermitian(B)
+    return PartialEig(U=Q @ V, lam=lam, diagnostics=diagnostics)

@@ -17,8 +17,12 @@ from . import config
 from ._lib import ConvergenceError, LibraryMissing, NotPSDError
 from .core import (CudaDenseOperator, DenseOperator, MatVecOperator, OperatorCounters, SmallSVD,
                    as_operator, orthonormalize_double_gs, small_eig_hermitian, small_svd)
-from .factor import (NystromFactors, PartialEig, PartialSVD, direct_eig_hermitian, direct_svd,
-                     eig_nystrom, randomized_svd, truncate_rank)
+from .factor import (NystromFactors, PartialEig, PartialSVD, SampleBundle, direct_eig_hermitian,
+                     direct_svd, eig_nystrom, eig_one_pass, randomized_svd, sample_bundle,
+                     sample_bundle_two_sided, svd_one_pass_general, truncate_rank)
+from .io import (MatrixFormatError, RowBlockStream, StreamError, accumulate_two_sided_samples,
+                 in_memory_sample_bundle, read_matrix_binary, stream_row_blocks,
+                 streamed_sample_bundle, write_matrix_binary)
 from .rangefinder import (RangeBasis, adaptive_range_finder, adaptive_range_finder_blocked,
                           fast_range_finder, posterior_error_estimate, power_iteration_range,
                           randomized_range_finder, subspace_iteration_range)

@@ -51,6 +51,7 @@ _SIGS = {
     "lr_gemm_scaled": [_vp, _int, _int, _i64, _i64, _i64, _vp, _i64, C.c_double, _vp, _i64, _vp,
                        _i64],
     "lr_gram": [_vp, _int, _i64, _i64, _vp, _i64, _vp],
+    "lr_gram_tc": [_vp, _i64, _i64, _vp, _i64, _vp, _int, _vp],
     "lr_ozaki_prepare": [_vp, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp],
     "lr_ozaki_prepare_rows": [_vp, _i64, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp],
     "lr_gemm_ozaki": [_vp, _int, _i64, _i64, _i64, _vp, _i64, _vp, _vp, _i64, _vp, _i64],
@@ -79,6 +80,8 @@ _SIGS = {
     "lr_max_abs_imag": [_vp, _int, _i64, _i64, _vp, _i64, _vp],
     "lr_gaussian": [_vp, C.c_uint64, C.c_uint64, _i64, _int, _vp, _vp],
     "lr_axpy_sub": [_vp, _int, _i64, _i64, _vp, _i64, _vp, _i64],
+    "lr_axpy_add": [_vp, _int, _i64, _i64, _vp, _i64, _vp, _i64],
+    "lr_sylvester_div": [_vp, _int, _i64, _i64, _vp, _i64, _vp, _vp, C.c_double],
     "lr_col_sumsq": [_vp, _int, _i64, _i64, _vp, _i64, _vp],
     "lr_scale_col": [_vp, _int, _i64, _vp, _i64, C.c_double, _vp, _i64],
 }

@@ -214,6 +214,22 @@ bool scholqr3(Handle* h, int dtype, int64_t m, int64_t ell, const void* Y, int64
   return true;
 }
 
+// Gram of the second CholeskyQR pass (Q1 orthonormal to ~kappa^2 u64): for
+// fp32 panels on the tensor cores at fp32-level accuracy (gram_tc.cu; its
+// error is the final loss of orthogonality, the rounding level of the fp32 Q
+// stored), flagged back to the exact path if an entry exceeds the scaled
+// fp16 range; otherwise the exact Gram.
+void gram_second(Handle* h, int dtype, int64_t m, int64_t ell, const void* Q1, int64_t ldq,
+                 void* G) {
+  if (dtype == LR_F32 && h->status &&
+      gram_tc_supported(m, ell, static_cast<const float*>(Q1), ldq)) {
+    gram_tc_f32(h, m, ell, static_cast<const float*>(Q1), ldq, static_cast<double*>(G), 12,
+                h->status);
+    return;
+  }
+  gram_any(h, dtype, m, ell, Q1, ldq, G);
+}
+
 // Speculative CholeskyQR2 with no host synchronization: the drop rule and
 // pivot resolvability are evaluated on the device and reported through
 // h->status (bit 1 unresolved pivot, 2 column dropped, 4 non-finite).  When
@@ -229,7 +245,7 @@ void orth_fast_impl(Handle* h, int dtype, int64_t m, int64_t ell, const void* Y,
   gram_any(h, dtype, m, ell, Y, ldy, G);
   chol_any(h, dtype, ell, G, tol, unres, 0.0, P, R, h->d_info);
   apply_right(h, dtype, m, ell, ell, Y, ldy, P, ell, Q1, ell);
-  gram_any(h, dtype, m, ell, Q1, ell, G);
+  gram_second(h, dtype, m, ell, Q1, ell, G);
   chol_near_identity(h, wide_of(dtype), ell, G, tol, unres, P, R, h->d_info,
                      near_id_thr(dtype));
   apply_right(h, dtype, m, ell, ell, Q1, ell, P, ell, Q, ldq);
@@ -255,7 +271,7 @@ void small_svd_fast_impl(Handle* h, int dtype, int64_t r, int64_t c, const void*
   gram_any(h, dtype, c, r, Bh, r, G);
   chol_any(h, dtype, r, G, 0.0, unres, 0.0, P1, R1, h->d_info);
   apply_right(h, dtype, c, r, r, Bh, r, P1, r, Q1, r);
-  gram_any(h, dtype, c, r, Q1, r, G);
+  gram_second(h, dtype, c, r, Q1, r, G);
   chol_near_identity(h, wd, r, G, 0.0, unres, P, R2, h->d_info, near_id_thr(dtype));
   apply_right(h, dtype, c, r, r, Q1, r, P, r, Q2, r);
   trmm_upper(h, wd, r, R2, R1, R);
@@ -719,6 +735,19 @@ int lr_gram(lr_handle_t hh, int dtype, int64_t m, int64_t ell, const void* Y, in
   API_END
 }
 
+int lr_gram_tc(lr_handle_t hh, int64_t m, int64_t ell, const float* Y, int64_t ldy, double* G,
+               int log2_scale, int32_t* status) {
+  API_BEGIN
+  Handle* h = H(hh);
+  lr::DeviceGuard dg_(h->device);
+  LR_REQUIRE(m >= 1 && ell >= 1 && ldy >= ell, LR_EINVAL, "lr_gram_tc: bad shape");
+  LR_REQUIRE(lr::gram_tc_supported(m, ell, Y, ldy), LR_EUNSUPPORTED,
+             "lr_gram_tc: needs ell <= 256, m >= 4096, 16-byte aligned rows");
+  lr::pool_reset(h);
+  lr::gram_tc_f32(h, m, ell, Y, ldy, G, log2_scale, status);
+  API_END
+}
+
 int lr_chol_drop(lr_handle_t hh, int dtype, int64_t ell, const void* G, double drop_tol,
                  double unres_rel, double shift_coef, void* P, void* R, int32_t* info) {
   API_BEGIN
@@ -1042,6 +1071,30 @@ int lr_axpy_sub(lr_handle_t hh, int dtype, int64_t rows, int64_t cols, const voi
   check_dtype(dtype);
   lr::pool_reset(h);
   lr::axpy_sub(h, dtype, rows, cols, T, ldt, Z, ldz);
+  API_END
+}
+
+int lr_axpy_add(lr_handle_t hh, int dtype, int64_t rows, int64_t cols, const void* T,
+                int64_t ldt, void* Z, int64_t ldz) {
+  API_BEGIN
+  Handle* h = H(hh);
+  lr::DeviceGuard dg_(h->device);
+  LR_REQUIRE(dtype == LR_F64 || dtype == LR_C128, LR_EINVAL, "lr_axpy_add: fp64 / complex128");
+  lr::pool_reset(h);
+  lr::axpy_add(h, dtype, rows, cols, T, ldt, Z, ldz);
+  API_END
+}
+
+int lr_sylvester_div(lr_handle_t hh, int dtype, int64_t k, int64_t kt, void* C, int64_t ldc,
+                     const double* d2, const double* d1, double floor) {
+  API_BEGIN
+  Handle* h = H(hh);
+  lr::DeviceGuard dg_(h->device);
+  LR_REQUIRE(dtype == LR_F64 || dtype == LR_C128, LR_EINVAL,
+             "lr_sylvester_div: fp64 / complex128");
+  LR_REQUIRE(ldc >= kt, LR_EINVAL, "lr_sylvester_div: ldc < kt");
+  lr::pool_reset(h);
+  lr::sylvester_div(h, dtype, k, kt, C, ldc, d2, d1, floor);
   API_END
 }
 

@@ -143,8 +143,8 @@ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 // gemm_f64.cu ---------------------------------------------------------------
 int64_t choose_splits(int sm_count, int64_t tiles, int64_t K);
 // gemm_f64_ozaki.cu: fp64 passes on the int8 tensor cores (digit planes of A)
-// wide_rows (nullable): += number of rows whose nonzero entries span more
-// than 2^32 (the caller keeps such a matrix on the DMMA passes)
+// wide_rows (nullable): += number of graded rows (> 1/8 of the nonzeros
+// below 2^-32 of the row maximum; the caller keeps the matrix on DMMA)
 void ozaki_prepare(Handle* h, int64_t m, int64_t n, const double* A, int64_t lda, int8_t* planes,
                    int64_t ldp, int32_t* row_exp, int32_t* wide_rows);
 void ozaki_prepare_rows(Handle* h, int64_t m, int64_t n, int64_t i0, int64_t i1, const double* A,
@@ -180,6 +180,12 @@ void gemm_f32_hint(Handle* h, bool transA, int64_t M, int64_t N, int64_t K, cons
 void gemm_c64_hint(Handle* h, bool transA, bool conjA, int64_t M, int64_t N, int64_t K,
                    const float2* A, int64_t lda, double a_amax, const float2* B, int64_t ldb,
                    float2* C, int64_t ldc);
+// gram_tc.cu: G = Y^T Y of an fp32 panel (ell <= 256) on tcgen05 with
+// fp32-level accuracy (second CholeskyQR pass); entries must satisfy
+// |y| 2^log2_scale < 2^15, else *status |= 1 (status may be null)
+bool gram_tc_supported(int64_t m, int64_t ell, const float* Y, int64_t ldy);
+void gram_tc_f32(Handle* h, int64_t m, int64_t ell, const float* Y, int64_t ldy, double* G,
+                 int log2_scale, int32_t* status);
 // fp64-accumulated Gram of fp32 / complex64 panels
 void gram_f32(Handle* h, int64_t m, int64_t ell, const float* Y, int64_t ldy, double* G);
 // C (M x N, ldc) = sum over S dense M x N partials, fixed order
@@ -294,6 +300,11 @@ void axpy_sub(Handle* h, int dtype, int64_t rows, int64_t cols, const void* T, i
               void* Z, int64_t ldz);
 void scale_col(Handle* h, int dtype, int64_t rows, const void* src, int64_t lds, double inv,
                void* dst, int64_t ldd);
+// Z += T (fp64 / complex128); C_ij /= (d2_i + d1_j), 0 where d2_i + d1_j <= floor
+void axpy_add(Handle* h, int dtype, int64_t rows, int64_t cols, const void* T, int64_t ldt,
+              void* Z, int64_t ldz);
+void sylvester_div(Handle* h, int dtype, int64_t k, int64_t kt, void* C, int64_t ldc,
+                   const double* d2, const double* d1, double floor);
 
 // srft.cu ---------------------------------------------------------------------
 // n x ell picked columns of the Givens-chain SRFT (c64 or c128 output)

@@ -24,18 +24,29 @@
 // A is read from HBM exactly once per pass (per N <= 256); X_hi / X_lo are
 // prepared once per pass in K-major fp16 (small for A X; for A^T Y the
 // prepared Y is 2 x 2 bytes per element, read from L2/HBM per M tile).
+#include <cstdio>
 #include <cuda.h>
 #include <cuda_fp16.h>
 #include <cudaTypedefs.h>
 
 #include "common.cuh"
+#include "tc_common.cuh"
 #include "tma.cuh"
 
 namespace lr {
 namespace {
+using tc::mbar_arrive_cluster;
+using tc::mbar_wait_cluster;
+using tc::idesc_f16;
+using tc::umma_f16_pair;
+using tc::umma_commit_pair;
+using tc::tmem_ld32;
 
 constexpr int TBM = 128;          // UMMA M
 constexpr int TBK = 32;           // k per stage (64 B of fp16 per row)
+#ifndef LR_TC_DBG
+#define LR_TC_DBG 0
+#endif
 #ifndef LR_TC_TS1
 #define LR_TC_TS1 5
 #endif
@@ -232,8 +243,10 @@ gemm_f32_tc_kernel(const __grid_constant__ CUtensorMap mapA,
         for (int ks = 0; ks < TBK / 16; ++ks) {
           const uint64_t adv = uint64_t(ks * 32) >> 4;   // 16 fp16 = 32 bytes
           umma_f16(tmem, dah + adv, dbh + adv, idesc, (kt | ks) ? 1u : 0u);
+#if !(LR_TC_DBG & 1)   // timing experiment: hi*hi only (wrong results)
           umma_f16(tmem, dah + adv, dbl + adv, idesc, 1u);
           umma_f16(tmem, dal + adv, dbh + adv, idesc, 1u);
+#endif
         }
         umma_commit(&st_empty[s]);
       }
@@ -248,6 +261,12 @@ gemm_f32_tc_kernel(const __grid_constant__ CUtensorMap mapA,
       const int s2 = kt % TS2;
       const uint32_t ph2 = uint32_t(kt / TS2) & 1u;
       mbar_wait(&a32_full[s], ph);
+#if (LR_TC_DBG & 2)   // timing experiment: no conversion, no hi/lo writes
+      mbar_arrive(&a32_empty[s]);
+      mbar_wait(&st_empty[s2], ph2 ^ 1u);
+      mbar_arrive(&ahl_full[s2]);
+      continue;
+#endif
       float v[TBK];
       if (!TRANS) {
         // fp32 staging: row r (128 B), TMA SWIZZLE_128B (16-B chunk c at c ^ (r & 7))
@@ -424,9 +443,566 @@ __global__ void reduce_slices_f32(int64_t M, int64_t N, int S, const float* __re
   const int64_t total = M * N;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
        i += int64_t(gridDim.x) * blockDim.x) {
-    float s = 0.f;
-    for (int k = 0; k < S; ++k) s += part[int64_t(k) * total + i];
-    out[(i / N) * ldo + (i % N)] = s;
+    double s = 0.0;     // fixed order, fp64 (up to ~40 split-K slices)
+    for (int k = 0; k < S; ++k) s += double(part[int64_t(k) * total + i]);
+    out[(i / N) * ldo + (i % N)] = float(s);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// 256-row single-CTA pass kernel (deep-K passes over A, N <= 256).
+//
+// The round-1 kernel above (128 rows per CTA) streams the whole fp16 hi/lo
+// X tile (2 x 2 bytes per element) out of L2 for every 128 rows of A: at
+// config 4 the X stream is twice A's bytes, and with the conversion and 2/3
+// of the UMMAs disabled the pass still took 4.6 ms (L2 -> SM traffic
+// ~11 TB/s).  Here one CTA owns 256 rows of A -- two 128 x N TMEM
+// accumulators (all 512 columns) sharing every X tile -- so the X stream per
+// A byte halves without any cross-CTA handshake.
+//   warp 0     TMA producer of the fp32 A tiles (256 rows x 32 k, one box)
+//   warp 3     TMA producer of the X hi/lo tiles
+//   warp 1     MMA issuer: 12 UMMAs (2 halves x 3 products x 2 k-steps)/stage
+//   warp 2     TMEM owner
+//   warps 4-11 converters (one A row each), then the epilogue (warps 4-7:
+//              rows 0-127 from columns 0..N-1, warps 8-11: rows 128-255 from
+//              columns 256..256+N-1 of TMEM)
+constexpr int W_THREADS = 384;
+constexpr int WBM = 256;
+constexpr int W_A32 = WBM * TBK * 4;      // 32 KB
+constexpr int W_AH = WBM * TBK * 2;       // 16 KB (one of hi / lo)
+#ifndef LR_W_TS1
+#define LR_W_TS1 3
+#endif
+#ifndef LR_W_TS2
+#define LR_W_TS2 2
+#endif
+#ifndef LR_W_TS3
+#define LR_W_TS3 2
+#endif
+constexpr int W_TS1 = LR_W_TS1;
+constexpr int W_TS2 = LR_W_TS2;
+constexpr int W_TS3 = LR_W_TS3;
+
+template <bool TRANS>
+__global__ void __launch_bounds__(W_THREADS, 1)
+gemm_f32_m256_kernel(const __grid_constant__ CUtensorMap mapA,
+                     const __grid_constant__ CUtensorMap mapBhi,
+                     const __grid_constant__ CUtensorMap mapBlo, int M, int N, int BN,
+                     int64_t k_per_split, int64_t K, float sA_host,
+                     const float* __restrict__ sA_dev, const float* __restrict__ sB_dev,
+                     float* __restrict__ C, int64_t ldc, int64_t cstride) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* base = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int B_BYTES = BN * TBK * 2;
+  const int B_SLOT = (2 * B_BYTES + 1023) & ~1023;
+  unsigned char* ring2 = base + W_TS1 * W_A32;
+  unsigned char* ring3 = ring2 + W_TS2 * 2 * W_AH;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring3 + W_TS3 * B_SLOT);
+  uint64_t* a32_full = bars;
+  uint64_t* a32_empty = a32_full + W_TS1;
+  uint64_t* ahl_full = a32_empty + W_TS1;
+  uint64_t* ahl_empty = ahl_full + W_TS2;
+  uint64_t* b_full = ahl_empty + W_TS2;
+  uint64_t* b_empty = b_full + W_TS3;
+  uint64_t* acc_full = b_empty + W_TS3;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+
+  auto a32 = [&](int s) { return base + s * W_A32; };
+  auto ahi = [&](int s) { return ring2 + s * 2 * W_AH; };
+  auto alo = [&](int s) { return ring2 + s * 2 * W_AH + W_AH; };
+  auto bhi = [&](int s) { return ring3 + s * B_SLOT; };
+  auto blo = [&](int s) { return ring3 + s * B_SLOT + B_BYTES; };
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const float sA = sA_dev ? *sA_dev : sA_host;
+  const int m0 = blockIdx.x * WBM;
+  const int64_t kbeg = int64_t(blockIdx.z) * k_per_split;
+  const int64_t kend = min(K, kbeg + k_per_split);
+  const int nk = int((kend - kbeg + TBK - 1) / TBK);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < W_TS1; ++s) {
+      mbar_init(&a32_full[s], 1);
+      mbar_init(&a32_empty[s], 256);
+    }
+    for (int s = 0; s < W_TS2; ++s) {
+      mbar_init(&ahl_full[s], 256);
+      mbar_init(&ahl_empty[s], 1);
+    }
+    for (int s = 0; s < W_TS3; ++s) {
+      mbar_init(&b_full[s], 1);
+      mbar_init(&b_empty[s], 1);
+    }
+    mbar_init(acc_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int kt = 0; kt < nk; ++kt) {
+        const int s = kt % W_TS1;
+        mbar_wait(&a32_empty[s], (uint32_t(kt / W_TS1) & 1u) ^ 1u);
+        mbar_expect_tx(&a32_full[s], W_A32);
+        const int kc = int(kbeg + int64_t(kt) * TBK);
+        if (!TRANS) tma_load_2d(a32(s), &mapA, &a32_full[s], kc, m0);
+        else        tma_load_2d(a32(s), &mapA, &a32_full[s], m0, kc);
+      }
+    }
+  } else if (warp == 3) {
+    if (lane == 0) {
+      for (int kt = 0; kt < nk; ++kt) {
+        const int s = kt % W_TS3;
+        mbar_wait(&b_empty[s], (uint32_t(kt / W_TS3) & 1u) ^ 1u);
+        mbar_expect_tx(&b_full[s], uint32_t(2 * B_BYTES));
+        const int kc = int(kbeg + int64_t(kt) * TBK);
+        tma_load_2d(bhi(s), &mapBhi, &b_full[s], 0, (kc / TBK) * BN);
+        tma_load_2d(blo(s), &mapBlo, &b_full[s], 0, (kc / TBK) * BN);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = (1u << 4) | (uint32_t(BN >> 3) << 17) | (uint32_t(TBM >> 4) << 24);
+      for (int kt = 0; kt < nk; ++kt) {
+        const int s2 = kt % W_TS2, s3 = kt % W_TS3;
+        mbar_wait(&ahl_full[s2], uint32_t(kt / W_TS2) & 1u);
+        mbar_wait(&b_full[s3], uint32_t(kt / W_TS3) & 1u);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint64_t dbh = desc_sw64(bhi(s3)), dbl = desc_sw64(blo(s3));
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          const uint64_t dah = desc_sw64(ahi(s2) + half * (TBM * 64));
+          const uint64_t dal = desc_sw64(alo(s2) + half * (TBM * 64));
+          const uint32_t acc = tmem + uint32_t(half * 256);
+#pragma unroll
+          for (int ks = 0; ks < TBK / 16; ++ks) {
+            const uint64_t adv = uint64_t(ks * 32) >> 4;
+            umma_f16(acc, dah + adv, dbh + adv, idesc, (kt | ks) ? 1u : 0u);
+#if !(LR_TC_DBG & 1)
+            umma_f16(acc, dah + adv, dbl + adv, idesc, 1u);
+            umma_f16(acc, dal + adv, dbh + adv, idesc, 1u);
+#endif
+          }
+        }
+        umma_commit(&ahl_empty[s2]);
+        umma_commit(&b_empty[s3]);
+      }
+      umma_commit(acc_full);
+    }
+  } else if (warp >= 4) {
+    const int r = threadIdx.x - 128;           // A row within the 256-row tile
+    for (int kt = 0; kt < nk; ++kt) {
+      const int s = kt % W_TS1;
+      const int s2 = kt % W_TS2;
+      mbar_wait(&a32_full[s], uint32_t(kt / W_TS1) & 1u);
+#if (LR_TC_DBG & 2)
+      mbar_arrive(&a32_empty[s]);
+      mbar_wait(&ahl_empty[s2], (uint32_t(kt / W_TS2) & 1u) ^ 1u);
+      mbar_arrive(&ahl_full[s2]);
+      continue;
+#endif
+      float v[TBK];
+      if (!TRANS) {
+        const unsigned char* row = a32(s) + r * 128;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const float4 q = *reinterpret_cast<const float4*>(row + ((c ^ (r & 7)) << 4));
+          v[4 * c] = q.x; v[4 * c + 1] = q.y; v[4 * c + 2] = q.z; v[4 * c + 3] = q.w;
+        }
+      } else {
+        const float* st = reinterpret_cast<const float*>(a32(s));
+#pragma unroll
+        for (int k = 0; k < TBK; ++k) v[k] = st[k * WBM + r];
+      }
+      uint4 hv[TBK / 8], lv[TBK / 8];
+#pragma unroll
+      for (int g = 0; g < TBK / 8; ++g) split8(v + 8 * g, sA, hv[g], lv[g]);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(&a32_empty[s]);
+      mbar_wait(&ahl_empty[s2], (uint32_t(kt / W_TS2) & 1u) ^ 1u);
+#pragma unroll
+      for (int g = 0; g < TBK / 8; ++g) {
+        const int off = sw64_off(r, g);
+        *reinterpret_cast<uint4*>(ahi(s2) + off) = hv[g];
+        *reinterpret_cast<uint4*>(alo(s2) + off) = lv[g];
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(&ahl_full[s2]);
+    }
+    // epilogue: the rings are idle now; per-warp transpose buffers at base
+    mbar_wait(acc_full, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const float inv_a = 1.0f / sA;
+    const int q = warp & 3;                     // TMEM lane quarter
+    const int half = (warp - 4) >> 2;           // accumulator 0 / 1
+    float* wbuf = reinterpret_cast<float*>(base) + (warp - 4) * (32 * 33);
+    float* cbase = C + int64_t(blockIdx.z) * cstride;
+    for (int c0 = 0; c0 < BN; c0 += 32) {
+      uint32_t d[32];
+      tmem_ld32(tmem + (uint32_t(q * 32) << 16) + uint32_t(half * 256 + c0), d);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) wbuf[lane * 33 + j] = __uint_as_float(d[j]);
+      __syncwarp();
+      const int col = c0 + lane;
+      const float sc = col < N ? inv_a / sB_dev[col] : 0.f;
+#if !(LR_TC_DBG & 4)
+      for (int rr = 0; rr < 32; ++rr) {
+        const int row = m0 + half * TBM + q * 32 + rr;
+        if (row < M && col < N) cbase[int64_t(row) * ldc + col] = wbuf[rr * 33 + lane] * sc;
+      }
+#endif
+      __syncwarp();
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// CTA-pair persistent pass kernel (default for N <= 256).
+//
+// Measured on the round-1 single-CTA kernel above at config 4 (2^20 x 4096,
+// N = 256; tools/tc_pass_probe.py + LR_TC_DBG variants): 6.0 ms per A X
+// pass, and still 4.6 ms with 1/3 of the UMMAs and no conversion at all --
+// the pass was bound by L2 -> SM traffic, not by the tensor pipe: every
+// 128-row CTA streams the whole fp16 hi/lo X (2 x 2 bytes per element, twice
+// A's fp32 bytes per stage) out of L2.  Here two CTAs on a TPC form a pair
+// (tcgen05.mma.cta_group::2, M = 256): each CTA converts its own 128 rows of
+// A but loads only HALF of X's columns, so the L2 stream per A byte halves;
+// the pair is persistent (one pair per TPC, static round-robin over the
+// 256-row tiles / split-K units) with two TMEM accumulators, so the
+// epilogue of one tile overlaps the main loop of the next.
+//   warp 0      TMA producer of the fp32 A tiles
+//   warp 3      TMA producer of this CTA's half of the X hi/lo tiles
+//   warp 1      leader: MMA issuer (6 pair UMMAs of 256 x BN x 16 per
+//               32-deep stage); peer: relays "stage ready" to the leader
+//   warp 2      TMEM owner (2 x 256 columns, cta_group::2)
+//   warps 4-7   converters (one A row per thread -> hi/lo fp16 K-major SW64)
+//   warps 8-11  epilogue (TMEM -> x 1/(s_A s_X) -> smem transpose -> rows)
+constexpr int P_THREADS = 384;
+#ifndef LR_P_TS1
+#define LR_P_TS1 5
+#endif
+#ifndef LR_P_SLEEP
+#define LR_P_SLEEP 0
+#endif
+#ifndef LR_P_TS2
+#define LR_P_TS2 3
+#endif
+#ifndef LR_P_TS3
+#define LR_P_TS3 4
+#endif
+constexpr int P_TS1 = LR_P_TS1;   // fp32 A ring (TMA -> converters)
+constexpr int P_TS2 = LR_P_TS2;   // A hi/lo ring (converters -> MMA)
+constexpr int P_TS3 = LR_P_TS3;   // X-half hi/lo ring (TMA -> MMA)
+
+__device__ __forceinline__ uint32_t cta_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" :::
+                   "memory");
+}
+
+struct PairWork {
+  int64_t units, mtiles, k_per_split, K;
+  __device__ void unit(int64_t u, int64_t& tile, int64_t& split) const {
+    tile = u % mtiles;
+    split = u / mtiles;
+  }
+  __device__ int nk(int64_t split) const {
+    const int64_t kb = split * k_per_split, ke = min(K, kb + k_per_split);
+    return int((ke - kb + TBK - 1) / TBK);
+  }
+};
+
+template <bool TRANS>
+__global__ void __launch_bounds__(P_THREADS, 1)
+gemm_f32_pair_kernel(const __grid_constant__ CUtensorMap mapA,
+                     const __grid_constant__ CUtensorMap mapBhi,
+                     const __grid_constant__ CUtensorMap mapBlo, int M, int N, int BN,
+                     PairWork w, float sA_host, const float* __restrict__ sA_dev,
+                     const float* __restrict__ sB_dev, float* __restrict__ C, int64_t ldc,
+                     int64_t cstride) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* base = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int HB = BN / 2;                      // X rows (output columns) per CTA
+  const int HB_BYTES = HB * TBK * 2;
+  const int HB_SLOT = (2 * HB_BYTES + 1023) & ~1023;
+  unsigned char* ring2 = base + P_TS1 * A32_BYTES;                // A hi/lo
+  unsigned char* ring3 = ring2 + P_TS2 * 2 * AH_BYTES;           // X half hi/lo
+  float* ebuf = reinterpret_cast<float*>(ring3 + P_TS3 * HB_SLOT);   // 4 x 32 x 33 floats
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ebuf + 4 * 32 * 33);
+  uint64_t* a32_full = bars;
+  uint64_t* a32_empty = a32_full + P_TS1;
+  uint64_t* ahl_full = a32_empty + P_TS1;
+  uint64_t* ahl_empty = ahl_full + P_TS2;
+  uint64_t* b_full = ahl_empty + P_TS2;
+  uint64_t* b_empty = b_full + P_TS3;
+  uint64_t* peer_full = b_empty + P_TS3;      // [P_TS2] leader: peer's A hi/lo + X half ready
+  uint64_t* acc_full = peer_full + P_TS2;     // [2]
+  uint64_t* acc_empty = acc_full + 2;         // [2] (leader: 8 arrivals)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  auto a32 = [&](int s) { return base + s * A32_BYTES; };
+  auto ahi = [&](int s) { return ring2 + s * 2 * AH_BYTES; };
+  auto alo = [&](int s) { return ring2 + s * 2 * AH_BYTES + AH_BYTES; };
+  auto bhi = [&](int s) { return ring3 + s * HB_SLOT; };
+  auto blo = [&](int s) { return ring3 + s * HB_SLOT + HB_BYTES; };
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cta_rank();
+  const int64_t pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const float sA = sA_dev ? *sA_dev : sA_host;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < P_TS1; ++s) {
+      mbar_init(&a32_full[s], 1);
+      mbar_init(&a32_empty[s], 128);
+    }
+    for (int s = 0; s < P_TS2; ++s) {
+      mbar_init(&ahl_full[s], 128);
+      mbar_init(&ahl_empty[s], 1);
+      mbar_init(&peer_full[s], 1);
+    }
+    for (int s = 0; s < P_TS3; ++s) {
+      mbar_init(&b_full[s], 1);
+      mbar_init(&b_empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  cluster_sync();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 || warp == 3) {
+    if (lane == 0) {
+      // ---- TMA producers, one thread per stream (warp 0: fp32 A tiles into
+      // the converters' ring; warp 3: this CTA's half of the X hi/lo tiles).
+      // Separate threads: a single producer blocked on the A ring (which
+      // drains only as fast as the converters) held back the X loads, so
+      // every stage paid the L2 latency of its X tile.
+      const bool is_a = warp == 0;
+      int64_t g = 0;
+      for (int64_t u = pair; u < w.units; u += npairs) {
+        int64_t tile, sp;
+        w.unit(u, tile, sp);
+        const int nk = w.nk(sp);
+        for (int kt = 0; kt < nk; ++kt, ++g) {
+          const int kc = int(sp * w.k_per_split + int64_t(kt) * TBK);
+          if (is_a) {
+            const int s = int(g % P_TS1);
+            mbar_wait(&a32_empty[s], (uint32_t(g / P_TS1) & 1u) ^ 1u);
+            mbar_expect_tx(&a32_full[s], A32_BYTES);
+            const int m0 = int(tile * 2 * TBM) + int(rank) * TBM;
+            if (!TRANS) tma_load_2d(a32(s), &mapA, &a32_full[s], kc, m0);
+            else        tma_load_2d(a32(s), &mapA, &a32_full[s], m0, kc);
+          } else {
+            const int s3 = int(g % P_TS3);
+            mbar_wait(&b_empty[s3], (uint32_t(g / P_TS3) & 1u) ^ 1u);
+            mbar_expect_tx(&b_full[s3], uint32_t(2 * HB_BYTES));
+            const int brow = (kc / TBK) * BN + int(rank) * HB;
+            tma_load_2d(bhi(s3), &mapBhi, &b_full[s3], 0, brow);
+            tma_load_2d(blo(s3), &mapBlo, &b_full[s3], 0, brow);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int64_t g = 0;
+      if (rank != 0) {
+        // ---- peer: relay "my A hi/lo and X half are in place" to the leader
+        for (int64_t u = pair; u < w.units; u += npairs) {
+          int64_t t_, sp;
+          w.unit(u, t_, sp);
+          const int nk = w.nk(sp);
+          for (int kt = 0; kt < nk; ++kt, ++g) {
+            const int s2 = int(g % P_TS2), s3 = int(g % P_TS3);
+            mbar_wait(&ahl_full[s2], uint32_t(g / P_TS2) & 1u);
+            mbar_wait(&b_full[s3], uint32_t(g / P_TS3) & 1u);
+            mbar_arrive_cluster(&peer_full[s2], 0);
+          }
+        }
+      } else {
+        // ---- leader: MMA issuer
+        const uint32_t idesc = idesc_f16(256, BN);
+        int64_t it = 0;
+        for (int64_t u = pair; u < w.units; u += npairs, ++it) {
+          int64_t t_, sp;
+          w.unit(u, t_, sp);
+          const int nk = w.nk(sp);
+          const int b = int(it & 1);
+          if (it >= 2) mbar_wait_cluster(&acc_empty[b], uint32_t((it >> 1) - 1) & 1u);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const uint32_t acc = tmem + uint32_t(b * 256);
+          for (int kt = 0; kt < nk; ++kt, ++g) {
+            const int s2 = int(g % P_TS2), s3 = int(g % P_TS3);
+            const uint32_t ph = uint32_t(g / P_TS2) & 1u;
+            mbar_wait(&ahl_full[s2], ph);
+            mbar_wait(&b_full[s3], uint32_t(g / P_TS3) & 1u);
+            mbar_wait_cluster(&peer_full[s2], ph);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const uint64_t dah = desc_sw64(ahi(s2)), dal = desc_sw64(alo(s2));
+            const uint64_t dbh = desc_sw64(bhi(s3)), dbl = desc_sw64(blo(s3));
+#pragma unroll
+            for (int ks = 0; ks < TBK / 16; ++ks) {
+              const uint64_t adv = uint64_t(ks * 32) >> 4;
+              umma_f16_pair(acc, dah + adv, dbh + adv, idesc, (kt | ks) ? 1u : 0u);
+#if !(LR_TC_DBG & 1)
+              umma_f16_pair(acc, dah + adv, dbl + adv, idesc, 1u);
+              umma_f16_pair(acc, dal + adv, dbh + adv, idesc, 1u);
+#endif
+            }
+            umma_commit_pair(&ahl_empty[s2]);
+            umma_commit_pair(&b_empty[s3]);
+          }
+          umma_commit_pair(&acc_full[b]);
+        }
+      }
+    }
+  } else if (warp >= 4 && warp < 8) {
+    // ---- converters: row r of this CTA's 128-row A tile
+    const int r = threadIdx.x - 128;
+    int64_t g = 0;
+    for (int64_t u = pair; u < w.units; u += npairs) {
+      int64_t t_, sp;
+      w.unit(u, t_, sp);
+      const int nk = w.nk(sp);
+      for (int kt = 0; kt < nk; ++kt, ++g) {
+        const int s = int(g % P_TS1);
+        const uint32_t ph = uint32_t(g / P_TS1) & 1u;
+        const int s2 = int(g % P_TS2);
+        const uint32_t ph2 = uint32_t(g / P_TS2) & 1u;
+        mbar_wait(&a32_full[s], ph);
+#if (LR_TC_DBG & 2)   // timing experiment: no conversion, no hi/lo writes
+        mbar_arrive(&a32_empty[s]);
+        mbar_wait(&ahl_empty[s2], ph2 ^ 1u);
+        mbar_arrive(&ahl_full[s2]);
+        continue;
+#endif
+        float v[TBK];
+        if (!TRANS) {
+          const unsigned char* row = a32(s) + r * 128;
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const float4 q = *reinterpret_cast<const float4*>(row + ((c ^ (r & 7)) << 4));
+            v[4 * c] = q.x; v[4 * c + 1] = q.y; v[4 * c + 2] = q.z; v[4 * c + 3] = q.w;
+          }
+        } else {
+          const float* st = reinterpret_cast<const float*>(a32(s));
+#pragma unroll
+          for (int k = 0; k < TBK; ++k) v[k] = st[k * TBM + r];
+        }
+        uint4 hv[TBK / 8], lv[TBK / 8];
+#pragma unroll
+        for (int q = 0; q < TBK / 8; ++q) split8(v + 8 * q, sA, hv[q], lv[q]);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(&a32_empty[s]);
+        mbar_wait(&ahl_empty[s2], ph2 ^ 1u);
+#pragma unroll
+        for (int q = 0; q < TBK / 8; ++q) {
+          const int off = sw64_off(r, q);
+          *reinterpret_cast<uint4*>(ahi(s2) + off) = hv[q];
+          *reinterpret_cast<uint4*>(alo(s2) + off) = lv[q];
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(&ahl_full[s2]);
+      }
+    }
+  } else if (warp >= 8) {
+    // ---- epilogue: this CTA's 128 rows of the 256-row pair tile
+    const int q = warp - 8;                  // TMEM lane quarter (warp % 4)
+    float* wbuf = ebuf + q * (32 * 33);
+    const float inv_a = 1.0f / sA;
+    int64_t it = 0;
+    for (int64_t u = pair; u < w.units; u += npairs, ++it) {
+      int64_t tile, sp;
+      w.unit(u, tile, sp);
+      const int b = int(it & 1);
+#if LR_P_SLEEP
+      // a whole tile's main loop passes before the accumulator is ready:
+      // back off instead of spinning on the issue slots the converters use
+      {
+        const uint32_t par = uint32_t(it >> 1) & 1u;
+        uint32_t done = 0;
+        while (true) {
+          asm volatile(
+              "{\n\t.reg .pred p;\n\t"
+              "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+              "selp.u32 %0, 1, 0, p;\n}"
+              : "=r"(done)
+              : "r"(smem_u32(&acc_full[b])), "r"(par)
+              : "memory");
+          if (done) break;
+          __nanosleep(256);
+        }
+      }
+#else
+      mbar_wait_cluster(&acc_full[b], uint32_t(it >> 1) & 1u);
+#endif
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const int64_t mrow0 = tile * 2 * TBM + int64_t(rank) * TBM + q * 32;
+      float* cbase = C + sp * cstride;
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t d[32];
+        tmem_ld32(tmem + (uint32_t(q * 32) << 16) + uint32_t(b * 256 + c0), d);
+        if (c0 + 32 >= BN) {
+          // this warp's reads of buffer b are complete: hand it back
+          asm volatile("tcgen05.fence::before_thread_sync;");
+          if (lane == 0) {
+            if (rank == 0) mbar_arrive(&acc_empty[b]);
+            else           mbar_arrive_cluster(&acc_empty[b], 0);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) wbuf[lane * 33 + j] = __uint_as_float(d[j]);
+        __syncwarp();
+        const int col = c0 + lane;
+        const float sc = col < N ? inv_a / sB_dev[col] : 0.f;
+#if !(LR_TC_DBG & 4)
+        for (int rr = 0; rr < 32; ++rr) {
+          const int64_t row = mrow0 + rr;
+          if (row < M && col < N) cbase[row * ldc + col] = wbuf[rr * 33 + lane] * sc;
+        }
+#endif
+        __syncwarp();
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  cluster_sync();
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
   }
 }
 
@@ -491,6 +1067,182 @@ CUtensorMap make_map_3d(CUtensorMapDataType dt, const void* ptr, const uint64_t 
   return m;
 }
 
+// LR_TC_PAIR=0 keeps the single-CTA kernel (round 1) for every pass
+bool pair_enabled() {
+  const char* e = getenv("LR_TC_PAIR");
+  return !(e && e[0] == '0');
+}
+
+// units = 256-row tiles x split-K slices, spread round-robin over the
+// persistent pairs: pick the split count that fills the pairs' rounds best
+// (>= 97 % of the last round busy), preferring fewer slices
+int64_t pair_splits(int64_t mtiles, int64_t npairs, int64_t K) {
+  if (mtiles >= 4 * npairs) return 1;
+  const int64_t smax = std::max<int64_t>(1, std::min<int64_t>(K / (16 * TBK), 64));
+  int64_t best = 1;
+  double best_eff = 0.0;
+  for (int64_t sp = 1; sp <= smax; ++sp) {
+    const int64_t u = mtiles * sp;
+    const int64_t rounds = ceil_div(u, npairs);
+    const double eff = double(u) / double(rounds * npairs);
+    if (eff > best_eff + 1e-9) {
+      best_eff = eff;
+      best = sp;
+    }
+    if (eff >= 0.97 && rounds >= 2) return sp;
+  }
+  return best;
+}
+
+void gemm_f32_pair(Handle* h, bool transA, int64_t M, int64_t N, int64_t K, const float* A,
+                   int64_t lda, float sA, const float* sA_dev, const float* sB, const float* B,
+                   int64_t ldb, float* C, int64_t ldc) {
+  const int BN = int(ceil_div(N, 32) * 32);          // two halves of multiples of 16
+  const int64_t Kp = ceil_div(K, TBK) * TBK;
+  __half* Bhi = pool_alloc_t<__half>(h, size_t(BN) * Kp);
+  __half* Blo = pool_alloc_t<__half>(h, size_t(BN) * Kp);
+  if (BN != N) {
+    LR_CUDA(cudaMemsetAsync(Bhi, 0, sizeof(__half) * BN * Kp, h->stream));
+    LR_CUDA(cudaMemsetAsync(Blo, 0, sizeof(__half) * BN * Kp, h->stream));
+  }
+  {
+    dim3 grid(unsigned(ceil_div(Kp, 64)), unsigned(ceil_div(N, 32)));
+    split_transpose_kernel<<<grid, dim3(32, 8), 0, h->stream>>>(K, N, B, ldb, Kp, BN, sB, Bhi,
+                                                                 Blo);
+    LR_CHECK_LAUNCH();
+  }
+  CUtensorMap mapA = transA
+      ? make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, A, uint64_t(M), uint64_t(K), uint64_t(lda) * 4,
+                    TBM, TBK, CU_TENSOR_MAP_SWIZZLE_NONE)
+      : make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, A, uint64_t(K), uint64_t(M), uint64_t(lda) * 4,
+                    TBK, TBM, CU_TENSOR_MAP_SWIZZLE_128B);
+  const uint64_t brows = uint64_t(Kp / TBK) * BN;
+  CUtensorMap mapBh = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT16, Bhi, TBK, brows, TBK * 2, TBK,
+                                  uint32_t(BN / 2), CU_TENSOR_MAP_SWIZZLE_64B);
+  CUtensorMap mapBl = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT16, Blo, TBK, brows, TBK * 2, TBK,
+                                  uint32_t(BN / 2), CU_TENSOR_MAP_SWIZZLE_64B);
+  const size_t hb_slot = (size_t(2) * (BN / 2) * TBK * 2 + 1023) & ~size_t(1023);
+  const size_t smem = size_t(P_TS1) * A32_BYTES + size_t(P_TS2) * 2 * AH_BYTES +
+                      size_t(P_TS3) * hb_slot + 4 * 32 * 33 * sizeof(float) + 1024 /*align*/ +
+                      256 /*barriers*/;
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(P_THREADS, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = h->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  auto kern = transA ? gemm_f32_pair_kernel<true> : gemm_f32_pair_kernel<false>;
+  LR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  // a persistent grid must be co-resident: TPCs with a disabled SM cannot
+  // host a pair, so ask the occupancy API how many pairs fit at once
+  // (a grid of sm_count / 2 pairs would leave a few for a second wave)
+  static int resident[16] = {0};
+  const int dev = h->device >= 0 && h->device < 16 ? h->device : 0;
+  if (!resident[dev]) {
+    cfg.gridDim = dim3(unsigned(h->sm_count), 1, 1);
+    int nc = 0;
+    if (cudaOccupancyMaxActiveClusters(&nc, kern, &cfg) != cudaSuccess || nc < 1) {
+      cudaGetLastError();
+      nc = h->sm_count / 2;
+    }
+    resident[dev] = nc;
+    if (getenv("LR_TC_INFO"))
+      fprintf(stderr, "[lr] pair kernel: %d co-resident pairs (sm_count %d)\n", nc, h->sm_count);
+  }
+  const int64_t npairs_max = std::min<int64_t>(resident[dev], h->sm_count / 2);
+  const int64_t mtiles = ceil_div(M, 2 * TBM);
+  const int64_t splits0 = pair_splits(mtiles, npairs_max, K);
+  const int64_t kps = ceil_div(ceil_div(K, splits0), TBK) * TBK;
+  const int64_t splits = ceil_div(K, kps);
+  PairWork w{mtiles * splits, mtiles, kps, K};
+  const int64_t npairs = std::min<int64_t>(npairs_max, w.units);
+  float* out = C;
+  int64_t ldo = ldc, cstride = 0;
+  if (splits > 1) {
+    out = pool_alloc_t<float>(h, size_t(splits) * M * N);
+    ldo = N;
+    cstride = M * N;
+  }
+  cfg.gridDim = dim3(unsigned(2 * npairs), 1, 1);
+  LR_CUDA(cudaLaunchKernelEx(&cfg, kern, mapA, mapBh, mapBl, int(M), int(N), BN, w, sA, sA_dev,
+                             sB, out, ldo, cstride));
+  LR_CHECK_LAUNCH();
+  if (splits > 1) {
+    const int blocks = int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(M * N, 256), 8192)));
+    reduce_slices_f32<<<blocks, 256, 0, h->stream>>>(M, N, int(splits), out, C, ldc);
+    LR_CHECK_LAUNCH();
+  }
+}
+
+// LR_TC_M256=0 keeps the 128-row kernel for the deep-K passes
+bool m256_enabled() {
+  const char* e = getenv("LR_TC_M256");
+  return !(e && e[0] == '0');
+}
+
+int64_t wave_splits(int64_t mt, int sm_count, int64_t K) {
+  if (mt >= sm_count) return 1;
+  const int64_t smax = std::max<int64_t>(1, std::min<int64_t>(ceil_div(K, 8 * TBK), 64));
+  const int64_t smin = std::min<int64_t>(smax, ceil_div(sm_count, mt));
+  double best_eff = 0.0;
+  int64_t best = smin;
+  for (int64_t sp = smin; sp <= smax; ++sp) {
+    const int64_t ctas = mt * sp;
+    const double eff = double(ctas) / double(ceil_div(ctas, sm_count) * sm_count);
+    if (eff > best_eff + 1e-9) {
+      best_eff = eff;
+      best = sp;
+    }
+    if (eff >= 0.97) break;
+  }
+  return best;
+}
+
+void gemm_f32_m256(Handle* h, bool transA, int64_t M, int64_t N, int64_t K, const float* A,
+                   int64_t lda, float sA, const float* sA_dev, const float* sB, int BN,
+                   int64_t Kp, const __half* Bhi, const __half* Blo, float* C, int64_t ldc) {
+  CUtensorMap mapA = transA
+      ? make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, A, uint64_t(M), uint64_t(K), uint64_t(lda) * 4,
+                    WBM, TBK, CU_TENSOR_MAP_SWIZZLE_NONE)
+      : make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, A, uint64_t(K), uint64_t(M), uint64_t(lda) * 4,
+                    TBK, WBM, CU_TENSOR_MAP_SWIZZLE_128B);
+  const uint64_t brows = uint64_t(Kp / TBK) * BN;
+  CUtensorMap mapBh = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT16, Bhi, TBK, brows, TBK * 2, TBK,
+                                  uint32_t(BN), CU_TENSOR_MAP_SWIZZLE_64B);
+  CUtensorMap mapBl = make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT16, Blo, TBK, brows, TBK * 2, TBK,
+                                  uint32_t(BN), CU_TENSOR_MAP_SWIZZLE_64B);
+  const size_t b_slot = (size_t(2) * BN * TBK * 2 + 1023) & ~size_t(1023);
+  const size_t smem = size_t(W_TS1) * W_A32 + size_t(W_TS2) * 2 * W_AH + size_t(W_TS3) * b_slot +
+                      1024 /*align*/ + 256 /*barriers*/;
+  const int64_t mt = ceil_div(M, WBM);
+  const int64_t splits0 = wave_splits(mt, h->sm_count, K);
+  const int64_t kps = ceil_div(ceil_div(K, splits0), TBK) * TBK;
+  const int64_t splits = ceil_div(K, kps);
+  float* out = C;
+  int64_t ldo = ldc, cstride = 0;
+  if (splits > 1) {
+    out = pool_alloc_t<float>(h, size_t(splits) * M * N);
+    ldo = N;
+    cstride = M * N;
+  }
+  dim3 grid(unsigned(mt), 1, unsigned(splits));
+  auto kern = transA ? gemm_f32_m256_kernel<true> : gemm_f32_m256_kernel<false>;
+  LR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  kern<<<grid, W_THREADS, smem, h->stream>>>(mapA, mapBh, mapBl, int(M), int(N), BN, kps, K, sA,
+                                             sA_dev, sB, out, ldo, cstride);
+  LR_CHECK_LAUNCH();
+  if (splits > 1) {
+    const int blocks = int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(M * N, 256), 8192)));
+    reduce_slices_f32<<<blocks, 256, 0, h->stream>>>(M, N, int(splits), out, C, ldc);
+    LR_CHECK_LAUNCH();
+  }
+}
+
 bool gemm_f32_tc_supported(bool transA, int64_t N, const float* A, int64_t lda) {
   return N >= 1 && N <= 256 && (lda % 4) == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0;
 }
@@ -533,6 +1285,17 @@ void gemm_f32_tc(Handle* h, bool transA, int64_t M, int64_t N, int64_t K, const 
     col_scale_kernel<<<unsigned(ceil_div(N, 256)), 256, 0, h->stream>>>(N, cb, sB);
     LR_CHECK_LAUNCH();
   }
+  // the CTA-pair persistent kernel wins where the single-CTA kernel pays
+  // per-tile prologue / epilogue on short K (the m x 256 . 256 x 256 panel
+  // products: 1.1 vs 1.7 ms at config 4); on the deep-K passes over A its
+  // per-stage pair handshake measured ~1 us (7.0 vs 6.0 ms per A X pass),
+  // so those stay on the single-CTA kernel
+  const char* pe = getenv("LR_TC_PAIR");
+  const bool force_pair = pe && pe[0] == '1';
+  if (pair_enabled() && (h->sm_count % 2) == 0 && (force_pair || K <= 1024)) {
+    gemm_f32_pair(h, transA, M, N, K, A, lda, sA, sA_dev, sB, B, ldb, C, ldc);
+    return;
+  }
   const int BN = int(ceil_div(N, 16) * 16);
   const int64_t Kp = ceil_div(K, TBK) * TBK;
   __half* Bhi = pool_alloc_t<__half>(h, size_t(BN) * Kp);
@@ -546,6 +1309,10 @@ void gemm_f32_tc(Handle* h, bool transA, int64_t M, int64_t N, int64_t K, const 
     split_transpose_kernel<<<grid, dim3(32, 8), 0, h->stream>>>(K, N, B, ldb, Kp, BN, sB, Bhi,
                                                                  Blo);
     LR_CHECK_LAUNCH();
+  }
+  if (m256_enabled() && M >= 8 * 256) {
+    gemm_f32_m256(h, transA, M, N, K, A, lda, sA, sA_dev, sB, BN, Kp, Bhi, Blo, C, ldc);
+    return;
   }
   CUtensorMap mapA = transA
       ? make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, A, uint64_t(M), uint64_t(K), uint64_t(lda) * 4,
@@ -573,8 +1340,22 @@ void gemm_f32_tc(Handle* h, bool transA, int64_t M, int64_t N, int64_t K, const 
   const int64_t mt = ceil_div(M, TBM);
   int64_t splits = 1;
   if (mt < h->sm_count) {
-    splits = std::max<int64_t>(1, std::min<int64_t>(ceil_div(2 * h->sm_count, mt),
-                                                    ceil_div(K, 8 * TBK)));
+    // one CTA per SM: choose the split count so the CTAs fill whole waves
+    // (A^T Y at config 4: 32 tiles x 10 splits = 2.16 waves ran at 72 %)
+    const int64_t smax = std::max<int64_t>(1, std::min<int64_t>(ceil_div(K, 8 * TBK), 64));
+    const int64_t smin = std::min<int64_t>(smax, ceil_div(h->sm_count, mt));
+    double best_eff = 0.0;
+    splits = smin;
+    for (int64_t sp = smin; sp <= smax; ++sp) {
+      const int64_t ctas = mt * sp;
+      const int64_t waves = ceil_div(ctas, h->sm_count);
+      const double eff = double(ctas) / double(waves * h->sm_count);
+      if (eff > best_eff + 1e-9) {
+        best_eff = eff;
+        splits = sp;
+      }
+      if (eff >= 0.97) break;
+    }
   }
   const int64_t kps = ceil_div(ceil_div(K, splits), TBK) * TBK;
   splits = ceil_div(K, kps);

@@ -314,6 +314,62 @@ void cast_copy(Handle* h, int sd, const void* src, int64_t lds, int dd, void* ds
   throw Error{LR_EINVAL, "cast_copy: unsupported dtype pair"};
 }
 
+// Z (rows x cols) += T, fp64 / complex128 (row-block accumulation of the
+// one-pass sketch, reference io.py:381 "Yt += block* Omega_t[rows]")
+template <typename T>
+__global__ void axpy_add_kernel(int64_t rows, int64_t cols, const T* __restrict__ Tm, int64_t ldt,
+                                T* __restrict__ Z, int64_t ldz) {
+  using S = Sc<T>;
+  const int64_t total = rows * cols;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e / cols, j = e % cols;
+    Z[i * ldz + j] = S::add(Z[i * ldz + j], Tm[i * ldt + j]);
+  }
+}
+
+// C_ij <- C_ij / (d2_i + d1_j) (zero where the denominator is not positive
+// beyond roundoff): the diagonalized Sylvester normal equations of the
+// one-pass least-squares problem (see factor.svd_one_pass_general)
+template <typename T>
+__global__ void sylvester_div_kernel(int64_t k, int64_t kt, T* __restrict__ C, int64_t ldc,
+                                     const double* __restrict__ d2, const double* __restrict__ d1,
+                                     double floor) {
+  using S = Sc<T>;
+  const int64_t total = k * kt;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = e / kt, j = e % kt;
+    const double den = d2[i] + d1[j];
+    C[i * ldc + j] = den > floor ? S::scale(C[i * ldc + j], 1.0 / den) : S::zero();
+  }
+}
+
+void axpy_add(Handle* h, int dtype, int64_t rows, int64_t cols, const void* Tm, int64_t ldt,
+              void* Z, int64_t ldz) {
+  if (rows == 0 || cols == 0) return;
+  const int blocks = int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(rows * cols, 256),
+                                                                int64_t(h->sm_count) * 16)));
+  switch (dtype) {
+    case LR_F64: axpy_add_kernel<double><<<blocks, 256, 0, h->stream>>>(rows, cols, static_cast<const double*>(Tm), ldt, static_cast<double*>(Z), ldz); break;
+    case LR_C128: axpy_add_kernel<double2><<<blocks, 256, 0, h->stream>>>(rows, cols, static_cast<const double2*>(Tm), ldt, static_cast<double2*>(Z), ldz); break;
+    default: throw Error{LR_EINVAL, "axpy_add: fp64 / complex128 only"};
+  }
+  LR_CHECK_LAUNCH();
+}
+
+void sylvester_div(Handle* h, int dtype, int64_t k, int64_t kt, void* C, int64_t ldc,
+                   const double* d2, const double* d1, double floor) {
+  if (k == 0 || kt == 0) return;
+  const int blocks = int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(k * kt, 256), 1024)));
+  switch (dtype) {
+    case LR_F64: sylvester_div_kernel<double><<<blocks, 256, 0, h->stream>>>(k, kt, static_cast<double*>(C), ldc, d2, d1, floor); break;
+    case LR_C128: sylvester_div_kernel<double2><<<blocks, 256, 0, h->stream>>>(k, kt, static_cast<double2*>(C), ldc, d2, d1, floor); break;
+    default: throw Error{LR_EINVAL, "sylvester_div: fp64 / complex128 only"};
+  }
+  LR_CHECK_LAUNCH();
+}
+
 void axpy_sub(Handle* h, int dtype, int64_t rows, int64_t cols, const void* Tm, int64_t ldt,
               void* Z, int64_t ldz) {
   if (rows == 0 || cols == 0) return;

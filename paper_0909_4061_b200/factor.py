@@ -8,8 +8,9 @@ direct_svd + posterior estimate with seed + 13, cli.py:222-262) as
 ``randomized_svd``, which keeps every intermediate in HBM and only copies
 the final factors back.  ``direct_eig_hermitian`` (factor.py:168-191) and
 ``eig_nystrom`` (factor.py:300-335) reuse the passes, the Cholesky kernel in
-its PSD mode and the small SVD.  ID / row extraction and
-the one-pass sketches are outside this build's scope.
+its PSD mode and the small SVD.  Sample bundles and the
+one-pass factorizations (factor.py:95-147,338-401) solve their small
+problems on the device; io.py accumulates the same bundles from row blocks.
 """
 
 from __future__ import annotations
@@ -21,8 +22,8 @@ import numpy as np
 from . import config
 from . import _lib
 from .core import (_out, _outs, _torch, _wide, apply_dev, as_operator, cast_dev, gemm, gemm_dev,
-                   is_device_array, small_eig_hermitian_dev, small_svd_from_adjoint, speculate,
-                   to_device)
+                   is_device_array, small_eig_hermitian_dev, small_svd_dev,
+                   small_svd_from_adjoint, speculate, to_device)
 from .rangefinder import (RangeBasis, SketchSpec, _cast_like_op, _check_ell, _host_io,
                           _sketch_dev, orth_dev, posterior_error_estimate_dev, probes_dev,
                           subspace_iteration_range_dev)
@@ -234,6 +235,184 @@ def eig_nystrom(A, Q, psd_tol=config.PSD_TOL):
     lam = S * S
     f = PartialEig(U=_out(UF, host), lam=_out(lam, host), diagnostics=diagnostics)
     return f, NystromFactors(F=_out(F, host))
+
+
+# ---------------------------------------------------------------------------
+# sample bundles and the one-pass factorizations (reference factor.py:95-147,
+# 338-401; io.py:364-430 accumulates the same bundles from row blocks)
+
+@dataclass
+class SampleBundle:
+    """Everything Stage A knows: test matrices, samples and bases
+    (reference factor.py:95-113).  Two-sided bundles add Omega_tilde,
+    Y_tilde = A* Omega_tilde and Q_tilde; q_choice records whether Q came
+    from Gram-Schmidt on Y ("gs") or the leading left singular vectors
+    ("svd")."""
+
+    Omega: object
+    Y: object
+    Q: object
+    Omega_tilde: object = None
+    Y_tilde: object = None
+    Q_tilde: object = None
+    q_choice: str = "gs"
+    seed: int = None
+
+
+def _basis_from_samples_dev(Y, rank=None, ortho_tol=config.GS_DROP_TOL):
+    """factor.py:116-120 on the device: DGS of Y, or the `rank` leading left
+    singular vectors of Y (the oversampled one-pass variant)."""
+    from .core import small_svd_dev
+    if rank is None:
+        return orth_dev(Y, ortho_tol), "gs"
+    U, _, _ = small_svd_dev(Y)
+    return U[:, :rank].contiguous(), "svd"
+
+
+def sample_bundle(A, ell, seed, rank=None):
+    """One-sided bundle (Omega, Y = A Omega, Q) in a single pass
+    (factor.py:123-133)."""
+    op = as_operator(A)
+    host = _host_io(A, op)
+    Omega = gaussian_dev_like(op, op.n, ell, seed)
+    Y = apply_dev(op, _cast_like_op(op, Omega))
+    Q, choice = _basis_from_samples_dev(Y, rank)
+    Omega, Y, Q = _outs(host, Omega, Y, Q)
+    return SampleBundle(Omega=Omega, Y=Y, Q=Q, q_choice=choice, seed=seed)
+
+
+def gaussian_dev_like(op, rows, cols, seed):
+    """gaussian_matrix(rows, cols, seed) on the device (float64, as the
+    reference draws it; cast to the operator's precision where applied)."""
+    from .sketch import gaussian_dev
+    del op
+    return gaussian_dev(rows, cols, seed)
+
+
+def sample_bundle_two_sided(A, ell, ell_tilde=None, seed=0, rank=None):
+    """Sketches of A and A* (two passes here; io.accumulate_two_sided_samples
+    is the one-traversal form) and both bases (factor.py:136-147)."""
+    op = as_operator(A)
+    host = _host_io(A, op)
+    if ell_tilde is None:
+        ell_tilde = ell
+    Omega = gaussian_dev_like(op, op.n, ell, seed)
+    Omega_t = gaussian_dev_like(op, op.m, ell_tilde, seed + 1)
+    Y = apply_dev(op, _cast_like_op(op, Omega))
+    Yt = apply_dev(op, _cast_like_op(op, Omega_t), adjoint=True)
+    Q, choice = _basis_from_samples_dev(Y, rank)
+    Qt, _ = _basis_from_samples_dev(Yt, rank)
+    Omega, Y, Q, Omega_t, Yt, Qt = _outs(host, Omega, Y, Q, Omega_t, Yt, Qt)
+    return SampleBundle(Omega=Omega, Y=Y, Q=Q, Omega_tilde=Omega_t, Y_tilde=Yt, Q_tilde=Qt,
+                        q_choice=choice, seed=seed)
+
+
+def _dev_wide(*arrs):
+    """Device copies in the common wide dtype (float64 / complex128)."""
+    torch = _torch()
+    cplx = any((a.is_complex() if torch.is_tensor(a) else np.iscomplexobj(a)) for a in arrs)
+    wd = torch.complex128 if cplx else torch.float64
+    return [cast_dev(to_device(a), wd).contiguous() for a in arrs], wd
+
+
+def _mm(A, B, ha=False):
+    """A @ B (or A^H @ B) for small device matrices (lr_gemm)."""
+    torch = _torch()
+    rows = A.shape[1] if ha else A.shape[0]
+    out = torch.empty((rows, B.shape[1]), dtype=A.dtype, device=A.device)
+    gemm(A, B, out, adjoint=ha)
+    return out
+
+
+def _ct(A):
+    """Conjugate transpose of a small device matrix (lr_copy)."""
+    torch = _torch()
+    out = torch.empty((A.shape[1], A.shape[0]), dtype=A.dtype, device=A.device)
+    _lib.call("lr_copy", _lib.handle(A.device.index), _lib.dtype_code(A.dtype), _lib.ptr(A),
+              _lib.ld(A), _lib.dtype_code(A.dtype), _lib.ptr(out), _lib.ld(out), A.shape[1],
+              A.shape[0], 1)
+    return out
+
+
+def svd_one_pass_general(bundle):
+    """General one-pass SVD from a two-sided bundle (factor.py:364-401).
+
+    B (k x k~) minimizes ||B (Q~* Omega) - Q* Y||^2 + ||B* (Q* Omega~) -
+    Q~* Y~||^2; the reference solves the dense least-squares problem over
+    vec(B).  Its normal equations are the Sylvester equation
+        B (P P*) + (S S*) B = N1 P* + S N2*,
+    P = Q~* Omega, S = Q* Omega~, N1 = Q* Y, N2 = Q~* Y~, which the two
+    Hermitian eigendecompositions P P* = V1 D1 V1*, S S* = V2 D2 V2* reduce to
+    an entrywise division (lr_sylvester_div): the same minimizer for a
+    full-rank problem, in O(k^3) on the device instead of O((k k~)^3).
+    Then the small SVD of B and U = Q U_B, V = Q~ V_B."""
+    torch = _torch()
+    if bundle.Omega_tilde is None or bundle.Y_tilde is None or bundle.Q_tilde is None:
+        raise ValueError("two-sided bundle required")
+    host = not is_device_array(bundle.Q)
+    k, kt = bundle.Q.shape[1], bundle.Q_tilde.shape[1]
+    if k * kt > config.ONE_PASS_DIM_CAP:
+        raise ValueError(f"reduced problem has {k * kt} unknowns, above the cap "
+                         f"{config.ONE_PASS_DIM_CAP}; use the two-pass path")
+    (Q, Qt, Om, Y, Omt, Yt), wd = _dev_wide(bundle.Q, bundle.Q_tilde, bundle.Omega, bundle.Y,
+                                            bundle.Omega_tilde, bundle.Y_tilde)
+    if k == 0 or kt == 0:
+        outs = (torch.zeros((Q.shape[0], 0), dtype=wd, device=Q.device),
+                torch.zeros(0, dtype=torch.float64, device=Q.device),
+                torch.zeros((Qt.shape[0], 0), dtype=wd, device=Q.device))
+        return PartialSVD(*_outs(host, *outs))
+    P = _mm(Qt, Om, ha=True)                 # kt x ell
+    N1 = _mm(Q, Y, ha=True)                  # k x ell
+    S = _mm(Q, Omt, ha=True)                 # k x ell~
+    N2 = _mm(Qt, Yt, ha=True)                # kt x ell~
+    X1 = _mm(P, _ct(P))                      # kt x kt  P P*
+    X2 = _mm(S, _ct(S))                      # k x k    S S*
+    C = _mm(N1, _ct(P))
+    C2 = _mm(S, _ct(N2))
+    _lib.call("lr_axpy_add", _lib.handle(Q.device.index), _lib.dtype_code(wd), k, kt,
+              _lib.ptr(C2), _lib.ld(C2), _lib.ptr(C), _lib.ld(C))     # N1 P* + S N2*
+    V1, d1 = small_eig_hermitian_dev(X1)
+    V2, d2 = small_eig_hermitian_dev(X2)
+    Ct = _mm(V2, _mm(C, V1), ha=True)        # V2* C V1
+    scale = float(max(d1.abs().max().item(), d2.abs().max().item()))
+    _lib.call("lr_sylvester_div", _lib.handle(Q.device.index), _lib.dtype_code(wd), k, kt,
+              _lib.ptr(Ct), _lib.ld(Ct), _lib.ptr(d2.contiguous()), _lib.ptr(d1.contiguous()),
+              float(1e-14 * scale))
+    B = _mm(V2, _mm(Ct, _ct(V1)))            # V2 B~ V1*
+    Ub, Sb, Vb = small_svd_dev(B)
+    U = _mm(Q, Ub)
+    V = _mm(Qt, Vb)
+    return PartialSVD(*_outs(host, U, Sb, V))
+
+
+def eig_one_pass(bundle):
+    """Hermitian eigendecomposition from the sketch alone (factor.py:338-361):
+    B (Q* Omega) ~= Q* Y in least squares (the reference's pivoted-QR
+    solve; here B = N M^+ through the small SVD of M = Q* Omega, truncating
+    singular values below 1e-12 of the largest like its triangular solve),
+    symmetrized, eigenpairs of B, U = Q V.  Diagnostics: q_choice, tau_min =
+    smallest singular value of M, ill_conditioned past ONE_PASS_COND_WARN."""
+    from .core import small_svd_dev
+    host = not is_device_array(bundle.Q)
+    (Q, Om, Y), wd = _dev_wide(bundle.Q, bundle.Omega, bundle.Y)
+    M = _mm(Q, Om, ha=True)                  # k x ell
+    N = _mm(Q, Y, ha=True)                   # k x ell
+    Um, sm, Vm = small_svd_dev(M)            # M = Um diag(sm) Vm*
+    sv = sm.cpu().numpy()
+    inv = np.where(sv > 1e-12 * (sv.max() if sv.size else 0.0), 1.0 / np.where(sv > 0, sv, 1.0),
+                   0.0)
+    W = _mm(N, Vm)                           # k x r
+    D = to_device(np.diag(inv).astype(np.complex128 if wd == _torch().complex128 else np.float64),
+                  wd, Q.device.index)
+    B = _mm(_mm(W, D), _ct(Um))              # N M^+ (symmetrized by the eigensolver)
+    diagnostics = {"q_choice": bundle.q_choice}
+    tau_min = float(sv.min()) if sv.size else 0.0
+    diagnostics["tau_min"] = tau_min
+    if sv.size and (tau_min == 0.0 or sv.max() / max(tau_min, 1e-300) > config.ONE_PASS_COND_WARN):
+        diagnostics["ill_conditioned"] = True
+    V, lam = small_eig_hermitian_dev(B)
+    U = _mm(Q, V)
+    return PartialEig(U=_out(U, host), lam=_out(lam, host), diagnostics=diagnostics)
 
 
 def truncate_rank(f, k):

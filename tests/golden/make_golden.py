@@ -246,7 +246,53 @@ def g_stageb():
     save("stageb", **out)
 
 
-ALL = {"kats": g_kats, "stageb": g_stageb, "cfg1": g_cfg1, "cfg3": g_cfg3, "cfg4s": g_cfg4s, "cfg5s": g_cfg5s,
+def g_onepass():
+    """One-pass sketches (reference factor.py:123-147,338-401) and the
+    LRKMAT00 / row-block streaming path (io.py:178-204,319-430)."""
+    import tempfile
+    from lowrank import io as rio
+    from lowrank.oracle import synthetic_psd
+    out = {}
+    A, _ = synthetic_matrix(SyntheticSpec(m=40, n=30, kind="exact_rank", param=5, seed=20))
+    b = factor.sample_bundle_two_sided(A, 15, seed=6)
+    f = factor.svd_one_pass_general(b)
+    out.update(gen_A=A, gen_Q=b.Q, gen_Qt=b.Q_tilde, gen_Y=b.Y, gen_Yt=b.Y_tilde,
+               gen_sigma=f.sigma, gen_comp=f.compose())
+    rng = np.random.default_rng(23)
+    A2 = (rng.standard_normal((120, 12)) * np.exp(-np.arange(12) / 3.0)) @ rng.standard_normal((12, 90))
+    A2 += 1e-3 * rng.standard_normal((120, 90))
+    b = factor.sample_bundle_two_sided(A2, 20, ell_tilde=24, seed=9)
+    f = factor.svd_one_pass_general(b)
+    out.update(gen2_A=A2, gen2_sigma=f.sigma, gen2_comp=f.compose(), gen2_Q=b.Q, gen2_Qt=b.Q_tilde)
+    b = factor.sample_bundle_two_sided(A2, 20, ell_tilde=24, seed=9, rank=10)
+    f = factor.svd_one_pass_general(b)
+    out.update(gen2r_sigma=f.sigma, gen2r_comp=f.compose())
+    H, _ = synthetic_psd(40, "exact_rank", 6, seed=19)
+    b = factor.sample_bundle(core.DenseOperator(H), 16, seed=5)
+    f = factor.eig_one_pass(b)
+    out.update(herm_H=H, herm_Q=b.Q, herm_lam=f.lam, herm_comp=f.compose(),
+               herm_tau=np.array([f.diagnostics["tau_min"]]))
+    H2, _ = synthetic_psd(40, "exp_decay", 0.9, seed=4)
+    b = factor.sample_bundle(core.DenseOperator(H2), 20, seed=5, rank=10)
+    f = factor.eig_one_pass(b)
+    out.update(herm2_H=H2, herm2_lam=f.lam, herm2_tau=np.array([f.diagnostics["tau_min"]]),
+               herm2_comp=f.compose())
+    # streamed bundle of a stored matrix (block_rows 8), complex too
+    rng = np.random.default_rng(10)
+    S = rng.standard_normal((64, 32))
+    Sc = rng.standard_normal((33, 20)) + 1j * rng.standard_normal((33, 20))
+    with tempfile.TemporaryDirectory() as d:
+        for tag, M, br, ell in (("st", S, 8, 6), ("stc", Sc, 5, 4)):
+            pth = os.path.join(d, f"{tag}.bin")
+            rio.write_matrix_binary(M, pth)
+            sb = rio.streamed_sample_bundle(rio.stream_row_blocks(pth, br), ell=ell, seed=4)
+            out.update({f"{tag}_A": M, f"{tag}_Y": sb.Y, f"{tag}_Yt": sb.Y_tilde, f"{tag}_Q": sb.Q,
+                        f"{tag}_Qt": sb.Q_tilde, f"{tag}_Om": sb.Omega, f"{tag}_Omt": sb.Omega_tilde,
+                        f"{tag}_bytes": np.frombuffer(open(pth, "rb").read()[:64], dtype=np.uint8)})
+    save("onepass", **out)
+
+
+ALL = {"onepass": g_onepass, "kats": g_kats, "stageb": g_stageb, "cfg1": g_cfg1, "cfg3": g_cfg3, "cfg4s": g_cfg4s, "cfg5s": g_cfg5s,
        "cfg2": g_cfg2}
 
 if __name__ == "__main__":

@@ -160,3 +160,33 @@ def test_stageb_hermitian_routes(golden):
     with pytest.raises(ValueError):
         O.direct_eig_hermitian(np.random.default_rng(13).standard_normal((10, 10)),
                                np.eye(10)[:, :3])
+
+
+def test_oracle_one_pass_and_streaming(golden, tmp_path):
+    """The oracle's one-pass factorizations and row-block streaming against
+    the reference's own outputs (tests/golden/onepass.npz)."""
+    g = golden("onepass")
+    b = O.sample_bundle_two_sided(g["gen_A"], 15, seed=6)
+    f = O.svd_one_pass_general(b)
+    assert np.abs(f.sigma - g["gen_sigma"]).max() <= 1e-10 * g["gen_sigma"][0]
+    assert np.abs(f.U * f.sigma @ f.V.conj().T - g["gen_comp"]).max() <= 1e-9
+    b = O.sample_bundle_two_sided(g["gen2_A"], 20, ell_tilde=24, seed=9)
+    f = O.svd_one_pass_general(b)
+    assert np.abs(f.sigma - g["gen2_sigma"]).max() <= 1e-10 * g["gen2_sigma"][0]
+    b = O.sample_bundle_two_sided(g["gen2_A"], 20, ell_tilde=24, seed=9, rank=10)
+    f = O.svd_one_pass_general(b)
+    assert np.abs(f.sigma - g["gen2r_sigma"]).max() <= 1e-10 * g["gen2r_sigma"][0]
+    for tag, rank in (("herm", None), ("herm2", 10)):
+        H = g[f"{tag}_H"]
+        b = O.sample_bundle(H, 16 if tag == "herm" else 20, seed=5, rank=rank)
+        e = O.eig_one_pass(b)
+        assert np.abs(e.lam - g[f"{tag}_lam"]).max() <= 1e-9 * np.abs(g[f"{tag}_lam"]).max()
+        assert e.diagnostics["tau_min"] == pytest.approx(g[f"{tag}_tau"][0], rel=1e-9)
+    for tag, br, ell in (("st", 8, 6), ("stc", 5, 4)):
+        p = tmp_path / f"{tag}.bin"
+        O.write_matrix_binary(g[f"{tag}_A"], p)
+        assert np.array_equal(np.frombuffer(p.read_bytes()[:64], dtype=np.uint8), g[f"{tag}_bytes"])
+        sb = O.streamed_sample_bundle(str(p), br, ell, seed=4)
+        assert np.array_equal(sb.Omega, g[f"{tag}_Om"])
+        assert np.array_equal(sb.Y, g[f"{tag}_Y"]) and np.array_equal(sb.Y_tilde, g[f"{tag}_Yt"])
+        assert np.abs(sb.Q - g[f"{tag}_Q"]).max() <= 1e-13
