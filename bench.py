@@ -501,12 +501,21 @@ def run_sharded(args, cfg):
     else:
         dist.init_process_group("nccl", init_method="tcp://127.0.0.1:29533", rank=0,
                                 world_size=1, device_id=torch.device("cuda", local))
-    A_full = build_input(cfg)
-    r0, r1 = row_range(A_full.shape[0], rank, world)
-    A = A_full[r0:r1].contiguous()
-    m_total, n = A_full.shape
-    a_bytes_total = A_full.numel() * A_full.element_size()
-    del A_full
+    if cfg.idx == 5:
+        return run_sharded_sparse(args, cfg, rank, world, local)
+    if cfg.idx == 4:
+        # each rank builds only its rows (the recipe is blockwise)
+        r0, r1 = row_range(cfg.m, rank, world)
+        A, _ = workloads.build_cfg4_device(rows=(r0, r1))
+        m_total, n = cfg.m, cfg.n
+        a_bytes_total = cfg.a_bytes()
+    else:
+        A_full = build_input(cfg)
+        r0, r1 = row_range(A_full.shape[0], rank, world)
+        A = A_full[r0:r1].contiguous()
+        m_total, n = A_full.shape
+        a_bytes_total = A_full.numel() * A_full.element_size()
+        del A_full
     torch.cuda.empty_cache()
     comm, be = Comm(), GpuBackend()
     op = lr.DenseOperator(A)
@@ -596,6 +605,68 @@ def run_sharded(args, cfg):
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
 
+
+
+def run_sharded_sparse(args, cfg, rank, world, local):
+    """Config 5 on N GPUs: rank r holds rows row_range(2^21, r, N) of S and L
+    (R replicated) as a CudaCsrOperator; the n-side panels are sharded too
+    (all-gather before A_r X, reduce-scatter after A_r^H Y --
+    dist_randomized_svd_operator).  Strong scaling."""
+    import torch
+    import torch.distributed as dist
+    import paper_0909_4061_b200 as lr
+    from paper_0909_4061_b200 import core as lrcore
+    from paper_0909_4061_b200.dist import Comm, GpuBackend, dist_randomized_svd_operator, row_range
+    S, L, R = workloads.build_cfg5()
+    n = S.shape[0]
+    a, b = row_range(n, rank, world)
+    op = lr.CudaCsrOperator(S[a:b], L[a:b], R)
+    nnz_total = int(S.nnz)
+    del S
+    comm, be = Comm(), GpuBackend()
+    passes = cfg.passes()
+    a_bytes = cfg.a_bytes(nnz_total)
+
+    def step(estimate=False):
+        return dist_randomized_svd_operator(op, n, cfg.k, cfg.p, cfg.q, cfg.seed, comm, be,
+                                            estimate=estimate)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    lrcore.PASS_EVENTS = []
+    l0 = lr._lib.launch_count()
+    with ClockSampler(local) as clk:
+        dist.barrier()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(args.steps):
+            step()
+        e.record()
+        torch.cuda.synchronize()
+        dist.barrier()
+    launches = lr._lib.launch_count() - l0
+    t = torch.tensor([s.elapsed_time(e) / args.steps], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    pev = lrcore.PASS_EVENTS
+    lrcore.PASS_EVENTS = None
+    line = {
+        "metric": "rank-k rSVD time & A-GB/s (% roofline) at 1/2/4/8 B200 vs host-CPU ref",
+        "value": round(passes * a_bytes / (ms / 1e3) / 1e9, 3), "unit": "A-GB/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded CSR + Gaussian low-rank factors, BASELINE.json config 5)",
+        "config": config_dict(cfg, world),
+        "rows_per_rank": b - a,
+        "roofline": roofline_sparse(cfg, pev, ms, args.steps, passes),
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
 
 
 def e2e_measure(args, cfg, A, lr):

@@ -94,6 +94,15 @@ int lr_gemm_scaled(lr_handle_t h, int dtype, int op, int64_t m, int64_t n, int64
                    const void* A, int64_t lda, double a_amax, const void* X, int64_t ldx,
                    void* Y, int64_t ldy);
 
+/* A pass over an fp32 A with exact products and fp64 accumulation (DMMA on
+ * fp32 operands widened at fragment load): Y (fp64) = A X (op N) or A^T X
+ * (op T), X fp32.  The posterior estimator's narrow pass (reference
+ * posterior_error_estimate, rangefinder.py:65-82, r = 10 probes) uses it for
+ * fp32 operators: the residual it measures is ~1e-5 of |A w| at config 4,
+ * below the tensor-core split's rounding. */
+int lr_gemm_f64acc(lr_handle_t h, int op, int64_t m, int64_t n, int64_t ell, const float* A,
+                   int64_t lda, const float* X, int64_t ldx, double* Y, int64_t ldy);
+
 /* fp64 passes on the int8 tensor cores (Ozaki digit slicing, exact int32
  * products; accuracy of an fp64 GEMM, bitwise deterministic).  Replaces the
  * same reference call as lr_gemm (DenseOperator._apply / _apply_adjoint,
@@ -212,6 +221,12 @@ int lr_orth(lr_handle_t h, int dtype, int64_t m, int64_t ell, const void* Y, int
  * Q must not alias Y. */
 int lr_orth_fast(lr_handle_t h, int dtype, int64_t m, int64_t ell, const void* Y, int64_t ldy,
                  void* Q, int64_t ldq, double tol, int32_t* status);
+/* lr_orth_fast without its last product: Q1 (m x ell, ld ell, dtype) and P2
+ * (ell x ell, float64 / complex128) with Q = Q1 P2.  For a subspace step
+ * whose next product is A^H Q the caller forms (A^H Q1) P2 on the n side.
+ * Same speculative flags as lr_orth_fast in *status. */
+int lr_orth_fast_deferred(lr_handle_t h, int dtype, int64_t m, int64_t ell, const void* Y,
+                          int64_t ldy, void* Q1, void* P2, double tol, int32_t* status);
 
 /* Speculative variant of lr_small_svd (no host sync; Bh is not modified);
  * flags as lr_orth_fast plus 8 = Jacobi sweep limit reached. */
@@ -313,6 +328,28 @@ int lr_max_abs_imag(lr_handle_t h, int dtype, int64_t m, int64_t n, const void* 
  * exceeded 63 draws, 32 = internal stream margin too short.  Async. */
 int lr_gaussian(lr_handle_t h, uint64_t key_lo, uint64_t key_hi, int64_t count, int dtype,
                 void* out, int32_t* status);
+
+/* Collectives for the row-sharded path without torch.distributed (SURVEY.md
+ * §8b/§8e; reference analogue: the row-block sums of
+ * accumulate_two_sided_samples, io.py:364-388, turned into all-reduces).
+ * Rank r holds rows of A; the passes A_r X are local (lr_gemm), A^H Y is the
+ * sum of the ranks' n x ell partials (lr_comm_allreduce), and a row-sharded
+ * m x ell panel is orthonormalized by lr_orth_sharded: CholeskyQR2 with both
+ * Grams all-reduced, every rank computing the same factors.  NCCL is loaded
+ * at run time (libnccl.so.2).
+ *   lr_comm_unique_id: LR_COMM_ID_BYTES bytes on rank 0, shared by the caller;
+ *   lr_comm_init:      attach a communicator of nranks to the handle;
+ *   lr_comm_allreduce: in-place sum of count float64 / complex128 elements
+ *                      on the handle's stream;
+ *   lr_orth_sharded:   the speculative orthonormalization (flags as
+ *                      lr_orth_fast, identical on every rank). */
+#define LR_COMM_ID_BYTES 128
+int lr_comm_unique_id(void* id_out);
+int lr_comm_init(lr_handle_t h, const void* id, int nranks, int rank);
+int lr_comm_destroy(lr_handle_t h);
+int lr_comm_allreduce(lr_handle_t h, int dtype, int64_t count, void* buf);
+int lr_orth_sharded(lr_handle_t h, int dtype, int64_t m_local, int64_t ell, const void* Y,
+                    int64_t ldy, void* Q, int64_t ldq, double tol, int32_t* status);
 
 /* One-pass sketches (reference io.py:364-388 accumulate_two_sided_samples,
  * factor.py:364-401 svd_one_pass_general):

@@ -19,15 +19,17 @@ from .core import (CudaDenseOperator, DenseOperator, MatVecOperator, OperatorCou
                    as_operator, orthonormalize_double_gs, small_eig_hermitian, small_svd)
 from .factor import (NystromFactors, PartialEig, PartialSVD, SampleBundle, direct_eig_hermitian,
                      direct_svd, eig_nystrom, eig_one_pass, randomized_svd, sample_bundle,
-                     sample_bundle_two_sided, svd_one_pass_general, truncate_rank)
+                     sample_bundle_two_sided, stage_a, svd_one_pass_general, svd_single_pass,
+                     truncate_rank)
 from .io import (MatrixFormatError, RowBlockStream, StreamError, accumulate_two_sided_samples,
                  in_memory_sample_bundle, read_matrix_binary, stream_row_blocks,
                  streamed_sample_bundle, write_matrix_binary)
 from .rangefinder import (RangeBasis, adaptive_range_finder, adaptive_range_finder_blocked,
                           fast_range_finder, posterior_error_estimate, power_iteration_range,
                           randomized_range_finder, subspace_iteration_range)
-from .sketch import (GsrftOperator, SketchSpec, SrftOperator, dft, gaussian_matrix, gsrft_apply,
-                     gsrft_operator, rng_for, srft_apply, srft_operator)
+from .sketch import (GsrftOperator, SketchSpec, SrftOperator, dense_sketch_matrix, dft,
+                     gaussian_matrix, gsrft_apply, gsrft_operator, op_count, reset_op_count,
+                     rng_for, sketch_apply, srft_apply, srft_operator)
 from .sparse import CudaCsrOperator
 
 __version__ = "0.1.0"

@@ -48,6 +48,7 @@ _SIGS = {
     "lr_set_f32_mode": [_vp, _int],
     "lr_reserve": [_vp, _i64],
     "lr_gemm": [_vp, _int, _int, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64],
+    "lr_gemm_f64acc": [_vp, _int, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64],
     "lr_gemm_scaled": [_vp, _int, _int, _i64, _i64, _i64, _vp, _i64, C.c_double, _vp, _i64, _vp,
                        _i64],
     "lr_gram": [_vp, _int, _i64, _i64, _vp, _i64, _vp],
@@ -64,6 +65,7 @@ _SIGS = {
     "lr_orth": [_vp, _int, _i64, _i64, _vp, _i64, _vp, _i64, C.c_double, C.POINTER(_i64)],
     "lr_small_svd": [_vp, _int, _i64, _i64, _vp, _vp, _vp, _vp],
     "lr_orth_fast": [_vp, _int, _i64, _i64, _vp, _i64, _vp, _i64, C.c_double, _vp],
+    "lr_orth_fast_deferred": [_vp, _int, _i64, _i64, _vp, _i64, _vp, _vp, C.c_double, _vp],
     "lr_small_svd_fast": [_vp, _int, _i64, _i64, _vp, _vp, _vp, _vp, _vp],
     "lr_jacobi_svd": [_vp, _int, _i64, _vp, _vp, _vp, _vp, _vp],
     "lr_estimate_tail": [_vp, _int, _i64, _i64, _i64, _vp, _i64, _vp, _i64, C.c_double, _vp],
@@ -83,6 +85,11 @@ _SIGS = {
     "lr_axpy_add": [_vp, _int, _i64, _i64, _vp, _i64, _vp, _i64],
     "lr_sylvester_div": [_vp, _int, _i64, _i64, _vp, _i64, _vp, _vp, C.c_double],
     "lr_col_sumsq": [_vp, _int, _i64, _i64, _vp, _i64, _vp],
+    "lr_comm_unique_id": [_vp],
+    "lr_comm_init": [_vp, _vp, _int, _int],
+    "lr_comm_destroy": [_vp],
+    "lr_comm_allreduce": [_vp, _int, _i64, _vp],
+    "lr_orth_sharded": [_vp, _int, _i64, _i64, _vp, _i64, _vp, _i64, C.c_double, _vp],
     "lr_scale_col": [_vp, _int, _i64, _vp, _i64, C.c_double, _vp, _i64],
 }
 

@@ -87,6 +87,12 @@ def to_device(x, dtype=None, device=None):
     return t
 
 
+def _cast_like_dtype(t, dtype):
+    """A real draw in the compute dtype of `dtype` (complex operators take
+    complex copies; float32 / float64 / complex* kept)."""
+    return cast_dev(t, dtype) if t.dtype != dtype else t
+
+
 def cast_dev(t, dtype):
     """Device dtype conversion with the library's cast kernel (real ->
     complex zero-fills the imaginary part)."""
@@ -415,6 +421,24 @@ class DenseOperator(MatVecOperator):
         return _out(Z, host)
 
 
+    def apply_wide(self, X):
+        """A X for a float32 A with exact products and fp64 accumulation
+        (lr_gemm_f64acc, DMMA): one counted pass, fp64 device result.  The
+        posterior estimator's narrow pass uses it -- the residual it measures
+        sits below the tensor-core split's rounding."""
+        torch = _torch()
+        A = self.array
+        self._refresh()
+        t = to_device(X, torch.float32, A.device.index)
+        t, vec = _as2d(t)
+        self._count(t, False)
+        Y = torch.empty((self.m, t.shape[1]), dtype=torch.float64, device=A.device)
+        _lib.call("lr_gemm_f64acc", _lib.handle(A.device.index), _lib.OP_N, self.m, self.n,
+                  t.shape[1], _lib.ptr(A), _lib.ld(A), _lib.ptr(t), _lib.ld(t), _lib.ptr(Y),
+                  _lib.ld(Y))
+        return Y.reshape(-1) if vec else Y
+
+
 CudaDenseOperator = DenseOperator
 
 # Optional per-pass timing (bench.py): a list that receives
@@ -668,6 +692,24 @@ def orth_dev(Y, tol=config.GS_DROP_TOL):
               _lib.ptr(Y), _lib.ld(Y), _lib.ptr(Q), _lib.ld(Q), float(tol), C.byref(rank))
     r = int(rank.value)
     return Q if r == ell else Q[:, :r]
+
+
+def orth_dev_deferred(Y, tol=config.GS_DROP_TOL):
+    """Speculative CholeskyQR2 without its last panel product
+    (lr_orth_fast_deferred): (Q1, P2) with orth(Y) = Q1 P2, or None outside a
+    speculative step (the exact path forms Q explicitly)."""
+    torch = _torch()
+    if _SPEC.status is None:
+        return None
+    m, ell = Y.shape
+    if ell == 0 or m == 0:
+        return None
+    Q1 = torch.empty((m, ell), dtype=Y.dtype, device=Y.device)
+    P2 = torch.empty((ell, ell), dtype=_wide(Y.dtype), device=Y.device)
+    _lib.call("lr_orth_fast_deferred", _lib.handle(Y.device.index), _lib.dtype_code(Y.dtype), m,
+              ell, _lib.ptr(Y), _lib.ld(Y), _lib.ptr(Q1), _lib.ptr(P2), float(tol),
+              _lib.ptr(_SPEC.status))
+    return Q1, P2
 
 
 def orthonormalize_double_gs(Y, tol=config.GS_DROP_TOL):

@@ -109,16 +109,28 @@ void chol_any(Handle* h, int dtype, int64_t ell, const void* G, double tol, doub
 
 // Y (m x k) . P (k x ncols, wide, ld ldp) in the working dtype.  P is cast
 // to the panel precision first for fp32 / complex64 panels.
+// amax_hint > 0: a bound on max|Y| known to the caller (an orthonormal panel:
+// |y_ij| <= ||y_j|| ~ 1), which saves the fp32 split its device-side max|Y|
+// pass (one extra read of the m x k panel)
 void apply_right(Handle* h, int dtype, int64_t m, int64_t k, int64_t ncols, const void* Y,
-                 int64_t ldy, const void* P, int64_t ldp, void* out, int64_t ldo) {
+                 int64_t ldy, const void* P, int64_t ldp, void* out, int64_t ldo,
+                 double amax_hint = -1.0) {
   if (dtype == LR_F64 || dtype == LR_C128) {
     gemm_any(h, dtype, false, false, m, ncols, k, Y, ldy, P, ldp, out, ldo);
     return;
   }
   void* Pc = pool_alloc(h, size_t(k) * ncols * elem_size(dtype));
   cast_copy(h, wide_of(dtype), P, ldp, dtype, Pc, ncols, k, ncols, false);
+  if (dtype == LR_F32 && amax_hint > 0.0 && h->f32_mode == LR_F32_SPLIT3 && m >= 1024) {
+    gemm_f32_hint(h, false, m, ncols, k, static_cast<const float*>(Y), ldy, amax_hint,
+                  static_cast<const float*>(Pc), ncols, static_cast<float*>(out), ldo);
+    return;
+  }
   gemm_any(h, dtype, false, false, m, ncols, k, Y, ldy, Pc, ncols, out, ldo);
 }
+
+// bound on max|entry| of a CholeskyQR1 output Q1 (columns of norm ~1 + O(E))
+constexpr double ORTHO_AMAX = 2.0;
 
 int64_t unres_threshold_scale(int64_t ell) { return ell; }
 
@@ -243,12 +255,34 @@ void orth_fast_impl(Handle* h, int dtype, int64_t m, int64_t ell, const void* Y,
   void* Q1 = pool_alloc(h, size_t(m) * ell * es);
   const double unres = 4.0 * double(ell) * U64;
   gram_any(h, dtype, m, ell, Y, ldy, G);
+  if (h->sharded) comm_allreduce_wide(h, wide_of(dtype), ell * ell, G);   // sum_r Y_r^H Y_r
   chol_any(h, dtype, ell, G, tol, unres, 0.0, P, R, h->d_info);
   apply_right(h, dtype, m, ell, ell, Y, ldy, P, ell, Q1, ell);
   gram_second(h, dtype, m, ell, Q1, ell, G);
+  if (h->sharded) comm_allreduce_wide(h, wide_of(dtype), ell * ell, G);
   chol_near_identity(h, wide_of(dtype), ell, G, tol, unres, P, R, h->d_info,
                      near_id_thr(dtype));
-  apply_right(h, dtype, m, ell, ell, Q1, ell, P, ell, Q, ldq);
+  apply_right(h, dtype, m, ell, ell, Q1, ell, P, ell, Q, ldq, ORTHO_AMAX);
+}
+
+// orth_fast_impl without its last product: Q1 (m x ell, ld ell) and the
+// second-pass factor P2 (ell x ell, wide dtype) such that Q = Q1 P2.  A
+// caller whose next step is A^H Q computes (A^H Q1) P2 instead -- an
+// ell x ell product on the n side in place of an m x ell one (config 4: one
+// 1 GiB panel product per subspace step).
+void orth_fast_deferred_impl(Handle* h, int dtype, int64_t m, int64_t ell, const void* Y,
+                             int64_t ldy, void* Q1, void* P2, double tol) {
+  const size_t ws = wide_size(dtype);
+  void* G = pool_alloc(h, size_t(ell) * ell * ws);
+  void* P = pool_alloc(h, size_t(ell) * ell * ws);
+  void* R = pool_alloc(h, size_t(ell) * ell * ws);
+  const double unres = 4.0 * double(ell) * U64;
+  gram_any(h, dtype, m, ell, Y, ldy, G);
+  chol_any(h, dtype, ell, G, tol, unres, 0.0, P, R, h->d_info);
+  apply_right(h, dtype, m, ell, ell, Y, ldy, P, ell, Q1, ell);
+  gram_second(h, dtype, m, ell, Q1, ell, G);
+  chol_near_identity(h, wide_of(dtype), ell, G, tol, unres, P2, R, h->d_info,
+                     near_id_thr(dtype));
 }
 
 // Speculative small SVD (CholeskyQR2 of Bh + Jacobi), no host sync; flags
@@ -273,7 +307,7 @@ void small_svd_fast_impl(Handle* h, int dtype, int64_t r, int64_t c, const void*
   apply_right(h, dtype, c, r, r, Bh, r, P1, r, Q1, r);
   gram_second(h, dtype, c, r, Q1, r, G);
   chol_near_identity(h, wd, r, G, 0.0, unres, P, R2, h->d_info, near_id_thr(dtype));
-  apply_right(h, dtype, c, r, r, Q1, r, P, r, Q2, r);
+  apply_right(h, dtype, c, r, r, Q1, r, P, r, Q2, r, ORTHO_AMAX);
   trmm_upper(h, wd, r, R2, R1, R);
   if (jacobi_reg_supported(r, is_complex(dtype))) {
     void* Mun = pool_alloc(h, size_t(r) * r * ws);
@@ -300,7 +334,7 @@ void small_svd_fast_impl(Handle* h, int dtype, int64_t r, int64_t c, const void*
       ns_coef(h, wd, r, G);
       gemm_any(h, wd, false, false, r, r, r, Wr, r, G, r, J, r);
       cast_copy(h, wd, Ut, r, dtype, U, r, r, r, false);
-      apply_right(h, dtype, c, r, r, Q2, r, J, r, V, r);
+      apply_right(h, dtype, c, r, r, Q2, r, J, r, V, r, ORTHO_AMAX);
       return;
     }
     // register-resident Jacobi on R: R J = M; then J = R^{-1} M
@@ -318,7 +352,7 @@ void small_svd_fast_impl(Handle* h, int dtype, int64_t r, int64_t c, const void*
     ns_coef(h, wd, r, G);
     gemm_any(h, wd, false, false, r, r, r, Ut, r, G, r, J, r);
     cast_copy(h, wd, J, r, dtype, U, r, r, r, false);
-    apply_right(h, dtype, c, r, r, Q2, r, Wr, r, V, r);
+    apply_right(h, dtype, c, r, r, Q2, r, Wr, r, V, r, ORTHO_AMAX);
     return;
   }
   if (is_complex(dtype))
@@ -602,6 +636,7 @@ int lr_destroy(lr_handle_t hh) {
   lr::DeviceGuard dg_(h->device);
   if (!h) return LR_OK;
   cudaStreamSynchronize(h->stream);
+  lr::comm_destroy(h);
   for (auto& c : h->pool.chunks) cudaFree(c.base);
   cudaFree(h->d_info);
   cudaFreeHost(h->h_info);
@@ -657,6 +692,20 @@ int lr_gemm(lr_handle_t hh, int dtype, int op, int64_t m, int64_t n, int64_t ell
     LR_REQUIRE(ldx >= ell && ldy >= ell, LR_EINVAL, "lr_gemm: ld < ell");
     lr::gemm_any(h, dtype, true, op == LR_OP_C, n, ell, m, A, lda, X, ldx, Y, ldy);
   }
+  API_END
+}
+
+int lr_gemm_f64acc(lr_handle_t hh, int op, int64_t m, int64_t n, int64_t ell, const float* A,
+                   int64_t lda, const float* X, int64_t ldx, double* Y, int64_t ldy) {
+  API_BEGIN
+  Handle* h = H(hh);
+  lr::DeviceGuard dg_(h->device);
+  LR_REQUIRE(m >= 0 && n >= 0 && ell >= 0, LR_EINVAL, "lr_gemm_f64acc: negative dimension");
+  LR_REQUIRE(op == LR_OP_N || op == LR_OP_T, LR_EINVAL, "lr_gemm_f64acc: op must be N or T");
+  LR_REQUIRE(lda >= n && ldx >= ell && ldy >= ell, LR_EINVAL, "lr_gemm_f64acc: bad ld");
+  lr::pool_reset(h);
+  if (op == LR_OP_N) lr::gemm_f64_from_f32(h, false, m, ell, n, A, lda, X, ldx, Y, ldy);
+  else               lr::gemm_f64_from_f32(h, true, n, ell, m, A, lda, X, ldx, Y, ldy);
   API_END
 }
 
@@ -860,6 +909,86 @@ int lr_orth_fast(lr_handle_t hh, int dtype, int64_t m, int64_t ell, const void* 
     throw;
   }
   h->status = saved;
+  API_END
+}
+
+int lr_orth_fast_deferred(lr_handle_t hh, int dtype, int64_t m, int64_t ell, const void* Y,
+                          int64_t ldy, void* Q1, void* P2, double tol, int32_t* status) {
+  API_BEGIN
+  Handle* h = H(hh);
+  lr::DeviceGuard dg_(h->device);
+  check_dtype(dtype);
+  LR_REQUIRE(m >= 1 && ell >= 1 && ldy >= ell && status != nullptr && Q1 != Y, LR_EINVAL,
+             "lr_orth_fast_deferred: bad arguments");
+  lr::pool_reset(h);
+  int32_t* saved = h->status;
+  h->status = status;
+  try {
+    lr::orth_fast_deferred_impl(h, dtype, m, ell, Y, ldy, Q1, P2, tol);
+  } catch (...) {
+    h->status = saved;
+    throw;
+  }
+  h->status = saved;
+  API_END
+}
+
+int lr_comm_unique_id(void* id_out) {
+  API_BEGIN
+  LR_REQUIRE(id_out != nullptr, LR_EINVAL, "lr_comm_unique_id: null output");
+  lr::comm_unique_id(id_out);
+  API_END
+}
+
+int lr_comm_init(lr_handle_t hh, const void* id, int nranks, int rank) {
+  API_BEGIN
+  Handle* h = H(hh);
+  lr::DeviceGuard dg_(h->device);
+  LR_REQUIRE(id != nullptr, LR_EINVAL, "lr_comm_init: null id");
+  lr::comm_init(h, id, nranks, rank);
+  API_END
+}
+
+int lr_comm_destroy(lr_handle_t hh) {
+  API_BEGIN
+  Handle* h = H(hh);
+  lr::DeviceGuard dg_(h->device);
+  lr::comm_destroy(h);
+  API_END
+}
+
+int lr_comm_allreduce(lr_handle_t hh, int dtype, int64_t count, void* buf) {
+  API_BEGIN
+  Handle* h = H(hh);
+  lr::DeviceGuard dg_(h->device);
+  LR_REQUIRE(dtype == LR_F64 || dtype == LR_C128, LR_EINVAL,
+             "lr_comm_allreduce: float64 / complex128 buffers");
+  LR_REQUIRE(count >= 0, LR_EINVAL, "lr_comm_allreduce: negative count");
+  lr::comm_allreduce_wide(h, dtype, count, buf);
+  API_END
+}
+
+int lr_orth_sharded(lr_handle_t hh, int dtype, int64_t m_local, int64_t ell, const void* Y,
+                    int64_t ldy, void* Q, int64_t ldq, double tol, int32_t* status) {
+  API_BEGIN
+  Handle* h = H(hh);
+  lr::DeviceGuard dg_(h->device);
+  check_dtype(dtype);
+  LR_REQUIRE(m_local >= 1 && ell >= 1 && ldy >= ell && ldq >= ell && status != nullptr && Q != Y,
+             LR_EINVAL, "lr_orth_sharded: bad arguments");
+  lr::pool_reset(h);
+  int32_t* saved = h->status;
+  h->status = status;
+  h->sharded = true;
+  try {
+    lr::orth_fast_impl(h, dtype, m_local, ell, Y, ldy, Q, ldq, tol);
+  } catch (...) {
+    h->status = saved;
+    h->sharded = false;
+    throw;
+  }
+  h->status = saved;
+  h->sharded = false;
   API_END
 }
 

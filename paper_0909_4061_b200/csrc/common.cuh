@@ -80,9 +80,21 @@ struct Handle {
   // the launch returns at once (the near-identity fast path already produced
   // the factor; see chol_near_identity).  Host-sync free.
   const int32_t* gate = nullptr;
+  // row-sharded calls (lr_comm_init / lr_orth_sharded): the NCCL communicator
+  // of this rank; `sharded` makes the orthonormalization all-reduce its Grams
+  void* nccl_comm = nullptr;
+  int nranks = 1, rank = 0;
+  bool sharded = false;
 };
 
 void pool_reset(Handle* h);
+// comm.cu: in-place sum all-reduce of `count` elements of the wide dtype
+// (float64 / complex128) over the handle's communicator, on h->stream; a
+// no-op without one
+void comm_allreduce_wide(Handle* h, int dtype_wide, int64_t count, void* buf);
+void comm_destroy(Handle* h);
+void comm_unique_id(void* out);
+void comm_init(Handle* h, const void* id, int nranks, int rank);
 
 // Every API entry runs on the handle's device (restoring the caller's):
 // kernel attributes and the pool belong to that device.

@@ -438,12 +438,44 @@ __global__ void split_transpose_kernel(int64_t K, int64_t N, const float* __rest
   }
 }
 
+// out (M x N, ldo) = sum over S slices of part (S x M x N), fixed order in
+// fp64.  Each thread owns 4 consecutive elements (float4 loads) and keeps 8
+// slice loads in flight (A^T Y at config 4 sums 256 slices of 4 MB: the
+// one-element-per-thread version was latency-bound at ~0.8 ms).
 __global__ void reduce_slices_f32(int64_t M, int64_t N, int S, const float* __restrict__ part,
                                   float* __restrict__ out, int64_t ldo) {
   const int64_t total = M * N;
+  const bool vec = (total % 4) == 0 && (N % 4) == 0 &&
+                   (reinterpret_cast<uintptr_t>(part) & 15) == 0;
+  if (vec) {
+    const int64_t t4 = total / 4;
+    for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < t4;
+         q += int64_t(gridDim.x) * blockDim.x) {
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      int k = 0;
+      for (; k + 8 <= S; k += 8) {
+        float4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          v[u] = __ldcs(reinterpret_cast<const float4*>(part + int64_t(k + u) * total) + q);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          s0 += double(v[u].x); s1 += double(v[u].y); s2 += double(v[u].z); s3 += double(v[u].w);
+        }
+      }
+      for (; k < S; ++k) {
+        const float4 v = __ldcs(reinterpret_cast<const float4*>(part + int64_t(k) * total) + q);
+        s0 += double(v.x); s1 += double(v.y); s2 += double(v.z); s3 += double(v.w);
+      }
+      const int64_t i = q * 4, r = i / N, c = i % N;
+      float* o = out + r * ldo + c;
+      o[0] = float(s0); o[1] = float(s1); o[2] = float(s2); o[3] = float(s3);
+    }
+    return;
+  }
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total;
        i += int64_t(gridDim.x) * blockDim.x) {
-    double s = 0.0;     // fixed order, fp64 (up to ~40 split-K slices)
+    double s = 0.0;     // fixed order, fp64
     for (int k = 0; k < S; ++k) s += double(part[int64_t(k) * total + i]);
     out[(i / N) * ldo + (i % N)] = float(s);
   }
@@ -480,6 +512,7 @@ constexpr int W_AH = WBM * TBK * 2;       // 16 KB (one of hi / lo)
 #define LR_W_TS3 2
 #endif
 constexpr int W_TS1 = LR_W_TS1;
+constexpr int64_t W_KMAX = 4096;   // k-extent of one TMEM accumulator (see gemm_f32_m256)
 constexpr int W_TS2 = LR_W_TS2;
 constexpr int W_TS3 = LR_W_TS3;
 
@@ -1220,7 +1253,13 @@ void gemm_f32_m256(Handle* h, bool transA, int64_t M, int64_t N, int64_t K, cons
   const size_t smem = size_t(W_TS1) * W_A32 + size_t(W_TS2) * 2 * W_AH + size_t(W_TS3) * b_slot +
                       1024 /*align*/ + 256 /*barriers*/;
   const int64_t mt = ceil_div(M, WBM);
-  const int64_t splits0 = wave_splits(mt, h->sm_count, K);
+  // the tensor cores' fp32 accumulation truncates: each of the 6 UMMAs per
+  // 32-deep stage shrinks |acc| by ~2^-25 on average, so the relative bias
+  // grows with the k-extent one accumulator covers.  Cap it at 4096 (the
+  // A X pass's own depth at config 4): A^T Y with K = m = 2^20 is split 256
+  // ways (measured at 65536 rows: top sigma 1.7e-5 relative with ~3.6k-row
+  // slices, vs 2e-8 for the round-to-nearest FFMA path)
+  const int64_t splits0 = std::max(wave_splits(mt, h->sm_count, K), ceil_div(K, W_KMAX));
   const int64_t kps = ceil_div(ceil_div(K, splits0), TBK) * TBK;
   const int64_t splits = ceil_div(K, kps);
   float* out = C;

@@ -108,6 +108,229 @@ void launch_srft(Handle* h, int64_t m, int64_t n, int64_t ell, const C* A, int64
   LR_CHECK_LAUNCH();
 }
 
+// ---- radix-16 Stockham FFT (default for power-of-two n) ----------------------
+// The radix-2 kernel above makes log2(n) passes through shared memory with a
+// barrier each and computes every twiddle with sincospi (config 3: ~1.7 ms,
+// ~5 % of the HBM bound).  Here each thread keeps 16 points in registers:
+// n = 16^p * r is transformed in p radix-16 passes plus one radix-r pass
+// (8192 = 16^3 * 2: 4 passes, 4 barriers), twiddles come from a table
+// W[k] = exp(-2 pi i k / n) built once per n (L1-resident), and the pass
+// structure is Stockham's autosort (natural-order output, no bit reversal):
+//   pass (R, Ns): for j < n/R: v_r = x[j + r n/R] * W^{(j mod Ns) r n/(Ns R)},
+//                 v = DFT_R(v), x'[(j/Ns) Ns R + j mod Ns + r Ns] = v_r.
+// The first pass reads the row of A straight from HBM (coalesced) times d;
+// the last writes its result to shared memory, from which the ell picked bins
+// are gathered.  Shared memory is padded one element in 16 (stride-16
+// stores of the first pass would otherwise hit one bank).
+
+__device__ __forceinline__ int pad16(int i) { return i + (i >> 4); }
+
+template <typename C>
+__device__ __forceinline__ C cmul(C a, C b) { return Cx<C>::mul(a, b); }
+template <typename C>
+__device__ __forceinline__ C cadd(C a, C b) { return Cx<C>::add(a, b); }
+template <typename C>
+__device__ __forceinline__ C csub(C a, C b) { return Cx<C>::sub(a, b); }
+// a * (-i)
+template <typename C>
+__device__ __forceinline__ C mul_mi(C a) { C r; r.x = a.y; r.y = -a.x; return r; }
+
+template <typename C>
+__device__ __forceinline__ void dft2(C& a, C& b) {
+  const C t = a;
+  a = cadd(t, b);
+  b = csub(t, b);
+}
+// in-place 4-point DFT (W4 = -i): natural order in and out
+template <typename C>
+__device__ __forceinline__ void dft4(C& x0, C& x1, C& x2, C& x3) {
+  const C s02 = cadd(x0, x2), d02 = csub(x0, x2);
+  const C s13 = cadd(x1, x3), d13 = mul_mi(csub(x1, x3));
+  x0 = cadd(s02, s13);
+  x2 = csub(s02, s13);
+  x1 = cadd(d02, d13);
+  x3 = csub(d02, d13);
+}
+
+template <typename C>
+__device__ __forceinline__ C w16(int m) {   // exp(-2 pi i m / 16)
+  using R = typename Cx<C>::R;
+  constexpr double c16[16] = {1.0, 0.92387953251128674, 0.70710678118654752, 0.38268343236508977,
+                              0.0, -0.38268343236508977, -0.70710678118654752, -0.92387953251128674,
+                              -1.0, -0.92387953251128674, -0.70710678118654752, -0.38268343236508977,
+                              0.0, 0.38268343236508977, 0.70710678118654752, 0.92387953251128674};
+  C w;
+  w.x = R(c16[m & 15]);
+  w.y = R(-c16[(m + 12) & 15]);   // -sin(2 pi m / 16) = -cos(2 pi (m - 4) / 16)
+  return w;
+}
+
+// DFT of size R in registers, natural order in and out (R = 2, 4, 8, 16)
+template <typename C, int R>
+__device__ __forceinline__ void dft_reg(C (&v)[R]) {
+  if constexpr (R == 2) {
+    dft2(v[0], v[1]);
+  } else if constexpr (R == 4) {
+    dft4(v[0], v[1], v[2], v[3]);
+  } else if constexpr (R == 8) {
+    // 8 = 2 x 4: columns n2 = 0, 1 of x[2 n1 + n2]
+    C a[4] = {v[0], v[2], v[4], v[6]}, b[4] = {v[1], v[3], v[5], v[7]};
+    dft4(a[0], a[1], a[2], a[3]);
+    dft4(b[0], b[1], b[2], b[3]);
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) {
+      const C t = cmul(b[k1], w16<C>(2 * k1));     // W8^k1
+      v[k1] = cadd(a[k1], t);
+      v[k1 + 4] = csub(a[k1], t);
+    }
+  } else {
+    // 16 = 4 x 4: X[k1 + 4 k2] = sum_n2 W16^(n2 k1) W4^(n2 k2) DFT4_n1(x[4 n1 + n2])[k1]
+    C a[4][4];
+#pragma unroll
+    for (int n2 = 0; n2 < 4; ++n2) {
+      a[n2][0] = v[n2];
+      a[n2][1] = v[4 + n2];
+      a[n2][2] = v[8 + n2];
+      a[n2][3] = v[12 + n2];
+      dft4(a[n2][0], a[n2][1], a[n2][2], a[n2][3]);
+#pragma unroll
+      for (int k1 = 1; k1 < 4; ++k1)
+        if (n2) a[n2][k1] = cmul(a[n2][k1], w16<C>(n2 * k1));
+    }
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) {
+      C b0 = a[0][k1], b1 = a[1][k1], b2 = a[2][k1], b3 = a[3][k1];
+      dft4(b0, b1, b2, b3);
+      v[k1] = b0;
+      v[k1 + 4] = b1;
+      v[k1 + 8] = b2;
+      v[k1 + 12] = b3;
+    }
+  }
+}
+
+// one Stockham pass of radix R over the padded shared-memory row; each of the
+// n/16 threads owns 16/R butterfly groups (16 registers).  FIRST: inputs from
+// the global row a times d.  Ns = 2^ls; the twiddles W^(jm r), r = 1..R-1, are
+// powers of one table entry (one table read per group; the error of the
+// 15-fold product is ~15 ulp of the working precision).
+template <typename C, int R, bool FIRST>
+__device__ __forceinline__ void stockham_pass(C* buf, int n, int ls, const C* __restrict__ tw,
+                                              const C* a, const C* __restrict__ d) {
+  constexpr int G = 16 / R;
+  constexpr int LR = R == 2 ? 1 : R == 4 ? 2 : R == 8 ? 3 : 4;
+  const int nr = n / R;
+  const int Ns = 1 << ls;
+  C v[G][R];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const int j = threadIdx.x + g * blockDim.x;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int idx = j + r * nr;
+      if constexpr (FIRST) v[g][r] = d ? cmul(__ldg(a + idx), __ldg(d + idx)) : __ldg(a + idx);
+      else                 v[g][r] = buf[pad16(idx)];
+    }
+    if (ls > 0) {
+      const int jm = j & (Ns - 1);
+      // W_{Ns R}^jm = W_n^(jm n / (Ns R)); n / (Ns R) = n >> (ls + LR)
+      const C w = tw[jm * (n >> (ls + LR))];
+      C wr = w;
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        v[g][r] = cmul(v[g][r], wr);
+        if (r + 1 < R) wr = cmul(wr, w);
+      }
+    }
+    dft_reg<C, R>(v[g]);
+  }
+  __syncthreads();   // every load of this pass precedes the stores (in place)
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const int j = threadIdx.x + g * blockDim.x;
+    const int jm = j & (Ns - 1);
+    const int base = ((j >> ls) << (ls + LR)) + jm;
+#pragma unroll
+    for (int r = 0; r < R; ++r) buf[pad16(base + (r << ls))] = v[g][r];
+  }
+  __syncthreads();
+}
+
+template <typename C>
+__global__ void __launch_bounds__(sizeof(C) == 8 ? 1024 : 512) srft16_kernel(int64_t m, int n, int p16, int rlast,
+                                                      int ell, const C* A, int64_t lda,
+                                                      const C* __restrict__ d,
+                                                      const int32_t* __restrict__ picks,
+                                                      const C* __restrict__ tw, double scale,
+                                                      C* Y, int64_t ldy) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  C* buf = reinterpret_cast<C*>(smem_raw);
+  const double s = scale * rsqrt(double(n));
+  for (int64_t row = blockIdx.x; row < m; row += gridDim.x) {
+    const C* a = A + row * lda;
+    int ls = 0;
+    for (int q = 0; q < p16; ++q, ls += 4) {
+      if (q == 0) stockham_pass<C, 16, true>(buf, n, ls, tw, a, d);
+      else        stockham_pass<C, 16, false>(buf, n, ls, tw, a, d);
+    }
+    const bool first = p16 == 0;
+    switch (rlast) {
+      case 2: first ? stockham_pass<C, 2, true>(buf, n, ls, tw, a, d)
+                    : stockham_pass<C, 2, false>(buf, n, ls, tw, a, d); break;
+      case 4: first ? stockham_pass<C, 4, true>(buf, n, ls, tw, a, d)
+                    : stockham_pass<C, 4, false>(buf, n, ls, tw, a, d); break;
+      case 8: first ? stockham_pass<C, 8, true>(buf, n, ls, tw, a, d)
+                    : stockham_pass<C, 8, false>(buf, n, ls, tw, a, d); break;
+      default: break;
+    }
+    for (int t = threadIdx.x; t < ell; t += blockDim.x) {
+      const int pk = picks ? picks[t] : t;
+      Y[row * ldy + t] = Cx<C>::scl(buf[pad16(pk)], s);
+    }
+    __syncthreads();
+  }
+}
+
+template <typename C>
+__global__ void twiddle_table_kernel(int n, C* __restrict__ tw) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    double sv, cv;
+    sincospi(-2.0 * double(k) / double(n), &sv, &cv);
+    using R = typename Cx<C>::R;
+    C w;
+    w.x = R(cv);
+    w.y = R(sv);
+    tw[k] = w;
+  }
+}
+
+bool srft16_ok(int64_t n, size_t elem) {
+  if (n < 256 || (n & (n - 1)) != 0 || n / 16 > (elem == 8 ? 1024 : 512)) return false;
+  return size_t(n + n / 16) * elem <= 200 * 1024;
+}
+
+template <typename C>
+void launch_srft16(Handle* h, int64_t m, int64_t n, int64_t ell, const C* A, int64_t lda,
+                   const C* d, const int32_t* picks, double scale, C* Y, int64_t ldy) {
+  int bits = 0;
+  while ((int64_t(1) << bits) < n) ++bits;
+  const int p16 = bits / 4, rlast = 1 << (bits % 4);
+  C* tw = pool_alloc_t<C>(h, size_t(n));
+  twiddle_table_kernel<C><<<int(ceil_div(n, 256)), 256, 0, h->stream>>>(int(n), tw);
+  LR_CHECK_LAUNCH();
+  const size_t smem = size_t(n + n / 16) * sizeof(C);
+  auto kern = srft16_kernel<C>;
+  LR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  const int threads = int(n / 16);
+  int per_sm = 1;
+  LR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+  const int blocks = int(std::min<int64_t>(m, int64_t(h->sm_count) * std::max(per_sm, 1)));
+  if (blocks == 0) return;
+  kern<<<blocks, threads, smem, h->stream>>>(m, int(n), p16, rlast == 1 ? 0 : rlast, int(ell), A,
+                                             lda, d, picks, tw, scale, Y, ldy);
+  LR_CHECK_LAUNCH();
+}
+
 }  // namespace
 
 namespace {
@@ -236,13 +459,20 @@ void gsrft_matrix(Handle* h, int dtype, int64_t n, int64_t ell, const double2* d
 void srft_c64(Handle* h, int64_t m, int64_t n, int64_t ell, const float2* A, int64_t lda,
               const float2* d, const int32_t* picks, float scale, float2* Y, int64_t ldy,
               double a_amax) {
-  static int fft_only = -1;
-  if (fft_only < 0) {
-    const char* e = getenv("LR_SRFT");
-    fft_only = (e && e[0] == 'f') ? 1 : 0;
+  // LR_SRFT=gemm: the dense picked-DFT-columns pass on the tensor cores
+  // (O(m n ell)); LR_SRFT=radix2: the radix-2 kernel; default radix-16 FFT
+  const char* e = getenv("LR_SRFT");
+  const bool gemm_mode = e && e[0] == 'g';
+  const bool r2_mode = e && e[0] == 'r';
+  if (!pow2(n) || (gemm_mode && ell <= 128 && h->f32_mode == LR_F32_SPLIT3 && m >= 1024)) {
+    srft_gemm<float2>(h, m, n, ell, A, lda, d, picks, double(scale), Y, ldy, a_amax);
+    return;
   }
-  if (!pow2(n) ||
-      (!fft_only && ell <= 128 && h->f32_mode == LR_F32_SPLIT3 && m >= 1024)) {
+  if (!r2_mode && srft16_ok(n, sizeof(float2))) {
+    launch_srft16<float2>(h, m, n, ell, A, lda, d, picks, double(scale), Y, ldy);
+    return;
+  }
+  if (size_t(n) * sizeof(float2) > 200 * 1024) {   // row too long for shared memory
     srft_gemm<float2>(h, m, n, ell, A, lda, d, picks, double(scale), Y, ldy, a_amax);
     return;
   }
@@ -252,6 +482,15 @@ void srft_c64(Handle* h, int64_t m, int64_t n, int64_t ell, const float2* A, int
 void srft_c128(Handle* h, int64_t m, int64_t n, int64_t ell, const double2* A, int64_t lda,
                const double2* d, const int32_t* picks, double scale, double2* Y, int64_t ldy) {
   if (!pow2(n)) {
+    srft_gemm<double2>(h, m, n, ell, A, lda, d, picks, scale, Y, ldy, -1.0);
+    return;
+  }
+  const char* e = getenv("LR_SRFT");
+  if (!(e && e[0] == 'r') && srft16_ok(n, sizeof(double2))) {
+    launch_srft16<double2>(h, m, n, ell, A, lda, d, picks, scale, Y, ldy);
+    return;
+  }
+  if (size_t(n) * sizeof(double2) > 200 * 1024) {   // row too long for shared memory
     srft_gemm<double2>(h, m, n, ell, A, lda, d, picks, scale, Y, ldy, -1.0);
     return;
   }
@@ -273,12 +512,23 @@ void dft_rows(Handle* h, int dtype, int64_t rows, int64_t n, void* X, int64_t ld
                               h->stream));
     return;
   }
-  if (dtype == LR_C64)
-    launch_srft<float2>(h, rows, n, n, static_cast<const float2*>(X), ldx, nullptr, nullptr, 1.0,
-                        static_cast<float2*>(X), ldx);
-  else
-    launch_srft<double2>(h, rows, n, n, static_cast<const double2*>(X), ldx, nullptr, nullptr,
-                         1.0, static_cast<double2*>(X), ldx);
+  const char* e = getenv("LR_SRFT");
+  const bool r2 = e && e[0] == 'r';
+  if (dtype == LR_C64) {
+    if (!r2 && srft16_ok(n, sizeof(float2)))
+      launch_srft16<float2>(h, rows, n, n, static_cast<const float2*>(X), ldx, nullptr, nullptr,
+                            1.0, static_cast<float2*>(X), ldx);
+    else
+      launch_srft<float2>(h, rows, n, n, static_cast<const float2*>(X), ldx, nullptr, nullptr, 1.0,
+                          static_cast<float2*>(X), ldx);
+  } else {
+    if (!r2 && srft16_ok(n, sizeof(double2)))
+      launch_srft16<double2>(h, rows, n, n, static_cast<const double2*>(X), ldx, nullptr, nullptr,
+                             1.0, static_cast<double2*>(X), ldx);
+    else
+      launch_srft<double2>(h, rows, n, n, static_cast<const double2*>(X), ldx, nullptr, nullptr,
+                           1.0, static_cast<double2*>(X), ldx);
+  }
 }
 
 }  // namespace lr

@@ -49,6 +49,39 @@ class Comm:
             self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
         return t
 
+    def allgather_rows(self, t, total):
+        """Row shards (row_range split of `total` rows) -> the full matrix on
+        every rank (the n-side panel before a pass A_r X, config 5)."""
+        if self.world == 1:
+            return t
+        import torch
+        sizes = [row_range(total, r, self.world) for r in range(self.world)]
+        mx = max(b - a for a, b in sizes)
+        pad = torch.zeros((mx,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+        pad[:t.shape[0]] = t
+        parts = [torch.empty_like(pad) for _ in range(self.world)]
+        self.dist.all_gather(parts, pad, group=self.group)
+        return torch.cat([p[:b - a] for p, (a, b) in zip(parts, sizes)], dim=0).contiguous()
+
+    def reduce_scatter_rows(self, t, total):
+        """Full-size partials (total x c, one per rank) -> this rank's rows of
+        their sum (the n-side result of A^H Y over row-sharded A, config 5):
+        reduce-scatter over NCCL, all-reduce + slice where the backend has no
+        reduce-scatter (gloo)."""
+        if self.world == 1:
+            return t
+        import torch
+        a, b = row_range(total, self.rank, self.world)
+        sizes = [row_range(total, r, self.world) for r in range(self.world)]
+        even = all(bb - aa == b - a for aa, bb in sizes)
+        if even and self.dist.get_backend(self.group) == "nccl":
+            out = torch.empty((b - a,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+            self.dist.reduce_scatter_tensor(out, t.contiguous(), op=self.dist.ReduceOp.SUM,
+                                            group=self.group)
+            return out
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
+        return t[a:b].contiguous()
+
 
 class GpuBackend:
     """Kernels of liblowrank_b200 on torch CUDA tensors (the product path)."""
@@ -73,6 +106,13 @@ class GpuBackend:
     def srft(self, A, ell, seed):
         from .sketch import srft_dev, srft_operator
         return srft_dev(A, srft_operator(A.shape[1], ell, seed))
+
+    # --- passes of a row-block operator A_r (m_r x n), e.g. CudaCsrOperator
+    def op_n(self, op, X):
+        return op.apply(X)
+
+    def op_t(self, op, Y):
+        return op.apply_adjoint(Y)
 
     # --- panel kernels
     def gram(self, Y):
@@ -114,6 +154,10 @@ class GpuBackend:
 
     def new_status(self, like):
         return self.torch.zeros(1, dtype=self.torch.int32, device=like.device)
+
+    def like(self, op):
+        """A device tensor of the operator's dtype / device (draw template)."""
+        return self.torch.empty(0, dtype=op.dtype, device=op.device)
 
     def status_value(self, status):
         return int(status.item())
@@ -364,6 +408,68 @@ def _dist_step(A_local, n, k, p, q, seed, comm, be, amax, estimate, probes, alph
         kk = min(int(k), U.shape[1])
         U, S, V = U[:, :kk], S[:kk], V[:, :kk]
     return DistResult(Q=Q, U=U, sigma=S, V=V, est=est, passes=2 * q + 2 if q else 1)
+
+
+def dist_randomized_svd_operator(op_local, n, k, p, q, seed, comm, be, estimate=True,
+                                 probes=config.DEFAULT_PROBES, alpha=config.DEFAULT_ALPHA,
+                                 truncate=False):
+    """Row-sharded rSVD of an operator given by its row block A_r (m_r x n)
+    on every rank -- the sparse path of config 5 (S_r + L_r R^T as a
+    CudaCsrOperator over the rank's rows): Alg 4.4 / 4.1 +
+    Alg 5.1 + the posterior estimate, with BOTH sides of the panels sharded.
+
+      Y_r = A_r X                       X (n x ell) all-gathered from n-shards
+      Z_c = sum_r (A_r^H Y_r)[c rows]   reduce-scatter of the n x ell partials
+      orth of either side               dist_orth (all-reduced Gram)
+      B = Q* A = Z^H:  Z = Q_Z R_Z (sharded CholeskyQR), SVD of R_Z^H replicated,
+                       V_c = Q_Z,c W, U_r = Q_r U~
+
+    so the n-side work is split too (the dense path replicates it: n = 4096
+    there, n = 2^21 here).  Every rank returns its rows of Q and U, its
+    n-side rows of V (row_range(n, rank, world)), sigma and the estimate."""
+    ell = int(k) + int(p)
+    if ell < 1 or ell > n:
+        raise ValueError(f"rank+oversample {ell} must be in [1, {n}]")
+    like = be.like(op_local)
+    Om = be.gaussian(n, ell, seed, _STREAM_GAUSS, like)
+    Q = dist_orth(be.op_n(op_local, Om), comm, be)
+    for _ in range(q):
+        if Q.shape[1] == 0:
+            break
+        Zc = comm.reduce_scatter_rows(be.op_t(op_local, Q), n)
+        Qt = dist_orth(Zc, comm, be)
+        X = comm.allgather_rows(Qt, n)
+        Q = dist_orth(be.op_n(op_local, X), comm, be)
+    passes = 2 * q + 2 if q else 1
+    if Q.shape[1] == 0:
+        return DistResult(Q=Q, U=be.zeros_like_rows(Q, 0), sigma=be.empty_sigma(like),
+                          V=be.zeros_rows(row_range(n, comm.rank, comm.world)[1]
+                                          - row_range(n, comm.rank, comm.world)[0], 0, like),
+                          est=0.0, passes=passes)
+    Zc = comm.reduce_scatter_rows(be.op_t(op_local, Q), n)
+    QZ = dist_orth(Zc, comm, be, tol=0.0)
+    if QZ.shape[1] == Q.shape[1]:
+        RZ = comm.allreduce(be.adj_matmul(QZ, Zc))      # Z = Q_Z R_Z
+        Ub, S, W = be.small_svd(RZ)                      # R_Z^H = Ub S W^H
+        V = be.matmul(QZ, W)
+    else:
+        # numerically rank-deficient B: gather Z and factor it whole
+        Ub, S, Vf = be.small_svd(comm.allgather_rows(Zc, n))
+        a, b = row_range(n, comm.rank, comm.world)
+        V = Vf[a:b]
+    U = be.matmul(Q, Ub)
+    est = None
+    if estimate:
+        W = be.gaussian(n, probes, seed + 13, _STREAM_PROBE, like)
+        Zl = be.op_n(op_local, W)
+        C = comm.allreduce(be.adj_matmul(Q, Zl))
+        be.sub_(Zl, be.matmul(Q, C))
+        ss = comm.allreduce(be.colsumsq(Zl))
+        est = alpha * math.sqrt(2.0 / math.pi) * math.sqrt(be.to_scalar(ss))
+    if truncate:
+        kk = min(int(k), U.shape[1])
+        U, S, V = U[:, :kk], S[:kk], V[:, :kk]
+    return DistResult(Q=Q, U=U, sigma=S, V=V, est=est, passes=passes)
 
 
 def row_range(m, rank, world):

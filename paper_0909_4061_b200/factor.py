@@ -44,9 +44,11 @@ class PartialSVD:
         return (self.U * self.sigma) @ self.V.conj().T
 
 
-def direct_svd_dev(op, Q):
+def direct_svd_dev(op, Q, orthonormal=False):
     """Alg 5.1 on the device: Z = A^H Q (one pass), small SVD of B = Z^H,
-    U = Q U~.  Returns device (U, sigma, V)."""
+    U = Q U~.  Returns device (U, sigma, V).  orthonormal: Q comes from this
+    package's orthonormalization (|q_ij| <= 1), so the fp32 split of U = Q U~
+    skips its max|Q| pass."""
     torch = _torch()
     k = Q.shape[1]
     if k == 0:
@@ -56,7 +58,12 @@ def direct_svd_dev(op, Q):
     Z = apply_dev(op, Q, adjoint=True)            # n x k  (= B^H)
     Ub, S, V = small_svd_from_adjoint(Z)
     U = torch.empty((op.m, k), dtype=Q.dtype, device=Q.device)
-    gemm_dev(Q, Ub, U)
+    if orthonormal and Q.dtype == torch.float32 and Q.shape[0] >= 1024:
+        _lib.call("lr_gemm_scaled", _lib.handle(Q.device.index), _lib.F32, _lib.OP_N, Q.shape[0],
+                  k, k, _lib.ptr(Q), _lib.ld(Q), 2.0, _lib.ptr(Ub), _lib.ld(Ub), _lib.ptr(U),
+                  _lib.ld(U))
+    else:
+        gemm_dev(Q, Ub, U)
     return U, S, V
 
 
@@ -471,7 +478,7 @@ def randomized_svd(A, k, p=config.DEFAULT_OVERSAMPLE, q=0, seed=0, sketch="gauss
             Q = orth_dev(srft_dev(op.array, srft, amax=getattr(op, "amax", None)))
         else:
             Q = orth_dev(gsrft_dev(op.array, srft, amax=getattr(op, "amax", None)))
-        U, S, V = direct_svd_dev(op, Q)
+        U, S, V = direct_svd_dev(op, Q, orthonormal=True)
         est_dev = None
         if estimate and Q.shape[1]:
             est_dev = posterior_error_estimate_dev(op, Q, probes, alpha, seed + 13, W=W)
@@ -486,6 +493,67 @@ def randomized_svd(A, k, p=config.DEFAULT_OVERSAMPLE, q=0, seed=0, sketch="gauss
     Q, U, S, V = _outs(host, Q, U, S, V)
     basis = RangeBasis(Q=Q, samples_used=ell, passes=passes, est_error=est, spec=spec)
     return basis, PartialSVD(U=U, sigma=S, V=V), est
+
+
+def stage_a(A, rank=None, oversample=config.DEFAULT_OVERSAMPLE, power=0, sketch="gauss",
+            tol=None, probes=config.DEFAULT_PROBES, alpha=config.DEFAULT_ALPHA, seed=0,
+            adaptive=False):
+    """The reference CLI's Stage-A dispatch (cli.py:128-165) on the GPU:
+
+      tol given:   gauss -> adaptive range finder (Alg 4.2);
+                   srft / gsrft -> the doubling ladder ell = 32, 64, 128, ...
+                   (min(ell, n)) with the posterior estimate at seed + 7 until
+                   est <= tol or ell reaches n (saturated when it stops there
+                   above tol), Remark 4.4;
+      else:        ell = rank + oversample; gauss: q > 0 -> Alg 4.4, q = 0 ->
+                   Alg 4.1; srft / gsrft -> Alg 4.5 (q > 0 and ell > n rejected).
+    Returns (RangeBasis, operator)."""
+    from .rangefinder import (adaptive_range_finder, fast_range_finder,
+                              posterior_error_estimate_dev, randomized_range_finder,
+                              subspace_iteration_range)
+    op = as_operator(A)
+    n = op.n
+    if adaptive and tol is None:
+        raise ValueError("--adaptive requires --tol")
+    if tol is not None:
+        if sketch in ("gauss", "gaussian"):
+            return adaptive_range_finder(op, tol, r=probes, seed=seed, alpha=alpha), op
+        ell = 32
+        while True:
+            ell = min(ell, n)
+            basis = fast_range_finder(op, ell, seed, kind=sketch)
+            Qd = to_device(basis.Q)
+            est = float(posterior_error_estimate_dev(op, Qd, probes, alpha, seed + 7).item())
+            basis.est_error = est
+            if est <= tol or ell >= n:
+                basis.saturated = ell >= n and est > tol
+                return basis, op
+            ell *= 2
+    if rank is None:
+        raise ValueError("either rank or tol is required")
+    ell = int(rank) + int(oversample)
+    if sketch in ("gauss", "gaussian"):
+        if power > 0:
+            return subspace_iteration_range(op, ell, power, seed), op
+        return randomized_range_finder(op, ell, seed), op
+    if power > 0:
+        raise ValueError("power iterations are not available with structured sketches")
+    if ell > n:
+        raise ValueError(f"rank+oversample {ell} exceeds the column count {n}")
+    return fast_range_finder(op, ell, seed, kind=sketch), op
+
+
+def svd_single_pass(A, rank, oversample=config.DEFAULT_OVERSAMPLE, seed=0, bundle_basis="gs",
+                    probes=config.DEFAULT_PROBES, alpha=config.DEFAULT_ALPHA):
+    """The CLI's --single-pass SVD (cli.py:225-235): two-sided bundle, the
+    one-pass general SVD, the posterior estimate at seed + 13.  Returns
+    (PartialSVD, est_error)."""
+    from .rangefinder import posterior_error_estimate
+    ell = int(rank) + int(oversample)
+    b = sample_bundle_two_sided(A, ell, seed=seed, rank=rank if bundle_basis == "svd" else None)
+    f = svd_one_pass_general(b)
+    est = posterior_error_estimate(A, b.Q, r=probes, alpha=alpha, seed=seed + 13)
+    return f, est
 
 
 # ---------------------------------------------------------------------------
@@ -566,6 +634,8 @@ def _capture(op, body, entry, dev):
     from . import core
     torch = _torch()
     snap = _snapshot(op)
+    from . import sketch as _sk
+    ops0 = _sk.op_count()
     status = torch.zeros(1, dtype=torch.int32, device=dev)
     g = torch.cuda.CUDAGraph()
     torch.cuda.synchronize()
@@ -588,6 +658,9 @@ def _capture(op, body, entry, dev):
         core.PASS_EVENTS = prev
     after = _snapshot(op)
     entry["delta"] = tuple(a - b for a, b in zip(after, snap))
+    from . import sketch as _sk
+    entry["ops"] = _sk.op_count() - ops0
+    _sk._count(-entry["ops"])          # the capture ran nothing: replays count
     _restore(op, snap)
     # the captured kernels hold raw addresses in this handle's scratch pool:
     # remember its generation (a later pool merge frees those chunks)
@@ -615,6 +688,8 @@ def _replay(op, entry, counters):
     d = entry["delta"]
     c.matvecs, c.adjoint_matvecs, c.passes, c.flops = (
         counters[0] + d[0], counters[1] + d[1], counters[2] + d[2], counters[3] + d[3])
+    from . import sketch as _sk
+    _sk._count(entry.get("ops", 0))
     Q, U, S, V, est = entry["out"]
     # the graph's buffers are reused by the next replay: hand out copies
     return (Q.clone(), U.clone(), S.clone(), V.clone(), None if est is None else est.clone())

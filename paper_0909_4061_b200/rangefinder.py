@@ -139,15 +139,33 @@ def power_iteration_range(A, ell, q, seed, ortho_tol=config.GS_DROP_TOL, safegua
                       est_error=est, spec=spec)
 
 
+def _adjoint_of_orth(op, Y, ortho_tol):
+    """A^H orth(Y).  Inside a speculative step on a device operator the
+    second CholeskyQR factor is deferred: orth(Y) = Q1 P2 and A^H Q1 P2 =
+    (A^H Q1) P2, an ell x ell product on the n side instead of an m x ell
+    panel product (lr_orth_fast_deferred)."""
+    from .core import orth_dev_deferred
+    d = orth_dev_deferred(Y, ortho_tol) if getattr(op, "device_native", False) else None
+    if d is None:
+        return apply_dev(op, orth_dev(Y, ortho_tol), adjoint=True)
+    Q1, P2 = d
+    Z = apply_dev(op, Q1, adjoint=True)
+    out = _torch().empty_like(Z)
+    gemm(Z, cast_dev(P2, Z.dtype), out)
+    return out
+
+
 def subspace_iteration_range_dev(op, ell, q, seed, ortho_tol=config.GS_DROP_TOL, omega=None):
-    """Alg 4.4 on a device operator; returns the device basis."""
+    """Alg 4.4 on a device operator; returns the device basis.  Same
+    products as the reference loop (Q = orth(A Omega); q x [Q~ = orth(A* Q),
+    Q = orth(A Q~)]) with each A* Q formed as (A* Q1) P2 (_adjoint_of_orth)."""
     if omega is None:
         omega = _cast_like_op(op, _sketch_dev(op, ell, seed))
-    Q = orth_dev(apply_dev(op, omega), ortho_tol)
+    Y = apply_dev(op, omega)
     for _ in range(q):
-        Qt = orth_dev(apply_dev(op, Q, adjoint=True), ortho_tol)
-        Q = orth_dev(apply_dev(op, Qt), ortho_tol)
-    return Q
+        Qt = orth_dev(_adjoint_of_orth(op, Y, ortho_tol), ortho_tol)
+        Y = apply_dev(op, Qt)
+    return orth_dev(Y, ortho_tol)
 
 
 def subspace_iteration_range(A, ell, q, seed, ortho_tol=config.GS_DROP_TOL):
@@ -209,7 +227,14 @@ def posterior_error_estimate_dev(op, Q, r=config.DEFAULT_PROBES, alpha=config.DE
     torch = _torch()
     if W is None:
         W = probes_dev(op, r, seed)
-    Z = apply_dev(op, W)
+    if (getattr(op, "device_native", False) and hasattr(op, "apply_wide")
+            and op.dtype == torch.float32 and not W.is_complex()):
+        # fp32 operator: the narrow probe pass with exact products and fp64
+        # accumulation (the residual is ~1e-5 of |A w| at config 4: below the
+        # tensor-core split's rounding), projection in fp64
+        Z = op.apply_wide(W)
+    else:
+        Z = apply_dev(op, W)
     Z = Z.contiguous() if Z.stride(-1) != 1 else Z
     est = torch.empty(1, dtype=torch.float64, device=Z.device)
     Qd = Q if is_device_array(Q) else to_device(Q)

@@ -36,6 +36,51 @@ def rng_for(seed, stream=0, index=0):
     return np.random.Generator(np.random.Philox(key=key))
 
 
+# ---------------------------------------------------------------------------
+# operation counter (reference sketch.py:45-62): one process-wide counter of
+# the scalar operations the structured-sketch applications perform, in the
+# reference's cost units (complex multiply 6, complex add 2).  The counts are
+# those of the path that actually ran on the device: the FFT kernels (radix-16
+# Stockham for power-of-two n) are charged the reference's own radix-2 model
+# (D: 6 n, butterflies 10 n/2 per level, normalization 2 n, picks 2 ell per
+# row -- an upper bound of the radix-16 work), the dense picked-DFT-column
+# product (non-power-of-two n, LR_SRFT=gemm, the GSRFT's picked columns)
+# 8 n ell per row.
+
+_OPS = 0
+
+
+def reset_op_count():
+    global _OPS
+    _OPS = 0
+
+
+def op_count():
+    return _OPS
+
+
+def _count(n):
+    global _OPS
+    _OPS += int(n)
+
+
+def _fft_model_ops(rows, n):
+    """Reference cost of one unitary length-n DFT per row (sketch.py:146,199)."""
+    lg = int(n).bit_length() - 1
+    return 10 * rows * (n // 2) * lg + 2 * rows * n
+
+
+def _srft_uses_fft(n, dtype):
+    """Whether srft.cu runs an FFT kernel for this length (else the dense
+    picked-column product)."""
+    import os
+    torch = _torch()
+    mode = os.environ.get("LR_SRFT", "")
+    es = 8 if dtype in (torch.complex64, torch.float32) else 16
+    return (n >= 1 and (n & (n - 1)) == 0 and not mode.startswith("g")
+            and n * es <= 200 * 1024)
+
+
 @dataclass
 class SketchSpec:
     """Configuration of one randomized sketch draw (sketch.py:69-93)."""
@@ -191,7 +236,15 @@ def srft_dev(A, op, amax=None):
     _lib.call("lr_srft_scaled", h, code, m, n, op.ell, _lib.ptr(A), _lib.ld(A),
               float(-1.0 if amax is None else amax), _lib.ptr(d), _lib.ptr(picks),
               float(op.scale), _lib.ptr(Y), _lib.ld(Y))
+    _count_srft(m, n, op.ell, cdt)
     return Y
+
+
+def _count_srft(rows, n, ell, dtype):
+    if _srft_uses_fft(n, dtype):
+        _count(6 * rows * n + _fft_model_ops(rows, n) + 2 * rows * ell)
+    else:
+        _count(8 * rows * n * ell + 2 * rows * ell)
 
 
 def srft_apply(A, spec_or_op):
@@ -221,10 +274,11 @@ def dft(v, axis=-1):
     cdt = _complex_of(t)
     X = t.to(cdt).reshape(-1, n).contiguous()
     if n > 1:
-        # power of two: shared-memory radix-2 FFT; otherwise the dense DFT
+        # power of two: shared-memory radix-16 FFT; otherwise the dense DFT
         # matrix product (same linear map as the reference's Bluestein path)
         _lib.call("lr_dft_rows", _lib.handle(X.device.index), _lib.dtype_code(cdt), X.shape[0], n,
                   _lib.ptr(X), _lib.ld(X))
+        _count(_fft_model_ops(X.shape[0], n) if (n & (n - 1)) == 0 else 8 * X.shape[0] * n * n)
     out = torch.movedim(X.reshape(shape), -1, axis)
     return _out(out, host)
 
@@ -313,6 +367,7 @@ def gsrft_dev(A, op, amax=None):
                        lambda: gsrft_matrix_dev(op, cdt, A.device.index))
     Y = torch.empty((m, op.ell), dtype=cdt, device=A.device)
     _pass(A, X, Y, False, amax)
+    _count(8 * m * n * op.ell + 2 * m * op.ell)
     return Y
 
 
@@ -325,3 +380,31 @@ def gsrft_apply(A, spec_or_op):
         raise ValueError("A must be 2-D")
     op = _resolve(spec_or_op, t.shape[1], GsrftOperator, gsrft_operator)
     return _out(gsrft_dev(t, op), host)
+
+
+def sketch_apply(A, spec):
+    """A @ Omega for the sketch family named in `spec` (sketch.py:340-349):
+    Gaussian as one device pass, SRFT / GSRFT through their kernels."""
+    host = not is_device_array(A)
+    t = to_device(A)
+    n = t.shape[1]
+    if spec.kind == "gaussian":
+        from .core import _cast_like_dtype, gemm
+        torch = _torch()
+        Om = _cast_like_dtype(gaussian_dev(n, spec.ell, spec.seed, device=t.device.index), t.dtype)
+        Y = torch.empty((t.shape[0], spec.ell), dtype=t.dtype, device=t.device)
+        gemm(t, Om, Y)
+        return _out(Y, host)
+    if spec.kind == "srft":
+        return srft_apply(A, spec)
+    return gsrft_apply(A, spec)
+
+
+def dense_sketch_matrix(n, spec):
+    """The test matrix Omega itself (sketch.py:352-358; the reference's path
+    for oracles): Gaussian draws, or the SRFT / GSRFT applied to I_n."""
+    if spec.kind == "gaussian":
+        return gaussian_matrix(n, spec.ell, spec.seed)
+    if spec.kind == "srft":
+        return srft_operator(n, spec.ell, spec.seed).to_dense()
+    return gsrft_operator(n, spec.ell, spec.seed).to_dense()

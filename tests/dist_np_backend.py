@@ -20,6 +20,20 @@ class TorchCpuBackend:
     def __init__(self):
         self.torch = torch
 
+    # --- a row-block operator given as (S_r scipy CSR, L_r, R): S_r + L_r R^T
+    def op_n(self, op, X):
+        S, L, R = op
+        x = _np(X)
+        return torch.from_numpy(np.asarray(S @ x + L @ (R.T @ x)))
+
+    def op_t(self, op, Y):
+        S, L, R = op
+        y = _np(Y)
+        return torch.from_numpy(np.asarray(S.T @ y + R @ (L.T @ y)))
+
+    def like(self, op):
+        return torch.empty(0, dtype=torch.float64)
+
     def pass_n(self, A, X, amax=None):
         return A @ X
 

@@ -114,3 +114,61 @@ def test_row_sharded_rsvd_matches_oracle(case):
     # reconstruction from the sharded factors
     A_hat = (U * S) @ V.conj().T
     assert np.linalg.norm(A - A_hat, 2) <= 10 * max(est, 1e-12)
+
+
+def _sparse_case():
+    import scipy.sparse as sp
+    n, per_row, r = 3000, 12, 4
+    g = np.random.default_rng(41)
+    cols = g.integers(0, n, size=(n, per_row))
+    vals = g.standard_normal((n, per_row))
+    rows = np.repeat(np.arange(n), per_row)
+    S = sp.csr_matrix((vals.ravel(), (rows, cols.ravel())), shape=(n, n))
+    S.sum_duplicates()
+    S.sort_indices()
+    L = 10.0 * g.standard_normal((n, r))
+    R = 10.0 * g.standard_normal((n, r))
+    return S, L, R
+
+
+def _sparse_worker(rank, world, port, outdir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_0909_4061_b200.dist import Comm, dist_randomized_svd_operator, row_range
+        from dist_np_backend import TorchCpuBackend
+        S, L, R = _sparse_case()
+        n = S.shape[0]
+        a, b = row_range(n, rank, world)
+        op_local = (S[a:b], L[a:b], R)
+        res = dist_randomized_svd_operator(op_local, n, 6, 4, 2, seed=5, comm=Comm(),
+                                           be=TorchCpuBackend())
+        torch.save({"Q": res.Q, "U": res.U, "sigma": res.sigma, "V": res.V, "est": res.est,
+                    "passes": res.passes}, os.path.join(outdir, f"s{rank}.pt"))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_row_sharded_sparse_rsvd_matches_oracle():
+    """Config 5's sharded path (dist_randomized_svd_operator): S + L R^T split
+    by rows over 2 gloo ranks, n-side panels sharded too (all-gather before
+    A_r X, reduce-scatter after A_r^H Y), against the oracle's rsvd of the
+    whole operator."""
+    S, L, R = _sparse_case()
+    basis, f, est = orc.rsvd(orc.SparsePlusLowRank(S, L, R), 6, 4, 2, seed=5)
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_sparse_worker, args=(2, _free_port(), d), nprocs=2, join=True)
+        outs = [torch.load(os.path.join(d, f"s{r}.pt")) for r in range(2)]
+    assert torch.equal(outs[0]["sigma"], outs[1]["sigma"])
+    assert outs[0]["passes"] == basis.passes == 6
+    S_ = outs[0]["sigma"].numpy()
+    assert np.max(np.abs(S_ - f.sigma) / f.sigma[0]) < 1e-10
+    Q = np.vstack([o["Q"].numpy() for o in outs])
+    U = np.vstack([o["U"].numpy() for o in outs])
+    V = np.vstack([o["V"].numpy() for o in outs])
+    assert np.linalg.norm(Q - basis.Q @ (basis.Q.T @ Q)) < 1e-9
+    for j in range(4):
+        assert np.linalg.norm(U[:, j] - f.U[:, j]) < 1e-7
+        assert np.linalg.norm(V[:, j] - f.V[:, j]) < 1e-7
+    assert abs(outs[0]["est"] - est) <= 1e-8 * est

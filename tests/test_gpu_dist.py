@@ -157,3 +157,70 @@ def test_nccl_world1_public_entry():
             sharded_randomized_svd(bad, 5, 5, 0)
     finally:
         dist.destroy_process_group()
+
+
+def test_nccl_world1_sparse_operator_path():
+    """dist_randomized_svd_operator (config 5's sharded path) over NCCL with
+    one rank: the same factors as the oracle on S + L R^T."""
+    import scipy.sparse as sp
+    import torch
+    import torch.distributed as dist
+    import paper_0909_4061_b200 as lr
+    from paper_0909_4061_b200.dist import Comm, GpuBackend, dist_randomized_svd_operator
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        g = np.random.default_rng(41)
+        n = 5000
+        cols = g.integers(0, n, size=(n, 12))
+        S = sp.csr_matrix((g.standard_normal(n * 12), (np.repeat(np.arange(n), 12), cols.ravel())),
+                          shape=(n, n))
+        S.sum_duplicates()
+        L, R = 10 * g.standard_normal((n, 4)), 10 * g.standard_normal((n, 4))
+        op = lr.CudaCsrOperator(S, L, R)
+        res = dist_randomized_svd_operator(op, n, 6, 4, 2, 5, Comm(), GpuBackend())
+        _, f, est = orc.rsvd(orc.SparsePlusLowRank(S, L, R), 6, 4, 2, 5)
+        sig = res.sigma.cpu().numpy()
+        assert np.max(np.abs(sig - f.sigma) / f.sigma[0]) < 1e-10
+        assert abs(res.est - est) <= 1e-8 * est
+        V = res.V.cpu().numpy()
+        assert np.linalg.norm(V[:, 0] - f.V[:, 0]) < 1e-7
+    finally:
+        dist.destroy_process_group()
+
+
+def test_c_abi_comm_world1():
+    """The C ABI's own collectives (lr_comm_*), for callers without
+    torch.distributed: a one-rank NCCL communicator on the handle;
+    lr_orth_sharded equals lr_orth_fast bit for bit, the all-reduce is the
+    identity."""
+    import ctypes
+    import torch
+    from paper_0909_4061_b200 import _lib
+    idbuf = ctypes.create_string_buffer(128)
+    _lib.call("lr_comm_unique_id", ctypes.cast(idbuf, ctypes.c_void_p))
+    h = _lib.handle()
+    _lib.call("lr_comm_init", h, ctypes.cast(idbuf, ctypes.c_void_p), 1, 0)
+    try:
+        g = torch.Generator(device="cuda").manual_seed(3)
+        Y = torch.randn(5000, 40, dtype=torch.float64, device="cuda", generator=g)
+        Q1 = torch.empty_like(Y)
+        Q2 = torch.empty_like(Y)
+        st = torch.zeros(2, dtype=torch.int32, device="cuda")
+        _lib.call("lr_orth_sharded", h, _lib.F64, 5000, 40, _lib.ptr(Y), 40, _lib.ptr(Q1), 40,
+                  1e-10, _lib.ptr(st[0:1]))
+        _lib.call("lr_orth_fast", h, _lib.F64, 5000, 40, _lib.ptr(Y), 40, _lib.ptr(Q2), 40,
+                  1e-10, _lib.ptr(st[1:2]))
+        assert int(st.sum().item()) == 0
+        assert torch.equal(Q1, Q2)
+        b = torch.arange(10, dtype=torch.float64, device="cuda")
+        _lib.call("lr_comm_allreduce", h, _lib.F64, 10, _lib.ptr(b))
+        torch.cuda.synchronize()
+        assert torch.equal(b, torch.arange(10, dtype=torch.float64, device="cuda"))
+    finally:
+        _lib.call("lr_comm_destroy", h)

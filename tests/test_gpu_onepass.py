@@ -83,7 +83,8 @@ def test_streamed_bundle_vs_reference(golden, tmp_path, tag, br, ell):
     lio.write_matrix_binary(A, p)
     assert np.array_equal(np.frombuffer(p.read_bytes()[:64], dtype=np.uint8), g[f"{tag}_bytes"])
     sb = lio.streamed_sample_bundle(lio.stream_row_blocks(p, br), ell=ell, seed=4)
-    assert np.array_equal(sb.Omega, g[f"{tag}_Om"]) and np.array_equal(sb.Omega_tilde, g[f"{tag}_Omt"])
+    assert np.abs(sb.Omega - g[f"{tag}_Om"]).max() <= 4e-16 * np.abs(g[f"{tag}_Om"]).max()
+    assert np.abs(sb.Omega_tilde - g[f"{tag}_Omt"]).max() <= 4e-16 * np.abs(g[f"{tag}_Omt"]).max()
     scale = np.abs(A).max() * A.shape[1]
     assert np.abs(sb.Y - g[f"{tag}_Y"]).max() <= 1e-13 * scale
     assert np.abs(sb.Y_tilde - g[f"{tag}_Yt"]).max() <= 1e-13 * np.abs(A).max() * A.shape[0]
@@ -143,6 +144,9 @@ def test_streamed_large_blocks_device_accumulation(tmp_path):
     lio.write_matrix_binary(A, p)
     sb = lio.streamed_sample_bundle(lio.stream_row_blocks(p, 10000), ell=24, ell_tilde=20, seed=7)
     Om, Omt = O.gaussian_matrix(n, 24, 7), O.gaussian_matrix(m, 20, 8)
-    assert np.array_equal(sb.Omega, Om) and np.array_equal(sb.Omega_tilde, Omt)
+    # the device generator matches numpy's stream to the last ulp on rare
+    # ziggurat tail draws (tests/test_gpu_kernels.py)
+    assert np.abs(sb.Omega - Om).max() <= 4e-16 * np.abs(Om).max()
+    assert np.abs(sb.Omega_tilde - Omt).max() <= 4e-16 * np.abs(Omt).max()
     assert np.abs(sb.Y - A @ Om).max() <= 1e-12 * n
     assert np.abs(sb.Y_tilde - A.T @ Omt).max() <= 1e-12 * m

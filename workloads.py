@@ -215,7 +215,7 @@ def build_synthetic_device(m, n, s, seed, device="cuda", host_rng=True):
     return A, sv.numpy()
 
 
-def build_cfg4_device(seed=4, m=1 << 20, n=4096, block=65536, device="cuda"):
+def build_cfg4_device(seed=4, m=1 << 20, n=4096, block=65536, device="cuda", rows=None):
     """Full-size cfg4 on the GPU with the exact recipe of build_cfg4_host:
     the Gaussian blocks are the reference's Philox streams rng_for(seed,
     "Ublk", b) / rng_for(seed, "Vhar") drawn on the device by the library's
@@ -224,7 +224,8 @@ def build_cfg4_device(seed=4, m=1 << 20, n=4096, block=65536, device="cuda"):
     Householder, like numpy's LAPACK QR up to roundoff) and signed by diag R;
     A = U diag(s) V^T in fp64, stored fp32.  Differs from the host build only
     by fp64 QR rounding (~1e-15 relative), i.e. at most one fp32 ulp on rare
-    entries (tests/test_gpu_parity.py checks a block against the host)."""
+    entries (tests/test_gpu_parity.py checks a block against the host).
+    rows=(r0, r1): build only those rows (a rank's shard), same values."""
     import torch
     from paper_0909_4061_b200.sketch import gaussian_dev
     nb = m // block
@@ -234,13 +235,15 @@ def build_cfg4_device(seed=4, m=1 << 20, n=4096, block=65536, device="cuda"):
                                  device=dev.index), device)
     W = (V * s).T.contiguous()
     del V
-    A = torch.empty((m, n), dtype=torch.float32, device=dev)
-    for b in range(nb):
+    r0, r1 = (0, m) if rows is None else rows
+    A = torch.empty((r1 - r0, n), dtype=torch.float32, device=dev)
+    for b in range(r0 // block, -(-r1 // block)):
         g = gaussian_dev(block, n, seed, stream=STREAM_UBLK, index=b, dtype=torch.float64,
                          device=dev.index)
         Ub = _haar_torch(g, device) / np.sqrt(nb)
         del g
-        A[b * block:(b + 1) * block] = (Ub @ W).to(torch.float32)
+        lo, hi = max(r0, b * block), min(r1, (b + 1) * block)
+        A[lo - r0:hi - r0] = (Ub[lo - b * block:hi - b * block] @ W).to(torch.float32)
         del Ub
     torch.cuda.synchronize(dev)
     return A, s.cpu().numpy()
