@@ -329,6 +329,18 @@ int lr_max_abs_imag(lr_handle_t h, int dtype, int64_t m, int64_t n, const void* 
 int lr_gaussian(lr_handle_t h, uint64_t key_lo, uint64_t key_hi, int64_t count, int dtype,
                 void* out, int32_t* status);
 
+/* Row interpolative decomposition M ~= X M[J, :] (reference row_id /
+ * _column_id, factor.py:198-246, with the Businger-Golub pivoted QR of
+ * core.py:133-186): M m x ncols (float64 / complex128, row-major, ldm),
+ * k <= ncols skeleton rows, perm
+ * (device int32, m): out = the column order of B = M^H (perm[:k] = J);
+ * forced = 1 takes perm as the given order (the Gu-Eisenstat refinement's
+ * recomputation).  X m x k (ldx): X[J] = I, X[free] = (R11^{-1} R12)^H with
+ * truncated back substitution (rows |r_ii| <= 1e-12 max give zero);
+ * *tmax (device double) = max |X[free]|, the refinement test. */
+int lr_row_id(lr_handle_t h, int dtype, int64_t m, int64_t ncols, int64_t k, const void* M,
+              int64_t ldm, int32_t* perm, int forced, void* X, int64_t ldx, double* tmax);
+
 /* Collectives for the row-sharded path without torch.distributed (SURVEY.md
  * §8b/§8e; reference analogue: the row-block sums of
  * accumulate_two_sided_samples, io.py:364-388, turned into all-reduces).

@@ -958,3 +958,97 @@ def eig_one_pass(bundle):
         diagnostics["ill_conditioned"] = True
     V, lam = small_eig_hermitian(B)
     return PartialEig(U=Q @ V, lam=lam, diagnostics=diagnostics)
+
+
+# ---------------------------------------------------------------------------
+# Interpolative decomposition and row extraction (reference factor.py:198-296)
+
+def pivoted_qr_full(A, max_rank=None):
+    """Businger-Golub column-pivoted Householder QR, norms recomputed every
+    step, ties to the lowest position (core.py:133-186): (Rp in pivoted
+    order k x n with a real nonnegative diagonal, perm)."""
+    W = np.array(A, dtype=np.complex128 if np.iscomplexobj(A) else np.float64)
+    m, n = W.shape
+    steps = min(m, n) if max_rank is None else min(max_rank, m, n)
+    perm = np.arange(n)
+    for j in range(steps):
+        norms = np.linalg.norm(W[j:, j:], axis=0)
+        piv = int(np.argmax(norms)) + j
+        if piv != j:
+            W[:, [j, piv]] = W[:, [piv, j]]
+            perm[[j, piv]] = perm[[piv, j]]
+        x = W[j:, j]
+        xnorm = np.linalg.norm(x)
+        if xnorm > 0:
+            ph = x[0] / abs(x[0]) if abs(x[0]) > 0 else 1.0
+            v = x.copy()
+            v[0] += ph * xnorm
+            vnorm = np.linalg.norm(v)
+            if vnorm > 0:
+                v = v / vnorm
+                W[j:, j:] -= 2.0 * np.outer(v, v.conj() @ W[j:, j:])
+    Rp = np.triu(W[:steps, :])
+    d = np.diagonal(Rp)
+    ph = np.ones_like(d)
+    nz = np.abs(d) > 0
+    ph[nz] = d[nz] / np.abs(d[nz])
+    Rp = Rp * np.conj(ph)[:, None]
+    return Rp, perm
+
+
+def _column_id(B, k, trunc_tol=TRIANGULAR_TRUNC_TOL):
+    """factor.py:198-229 (with the Gu-Eisenstat refinement)."""
+    B = np.asarray(B)
+    n = B.shape[1]
+    Rp, perm0 = pivoted_qr_full(B, max_rank=k)
+    perm = list(perm0)
+    cap = max(int(3 * k * math.log(max(n, 2))), 8)
+
+    def coefficients(order):
+        R = np.linalg.qr(B[:, order], mode="r")
+        return solve_triangular_trunc(R[:k, :k], R[:k, k:], trunc_tol=trunc_tol)
+
+    T = solve_triangular_trunc(Rp[:k, :k], Rp[:k, k:], trunc_tol=trunc_tol)
+    swaps = 0
+    while T.size and np.abs(T).max() > 2.0 * (1.0 + 1e-12):
+        i, j = np.unravel_index(int(np.argmax(np.abs(T))), T.shape)
+        perm[i], perm[k + j] = perm[k + j], perm[i]
+        T = coefficients(perm)
+        swaps += 1
+        if swaps > cap:
+            raise RuntimeError("interpolative decomposition refinement did not settle")
+    return np.asarray(perm[:k]), np.asarray(perm[k:]), T
+
+
+def row_id(M, k):
+    """factor.py:232-246: M ~= X M[J, :]."""
+    M = np.asarray(M)
+    J, free, T = _column_id(M.conj().T, k)
+    X = np.zeros((M.shape[0], k), dtype=np.promote_types(T.dtype, M.dtype))
+    X[J, :] = np.eye(k)
+    X[free, :] = T.conj().T
+    return J, X
+
+
+def householder_qr(A):
+    """core.py:67-81 (economy, diagonal of R real nonnegative)."""
+    Q, R = np.linalg.qr(np.asarray(A), mode="reduced")
+    k = min(np.shape(A))
+    d = np.diagonal(R)[:k]
+    ph = np.ones_like(d)
+    nz = np.abs(d) > 0
+    ph[nz] = d[nz] / np.abs(d[nz])
+    Q[:, :k] *= ph
+    R[:k, :] *= np.conj(ph)[:, None]
+    return Q, R
+
+
+def svd_via_row_extraction(A, QorY):
+    """factor.py:267-281."""
+    A = np.asarray(A)
+    QorY = np.asarray(QorY)
+    k = QorY.shape[1]
+    J, X = row_id(QorY, k)
+    W, Rh = householder_qr(A[J, :].conj().T)
+    f = small_svd(X @ Rh.conj().T)
+    return PartialSVD(U=f.U, sigma=f.sigma, V=W @ f.V)

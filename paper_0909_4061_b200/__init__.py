@@ -17,8 +17,10 @@ from . import config
 from ._lib import ConvergenceError, LibraryMissing, NotPSDError
 from .core import (CudaDenseOperator, DenseOperator, MatVecOperator, OperatorCounters, SmallSVD,
                    as_operator, orthonormalize_double_gs, small_eig_hermitian, small_svd)
-from .factor import (NystromFactors, PartialEig, PartialSVD, SampleBundle, direct_eig_hermitian,
-                     direct_svd, eig_nystrom, eig_one_pass, randomized_svd, sample_bundle,
+from .factor import (InterpolativeDecomp, NystromFactors, PartialEig, PartialSVD, SampleBundle,
+                     column_id, direct_eig_hermitian, direct_svd, eig_nystrom, eig_one_pass,
+                     eig_via_row_extraction, randomized_svd, row_id, sample_bundle,
+                     svd_via_row_extraction,
                      sample_bundle_two_sided, stage_a, svd_one_pass_general, svd_single_pass,
                      truncate_rank)
 from .io import (MatrixFormatError, RowBlockStream, StreamError, accumulate_two_sided_samples,

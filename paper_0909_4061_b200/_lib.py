@@ -85,6 +85,7 @@ _SIGS = {
     "lr_axpy_add": [_vp, _int, _i64, _i64, _vp, _i64, _vp, _i64],
     "lr_sylvester_div": [_vp, _int, _i64, _i64, _vp, _i64, _vp, _vp, C.c_double],
     "lr_col_sumsq": [_vp, _int, _i64, _i64, _vp, _i64, _vp],
+    "lr_row_id": [_vp, _int, _i64, _i64, _i64, _vp, _i64, _vp, _int, _vp, _i64, _vp],
     "lr_comm_unique_id": [_vp],
     "lr_comm_init": [_vp, _vp, _int, _int],
     "lr_comm_destroy": [_vp],

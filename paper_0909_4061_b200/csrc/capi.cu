@@ -933,6 +933,19 @@ int lr_orth_fast_deferred(lr_handle_t hh, int dtype, int64_t m, int64_t ell, con
   API_END
 }
 
+int lr_row_id(lr_handle_t hh, int dtype, int64_t m, int64_t ncols, int64_t k, const void* M,
+              int64_t ldm, int32_t* perm, int forced, void* X, int64_t ldx, double* tmax) {
+  API_BEGIN
+  Handle* h = H(hh);
+  lr::DeviceGuard dg_(h->device);
+  LR_REQUIRE(dtype == LR_F64 || dtype == LR_C128, LR_EINVAL, "lr_row_id: float64 / complex128");
+  LR_REQUIRE(m >= 1 && k >= 1 && k <= m && k <= ncols && ldm >= ncols && ldx >= k, LR_EINVAL,
+             "lr_row_id: bad shape");
+  lr::pool_reset(h);
+  lr::row_id(h, dtype, m, ncols, k, M, ldm, perm, forced, X, ldx, tmax);
+  API_END
+}
+
 int lr_comm_unique_id(void* id_out) {
   API_BEGIN
   LR_REQUIRE(id_out != nullptr, LR_EINVAL, "lr_comm_unique_id: null output");

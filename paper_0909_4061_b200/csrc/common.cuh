@@ -331,6 +331,10 @@ void srft_c128(Handle* h, int64_t m, int64_t n, int64_t ell, const double2* A, i
                const double2* d, const int32_t* picks, double scale, double2* Y, int64_t ldy);
 void dft_rows(Handle* h, int dtype, int64_t rows, int64_t n, void* X, int64_t ldx);
 
+// rowid.cu: row interpolative decomposition (pivoted-QR skeleton + T)
+void row_id(Handle* h, int dtype, int64_t m, int64_t kc, int64_t k, const void* M, int64_t ldm,
+            int32_t* perm, int forced, void* X, int64_t ldx, double* tmax_dev);
+
 // gauss.cu ----------------------------------------------------------------------
 // first `count` draws of numpy Generator(Philox(key)).standard_normal
 void gaussian_stream(Handle* h, uint64_t key_lo, uint64_t key_hi, int64_t count, int out_dtype,

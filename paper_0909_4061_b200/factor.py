@@ -15,6 +15,7 @@ problems on the device; io.py accumulates the same bundles from row blocks.
 
 from __future__ import annotations
 
+import math
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -420,6 +421,131 @@ def eig_one_pass(bundle):
     V, lam = small_eig_hermitian_dev(B)
     U = _mm(Q, V)
     return PartialEig(U=_out(U, host), lam=_out(lam, host), diagnostics=diagnostics)
+
+
+# ---------------------------------------------------------------------------
+# interpolative decomposition and row extraction (reference factor.py:198-296)
+
+@dataclass
+class InterpolativeDecomp:
+    """Index skeleton plus bounded interpolation coefficients
+    (factor.py:65-75): row form M ~= X M[J, :] (X[J] = I, |X| <= 2); column
+    form M ~= M[:, J] X."""
+
+    J: object
+    X: object
+    side: str
+
+
+def _row_id_dev(M, k):
+    """Row ID of a device matrix M (m x k_cols) on the device (lr_row_id):
+    the pivoted-QR skeleton, then the Gu-Eisenstat refinement of
+    factor.py:213-229 -- while some |T| exceeds 2 the offending skeleton and
+    free rows are swapped and the coefficients recomputed from the QR of the
+    reordered B = M^H (the forced-order mode), at most
+    max(3 k log(max(m, 2)), 8) swaps.  Returns (J int64 device, X)."""
+    torch = _torch()
+    m = M.shape[0]
+    if not 1 <= k <= min(M.shape):
+        raise ValueError("k must satisfy 1 <= k <= min(m, n)")
+    wd = _wide(M.dtype)
+    Mw = cast_dev(M, wd).contiguous()
+    h = _lib.handle(Mw.device.index)
+    perm = torch.empty(m, dtype=torch.int32, device=Mw.device)
+    X = torch.empty((m, k), dtype=wd, device=Mw.device)
+    tmax = torch.zeros(1, dtype=torch.float64, device=Mw.device)
+    code = _lib.dtype_code(wd)
+    _lib.call("lr_row_id", h, code, m, Mw.shape[1], k, _lib.ptr(Mw), _lib.ld(Mw), _lib.ptr(perm),
+              0, _lib.ptr(X), _lib.ld(X), _lib.ptr(tmax))
+    cap = max(int(3 * k * math.log(max(m, 2))), 8)
+    swaps = 0
+    while float(tmax.item()) > 2.0 * (1.0 + 1e-12):
+        free = perm[k:].long()
+        T = X[free].abs().T.contiguous()               # k x (m - k), as the reference's T
+        flat = int(torch.argmax(T.reshape(-1)).item())
+        i, j = divmod(flat, m - k)
+        a, b = int(perm[i].item()), int(perm[k + j].item())
+        perm[i], perm[k + j] = b, a
+        _lib.call("lr_row_id", h, code, m, Mw.shape[1], k, _lib.ptr(Mw), _lib.ld(Mw),
+                  _lib.ptr(perm), 1, _lib.ptr(X), _lib.ld(X), _lib.ptr(tmax))
+        swaps += 1
+        if swaps > cap:
+            raise RuntimeError("interpolative decomposition refinement did not settle")
+    return perm[:k].long(), X
+
+
+def row_id(M, k):
+    """Row interpolative decomposition M ~= X @ M[J, :] (factor.py:232-246):
+    X holds the k x k identity on the selected rows and no entry larger than
+    2 after refinement."""
+    host = not is_device_array(M)
+    Md = to_device(M)
+    J, X = _row_id_dev(Md, k)
+    J, X = _outs(host, J, X)
+    return InterpolativeDecomp(J=J, X=X, side="row")
+
+
+def column_id(M, k):
+    """Column interpolative decomposition M ~= M[:, J] @ X (factor.py:249-258),
+    as the row ID of M^H."""
+    host = not is_device_array(M)
+    Md = to_device(M)
+    J, X = _row_id_dev(_ct(cast_dev(Md, _wide(Md.dtype)).contiguous()), k)
+    Xc = _ct(X)
+    J, Xc = _outs(host, J, Xc)
+    return InterpolativeDecomp(J=J, X=Xc, side="column")
+
+
+def _qr_pos_dev(Y):
+    """Q R of a tall device matrix with R's diagonal real positive (the
+    reference householder_qr, core.py:67-81, for full column rank): Q by
+    CholeskyQR2 without drops, R = Q^H Y."""
+    Q = orth_dev(Y, 0.0)
+    if Q.shape[1] != Y.shape[1]:
+        raise ValueError("QR of a numerically rank-deficient panel")
+    return Q, _mm(Q, Y, ha=True)
+
+
+def svd_via_row_extraction(A, QorY):
+    """Partial SVD touching only k rows of A (factor.py:267-281): row ID of
+    the basis (or the raw samples), W R = QR of A[J, :]^H, Z = X R^H, small
+    SVD of Z, V = W V_Z.  All on the device."""
+    torch = _torch()
+    host = not is_device_array(A) and not is_device_array(QorY)
+    Ad = to_device(A)
+    Bd = to_device(QorY)
+    if Bd.dim() == 1:
+        Bd = Bd.reshape(-1, 1)
+    k = Bd.shape[1]
+    J, X = _row_id_dev(Bd, k)
+    (Aw,), wd = _dev_wide(Ad)
+    rows = Aw.index_select(0, J).contiguous()              # k x n
+    W, Rh = _qr_pos_dev(_ct(rows))                          # rows^H = W Rh
+    Z = _mm(cast_dev(X, wd).contiguous(), _ct(Rh))          # m x k
+    U, S, Vz = small_svd_dev(Z)
+    V = _mm(W, Vz)
+    del torch
+    return PartialSVD(*_outs(host, U, S, V))
+
+
+def eig_via_row_extraction(A, QorY):
+    """Hermitian eigendecomposition touching only the (J, J) block of A
+    (factor.py:284-296): row ID, V R = QR of X, Z = R A[J, J] R^H, eigenpairs
+    of Z, U = V W."""
+    host = not is_device_array(A) and not is_device_array(QorY)
+    Ad = to_device(A)
+    Bd = to_device(QorY)
+    if Bd.dim() == 1:
+        Bd = Bd.reshape(-1, 1)
+    k = Bd.shape[1]
+    J, X = _row_id_dev(Bd, k)
+    (Aw,), wd = _dev_wide(Ad)
+    AJJ = Aw.index_select(0, J).index_select(1, J).contiguous()
+    V, R = _qr_pos_dev(cast_dev(X, wd).contiguous())
+    Z = _mm(_mm(R, AJJ), _ct(R))
+    Wz, lam = small_eig_hermitian_dev(Z)
+    U = _mm(V, cast_dev(Wz, wd))
+    return PartialEig(U=_out(U, host), lam=_out(lam, host))
 
 
 def truncate_rank(f, k):

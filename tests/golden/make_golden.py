@@ -292,7 +292,56 @@ def g_onepass():
     save("onepass", **out)
 
 
-ALL = {"onepass": g_onepass, "kats": g_kats, "stageb": g_stageb, "cfg1": g_cfg1, "cfg3": g_cfg3, "cfg4s": g_cfg4s, "cfg5s": g_cfg5s,
+def g_rowid():
+    """Interpolative decomposition and row extraction (reference
+    factor.py:198-296, pivoted QR core.py:133-186)."""
+    from lowrank.oracle import synthetic_psd
+    out = {}
+    cases = {"small": np.array([[1.0, 0.0], [0.0, 1.0], [1.0, 1.0]]),
+             "dup": np.array([[1.0, 2.0], [1.0, 2.0], [0.0, 1.0]])}
+    rng = np.random.default_rng(4)
+    for t in range(12):
+        cases[f"rand{t}"] = rng.standard_normal((25, 6))
+    rng = np.random.default_rng(5)
+    cases["lowrank"] = rng.standard_normal((15, 3)) @ rng.standard_normal((3, 8))
+    rng = np.random.default_rng(7)
+    cases["cplx"] = rng.standard_normal((14, 4)) + 1j * rng.standard_normal((14, 4))
+    rng = np.random.default_rng(3)
+    cases["tall"] = np.linalg.qr(rng.standard_normal((3000, 40)))[0]
+    ks = {"small": 2, "dup": 2, "lowrank": 5}
+    for name, M in cases.items():
+        k = ks.get(name, M.shape[1])
+        f = factor.row_id(M, k)
+        if name == "tall":      # regenerated by the tests (same rng, numpy QR)
+            out["rid_tall_J"], out["rid_tall_Xhead"] = f.J, f.X[:64]
+            continue
+        out[f"rid_{name}_M"], out[f"rid_{name}_J"], out[f"rid_{name}_X"] = M, f.J, f.X
+    rng = np.random.default_rng(6)
+    M = rng.standard_normal((12, 4)) @ rng.standard_normal((4, 18))
+    c = factor.column_id(M, 4)
+    out.update(cid_M=M, cid_J=c.J, cid_X=c.X)
+    A, _ = synthetic_matrix(SyntheticSpec(m=30, n=25, kind="exact_rank", param=5, seed=8))
+    b = rangefinder.randomized_range_finder(core.DenseOperator(A), 5, seed=1)
+    f = factor.svd_via_row_extraction(A, b.Q)
+    out.update(sre_A=A, sre_Q=b.Q, sre_sigma=f.sigma, sre_comp=f.compose())
+    rng = np.random.default_rng(9)
+    A = rng.standard_normal((50, 50))
+    b = rangefinder.randomized_range_finder(core.DenseOperator(A), 8, seed=3)
+    f = factor.svd_via_row_extraction(A, b.Q)
+    out.update(sre2_A=A, sre2_Q=b.Q, sre2_sigma=f.sigma, sre2_comp=f.compose())
+    rng = np.random.default_rng(11)
+    A = rng.standard_normal((30, 30))
+    Y = A @ rng.standard_normal((30, 6))
+    f = factor.svd_via_row_extraction(A, Y)
+    out.update(sre3_A=A, sre3_Y=Y, sre3_sigma=f.sigma, sre3_comp=f.compose())
+    H, _ = synthetic_psd(30, "exact_rank", 5, seed=14)
+    b = rangefinder.randomized_range_finder(core.DenseOperator(H), 5, seed=2)
+    f = factor.eig_via_row_extraction(H, b.Q)
+    out.update(ere_H=H, ere_Q=b.Q, ere_lam=f.lam, ere_comp=f.compose())
+    save("rowid", **out)
+
+
+ALL = {"rowid": g_rowid, "onepass": g_onepass, "kats": g_kats, "stageb": g_stageb, "cfg1": g_cfg1, "cfg3": g_cfg3, "cfg4s": g_cfg4s, "cfg5s": g_cfg5s,
        "cfg2": g_cfg2}
 
 if __name__ == "__main__":

@@ -190,3 +190,18 @@ def test_oracle_one_pass_and_streaming(golden, tmp_path):
         assert np.array_equal(sb.Omega, g[f"{tag}_Om"])
         assert np.array_equal(sb.Y, g[f"{tag}_Y"]) and np.array_equal(sb.Y_tilde, g[f"{tag}_Yt"])
         assert np.abs(sb.Q - g[f"{tag}_Q"]).max() <= 1e-13
+
+
+def test_oracle_row_id_and_extraction(golden):
+    """The oracle's interpolative decomposition / row extraction against the
+    reference's outputs (tests/golden/rowid.npz)."""
+    g = golden("rowid")
+    ks = {"small": 2, "dup": 2, "lowrank": 5}
+    names = sorted({k[4:-2] for k in g if k.startswith("rid_") and k.endswith("_M")})
+    for name in names:
+        M = g[f"rid_{name}_M"]
+        J, X = O.row_id(M, ks.get(name, M.shape[1]))
+        assert np.array_equal(J, g[f"rid_{name}_J"]), name
+        assert np.abs(X - g[f"rid_{name}_X"]).max() <= 1e-10, name
+    f = O.svd_via_row_extraction(g["sre2_A"], g["sre2_Q"])
+    assert np.abs(f.sigma - g["sre2_sigma"]).max() <= 1e-10 * g["sre2_sigma"][0]
