@@ -93,6 +93,12 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(map),
+               "r"(c0), "r"(c1)
+               : "memory");
+}
+
 // canonical K-major SWIZZLE_64B UMMA smem descriptor (rows of 64 B, 8-row
 // groups 512 B apart; sm100 descriptor version 1)
 __device__ __forceinline__ uint64_t desc_sw64(const void* p) {
@@ -512,7 +518,11 @@ constexpr int W_AH = WBM * TBK * 2;       // 16 KB (one of hi / lo)
 #define LR_W_TS3 2
 #endif
 constexpr int W_TS1 = LR_W_TS1;
-constexpr int64_t W_KMAX = 4096;   // k-extent of one TMEM accumulator (see gemm_f32_m256)
+constexpr int64_t W_KMAX = 4096;
+#ifndef LR_W_PF
+#define LR_W_PF 0      // measured: 0 / 3 / 6 / 12 stages ahead -> 5.50 / 5.67 / 5.71 / 6.47 ms
+#endif
+constexpr int W_PF = LR_W_PF;      // A stages prefetched into L2 ahead of the ring   // k-extent of one TMEM accumulator (see gemm_f32_m256)
 constexpr int W_TS2 = LR_W_TS2;
 constexpr int W_TS3 = LR_W_TS3;
 
@@ -583,7 +593,17 @@ gemm_f32_m256_kernel(const __grid_constant__ CUtensorMap mapA,
 
   if (warp == 0) {
     if (lane == 0) {
+      // the fp32 ring holds only W_TS1 stages (32 KB each): A tiles further
+      // ahead are prefetched into L2 so the ring's loads see L2, not HBM,
+      // latency (the A stream needs ~40 GB/s per SM at the UMMA rate)
+      auto prefetch = [&](int kt) {
+        const int kc = int(kbeg + int64_t(kt) * TBK);
+        if (!TRANS) tma_prefetch_2d(&mapA, kc, m0);
+        else        tma_prefetch_2d(&mapA, m0, kc);
+      };
+      for (int kt = 0; kt < W_PF && kt < nk; ++kt) prefetch(kt);
       for (int kt = 0; kt < nk; ++kt) {
+        if (W_PF > 0 && kt + W_PF < nk) prefetch(kt + W_PF);
         const int s = kt % W_TS1;
         mbar_wait(&a32_empty[s], (uint32_t(kt / W_TS1) & 1u) ^ 1u);
         mbar_expect_tx(&a32_full[s], W_A32);
