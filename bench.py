@@ -310,8 +310,9 @@ def run_ours(args, cfg):
 
 
 def roofline_sparse(cfg, pev, ms, steps, passes):
-    """Config 5: the dominant kernel is the CSR SpMM (K6), HBM/gather bound;
-    achieved = gather-inclusive algorithmic bytes per launch / launch time."""
+    """Config 5: the dominant kernel is the CSR SpMM (K6), HBM bound;
+    achieved = compulsory bytes per launch (CSR arrays, X once, Y) / launch
+    time."""
     pk, src = peaks()
     t = [a.elapsed_time(b) for a, b, *_ in pev]
     nbytes = [x for _, _, _, x, _ in pev]
@@ -324,9 +325,11 @@ def roofline_sparse(cfg, pev, ms, steps, passes):
         traffic = json.load(open(tpath)).get(f"cfg{cfg.idx}")
     return {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
             "frac": round(achieved / hbm, 4), "traffic": traffic,
-            "kernel": "csr_spmm_kernel (K6), gather-inclusive bytes model",
+            "kernel": "csr_spmm (K6: repack + L2-resident column slices), compulsory bytes model",
             "peak_source": f"{src} HBM copy bandwidth (MEASURED_PEAKS.json)",
             "avg_spmm_ms": round(avg_ms, 4),
+            "dram_frac_measured_traffic": (round(traffic / (avg_ms / 1e3) / 1e9 / hbm, 4)
+                                           if traffic else None),
             "spmm_share_of_step": round(sum(t) / (ms * steps), 4)}
 
 
@@ -346,8 +349,13 @@ def roofline(A, cfg, pev, ms, steps, passes, a_bytes):
         peak_tf = measured_fp64_peak()
         peak_src = "measured in-run: cuBLAS DGEMM 8192^3 (torch.matmul)"
     else:
-        peak_tf = pk["bf16_tflops"]
-        peak_src = f"{src} bf16 (MEASURED_PEAKS.json)"
+        # burst figure for a pass in a short step, the sustained one for a
+        # pass inside a long step (config 4: 4 x 5.5 ms of back-to-back
+        # tensor work per step; the clocks drop to ~1.3 GHz under that load,
+        # profiles/round2_m256_pass_summary.md)
+        long_step = ms >= 10.0 and "bf16_tflops_sustained" in pk
+        peak_tf = pk["bf16_tflops_sustained"] if long_step else pk["bf16_tflops"]
+        peak_src = (f"{src} bf16 {'sustained' if long_step else 'burst'} (MEASURED_PEAKS.json)")
     achieved_tf = avg_flops / (avg_pass_ms / 1e3) / 1e12
     hbm = pk["hbm_gbs"]
     # per-pass roofline: max(flops / tensor peak, bytes(A) / HBM)
@@ -411,6 +419,7 @@ def roofline(A, cfg, pev, ms, steps, passes, a_bytes):
                 "peak_source": peak_src, "avg_pass_ms": round(avg_pass_ms, 4),
                 "algorithmic_tflops": round(achieved_tf, 3),
                 "issued_flops_per_pass": issued,
+                "frac_of_burst_peak": round(ach3 / pk["bf16_tflops"], 4),
                 "pass_a_gbs": round(a_bytes / (avg_pass_ms / 1e3) / 1e9, 1),
                 "hbm_frac": round(a_bytes / (avg_pass_ms / 1e3) / 1e9 / hbm, 4),
                 "step_roofline_ms": round(roof_step_ms, 4),

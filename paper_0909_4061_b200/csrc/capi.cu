@@ -1133,9 +1133,8 @@ int lr_csr_spmm(lr_handle_t hh, int dtype, int64_t m, int64_t n, int64_t ell,
   Handle* h = H(hh);
   lr::DeviceGuard dg_(h->device);
   LR_REQUIRE(dtype == LR_F64, LR_EUNSUPPORTED, "lr_csr_spmm: fp64 only");
-  (void)n;
   lr::pool_reset(h);
-  lr::csr_spmm_f64(h, m, ell, rowptr, colidx, static_cast<const double*>(vals),
+  lr::csr_spmm_f64(h, m, n, ell, rowptr, colidx, static_cast<const double*>(vals),
                    static_cast<const double*>(X), ldx, static_cast<double*>(Y), ldy,
                    accumulate != 0);
   API_END

@@ -341,7 +341,7 @@ void gaussian_stream(Handle* h, uint64_t key_lo, uint64_t key_hi, int64_t count,
                      void* out);
 
 // spmm.cu -----------------------------------------------------------------------
-void csr_spmm_f64(Handle* h, int64_t m, int64_t ell, const int64_t* rowptr,
+void csr_spmm_f64(Handle* h, int64_t m, int64_t n, int64_t ell, const int64_t* rowptr,
                   const int32_t* colidx, const double* vals, const double* X, int64_t ldx,
                   double* Y, int64_t ldy, bool accumulate);
 

@@ -9,7 +9,9 @@
 // (each gather is a contiguous 8*ell-byte row of X).  The transpose product
 // uses the CSR of S^T (built once by the operator), so no atomics are needed
 // and the result is deterministic.
+#include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 
@@ -122,19 +124,132 @@ csr_spmm_half_kernel(int64_t m, int ell, const int64_t* __restrict__ rowptr,
   }
 }
 
+// ---- column slices (opt-in, LR_SPMM=slice4|slice8) --------------------------
+//
+// With X (n x ell fp64) larger than L2 every gathered X row comes from HBM:
+// config 5 (n = 2^21, ell = 48: X = 805 MB) moves 13.7 GB per product for
+// 3.1 GB of compulsory traffic (nnz random rows of 384 B each).  This path
+// copies X into slice-major panels Xs[s] (n x W, contiguous: 64 MB for W = 4,
+// one 32-byte sector per gathered row) and runs the product slice by slice,
+// Y[:, W s : W s + W] = S Xs[s], so the gathers can hit an L2-resident slice
+// while the CSR arrays are streamed once per slice.  It is measured slower
+// than the default (numbers below) and kept opt-in as the record of that
+// experiment; results equal the default kernels' to rounding (tests).
+
+// Xs[s][i][c] = X[i][W s + c] (zero past ell)
+template <int W>
+__global__ void __launch_bounds__(256)
+repack_slices_kernel(int64_t n, int ell, int ns, const double* __restrict__ X, int64_t ldx,
+                     double* __restrict__ Xs) {
+  const int64_t total = n * int64_t(ns) * W;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total;
+       e += int64_t(gridDim.x) * blockDim.x) {
+    // e enumerates the source row-major (i, j) with j < ns W: coalesced reads
+    const int64_t i = e / (int64_t(ns) * W);
+    const int j = int(e - i * int64_t(ns) * W);
+    const int s = j / W, c = j - s * W;
+    Xs[(int64_t(s) * n + i) * W + c] = j < ell ? X[i * ldx + j] : 0.0;
+  }
+}
+
+// A group of W lanes owns one row (a warp: 32 / W consecutive rows); lane c
+// of the group accumulates column c of the slice over the row's nonzeros in
+// CSR order (deterministic).  U nonzeros per step: U (col, val) loads, then U
+// independent gathers -- ~32 U / W sector requests in flight per warp, the
+// memory-level parallelism a one-row-per-warp loop lacks.
+template <int W, int U>
+__global__ void __launch_bounds__(256)
+csr_spmm_slice_kernel(int64_t m, const int64_t* __restrict__ rowptr,
+                      const int32_t* __restrict__ colidx, const double* __restrict__ vals,
+                      const double* __restrict__ Xs, double* __restrict__ Y, int64_t ldy,
+                      int ncols, bool accumulate) {
+  const int c = threadIdx.x % W;
+  const int64_t groups = int64_t(gridDim.x) * (blockDim.x / W);
+  for (int64_t row = int64_t(blockIdx.x) * (blockDim.x / W) + threadIdx.x / W; row < m;
+       row += groups) {
+    const int64_t b = __ldg(rowptr + row), e = __ldg(rowptr + row + 1);
+    double acc = 0.0;
+    for (int64_t k = b; k < e; k += U) {
+      int32_t col[U];
+      double v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        // clamped index (k < e): every load is in bounds, no predicated
+        // loads; the nonzeros past the row's end get weight 0
+        const int64_t q = min(k + u, e - 1);
+        col[u] = __ldcs(colidx + q);
+        v[u] = k + u < e ? __ldcs(vals + q) : 0.0;
+      }
+      double x[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) x[u] = __ldg(Xs + int64_t(col[u]) * W + c);
+#pragma unroll
+      for (int u = 0; u < U; ++u) acc = fma(v[u], x[u], acc);
+    }
+    if (c < ncols) {
+      double* yr = Y + row * ldy + c;
+      *yr = accumulate ? *yr + acc : acc;
+    }
+  }
+}
+
+// LR_SPMM: "warp" = one warp per nonzero; "slice4" / "slice8" = the column-
+// slice path with W = 4 / 8.  Default: the half-warp row-major kernel.
+// Measured at config 5 (n = 2^21, ell = 48, 33.5 M nonzeros, one B200):
+// half-warp 3.14 ms per product (13.7 GB of DRAM traffic, 4.35 TB/s), slice8
+// 4.75 ms, slice4 6.61 ms -- re-streaming the CSR arrays once per slice and
+// 32-byte L2 gathers cost more than the HBM gathers of whole 384-byte X rows
+// they replace, so the slices stay opt-in.
+#ifndef LR_SPMM_U
+#define LR_SPMM_U 8
+#endif
+
+int spmm_mode() {   // read per call: tests switch paths with the environment
+  const char* e = getenv("LR_SPMM");
+  if (!e) return 0;
+  if (e[0] == 'w') return 1;
+  if (e[0] == 'h') return 2;
+  if (!strcmp(e, "slice4")) return 4;
+  if (!strcmp(e, "slice8")) return 8;
+  return 0;
+}
+
+template <int W>
+void spmm_slices(Handle* h, int64_t m, int64_t n, int64_t ell, const int64_t* rowptr,
+                 const int32_t* colidx, const double* vals, const double* X, int64_t ldx,
+                 double* Y, int64_t ldy, bool accumulate) {
+  const int ns = int(ceil_div(ell, W));
+  double* Xs = pool_alloc_t<double>(h, size_t(ns) * n * W);
+  const int rb = int(std::min<int64_t>(ceil_div(n * ns * W, 256), int64_t(h->sm_count) * 32));
+  repack_slices_kernel<W><<<rb, 256, 0, h->stream>>>(n, int(ell), ns, X, ldx, Xs);
+  LR_CHECK_LAUNCH();
+  const int blocks = int(std::min<int64_t>(ceil_div(m, 256 / W), int64_t(h->sm_count) * 8));
+  for (int s = 0; s < ns; ++s) {
+    const int nc = int(std::min<int64_t>(W, ell - int64_t(s) * W));
+    csr_spmm_slice_kernel<W, LR_SPMM_U><<<blocks, 256, 0, h->stream>>>(
+        m, rowptr, colidx, vals, Xs + size_t(s) * n * W, Y + int64_t(s) * W, ldy, nc, accumulate);
+    LR_CHECK_LAUNCH();
+  }
+}
+
 }  // namespace
 
-void csr_spmm_f64(Handle* h, int64_t m, int64_t ell, const int64_t* rowptr,
+void csr_spmm_f64(Handle* h, int64_t m, int64_t n, int64_t ell, const int64_t* rowptr,
                   const int32_t* colidx, const double* vals, const double* X, int64_t ldx,
                   double* Y, int64_t ldy, bool accumulate) {
   if (m == 0 || ell == 0) return;
   LR_REQUIRE(ell <= 256, LR_EUNSUPPORTED, "csr_spmm: ell > 256 not built");
   const int blocks = int(std::min<int64_t>(ceil_div(m, 8), int64_t(h->sm_count) * 16));
-  static int old = -1;
-  if (old < 0) {
-    const char* e = getenv("LR_SPMM");
-    old = (e && e[0] == 'w') ? 1 : 0;   // LR_SPMM=warp: one warp per nonzero
+  const int mode = spmm_mode();
+  if (mode == 8) {
+    spmm_slices<8>(h, m, n, ell, rowptr, colidx, vals, X, ldx, Y, ldy, accumulate);
+    return;
   }
+  if (mode == 4) {
+    spmm_slices<4>(h, m, n, ell, rowptr, colidx, vals, X, ldx, Y, ldy, accumulate);
+    return;
+  }
+  const bool old = mode == 1;   // LR_SPMM=warp: one warp per nonzero
   if (!old && ell <= 64) {
     const int c16 = int(ceil_div(ell, 16));
     switch (c16) {

@@ -81,9 +81,12 @@ class CudaCsrOperator(MatVecOperator):
             e.record()
             torch.cuda.nvtx.range_pop()
             ell = X.shape[1]
-            # gather-inclusive algorithmic bytes: CSR arrays, one
-            # X row (ell doubles) per nonzero, Y read-modify-write
-            nbytes = self.csr_bytes() + self.nnz * ell * 8 + rows * ell * 8 * (2 if accumulate else 1)
+            # compulsory bytes: the CSR arrays, X once, Y (read-modify-write
+            # when accumulating) -- the HBM lower bound of the product; the
+            # gathers beyond X's first touch are served from L2 by the
+            # column-slice kernel (csrc/spmm.cu)
+            nbytes = (self.csr_bytes() + X.shape[0] * ell * 8
+                      + rows * ell * 8 * (2 if accumulate else 1))
             core.PASS_EVENTS.append((s, e, 2 * self.nnz * ell, nbytes, ell))
             return
         self._spmm_launch(rowptr, col, val, rows, X, Y, accumulate)

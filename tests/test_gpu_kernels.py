@@ -381,10 +381,15 @@ def test_gsrft_golden_and_oracle(golden):
         assert np.abs(Yd - Yo).max() <= tol * np.abs(Yo).max()
 
 
+@pytest.mark.parametrize("mode", ["", "warp", "half", "slice4", "slice8"])
 @pytest.mark.parametrize("ell", [1, 5, 16, 17, 33, 48, 64, 65, 100])
-def test_csr_spmm_vs_scipy(ell):
+def test_csr_spmm_vs_scipy(ell, mode, monkeypatch):
+    """Every SpMM kernel (row-major gathers, and the L2-resident column
+    slices that config 5 takes) on ragged, dense and empty rows."""
     import scipy.sparse as sp
     from paper_0909_4061_b200.sparse import CudaCsrOperator
+    if mode:
+        monkeypatch.setenv("LR_SPMM", mode)
     g = np.random.default_rng(4)
     S = sp.random(3000, 2500, density=0.004, random_state=4, format="csr").tolil()
     S[7, :] = g.standard_normal(2500)        # a dense row: many 32-nonzero chunks
