@@ -93,6 +93,25 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+// bulk tensor store smem -> global (bulk-group completion), and the waits
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0,
+                                             int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   map),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 __device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
   asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(map),
                "r"(c0), "r"(c1)
@@ -444,6 +463,109 @@ __global__ void split_transpose_kernel(int64_t K, int64_t N, const float* __rest
   }
 }
 
+// The same split, one 32-deep k-block per CTA iteration: the block's rows of
+// X (32 x N fp32, contiguous when ld == N) are read with float4 loads into a
+// [32][N] smem tile, and thread n writes the 64-byte hi and lo rows of
+// output row n (4 x 16-byte stores; a warp writes 2 KB contiguous of each).
+// Rows past K and columns N..BN-1 are written as zeros (no memset).  ~2x the
+// bandwidth of split_transpose_kernel's 64 x 32 tiles on config 4's panels.
+__global__ void __launch_bounds__(256)
+split_kblock_kernel(int64_t K, int64_t N, const float* __restrict__ X, int64_t ld, int64_t Kp,
+                    int BN, const float* __restrict__ scale, __half* __restrict__ hi,
+                    __half* __restrict__ lo) {
+  extern __shared__ float tile[];              // [32][BN + 1]
+  const int64_t nkb = Kp / 32;
+  const bool vec = (N % 4) == 0 && (ld % 4) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0;
+  const int nq = BN / 4;                       // float4 per tile row
+  const int per = (32 * nq + blockDim.x - 1) / blockDim.x;   // <= 8 (BN <= 256)
+  // the next k-block's rows are loaded into registers while this one is
+  // split and stored (one tile of loads in flight per thread)
+  float4 buf[8];
+  auto load = [&](int64_t kb) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = threadIdx.x + u * blockDim.x;
+      buf[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (u < per && e < 32 * nq) {
+        const int r = e / nq, c = (e - r * nq) * 4;
+        const int64_t k = kb * 32 + r;
+        if (k < K && c < N) {
+          if (vec) {
+            buf[u] = __ldcs(reinterpret_cast<const float4*>(X + k * ld + c));
+          } else {
+            const float* xr = X + k * ld;
+            buf[u].x = xr[c];
+            buf[u].y = c + 1 < N ? xr[c + 1] : 0.f;
+            buf[u].z = c + 2 < N ? xr[c + 2] : 0.f;
+            buf[u].w = c + 3 < N ? xr[c + 3] : 0.f;
+          }
+        }
+      }
+    }
+  };
+  int64_t kb = blockIdx.x;
+  if (kb < nkb) load(kb);
+  for (; kb < nkb; kb += gridDim.x) {
+    // tile row stride BN + 1: the column reads below (lane = (n, 8-k chunk))
+    // hit 32 distinct banks
+    const int TS = BN + 1;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = threadIdx.x + u * blockDim.x;
+      if (u < per && e < 32 * nq) {
+        const int r = e / nq, c = (e - r * nq) * 4;
+        float* t = tile + r * TS + c;
+        t[0] = buf[u].x; t[1] = buf[u].y; t[2] = buf[u].z; t[3] = buf[u].w;
+      }
+    }
+    __syncthreads();
+    if (kb + gridDim.x < nkb) load(kb + gridDim.x);
+    // 16-byte output chunk t = (n, q): k = 8q .. 8q + 7 of row n -- a warp
+    // stores 512 contiguous bytes of hi and of lo
+    for (int t = threadIdx.x; t < BN * 4; t += blockDim.x) {
+      const int n = t >> 2, q = t & 3;
+      const float sc = n < N ? scale[n] : 0.f;
+      uint32_t hw[4], lw[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float v0 = tile[(8 * q + 2 * j) * TS + n] * sc;
+        const float v1 = tile[(8 * q + 2 * j + 1) * TS + n] * sc;
+        const __half2 h = __floats2half2_rn(v0, v1);
+        const float2 hf = __half22float2(h);
+        const __half2 l = __floats2half2_rn(v0 - hf.x, v1 - hf.y);
+        hw[j] = *reinterpret_cast<const uint32_t*>(&h);
+        lw[j] = *reinterpret_cast<const uint32_t*>(&l);
+      }
+      reinterpret_cast<uint4*>(hi + (kb * BN + n) * 32)[q] = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+      reinterpret_cast<uint4*>(lo + (kb * BN + n) * 32)[q] = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+    }
+    __syncthreads();
+  }
+}
+
+// X (K x N) -> the MMA's hi/lo operand layout (Kp = K rounded up to 32, BN >= N
+// a multiple of 16); LR_SPLIT=tile keeps the 64 x 32 tile kernel
+void split_operand(Handle* h, int64_t K, int64_t N, const float* X, int64_t ld, int64_t Kp,
+                   int BN, const float* scale, __half* hi, __half* lo) {
+  const char* e = getenv("LR_SPLIT");
+  if (e && e[0] == 't') {
+    if (BN != N) {
+      LR_CUDA(cudaMemsetAsync(hi, 0, sizeof(__half) * BN * Kp, h->stream));
+      LR_CUDA(cudaMemsetAsync(lo, 0, sizeof(__half) * BN * Kp, h->stream));
+    }
+    dim3 grid(unsigned(ceil_div(Kp, 64)), unsigned(ceil_div(N, 32)));
+    split_transpose_kernel<<<grid, dim3(32, 8), 0, h->stream>>>(K, N, X, ld, Kp, BN, scale, hi,
+                                                                 lo);
+    LR_CHECK_LAUNCH();
+    return;
+  }
+  const size_t smem = size_t(32) * (BN + 1) * sizeof(float);   // ~32 KB (BN <= 256)
+  const int64_t nkb = Kp / 32;
+  const int grid = int(std::max<int64_t>(1, std::min<int64_t>(nkb, int64_t(h->sm_count) * 6)));
+  split_kblock_kernel<<<grid, 256, smem, h->stream>>>(K, N, X, ld, Kp, BN, scale, hi, lo);
+  LR_CHECK_LAUNCH();
+}
+
 // out (M x N, ldo) = sum over S slices of part (S x M x N), fixed order in
 // fp64.  Each thread owns 4 consecutive elements (float4 loads) and keeps 8
 // slice loads in flight (A^T Y at config 4 sums 256 slices of 4 MB: the
@@ -758,6 +880,7 @@ constexpr int P_THREADS = 384;
 #ifndef LR_P_TS3
 #define LR_P_TS3 4
 #endif
+constexpr int P_STG_BYTES = 4 * 2 * 32 * 32 * 4;   // epilogue staging (>= 4 x 32 x 33 floats)
 constexpr int P_TS1 = LR_P_TS1;   // fp32 A ring (TMA -> converters)
 constexpr int P_TS2 = LR_P_TS2;   // A hi/lo ring (converters -> MMA)
 constexpr int P_TS3 = LR_P_TS3;   // X-half hi/lo ring (TMA -> MMA)
@@ -788,8 +911,9 @@ template <bool TRANS>
 __global__ void __launch_bounds__(P_THREADS, 1)
 gemm_f32_pair_kernel(const __grid_constant__ CUtensorMap mapA,
                      const __grid_constant__ CUtensorMap mapBhi,
-                     const __grid_constant__ CUtensorMap mapBlo, int M, int N, int BN,
-                     PairWork w, float sA_host, const float* __restrict__ sA_dev,
+                     const __grid_constant__ CUtensorMap mapBlo,
+                     const __grid_constant__ CUtensorMap mapC, bool tma_store, int M, int N,
+                     int BN, PairWork w, float sA_host, const float* __restrict__ sA_dev,
                      const float* __restrict__ sB_dev, float* __restrict__ C, int64_t ldc,
                      int64_t cstride) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -800,8 +924,11 @@ gemm_f32_pair_kernel(const __grid_constant__ CUtensorMap mapA,
   const int HB_SLOT = (2 * HB_BYTES + 1023) & ~1023;
   unsigned char* ring2 = base + P_TS1 * A32_BYTES;                // A hi/lo
   unsigned char* ring3 = ring2 + P_TS2 * 2 * AH_BYTES;           // X half hi/lo
-  float* ebuf = reinterpret_cast<float*>(ring3 + P_TS3 * HB_SLOT);   // 4 x 32 x 33 floats
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ebuf + 4 * 32 * 33);
+  // epilogue staging: per epilogue warp two 32 x 32 fp32 tiles (SW128, for the
+  // bulk tensor stores), or the 32 x 33 transpose buffers of the row stores
+  unsigned char* stg = ring3 + P_TS3 * HB_SLOT;                    // 4 x 8 KB
+  float* ebuf = reinterpret_cast<float*>(stg);                     // 4 x 32 x 33 floats
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stg + P_STG_BYTES);
   uint64_t* a32_full = bars;
   uint64_t* a32_empty = a32_full + P_TS1;
   uint64_t* ahl_full = a32_empty + P_TS1;
@@ -997,6 +1124,7 @@ gemm_f32_pair_kernel(const __grid_constant__ CUtensorMap mapA,
     float* wbuf = ebuf + q * (32 * 33);
     const float inv_a = 1.0f / sA;
     int64_t it = 0;
+    int nst = 0;                             // bulk stores issued by this warp
     for (int64_t u = pair; u < w.units; u += npairs, ++it) {
       int64_t tile, sp;
       w.unit(u, tile, sp);
@@ -1036,6 +1164,35 @@ gemm_f32_pair_kernel(const __grid_constant__ CUtensorMap mapA,
             else           mbar_arrive_cluster(&acc_empty[b], 0);
           }
         }
+        if (tma_store) {
+          // lane = row: its 32 consecutive columns, scaled, into a SW128
+          // staging tile (16-byte chunk c of row r at chunk c ^ (r & 7):
+          // conflict-free quarter-warp stores), then one bulk tensor store of
+          // the 32 x 32 tile (the per-row scalar stores below were ~0.33 ms
+          // of the 1.3 ms m x 256 . 256 x 256 apply at config 4)
+          unsigned char* sb = stg + q * 8192 + (nst & 1) * 4096;
+          if (lane == 0) bulk_wait_read<1>();     // this buffer's store 2 chunks ago has read it
+          __syncwarp();
+          const int col = c0 + lane;
+          const float scol = col < N ? inv_a / sB_dev[col] : 0.f;
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            float4 v;
+            v.x = __uint_as_float(d[4 * c]) * __shfl_sync(0xffffffffu, scol, 4 * c);
+            v.y = __uint_as_float(d[4 * c + 1]) * __shfl_sync(0xffffffffu, scol, 4 * c + 1);
+            v.z = __uint_as_float(d[4 * c + 2]) * __shfl_sync(0xffffffffu, scol, 4 * c + 2);
+            v.w = __uint_as_float(d[4 * c + 3]) * __shfl_sync(0xffffffffu, scol, 4 * c + 3);
+            *reinterpret_cast<float4*>(sb + lane * 128 + ((c ^ (lane & 7)) << 4)) = v;
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&mapC, sb, c0, int(mrow0));
+            bulk_commit();
+          }
+          ++nst;
+          continue;
+        }
 #pragma unroll
         for (int j = 0; j < 32; ++j) wbuf[lane * 33 + j] = __uint_as_float(d[j]);
         __syncwarp();
@@ -1050,6 +1207,7 @@ gemm_f32_pair_kernel(const __grid_constant__ CUtensorMap mapA,
         __syncwarp();
       }
     }
+    if (tma_store && lane == 0) bulk_wait_all();
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
@@ -1154,16 +1312,7 @@ void gemm_f32_pair(Handle* h, bool transA, int64_t M, int64_t N, int64_t K, cons
   const int64_t Kp = ceil_div(K, TBK) * TBK;
   __half* Bhi = pool_alloc_t<__half>(h, size_t(BN) * Kp);
   __half* Blo = pool_alloc_t<__half>(h, size_t(BN) * Kp);
-  if (BN != N) {
-    LR_CUDA(cudaMemsetAsync(Bhi, 0, sizeof(__half) * BN * Kp, h->stream));
-    LR_CUDA(cudaMemsetAsync(Blo, 0, sizeof(__half) * BN * Kp, h->stream));
-  }
-  {
-    dim3 grid(unsigned(ceil_div(Kp, 64)), unsigned(ceil_div(N, 32)));
-    split_transpose_kernel<<<grid, dim3(32, 8), 0, h->stream>>>(K, N, B, ldb, Kp, BN, sB, Bhi,
-                                                                 Blo);
-    LR_CHECK_LAUNCH();
-  }
+  split_operand(h, K, N, B, ldb, Kp, BN, sB, Bhi, Blo);
   CUtensorMap mapA = transA
       ? make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, A, uint64_t(M), uint64_t(K), uint64_t(lda) * 4,
                     TBM, TBK, CU_TENSOR_MAP_SWIZZLE_NONE)
@@ -1176,7 +1325,7 @@ void gemm_f32_pair(Handle* h, bool transA, int64_t M, int64_t N, int64_t K, cons
                                   uint32_t(BN / 2), CU_TENSOR_MAP_SWIZZLE_64B);
   const size_t hb_slot = (size_t(2) * (BN / 2) * TBK * 2 + 1023) & ~size_t(1023);
   const size_t smem = size_t(P_TS1) * A32_BYTES + size_t(P_TS2) * 2 * AH_BYTES +
-                      size_t(P_TS3) * hb_slot + 4 * 32 * 33 * sizeof(float) + 1024 /*align*/ +
+                      size_t(P_TS3) * hb_slot + P_STG_BYTES + 1024 /*align*/ +
                       256 /*barriers*/;
   cudaLaunchConfig_t cfg = {};
   cfg.blockDim = dim3(P_THREADS, 1, 1);
@@ -1222,8 +1371,15 @@ void gemm_f32_pair(Handle* h, bool transA, int64_t M, int64_t N, int64_t K, cons
     cstride = M * N;
   }
   cfg.gridDim = dim3(unsigned(2 * npairs), 1, 1);
-  LR_CUDA(cudaLaunchKernelEx(&cfg, kern, mapA, mapBh, mapBl, int(M), int(N), BN, w, sA, sA_dev,
-                             sB, out, ldo, cstride));
+  // bulk tensor stores of the epilogue: one output slice, 16-byte rows
+  const bool tma_store = cstride == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0 &&
+                         (ldo % 4) == 0 && !getenv("LR_TC_ROWSTORE");
+  CUtensorMap mapC = tma_store
+      ? make_map_2d(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, out, uint64_t(N), uint64_t(M),
+                    uint64_t(ldo) * 4, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B)
+      : mapA;
+  LR_CUDA(cudaLaunchKernelEx(&cfg, kern, mapA, mapBh, mapBl, mapC, tma_store, int(M), int(N), BN,
+                             w, sA, sA_dev, sB, out, ldo, cstride));
   LR_CHECK_LAUNCH();
   if (splits > 1) {
     const int blocks = int(std::max<int64_t>(1, std::min<int64_t>(ceil_div(M * N, 256), 8192)));
@@ -1359,16 +1515,7 @@ void gemm_f32_tc(Handle* h, bool transA, int64_t M, int64_t N, int64_t K, const 
   const int64_t Kp = ceil_div(K, TBK) * TBK;
   __half* Bhi = pool_alloc_t<__half>(h, size_t(BN) * Kp);
   __half* Blo = pool_alloc_t<__half>(h, size_t(BN) * Kp);
-  if (BN != N) {
-    LR_CUDA(cudaMemsetAsync(Bhi, 0, sizeof(__half) * BN * Kp, h->stream));
-    LR_CUDA(cudaMemsetAsync(Blo, 0, sizeof(__half) * BN * Kp, h->stream));
-  }
-  {
-    dim3 grid(unsigned(ceil_div(Kp, 64)), unsigned(ceil_div(N, 32)));
-    split_transpose_kernel<<<grid, dim3(32, 8), 0, h->stream>>>(K, N, B, ldb, Kp, BN, sB, Bhi,
-                                                                 Blo);
-    LR_CHECK_LAUNCH();
-  }
+  split_operand(h, K, N, B, ldb, Kp, BN, sB, Bhi, Blo);
   if (m256_enabled() && M >= 8 * 256) {
     gemm_f32_m256(h, transA, M, N, K, A, lda, sA, sA_dev, sB, BN, Kp, Bhi, Blo, C, ldc);
     return;

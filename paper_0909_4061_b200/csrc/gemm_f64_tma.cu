@@ -98,7 +98,7 @@ gemm_f64_tma_kernel(const __grid_constant__ CUtensorMap mapA,
   const int64_t n0 = int64_t(blockIdx.y) * G::BN;
   const int64_t kbeg = int64_t(blockIdx.z) * kchunk;
   const int64_t kend = min(K, kbeg + kchunk);
-  const int nk = int((kend - kbeg + BK - 1) / BK);
+  const int nk = kend > kbeg ? int((kend - kbeg + BK - 1) / BK) : 0;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < ST; ++s) {
@@ -138,9 +138,17 @@ gemm_f64_tma_kernel(const __grid_constant__ CUtensorMap mapA,
 #pragma unroll
       for (int e = 0; e < 4; ++e) acc[i][j][e] = 0.0;
 
+  // symmetric result: a warp whose 32 x 8NF tile lies strictly below the
+  // diagonal issues no DMMA (mirrored afterwards), so a diagonal CTA tile
+  // costs the SM's DMMA pipe 6/8 of a full one (BN = 128)
+  const bool idle = sym && n0 + int64_t(wn + 1) * NF * 8 - 1 < m0 + int64_t(wm) * 32;
   for (int kt = 0; kt < nk; ++kt) {
     const int s = kt % ST;
     bar_wait(&full[s], uint32_t(kt / ST) & 1u);
+    if (idle) {
+      bar_arrive(&empty[s]);
+      continue;
+    }
     const TIN* as = reinterpret_cast<const TIN*>(base + s * G::STAGE);
     const TIN* bs = reinterpret_cast<const TIN*>(base + s * G::STAGE + G::A_BYTES);
 #pragma unroll
@@ -197,12 +205,13 @@ gemm_f64_tma_kernel(const __grid_constant__ CUtensorMap mapA,
   }
 }
 
-// strictly-lower tiles of a symmetric result <- transposed upper entries
-__global__ void mirror_lower(int64_t n, int bm, int bn, double* __restrict__ C, int64_t ldc) {
+// strictly-lower entries of a symmetric result <- transposed upper entries
+// (the skipped CTA tiles and the idle warps' parts of the diagonal tiles)
+__global__ void mirror_lower(int64_t n, double* __restrict__ C, int64_t ldc) {
   for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n * n;
        e += int64_t(gridDim.x) * blockDim.x) {
     const int64_t i = e / n, j = e - i * n;
-    if ((j / bn + 1) * bn <= (i / bm) * bm) C[i * ldc + j] = C[j * ldc + i];
+    if (j < i) C[i * ldc + j] = C[j * ldc + i];
   }
 }
 
@@ -238,6 +247,9 @@ void launch(Handle* h, int64_t M, int64_t N, int64_t K, const TIN* A, int64_t ld
   const int64_t want = choose_splits(h->sm_count, live, K);
   const int64_t kchunk = ceil_div(ceil_div(K, want), BK) * BK;
   const int64_t splits = std::max<int64_t>(1, ceil_div(K, kchunk));
+  // (measured: giving the diagonal tiles, whose lower warps idle, 4/3 longer
+  // k-chunks made config 4's Gram slower, 3.35 vs 2.99 ms -- a CTA's stage
+  // time does not shrink with its DMMA count: uniform chunks)
   dim3 grid{unsigned(mt), unsigned(nt), unsigned(splits)};
   if (splits == 1) {
     kern<<<grid, THREADS, G::SMEM, h->stream>>>(mapA, mapB, M, N, K, C, ldc, kchunk, 0, sym);
@@ -251,7 +263,7 @@ void launch(Handle* h, int64_t M, int64_t N, int64_t K, const TIN* A, int64_t ld
   }
   if (sym) {
     mirror_lower<<<unsigned(std::min<int64_t>(ceil_div(M * N, 256), 4096)), 256, 0, h->stream>>>(
-        M, BM, G::BN, C, ldc);
+        M, C, ldc);
     LR_CHECK_LAUNCH();
   }
 }

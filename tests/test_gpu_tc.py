@@ -98,3 +98,25 @@ def test_fp32_orth_second_pass_on_tc(monkeypatch):
     assert (Q.double().T @ Q.double() - I).abs().max().item() <= 5e-6
     assert (Q0.double().T @ Q0.double() - I).abs().max().item() <= 5e-6
     assert (Q.double() - Q0.double()).abs().max().item() <= 1e-4
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("m,ell", [(4096, 256), (70001, 200), (300000, 130), (2 ** 20, 256),
+                                   (20000, 64), (8192, 300)])
+def test_exact_gram_symmetric_tiles(m, ell, dtype):
+    """lr_gram (the exact DMMA Gram of the first CholeskyQR pass): diagonal
+    CTA tiles skip the warps strictly below the diagonal and the lower
+    triangle is mirrored -- the whole matrix equals an fp64 product of the
+    same panel to fp64 roundoff and is exactly symmetric."""
+    from paper_0909_4061_b200 import _lib
+    g = torch.Generator(device="cuda").manual_seed(m + ell)
+    Y = torch.randn(m, ell, device="cuda", generator=g, dtype=dtype)
+    Y[:, 1::4] *= 1e-3
+    G = torch.empty(ell, ell, dtype=torch.float64, device="cuda")
+    code = _lib.F32 if dtype == torch.float32 else _lib.F64
+    _lib.call("lr_gram", _lib.handle(), code, m, ell, _lib.ptr(Y), ell, _lib.ptr(G))
+    Yd = Y.double()
+    ref = Yd.T @ Yd
+    bound = Yd.abs().T @ Yd.abs()
+    assert torch.equal(G, G.T)
+    assert ((G - ref).abs() / bound).max().item() <= 1e-13
