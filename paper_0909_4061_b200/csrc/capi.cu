@@ -242,6 +242,40 @@ void gram_second(Handle* h, int dtype, int64_t m, int64_t ell, const void* Q1, i
   gram_any(h, dtype, m, ell, Q1, ldq, G);
 }
 
+// Sketch-preconditioned CholeskyQR for tall fp32 panels (sketch_rows.cu): R0
+// from the Cholesky factor of the Gram of the d x ell sketch S Y (fp64), Q1 = Y
+// R0^{-1} (kappa(Q1) <= ~3), then the tensor-core Gram of Q1 and its true
+// Cholesky factor P2^{-1}.  Rank decisions: the sketch reproduces the pivots
+// of the exact Gram within the embedding's distortion (< 2x), so the first
+// factorization runs with 4x the drop tolerance -- any pivot within 16x of the
+// drop threshold counts as a drop and flags the step to the exact path; so
+// does a second-pass pivot below 1e-3 of its diagonal (the embedding failed).
+// Q1 (m x ell, ld ell) and P2 (wide) are left for the caller.
+void orth_sketch_core(Handle* h, int64_t m, int64_t ell, const float* Y, int64_t ldy, float* Q1,
+                      double* P2, double tol) {
+  const int64_t d = sketch_rows_dim();
+  double* SY = pool_alloc_t<double>(h, size_t(d) * ell);
+  unsigned int* bits = pool_alloc_t<unsigned int>(h, 4);
+  double* G = pool_alloc_t<double>(h, size_t(ell) * ell);
+  double* P = pool_alloc_t<double>(h, size_t(ell) * ell);
+  double* R = pool_alloc_t<double>(h, size_t(ell) * ell);
+  sketch_rows_f32(h, m, ell, Y, ldy, 0x243f6a8885a308d3ull + uint64_t(h->rank), SY, bits);
+  gemm_f64(h, true, ell, ell, d, SY, ell, SY, ell, G, ell);
+  chol_any(h, LR_F64, ell, G, 4.0 * tol, 4.0 * double(ell) * U64, 0.0, P, R, h->d_info);
+  h->amax_bits_hint = bits;
+  apply_right(h, LR_F32, m, ell, ell, Y, ldy, P, ell, Q1, ell);
+  h->amax_bits_hint = nullptr;
+  gram_second(h, LR_F32, m, ell, Q1, ell, G);
+  chol_any(h, LR_F64, ell, G, tol, 1e-3, 0.0, P2, R, h->d_info);
+}
+
+bool orth_sketch_ok(Handle* h, int dtype, int64_t m, int64_t ell) {
+  // (row-sharded callers keep the exact Gram: every rank must take the same
+  // branch, and the local row counts may straddle the size threshold)
+  return dtype == LR_F32 && h->status && !h->sharded && h->f32_mode == LR_F32_SPLIT3 &&
+         sketch_rows_supported(m, ell);
+}
+
 // Speculative CholeskyQR2 with no host synchronization: the drop rule and
 // pivot resolvability are evaluated on the device and reported through
 // h->status (bit 1 unresolved pivot, 2 column dropped, 4 non-finite).  When
@@ -249,6 +283,27 @@ void gram_second(Handle* h, int dtype, int64_t m, int64_t ell, const void* Q1, i
 void orth_fast_impl(Handle* h, int dtype, int64_t m, int64_t ell, const void* Y, int64_t ldy,
                     void* Q, int64_t ldq, double tol) {
   const size_t ws = wide_size(dtype), es = elem_size(dtype);
+  if (orth_sketch_ok(h, dtype, m, ell)) {
+    float* Q1 = pool_alloc_t<float>(h, size_t(m) * ell);
+    double* P2 = pool_alloc_t<double>(h, size_t(ell) * ell);
+    orth_sketch_core(h, m, ell, static_cast<const float*>(Y), ldy, Q1, P2, tol);
+    // Q2 = Q1 P2 is orthonormal to ~2e-5 only: the tensor-core Gram of the
+    // kappa ~ 3 panel Q1 carries the TMEM truncation as a coherent shrink of
+    // its off-diagonal entries (tools/gram_tc_probe.py: E_off = -2.2e-5
+    // G_off).  Harmless where only range(Q) matters (the deferred variant,
+    // inside the subspace iteration); the basis returned here takes one more
+    // near-identity pass, whose Gram entries are too small to be biased.
+    float* Q2 = pool_alloc_t<float>(h, size_t(m) * ell);
+    double* G3 = pool_alloc_t<double>(h, size_t(ell) * ell);
+    double* P3 = pool_alloc_t<double>(h, size_t(ell) * ell);
+    double* R3 = pool_alloc_t<double>(h, size_t(ell) * ell);
+    apply_right(h, dtype, m, ell, ell, Q1, ell, P2, ell, Q2, ell, ORTHO_AMAX);
+    gram_second(h, dtype, m, ell, Q2, ell, G3);
+    chol_near_identity(h, LR_F64, ell, G3, tol, 4.0 * double(ell) * U64, P3, R3, h->d_info,
+                       near_id_thr(dtype));
+    apply_right(h, dtype, m, ell, ell, Q2, ell, P3, ell, Q, ldq, ORTHO_AMAX);
+    return;
+  }
   void* G = pool_alloc(h, size_t(ell) * ell * ws);
   void* P = pool_alloc(h, size_t(ell) * ell * ws);
   void* R = pool_alloc(h, size_t(ell) * ell * ws);
@@ -273,6 +328,11 @@ void orth_fast_impl(Handle* h, int dtype, int64_t m, int64_t ell, const void* Y,
 void orth_fast_deferred_impl(Handle* h, int dtype, int64_t m, int64_t ell, const void* Y,
                              int64_t ldy, void* Q1, void* P2, double tol) {
   const size_t ws = wide_size(dtype);
+  if (orth_sketch_ok(h, dtype, m, ell)) {
+    orth_sketch_core(h, m, ell, static_cast<const float*>(Y), ldy, static_cast<float*>(Q1),
+                     static_cast<double*>(P2), tol);
+    return;
+  }
   void* G = pool_alloc(h, size_t(ell) * ell * ws);
   void* P = pool_alloc(h, size_t(ell) * ell * ws);
   void* R = pool_alloc(h, size_t(ell) * ell * ws);

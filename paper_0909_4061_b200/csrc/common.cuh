@@ -80,6 +80,10 @@ struct Handle {
   // the launch returns at once (the near-identity fast path already produced
   // the factor; see chol_near_identity).  Host-sync free.
   const int32_t* gate = nullptr;
+  // float bits of max|A| of the next fp32 tensor-core product's left operand,
+  // already reduced on the device by an earlier kernel (sketch_rows.cu): the
+  // split then skips its own max pass over the panel
+  const unsigned int* amax_bits_hint = nullptr;
   // row-sharded calls (lr_comm_init / lr_orth_sharded): the NCCL communicator
   // of this rank; `sharded` makes the orthonormalization all-reduce its Grams
   void* nccl_comm = nullptr;
@@ -195,6 +199,11 @@ void gemm_c64_hint(Handle* h, bool transA, bool conjA, int64_t M, int64_t N, int
 // gram_tc.cu: G = Y^T Y of an fp32 panel (ell <= 256) on tcgen05 with
 // fp32-level accuracy (second CholeskyQR pass); entries must satisfy
 // |y| 2^log2_scale < 2^15, else *status |= 1 (status may be null)
+// sketch_rows.cu: sparse-sign row sketch S Y (fp64, d x ell) of a tall fp32 panel
+int64_t sketch_rows_dim();
+bool sketch_rows_supported(int64_t m, int64_t ell);
+void sketch_rows_f32(Handle* h, int64_t m, int64_t ell, const float* Y, int64_t ldy,
+                     uint64_t seed, double* SY, unsigned int* amax_bits);
 bool gram_tc_supported(int64_t m, int64_t ell, const float* Y, int64_t ldy);
 void gram_tc_f32(Handle* h, int64_t m, int64_t ell, const float* Y, int64_t ldy, double* G,
                  int log2_scale, int32_t* status);

@@ -1476,7 +1476,12 @@ void gemm_f32_tc(Handle* h, bool transA, int64_t M, int64_t N, int64_t K, const 
   float* sB = pool_alloc_t<float>(h, size_t(N));
   float sA = 1.f;
   float* sA_dev = nullptr;
-  if (a_amax < 0) {
+  if (a_amax < 0 && h->amax_bits_hint) {
+    // max|A| already reduced on the device by the caller's previous kernel
+    sA_dev = reinterpret_cast<float*>(bits + 2);
+    make_scale_kernel<<<1, 1, 0, h->stream>>>(h->amax_bits_hint, sA_dev);
+    LR_CHECK_LAUNCH();
+  } else if (a_amax < 0) {
     // unknown max|A|: reduce it on the device (no host synchronization)
     sA_dev = reinterpret_cast<float*>(bits + 2);
     LR_CUDA(cudaMemsetAsync(bits + 1, 0, sizeof(unsigned int), h->stream));

@@ -127,3 +127,84 @@ def test_ozaki_wide_rows_fall_back_to_dmma(monkeypatch):
     bound = np.abs(A) @ np.abs(X)
     err = np.abs(Y.astype(np.longdouble) - ref)
     assert float((err / bound).max()) <= 2.0 ** -44
+
+
+# ---- sketch-preconditioned CholeskyQR of tall fp32 panels (sketch_rows.cu) ----------
+
+def _tall_panel(m, ell, kappa, seed, heavy_rows=False):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    U = torch.randn(m, ell, device="cuda", dtype=torch.float64, generator=g)
+    if heavy_rows:
+        U[:: m // 64] *= 300.0
+    U, _ = torch.linalg.qr(U)
+    W, _ = torch.linalg.qr(torch.randn(ell, ell, device="cuda", dtype=torch.float64, generator=g))
+    s = torch.logspace(0, -float(np.log10(kappa)), ell, device="cuda", dtype=torch.float64)
+    return ((U * s) @ W.T).float().contiguous()
+
+
+def _orth_quality(Y, Q):
+    Qd, Yd = Q.double(), Y.double()
+    ell = Q.shape[1]
+    orth = (Qd.T @ Qd - torch.eye(ell, device="cuda", dtype=torch.float64)).abs().max().item()
+    R = Qd.T @ Yd
+    span = (torch.linalg.norm(Yd - Qd @ R) / torch.linalg.norm(Yd)).item()
+    low = (torch.linalg.norm(torch.tril(R, -1)) / torch.linalg.norm(R)).item()
+    return orth, span, low
+
+
+@pytest.mark.parametrize("m,ell,kappa,heavy", [(131072, 256, 1e6, False), (262144, 128, 1e3, False),
+                                               (131072, 256, 1e6, True), (100003, 72, 1e4, False)])
+def test_sketch_preconditioned_orth(m, ell, kappa, heavy):
+    """Tall fp32 panels take the sketch-preconditioned CholeskyQR (no exact
+    Gram): the speculative step must report no flag and return the
+    Gram-Schmidt basis of Y -- orthonormal at the fp32 rounding level, the
+    same span, Q^T Y upper triangular (reference core.py:84-115 builds the
+    columns in order).  Heavy rows are the hard case for a sparse embedding."""
+    from paper_0909_4061_b200 import core
+    Y = _tall_panel(m, ell, kappa, 11, heavy)
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    with core.speculate(status):
+        Q = core.orth_dev(Y)
+        Q1, P2 = core.orth_dev_deferred(Y)
+    torch.cuda.synchronize()
+    assert int(status.item()) == 0
+    orth, span, low = _orth_quality(Y, Q)
+    assert orth <= (2e-5 if heavy else 1e-6), orth
+    assert span <= (3e-5 if heavy else 5e-6), span
+    assert low <= (2e-5 if heavy else 2e-6), low
+    # the deferred pair spans the same space (range only: its Q1 P2 is
+    # orthonormal to the tensor-core Gram's ~2e-5)
+    Qd = (Q1.double() @ P2)
+    assert (Qd.T @ Qd - torch.eye(ell, device="cuda", dtype=torch.float64)).abs().max().item() <= 2e-4
+    Yd = Y.double()
+    Qo, _ = torch.linalg.qr(Qd)
+    assert (torch.linalg.norm(Yd - Qo @ (Qo.T @ Yd)) / torch.linalg.norm(Yd)).item() <= (3e-5 if heavy else 5e-6)
+
+
+def test_sketch_preconditioned_orth_flags_rank_deficiency():
+    """A dependent column must not be decided from the sketch: the speculative
+    step flags it (drop bit) and the exact path drops it like the reference."""
+    from paper_0909_4061_b200 import core
+    Y = _tall_panel(131072, 64, 10.0, 5)
+    Y[:, 40] = Y[:, 3] * 0.5 + Y[:, 7]
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    with core.speculate(status):
+        core.orth_dev(Y)
+    torch.cuda.synchronize()
+    assert int(status.item()) & 2
+    Q = core.orth_dev(Y)
+    assert Q.shape[1] == 63
+    orth, span, _ = _orth_quality(Y, Q)
+    assert orth <= 1e-6 and span <= 5e-6
+
+
+def test_sketch_preconditioned_orth_repeatable():
+    """Bitwise run-to-run determinism (fixed-order partial sums, no atomics on data)."""
+    from paper_0909_4061_b200 import core
+    Y = _tall_panel(131072, 128, 1e5, 9)
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    outs = []
+    for _ in range(2):
+        with core.speculate(status):
+            outs.append(core.orth_dev(Y).clone())
+    assert torch.equal(outs[0], outs[1])
