@@ -691,13 +691,22 @@ def e2e_measure(args, cfg, A, lr):
                                     estimate=False)
         return f
 
-    for _ in range(3):          # warm-up: allocator / pinned-buffer caches settle by the 3rd call
-        once()
+    # warm-up: allocator / pinned-buffer caches settle by the 3rd call.  The
+    # previous call's factors stay referenced while the next call runs, as in
+    # the timed loop (their pinned host buffers are then not recycled: the
+    # second set is allocated here, ~0.5 s of page pinning, not in a timed call)
+    for _ in range(3):
+        f = once()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
+    per_call = []
     for _ in range(steps):
+        tc = time.perf_counter()
         f = once()
+        per_call.append(time.perf_counter() - tc)
     dt = (time.perf_counter() - t0) / steps
+    if os.environ.get("LR_E2E_DEBUG"):
+        print("e2e per call (ms):", [round(1e3 * x, 1) for x in per_call], file=sys.stderr)
     a_bytes = A.numel() * A.element_size()
     d2h = f.U.nbytes + f.sigma.nbytes + f.V.nbytes
     return {"value": round(cfg.passes() * a_bytes / dt / 1e9, 3), "unit": "A-GB/s",

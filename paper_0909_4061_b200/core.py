@@ -23,6 +23,8 @@ import ctypes as C
 import threading
 from dataclasses import dataclass
 
+import os
+
 import numpy as np
 
 from . import _lib, config
@@ -124,6 +126,33 @@ def _stage_host(t):
     if t.numel():
         h.copy_(t, non_blocking=True)
     return h
+
+
+class HostPrefetch:
+    """A device -> pinned-host copy started early on the copy stream, so it
+    overlaps the kernels enqueued after it (the basis Q of a randomized SVD
+    is final two passes before its factors are)."""
+
+    def __init__(self, t):
+        torch = _torch()
+        t = t.detach()
+        self.src = t
+        self.host = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        self.event = None
+        if t.numel():
+            cur = torch.cuda.current_stream(t.device)
+            side = _copy_stream(t.device)
+            side.wait_stream(cur)
+            with torch.cuda.stream(side):
+                self.host.copy_(t, non_blocking=True)
+                self.event = torch.cuda.Event()
+                self.event.record(side)
+            t.record_stream(side)
+
+    def numpy(self):
+        if self.event is not None:
+            self.event.synchronize()
+        return self.host.numpy()
 
 
 def to_host(t):
@@ -229,6 +258,7 @@ class DenseOperator(MatVecOperator):
     # chunk behind the copy (fp64 / complex128: no max|A| needed up front)
     STREAM_MIN_BYTES = 256 << 20
     STREAM_CHUNK_BYTES = 64 << 20
+    STREAM_MAX_CHUNKS = 32
 
     def __init__(self, A, device=None, validate=True):
         torch = _torch()
@@ -245,7 +275,13 @@ class DenseOperator(MatVecOperator):
             super().__init__(*shape)
             self._upload_streamed(A, device)
             if self._array.dtype not in (torch.float64, torch.complex128):
-                self._finalize()       # the scaled passes need max|A| first
+                # fp32 / complex64: join the upload here.  Running the first
+                # pass chunk by chunk behind the copy (each chunk scaled by its
+                # own max, reduced on the device) measured SLOWER end to end at
+                # config 4 (380.0 vs 371.8 ms per call with 32 chunks, 408 ms
+                # with 256): the whole-matrix pass after the join costs 5.5 ms,
+                # the chunk passes' fixed costs more
+                self._finalize()
             return
         t = to_device(A, _torch_compute_dtype(A) if torch.is_tensor(A) else None, device)
         super().__init__(*t.shape)
@@ -271,7 +307,11 @@ class DenseOperator(MatVecOperator):
         self._array = t
         self.code = _lib.dtype_code(t.dtype)
         m, n = A.shape
-        rows = max(128, (self.STREAM_CHUNK_BYTES // (n * A.element_size())) // 128 * 128)
+        # at most ~STREAM_MAX_CHUNKS chunks: every chunk costs a fixed host-side
+        # price per pass (a 16 GiB upload in 64 MiB chunks ran 256 chunk passes
+        # of 16 row tiles each and became launch-bound: +25 ms)
+        cbytes = max(self.STREAM_CHUNK_BYTES, A.numel() * A.element_size() // self.STREAM_MAX_CHUNKS)
+        rows = max(128, (cbytes // (n * A.element_size())) // 128 * 128)
         bounds = [(r, min(m, r + rows)) for r in range(0, m, rows)]
         bad = torch.empty(len(bounds), dtype=torch.int64, device=dev)
         res = torch.empty((len(bounds), 2), dtype=torch.float64, device=dev)

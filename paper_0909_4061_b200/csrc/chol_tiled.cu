@@ -319,8 +319,13 @@ __global__ void assemble_kernel(int n, int n1, const T* __restrict__ X11, const 
                                 const T* __restrict__ R12, const T* __restrict__ R22,
                                 const int32_t* __restrict__ info1,
                                 const int32_t* __restrict__ info2, T* __restrict__ P,
-                                T* __restrict__ Rout, int32_t* __restrict__ info) {
+                                T* __restrict__ Rout, int32_t* __restrict__ info,
+                                const int32_t* __restrict__ gate) {
   using S = Sc<T>;
+  // gated off: the near-identity factor is already in P / Rout / info (the
+  // block factorizations returned at once; the block products in between ran
+  // on scratch nobody reads)
+  if (gate && *gate == 0) return;
   const int n2 = n - n1;
   __shared__ int pos[256];
   __shared__ int kidx[256];
@@ -420,7 +425,7 @@ void chol_blocked(Handle* h, int dtype, int n, const T* G, double drop_tol, doub
   gemm_any(h, dtype, false, false, n1, n2, n1, X11, n1, R12, n2, T1, n2);
   gemm_any(h, dtype, false, false, n1, n2, n2, T1, n2, X22, n2, X12, n2);
   assemble_kernel<T><<<64, 256, 0, h->stream>>>(n, n1, X11, X12, X22, R11, R12, R22, inf,
-                                                 inf + 4, P, R, info);
+                                                 inf + 4, P, R, info, h->gate);
   LR_CHECK_LAUNCH();
 }
 
@@ -498,7 +503,7 @@ void chol_near_identity(Handle* h, int dtype, int64_t n, const void* G, double d
     const char* e = getenv("LR_CHOL_NEARID");
     mode = (e && e[0] == '0') ? 0 : 1;
   }
-  if (!mode || (n > MAXN && !chol_panel_supported(n, cplx))) {   // exact (blocked: not gated)
+  if (!mode || (n > MAXN && !chol_panel_supported(n, cplx) && !chol_blocked_supported(n))) {
     if (cplx) chol_drop_c128(h, n, static_cast<const double2*>(G), drop_tol, unres_rel, 0.0,
                              static_cast<double2*>(P), static_cast<double2*>(R), info);
     else chol_drop_f64(h, n, static_cast<const double*>(G), drop_tol, unres_rel, 0.0,

@@ -18,11 +18,13 @@ from __future__ import annotations
 import math
 from dataclasses import dataclass, field
 
+import os
+
 import numpy as np
 
 from . import config
 from . import _lib
-from .core import (_out, _outs, _torch, _wide, apply_dev, as_operator, cast_dev, gemm, gemm_dev,
+from .core import (HostPrefetch, _out, _outs, _torch, _wide, apply_dev, as_operator, cast_dev, gemm, gemm_dev,
                    is_device_array, small_eig_hermitian_dev, small_svd_dev,
                    small_svd_from_adjoint, speculate, to_device)
 from .rangefinder import (RangeBasis, SketchSpec, _cast_like_op, _check_ell, _host_io,
@@ -570,6 +572,10 @@ def randomized_svd(A, k, p=config.DEFAULT_OVERSAMPLE, q=0, seed=0, sketch="gauss
     est_error) with numpy outputs for numpy input."""
     torch = _torch()
     op = as_operator(A)
+    if op is not A:
+        # an operator made for this call only (a host array is uploaded per
+        # call): nothing to replay later, so never pay a graph capture for it
+        op._ephemeral = True
     ell = int(k) + int(p)
     host = _host_io(A, op)
     if sketch in ("gauss", "gaussian"):
@@ -604,19 +610,29 @@ def randomized_svd(A, k, p=config.DEFAULT_OVERSAMPLE, q=0, seed=0, sketch="gauss
             Q = orth_dev(srft_dev(op.array, srft, amax=getattr(op, "amax", None)))
         else:
             Q = orth_dev(gsrft_dev(op.array, srft, amax=getattr(op, "amax", None)))
+        if (host and Q.is_cuda and not torch.cuda.is_current_stream_capturing()
+                and os.environ.get("LR_NO_PREFETCH") != "1"):
+            # host outputs: Q's download runs behind the last pass and the small SVD
+            early["Q"] = (Q, HostPrefetch(Q))
         U, S, V = direct_svd_dev(op, Q, orthonormal=True)
         est_dev = None
         if estimate and Q.shape[1]:
             est_dev = posterior_error_estimate_dev(op, Q, probes, alpha, seed + 13, W=W)
         return Q, U, S, V, est_dev
 
+    early = {}
     result = _run_step(op, body, key=(k, p, q, seed, spec.kind, probes, alpha, estimate))
     Q, U, S, V, est_dev = result
     est = 0.0 if Q.shape[1] == 0 else (float(est_dev.item()) if est_dev is not None else None)
     if truncate:
         kk = min(int(k), U.shape[1])
         U, S, V = U[:, :kk], S[:kk], V[:, :kk]
-    Q, U, S, V = _outs(host, Q, U, S, V)
+    pre = early.get("Q")
+    if host and pre is not None and pre[0] is Q:
+        U, S, V = _outs(host, U, S, V)
+        Q = pre[1].numpy()
+    else:
+        Q, U, S, V = _outs(host, Q, U, S, V)
     basis = RangeBasis(Q=Q, samples_used=ell, passes=passes, est_error=est, spec=spec)
     return basis, PartialSVD(U=U, sigma=S, V=V), est
 
@@ -717,7 +733,8 @@ def _run_step(op, body, key):
     torch = _torch()
     counters = _snapshot(op)
     gk = _graph_key(op)
-    graphable = gk is not None and _graph_enabled() and key[4] in ("gaussian", "srft", "gsrft")
+    graphable = (gk is not None and _graph_enabled() and key[4] in ("gaussian", "srft", "gsrft")
+                 and not getattr(op, "_ephemeral", False))
     if graphable:
         gkey = (id(op),) + gk + (torch.cuda.current_device(),) + tuple(key)
         entry = _GRAPHS.get(gkey)
