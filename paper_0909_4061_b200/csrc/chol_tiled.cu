@@ -454,43 +454,62 @@ namespace {
 // dependency.  One CTA checks max|E|, writes the first-order P / R / info
 // and clears *gate; otherwise it sets *gate and the exact kernel (launched
 // right behind it, gated) runs.
+// Two grid-wide kernels (one CTA moved 4 n^2 elements through a single SM:
+// 61 us at n = 256): the check ORs "not near-identity" into *gate (zeroed by
+// the caller), the write runs only when the gate stayed clear.
 template <typename T>
-__global__ void near_identity_kernel(int n, const T* __restrict__ G, T* __restrict__ P,
-                                     T* __restrict__ Rout, int32_t* __restrict__ info,
-                                     int32_t* __restrict__ gate, double thr) {
+__global__ void near_identity_check(int n, const T* __restrict__ G, int32_t* __restrict__ gate,
+                                    double thr) {
   using S = Sc<T>;
-  __shared__ int s_bad;
-  if (threadIdx.x == 0) s_bad = 0;
-  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   int bad = 0;
-  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
-    const int i = e / n, k = e - i * n;
-    const T g = G[e];
-    const double dev = (i == k) ? fabs(S::re(g) - 1.0) + fabs(S::abs2(g) - S::re(g) * S::re(g))
-                                : sqrt(S::abs2(g));
-    if (!(dev <= thr)) bad = 1;   // also catches NaN
+  for (int i = blockIdx.x * nw + warp; i < n; i += gridDim.x * nw) {
+    const T* row = G + size_t(i) * n;
+#pragma unroll 8
+    for (int k = lane; k < n; k += 32) {
+      const T g = row[k];
+      const double dev = (i == k) ? fabs(S::re(g) - 1.0) + fabs(S::abs2(g) - S::re(g) * S::re(g))
+                                  : sqrt(S::abs2(g));
+      if (!(dev <= thr)) bad = 1;   // also catches NaN
+    }
   }
-  if (bad) atomicOr(&s_bad, 1);
-  __syncthreads();
-  const bool ok = s_bad == 0;
-  if (ok) {
-    for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
-      const int i = e / n, k = e - i * n;
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(gate, 1);
+}
+
+template <typename T>
+__global__ void near_identity_write(int n, const T* __restrict__ G, T* __restrict__ P,
+                                    T* __restrict__ Rout, int32_t* __restrict__ info,
+                                    const int32_t* __restrict__ gate) {
+  using S = Sc<T>;
+  if (*gate != 0) return;   // the exact kernels behind this one run instead
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int i = blockIdx.x * nw + warp; i < n; i += gridDim.x * nw) {
+    const size_t ro = size_t(i) * n;
+#pragma unroll 8
+    for (int k = lane; k < n; k += 32) {
       T nv = S::zero();
-      if (k > i) nv = G[e];
-      else if (k == i) nv = S::make(0.5 * (S::re(G[e]) - 1.0), 0.0);
-      Rout[e] = (k == i) ? S::add(S::one(), nv) : nv;
-      P[e] = (k == i) ? S::sub(S::one(), nv) : S::scale(nv, -1.0);
+      if (k > i) nv = G[ro + k];
+      else if (k == i) nv = S::make(0.5 * (S::re(G[ro + k]) - 1.0), 0.0);
+      Rout[ro + k] = (k == i) ? S::add(S::one(), nv) : nv;
+      P[ro + k] = (k == i) ? S::sub(S::one(), nv) : S::scale(nv, -1.0);
     }
   }
-  if (threadIdx.x == 0) {
-    if (ok) {
-      info[0] = n;
-      info[1] = 0;
-      info[2] = 0;
-    }
-    *gate = ok ? 0 : 1;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    info[0] = n;
+    info[1] = 0;
+    info[2] = 0;
   }
+}
+
+template <typename T>
+void launch_near_identity(Handle* h, int n, const T* G, T* P, T* R, int32_t* info, int32_t* gate,
+                          double thr) {
+  LR_CUDA(cudaMemsetAsync(gate, 0, sizeof(int32_t), h->stream));
+  const int blocks = (n + 7) / 8;   // 8 warps per CTA, one row per warp
+  near_identity_check<T><<<blocks, 256, 0, h->stream>>>(n, G, gate, thr);
+  LR_CHECK_LAUNCH();
+  near_identity_write<T><<<blocks, 256, 0, h->stream>>>(n, G, P, R, info, gate);
+  LR_CHECK_LAUNCH();
 }
 
 }  // namespace
@@ -512,14 +531,12 @@ void chol_near_identity(Handle* h, int dtype, int64_t n, const void* G, double d
   }
   int32_t* gate = pool_alloc_t<int32_t>(h, 1);
   if (cplx)
-    near_identity_kernel<double2><<<1, 1024, 0, h->stream>>>(
-        int(n), static_cast<const double2*>(G), static_cast<double2*>(P),
-        static_cast<double2*>(R), info, gate, thr);
+    launch_near_identity<double2>(h, int(n), static_cast<const double2*>(G),
+                                  static_cast<double2*>(P), static_cast<double2*>(R), info, gate,
+                                  thr);
   else
-    near_identity_kernel<double><<<1, 1024, 0, h->stream>>>(
-        int(n), static_cast<const double*>(G), static_cast<double*>(P), static_cast<double*>(R),
-        info, gate, thr);
-  LR_CHECK_LAUNCH();
+    launch_near_identity<double>(h, int(n), static_cast<const double*>(G),
+                                 static_cast<double*>(P), static_cast<double*>(R), info, gate, thr);
   const int32_t* saved = h->gate;
   h->gate = gate;
   try {

@@ -212,6 +212,10 @@ void gram_f32(Handle* h, int64_t m, int64_t ell, const float* Y, int64_t ldy, do
 // C (M x N, ldc) = sum over S dense M x N partials, fixed order
 void splitk_reduce(Handle* h, int64_t M, int64_t N, int S, const double* part, double* C,
                    int64_t ldc);
+// gemm_small.cu: fp64 products small in every dimension (one 32 x 32 tile per CTA)
+bool gemm_small_ok(int64_t M, int64_t N, int64_t K);
+void gemm_small_f64(Handle* h, bool transA, int64_t M, int64_t N, int64_t K, const double* A,
+                    int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc);
 // gemm_skinny.cu: A^T B for K >> M, N <= 64 (fp64)
 bool gemm_skinny_ok(bool transA, int64_t M, int64_t N, int64_t K);
 void gemm_skinny_tn(Handle* h, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,

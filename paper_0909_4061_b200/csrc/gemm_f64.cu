@@ -372,6 +372,10 @@ void gemm_f64(Handle* h, bool transA, int64_t M, int64_t N, int64_t K, const dou
       LR_CUDA(cudaMemsetAsync(C + r * ldc, 0, N * sizeof(double), h->stream));
     return;
   }
+  if (gemm_small_ok(M, N, K)) {
+    gemm_small_f64(h, transA, M, N, K, A, lda, B, ldb, C, ldc);
+    return;
+  }
   if (gemm_skinny_nn_ok(transA, M, N, K, C, ldc)) {
     gemm_skinny_nn(h, M, N, K, A, lda, B, ldb, C, ldc);
     return;
