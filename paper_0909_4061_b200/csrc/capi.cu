@@ -112,9 +112,17 @@ void chol_any(Handle* h, int dtype, int64_t ell, const void* G, double tol, doub
 // amax_hint > 0: a bound on max|Y| known to the caller (an orthonormal panel:
 // |y_ij| <= ||y_j|| ~ 1), which saves the fp32 split its device-side max|Y|
 // pass (one extra read of the m x k panel)
+// tri: P is a square upper-triangular factor (no dropped columns -- the
+// speculative paths, whose result is discarded when a column was dropped)
 void apply_right(Handle* h, int dtype, int64_t m, int64_t k, int64_t ncols, const void* Y,
                  int64_t ldy, const void* P, int64_t ldp, void* out, int64_t ldo,
-                 double amax_hint = -1.0) {
+                 double amax_hint = -1.0, bool tri = false) {
+  if (tri && dtype == LR_F64 && k == ncols &&
+      gemm_skinny_tri_ok(m, ncols, k, static_cast<const double*>(out), ldo)) {
+    gemm_skinny_tri(h, m, ncols, k, static_cast<const double*>(Y), ldy,
+                    static_cast<const double*>(P), ldp, static_cast<double*>(out), ldo);
+    return;
+  }
   if (dtype == LR_F64 || dtype == LR_C128) {
     gemm_any(h, dtype, false, false, m, ncols, k, Y, ldy, P, ldp, out, ldo);
     return;
@@ -312,12 +320,12 @@ void orth_fast_impl(Handle* h, int dtype, int64_t m, int64_t ell, const void* Y,
   gram_any(h, dtype, m, ell, Y, ldy, G);
   if (h->sharded) comm_allreduce_wide(h, wide_of(dtype), ell * ell, G);   // sum_r Y_r^H Y_r
   chol_any(h, dtype, ell, G, tol, unres, 0.0, P, R, h->d_info);
-  apply_right(h, dtype, m, ell, ell, Y, ldy, P, ell, Q1, ell);
+  apply_right(h, dtype, m, ell, ell, Y, ldy, P, ell, Q1, ell, -1.0, true);
   gram_second(h, dtype, m, ell, Q1, ell, G);
   if (h->sharded) comm_allreduce_wide(h, wide_of(dtype), ell * ell, G);
   chol_near_identity(h, wide_of(dtype), ell, G, tol, unres, P, R, h->d_info,
                      near_id_thr(dtype));
-  apply_right(h, dtype, m, ell, ell, Q1, ell, P, ell, Q, ldq, ORTHO_AMAX);
+  apply_right(h, dtype, m, ell, ell, Q1, ell, P, ell, Q, ldq, ORTHO_AMAX, true);
 }
 
 // orth_fast_impl without its last product: Q1 (m x ell, ld ell) and the
@@ -339,7 +347,7 @@ void orth_fast_deferred_impl(Handle* h, int dtype, int64_t m, int64_t ell, const
   const double unres = 4.0 * double(ell) * U64;
   gram_any(h, dtype, m, ell, Y, ldy, G);
   chol_any(h, dtype, ell, G, tol, unres, 0.0, P, R, h->d_info);
-  apply_right(h, dtype, m, ell, ell, Y, ldy, P, ell, Q1, ell);
+  apply_right(h, dtype, m, ell, ell, Y, ldy, P, ell, Q1, ell, -1.0, true);
   gram_second(h, dtype, m, ell, Q1, ell, G);
   chol_near_identity(h, wide_of(dtype), ell, G, tol, unres, P2, R, h->d_info,
                      near_id_thr(dtype));

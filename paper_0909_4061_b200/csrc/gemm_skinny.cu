@@ -34,8 +34,10 @@ __device__ __forceinline__ void dmma_sk(double (&c)[4], double a0, double a1, do
       : "d"(a0), "d"(a1), "d"(b0));
 }
 
-// grid.x = CTAs, each owns rows [blockIdx.x * rows_per, ...) of A and B
-template <int MF, int NF8>
+// grid.x = CTAs, each owns rows [blockIdx.x * rows_per, ...) of A and B.
+// SYM (A == B, a Gram): tiles entirely below the diagonal (8 nf + 7 < 16 mf)
+// are skipped -- 12 of 18 tiles at 48 x 48 -- and mirrored after the reduction.
+template <int MF, int NF8, bool SYM>
 __global__ void __launch_bounds__(SK_THREADS)
 skinny_tn_kernel(int64_t M, int64_t N, int64_t K, const double* __restrict__ A, int64_t lda,
                  const double* __restrict__ B, int64_t ldb, double* __restrict__ part,
@@ -53,35 +55,68 @@ skinny_tn_kernel(int64_t M, int64_t N, int64_t K, const double* __restrict__ A, 
 #pragma unroll
       for (int e = 0; e < 4; ++e) acc[i][j][e] = 0.0;
 
-  constexpr int SK_UNROLL = sk_unroll<MF, NF8>();
+  // SYM with NF8 == 2 MF: the B fragments ARE the A fragments (lane (g, t)
+  // holds Y[k + t][16 mf + g (+ 8)] either way), so B is never loaded and the
+  // registers go to a deeper unroll -- the Gram was latency-bound at 39 % of
+  // HBM with two k4-steps in flight per warp (24 KB per SM)
+  constexpr bool REUSE = SYM && NF8 == 2 * MF;
+  constexpr int SK_UNROLL = REUSE ? 4 : sk_unroll<MF, NF8>();
   // warp w takes k4-steps w, w + 8, ... of the CTA's rows, SK_UNROLL at a time
   const int64_t nsteps = (r1 - r0 + 3) / 4;
-  for (int64_t s0 = int64_t(warp) * SK_UNROLL; s0 < nsteps; s0 += int64_t(SK_WARPS) * SK_UNROLL) {
-    double a[SK_UNROLL][MF][2], b[SK_UNROLL][NF8];
+  auto load = [&](int64_t s0, double (&a)[SK_UNROLL][MF][2], double (&b)[SK_UNROLL][REUSE ? 1 : NF8]) {
 #pragma unroll
     for (int u = 0; u < SK_UNROLL; ++u) {
       const int64_t k = r0 + (s0 + u) * 4 + t;
       const bool kin = (s0 + u) < nsteps && k < r1;
       const double* ar = A + k * lda;
-      const double* br = B + k * ldb;
 #pragma unroll
       for (int mf = 0; mf < MF; ++mf) {
         const int i0 = mf * 16 + g, i1 = i0 + 8;
         a[u][mf][0] = (kin && i0 < M) ? __ldg(ar + i0) : 0.0;
         a[u][mf][1] = (kin && i1 < M) ? __ldg(ar + i1) : 0.0;
       }
+      if constexpr (!REUSE) {
+        const double* br = B + k * ldb;
 #pragma unroll
-      for (int nf = 0; nf < NF8; ++nf) {
-        const int j = nf * 8 + g;
-        b[u][nf] = (kin && j < N) ? __ldg(br + j) : 0.0;
+        for (int nf = 0; nf < NF8; ++nf) {
+          const int j = nf * 8 + g;
+          b[u][nf] = (kin && j < N) ? __ldg(br + j) : 0.0;
+        }
       }
     }
+  };
+  auto mma = [&](double (&a)[SK_UNROLL][MF][2], double (&b)[SK_UNROLL][REUSE ? 1 : NF8]) {
 #pragma unroll
     for (int u = 0; u < SK_UNROLL; ++u)
 #pragma unroll
       for (int nf = 0; nf < NF8; ++nf)
 #pragma unroll
-        for (int mf = 0; mf < MF; ++mf) dmma_sk(acc[mf][nf], a[u][mf][0], a[u][mf][1], b[u][nf]);
+        for (int mf = 0; mf < MF; ++mf)
+          if (!SYM || 8 * nf + 7 >= 16 * mf) {
+            const double bv = REUSE ? a[u][nf >> 1][nf & 1] : b[u][REUSE ? 0 : nf];
+            dmma_sk(acc[mf][nf], a[u][mf][0], a[u][mf][1], bv);
+          }
+  };
+  const int64_t sstride = int64_t(SK_WARPS) * SK_UNROLL;
+  if constexpr (REUSE) {
+    // software pipeline: the next batch of fragments is in flight while this
+    // batch's DMMAs run (without it every batch paid a full HBM round trip:
+    // 289 us for 805 MB, 43 % of the copy rate)
+    double a0[SK_UNROLL][MF][2], a1[SK_UNROLL][MF][2], bd[SK_UNROLL][1];
+    int64_t s0 = int64_t(warp) * SK_UNROLL;
+    load(s0, a0, bd);
+    for (; s0 < nsteps; s0 += 2 * sstride) {
+      load(s0 + sstride, a1, bd);
+      mma(a0, bd);
+      load(s0 + 2 * sstride, a0, bd);
+      mma(a1, bd);
+    }
+  } else {
+    for (int64_t s0 = int64_t(warp) * SK_UNROLL; s0 < nsteps; s0 += sstride) {
+      double a[SK_UNROLL][MF][2], b[SK_UNROLL][NF8];
+      load(s0, a, b);
+      mma(a, b);
+    }
   }
   // accumulator layout (m16n8 fp64): c0,c1 at (g, 2t..2t+1), c2,c3 at (g+8, 2t..2t+1);
   // warps add their partials in a fixed order (deterministic)
@@ -114,6 +149,13 @@ skinny_tn_kernel(int64_t M, int64_t N, int64_t K, const double* __restrict__ A, 
   }
 }
 
+__global__ void skinny_mirror_kernel(int n, double* __restrict__ C, int64_t ldc) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n * n; e += gridDim.x * blockDim.x) {
+    const int i = e / n, j = e - i * n;
+    if (j < i) C[int64_t(i) * ldc + j] = C[int64_t(j) * ldc + i];
+  }
+}
+
 template <int MF, int NF8>
 void launch_skinny(Handle* h, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
                    const double* B, int64_t ldb, double* C, int64_t ldc) {
@@ -122,17 +164,30 @@ void launch_skinny(Handle* h, int64_t M, int64_t N, int64_t K, const double* A, 
   const int64_t rows_per = ((ceil_div(K, ctas) + 3) / 4) * 4;
   ctas = ceil_div(K, rows_per);
   double* part = pool_alloc_t<double>(h, size_t(ctas) * M * N);
-  skinny_tn_kernel<MF, NF8><<<unsigned(ctas), SK_THREADS, 0, h->stream>>>(M, N, K, A, lda, B, ldb,
-                                                                          part, rows_per);
+  const bool sym = (A == B && lda == ldb && M == N);
+  if (sym)
+    skinny_tn_kernel<MF, NF8, true><<<unsigned(ctas), SK_THREADS, 0, h->stream>>>(
+        M, N, K, A, lda, B, ldb, part, rows_per);
+  else
+    skinny_tn_kernel<MF, NF8, false><<<unsigned(ctas), SK_THREADS, 0, h->stream>>>(
+        M, N, K, A, lda, B, ldb, part, rows_per);
   LR_CHECK_LAUNCH();
   splitk_reduce(h, M, N, int(ctas), part, C, ldc);
+  if (sym) {
+    skinny_mirror_kernel<<<unsigned(ceil_div(M * N, 256)), 256, 0, h->stream>>>(int(M), C, ldc);
+    LR_CHECK_LAUNCH();
+  }
 }
 
 // C (M x N) = A (M x K) B (K x N) for M >> K, N <= 64 (the applies Y P of a
 // narrow panel and config 5's L Z): B staged in shared memory once per CTA,
 // every warp streams 16-row tiles of A (fragments straight from global),
 // K/4 x NF8 DMMAs per tile, 16-byte stores of the accumulator pairs.
-template <int NF8, int KS>   // KS = k4 steps (K <= 4 KS)
+// TRI: B is upper triangular (an inverse Cholesky factor): output columns
+// 8 nf .. 8 nf + 7 only take k <= 8 nf + 7, i.e. the k4 steps ks <= 2 nf + 1 --
+// 42 of 72 DMMAs at 48 x 48, which moves the product from the DMMA pipe's bound
+// to HBM's.
+template <int NF8, int KS, bool TRI>   // KS = k4 steps (K <= 4 KS)
 __global__ void __launch_bounds__(SK_THREADS)
 skinny_nn_kernel(int64_t M, int64_t N, int64_t K, const double* __restrict__ A, int64_t lda,
                  const double* __restrict__ B, int64_t ldb, double* __restrict__ C,
@@ -175,7 +230,7 @@ skinny_nn_kernel(int64_t M, int64_t N, int64_t K, const double* __restrict__ A, 
     for (int ks = 0; ks < KS; ++ks)
 #pragma unroll
       for (int nf = 0; nf < NF8; ++nf)
-        dmma_sk(acc[nf], a[ks][0], a[ks][1], bs[4 * ks + t][nf * 8 + g]);
+        if (!TRI || ks <= 2 * nf + 1) dmma_sk(acc[nf], a[ks][0], a[ks][1], bs[4 * ks + t][nf * 8 + g]);
 #pragma unroll
     for (int nf = 0; nf < NF8; ++nf) {
       const int64_t j = nf * 8 + 2 * t;
@@ -195,13 +250,13 @@ skinny_nn_kernel(int64_t M, int64_t N, int64_t K, const double* __restrict__ A, 
   }
 }
 
-template <int NF8, int KS>
+template <int NF8, int KS, bool TRI = false>
 void launch_skinny_nn(Handle* h, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
                       const double* B, int64_t ldb, double* C, int64_t ldc) {
   const int64_t ntiles = ceil_div(M, 16);
   const int64_t ctas = std::min<int64_t>(4 * h->sm_count, ceil_div(ntiles, SK_WARPS));
-  skinny_nn_kernel<NF8, KS><<<unsigned(ctas), SK_THREADS, 0, h->stream>>>(M, N, K, A, lda, B, ldb,
-                                                                          C, ldc);
+  skinny_nn_kernel<NF8, KS, TRI><<<unsigned(ctas), SK_THREADS, 0, h->stream>>>(M, N, K, A, lda, B,
+                                                                               ldb, C, ldc);
   LR_CHECK_LAUNCH();
 }
 
@@ -245,6 +300,26 @@ bool gemm_skinny_nn_ok(bool transA, int64_t M, int64_t N, int64_t K, const doubl
   // at K = 48 where the tiled kernel's larger warp tile wins -- K <= 32 only
   return !off && !transA && K <= 32 && N <= 64 && M >= 65536 && (ldc % 2) == 0 &&
          (reinterpret_cast<uintptr_t>(C) & 15) == 0;
+}
+
+// C = A B with B (K x N, K == N) upper triangular: a tall panel times an
+// inverse Cholesky factor (orthonormalize_double_gs' Y R^{-1}, core.py:84-115)
+bool gemm_skinny_tri_ok(int64_t M, int64_t N, int64_t K, const double* C, int64_t ldc) {
+  static int off = -1;
+  if (off < 0) {
+    const char* e = getenv("LR_SKINNY");
+    off = (e && e[0] == '0') ? 1 : 0;
+  }
+  return !off && K == N && N <= 64 && N >= 8 && M >= 65536 && (ldc % 2) == 0 &&
+         (reinterpret_cast<uintptr_t>(C) & 15) == 0;
+}
+
+void gemm_skinny_tri(Handle* h, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
+                     const double* B, int64_t ldb, double* C, int64_t ldc) {
+  const int nf = int(ceil_div(N, 8));
+  if (nf <= 4) launch_skinny_nn<4, 8, true>(h, M, N, K, A, lda, B, ldb, C, ldc);
+  else if (nf <= 6) launch_skinny_nn<6, 12, true>(h, M, N, K, A, lda, B, ldb, C, ldc);
+  else launch_skinny_nn<8, 16, true>(h, M, N, K, A, lda, B, ldb, C, ldc);
 }
 
 void gemm_skinny_nn(Handle* h, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
