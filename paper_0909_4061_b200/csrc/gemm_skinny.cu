@@ -60,7 +60,9 @@ skinny_tn_kernel(int64_t M, int64_t N, int64_t K, const double* __restrict__ A, 
   // registers go to a deeper unroll -- the Gram was latency-bound at 39 % of
   // HBM with two k4-steps in flight per warp (24 KB per SM)
   constexpr bool REUSE = SYM && NF8 == 2 * MF;
-  constexpr int SK_UNROLL = REUSE ? 4 : sk_unroll<MF, NF8>();
+  // two register buffers of fragments (software pipeline) where they fit
+  constexpr bool PIPE = REUSE || MF * NF8 <= 12;
+  constexpr int SK_UNROLL = REUSE ? 4 : (PIPE ? 2 : sk_unroll<MF, NF8>());
   // warp w takes k4-steps w, w + 8, ... of the CTA's rows, SK_UNROLL at a time
   const int64_t nsteps = (r1 - r0 + 3) / 4;
   auto load = [&](int64_t s0, double (&a)[SK_UNROLL][MF][2], double (&b)[SK_UNROLL][REUSE ? 1 : NF8]) {
@@ -98,18 +100,19 @@ skinny_tn_kernel(int64_t M, int64_t N, int64_t K, const double* __restrict__ A, 
           }
   };
   const int64_t sstride = int64_t(SK_WARPS) * SK_UNROLL;
-  if constexpr (REUSE) {
+  if constexpr (PIPE) {
     // software pipeline: the next batch of fragments is in flight while this
     // batch's DMMAs run (without it every batch paid a full HBM round trip:
-    // 289 us for 805 MB, 43 % of the copy rate)
-    double a0[SK_UNROLL][MF][2], a1[SK_UNROLL][MF][2], bd[SK_UNROLL][1];
+    // 289 us for the 805 MB Gram, 43 % of the copy rate)
+    constexpr int NB = REUSE ? 1 : NF8;
+    double a0[SK_UNROLL][MF][2], a1[SK_UNROLL][MF][2], b0[SK_UNROLL][NB], b1[SK_UNROLL][NB];
     int64_t s0 = int64_t(warp) * SK_UNROLL;
-    load(s0, a0, bd);
+    load(s0, a0, b0);
     for (; s0 < nsteps; s0 += 2 * sstride) {
-      load(s0 + sstride, a1, bd);
-      mma(a0, bd);
-      load(s0 + 2 * sstride, a0, bd);
-      mma(a1, bd);
+      load(s0 + sstride, a1, b1);
+      mma(a0, b0);
+      load(s0 + 2 * sstride, a0, b0);
+      mma(a1, b1);
     }
   } else {
     for (int64_t s0 = int64_t(warp) * SK_UNROLL; s0 < nsteps; s0 += sstride) {
