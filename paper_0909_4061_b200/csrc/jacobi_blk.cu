@@ -384,12 +384,17 @@ jacobi_cl_kernel(int n, const T* __restrict__ Rin, T* __restrict__ Mout, double*
       subround<T, R, 0, 3, 1, 2, 4, 7, 5, 6>(x, nrmv, lane, tol, did);
     }
     for (int rd = 0; rd < nbp - 1; ++rd) {
+#ifndef LR_JAC_NOSUB     // development: time the exchange alone
       if (active) {
         subround<T, R, 0, 4, 1, 5, 2, 6, 3, 7>(x, nrmv, lane, tol, did);
         subround<T, R, 0, 5, 1, 6, 2, 7, 3, 4>(x, nrmv, lane, tol, did);
         subround<T, R, 0, 6, 1, 7, 2, 4, 3, 5>(x, nrmv, lane, tol, did);
         subround<T, R, 0, 7, 1, 4, 2, 5, 3, 6>(x, nrmv, lane, tol, did);
       }
+#endif
+#ifdef LR_JAC_NOXCHG     // development: time the rotations alone
+      continue;
+#endif
       cluster.sync();   // every slot has been read
       if (active) {
         const int dt = (w == 0) ? -1 : (w + 1 < P ? w + 1 : 2 * P - 1);
