@@ -483,9 +483,27 @@ def run_sparse(args, cfg):
         "roofline": roofline_sparse(cfg, pev, ms, args.steps, passes),
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
-        "e2e": {"skipped": "host CSR transpose of the operator constructor dominates; "
-                           "not measured for config 5 in this round"},
     }
+    if not args.no_e2e and rank == 0:
+        # end to end: scipy CSR + numpy factors on the host in (operator built
+        # per call: upload, device-side transpose), numpy factors out
+        def once():
+            o = lr.CudaCsrOperator(S, L, R, host_io=True)
+            return lr.randomized_svd(o, cfg.k, cfg.p, cfg.q, cfg.seed, estimate=False)
+        for _ in range(3):
+            res = once()
+        torch.cuda.synchronize()
+        k_e2e = max(1, min(args.steps, 5))
+        t0 = time.perf_counter()
+        for _ in range(k_e2e):
+            res = once()
+        dt = (time.perf_counter() - t0) / k_e2e
+        f = res[1]
+        h2d = S.data.nbytes + S.indices.nbytes + (S.shape[0] + 1) * 8 + L.nbytes + R.nbytes
+        d2h = res[0].Q.nbytes + f.U.nbytes + f.sigma.nbytes + f.V.nbytes
+        line["e2e"] = {"value": round(passes * a_bytes / dt / 1e9, 3), "unit": "A-GB/s",
+                       "ms_per_step": round(dt * 1e3, 3), "h2d_bytes_per_step": int(h2d),
+                       "d2h_bytes_per_step": int(d2h), "steps": k_e2e}
     if not args.no_cpu and rank == 0:
         line["cpu_baseline"] = cpu_baseline(cfg)
     if rank == 0:
@@ -689,7 +707,7 @@ def e2e_measure(args, cfg, A, lr):
         # pinned CPU tensor in (async H2D at full PCIe rate), numpy factors out
         b, f, _ = lr.randomized_svd(host, cfg.k, cfg.p, cfg.q, cfg.seed, sketch=cfg.sketch,
                                     estimate=False)
-        return f
+        return b, f
 
     # warm-up: allocator / pinned-buffer caches settle by the 3rd call.  The
     # previous call's factors stay referenced while the next call runs, as in
@@ -702,13 +720,13 @@ def e2e_measure(args, cfg, A, lr):
     per_call = []
     for _ in range(steps):
         tc = time.perf_counter()
-        f = once()
+        b, f = once()
         per_call.append(time.perf_counter() - tc)
     dt = (time.perf_counter() - t0) / steps
     if os.environ.get("LR_E2E_DEBUG"):
         print("e2e per call (ms):", [round(1e3 * x, 1) for x in per_call], file=sys.stderr)
     a_bytes = A.numel() * A.element_size()
-    d2h = f.U.nbytes + f.sigma.nbytes + f.V.nbytes
+    d2h = b.Q.nbytes + f.U.nbytes + f.sigma.nbytes + f.V.nbytes   # the basis comes back too
     return {"value": round(cfg.passes() * a_bytes / dt / 1e9, 3), "unit": "A-GB/s",
             "ms_per_step": round(dt * 1e3, 3), "h2d_bytes_per_step": int(a_bytes),
             "d2h_bytes_per_step": int(d2h), "steps": steps}
