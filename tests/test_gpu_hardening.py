@@ -208,3 +208,18 @@ def test_sketch_preconditioned_orth_repeatable():
         with core.speculate(status):
             outs.append(core.orth_dev(Y).clone())
     assert torch.equal(outs[0], outs[1])
+
+
+def test_sketch_preconditioned_orth_strided_panel():
+    """The panel may be a column slice of a wider array (row stride > ell)."""
+    from paper_0909_4061_b200 import core
+    wide = _tall_panel(131072, 256, 1e5, 21)
+    Y = wide[:, 64:192]
+    assert Y.stride(0) == 256 and Y.shape[1] == 128
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    with core.speculate(status):
+        Q = core.orth_dev(Y)
+    torch.cuda.synchronize()
+    assert int(status.item()) == 0
+    orth, span, low = _orth_quality(Y.contiguous(), Q)
+    assert orth <= 1e-6 and span <= 5e-6 and low <= 2e-6

@@ -515,3 +515,48 @@ def test_ozaki_fp64_pass(m, n, ell, adjoint):
     bound = (np.abs(A).T @ np.abs(X)) if adjoint else (np.abs(A) @ np.abs(X))
     err = np.abs(Y.cpu().numpy().astype(np.longdouble) - ref)
     assert float((err / np.maximum(bound, 1e-300)).max()) <= 2.0 ** -50
+
+
+@pytest.mark.parametrize("M,N,K", [(256, 256, 256), (110, 110, 110), (30, 30, 30), (16, 500, 33),
+                                   (257, 19, 512), (120, 240, 240), (48, 48, 1)])
+@pytest.mark.parametrize("trans", [False, True])
+def test_gemm_small(M, N, K, trans):
+    """fp64 products small in every dimension (gemm_small.cu: one 32 x 32 tile
+    per CTA, no split-K) -- the ell^3 algebra around the factorizations --
+    against numpy, both operand orientations, ragged tiles, and a strided C."""
+    from paper_0909_4061_b200 import _lib
+    g = np.random.default_rng(M + 7 * N + 13 * K)
+    A = torch.from_numpy(g.standard_normal((K, M) if trans else (M, K))).cuda()
+    B = torch.from_numpy(g.standard_normal((K, N))).cuda()
+    Cfull = torch.zeros((M, N + 3), dtype=torch.float64, device="cuda")
+    C = Cfull[:, :N]
+    rows, cols = A.shape
+    _lib.call("lr_gemm", _lib.handle(), _lib.F64, _lib.OP_T if trans else _lib.OP_N, rows, cols, N,
+              _lib.ptr(A), _lib.ld(A), _lib.ptr(B), _lib.ld(B), _lib.ptr(C), _lib.ld(C))
+    An = A.cpu().numpy()
+    ref = (An.T if trans else An) @ B.cpu().numpy()
+    assert np.abs(C.cpu().numpy() - ref).max() <= 1e-14 * max(K, 16) * 4
+    assert float(Cfull[:, N:].abs().max()) == 0.0        # nothing written past N
+
+
+def test_csr_transpose_on_device_is_canonical():
+    """The CSR of S^T built on the device (stable sort by column) equals
+    scipy's canonical transpose: same row pointers, indices ascending in every
+    row, same values -- including empty rows / columns and merged duplicates."""
+    import scipy.sparse as sp
+    from paper_0909_4061_b200.sparse import CudaCsrOperator
+    g = np.random.default_rng(12)
+    rows = g.integers(0, 900, 6000)
+    cols = g.integers(0, 700, 6000)
+    cols[cols == 5] = 6                      # an empty column
+    rows[rows == 17] = 18                    # an empty row
+    vals = g.standard_normal(6000)
+    S = sp.coo_matrix((vals, (rows, cols)), shape=(900, 700)).tocsr()   # duplicates are summed
+    op = CudaCsrOperator(S)
+    St = S.T.tocsr()
+    St.sum_duplicates()
+    St.sort_indices()
+    ptr, idx, val = (t.cpu().numpy() for t in op.St)
+    assert np.array_equal(ptr, St.indptr.astype(np.int64))
+    assert np.array_equal(idx, St.indices.astype(np.int32))
+    assert np.array_equal(val, St.data)
