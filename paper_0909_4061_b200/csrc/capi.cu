@@ -118,6 +118,12 @@ void apply_right(Handle* h, int dtype, int64_t m, int64_t k, int64_t ncols, cons
                  int64_t ldy, const void* P, int64_t ldp, void* out, int64_t ldo,
                  double amax_hint = -1.0, bool tri = false) {
   if (tri && dtype == LR_F64 && k == ncols &&
+      gemm_skinny_wide_ok(false, m, ncols, k, static_cast<const double*>(out), ldo)) {
+    gemm_skinny_wide(h, true, m, ncols, k, static_cast<const double*>(Y), ldy,
+                     static_cast<const double*>(P), ldp, static_cast<double*>(out), ldo);
+    return;
+  }
+  if (tri && dtype == LR_F64 && k == ncols &&
       gemm_skinny_tri_ok(m, ncols, k, static_cast<const double*>(out), ldo)) {
     gemm_skinny_tri(h, m, ncols, k, static_cast<const double*>(Y), ldy,
                     static_cast<const double*>(P), ldp, static_cast<double*>(out), ldo);

@@ -220,6 +220,10 @@ void gemm_small_f64(Handle* h, bool transA, int64_t M, int64_t N, int64_t K, con
 bool gemm_skinny_ok(bool transA, int64_t M, int64_t N, int64_t K);
 void gemm_skinny_tn(Handle* h, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
                     const double* B, int64_t ldb, double* C, int64_t ldc);
+bool gemm_skinny_wide_ok(bool transA, int64_t M, int64_t N, int64_t K, const double* C,
+                         int64_t ldc);
+void gemm_skinny_wide(Handle* h, bool tri, int64_t M, int64_t N, int64_t K, const double* A,
+                      int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc);
 bool gemm_skinny_tri_ok(int64_t M, int64_t N, int64_t K, const double* C, int64_t ldc);
 void gemm_skinny_tri(Handle* h, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
                      const double* B, int64_t ldb, double* C, int64_t ldc);

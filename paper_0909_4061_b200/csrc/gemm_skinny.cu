@@ -263,6 +263,125 @@ void launch_skinny_nn(Handle* h, int64_t M, int64_t N, int64_t K, const double* 
   LR_CHECK_LAUNCH();
 }
 
+
+// Wider B (64 < N <= 128, K <= 128): config 2's panel applies Y P / Q U~ with
+// ell = 110 (reference orthonormalize_double_gs / direct_svd, core.py:84-115,
+// factor.py:154-165).  The 128-row tiled kernel runs them on 64 CTAs at ~26 us
+// (8192 x 110 x 110: 0.2 GFLOP, 14 MB -- under 10 us of either roofline).  Here
+// a warp owns a 16-row tile over all N columns (14 x 4 accumulators); the K
+// extent is walked in chunks of 8 k4-steps with the next chunk's A fragments
+// in flight; B sits in shared memory (dynamic, K x (N8 + 1) doubles).  TRI as
+// in skinny_nn_kernel.  4 warps per CTA so that 8192 rows already fill 128 SMs.
+constexpr int SW_THREADS = 128;
+constexpr int SW_KC = 8;   // k4-steps per chunk
+
+template <int NF8, bool TRI>
+__global__ void __launch_bounds__(SW_THREADS)
+skinny_nn_wide_kernel(int64_t M, int64_t N, int64_t K, const double* __restrict__ A, int64_t lda,
+                      const double* __restrict__ B, int64_t ldb, double* __restrict__ C,
+                      int64_t ldc) {
+  extern __shared__ double bsw[];             // [Kp][BS], Kp = K rounded up to 4
+  constexpr int BS = NF8 * 8 + 1;
+  const int Kp = int((K + 3) / 4) * 4;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int64_t ntiles = (M + 15) / 16;
+  const int nks = Kp / 4;                     // k4-steps
+  const int nch = (nks + SW_KC - 1) / SW_KC;  // chunks
+  bool staged = false;
+  auto stage = [&]() {
+    // staging: thread j streams column j, 16 rows in flight (the flat loop with a
+    // division per element kept ~4 loads in flight: ~10 us for 99 KB, longer than
+    // the tile's own work)
+    if (threadIdx.x < NF8 * 8) {
+      const int j = threadIdx.x;
+      const bool jin = j < N;
+      const double* bj = B + (jin ? j : 0);
+#pragma unroll 1
+      for (int k0 = 0; k0 < Kp; k0 += 16) {
+        double v[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) v[u] = (jin && k0 + u < K) ? __ldg(bj + int64_t(k0 + u) * ldb) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+          if (k0 + u < Kp) bsw[(k0 + u) * BS + j] = v[u];
+      }
+    }
+    __syncthreads();
+  };
+  for (int64_t tile = int64_t(blockIdx.x) * (SW_THREADS / 32) + warp; tile < ntiles;
+       tile += int64_t(gridDim.x) * (SW_THREADS / 32)) {
+    const int64_t r0 = tile * 16 + g, r1 = r0 + 8;
+    const double* a0p = A + r0 * lda;
+    const double* a1p = A + r1 * lda;
+    auto load = [&](int ch, double (&a)[SW_KC][2]) {
+#pragma unroll
+      for (int u = 0; u < SW_KC; ++u) {
+        const int k = 4 * (ch * SW_KC + u) + t;
+        a[u][0] = (ch < nch && r0 < M && k < K) ? __ldg(a0p + k) : 0.0;
+        a[u][1] = (ch < nch && r1 < M && k < K) ? __ldg(a1p + k) : 0.0;
+      }
+    };
+    double acc[NF8][4];
+#pragma unroll
+    for (int nf = 0; nf < NF8; ++nf)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[nf][e] = 0.0;
+    double a[SW_KC][2], an[SW_KC][2];
+    load(0, a);
+    if (!staged) {   // B is staged while the first tile's first fragments are in flight
+      stage();
+      staged = true;
+    }
+    for (int ch = 0; ch < nch; ++ch) {
+      load(ch + 1, an);
+#pragma unroll
+      for (int u = 0; u < SW_KC; ++u) {
+        const int ks = ch * SW_KC + u;
+        if (ks < nks) {
+          const double* brow = bsw + (4 * ks + t) * BS + g;
+#pragma unroll
+          for (int nf = 0; nf < NF8; ++nf)
+            if (!TRI || ks <= 2 * nf + 1) dmma_sk(acc[nf], a[u][0], a[u][1], brow[nf * 8]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < SW_KC; ++u) {
+        a[u][0] = an[u][0];
+        a[u][1] = an[u][1];
+      }
+    }
+#pragma unroll
+    for (int nf = 0; nf < NF8; ++nf) {
+      const int64_t j = nf * 8 + 2 * t;
+      if (j + 1 < N) {
+        if (r0 < M) *reinterpret_cast<double2*>(C + r0 * ldc + j) = make_double2(acc[nf][0], acc[nf][1]);
+        if (r1 < M) *reinterpret_cast<double2*>(C + r1 * ldc + j) = make_double2(acc[nf][2], acc[nf][3]);
+      } else if (j < N) {
+        if (r0 < M) C[r0 * ldc + j] = acc[nf][0];
+        if (r1 < M) C[r1 * ldc + j] = acc[nf][2];
+      }
+    }
+  }
+  if (!staged) stage();   // a warp without a tile still joins the CTA barrier
+}
+
+template <int NF8, bool TRI>
+void launch_skinny_wide(Handle* h, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,
+                        const double* B, int64_t ldb, double* C, int64_t ldc) {
+  const int Kp = int(ceil_div(K, 4) * 4);
+  const size_t smem = size_t(Kp) * (NF8 * 8 + 1) * sizeof(double);
+  auto kern = skinny_nn_wide_kernel<NF8, TRI>;
+  static AttrOnce once;
+  once([&] {
+    LR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 128 * 129 * 8));
+  });
+  const int64_t ntiles = ceil_div(M, 16);
+  const int64_t ctas = std::min<int64_t>(2 * h->sm_count, ceil_div(ntiles, SW_THREADS / 32));
+  kern<<<unsigned(ctas), SW_THREADS, smem, h->stream>>>(M, N, K, A, lda, B, ldb, C, ldc);
+  LR_CHECK_LAUNCH();
+}
+
 }  // namespace
 
 // LR_SKINNY=0 disables (A/B against the tiled DMMA kernels)
@@ -323,6 +442,33 @@ void gemm_skinny_tri(Handle* h, int64_t M, int64_t N, int64_t K, const double* A
   if (nf <= 4) launch_skinny_nn<4, 8, true>(h, M, N, K, A, lda, B, ldb, C, ldc);
   else if (nf <= 6) launch_skinny_nn<6, 12, true>(h, M, N, K, A, lda, B, ldb, C, ldc);
   else launch_skinny_nn<8, 16, true>(h, M, N, K, A, lda, B, ldb, C, ldc);
+}
+
+// 64 < N <= 128, K <= 128, tall A (the ell = 110 panel applies of config 2)
+bool gemm_skinny_wide_ok(bool transA, int64_t M, int64_t N, int64_t K, const double* C,
+                         int64_t ldc) {
+  static int off = -1;
+  if (off < 0) {
+    const char* e = getenv("LR_SKINNY");
+    off = (e && e[0] == '0') ? 1 : 0;
+  }
+  return !off && !transA && N > 64 && N <= 128 && K >= 8 && K <= 128 && M >= 4096 &&
+         (ldc % 2) == 0 && (reinterpret_cast<uintptr_t>(C) & 15) == 0;
+}
+
+void gemm_skinny_wide(Handle* h, bool tri, int64_t M, int64_t N, int64_t K, const double* A,
+                      int64_t lda, const double* B, int64_t ldb, double* C, int64_t ldc) {
+  const int nf = int(ceil_div(N, 8));
+  if (nf <= 12) {
+    if (tri) launch_skinny_wide<12, true>(h, M, N, K, A, lda, B, ldb, C, ldc);
+    else launch_skinny_wide<12, false>(h, M, N, K, A, lda, B, ldb, C, ldc);
+  } else if (nf <= 14) {
+    if (tri) launch_skinny_wide<14, true>(h, M, N, K, A, lda, B, ldb, C, ldc);
+    else launch_skinny_wide<14, false>(h, M, N, K, A, lda, B, ldb, C, ldc);
+  } else {
+    if (tri) launch_skinny_wide<16, true>(h, M, N, K, A, lda, B, ldb, C, ldc);
+    else launch_skinny_wide<16, false>(h, M, N, K, A, lda, B, ldb, C, ldc);
+  }
 }
 
 void gemm_skinny_nn(Handle* h, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda,

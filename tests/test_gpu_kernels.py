@@ -560,3 +560,32 @@ def test_csr_transpose_on_device_is_canonical():
     assert np.array_equal(ptr, St.indptr.astype(np.int64))
     assert np.array_equal(idx, St.indices.astype(np.int32))
     assert np.array_equal(val, St.data)
+
+
+@pytest.mark.parametrize("M,N,K", [(8192, 110, 110), (16384, 110, 110), (5000, 65, 128), (4099, 128, 9),
+                                   (70000, 96, 96), (4096, 127, 101)])
+def test_skinny_nn_wide(M, N, K):
+    """A B with 64 < N <= 128, K <= 128 and a tall A (config 2's ell = 110 panel
+    applies): the wide skinny kernel against numpy, ragged tiles and odd K; and
+    through the orthonormalization, whose triangular factor skips k-blocks."""
+    from paper_0909_4061_b200 import _lib, core
+    g = np.random.default_rng(M + N + K)
+    A = torch.from_numpy(g.standard_normal((M, K))).cuda()
+    B = torch.from_numpy(g.standard_normal((K, N))).cuda()
+    C = torch.empty((M, N + (N % 2)), dtype=torch.float64, device="cuda")[:, :N]
+    _lib.call("lr_gemm", _lib.handle(), _lib.F64, _lib.OP_N, M, K, N, _lib.ptr(A), _lib.ld(A),
+              _lib.ptr(B), _lib.ld(B), _lib.ptr(C), _lib.ld(C))
+    ref = A.cpu().numpy() @ B.cpu().numpy()
+    assert np.abs(C.cpu().numpy() - ref).max() <= 1e-13 * K
+    if N == K:
+        Y = (A * torch.logspace(0, -4, K, device="cuda", dtype=torch.float64)) @ B
+        status = torch.zeros(1, dtype=torch.int32, device="cuda")
+        with core.speculate(status):
+            Q = core.orth_dev(Y)
+        torch.cuda.synchronize()
+        assert int(status.item()) == 0
+        Qn, Yn = Q.cpu().numpy(), Y.cpu().numpy()
+        assert np.abs(Qn.T @ Qn - np.eye(N)).max() <= 1e-13
+        Rm = Qn.T @ Yn
+        assert np.linalg.norm(np.tril(Rm, -1)) <= 1e-12 * np.linalg.norm(Rm)
+        assert np.linalg.norm(Yn - Qn @ Rm) <= 1e-13 * np.linalg.norm(Yn)
