@@ -266,19 +266,10 @@ void launch_nf(Handle* h, int64_t M, int64_t N, int64_t K, const TIN* A, int64_t
                                  int(S::bytes)));
   });
   const int64_t mt = ceil_div(M, BM), nt = ceil_div(N, S::BN);
-  int64_t splits_wanted = choose_splits(h->sm_count, mt * nt, K);
-  {
-    // one-tile products of a short panel (the Gram of config 2's 8192 x 110
-    // n-side panels): a split per SM leaves each CTA two k-steps and the
-    // reduction 148 partial tiles; LR_SPLIT_MIN_ROWS rows per split at least
-    static int64_t min_rows = -1;
-    if (min_rows < 0) {
-      const char* e = getenv("LR_SPLIT_MIN_ROWS");
-      min_rows = e ? std::max<int64_t>(atoll(e), 1) : 0;
-    }
-    if (min_rows > 0 && mt * nt == 1 && K <= 65536)
-      splits_wanted = std::max<int64_t>(1, std::min<int64_t>(splits_wanted, K / min_rows));
-  }
+  // (one-tile products -- the Gram of config 2's 8192 x 110 panels -- keep one
+  // split per SM: capping the splits at >= 128 / 256 / 512 rows each measured
+  // 5.21 / 5.44 / 5.89 ms per config-2 step against 5.18)
+  const int64_t splits_wanted = choose_splits(h->sm_count, mt * nt, K);
   const int64_t kchunk = ceil_div(ceil_div(K, splits_wanted), BK) * BK;
   const int64_t splits = std::max<int64_t>(1, ceil_div(K, kchunk));
   constexpr int V = 16 / sizeof(TIN);
