@@ -3,11 +3,12 @@
 Mirrors the fixed-rank range finders of the reference's
 ``lowrank.rangefinder`` (/root/reference/pkg/src/lowrank/rangefinder.py)
 with identical signatures, validation, pass counting and RangeBasis fields.
-The sketch Omega and the estimator probes are drawn on the host with the
-reference's Philox streams (bitwise identical) and uploaded; the passes over
-A, the orthonormalizations and the estimator tail run on the device and the
-sample / basis panels stay in HBM between steps.  The adaptive
-(fixed-precision) finder is outside this build's scope.
+The sketch Omega and the estimator probes are drawn ON THE DEVICE from the
+reference's Philox streams (gaussian_dev: the same draws as numpy's
+Generator(Philox).standard_normal, csrc/gauss.cu); the passes over A, the
+orthonormalizations and the estimator tail run on the device and the sample
+/ basis panels stay in HBM between steps.  The adaptive (fixed-precision)
+finders (Alg 4.2, single-vector and blocked) are here too.
 """
 
 from __future__ import annotations
@@ -216,7 +217,7 @@ def fast_range_finder(A, ell, seed, kind="srft", ortho_tol=config.GS_DROP_TOL):
 
 
 def probes_dev(op, r, seed):
-    """Estimator probes W (rangefinder.py:78), drawn on the host and uploaded."""
+    """Estimator probes W (rangefinder.py:78), drawn on the device (gaussian_dev)."""
     Wd = gaussian_dev(op.n, r, seed, stream=_STREAM_PROBE, dtype=_real_of(_op_dtype(op)))
     return _cast_like_op(op, Wd)
 

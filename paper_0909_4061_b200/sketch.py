@@ -106,8 +106,9 @@ class SketchSpec:
 def gaussian_matrix(n, ell, seed):
     """n-by-ell i.i.d. standard normals keyed by seed (sketch.py:96-100).
 
-    Drawn on the host (bitwise identical to the reference); the range
-    finders upload it in the operator's precision."""
+    This is the reference-API function: a numpy array drawn on the host
+    (bitwise identical to the reference).  The range finders do not call it:
+    they draw the same stream on the device (gaussian_dev)."""
     if n < 1 or ell < 1:
         raise ValueError("dimensions must be >= 1")
     return rng_for(seed, _STREAM_GAUSS).standard_normal((n, ell))
