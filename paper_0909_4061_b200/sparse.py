@@ -98,9 +98,9 @@ class CudaCsrOperator(MatVecOperator):
             torch.cuda.nvtx.range_pop()
             ell = X.shape[1]
             # compulsory bytes: the CSR arrays, X once, Y (read-modify-write
-            # when accumulating) -- the HBM lower bound of the product; the
-            # gathers beyond X's first touch are served from L2 by the
-            # column-slice kernel (csrc/spmm.cu)
+            # when accumulating) -- the schedule-independent HBM lower bound of
+            # the product (bench.py adds the cache-capacity-aware bound for
+            # random column indices, which is what the gathers actually cost)
             nbytes = (self.csr_bytes() + X.shape[0] * ell * 8
                       + rows * ell * 8 * (2 if accumulate else 1))
             core.PASS_EVENTS.append((s, e, 2 * self.nnz * ell, nbytes, ell))
