@@ -78,7 +78,9 @@ def main(src, tag):
                           f"bench ({steps} steps, no ncu): {b['ms_per_step']} ms/step, "
                           f"{b['value']} {b['unit']}; roofline kernel frac "
                           f"{b['roofline']['frac']}", ""]
-        lines += ["```", summarize(lf, steps), "```", ""]
+        # the launch lists come from `bench.py --steps 2` (tools/profile_round.sh),
+        # whatever step count the bench line beside them was measured with
+        lines += ["```", summarize(lf, 2), "```", ""]
         for kind in ("pass", "small"):
             rep = os.path.join(src, f"full_{cfg}_{kind}.ncu-rep")
             if not os.path.exists(rep):
